@@ -1,0 +1,220 @@
+/*
+ * memfine.h — C ABI of libmemfine.so, the B200 (sm_100a) MemFine chunked MoE layer.
+ *
+ * MemFine (arXiv 2511.21431, PAPER.md) trains MoE layers without capping expert
+ * capacity by running dispatch -> expert -> combine in C token chunks (FCDA,
+ * Eq. 6), recomputing each chunk's expert activations just
+ * before its gradients (Eq. 7), with C chosen by the paper's
+ * activation-memory model under a memory threshold (MACT, Eqs. 8-9 and bins,
+ * PAPER.md:191-206).
+ *
+ * Conventions (all entry points):
+ *  - Plain C types and raw pointers only.  "dev" pointers are CUDA device
+ *    pointers on the handle's device; "host" pointers are CPU memory.
+ *  - The caller owns every buffer, including the workspace.  The library owns
+ *    only small per-handle metadata (counts mirror, status word, NCCL comm).
+ *  - Stream-ordered: kernels are enqueued on the given cudaStream_t (passed as
+ *    void*; NULL = legacy default stream).  One host thread per handle.
+ *  - No exception or longjmp crosses the ABI; every call returns a status code.
+ *    Synchronous argument checks return immediately.  Errors detected on the
+ *    device (bad expert id, workspace too small) are latched in the handle and
+ *    returned by the next memfine_sync() (or by the call itself when it already
+ *    synchronises, e.g. every call with ep_size > 1).
+ *  - There is no CPU fallback: every compute step runs in the library's CUDA
+ *    kernels; on a machine without a usable sm_100 device, memfine_create
+ *    returns MEMFINE_ERR_CUDA.
+ *
+ * Symbols (Table 1; SURVEY.md symbol table):
+ *   T tokens per rank (b*s), h hidden, g expert FFN size (g_e), E experts,
+ *   k top-k (t_k), EP expert-parallel size (e), E_l = E/EP local experts,
+ *   C chunk count (the paper's c of Eq. 9 — NOT its context-parallel c).
+ */
+#ifndef MEMFINE_H
+#define MEMFINE_H
+
+#include <stdint.h>
+#include <stddef.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define MEMFINE_ABI_VERSION 1
+
+/* Status codes.  1 and 2 mirror the SPEC CLI exit codes. */
+typedef enum {
+    MEMFINE_OK = 0,
+    MEMFINE_ERR_INVALID_ARG = 1,   /* null pointer, bad dims, bad bins, C < 1, ...        */
+    MEMFINE_ERR_INFEASIBLE = 2,    /* static + other >= alpha*M^GPU, or s'_max <= 0        */
+    MEMFINE_ERR_ROUTING = 3,       /* an expert id outside [0, E) (device-detected)        */
+    MEMFINE_ERR_CUDA = 4,          /* CUDA runtime error / no sm_100 device                */
+    MEMFINE_ERR_NCCL = 5,          /* NCCL missing or failed                               */
+    MEMFINE_ERR_WORKSPACE = 6,     /* workspace smaller than memfine_workspace_bytes()     */
+    MEMFINE_ERR_UNSUPPORTED = 7    /* shape outside what the kernels support (see below)  */
+} memfine_status;
+
+enum { MEMFINE_BF16 = 0, MEMFINE_FP32 = 1 };         /* memfine_dims.dtype  */
+enum { MEMFINE_RULE_EQ9 = 0, MEMFINE_RULE_EXACT = 1 }; /* memfine_budget.rule */
+enum { MEMFINE_FWD = 0, MEMFINE_BWD = 1 };           /* workspace pass      */
+
+typedef struct memfine_handle_s* memfine_handle_t;
+
+/* Layer dimensions.  Supported: tokens >= 0; hidden % 64 == 0; ffn % 64 == 0;
+ * 1 <= topk <= num_experts; num_experts % ep_size == 0; 0 <= ep_rank < ep_size. */
+typedef struct {
+    int64_t tokens;       /* T: tokens on this rank (every rank the same T)          */
+    int32_t hidden;       /* h                                                       */
+    int32_t ffn;          /* g (= g_e)                                               */
+    int32_t num_experts;  /* E (global)                                              */
+    int32_t topk;         /* k (= t_k)                                               */
+    int32_t ep_size;      /* EP; ranks hold contiguous expert blocks (reading R4)    */
+    int32_t ep_rank;      /* this rank                                               */
+    int32_t dtype;        /* MEMFINE_BF16 (bf16 storage, fp32 accumulate, tcgen05)    *
+                           * MEMFINE_FP32 (fp32 everywhere, CUDA-core FFMA; <=1e-5)   */
+} memfine_dims;
+
+/* Memory budget for MACT (Eq. 3; Eq. 8). */
+typedef struct {
+    uint64_t gpu_capacity_bytes; /* M^GPU                                                  */
+    double   alpha;              /* available ratio; budget B = floor(alpha * M^GPU) bytes  */
+    uint64_t static_bytes;       /* M^sta (Eq. 1), supplied by the caller                   */
+    uint64_t other_act_bytes;    /* the s-term of Eq. 2 (attention, norms, router), caller  */
+    uint32_t m_g;                /* Eq. 2 multiplier; 1 under full recompute */
+    uint32_t tp, cp;             /* the (t c) divisor of Eqs. 2 and 8; 1 on this path       */
+    uint32_t micro_batch;        /* b                                                       */
+    const int32_t* bins;         /* host; strictly increasing, bins[0] >= 1; NULL = {1,2,4,8}
+                                                                         */
+    int32_t  nbins;
+    int32_t  rule;               /* MEMFINE_RULE_EQ9: C = smallest bin >= ceil(s''/s'_max)
+                                    (Eq. 9 + "the large bin closest to c", reading R8);
+                                    MEMFINE_RULE_EXACT: smallest bin whose true per-chunk
+                                    maximum fits s'_max (every bin must divide nsub)        */
+} memfine_budget;
+
+/* Result of memfine_plan. */
+typedef struct {
+    int32_t  C;                  /* chosen chunk count                                      */
+    int32_t  c_theory;           /* Eq. 9: max(1, ceil(s''_max / s'_max))                   */
+    int32_t  clamped;            /* c exceeded the largest bin                */
+    int32_t  feasible;           /* max_{r,j} s''_{r,j}(C) <= s'_max                        */
+    int32_t  hot_rank;           /* argmax_r s''_r (lowest index on ties)                   */
+    int32_t  exact_peak;         /* 1: s_chunk_max exact (C | nsub); 0: ceil(s''_max / C)   */
+    int64_t  s_dd_max;           /* max_r s''_r: routed copies received by the hottest rank */
+    int64_t  s_prime_max;        /* Eq. 8 in integer bytes (reading R9)                     */
+    int64_t  s_chunk_max;        /* max_{r,j} s''_{r,j}(C)                                  */
+    uint64_t predicted_peak_bytes; /* paper model: m_g D_t b s_chunk_max (2h+2g) / (tp cp)
+                                      (Table 2 rows 11-13)                  */
+} memfine_plan_info;
+
+/* Statistics of the last fwd / bwd call on a handle (valid after memfine_sync). */
+typedef struct {
+    int32_t  C;
+    int32_t  pass;                  /* MEMFINE_FWD / MEMFINE_BWD                            */
+    int64_t  rows[64];              /* s''_{r,j}: rows this rank received per chunk (C<=64)  */
+    int64_t  rows_padded[64];       /* the same, each local expert padded to 128 rows       */
+    uint64_t workspace_used_bytes;  /* high-water of the workspace bump allocator           */
+    uint64_t workspace_given_bytes;
+    int32_t  device_error;          /* latched memfine_status from the device, or 0         */
+    int32_t  gemm_launches;         /* kernels launched by the last call                    */
+    int32_t  kernel_launches;
+} memfine_stats;
+
+/* ---------------------------------------------------------------------------------- */
+
+int32_t     memfine_abi_version(void);
+const char* memfine_status_str(memfine_status s);
+
+/* NCCL bootstrap for ep_size > 1: rank 0 calls this, broadcasts the 128 bytes over
+ * the caller's process group (e.g. torch.distributed), every rank passes them to
+ * memfine_create.  Returns MEMFINE_ERR_NCCL if libnccl.so.2 cannot be loaded. */
+memfine_status memfine_nccl_unique_id(uint8_t out_id[128]);
+
+/* Create a handle on the CURRENT CUDA device.  nccl_unique_id: host, 128 bytes from
+ * memfine_nccl_unique_id(), NULL iff dims->ep_size == 1.  Collective over the EP
+ * group when ep_size > 1 (ncclCommInitRank).  Fails with MEMFINE_ERR_CUDA if the
+ * current device is not sm_100. */
+memfine_status memfine_create(const memfine_dims* dims, const uint8_t* nccl_unique_id,
+                              memfine_handle_t* out);
+memfine_status memfine_destroy(memfine_handle_t h);
+
+/* A1 + A2: per-sub-chunk expert histogram of this rank's routing,
+ * then the all-gather of every rank's histogram ("the first notification",
+ * PAPER.md:200).  ids_dev: int32 [T][k] row-major.  counts_dev: int32
+ * [EP][nsub][E]; counts_dev[r][j][e] = copies of rank r's sub-chunk j routed to
+ * expert e, sub-chunk j = tokens [floor(jT/nsub), floor((j+1)T/nsub)).  Ids outside
+ * [0,E) are not counted and latch MEMFINE_ERR_ROUTING.  1 <= nsub <= 64.
+ * Collective when ep_size > 1. */
+memfine_status memfine_route_counts(memfine_handle_t h, const int32_t* ids_dev, int32_t nsub,
+                                    int32_t* counts_dev, void* stream);
+
+/* A3 (MACT): choose C from the counts.  counts: int32
+ * [EP][nsub][E], HOST or DEVICE memory (detected).  Device counts are evaluated
+ * by the library's single-CTA tuner kernel on the current device (one D2H of the
+ * 64-byte result); host counts by the identical host routine.  Pure: no handle,
+ * no communication.  Integer math throughout (reading R9):
+ *   B = floor(alpha*M^GPU); num = B - static - other (<= 0 -> INFEASIBLE);
+ *   s'_max = floor(num*tp*cp / (m_g*D_t*b*(2h+2g))) (<= 0 -> INFEASIBLE);
+ *   s''_r = sum of counts routed to rank r's experts; c = max(1, ceil(max_r s''_r / s'_max));
+ *   C = smallest bin >= c, else the largest bin with clamped = 1.
+ * D_t = 2 for MEMFINE_BF16, 4 for MEMFINE_FP32. */
+memfine_status memfine_plan(const int32_t* counts, int32_t nsub, const memfine_dims* dims,
+                            const memfine_budget* budget, memfine_plan_info* info);
+
+/* Exact workspace bytes the fwd (pass = MEMFINE_FWD) or bwd (MEMFINE_BWD) call
+ * needs for this routing and C.  counts_host: int32 [EP][nsub][E] from
+ * memfine_route_counts (copied to the host), C must divide nsub; or NULL for the
+ * routing-independent worst case.  The result is the byte high-water of the
+ * library's bump allocator: (per-row bytes) * max_j padded rows of chunk j +
+ * send/receive staging (ep_size > 1) + metadata.  See DESIGN.md "Workspace". */
+memfine_status memfine_workspace_bytes(const int32_t* counts_host, int32_t nsub,
+                                       const memfine_dims* dims, int32_t C, int32_t pass,
+                                       uint64_t* bytes);
+
+/* FCDA forward (Eq. 6): Y = concat_j combine(expert(dispatch(X_j))).
+ *   x       dev [T][h]        bf16 or fp32 (dims.dtype)
+ *   ids     dev [T][k]        int32 global expert ids
+ *   w       dev [T][k]        fp32 top-k scores
+ *   w_gate  dev [E_l][g][h]   local experts only (nn.Linear [out,in])
+ *   w_up    dev [E_l][g][h]
+ *   w_down  dev [E_l][h][g]
+ *   y       dev [T][h]        output (overwritten)
+ *   ws      dev, ws_bytes >= memfine_workspace_bytes(counts, C, MEMFINE_FWD)
+ * Nothing is saved for the backward (A11: the recompute discipline, m_g = 1).
+ * Collective when ep_size > 1 (then it synchronises once on the counts). */
+memfine_status memfine_moe_fwd(memfine_handle_t h, const void* x, const int32_t* ids, const float* w,
+                               const void* w_gate, const void* w_up, const void* w_down, int32_t C,
+                               void* y, void* ws, uint64_t ws_bytes, void* stream);
+
+/* FCDA backward (Eq. 7): for each chunk j, recompute the chunk's gate/up
+ * activations, then back-propagate dY_j.  Inputs as in memfine_moe_fwd plus
+ *   dy      dev [T][h]        upstream gradient
+ * Outputs:
+ *   dx      dev [T][h]        (overwritten)
+ *   dw_gate dev fp32 [E_l][g][h], dw_up fp32 [E_l][g][h], dw_down fp32 [E_l][h][g]
+ *           overwritten, or accumulated into when accumulate_dw != 0
+ *   dscore  dev fp32 [T][k]   dL/dw (nullable); 0 for ids outside [0,E)
+ * Collective when ep_size > 1. */
+memfine_status memfine_moe_bwd(memfine_handle_t h, const void* dy, const void* x, const int32_t* ids,
+                               const float* w, const void* w_gate, const void* w_up, const void* w_down,
+                               int32_t C, void* dx, float* dw_gate, float* dw_up, float* dw_down,
+                               float* dscore, int32_t accumulate_dw, void* ws, uint64_t ws_bytes,
+                               void* stream);
+
+/* Synchronise `stream` and return (and clear) any device-latched error. */
+memfine_status memfine_sync(memfine_handle_t h, void* stream);
+
+/* Statistics of the last fwd/bwd (call memfine_sync first). */
+memfine_status memfine_last_stats(memfine_handle_t h, memfine_stats* out);
+
+/* Debug: when enabled, fwd records each chunk's canonical dispatch order
+ * (reading R3: ascending local expert, src rank, token, slot; padding rows
+ * dropped) as src*T*k + i*k + slot.  memfine_debug_perm copies chunk `chunk`
+ * of the last fwd into perm_host (capacity cap) and sets *n. */
+memfine_status memfine_set_debug(memfine_handle_t h, int32_t enable);
+memfine_status memfine_debug_perm(memfine_handle_t h, int32_t chunk, int64_t* perm_host, int64_t cap,
+                                  int64_t* n);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* MEMFINE_H */

@@ -1,0 +1,117 @@
+"""Thin ctypes binding of libmemfine.so (include/memfine.h).  Argument marshalling only:
+every step of the path runs in the library's CUDA kernels.  There is no fallback — if the
+library is missing or cannot load, import-time use raises."""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+_PKG = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_PKG, "libmemfine.so")
+
+OK, ERR_INVALID_ARG, ERR_INFEASIBLE, ERR_ROUTING, ERR_CUDA, ERR_NCCL, ERR_WORKSPACE, ERR_UNSUPPORTED = range(8)
+BF16, FP32 = 0, 1
+RULE_EQ9, RULE_EXACT = 0, 1
+FWD, BWD = 0, 1
+
+# Every symbol include/memfine.h declares (checked by tests/test_abi.py).
+SYMBOLS = ("memfine_abi_version", "memfine_status_str", "memfine_nccl_unique_id", "memfine_create",
+           "memfine_destroy", "memfine_route_counts", "memfine_plan", "memfine_workspace_bytes",
+           "memfine_moe_fwd", "memfine_moe_bwd", "memfine_sync", "memfine_last_stats",
+           "memfine_set_debug", "memfine_debug_perm")
+
+
+class MemfineError(RuntimeError):
+    def __init__(self, status: int, where: str):
+        self.status = status
+        super().__init__(f"{where}: {status_str(status)} (status {status})")
+
+
+class Dims(C.Structure):
+    _fields_ = [("tokens", C.c_int64), ("hidden", C.c_int32), ("ffn", C.c_int32),
+                ("num_experts", C.c_int32), ("topk", C.c_int32), ("ep_size", C.c_int32),
+                ("ep_rank", C.c_int32), ("dtype", C.c_int32)]
+
+
+class Budget(C.Structure):
+    _fields_ = [("gpu_capacity_bytes", C.c_uint64), ("alpha", C.c_double), ("static_bytes", C.c_uint64),
+                ("other_act_bytes", C.c_uint64), ("m_g", C.c_uint32), ("tp", C.c_uint32), ("cp", C.c_uint32),
+                ("micro_batch", C.c_uint32), ("bins", C.POINTER(C.c_int32)), ("nbins", C.c_int32),
+                ("rule", C.c_int32)]
+
+
+class PlanInfo(C.Structure):
+    _fields_ = [("C", C.c_int32), ("c_theory", C.c_int32), ("clamped", C.c_int32), ("feasible", C.c_int32),
+                ("hot_rank", C.c_int32), ("exact_peak", C.c_int32), ("s_dd_max", C.c_int64),
+                ("s_prime_max", C.c_int64), ("s_chunk_max", C.c_int64), ("predicted_peak_bytes", C.c_uint64)]
+
+    def as_dict(self):
+        return {f: getattr(self, f) for f, _ in self._fields_}
+
+
+class Stats(C.Structure):
+    _fields_ = [("C", C.c_int32), ("pass_", C.c_int32), ("rows", C.c_int64 * 64), ("rows_padded", C.c_int64 * 64),
+                ("workspace_used_bytes", C.c_uint64), ("workspace_given_bytes", C.c_uint64),
+                ("device_error", C.c_int32), ("gemm_launches", C.c_int32), ("kernel_launches", C.c_int32)]
+
+    def as_dict(self):
+        n = self.C
+        return {"C": n, "pass": self.pass_, "rows": list(self.rows[:n]), "rows_padded": list(self.rows_padded[:n]),
+                "workspace_used_bytes": self.workspace_used_bytes,
+                "workspace_given_bytes": self.workspace_given_bytes, "device_error": self.device_error,
+                "gemm_launches": self.gemm_launches, "kernel_launches": self.kernel_launches}
+
+
+_lib = None
+
+
+def lib():
+    """Load libmemfine.so (built by __graft_entry__.build() / paper_2511_21431_b200/build.py)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise RuntimeError(f"{LIB_PATH} is missing: run `python -c 'import __graft_entry__ as g; g.build()'` "
+                               "(there is no CPU fallback)")
+        L = C.CDLL(LIB_PATH)
+        vp, i32, i64, u64 = C.c_void_p, C.c_int32, C.c_int64, C.c_uint64
+        L.memfine_abi_version.restype = i32
+        L.memfine_status_str.restype = C.c_char_p
+        L.memfine_status_str.argtypes = [C.c_int]
+        for name in SYMBOLS[2:]:
+            getattr(L, name).restype = C.c_int
+        L.memfine_nccl_unique_id.argtypes = [vp]
+        L.memfine_create.argtypes = [C.POINTER(Dims), vp, C.POINTER(vp)]
+        L.memfine_destroy.argtypes = [vp]
+        L.memfine_route_counts.argtypes = [vp, vp, i32, vp, vp]
+        L.memfine_plan.argtypes = [vp, i32, C.POINTER(Dims), C.POINTER(Budget), C.POINTER(PlanInfo)]
+        L.memfine_workspace_bytes.argtypes = [vp, i32, C.POINTER(Dims), i32, i32, C.POINTER(u64)]
+        L.memfine_moe_fwd.argtypes = [vp, vp, vp, vp, vp, vp, vp, i32, vp, vp, u64, vp]
+        L.memfine_moe_bwd.argtypes = [vp, vp, vp, vp, vp, vp, vp, vp, i32, vp, vp, vp, vp, vp, i32, vp, u64, vp]
+        L.memfine_sync.argtypes = [vp, vp]
+        L.memfine_last_stats.argtypes = [vp, C.POINTER(Stats)]
+        L.memfine_set_debug.argtypes = [vp, i32]
+        L.memfine_debug_perm.argtypes = [vp, i32, vp, i64, C.POINTER(i64)]
+        if L.memfine_abi_version() != 1:
+            raise RuntimeError("libmemfine.so ABI mismatch")
+        _lib = L
+    return _lib
+
+
+def status_str(s: int) -> str:
+    return lib().memfine_status_str(int(s)).decode()
+
+
+def check(status: int, where: str) -> None:
+    if status != OK:
+        raise MemfineError(status, where)
+
+
+def make_budget(gpu_capacity_bytes: int, alpha: float = 1.0, static_bytes: int = 0, other_act_bytes: int = 0,
+                m_g: int = 1, tp: int = 1, cp: int = 1, micro_batch: int = 1, bins=(1, 2, 4, 8),
+                rule: int = RULE_EQ9):
+    arr = (C.c_int32 * len(bins))(*bins) if bins is not None else None
+    b = Budget(int(gpu_capacity_bytes), float(alpha), int(static_bytes), int(other_act_bytes), m_g, tp, cp,
+               micro_batch, C.cast(arr, C.POINTER(C.c_int32)) if arr is not None else None,
+               len(bins) if bins is not None else 0, rule)
+    b._keep = arr  # keep the bins array alive
+    return b

@@ -1,0 +1,66 @@
+// common.cuh — shared device/host helpers of libmemfine.so (product code; no oracle code).
+#pragma once
+#include <cuda_runtime.h>
+#include <cuda_bf16.h>
+#include <stdint.h>
+#include "../../include/memfine.h"
+
+namespace memfine {
+
+constexpr int kRowAlign = 128;   // every local expert's row segment is padded to 128 rows
+constexpr int kTokPerBlk = 128;  // tokens per dispatch block
+constexpr int kMaxSub = 64;      // max sub-chunks / chunks per call (memfine_stats.rows)
+
+// info[] words written by the dispatch scan kernel, read by the GEMM schedulers.
+enum InfoWord {
+  kInfoRows = 0,       // s''_{r,j}: real rows received this chunk
+  kInfoRowsPad = 1,    // padded rows (multiple of 128)
+  kInfoSend = 2,       // copies of this rank's chunk tokens (valid ids)
+  kInfoSkip = 3,       // 1 => capacity exceeded, every kernel of the chunk is a no-op
+  kInfoWords = 8
+};
+
+// Latched device status word (pinned, mapped host memory, owned by the handle).
+__device__ __forceinline__ void latch_error(int* status, int code) {
+  if (status) atomicCAS(status, 0, code);
+}
+
+__host__ __device__ __forceinline__ int64_t ceil_div64(int64_t a, int64_t b) { return (a + b - 1) / b; }
+__host__ __device__ __forceinline__ int64_t round_up64(int64_t a, int64_t b) { return ceil_div64(a, b) * b; }
+__host__ __device__ __forceinline__ int64_t chunk_begin(int64_t T, int C, int j) {
+  // chunk j = [floor(jT/C), floor((j+1)T/C)) (reading R1).  T < 2^40 keeps j*T in range.
+  return (int64_t)((j * (long long)T) / C);
+}
+
+// Element type helpers: the data path stores activations in bf16 (MEMFINE_BF16)
+// or fp32 (MEMFINE_FP32); arithmetic is always fp32.
+template <typename T> struct Elt;
+template <> struct Elt<__nv_bfloat16> {
+  static __device__ __forceinline__ float to_f(__nv_bfloat16 v) { return __bfloat162float(v); }
+  static __device__ __forceinline__ __nv_bfloat16 from_f(float v) { return __float2bfloat16_rn(v); }
+};
+template <> struct Elt<float> {
+  static __device__ __forceinline__ float to_f(float v) { return v; }
+  static __device__ __forceinline__ float from_f(float v) { return v; }
+};
+
+__device__ __forceinline__ float silu_f(float z) { return z / (1.0f + __expf(-z)); }
+__device__ __forceinline__ float sigmoid_f(float z) { return 1.0f / (1.0f + __expf(-z)); }
+
+// Binary search: the local expert owning padded row `row` (seg has El+1 entries).
+__device__ __forceinline__ int expert_of_row(const int* __restrict__ seg, int El, int row) {
+  int lo = 0, hi = El;  // seg[lo] <= row < seg[hi]
+  while (hi - lo > 1) {
+    int mid = (lo + hi) >> 1;
+    if (__ldg(seg + mid) <= row) lo = mid; else hi = mid;
+  }
+  return lo;
+}
+
+}  // namespace memfine
+
+#define MF_CUDA_OK(expr)                                              \
+  do {                                                                \
+    cudaError_t _e = (expr);                                          \
+    if (_e != cudaSuccess) { return MEMFINE_ERR_CUDA; }               \
+  } while (0)

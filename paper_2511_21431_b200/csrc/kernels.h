@@ -1,0 +1,96 @@
+// kernels.h — host-side launchers of the libmemfine.so kernels (internal header).
+#pragma once
+#include "common.cuh"
+
+namespace memfine {
+
+// Per-chunk device metadata carved from the workspace.
+struct ChunkMeta {
+  int* blk_cnt;    // [NBmax][E]   per token-block expert counts, then (in place) block offsets
+  int* exp_cnt;    // [E]          this rank's chunk copies per global expert
+  int* recv_cnt;   // [E_l]        rows received per local expert (EP>1; == exp_cnt slice at EP=1)
+  int* seg;        // [E_l+1]      padded row segment starts of the local experts
+  int* info;       // [kInfoWords]
+  int* dest_of;    // [Tmax*k]     position of copy (i,slot): expert-major row (EP=1) or send row
+  int* src_of;     // [rows_cap]   copy index feeding each row (EP=1, debug/gather), -1 padding
+  float* w_row;    // [rows_cap]   top-k score of each row (0 on padding)
+  float* dw_row;   // [rows_cap]   d_score of each row (bwd)
+};
+
+// ---------------------------------------------------------------- routing (A1, A5, A10, B7)
+void launch_route_hist(const int32_t* ids, int64_t T, int k, int E, int nsub, int* counts,
+                       int* status, cudaStream_t st);
+void launch_dispatch_hist(const int32_t* ids, int64_t t0, int64_t t1, int k, int E, const ChunkMeta& m,
+                          int* status, cudaStream_t st);
+// ep_size == 1: expert-major padded layout; ep_size > 1: send layout (global expert order).
+void launch_dispatch_scan(int NB, int E, int El, int ep_size, int64_t rows_cap, const ChunkMeta& m,
+                          int64_t* stats_rows, int64_t* stats_rows_pad, int chunk, cudaStream_t st);
+void launch_ep_recv_seg(const int* counts, int C, int j, int E, int El, int me, int EP, int64_t rows_cap,
+                        const ChunkMeta& m, int64_t* stats_rows, int64_t* stats_rows_pad, cudaStream_t st);
+template <typename T>
+void launch_dispatch_scatter(const T* x, const T* dy, const int32_t* ids, const float* w, int64_t t0,
+                             int64_t t1, int k, int E, int h, const ChunkMeta& m, T* xd, T* dyd,
+                             cudaStream_t st);
+template <typename T>
+void launch_zero_padding(int El, int h, const ChunkMeta& m, T* xd, T* dyd, cudaStream_t st);
+template <typename T>
+void launch_combine(const T* O, const float* w, int64_t t0, int64_t t1, int k, int h, const ChunkMeta& m,
+                    T* y, cudaStream_t st);
+template <typename T>
+void launch_unpermute_reduce(const T* dXd, int64_t t0, int64_t t1, int k, int h, const ChunkMeta& m,
+                             T* dx, float* dscore, cudaStream_t st);
+
+// ---------------------------------------------------------------- MACT tuner (A3)
+struct PlanParams {
+  int32_t EP, nsub, E, h, g, D_t, nbins, rule;
+  int32_t bins[16];
+  uint64_t budget, static_bytes, other_bytes;
+  int64_t m_g, tp, cp, micro_batch;
+};
+// Shared host/device evaluation from per-(rank, sub-chunk) sums sub[r*nsub + j].
+__host__ __device__ int plan_from_subsums(const int64_t* sub, const PlanParams& p, memfine_plan_info* out);
+void launch_plan_kernel(const int32_t* counts_dev, const PlanParams& p, memfine_plan_info* out_mapped,
+                        int* rc_mapped, cudaStream_t st);
+
+// ---------------------------------------------------------------- expert GEMMs (A7, A8, B2-B5)
+enum GemmKind {
+  GK_GATEUP = 0,      // A7/B2: [R,h] x W_gate/W_up^T -> a = silu(G)*U (fwd) and/or G||U (bwd)
+  GK_DOWN = 1,        // A8:    [R,g] x W_down^T -> o
+  GK_DACT = 2,        // B3:    dY [R,h] x W_down -> u; epilogue d_w, dG, dU, a_w
+  GK_DX = 3,          // B4:    dGU [R,2g] x [W_gate; W_up] -> dX_disp
+  GK_WGRAD_DOWN = 4,  // B5:    dW_down[e] += dY^T a_w
+  GK_WGRAD_GU = 5     // B5:    dW_gate[e] || dW_up[e] += dGU^T X
+};
+
+template <typename T>
+struct GemmProblem {
+  int kind;
+  int El, h, g;
+  int64_t rows_cap;
+  const int* seg;    // [El+1]
+  const int* info;   // chunk info words
+  const T* X;        // X_disp [R][h]
+  const T* DY;       // dY_disp [R][h]
+  T* GU;             // [R][2g]   G||U (recompute), overwritten by dG||dU
+  T* A;              // [R][g]    a (fwd) / a_w (bwd)
+  T* O;              // [R][h]    o (fwd) / dX_disp (bwd)
+  const T* Wg;       // [El][g][h]
+  const T* Wu;       // [El][g][h]
+  const T* Wd;       // [El][h][g]
+  const float* w_row;
+  float* dw_row;
+  float* dWg;        // [El][g][h] fp32
+  float* dWu;
+  float* dWd;        // [El][h][g]
+  int store_a;       // GATEUP: store a
+  int store_gu;      // GATEUP: store G||U
+};
+
+// CUDA-core FFMA path (MEMFINE_FP32 mode; K12 of SURVEY §2.4).
+template <typename T>
+int launch_gemm_simt(const GemmProblem<T>& p, cudaStream_t st);
+// tcgen05 / TMEM / TMA path (MEMFINE_BF16).  Returns number of launches or <0 on error.
+int launch_gemm_sm100(const GemmProblem<__nv_bfloat16>& p, cudaStream_t st);
+int sm100_num_sms();
+
+}  // namespace memfine

@@ -1,0 +1,798 @@
+// memfine.cu — the C ABI of libmemfine.so: handle, MACT plan, workspace carving and the
+// FCDA chunk loops (Eq. 6 forward, Eq. 7 recompute backward).
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <cmath>
+#include <vector>
+#include <string>
+#include <algorithm>
+#include <type_traits>
+
+#include "kernels.h"
+#include "nccl_shim.h"
+
+using namespace memfine;
+
+struct memfine_handle_s {
+  memfine_dims d;
+  int device = 0;
+  int num_sms = 148;
+  int* status_h = nullptr;     // pinned, mapped: device-latched error word
+  int* status_d = nullptr;
+  int64_t* rows_h = nullptr;   // pinned, mapped: [2][kMaxSub] rows / padded rows per chunk
+  int64_t* rows_d = nullptr;
+  memfine_stats last{};
+  uint64_t last_meta = 0, last_row_bytes = 0;
+  int debug = 0;
+  std::vector<std::vector<int64_t>> debug_perm;
+  // expert parallel
+  NcclComm comm{};
+  int* counts_d = nullptr;     // [EP][C][E] all-gathered chunk counts (device)
+  int* counts_h = nullptr;     // pinned mirror
+  size_t counts_cap = 0;
+  cudaEvent_t ev = nullptr;
+};
+
+namespace {
+
+bool dims_ok(const memfine_dims* d) {
+  if (!d) return false;
+  if (d->tokens < 0 || d->tokens > (int64_t(1) << 31) / 64) return false;
+  if (d->hidden <= 0 || d->hidden % 64 || d->ffn <= 0 || d->ffn % 64) return false;
+  if (d->num_experts < 1 || d->topk < 1 || d->topk > d->num_experts || d->topk > 16) return false;
+  if (d->ep_size < 1 || d->num_experts % d->ep_size || d->ep_rank < 0 || d->ep_rank >= d->ep_size) return false;
+  if (d->num_experts > 1024) return false;
+  if (d->dtype != MEMFINE_BF16 && d->dtype != MEMFINE_FP32) return false;
+  return true;
+}
+
+int elt_bytes(const memfine_dims& d) { return d.dtype == MEMFINE_BF16 ? 2 : 4; }
+
+// ------------------------------------------------------------------ workspace carving
+// One bump allocator (256-byte aligned) defines the layout; the byte count it reaches is
+// the predicted high-water (memfine_workspace_bytes) and the carve used by fwd/bwd.
+struct Bump {
+  char* base;
+  uint64_t off = 0;
+  explicit Bump(void* b) : base((char*)b) {}
+  template <typename T>
+  T* take(uint64_t n) {
+    off = (off + 255) & ~uint64_t(255);
+    T* p = base ? (T*)(base + off) : nullptr;
+    off += n * sizeof(T);
+    return p;
+  }
+};
+
+struct Layout {
+  ChunkMeta m{};
+  void* X = nullptr;   // [R][h]
+  void* DY = nullptr;  // [R][h]   (bwd)
+  void* GU = nullptr;  // [R][2g]  (bwd)
+  void* A = nullptr;   // [R][g]
+  void* O = nullptr;   // [R][h]   (fwd: o; bwd: dX_disp aliases X)
+  void* send = nullptr;      // [S][h]   EP>1 staging (x out / o back)
+  void* send_dy = nullptr;   // [S][h]   EP>1 bwd
+  float* send_w = nullptr;   // [S]      EP>1 scores out / d_score back
+  int64_t rows_cap = 0;
+  uint64_t meta_bytes = 0, row_bytes = 0, total = 0;
+};
+
+uint64_t row_bytes_of(const memfine_dims& d, int pass) {
+  uint64_t D = elt_bytes(d), h = d.hidden, g = d.ffn;
+  if (pass == MEMFINE_FWD) return 4 + 4 + D * (h + g + h);        // src_of, w_row, X, A, O
+  return 4 + 4 + 4 + D * (h + h + 2 * g + g);                      // + dw_row, DY, GU; O aliases X
+}
+
+int64_t tmax_chunk(const memfine_dims& d, int C) { return ceil_div64(d.tokens, C); }
+
+// Carve: metadata, optional EP send staging (send_rows), then rows_cap rows.
+Layout carve(const memfine_dims& d, int C, int pass, void* ws, int64_t rows_cap, int64_t send_rows) {
+  Layout L;
+  Bump b(ws);
+  int E = d.num_experts, El = E / d.ep_size;
+  int64_t Tm = tmax_chunk(d, C);
+  int64_t NB = ceil_div64(Tm, kTokPerBlk);
+  uint64_t D = elt_bytes(d);
+  L.m.blk_cnt = b.take<int>((uint64_t)NB * E);
+  L.m.exp_cnt = b.take<int>(E);
+  L.m.recv_cnt = b.take<int>(El);
+  L.m.seg = b.take<int>(El + 1);
+  L.m.info = b.take<int>(kInfoWords);
+  L.m.dest_of = b.take<int>((uint64_t)Tm * d.topk);
+  if (d.ep_size > 1) {
+    L.send = b.take<char>((uint64_t)send_rows * d.hidden * D);
+    if (pass == MEMFINE_BWD) L.send_dy = b.take<char>((uint64_t)send_rows * d.hidden * D);
+    L.send_w = b.take<float>((uint64_t)send_rows);
+  }
+  b.off = (b.off + 255) & ~uint64_t(255);
+  L.meta_bytes = b.off;
+  L.row_bytes = row_bytes_of(d, pass);
+  L.rows_cap = rows_cap;
+  int64_t R = rows_cap;
+  L.m.src_of = b.take<int>(R);
+  L.m.w_row = b.take<float>(R);
+  if (pass == MEMFINE_BWD) L.m.dw_row = b.take<float>(R);
+  L.X = b.take<char>((uint64_t)R * d.hidden * D);
+  if (pass == MEMFINE_BWD) {
+    L.DY = b.take<char>((uint64_t)R * d.hidden * D);
+    L.GU = b.take<char>((uint64_t)R * 2 * d.ffn * D);
+    L.A = b.take<char>((uint64_t)R * d.ffn * D);
+    L.O = L.X;
+  } else {
+    L.A = b.take<char>((uint64_t)R * d.ffn * D);
+    L.O = b.take<char>((uint64_t)R * d.hidden * D);
+  }
+  b.off = (b.off + 255) & ~uint64_t(255);
+  L.total = b.off;
+  return L;
+}
+
+// rows_cap that fits ws_bytes (multiple of 128; each row array then stays 256-aligned).
+int64_t rows_fitting(const memfine_dims& d, int C, int pass, uint64_t ws_bytes, int64_t send_rows) {
+  Layout L0 = carve(d, C, pass, nullptr, 0, send_rows);
+  if (ws_bytes < L0.meta_bytes) return -1;
+  int64_t R = (int64_t)((ws_bytes - L0.meta_bytes) / L0.row_bytes);
+  R = (R / kRowAlign) * kRowAlign;
+  while (R > 0 && carve(d, C, pass, nullptr, R, send_rows).total > ws_bytes) R -= kRowAlign;
+  return R;
+}
+
+// Padded rows per chunk on rank r from host counts [EP][nsub][E] (C | nsub).
+void chunk_rows(const int32_t* counts, int nsub, const memfine_dims& d, int C, int r, std::vector<int64_t>& rows,
+                std::vector<int64_t>& rows_pad, std::vector<int64_t>* send) {
+  int E = d.num_experts, El = E / d.ep_size, per = nsub / C;
+  rows.assign(C, 0);
+  rows_pad.assign(C, 0);
+  if (send) send->assign(C, 0);
+  for (int jc = 0; jc < C; jc++) {
+    for (int e = r * El; e < (r + 1) * El; e++) {
+      int64_t c = 0;
+      for (int src = 0; src < d.ep_size; src++)
+        for (int j = jc * per; j < (jc + 1) * per; j++) c += counts[((int64_t)src * nsub + j) * E + e];
+      rows[jc] += c;
+      rows_pad[jc] += round_up64(c, kRowAlign);
+    }
+    if (send)
+      for (int e = 0; e < E; e++)
+        for (int j = jc * per; j < (jc + 1) * per; j++) (*send)[jc] += counts[((int64_t)r * nsub + j) * E + e];
+  }
+}
+
+bool is_device_ptr(const void* p) {
+  cudaPointerAttributes a;
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) { cudaGetLastError(); return false; }
+  return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
+}
+
+int budget_to_params(const memfine_dims* d, const memfine_budget* b, int nsub, PlanParams* p) {
+  static const int32_t kDefaultBins[4] = {1, 2, 4, 8};
+  if (!dims_ok(d) || !b || nsub < 1 || nsub > kMaxSub) return MEMFINE_ERR_INVALID_ARG;
+  const int32_t* bins = b->bins ? b->bins : kDefaultBins;
+  int nb = b->bins ? b->nbins : 4;
+  if (nb < 1 || nb > 16) return MEMFINE_ERR_INVALID_ARG;
+  for (int i = 0; i < nb; i++) {
+    if (bins[i] < 1) return MEMFINE_ERR_INVALID_ARG;
+    if (i && bins[i] <= bins[i - 1]) return MEMFINE_ERR_INVALID_ARG;
+    p->bins[i] = bins[i];
+  }
+  if (!(b->alpha > 0.0) || !std::isfinite(b->alpha)) return MEMFINE_ERR_INVALID_ARG;
+  if (b->m_g < 1 || b->tp < 1 || b->cp < 1 || b->micro_batch < 1) return MEMFINE_ERR_INVALID_ARG;
+  if (b->rule != MEMFINE_RULE_EQ9 && b->rule != MEMFINE_RULE_EXACT) return MEMFINE_ERR_INVALID_ARG;
+  long double B = (long double)b->alpha * (long double)b->gpu_capacity_bytes;
+  if (B >= 18446744073709551615.0L) B = 18446744073709551615.0L;
+  p->budget = (uint64_t)floorl(B);
+  p->EP = d->ep_size;
+  p->nsub = nsub;
+  p->E = d->num_experts;
+  p->h = d->hidden;
+  p->g = d->ffn;
+  p->D_t = elt_bytes(*d);
+  p->nbins = nb;
+  p->rule = b->rule;
+  p->static_bytes = b->static_bytes;
+  p->other_bytes = b->other_act_bytes;
+  p->m_g = b->m_g;
+  p->tp = b->tp;
+  p->cp = b->cp;
+  p->micro_batch = b->micro_batch;
+  return MEMFINE_OK;
+}
+
+template <typename T>
+GemmProblem<T> base_problem(const memfine_handle_s* h, const Layout& L, const void* wg, const void* wu,
+                            const void* wd) {
+  GemmProblem<T> p{};
+  p.El = h->d.num_experts / h->d.ep_size;
+  p.h = h->d.hidden;
+  p.g = h->d.ffn;
+  p.rows_cap = L.rows_cap;
+  p.seg = L.m.seg;
+  p.info = L.m.info;
+  p.X = (const T*)L.X;
+  p.DY = (const T*)L.DY;
+  p.GU = (T*)L.GU;
+  p.A = (T*)L.A;
+  p.O = (T*)L.O;
+  p.Wg = (const T*)wg;
+  p.Wu = (const T*)wu;
+  p.Wd = (const T*)wd;
+  p.w_row = L.m.w_row;
+  p.dw_row = L.m.dw_row;
+  return p;
+}
+
+bool bf16_use_simt() {
+  const char* s = getenv("MEMFINE_BF16_GEMM");
+  return s && !strcmp(s, "simt");
+}
+
+template <typename T>
+int run_gemm(memfine_handle_s* h, const GemmProblem<T>& p, cudaStream_t st) {
+  int n;
+  if constexpr (std::is_same<T, __nv_bfloat16>::value) {
+    if (bf16_use_simt()) n = launch_gemm_simt<T>(p, st);
+    else n = launch_gemm_sm100(p, st);
+  } else {
+    n = launch_gemm_simt<T>(p, st);
+  }
+  if (n < 0) return MEMFINE_ERR_UNSUPPORTED;
+  h->last.gemm_launches += n;
+  h->last.kernel_launches += n;
+  return MEMFINE_OK;
+}
+
+memfine_status latch_cuda(memfine_handle_s* h) {
+  (void)h;
+  cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? MEMFINE_OK : MEMFINE_ERR_CUDA;
+}
+
+// ------------------------------------------------------------------ the FCDA chunk loops (EP = 1)
+template <typename T>
+memfine_status fwd_ep1(memfine_handle_s* h, const T* x, const int32_t* ids, const float* w, const void* wg,
+                       const void* wu, const void* wd, int C, T* y, void* ws, uint64_t ws_bytes, cudaStream_t st) {
+  const memfine_dims& d = h->d;
+  int64_t R = rows_fitting(d, C, MEMFINE_FWD, ws_bytes, 0);
+  if (R < 0) return MEMFINE_ERR_WORKSPACE;
+  Layout L = carve(d, C, MEMFINE_FWD, ws, R, 0);
+  int E = d.num_experts, El = E, k = d.topk, hd = d.hidden;
+  h->last_meta = L.meta_bytes;
+  h->last_row_bytes = L.row_bytes;
+  if (h->debug) h->debug_perm.assign(C, {});
+  for (int j = 0; j < C; j++) {
+    int64_t t0 = chunk_begin(d.tokens, C, j), t1 = chunk_begin(d.tokens, C, j + 1);
+    if (t1 == t0) continue;
+    int NB = (int)ceil_div64(t1 - t0, kTokPerBlk);
+    launch_dispatch_hist(ids, t0, t1, k, E, L.m, h->status_d, st);
+    launch_dispatch_scan(NB, E, El, 1, R, L.m, h->rows_d, h->rows_d + kMaxSub, j, st);
+    launch_dispatch_scatter<T>(x, nullptr, ids, w, t0, t1, k, E, hd, L.m, (T*)L.X, nullptr, st);
+    launch_zero_padding<T>(El, hd, L.m, (T*)L.X, nullptr, st);
+    h->last.kernel_launches += 4;
+    if (h->debug) {
+      cudaStreamSynchronize(st);
+      int rp = (int)h->rows_h[kMaxSub + j];
+      std::vector<int> tmp(rp > 0 ? rp : 0);
+      if (rp > 0) cudaMemcpy(tmp.data(), L.m.src_of, sizeof(int) * rp, cudaMemcpyDeviceToHost);
+      for (int v : tmp)
+        if (v >= 0) h->debug_perm[j].push_back(v);
+    }
+    GemmProblem<T> p = base_problem<T>(h, L, wg, wu, wd);
+    p.kind = GK_GATEUP;
+    p.store_a = 1;
+    if (int rc = run_gemm<T>(h, p, st)) return (memfine_status)rc;
+    p.kind = GK_DOWN;
+    if (int rc = run_gemm<T>(h, p, st)) return (memfine_status)rc;
+    launch_combine<T>((const T*)L.O, w, t0, t1, k, hd, L.m, y, st);
+    h->last.kernel_launches += 1;
+  }
+  return latch_cuda(h);
+}
+
+template <typename T>
+memfine_status bwd_ep1(memfine_handle_s* h, const T* dy, const T* x, const int32_t* ids, const float* w,
+                       const void* wg, const void* wu, const void* wd, int C, T* dx, float* dwg, float* dwu,
+                       float* dwd, float* dscore, int accumulate, void* ws, uint64_t ws_bytes, cudaStream_t st) {
+  const memfine_dims& d = h->d;
+  int64_t R = rows_fitting(d, C, MEMFINE_BWD, ws_bytes, 0);
+  if (R < 0) return MEMFINE_ERR_WORKSPACE;
+  Layout L = carve(d, C, MEMFINE_BWD, ws, R, 0);
+  int E = d.num_experts, El = E, k = d.topk, hd = d.hidden, g = d.ffn;
+  h->last_meta = L.meta_bytes;
+  h->last_row_bytes = L.row_bytes;
+  if (!accumulate) {
+    size_t wb = sizeof(float) * (size_t)El * g * hd;
+    MF_CUDA_OK(cudaMemsetAsync(dwg, 0, wb, st));
+    MF_CUDA_OK(cudaMemsetAsync(dwu, 0, wb, st));
+    MF_CUDA_OK(cudaMemsetAsync(dwd, 0, wb, st));
+  }
+  if (dscore && d.tokens > 0) MF_CUDA_OK(cudaMemsetAsync(dscore, 0, sizeof(float) * d.tokens * k, st));
+  for (int j = 0; j < C; j++) {
+    int64_t t0 = chunk_begin(d.tokens, C, j), t1 = chunk_begin(d.tokens, C, j + 1);
+    if (t1 == t0) continue;
+    int NB = (int)ceil_div64(t1 - t0, kTokPerBlk);
+    // B1: re-dispatch x and dy of the chunk (the recompute of Eq. 7 starts from X_j)
+    launch_dispatch_hist(ids, t0, t1, k, E, L.m, h->status_d, st);
+    launch_dispatch_scan(NB, E, El, 1, R, L.m, h->rows_d, h->rows_d + kMaxSub, j, st);
+    launch_dispatch_scatter<T>(x, dy, ids, w, t0, t1, k, E, hd, L.m, (T*)L.X, (T*)L.DY, st);
+    launch_zero_padding<T>(El, hd, L.m, (T*)L.X, (T*)L.DY, st);
+    h->last.kernel_launches += 4;
+    GemmProblem<T> p = base_problem<T>(h, L, wg, wu, wd);
+    p.dWg = dwg;
+    p.dWu = dwu;
+    p.dWd = dwd;
+    // B2: recompute G || U for this chunk only
+    p.kind = GK_GATEUP;
+    p.store_a = 0;
+    p.store_gu = 1;
+    if (int rc = run_gemm<T>(h, p, st)) return (memfine_status)rc;
+    // B3: u = dY W_down, fused d_w / dG / dU / a_w epilogue
+    p.kind = GK_DACT;
+    if (int rc = run_gemm<T>(h, p, st)) return (memfine_status)rc;
+    // B5: weight gradients accumulate across chunks (reading R18)
+    p.kind = GK_WGRAD_DOWN;
+    if (int rc = run_gemm<T>(h, p, st)) return (memfine_status)rc;
+    p.kind = GK_WGRAD_GU;
+    if (int rc = run_gemm<T>(h, p, st)) return (memfine_status)rc;
+    // B4: dX_disp = dG W_gate + dU W_up (overwrites X_disp, dead after B5)
+    p.kind = GK_DX;
+    if (int rc = run_gemm<T>(h, p, st)) return (memfine_status)rc;
+    // B7: dX_i = sum_slot dX_disp[pos], d_score
+    launch_unpermute_reduce<T>((const T*)L.O, t0, t1, k, hd, L.m, dx, dscore, st);
+    h->last.kernel_launches += 1;
+  }
+  return latch_cuda(h);
+}
+
+// ------------------------------------------------------------------ expert parallel (EP > 1)
+// Per chunk: dispatch permute into the send layout (dest rank, local expert, token, slot),
+// NCCL all-to-allv with one message per (peer, local expert) segment so rows land directly in
+// the receiver's padded expert-major layout (local expert, src rank, token, slot; reading R3),
+// expert GEMMs, and the reverse exchange back into the send layout for the combine.
+struct EpChunk {
+  std::vector<int64_t> send_off;  // [E+1] prefix of my chunk copies over global experts
+  std::vector<int64_t> recv_off;  // [EP][El] row where src's rows of local expert el start
+  std::vector<int64_t> recv_cnt;  // [EP][El]
+  int64_t rows = 0, rows_pad = 0, send = 0;
+};
+
+EpChunk ep_chunk_table(const memfine_dims& d, const int* counts, int C, int j) {
+  int E = d.num_experts, EP = d.ep_size, El = E / EP, me = d.ep_rank;
+  EpChunk t;
+  t.send_off.assign(E + 1, 0);
+  for (int e = 0; e < E; e++) t.send_off[e + 1] = t.send_off[e] + counts[((int64_t)me * C + j) * E + e];
+  t.send = t.send_off[E];
+  t.recv_off.assign((size_t)EP * El, 0);
+  t.recv_cnt.assign((size_t)EP * El, 0);
+  int64_t acc = 0;
+  for (int el = 0; el < El; el++) {
+    int64_t run = acc;
+    for (int src = 0; src < EP; src++) {
+      int64_t c = counts[((int64_t)src * C + j) * E + me * El + el];
+      t.recv_off[(size_t)src * El + el] = run;
+      t.recv_cnt[(size_t)src * El + el] = c;
+      run += c;
+      t.rows += c;
+    }
+    acc += round_up64(run - acc, kRowAlign);
+  }
+  t.rows_pad = acc;
+  return t;
+}
+
+// One grouped exchange.  forward=true: send-layout rows -> receiver's expert-major rows;
+// forward=false: expert-major rows -> the source's send layout.  width = elements per row,
+// esize = bytes per element (row payload moved as bytes; NCCL dtype uint8) or 4 for fp32 scalars.
+int ep_exchange(memfine_handle_s* h, const EpChunk& t, const int* counts, int C, int j, bool forward, char* send_buf,
+                char* expert_buf, size_t row_bytes, cudaStream_t st) {
+  const memfine_dims& d = h->d;
+  int E = d.num_experts, EP = d.ep_size, El = E / EP, me = d.ep_rank;
+  if (nccl_group_start()) return 1;
+  int rc = 0;
+  for (int peer = 0; peer < EP && !rc; peer++) {
+    for (int el = 0; el < El && !rc; el++) {
+      // my copies for expert (peer, el): contiguous in my send layout
+      int eg = peer * El + el;
+      int64_t s0 = t.send_off[eg], sn = t.send_off[eg + 1] - s0;
+      // rows of src=peer for my local expert el in my expert-major buffer
+      int64_t r0 = t.recv_off[(size_t)peer * El + el], rn = t.recv_cnt[(size_t)peer * El + el];
+      if (peer == me) {
+        if (sn) {
+          char* a = send_buf + s0 * row_bytes;
+          char* b = expert_buf + r0 * row_bytes;
+          if (cudaMemcpyAsync(forward ? b : a, forward ? a : b, sn * row_bytes, cudaMemcpyDeviceToDevice, st))
+            rc = 1;
+        }
+        continue;
+      }
+      if (forward) {
+        if (sn) rc |= nccl_send(&h->comm, send_buf + s0 * row_bytes, sn * row_bytes, 0, peer, st);
+        if (rn) rc |= nccl_recv(&h->comm, expert_buf + r0 * row_bytes, rn * row_bytes, 0, peer, st);
+      } else {
+        if (rn) rc |= nccl_send(&h->comm, expert_buf + r0 * row_bytes, rn * row_bytes, 0, peer, st);
+        if (sn) rc |= nccl_recv(&h->comm, send_buf + s0 * row_bytes, sn * row_bytes, 0, peer, st);
+      }
+    }
+  }
+  (void)counts; (void)C; (void)j;
+  rc |= nccl_group_end();
+  return rc;
+}
+
+// All-gathered per-chunk counts [EP][C][E] on device and host (the layer's one D2H sync).
+int ep_gather_counts(memfine_handle_s* h, const int32_t* ids, int C, cudaStream_t st) {
+  const memfine_dims& d = h->d;
+  size_t need = (size_t)d.ep_size * C * d.num_experts;
+  if (need > h->counts_cap) {
+    if (h->counts_d) cudaFree(h->counts_d);
+    if (h->counts_h) cudaFreeHost(h->counts_h);
+    h->counts_d = nullptr;
+    h->counts_h = nullptr;
+    h->counts_cap = 0;
+    if (cudaMalloc((void**)&h->counts_d, need * sizeof(int)) ||
+        cudaHostAlloc((void**)&h->counts_h, need * sizeof(int), cudaHostAllocDefault))
+      return MEMFINE_ERR_CUDA;
+    h->counts_cap = need;
+  }
+  int* mine = h->counts_d + (int64_t)d.ep_rank * C * d.num_experts;
+  launch_route_hist(ids, d.tokens, d.topk, d.num_experts, C, mine, h->status_d, st);
+  if (nccl_all_gather_int(&h->comm, mine, h->counts_d, (size_t)C * d.num_experts, st)) return MEMFINE_ERR_NCCL;
+  MF_CUDA_OK(cudaMemcpyAsync(h->counts_h, h->counts_d, need * sizeof(int), cudaMemcpyDeviceToHost, st));
+  MF_CUDA_OK(cudaStreamSynchronize(st));
+  if (*h->status_h) return __atomic_exchange_n(h->status_h, 0, __ATOMIC_SEQ_CST);
+  return MEMFINE_OK;
+}
+
+template <typename T>
+memfine_status ep_run(memfine_handle_s* h, int pass, const T* dy, const T* x, const int32_t* ids, const float* w,
+                      const void* wg, const void* wu, const void* wd, int C, T* out, float* dwg, float* dwu,
+                      float* dwd, float* dscore, int accumulate, void* ws, uint64_t ws_bytes, cudaStream_t st) {
+  const memfine_dims& d = h->d;
+  int E = d.num_experts, El = E / d.ep_size, k = d.topk, hd = d.hidden, g = d.ffn;
+  if (int rc = ep_gather_counts(h, ids, C, st)) return (memfine_status)rc;
+  std::vector<EpChunk> tab;
+  int64_t rows_max = 0, send_max = 0;
+  for (int j = 0; j < C; j++) {
+    tab.push_back(ep_chunk_table(d, h->counts_h, C, j));
+    rows_max = std::max(rows_max, tab[j].rows_pad);
+    send_max = std::max(send_max, tab[j].send);
+  }
+  Layout L = carve(d, C, pass, ws, rows_max, send_max);
+  if (L.total > ws_bytes) return MEMFINE_ERR_WORKSPACE;
+  h->last_meta = L.meta_bytes;
+  h->last_row_bytes = L.row_bytes;
+  size_t rb = (size_t)hd * sizeof(T);
+  if (pass == MEMFINE_BWD) {
+    if (!accumulate) {
+      size_t wb = sizeof(float) * (size_t)El * g * hd;
+      MF_CUDA_OK(cudaMemsetAsync(dwg, 0, wb, st));
+      MF_CUDA_OK(cudaMemsetAsync(dwu, 0, wb, st));
+      MF_CUDA_OK(cudaMemsetAsync(dwd, 0, wb, st));
+    }
+    if (dscore && d.tokens > 0) MF_CUDA_OK(cudaMemsetAsync(dscore, 0, sizeof(float) * d.tokens * k, st));
+  }
+  for (int j = 0; j < C; j++) {
+    const EpChunk& t = tab[j];
+    int64_t t0 = chunk_begin(d.tokens, C, j), t1 = chunk_begin(d.tokens, C, j + 1);
+    int NB = (int)ceil_div64(t1 - t0, kTokPerBlk);
+    // A5/B1: permute my chunk into the send layout
+    ChunkMeta ms = L.m;
+    ms.src_of = nullptr;
+    ms.w_row = L.send_w;
+    ms.dw_row = nullptr;
+    if (NB) {
+      launch_dispatch_hist(ids, t0, t1, k, E, L.m, h->status_d, st);
+      launch_dispatch_scan(NB, E, El, d.ep_size, L.rows_cap, L.m, nullptr, nullptr, j, st);
+      launch_dispatch_scatter<T>(x, pass == MEMFINE_BWD ? dy : nullptr, ids, w, t0, t1, k, E, hd, ms, (T*)L.send,
+                                 pass == MEMFINE_BWD ? (T*)L.send_dy : nullptr, st);
+      h->last.kernel_launches += 3;
+    }
+    launch_ep_recv_seg(h->counts_d, C, j, E, El, d.ep_rank, d.ep_size, L.rows_cap, L.m, h->rows_d,
+                       h->rows_d + kMaxSub, st);
+    // A6/B1: dispatch all-to-allv
+    if (ep_exchange(h, t, h->counts_h, C, j, true, (char*)L.send, (char*)L.X, rb, st)) return MEMFINE_ERR_NCCL;
+    if (pass == MEMFINE_BWD) {
+      if (ep_exchange(h, t, h->counts_h, C, j, true, (char*)L.send_dy, (char*)L.DY, rb, st)) return MEMFINE_ERR_NCCL;
+      if (ep_exchange(h, t, h->counts_h, C, j, true, (char*)L.send_w, (char*)L.m.w_row, 4, st))
+        return MEMFINE_ERR_NCCL;
+      if (t.rows_pad) MF_CUDA_OK(cudaMemsetAsync(L.m.dw_row, 0, sizeof(float) * t.rows_pad, st));
+    }
+    launch_zero_padding<T>(El, hd, L.m, (T*)L.X, pass == MEMFINE_BWD ? (T*)L.DY : nullptr, st);
+    h->last.kernel_launches += 2;
+    GemmProblem<T> p = base_problem<T>(h, L, wg, wu, wd);
+    p.dWg = dwg;
+    p.dWu = dwu;
+    p.dWd = dwd;
+    if (pass == MEMFINE_FWD) {
+      p.kind = GK_GATEUP;
+      p.store_a = 1;
+      if (int rc = run_gemm<T>(h, p, st)) return (memfine_status)rc;
+      p.kind = GK_DOWN;
+      if (int rc = run_gemm<T>(h, p, st)) return (memfine_status)rc;
+      // A9: combine all-to-allv back into my send layout, then A10
+      if (ep_exchange(h, t, h->counts_h, C, j, false, (char*)L.send, (char*)L.O, rb, st)) return MEMFINE_ERR_NCCL;
+      if (t1 > t0) launch_combine<T>((const T*)L.send, w, t0, t1, k, hd, L.m, out, st);
+    } else {
+      p.kind = GK_GATEUP;
+      p.store_a = 0;
+      p.store_gu = 1;
+      if (int rc = run_gemm<T>(h, p, st)) return (memfine_status)rc;
+      p.kind = GK_DACT;
+      if (int rc = run_gemm<T>(h, p, st)) return (memfine_status)rc;
+      p.kind = GK_WGRAD_DOWN;
+      if (int rc = run_gemm<T>(h, p, st)) return (memfine_status)rc;
+      p.kind = GK_WGRAD_GU;
+      if (int rc = run_gemm<T>(h, p, st)) return (memfine_status)rc;
+      p.kind = GK_DX;
+      if (int rc = run_gemm<T>(h, p, st)) return (memfine_status)rc;
+      // B6: dX rows and d_w back to the source ranks, then B7
+      if (ep_exchange(h, t, h->counts_h, C, j, false, (char*)L.send, (char*)L.O, rb, st)) return MEMFINE_ERR_NCCL;
+      if (ep_exchange(h, t, h->counts_h, C, j, false, (char*)L.send_w, (char*)L.m.dw_row, 4, st))
+        return MEMFINE_ERR_NCCL;
+      ChunkMeta mb = L.m;
+      mb.dw_row = L.send_w;
+      if (t1 > t0) launch_unpermute_reduce<T>((const T*)L.send, t0, t1, k, hd, mb, out, dscore, st);
+    }
+    h->last.kernel_launches += 1;
+  }
+  return latch_cuda(h);
+}
+
+memfine_status memfine_ep_fwd(memfine_handle_s* h, const void* x, const int32_t* ids, const float* w, const void* wg,
+                              const void* wu, const void* wd, int C, void* y, void* ws, uint64_t ws_bytes,
+                              cudaStream_t st) {
+  if (h->d.dtype == MEMFINE_BF16)
+    return ep_run<__nv_bfloat16>(h, MEMFINE_FWD, nullptr, (const __nv_bfloat16*)x, ids, w, wg, wu, wd, C,
+                                 (__nv_bfloat16*)y, nullptr, nullptr, nullptr, nullptr, 0, ws, ws_bytes, st);
+  return ep_run<float>(h, MEMFINE_FWD, nullptr, (const float*)x, ids, w, wg, wu, wd, C, (float*)y, nullptr, nullptr,
+                       nullptr, nullptr, 0, ws, ws_bytes, st);
+}
+
+memfine_status memfine_ep_bwd(memfine_handle_s* h, const void* dy, const void* x, const int32_t* ids, const float* w,
+                              const void* wg, const void* wu, const void* wd, int C, void* dx, float* dwg, float* dwu,
+                              float* dwd, float* dscore, int accumulate, void* ws, uint64_t ws_bytes,
+                              cudaStream_t st) {
+  if (h->d.dtype == MEMFINE_BF16)
+    return ep_run<__nv_bfloat16>(h, MEMFINE_BWD, (const __nv_bfloat16*)dy, (const __nv_bfloat16*)x, ids, w, wg, wu,
+                                 wd, C, (__nv_bfloat16*)dx, dwg, dwu, dwd, dscore, accumulate, ws, ws_bytes, st);
+  return ep_run<float>(h, MEMFINE_BWD, (const float*)dy, (const float*)x, ids, w, wg, wu, wd, C, (float*)dx, dwg,
+                       dwu, dwd, dscore, accumulate, ws, ws_bytes, st);
+}
+
+void begin_call(memfine_handle_s* h, int C, int pass, uint64_t ws_bytes, cudaStream_t st) {
+  h->last = memfine_stats{};
+  h->last.C = C;
+  h->last.pass = pass;
+  h->last.workspace_given_bytes = ws_bytes;
+  // rows_h is written by the scan kernels in stream order; clear it in stream order too.
+  cudaMemsetAsync(h->rows_d, 0, sizeof(int64_t) * 2 * kMaxSub, st);
+}
+
+}  // namespace
+
+// =================================================================================== C ABI
+extern "C" {
+
+int32_t memfine_abi_version(void) { return MEMFINE_ABI_VERSION; }
+
+const char* memfine_status_str(memfine_status s) {
+  switch (s) {
+    case MEMFINE_OK: return "ok";
+    case MEMFINE_ERR_INVALID_ARG: return "invalid argument";
+    case MEMFINE_ERR_INFEASIBLE: return "infeasible: the static memory or the budget leaves no room (Eq. 3/8)";
+    case MEMFINE_ERR_ROUTING: return "routing: expert id outside [0, E)";
+    case MEMFINE_ERR_CUDA: return "CUDA error (or no sm_100 device)";
+    case MEMFINE_ERR_NCCL: return "NCCL error (or libnccl.so.2 not loadable)";
+    case MEMFINE_ERR_WORKSPACE: return "workspace smaller than memfine_workspace_bytes()";
+    case MEMFINE_ERR_UNSUPPORTED: return "unsupported shape";
+  }
+  return "unknown status";
+}
+
+memfine_status memfine_nccl_unique_id(uint8_t out_id[128]) {
+  if (!out_id) return MEMFINE_ERR_INVALID_ARG;
+  return nccl_get_unique_id(out_id) ? MEMFINE_ERR_NCCL : MEMFINE_OK;
+}
+
+memfine_status memfine_create(const memfine_dims* dims, const uint8_t* nccl_unique_id, memfine_handle_t* out) {
+  if (!out || !dims_ok(dims)) return MEMFINE_ERR_INVALID_ARG;
+  if ((dims->ep_size > 1) != (nccl_unique_id != nullptr)) return MEMFINE_ERR_INVALID_ARG;
+  *out = nullptr;
+  int dev;
+  if (cudaGetDevice(&dev) != cudaSuccess) { cudaGetLastError(); return MEMFINE_ERR_CUDA; }
+  cudaDeviceProp prop;
+  if (cudaGetDeviceProperties(&prop, dev) != cudaSuccess) { cudaGetLastError(); return MEMFINE_ERR_CUDA; }
+  if (prop.major != 10 || prop.minor != 0) return MEMFINE_ERR_CUDA;  // built for sm_100a only
+  memfine_handle_s* h = new memfine_handle_s();
+  h->d = *dims;
+  h->device = dev;
+  h->num_sms = prop.multiProcessorCount;
+  if (cudaHostAlloc((void**)&h->status_h, sizeof(int) * 4, cudaHostAllocMapped) != cudaSuccess ||
+      cudaHostAlloc((void**)&h->rows_h, sizeof(int64_t) * 2 * kMaxSub, cudaHostAllocMapped) != cudaSuccess) {
+    memfine_destroy(h);
+    return MEMFINE_ERR_CUDA;
+  }
+  memset(h->status_h, 0, sizeof(int) * 4);
+  memset(h->rows_h, 0, sizeof(int64_t) * 2 * kMaxSub);
+  cudaHostGetDevicePointer((void**)&h->status_d, h->status_h, 0);
+  cudaHostGetDevicePointer((void**)&h->rows_d, h->rows_h, 0);
+  cudaEventCreateWithFlags(&h->ev, cudaEventDisableTiming);
+  if (dims->ep_size > 1) {
+    if (nccl_comm_init(&h->comm, nccl_unique_id, dims->ep_size, dims->ep_rank)) {
+      memfine_destroy(h);
+      return MEMFINE_ERR_NCCL;
+    }
+  }
+  *out = h;
+  return MEMFINE_OK;
+}
+
+memfine_status memfine_destroy(memfine_handle_t h) {
+  if (!h) return MEMFINE_ERR_INVALID_ARG;
+  if (h->comm.comm) nccl_comm_destroy(&h->comm);
+  if (h->status_h) cudaFreeHost(h->status_h);
+  if (h->rows_h) cudaFreeHost(h->rows_h);
+  if (h->counts_d) cudaFree(h->counts_d);
+  if (h->counts_h) cudaFreeHost(h->counts_h);
+  if (h->ev) cudaEventDestroy(h->ev);
+  delete h;
+  return MEMFINE_OK;
+}
+
+memfine_status memfine_route_counts(memfine_handle_t h, const int32_t* ids_dev, int32_t nsub, int32_t* counts_dev,
+                                    void* stream) {
+  if (!h || (!ids_dev && h->d.tokens > 0) || !counts_dev || nsub < 1 || nsub > kMaxSub)
+    return MEMFINE_ERR_INVALID_ARG;
+  cudaStream_t st = (cudaStream_t)stream;
+  const memfine_dims& d = h->d;
+  int* mine = counts_dev + (int64_t)d.ep_rank * nsub * d.num_experts;
+  launch_route_hist(ids_dev, d.tokens, d.topk, d.num_experts, nsub, mine, h->status_d, st);
+  if (cudaGetLastError() != cudaSuccess) return MEMFINE_ERR_CUDA;
+  if (d.ep_size > 1) {
+    if (nccl_all_gather_int(&h->comm, mine, counts_dev, (size_t)nsub * d.num_experts, st)) return MEMFINE_ERR_NCCL;
+  }
+  return MEMFINE_OK;
+}
+
+memfine_status memfine_plan(const int32_t* counts, int32_t nsub, const memfine_dims* dims, const memfine_budget* budget,
+                            memfine_plan_info* info) {
+  if (!counts || !info) return MEMFINE_ERR_INVALID_ARG;
+  PlanParams p;
+  if (int rc = budget_to_params(dims, budget, nsub, &p)) return (memfine_status)rc;
+  memset(info, 0, sizeof *info);
+  if (is_device_ptr(counts)) {
+    // A3 on the device: the single-CTA tuner kernel reads the (all-gathered) counts in HBM.
+    memfine_plan_info* out_h = nullptr;
+    int* rc_h = nullptr;
+    if (cudaHostAlloc((void**)&out_h, sizeof(memfine_plan_info) + 16, cudaHostAllocMapped) != cudaSuccess)
+      return MEMFINE_ERR_CUDA;
+    rc_h = (int*)(out_h + 1);
+    *rc_h = -1;
+    memfine_plan_info* out_d;
+    int* rc_d;
+    cudaHostGetDevicePointer((void**)&out_d, out_h, 0);
+    rc_d = (int*)(out_d + 1);
+    cudaStream_t st;
+    cudaDeviceSynchronize();  // counts may come from any stream of the caller
+    cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking);
+    launch_plan_kernel(counts, p, out_d, rc_d, st);
+    cudaError_t e = cudaStreamSynchronize(st);
+    cudaStreamDestroy(st);
+    int rc = *rc_h;
+    *info = *out_h;
+    cudaFreeHost(out_h);
+    if (e != cudaSuccess) return MEMFINE_ERR_CUDA;
+    return (memfine_status)rc;
+  }
+  // Host counts: same evaluation on the CPU.
+  std::vector<int64_t> sub((size_t)p.EP * nsub, 0);
+  int El = p.E / p.EP;
+  for (int src = 0; src < p.EP; src++)
+    for (int j = 0; j < nsub; j++)
+      for (int e = 0; e < p.E; e++) sub[(size_t)(e / El) * nsub + j] += counts[((int64_t)src * nsub + j) * p.E + e];
+  return (memfine_status)plan_from_subsums(sub.data(), p, info);
+}
+
+memfine_status memfine_workspace_bytes(const int32_t* counts_host, int32_t nsub, const memfine_dims* dims, int32_t C,
+                                       int32_t pass, uint64_t* bytes) {
+  if (!dims_ok(dims) || !bytes || C < 1 || C > kMaxSub || (pass != MEMFINE_FWD && pass != MEMFINE_BWD))
+    return MEMFINE_ERR_INVALID_ARG;
+  const memfine_dims& d = *dims;
+  int El = d.num_experts / d.ep_size;
+  int64_t rows_pad_max = 0, send_max = 0;
+  if (counts_host) {
+    if (nsub < 1 || nsub > kMaxSub || nsub % C) return MEMFINE_ERR_INVALID_ARG;
+    std::vector<int64_t> rows, rows_pad, send;
+    chunk_rows(counts_host, nsub, d, C, d.ep_rank, rows, rows_pad, &send);
+    for (int j = 0; j < C; j++) {
+      rows_pad_max = std::max(rows_pad_max, rows_pad[j]);
+      send_max = std::max(send_max, send[j]);
+    }
+  } else {
+    int64_t Tm = tmax_chunk(d, C);
+    int64_t total = (int64_t)d.ep_size * Tm * d.topk;  // duplicates in a token's top-k are legal
+    rows_pad_max = round_up64(total + (int64_t)El * (kRowAlign - 1), kRowAlign);
+    send_max = Tm * d.topk;
+  }
+  Layout L = carve(d, C, pass, nullptr, rows_pad_max, d.ep_size > 1 ? send_max : 0);
+  *bytes = L.total;
+  return MEMFINE_OK;
+}
+
+memfine_status memfine_moe_fwd(memfine_handle_t h, const void* x, const int32_t* ids, const float* w,
+                               const void* w_gate, const void* w_up, const void* w_down, int32_t C, void* y, void* ws,
+                               uint64_t ws_bytes, void* stream) {
+  if (!h || C < 1 || C > kMaxSub) return MEMFINE_ERR_INVALID_ARG;
+  if (h->d.tokens > 0 && (!x || !ids || !w || !y)) return MEMFINE_ERR_INVALID_ARG;
+  if (!w_gate || !w_up || !w_down || !ws) return MEMFINE_ERR_INVALID_ARG;
+  cudaStream_t st = (cudaStream_t)stream;
+  begin_call(h, C, MEMFINE_FWD, ws_bytes, st);
+  if (h->d.ep_size > 1) return memfine_ep_fwd(h, x, ids, w, w_gate, w_up, w_down, C, y, ws, ws_bytes, st);
+  if (h->d.dtype == MEMFINE_BF16)
+    return fwd_ep1<__nv_bfloat16>(h, (const __nv_bfloat16*)x, ids, w, w_gate, w_up, w_down, C, (__nv_bfloat16*)y, ws,
+                                  ws_bytes, st);
+  return fwd_ep1<float>(h, (const float*)x, ids, w, w_gate, w_up, w_down, C, (float*)y, ws, ws_bytes, st);
+}
+
+memfine_status memfine_moe_bwd(memfine_handle_t h, const void* dy, const void* x, const int32_t* ids, const float* w,
+                               const void* w_gate, const void* w_up, const void* w_down, int32_t C, void* dx,
+                               float* dw_gate, float* dw_up, float* dw_down, float* dscore, int32_t accumulate_dw,
+                               void* ws, uint64_t ws_bytes, void* stream) {
+  if (!h || C < 1 || C > kMaxSub) return MEMFINE_ERR_INVALID_ARG;
+  if (h->d.tokens > 0 && (!dy || !x || !ids || !w || !dx)) return MEMFINE_ERR_INVALID_ARG;
+  if (!w_gate || !w_up || !w_down || !dw_gate || !dw_up || !dw_down || !ws) return MEMFINE_ERR_INVALID_ARG;
+  cudaStream_t st = (cudaStream_t)stream;
+  begin_call(h, C, MEMFINE_BWD, ws_bytes, st);
+  if (h->d.ep_size > 1)
+    return memfine_ep_bwd(h, dy, x, ids, w, w_gate, w_up, w_down, C, dx, dw_gate, dw_up, dw_down, dscore,
+                          accumulate_dw, ws, ws_bytes, st);
+  if (h->d.dtype == MEMFINE_BF16)
+    return bwd_ep1<__nv_bfloat16>(h, (const __nv_bfloat16*)dy, (const __nv_bfloat16*)x, ids, w, w_gate, w_up, w_down,
+                                  C, (__nv_bfloat16*)dx, dw_gate, dw_up, dw_down, dscore, accumulate_dw, ws, ws_bytes,
+                                  st);
+  return bwd_ep1<float>(h, (const float*)dy, (const float*)x, ids, w, w_gate, w_up, w_down, C, (float*)dx, dw_gate,
+                        dw_up, dw_down, dscore, accumulate_dw, ws, ws_bytes, st);
+}
+
+memfine_status memfine_sync(memfine_handle_t h, void* stream) {
+  if (!h) return MEMFINE_ERR_INVALID_ARG;
+  if (cudaStreamSynchronize((cudaStream_t)stream) != cudaSuccess) { cudaGetLastError(); return MEMFINE_ERR_CUDA; }
+  int e = __atomic_exchange_n(h->status_h, 0, __ATOMIC_SEQ_CST);
+  if (e) h->last.device_error = e;
+  // stats: rows per chunk and the workspace high-water they imply
+  uint64_t maxpad = 0;
+  for (int j = 0; j < h->last.C && j < kMaxSub; j++) {
+    h->last.rows[j] = h->rows_h[j];
+    h->last.rows_padded[j] = h->rows_h[kMaxSub + j];
+    maxpad = std::max<uint64_t>(maxpad, (uint64_t)h->rows_h[kMaxSub + j]);
+  }
+  if (h->last.C) h->last.workspace_used_bytes = h->last_meta + maxpad * h->last_row_bytes;
+  if (!e && h->last.workspace_used_bytes > h->last.workspace_given_bytes && h->last.C) e = MEMFINE_ERR_WORKSPACE;
+  return (memfine_status)e;
+}
+
+memfine_status memfine_last_stats(memfine_handle_t h, memfine_stats* out) {
+  if (!h || !out) return MEMFINE_ERR_INVALID_ARG;
+  *out = h->last;
+  return MEMFINE_OK;
+}
+
+memfine_status memfine_set_debug(memfine_handle_t h, int32_t enable) {
+  if (!h) return MEMFINE_ERR_INVALID_ARG;
+  h->debug = enable ? 1 : 0;
+  return MEMFINE_OK;
+}
+
+memfine_status memfine_debug_perm(memfine_handle_t h, int32_t chunk, int64_t* perm_host, int64_t cap, int64_t* n) {
+  if (!h || !n || chunk < 0 || chunk >= (int)h->debug_perm.size()) return MEMFINE_ERR_INVALID_ARG;
+  const auto& v = h->debug_perm[chunk];
+  *n = (int64_t)v.size();
+  if (perm_host) {
+    if (cap < (int64_t)v.size()) return MEMFINE_ERR_INVALID_ARG;
+    for (size_t i = 0; i < v.size(); i++) perm_host[i] = v[i];
+  }
+  return MEMFINE_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,486 @@
+// route.cu — routing histogram, stable dispatch permute, combine, unpermute-reduce and the
+// MACT tuner kernel.  HBM-bound data movement:
+// 16-byte vector loads/stores along contiguous rows, one warp per routed copy / token.
+#include "kernels.h"
+
+namespace memfine {
+
+// ------------------------------------------------------------------------------------------
+// A1: per-sub-chunk expert histogram ("first notification").
+// Token i belongs to sub-chunk j = floor((nsub*(i+1) - 1) / T)  (inverse of floor(jT/nsub)).
+// ------------------------------------------------------------------------------------------
+constexpr int kHistTok = 256;
+constexpr int kHistSpan = 4;  // sub-chunks one block may privatise in smem
+
+__global__ void route_hist_kernel(const int32_t* __restrict__ ids, int64_t T, int k, int E, int nsub,
+                                  int* __restrict__ counts, int* status) {
+  extern __shared__ int sh[];
+  int64_t b0 = (int64_t)blockIdx.x * kHistTok;
+  int64_t b1 = min(b0 + kHistTok, T);
+  if (b0 >= b1) return;
+  int j0 = (int)((nsub * (b0 + 1) - 1) / T);
+  int j1 = (int)((nsub * b1 - 1) / T);
+  bool priv = (j1 - j0 + 1) <= kHistSpan;
+  if (priv) {
+    for (int i = threadIdx.x; i < (j1 - j0 + 1) * E; i += blockDim.x) sh[i] = 0;
+    __syncthreads();
+  }
+  for (int64_t q = b0 * k + threadIdx.x; q < b1 * k; q += blockDim.x) {
+    int e = __ldg(ids + q);
+    int64_t i = q / k;
+    int j = (int)((nsub * (i + 1) - 1) / T);
+    if (e < 0 || e >= E) { latch_error(status, MEMFINE_ERR_ROUTING); continue; }
+    if (priv) atomicAdd(&sh[(j - j0) * E + e], 1);
+    else atomicAdd(&counts[(int64_t)j * E + e], 1);
+  }
+  if (priv) {
+    __syncthreads();
+    for (int i = threadIdx.x; i < (j1 - j0 + 1) * E; i += blockDim.x)
+      if (sh[i]) atomicAdd(&counts[(int64_t)j0 * E + i], sh[i]);
+  }
+}
+
+void launch_route_hist(const int32_t* ids, int64_t T, int k, int E, int nsub, int* counts, int* status,
+                       cudaStream_t st) {
+  cudaMemsetAsync(counts, 0, sizeof(int) * (size_t)nsub * E, st);
+  if (T == 0) return;
+  int64_t nb = ceil_div64(T, kHistTok);
+  size_t smem = sizeof(int) * (size_t)kHistSpan * E;
+  route_hist_kernel<<<(unsigned)nb, 256, smem, st>>>(ids, T, k, E, nsub, counts, status);
+}
+
+// ------------------------------------------------------------------------------------------
+// A5 dispatch, pass 1: per token-block expert histogram of the chunk.
+// ------------------------------------------------------------------------------------------
+__global__ void dispatch_hist_kernel(const int32_t* __restrict__ ids, int64_t t0, int64_t t1, int k, int E,
+                                     int* __restrict__ blk_cnt, int* status) {
+  extern __shared__ int sc[];
+  for (int e = threadIdx.x; e < E; e += blockDim.x) sc[e] = 0;
+  __syncthreads();
+  int64_t b0 = t0 + (int64_t)blockIdx.x * kTokPerBlk;
+  int64_t b1 = min(b0 + kTokPerBlk, t1);
+  for (int64_t q = b0 * k + threadIdx.x; q < b1 * k; q += blockDim.x) {
+    int e = __ldg(ids + q);
+    if (e >= 0 && e < E) atomicAdd(&sc[e], 1);
+    else latch_error(status, MEMFINE_ERR_ROUTING);
+  }
+  __syncthreads();
+  for (int e = threadIdx.x; e < E; e += blockDim.x) blk_cnt[(int64_t)blockIdx.x * E + e] = sc[e];
+}
+
+void launch_dispatch_hist(const int32_t* ids, int64_t t0, int64_t t1, int k, int E, const ChunkMeta& m,
+                          int* status, cudaStream_t st) {
+  int NB = (int)ceil_div64(t1 - t0, kTokPerBlk);
+  if (NB == 0) return;
+  dispatch_hist_kernel<<<NB, 256, sizeof(int) * E, st>>>(ids, t0, t1, k, E, m.blk_cnt, status);
+}
+
+// ------------------------------------------------------------------------------------------
+// A5 dispatch, pass 2 (one CTA): exclusive scan over blocks per expert, expert bases, info.
+//  ep_size == 1: base[e] = padded prefix (every local expert's segment padded to 128 rows);
+//  ep_size  > 1: base[e] = unpadded prefix over global experts (the NCCL send layout:
+//                dest rank major because ranks hold contiguous expert blocks).
+// ------------------------------------------------------------------------------------------
+__global__ void dispatch_scan_kernel(int NB, int E, int El, int ep_size, int64_t rows_cap,
+                                     int* __restrict__ blk, int* __restrict__ exp_cnt, int* __restrict__ recv_cnt,
+                                     int* __restrict__ seg, int* __restrict__ info,
+                                     int64_t* stats_rows, int64_t* stats_rows_pad, int chunk) {
+  __shared__ int base[1024];
+  for (int e = threadIdx.x; e < E; e += blockDim.x) {
+    int run = 0;
+    for (int b = 0; b < NB; b++) {
+      int c = blk[(int64_t)b * E + e];
+      blk[(int64_t)b * E + e] = run;
+      run += c;
+    }
+    exp_cnt[e] = run;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int acc = 0, send = 0;
+    for (int e = 0; e < E; e++) {
+      int c = exp_cnt[e];
+      send += c;
+      if (ep_size == 1) {
+        base[e] = acc;
+        seg[e] = acc;
+        recv_cnt[e] = c;
+        acc += (int)round_up64(c, kRowAlign);
+      } else {
+        base[e] = acc;
+        acc += c;
+      }
+    }
+    if (ep_size == 1) {
+      seg[El] = acc;
+      info[kInfoRows] = send;
+      info[kInfoRowsPad] = acc;
+      info[kInfoSkip] = (acc > rows_cap) ? 1 : 0;
+      if (stats_rows) { stats_rows[chunk] = send; stats_rows_pad[chunk] = acc; }
+    } else {
+      info[kInfoSkip] = 0;  // EP>1: the host checked the capacity exactly (it knows the counts)
+    }
+    info[kInfoSend] = send;
+  }
+  __syncthreads();
+  for (int64_t i = threadIdx.x; i < (int64_t)NB * E; i += blockDim.x) blk[i] += base[i % E];
+}
+
+void launch_dispatch_scan(int NB, int E, int El, int ep_size, int64_t rows_cap, const ChunkMeta& m,
+                          int64_t* stats_rows, int64_t* stats_rows_pad, int chunk, cudaStream_t st) {
+  dispatch_scan_kernel<<<1, 1024, 0, st>>>(NB, E, El, ep_size, rows_cap, m.blk_cnt, m.exp_cnt, m.recv_cnt,
+                                           m.seg, m.info, stats_rows, stats_rows_pad, chunk);
+}
+
+// ------------------------------------------------------------------------------------------
+// A5/B1 dispatch, pass 3: stable in-block rank (canonical order (expert, token, slot),
+// reading R3) then one warp per copy moves the token row(s) with 16-byte vectors.
+// ------------------------------------------------------------------------------------------
+template <typename T>
+__device__ __forceinline__ void copy_row(T* __restrict__ dst, const T* __restrict__ src, int h, int lane) {
+  constexpr int V = 16 / sizeof(T);
+  const uint4* s = reinterpret_cast<const uint4*>(src);
+  uint4* d = reinterpret_cast<uint4*>(dst);
+  int nv = h / V;
+  int i = lane;
+  for (; i + 96 < nv; i += 128) {
+    uint4 a = __ldg(s + i), b = __ldg(s + i + 32), c = __ldg(s + i + 64), e = __ldg(s + i + 96);
+    d[i] = a; d[i + 32] = b; d[i + 64] = c; d[i + 96] = e;
+  }
+  for (; i < nv; i += 32) d[i] = __ldg(s + i);
+}
+
+template <typename T>
+__global__ void __launch_bounds__(256) dispatch_scatter_kernel(
+    const T* __restrict__ x, const T* __restrict__ dy, const int32_t* __restrict__ ids, const float* __restrict__ w,
+    int64_t t0, int64_t t1, int k, int E, int h, const int* __restrict__ blk_off, int* __restrict__ dest_of,
+    int* __restrict__ src_of, float* __restrict__ w_row, float* __restrict__ dw_row, const int* __restrict__ info,
+    T* __restrict__ xd, T* __restrict__ dyd) {
+  if (info[kInfoSkip]) return;
+  extern __shared__ int smem[];
+  int* run = smem;        // [E]
+  int* spos = smem + E;   // [kTokPerBlk * k]
+  int64_t b0 = t0 + (int64_t)blockIdx.x * kTokPerBlk;
+  int64_t b1 = min(b0 + kTokPerBlk, t1);
+  int ncp = (int)(b1 - b0) * k;
+  for (int e = threadIdx.x; e < E; e += blockDim.x) run[e] = blk_off[(int64_t)blockIdx.x * E + e];
+  __syncthreads();
+  int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (warp == 0) {
+    unsigned lt = (1u << lane) - 1u;
+    for (int base = 0; base < ncp; base += 32) {
+      int q = base + lane;
+      int e = -1;
+      if (q < ncp) {
+        e = __ldg(ids + b0 * k + q);
+        if (e < 0 || e >= E) e = -1;
+      }
+      unsigned peers = __match_any_sync(0xffffffffu, e);
+      int p = -1;
+      if (e >= 0) p = run[e] + __popc(peers & lt);
+      __syncwarp();
+      bool last = (peers >> lane) == 1u;  // highest lane of its group
+      if (e >= 0 && last) run[e] += __popc(peers);
+      __syncwarp();
+      if (q < ncp) spos[q] = p;
+    }
+  }
+  __syncthreads();
+  int nw = blockDim.x >> 5;
+  for (int q = warp; q < ncp; q += nw) {
+    int p = spos[q];
+    int64_t qg = b0 * k + q;  // global copy index i*k + slot
+    if (lane == 0) dest_of[qg - t0 * k] = p;
+    if (p < 0) continue;
+    if (lane == 0) {
+      if (src_of) src_of[p] = (int)qg;
+      if (w_row) w_row[p] = __ldg(w + qg);
+      if (dw_row) dw_row[p] = 0.0f;
+    }
+    int64_t i = qg / k;
+    copy_row<T>(xd + (int64_t)p * h, x + i * h, h, lane);
+    if (dy) copy_row<T>(dyd + (int64_t)p * h, dy + i * h, h, lane);
+  }
+}
+
+template <typename T>
+void launch_dispatch_scatter(const T* x, const T* dy, const int32_t* ids, const float* w, int64_t t0, int64_t t1,
+                             int k, int E, int h, const ChunkMeta& m, T* xd, T* dyd, cudaStream_t st) {
+  int NB = (int)ceil_div64(t1 - t0, kTokPerBlk);
+  if (NB == 0) return;
+  size_t smem = sizeof(int) * ((size_t)E + (size_t)kTokPerBlk * k);
+  dispatch_scatter_kernel<T><<<NB, 256, smem, st>>>(x, dy, ids, w, t0, t1, k, E, h, m.blk_cnt, m.dest_of,
+                                                    m.src_of, m.w_row, dy ? m.dw_row : nullptr, m.info, xd, dyd);
+}
+
+// Zero the padding rows of each local expert segment (so padded rows contribute exact
+// zeros to the weight-gradient reductions over tokens).
+template <typename T>
+__global__ void zero_padding_kernel(const int* __restrict__ seg, const int* __restrict__ recv_cnt, int h,
+                                    const int* __restrict__ info, T* __restrict__ xd, T* __restrict__ dyd,
+                                    int* __restrict__ src_of, float* __restrict__ w_row, float* __restrict__ dw_row) {
+  if (info[kInfoSkip]) return;
+  int e = blockIdx.x;
+  int r0 = seg[e] + recv_cnt[e], r1 = seg[e + 1];
+  int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+  constexpr int V = 16 / sizeof(T);
+  for (int r = r0 + warp; r < r1; r += nw) {
+    uint4 z = make_uint4(0, 0, 0, 0);
+    uint4* a = reinterpret_cast<uint4*>(xd + (int64_t)r * h);
+    for (int i = lane; i < h / V; i += 32) a[i] = z;
+    if (dyd) {
+      uint4* b = reinterpret_cast<uint4*>(dyd + (int64_t)r * h);
+      for (int i = lane; i < h / V; i += 32) b[i] = z;
+    }
+    if (lane == 0) {
+      if (src_of) src_of[r] = -1;
+      if (w_row) w_row[r] = 0.0f;
+      if (dw_row) dw_row[r] = 0.0f;
+    }
+  }
+}
+
+template <typename T>
+void launch_zero_padding(int El, int h, const ChunkMeta& m, T* xd, T* dyd, cudaStream_t st) {
+  zero_padding_kernel<T><<<El, 256, 0, st>>>(m.seg, m.recv_cnt, h, m.info, xd, dyd, m.src_of, m.w_row,
+                                              dyd ? m.dw_row : nullptr);
+}
+
+// ------------------------------------------------------------------------------------------
+// A10: combine fused into the unpermute: Y_i = sum_{slot asc} w_{i,slot} * o[pos(i,slot)],
+// fp32 accumulation, one rounding (Table 2 row 13 "score mul").
+// ------------------------------------------------------------------------------------------
+template <typename T>
+__device__ __forceinline__ void load8(const T* p, float v[8]);
+template <>
+__device__ __forceinline__ void load8<__nv_bfloat16>(const __nv_bfloat16* p, float v[8]) {
+  uint4 u = __ldg(reinterpret_cast<const uint4*>(p));
+  const __nv_bfloat162* b = reinterpret_cast<const __nv_bfloat162*>(&u);
+#pragma unroll
+  for (int i = 0; i < 4; i++) { float2 f = __bfloat1622float2(b[i]); v[2 * i] = f.x; v[2 * i + 1] = f.y; }
+}
+template <>
+__device__ __forceinline__ void load8<float>(const float* p, float v[8]) {
+  float4 a = __ldg(reinterpret_cast<const float4*>(p)), b = __ldg(reinterpret_cast<const float4*>(p) + 1);
+  v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w; v[4] = b.x; v[5] = b.y; v[6] = b.z; v[7] = b.w;
+}
+template <typename T>
+__device__ __forceinline__ void store8(T* p, const float v[8]);
+template <>
+__device__ __forceinline__ void store8<__nv_bfloat16>(__nv_bfloat16* p, const float v[8]) {
+  uint4 u;
+  __nv_bfloat162* b = reinterpret_cast<__nv_bfloat162*>(&u);
+#pragma unroll
+  for (int i = 0; i < 4; i++) b[i] = __floats2bfloat162_rn(v[2 * i], v[2 * i + 1]);
+  *reinterpret_cast<uint4*>(p) = u;
+}
+template <>
+__device__ __forceinline__ void store8<float>(float* p, const float v[8]) {
+  reinterpret_cast<float4*>(p)[0] = make_float4(v[0], v[1], v[2], v[3]);
+  reinterpret_cast<float4*>(p)[1] = make_float4(v[4], v[5], v[6], v[7]);
+}
+
+template <typename T, bool WEIGHTED>
+__global__ void __launch_bounds__(256) gather_reduce_kernel(
+    const T* __restrict__ rows, const float* __restrict__ w, int64_t t0, int64_t t1, int k, int h,
+    const int* __restrict__ dest_of, const int* __restrict__ info, T* __restrict__ out,
+    const float* __restrict__ dw_row, float* __restrict__ dscore) {
+  if (info[kInfoSkip]) return;
+  int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  int64_t i = t0 + (int64_t)blockIdx.x * (blockDim.x >> 5) + warp;
+  if (i >= t1) return;
+  int pos[16];
+  float ws[16];
+  int kk = k < 16 ? k : 16;
+  for (int s = 0; s < kk; s++) {
+    pos[s] = dest_of[(i - t0) * k + s];
+    ws[s] = WEIGHTED ? __ldg(w + i * k + s) : 1.0f;
+  }
+  if (dscore && lane < k) {
+    int p = dest_of[(i - t0) * k + lane];
+    dscore[i * k + lane] = p >= 0 ? dw_row[p] : 0.0f;
+  }
+  for (int c = lane * 8; c < h; c += 256) {
+    float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    for (int s = 0; s < kk; s++) {
+      if (pos[s] < 0) continue;
+      float v[8];
+      load8<T>(rows + (int64_t)pos[s] * h + c, v);
+#pragma unroll
+      for (int u = 0; u < 8; u++) acc[u] = fmaf(ws[s], v[u], acc[u]);
+    }
+    store8<T>(out + i * h + c, acc);
+  }
+}
+
+template <typename T>
+void launch_combine(const T* O, const float* w, int64_t t0, int64_t t1, int k, int h, const ChunkMeta& m, T* y,
+                    cudaStream_t st) {
+  int64_t n = t1 - t0;
+  if (n == 0) return;
+  gather_reduce_kernel<T, true><<<(unsigned)ceil_div64(n, 8), 256, 0, st>>>(O, w, t0, t1, k, h, m.dest_of, m.info,
+                                                                           y, nullptr, nullptr);
+}
+
+template <typename T>
+void launch_unpermute_reduce(const T* dXd, int64_t t0, int64_t t1, int k, int h, const ChunkMeta& m, T* dx,
+                             float* dscore, cudaStream_t st) {
+  int64_t n = t1 - t0;
+  if (n == 0) return;
+  gather_reduce_kernel<T, false><<<(unsigned)ceil_div64(n, 8), 256, 0, st>>>(dXd, nullptr, t0, t1, k, h, m.dest_of,
+                                                                            m.info, dx, m.dw_row, dscore);
+}
+
+// EP > 1: received rows per local expert for chunk j from the all-gathered counts
+// [EP][C][E]; padded segment starts (expert-major: local expert, then src rank, reading R3).
+__global__ void ep_recv_seg_kernel(const int* __restrict__ counts, int C, int j, int E, int El, int me, int EP,
+                                   int64_t rows_cap, int* __restrict__ seg, int* __restrict__ recv_cnt,
+                                   int* __restrict__ info, int64_t* stats_rows, int64_t* stats_rows_pad) {
+  if (threadIdx.x != 0) return;
+  int acc = 0, rows = 0;
+  for (int el = 0; el < El; el++) {
+    int c = 0;
+    for (int src = 0; src < EP; src++) c += counts[((int64_t)src * C + j) * E + me * El + el];
+    recv_cnt[el] = c;
+    seg[el] = acc;
+    acc += (int)round_up64(c, kRowAlign);
+    rows += c;
+  }
+  seg[El] = acc;
+  info[kInfoRows] = rows;
+  info[kInfoRowsPad] = acc;
+  info[kInfoSkip] = acc > rows_cap ? 1 : 0;
+  if (stats_rows) { stats_rows[j] = rows; stats_rows_pad[j] = acc; }
+}
+
+void launch_ep_recv_seg(const int* counts, int C, int j, int E, int El, int me, int EP, int64_t rows_cap,
+                        const ChunkMeta& m, int64_t* stats_rows, int64_t* stats_rows_pad, cudaStream_t st) {
+  ep_recv_seg_kernel<<<1, 32, 0, st>>>(counts, C, j, E, El, me, EP, rows_cap, m.seg, m.recv_cnt, m.info, stats_rows,
+                                       stats_rows_pad);
+}
+
+// ------------------------------------------------------------------------------------------
+// A3: MACT tuner.  plan_from_subsums is the one evaluation used by both the host path and
+// the device kernel (same integer arithmetic, so both are bit-identical by construction).
+// ------------------------------------------------------------------------------------------
+__host__ __device__ int plan_from_subsums(const int64_t* sub, const PlanParams& p, memfine_plan_info* out) {
+  memfine_plan_info o;
+  o.C = o.c_theory = o.clamped = o.feasible = o.hot_rank = o.exact_peak = 0;
+  o.s_dd_max = o.s_prime_max = o.s_chunk_max = 0;
+  o.predicted_peak_bytes = 0;
+  // Eq. 8 numerator (bytes): B - M^sta - s-term.
+  unsigned long long B = p.budget;
+  unsigned long long used = p.static_bytes + p.other_bytes;
+  if (used < p.static_bytes || B <= used) { *out = o; return MEMFINE_ERR_INFEASIBLE; }
+  unsigned long long num = B - used;
+  // s'_max = floor(num * tp * cp / (m_g * D_t * b * (2h + 2g)))
+  unsigned long long den = (unsigned long long)p.m_g * p.D_t * p.micro_batch * (2ull * p.h + 2ull * p.g);
+  unsigned long long tc = (unsigned long long)p.tp * p.cp;
+  // num * tc may overflow 64 bits only beyond 2^64 bytes * tc; split the division.
+  unsigned long long q1 = num / den, r1 = num % den;
+  unsigned long long spm = q1 * tc + (r1 * tc) / den;
+  o.s_prime_max = (int64_t)spm;
+  if (spm == 0) { *out = o; return MEMFINE_ERR_INFEASIBLE; }
+  int64_t sdd = -1;
+  int hot = 0;
+  for (int r = 0; r < p.EP; r++) {
+    int64_t s = 0;
+    for (int j = 0; j < p.nsub; j++) s += sub[r * p.nsub + j];
+    if (s > sdd) { sdd = s; hot = r; }
+  }
+  o.s_dd_max = sdd;
+  o.hot_rank = hot;
+  int64_t c = (sdd + (int64_t)spm - 1) / (int64_t)spm;
+  if (c < 1) c = 1;
+  o.c_theory = (int32_t)(c > 0x7fffffff ? 0x7fffffff : c);
+  int C = -1;
+  if (p.rule == MEMFINE_RULE_EQ9) {
+    for (int i = 0; i < p.nbins; i++)
+      if (p.bins[i] >= c) { C = p.bins[i]; break; }
+  } else {
+    for (int i = 0; i < p.nbins; i++)
+      if (p.nsub % p.bins[i] != 0) { *out = o; return MEMFINE_ERR_INVALID_ARG; }
+    for (int i = 0; i < p.nbins && C < 0; i++) {
+      int Cb = p.bins[i], per = p.nsub / Cb;
+      int64_t mx = 0;
+      for (int r = 0; r < p.EP; r++)
+        for (int jc = 0; jc < Cb; jc++) {
+          int64_t s = 0;
+          for (int j = jc * per; j < (jc + 1) * per; j++) s += sub[r * p.nsub + j];
+          if (s > mx) mx = s;
+        }
+      if (mx <= (int64_t)spm) C = Cb;
+    }
+  }
+  if (C < 0) { C = p.bins[p.nbins - 1]; o.clamped = 1; }
+  o.C = C;
+  int64_t mx = 0;
+  if (p.nsub % C == 0) {
+    int per = p.nsub / C;
+    o.exact_peak = 1;
+    for (int r = 0; r < p.EP; r++)
+      for (int jc = 0; jc < C; jc++) {
+        int64_t s = 0;
+        for (int j = jc * per; j < (jc + 1) * per; j++) s += sub[r * p.nsub + j];
+        if (s > mx) mx = s;
+      }
+  } else {
+    o.exact_peak = 0;
+    mx = (sdd + C - 1) / C;
+  }
+  o.s_chunk_max = mx;
+  o.feasible = mx <= (int64_t)spm ? 1 : 0;
+  o.predicted_peak_bytes =
+      ((unsigned long long)p.m_g * p.D_t * p.micro_batch * (unsigned long long)mx * (2ull * p.h + 2ull * p.g)) / tc;
+  *out = o;
+  return MEMFINE_OK;
+}
+
+// One CTA: per-(rank, sub-chunk) received-copy sums via smem reduction, then thread 0
+// evaluates Eqs. 8-9 and the bins; the result lands in pinned mapped host memory.
+__global__ void plan_kernel(const int32_t* __restrict__ counts, PlanParams p, memfine_plan_info* out, int* rc) {
+  extern __shared__ unsigned long long sub_u[];  // [EP * nsub]
+  int n = p.EP * p.nsub;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) sub_u[i] = 0ull;
+  __syncthreads();
+  int El = p.E / p.EP;
+  int64_t total = (int64_t)p.EP * p.nsub * p.E;
+  for (int64_t q = threadIdx.x; q < total; q += blockDim.x) {
+    int e = (int)(q % p.E);
+    int j = (int)((q / p.E) % p.nsub);
+    int r = e / El;
+    int v = counts[q];
+    if (v) atomicAdd(&sub_u[r * p.nsub + j], (unsigned long long)v);
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    *rc = plan_from_subsums(reinterpret_cast<const int64_t*>(sub_u), p, out);
+    __threadfence_system();
+  }
+}
+
+void launch_plan_kernel(const int32_t* counts_dev, const PlanParams& p, memfine_plan_info* out_mapped, int* rc_mapped,
+                        cudaStream_t st) {
+  size_t smem = sizeof(unsigned long long) * (size_t)p.EP * p.nsub;
+  plan_kernel<<<1, 1024, smem, st>>>(counts_dev, p, out_mapped, rc_mapped);
+}
+
+// ------------------------------------------------------------------------------------------
+template void launch_dispatch_scatter<__nv_bfloat16>(const __nv_bfloat16*, const __nv_bfloat16*, const int32_t*,
+                                                     const float*, int64_t, int64_t, int, int, int, const ChunkMeta&,
+                                                     __nv_bfloat16*, __nv_bfloat16*, cudaStream_t);
+template void launch_dispatch_scatter<float>(const float*, const float*, const int32_t*, const float*, int64_t,
+                                             int64_t, int, int, int, const ChunkMeta&, float*, float*, cudaStream_t);
+template void launch_zero_padding<__nv_bfloat16>(int, int, const ChunkMeta&, __nv_bfloat16*, __nv_bfloat16*,
+                                                 cudaStream_t);
+template void launch_zero_padding<float>(int, int, const ChunkMeta&, float*, float*, cudaStream_t);
+template void launch_combine<__nv_bfloat16>(const __nv_bfloat16*, const float*, int64_t, int64_t, int, int,
+                                            const ChunkMeta&, __nv_bfloat16*, cudaStream_t);
+template void launch_combine<float>(const float*, const float*, int64_t, int64_t, int, int, const ChunkMeta&, float*,
+                                    cudaStream_t);
+template void launch_unpermute_reduce<__nv_bfloat16>(const __nv_bfloat16*, int64_t, int64_t, int, int,
+                                                     const ChunkMeta&, __nv_bfloat16*, float*, cudaStream_t);
+template void launch_unpermute_reduce<float>(const float*, int64_t, int64_t, int, int, const ChunkMeta&, float*,
+                                             float*, cudaStream_t);
+
+}  // namespace memfine

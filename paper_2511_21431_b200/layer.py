@@ -1,0 +1,150 @@
+"""Torch-facing wrapper of the C ABI: device memory, streams and EP process groups only.
+
+The names follow include/memfine.h: ``plan`` (memfine_plan), ``workspace_bytes``
+(memfine_workspace_bytes), and on a ``MemFine`` handle ``route_counts``, ``moe_fwd``,
+``moe_bwd``, ``sync``, ``last_stats``.  Nothing here computes any part of the layer.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from typing import Optional
+
+import torch
+
+from . import capi
+
+_DT = {torch.bfloat16: capi.BF16, torch.float32: capi.FP32}
+
+
+def _ptr(t: Optional[torch.Tensor]):
+    return C.c_void_p(t.data_ptr()) if t is not None else None
+
+
+def _stream(stream=None):
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return C.c_void_p(s.cuda_stream)
+
+
+def make_dims(tokens, hidden, ffn, num_experts, topk, ep_size=1, ep_rank=0, dtype=torch.bfloat16) -> capi.Dims:
+    return capi.Dims(int(tokens), int(hidden), int(ffn), int(num_experts), int(topk), int(ep_size), int(ep_rank),
+                     _DT[dtype])
+
+
+def plan(counts: torch.Tensor, dims: capi.Dims, budget: capi.Budget) -> dict:
+    """memfine_plan: counts int32 [EP][nsub][E] on the host (CPU tensor) or the device."""
+    assert counts.dtype == torch.int32 and counts.dim() == 3 and counts.is_contiguous()
+    info = capi.PlanInfo()
+    st = capi.lib().memfine_plan(_ptr(counts), counts.shape[1], C.byref(dims), C.byref(budget), C.byref(info))
+    d = info.as_dict()
+    d["status"] = int(st)
+    return d
+
+
+def workspace_bytes(counts_host: Optional[torch.Tensor], dims: capi.Dims, C_: int, pass_: int) -> int:
+    out = C.c_uint64()
+    if counts_host is not None:
+        assert counts_host.device.type == "cpu" and counts_host.dtype == torch.int32 and counts_host.is_contiguous()
+        nsub = counts_host.shape[1]
+    else:
+        nsub = 0
+    capi.check(capi.lib().memfine_workspace_bytes(_ptr(counts_host), nsub, C.byref(dims), C_, pass_, C.byref(out)),
+               "memfine_workspace_bytes")
+    return int(out.value)
+
+
+class MemFine:
+    """One handle = one EP rank of one MoE layer shape.  ``process_group``: the EP group
+    (torch.distributed) used only to broadcast the NCCL unique id when ep_size > 1."""
+
+    def __init__(self, tokens, hidden, ffn, num_experts, topk, ep_size=1, ep_rank=0, dtype=torch.bfloat16,
+                 process_group=None):
+        self.dims = make_dims(tokens, hidden, ffn, num_experts, topk, ep_size, ep_rank, dtype)
+        self.dtype = dtype
+        self.E_l = num_experts // ep_size
+        uid = None
+        if ep_size > 1:
+            import torch.distributed as dist
+            buf = (C.c_uint8 * 128)()
+            if ep_rank == 0:
+                capi.check(capi.lib().memfine_nccl_unique_id(buf), "memfine_nccl_unique_id")
+            obj = [bytes(buf)]
+            dist.broadcast_object_list(obj, src=dist.get_global_rank(process_group, 0) if process_group else 0,
+                                       group=process_group)
+            uid = (C.c_uint8 * 128).from_buffer_copy(obj[0])
+        h = C.c_void_p()
+        capi.check(capi.lib().memfine_create(C.byref(self.dims), uid, C.byref(h)), "memfine_create")
+        self.h = h
+        self._ws = None
+
+    def close(self):
+        if getattr(self, "h", None):
+            capi.lib().memfine_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    # ------------------------------------------------------------------ A1 + A2
+    def route_counts(self, ids: torch.Tensor, nsub: int = 8, stream=None) -> torch.Tensor:
+        d = self.dims
+        assert ids.dtype == torch.int32 and ids.is_cuda and ids.is_contiguous()
+        counts = torch.empty((d.ep_size, nsub, d.num_experts), dtype=torch.int32, device=ids.device)
+        capi.check(capi.lib().memfine_route_counts(self.h, _ptr(ids), nsub, _ptr(counts), _stream(stream)),
+                   "memfine_route_counts")
+        return counts
+
+    def workspace(self, counts_host, C_: int, pass_: int, device=None) -> torch.Tensor:
+        n = workspace_bytes(counts_host, self.dims, C_, pass_)
+        return torch.empty(n, dtype=torch.uint8, device=device or torch.cuda.current_device())
+
+    # ------------------------------------------------------------------ FCDA forward / backward
+    def moe_fwd(self, x, ids, w, w_gate, w_up, w_down, C_: int, ws: torch.Tensor, y=None, stream=None):
+        if y is None:
+            y = torch.empty_like(x)
+        capi.check(capi.lib().memfine_moe_fwd(self.h, _ptr(x), _ptr(ids), _ptr(w), _ptr(w_gate), _ptr(w_up),
+                                              _ptr(w_down), C_, _ptr(y), _ptr(ws), ws.numel(), _stream(stream)),
+                   "memfine_moe_fwd")
+        return y
+
+    def moe_bwd(self, dy, x, ids, w, w_gate, w_up, w_down, C_: int, ws: torch.Tensor, dx=None, dw_gate=None,
+                dw_up=None, dw_down=None, dscore=None, accumulate_dw=False, want_dscore=True, stream=None):
+        if dx is None:
+            dx = torch.empty_like(x)
+        f32 = dict(dtype=torch.float32, device=x.device)
+        if dw_gate is None:
+            dw_gate = torch.empty(w_gate.shape, **f32)
+        if dw_up is None:
+            dw_up = torch.empty(w_up.shape, **f32)
+        if dw_down is None:
+            dw_down = torch.empty(w_down.shape, **f32)
+        if dscore is None and want_dscore:
+            dscore = torch.empty(w.shape, **f32)
+        capi.check(capi.lib().memfine_moe_bwd(self.h, _ptr(dy), _ptr(x), _ptr(ids), _ptr(w), _ptr(w_gate),
+                                              _ptr(w_up), _ptr(w_down), C_, _ptr(dx), _ptr(dw_gate), _ptr(dw_up),
+                                              _ptr(dw_down), _ptr(dscore), int(bool(accumulate_dw)), _ptr(ws),
+                                              ws.numel(), _stream(stream)),
+                   "memfine_moe_bwd")
+        return dx, dw_gate, dw_up, dw_down, dscore
+
+    def sync(self, stream=None) -> int:
+        return int(capi.lib().memfine_sync(self.h, _stream(stream)))
+
+    def last_stats(self) -> dict:
+        s = capi.Stats()
+        capi.check(capi.lib().memfine_last_stats(self.h, C.byref(s)), "memfine_last_stats")
+        return s.as_dict()
+
+    def set_debug(self, on: bool = True):
+        capi.check(capi.lib().memfine_set_debug(self.h, int(on)), "memfine_set_debug")
+
+    def debug_perm(self, chunk: int):
+        import numpy as np
+        n = C.c_int64()
+        capi.check(capi.lib().memfine_debug_perm(self.h, chunk, None, 0, C.byref(n)), "memfine_debug_perm")
+        out = np.zeros(max(1, n.value), dtype=np.int64)
+        capi.check(capi.lib().memfine_debug_perm(self.h, chunk, out.ctypes.data_as(C.c_void_p), out.size,
+                                                 C.byref(n)), "memfine_debug_perm")
+        return out[:n.value]

@@ -55,15 +55,15 @@ def bf16_bits_to_f32(b: np.ndarray) -> np.ndarray:
     return (b.astype(np.uint32) << 16).view(np.float32)
 
 
-def make_x(T: int, h: int, rank: int = 0, seed: int = 1000) -> torch.Tensor:
-    """bf16 [T, h] activations for one rank (CPU tensor)."""
+def make_x(T: int, h: int, rank: int = 0, seed: int = 1000, dtype=torch.bfloat16) -> torch.Tensor:
+    """[T, h] activations for one rank (CPU tensor; bf16-rounded unless dtype=float32)."""
     gen = torch.Generator().manual_seed(seed + rank)
-    return torch.randn(T, h, generator=gen, dtype=torch.float32).to(torch.bfloat16)
+    return torch.randn(T, h, generator=gen, dtype=torch.float32).to(dtype)
 
 
-def make_dy(T: int, h: int, rank: int = 0, seed: int = 3000) -> torch.Tensor:
+def make_dy(T: int, h: int, rank: int = 0, seed: int = 3000, dtype=torch.bfloat16) -> torch.Tensor:
     gen = torch.Generator().manual_seed(seed + rank)
-    return torch.randn(T, h, generator=gen, dtype=torch.float32).to(torch.bfloat16)
+    return torch.randn(T, h, generator=gen, dtype=torch.float32).to(dtype)
 
 
 def make_expert(e: int, h: int, g: int, seed: int = 7000, dtype=torch.bfloat16):

@@ -1,0 +1,175 @@
+"""CUDA path vs the oracle, element by element, through the C ABI (run with -m gpu).
+
+Integer outputs (routing counts, permutation, C) bit-exact; floating point within the
+north star's tolerance: max|got-ref|/max|ref| <= 2e-2 (bf16), <= 1e-5 (fp32 mode)."""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+from paper_2511_21431_b200 import capi, layer
+from tests.harness import GpuRun, make_problem, oracle_dims, oracle_fwd_bwd, oracle_tokens, rel_err, tol
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _need_gpu():
+    if not torch.cuda.is_available():
+        pytest.skip("needs a CUDA device")
+
+
+def _check_all(p, run, C, ref):
+    y, st, stats, wsb = run.fwd(C)
+    assert st == 0, capi.status_str(st)
+    t = tol(p.dtype)
+    assert rel_err(y.float().cpu().numpy(), ref["y"]) <= t
+    (dx, dwg, dwu, dwd, ds), st, bstats, _ = run.bwd(C)
+    assert st == 0, capi.status_str(st)
+    errs = {
+        "dx": rel_err(dx.float().cpu().numpy(), ref["dx"]),
+        "dscore": rel_err(ds.cpu().numpy(), ref["dscore"]),
+        "dw_gate": rel_err(dwg.cpu().numpy(), ref["dwg"]),
+        "dw_up": rel_err(dwu.cpu().numpy(), ref["dwu"]),
+        "dw_down": rel_err(dwd.cpu().numpy(), ref["dwd"]),
+    }
+    for k_, v in errs.items():
+        assert v <= t, (k_, v, errs)
+    return y, dx, stats, bstats, wsb
+
+
+@pytest.mark.parametrize("dtype", [torch.bfloat16, torch.float32])
+@pytest.mark.parametrize("C", [1, 2, 4])
+def test_tiny_config(dtype, C):
+    """BASELINE configs[0]: 4 experts, top-2, h=64, FFN=128, 256 tokens, C = 1/2/4."""
+    p = make_problem(256, 64, 128, 4, 2, dtype=dtype)
+    run = GpuRun(p)
+    ref = oracle_fwd_bwd(p, C)
+    _check_all(p, run, C, ref)
+
+
+@pytest.mark.parametrize("dtype", [torch.bfloat16, torch.float32])
+def test_medium_ragged_skewed(dtype):
+    """Several M/N/K tiles, ragged token count (1000), Zipf(1.2) skew, C = 1 and 3."""
+    p = make_problem(1000, 256, 384, 8, 2, dtype=dtype, zipf_s=1.2, placement="contiguous", seed=1)
+    run = GpuRun(p)
+    for C in (1, 3):
+        _check_all(p, run, C, oracle_fwd_bwd(p, C))
+
+
+def test_counts_permutation_plan_bit_exact():
+    p = make_problem(1000, 64, 128, 8, 3, zipf_s=1.2, seed=2)
+    run = GpuRun(p)
+    d = oracle_dims(p)
+    for nsub in (1, 3, 8):
+        c = run.counts(nsub).cpu().numpy()[0]
+        ref, bad = oracle.route_counts(d, p.ids.numpy(), nsub)
+        assert bad == 0
+        np.testing.assert_array_equal(c, ref)
+    # canonical dispatch order (reading R3) of every chunk
+    run.mf.set_debug(True)
+    for C in (1, 2, 4, 3):
+        run.fwd(C)
+        for j in range(C):
+            np.testing.assert_array_equal(run.mf.debug_perm(j), oracle.dispatch_order(d, p.ids.numpy(), 0, C, j))
+    run.mf.set_debug(False)
+    # device tuner == host planner == oracle
+    counts_d = run.counts(8)
+    rng = np.random.default_rng(0)
+    for _ in range(20):
+        budget = int(rng.integers(10**5, 10**7))
+        b = capi.make_budget(budget, 1.0, int(rng.integers(0, 1000)), int(rng.integers(0, 1000)),
+                             rule=int(rng.integers(0, 2)))
+        dd = layer.plan(counts_d, run.mf.dims, b)
+        dh = layer.plan(counts_d.cpu(), run.mf.dims, b)
+        assert dd == dh
+        st, ro = oracle.plan(counts_d.cpu().numpy().astype(np.int64), d, budget_bytes=budget,
+                             static_bytes=b.static_bytes, other_act_bytes=b.other_act_bytes, rule=b.rule)
+        assert st == dh["status"]
+        if st == 0:
+            for f in ro:
+                assert ro[f] == dh[f], f
+
+
+def test_chunking_invariance_on_gpu():
+    """Eq. 6/7 on the device: Y and dX bit-identical for every C (row-local arithmetic)."""
+    p = make_problem(777, 128, 256, 6, 2, seed=3)
+    run = GpuRun(p)
+    y1, st, _, _ = run.fwd(1)
+    (dx1, *_), st, _, _ = run.bwd(1)
+    for C in (2, 4, 8, 5):
+        yc, st, _, _ = run.fwd(C)
+        assert st == 0
+        assert torch.equal(yc, y1)
+        (dxc, *_), st, _, _ = run.bwd(C)
+        assert torch.equal(dxc, dx1)
+
+
+def test_peak_workspace_scales_one_over_c():
+    """Measured workspace high-water == the prediction (memfine_workspace_bytes) exactly, and
+    peak(C)/peak(1) tracks max_j s''_j / s'' (Table 2 rows 11-13)."""
+    p = make_problem(4096, 256, 512, 8, 2, seed=4)
+    run = GpuRun(p)
+    peaks, maxrows = {}, {}
+    row_bytes = 4 + 4 + 2 * (256 + 512 + 256)
+    for C in (1, 2, 4, 8):
+        y, st, stats, wsb = run.fwd(C)
+        assert st == 0
+        assert stats["workspace_used_bytes"] == wsb
+        peaks[C] = wsb
+        rows = stats["rows"]
+        assert sum(rows) == 4096 * 2
+        maxrows[C] = max(rows)
+        # padded rows of the hottest chunk: at most 127 padding rows per local expert
+        assert max(stats["rows_padded"]) <= maxrows[C] + 8 * 127
+    assert peaks[1] > peaks[2] > peaks[4] > peaks[8]
+    for C in (2, 4, 8):
+        assert peaks[C] / peaks[1] <= (maxrows[C] + 8 * 128) / maxrows[1] + 0.01
+
+
+def test_edge_cases():
+    # T < C: empty chunks; duplicated ids inside a token's top-k; an expert with no tokens
+    ids = np.array([[0, 0], [2, 2], [0, 2]], np.int32)
+    p = make_problem(3, 64, 128, 4, 2, ids=ids)
+    run = GpuRun(p)
+    ref = oracle_fwd_bwd(p, 8)
+    _check_all(p, run, 8, ref)
+    # every token on one expert
+    p = make_problem(300, 64, 128, 4, 2, ids=np.tile(np.array([[3, 1]], np.int32), (300, 1)))
+    _check_all(p, GpuRun(p), 2, oracle_fwd_bwd(p, 2))
+
+
+def test_errors_surface():
+    p = make_problem(64, 64, 128, 4, 2)
+    run = GpuRun(p)
+    # workspace too small -> latched, reported by memfine_sync
+    y, st, stats, _ = run.fwd(1, ws_bytes=4096)
+    assert st == capi.ERR_WORKSPACE
+    # bad expert id -> MEMFINE_ERR_ROUTING at the next sync
+    bad = p.ids.clone()
+    bad[5, 1] = 99
+    run.ids = bad.to(run.dev)
+    y, st, stats, _ = run.fwd(1, counts_host=torch.zeros((1, 1, 4), dtype=torch.int32) + 64)
+    assert st == capi.ERR_ROUTING
+
+
+@pytest.mark.slow
+def test_mixtral_full_size_sampled():
+    """BASELINE configs[1] shape at EP=1 (8 experts, top-2, h=4096, FFN=14336, 16K tokens):
+    integer outputs in full; Y / dX / d_score on a sampled token subset vs the oracle."""
+    p = make_problem(16384, 4096, 14336, 8, 2, zipf_s=1.2, seed=5)
+    run = GpuRun(p)
+    d = oracle_dims(p)
+    c = run.counts(8).cpu().numpy()[0]
+    ref, _ = oracle.route_counts(d, p.ids.numpy(), 8)
+    np.testing.assert_array_equal(c, ref)
+    y, st, _, _ = run.fwd(2)
+    assert st == 0
+    (dx, dwg, dwu, dwd, ds), st, _, _ = run.bwd(2)
+    assert st == 0
+    toks = np.random.default_rng(0).choice(16384, 12, replace=False)
+    ry, rdx, rds = oracle_tokens(p, toks)
+    assert rel_err(y.float().cpu().numpy()[toks], ry) <= 2e-2
+    assert rel_err(dx.float().cpu().numpy()[toks], rdx) <= 2e-2
+    assert rel_err(ds.cpu().numpy()[toks], rds) <= 2e-2
+    assert torch.isfinite(dwg).all() and torch.isfinite(dwu).all() and torch.isfinite(dwd).all()
