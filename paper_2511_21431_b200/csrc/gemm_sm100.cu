@@ -1,6 +1,582 @@
-// gemm_sm100.cu — placeholder until the tcgen05 kernel lands (delegates to the FFMA path).
+// gemm_sm100.cu — grouped expert GEMMs on the 5th-generation tensor cores (sm_100a).
+//
+// One persistent, warp-specialised kernel template serves the six expert GEMMs of the
+// chunked MoE layer.  Per CTA (one per SM, 192 threads):
+//   warp 0      TMA producer: cp.async.bulk.tensor 2D/3D loads, 128B swizzle, mbarrier tx
+//   warp 1      TMEM allocator + MMA issuer: tcgen05.mma.cta_group::1.kind::f16, BF16 in,
+//               FP32 accumulators in TMEM, tcgen05.commit -> mbarriers
+//   warps 2..5  epilogue: tcgen05.ld 32x32b -> registers -> fused MoE epilogue -> global
+// A 4-stage smem ring (48 KB/stage) feeds the MMA; two TMEM accumulator stages (512 cols)
+// let the epilogue of tile i overlap the mainloop of tile i+1.
+//
+// Rows are the expert-major padded layout (every local expert's segment padded to 128
+// rows), so an M tile never straddles experts and the weight-gradient K loop (over tokens)
+// never straddles either; padded rows are zero.  Tile order is grouped (8 M tiles x all N
+// tiles) so the weights and activations a wave touches stay in the 126 MB L2.
+#include <cuda.h>
+#include <cudaTypedefs.h>
+#include <mutex>
 #include "kernels.h"
+
 namespace memfine {
-int launch_gemm_sm100(const GemmProblem<__nv_bfloat16>& p, cudaStream_t st) { return launch_gemm_simt(p, st); }
-int sm100_num_sms() { return 148; }
+namespace sm100 {
+
+constexpr int BM = 128, BK = 64, STAGES = 4, THREADS = 192;
+constexpr int A_BYTES = BM * BK * 2;  // 16 KB
+
+// ------------------------------------------------------------------ PTX wrappers
+__device__ __forceinline__ uint32_t su32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+__device__ __forceinline__ void mbar_init(uint64_t* b, uint32_t n) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(su32(b)), "r"(n) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* b, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(su32(b)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* b) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(su32(b)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra WAIT_%=;\n}" ::"r"(su32(b)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void tma_2d(void* dst, const CUtensorMap* m, uint64_t* bar, int c0, int c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];" ::"r"(
+          su32(dst)),
+      "l"(m), "r"(su32(bar)), "r"(c0), "r"(c1)
+      : "memory");
+}
+__device__ __forceinline__ void tma_3d(void* dst, const CUtensorMap* m, uint64_t* bar, int c0, int c1, int c2) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5}], "
+      "[%2];" ::"r"(su32(dst)),
+      "l"(m), "r"(su32(bar)), "r"(c0), "r"(c1), "r"(c2)
+      : "memory");
+}
+__device__ __forceinline__ void prefetch_tmap(const CUtensorMap* m) {
+  asm volatile("prefetch.tensormap [%0];" ::"l"(m) : "memory");
+}
+__device__ __forceinline__ void fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+
+// SMEM matrix descriptor (sm_100 UMMA): start>>4 [0,14), LBO>>4 [16,30), SBO>>4 [32,46),
+// version 1 at [46,48), base offset 0, layout SWIZZLE_128B (2) at [61,64).
+__device__ __forceinline__ uint64_t sdesc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+  uint64_t d = (uint64_t)((saddr & 0x3FFFFu) >> 4);
+  d |= (uint64_t)((lbo >> 4) & 0x3FFFu) << 16;
+  d |= (uint64_t)((sbo >> 4) & 0x3FFFu) << 32;
+  d |= (uint64_t)1 << 46;
+  d |= (uint64_t)2 << 61;
+  return d;
+}
+// Instruction descriptor, kind::f16: D f32, A/B bf16, majorness, N>>3, M>>4.
+__host__ __device__ constexpr uint32_t idesc_bf16(int M, int N, int a_mn, int b_mn) {
+  return (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)a_mn << 15) | ((uint32_t)b_mn << 16) |
+         ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
+}
+__device__ __forceinline__ void mma_bf16(uint32_t d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}" ::"r"(d),
+      "l"(a), "l"(b), "r"(idesc), "r"(acc)
+      : "memory");
+}
+__device__ __forceinline__ void mma_commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(su32(bar))
+               : "memory");
+}
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, "
+      "%15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31}, [%32];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]),
+        "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]),
+        "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+
+__device__ __forceinline__ uint32_t pack_bf16(float a, float b) {
+  __nv_bfloat162 v = __floats2bfloat162_rn(a, b);
+  return *reinterpret_cast<uint32_t*>(&v);
+}
+__device__ __forceinline__ void store32_bf16(__nv_bfloat16* dst, const float* v) {
+  uint4* d = reinterpret_cast<uint4*>(dst);
+#pragma unroll
+  for (int i = 0; i < 4; i++)
+    d[i] = make_uint4(pack_bf16(v[8 * i], v[8 * i + 1]), pack_bf16(v[8 * i + 2], v[8 * i + 3]),
+                      pack_bf16(v[8 * i + 4], v[8 * i + 5]), pack_bf16(v[8 * i + 6], v[8 * i + 7]));
+}
+__device__ __forceinline__ void load32_bf16(const __nv_bfloat16* src, float* v) {
+  const uint4* s = reinterpret_cast<const uint4*>(src);
+#pragma unroll
+  for (int i = 0; i < 4; i++) {
+    uint4 u = s[i];
+    const __nv_bfloat162* b = reinterpret_cast<const __nv_bfloat162*>(&u);
+#pragma unroll
+    for (int j = 0; j < 4; j++) {
+      float2 f = __bfloat1622float2(b[j]);
+      v[8 * i + 2 * j] = f.x;
+      v[8 * i + 2 * j + 1] = f.y;
+    }
+  }
+}
+
+// ------------------------------------------------------------------ per-kind configuration
+template <int KIND>
+struct Cfg;
+// A7/B2: X[R,h] x W_gate/W_up[g,h]^T, two accumulators (G, U) of 128 columns.
+template <> struct Cfg<GK_GATEUP> { static constexpr int BN = 128, NACC = 2, A_MN = 0, B_MN = 0; };
+// A8: a[R,g] x W_down[h,g]^T.
+template <> struct Cfg<GK_DOWN> { static constexpr int BN = 256, NACC = 1, A_MN = 0, B_MN = 0; };
+// B3: dY[R,h] x W_down[h,g]  (B(n,k) = W_down[k][n], MN-major).
+template <> struct Cfg<GK_DACT> { static constexpr int BN = 256, NACC = 1, A_MN = 0, B_MN = 1; };
+// B4: dGU[R,2g] x [W_gate; W_up][2g,h]  (MN-major B, K split at g).
+template <> struct Cfg<GK_DX> { static constexpr int BN = 256, NACC = 1, A_MN = 0, B_MN = 1; };
+// B5: dW[e] += rows^T rows  (A(m,k) = rows[s0+k][m], B(n,k) = rows[s0+k][n]; both MN-major).
+template <> struct Cfg<GK_WGRAD_DOWN> { static constexpr int BN = 256, NACC = 1, A_MN = 1, B_MN = 1; };
+template <> struct Cfg<GK_WGRAD_GU> { static constexpr int BN = 256, NACC = 1, A_MN = 1, B_MN = 1; };
+
+struct Params {
+  int El, h, g;
+  int M, N, K;       // M: rows of dW for WGRAD kinds; N: output columns; K: reduction (M-tiled kinds)
+  int num_mt_w;      // WGRAD: M tiles per expert
+  int64_t rows_cap;
+  const int* seg;
+  const int* info;
+  __nv_bfloat16* GU;
+  __nv_bfloat16* A;
+  __nv_bfloat16* O;
+  const float* w_row;
+  float* dw_row;
+  float* dW0;        // WGRAD_DOWN: dW_down; WGRAD_GU: dW_gate
+  float* dW1;        // WGRAD_GU: dW_up
+  int store_a, store_gu;
+};
+
+struct Tile {
+  int e, m0, n0, k0, nkb;  // expert, first row (M-tiled: padded row; WGRAD: dW row), first column, K origin, K blocks
+};
+
+constexpr int GROUP_M = 8;
+
+template <int KIND>
+__device__ __forceinline__ int num_tiles(const Params& p) {
+  constexpr int BN = Cfg<KIND>::BN;
+  int nt = (p.N + BN - 1) / BN;
+  if (KIND >= GK_WGRAD_DOWN) return p.El * p.num_mt_w * nt;
+  if (p.info[kInfoSkip]) return 0;
+  return (p.info[kInfoRowsPad] / BM) * nt;
+}
+
+template <int KIND>
+__device__ __forceinline__ Tile tile_of(const Params& p, int t) {
+  constexpr int BN = Cfg<KIND>::BN;
+  int nt = (p.N + BN - 1) / BN;
+  Tile T;
+  if (KIND >= GK_WGRAD_DOWN) {
+    int per = p.num_mt_w * nt;
+    T.e = t / per;
+    int r = t % per;
+    T.m0 = (r % p.num_mt_w) * BM;
+    T.n0 = (r / p.num_mt_w) * BN;
+    int s0 = __ldg(p.seg + T.e), s1 = __ldg(p.seg + T.e + 1);
+    T.k0 = s0;
+    T.nkb = (s1 - s0) / BK;
+    return T;
+  }
+  int num_mt = p.info[kInfoRowsPad] / BM;
+  int gsz = GROUP_M * nt;
+  int gi = t / gsz, first = gi * GROUP_M;
+  int gm = min(num_mt - first, GROUP_M);
+  int r = t % gsz;
+  int mt = first + r % gm;
+  T.m0 = mt * BM;
+  T.n0 = (r / gm) * BN;
+  T.e = expert_of_row(p.seg, p.El, T.m0);
+  T.k0 = 0;
+  T.nkb = p.K / BK;
+  return T;
+}
+
+// ------------------------------------------------------------------ the kernel
+template <int KIND>
+__global__ void __launch_bounds__(THREADS, 1)
+    gemm_kernel(const __grid_constant__ Params p, const __grid_constant__ CUtensorMap tmA,
+                const __grid_constant__ CUtensorMap tmB0, const __grid_constant__ CUtensorMap tmB1) {
+  using CF = Cfg<KIND>;
+  constexpr int BN = CF::BN, NACC = CF::NACC;
+  constexpr int B_BYTES = BN * BK * 2;
+  constexpr int NB_OPS = (KIND == GK_GATEUP) ? 2 : 1;                 // B tiles per stage
+  constexpr int STAGE_BYTES = A_BYTES + NB_OPS * B_BYTES;
+  constexpr int ACC_COLS = NACC * BN;                                 // per accumulator stage
+  constexpr uint32_t TMEM_COLS = 2 * ACC_COLS;                         // double-buffered
+  static_assert(TMEM_COLS <= 512, "TMEM");
+  constexpr uint32_t IDESC = idesc_bf16(BM, BN, CF::A_MN, CF::B_MN);
+
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  uint64_t* full = (uint64_t*)(smem + STAGES * STAGE_BYTES);
+  uint64_t* empty = full + STAGES;
+  uint64_t* tfull = empty + STAGES;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = (uint32_t*)(tempty + 2);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (warp == 0 && lane == 0) {
+    prefetch_tmap(&tmA);
+    prefetch_tmap(&tmB0);
+    if (NB_OPS == 2 || KIND == GK_DX) prefetch_tmap(&tmB1);
+    for (int s = 0; s < STAGES; s++) { mbar_init(full + s, 1); mbar_init(empty + s, 1); }
+    for (int a = 0; a < 2; a++) { mbar_init(tfull + a, 1); mbar_init(tempty + a, 4); }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(su32(tmem_slot)),
+                 "r"(TMEM_COLS)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  fence_before();
+  __syncthreads();
+  fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+  const int ntiles = num_tiles<KIND>(p);
+
+  if (warp == 0) {
+    // ================================================================ TMA producer
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
+        Tile T = tile_of<KIND>(p, t);
+        for (int kb = 0; kb < T.nkb; kb++) {
+          mbar_wait(empty + stage, phase ^ 1);
+          uint8_t* sa = smem + stage * STAGE_BYTES;
+          uint8_t* sb = sa + A_BYTES;
+          mbar_expect_tx(full + stage, STAGE_BYTES);
+          int kc = T.k0 + kb * BK;
+          if (CF::A_MN) {
+            // A(m,k) = rows[kc + k][m0 + m]: two 64-wide MN atoms of 64 K rows
+            tma_2d(sa, &tmA, full + stage, T.m0, kc);
+            tma_2d(sa + 8192, &tmA, full + stage, T.m0 + 64, kc);
+          } else {
+            tma_2d(sa, &tmA, full + stage, kc, T.m0);
+          }
+          if (KIND == GK_GATEUP) {
+            tma_3d(sb, &tmB0, full + stage, kc, T.n0, T.e);
+            tma_3d(sb + B_BYTES, &tmB1, full + stage, kc, T.n0, T.e);
+          } else if (KIND == GK_DOWN) {
+            tma_3d(sb, &tmB0, full + stage, kc, T.n0, T.e);
+          } else if (KIND == GK_DACT) {
+#pragma unroll
+            for (int i = 0; i < BN / 64; i++) tma_3d(sb + i * 8192, &tmB0, full + stage, T.n0 + 64 * i, kc, T.e);
+          } else if (KIND == GK_DX) {
+            const CUtensorMap* mb = kc < p.g ? &tmB0 : &tmB1;
+            int kk = kc < p.g ? kc : kc - p.g;
+#pragma unroll
+            for (int i = 0; i < BN / 64; i++) tma_3d(sb + i * 8192, mb, full + stage, T.n0 + 64 * i, kk, T.e);
+          } else {
+#pragma unroll
+            for (int i = 0; i < BN / 64; i++) tma_2d(sb + i * 8192, &tmB0, full + stage, T.n0 + 64 * i, kc);
+          }
+          if (++stage == STAGES) { stage = 0; phase ^= 1; }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ================================================================ MMA issuer
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      int it = 0;
+      for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
+        Tile T = tile_of<KIND>(p, t);
+        if (T.nkb == 0) continue;
+        int as = it & 1;
+        uint32_t aph = (it >> 1) & 1;
+        mbar_wait(tempty + as, aph ^ 1);
+        fence_after();
+        uint32_t dbase = tmem_base + as * ACC_COLS;
+        for (int kb = 0; kb < T.nkb; kb++) {
+          mbar_wait(full + stage, phase);
+          fence_after();
+          uint32_t sa = su32(smem + stage * STAGE_BYTES);
+          uint32_t sb = sa + A_BYTES;
+#pragma unroll
+          for (int k = 0; k < BK / 16; k++) {
+            uint64_t ad = CF::A_MN ? sdesc(sa + k * 2048, 8192, 1024) : sdesc(sa + k * 32, 16, 1024);
+#pragma unroll
+            for (int q = 0; q < NACC; q++) {
+              uint32_t bq = sb + q * B_BYTES;
+              uint64_t bd = CF::B_MN ? sdesc(bq + k * 2048, 8192, 1024) : sdesc(bq + k * 32, 16, 1024);
+              mma_bf16(dbase + q * BN, ad, bd, IDESC, (kb | k) != 0);
+            }
+          }
+          mma_commit(empty + stage);
+          if (++stage == STAGES) { stage = 0; phase ^= 1; }
+        }
+        mma_commit(tfull + as);
+        it++;
+      }
+    }
+  } else {
+    // ================================================================ epilogue (warps 2..5)
+    const int q = warp & 3;               // TMEM lane quarter this warp may access
+    const int rloc = q * 32 + lane;       // row within the 128-row tile
+    int it = 0;
+    for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
+      Tile T = tile_of<KIND>(p, t);
+      if (T.nkb == 0) continue;
+      int as = it & 1;
+      uint32_t aph = (it >> 1) & 1;
+      mbar_wait(tfull + as, aph);
+      fence_after();
+      uint32_t tb = tmem_base + as * ACC_COLS + ((uint32_t)(q * 32) << 16);
+      const int64_t row = (int64_t)T.m0 + rloc;
+      float dwp = 0.f;
+      float wrow = 0.f;
+      if (KIND == GK_DACT) wrow = p.w_row[row];
+#pragma unroll 1
+      for (int c = 0; c < BN; c += 32) {
+        const int n = T.n0 + c;
+        uint32_t r[32];
+        tmem_ld32(tb + c, r);
+        float v[32];
+#pragma unroll
+        for (int i = 0; i < 32; i++) v[i] = __uint_as_float(r[i]);
+        if (KIND == GK_GATEUP) {
+          uint32_t r2[32];
+          tmem_ld32(tb + BN + c, r2);
+          float u[32];
+#pragma unroll
+          for (int i = 0; i < 32; i++) u[i] = __uint_as_float(r2[i]);
+          if (n < p.g) {
+            if (p.store_gu) {
+              store32_bf16(p.GU + row * 2 * p.g + n, v);
+              store32_bf16(p.GU + row * 2 * p.g + p.g + n, u);
+            }
+            if (p.store_a) {
+              float a[32];
+#pragma unroll
+              for (int i = 0; i < 32; i++) a[i] = silu_f(v[i]) * u[i];
+              store32_bf16(p.A + row * p.g + n, a);
+            }
+          }
+        } else if (KIND == GK_DOWN || KIND == GK_DX) {
+          if (n < p.h) store32_bf16(p.O + row * p.h + n, v);
+        } else if (KIND == GK_DACT) {
+          if (n < p.g) {
+            float G[32], U[32], dG[32], dU[32], aw[32];
+            load32_bf16(p.GU + row * 2 * p.g + n, G);
+            load32_bf16(p.GU + row * 2 * p.g + p.g + n, U);
+#pragma unroll
+            for (int i = 0; i < 32; i++) {
+              float sg = sigmoid_f(G[i]);
+              float a = G[i] * sg * U[i];
+              dwp = fmaf(v[i], a, dwp);
+              float dA = wrow * v[i];
+              dG[i] = dA * U[i] * sg * (1.f + G[i] * (1.f - sg));
+              dU[i] = dA * G[i] * sg;
+              aw[i] = wrow * a;
+            }
+            store32_bf16(p.GU + row * 2 * p.g + n, dG);
+            store32_bf16(p.GU + row * 2 * p.g + p.g + n, dU);
+            store32_bf16(p.A + row * p.g + n, aw);
+          }
+        } else {
+          // WGRAD: fp32 read-modify-write of dW (each element owned by one tile; accumulates
+          // across chunks, reading R18)
+          const int m = T.m0 + rloc;
+          if (m < p.M && n < p.N) {
+            float* dst;
+            if (KIND == GK_WGRAD_DOWN) dst = p.dW0 + ((int64_t)T.e * p.h + m) * p.g + n;
+            else dst = (m < p.g) ? p.dW0 + ((int64_t)T.e * p.g + m) * p.h + n
+                                 : p.dW1 + ((int64_t)T.e * p.g + (m - p.g)) * p.h + n;
+            float4* d4 = reinterpret_cast<float4*>(dst);
+#pragma unroll
+            for (int i = 0; i < 8; i++) {
+              float4 o = d4[i];
+              o.x += v[4 * i];
+              o.y += v[4 * i + 1];
+              o.z += v[4 * i + 2];
+              o.w += v[4 * i + 3];
+              d4[i] = o;
+            }
+          }
+        }
+      }
+      if (KIND == GK_DACT) atomicAdd(p.dw_row + row, dwp);
+      fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(tempty + as);
+      it++;
+    }
+  }
+  fence_before();
+  __syncthreads();
+  fence_after();
+  if (warp == 1)
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(TMEM_COLS)
+                 : "memory");
+}
+
+// ------------------------------------------------------------------ host side
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    cudaDriverEntryPointQueryResult q;
+    void* p = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = (PFN_cuTensorMapEncodeTiled_v12000)p;
+  });
+  return fn;
+}
+
+// bf16 tensor map, 128B swizzle; dims/box innermost first; strides in bytes for dims 1..
+bool make_map(CUtensorMap* m, const void* base, int rank, const uint64_t* dims, const uint64_t* strides_bytes,
+              const uint32_t* box) {
+  auto fn = encode_fn();
+  if (!fn) return false;
+  cuuint64_t gd[3], gs[2];
+  cuuint32_t bx[3], es[3] = {1, 1, 1};
+  for (int i = 0; i < rank; i++) { gd[i] = dims[i]; bx[i] = box[i]; }
+  for (int i = 0; i < rank - 1; i++) gs[i] = strides_bytes[i];
+  CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, rank, const_cast<void*>(base), gd, gs, bx, es,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
+bool map2d(CUtensorMap* m, const void* base, uint64_t inner, uint64_t outer, uint32_t box_in, uint32_t box_out) {
+  uint64_t d[2] = {inner, outer}, s[1] = {inner * 2};
+  uint32_t b[2] = {box_in, box_out};
+  return make_map(m, base, 2, d, s, b);
+}
+bool map3d(CUtensorMap* m, const void* base, uint64_t d0, uint64_t d1, uint64_t d2, uint32_t b0, uint32_t b1) {
+  uint64_t d[3] = {d0, d1, d2}, s[2] = {d0 * 2, d0 * d1 * 2};
+  uint32_t b[3] = {b0, b1, 1};
+  return make_map(m, base, 3, d, s, b);
+}
+
+int g_num_sms = 0;
+
+template <int KIND>
+int launch(const GemmProblem<__nv_bfloat16>& gp, cudaStream_t st) {
+  using CF = Cfg<KIND>;
+  constexpr int BN = CF::BN;
+  constexpr int NB_OPS = (KIND == GK_GATEUP) ? 2 : 1;
+  constexpr int SMEM = STAGES * (A_BYTES + NB_OPS * BN * BK * 2) + 1024 + 256;
+  static bool attr_set = false;
+  if (!attr_set) {
+    if (cudaFuncSetAttribute(gemm_kernel<KIND>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM) != cudaSuccess)
+      return -1;
+    attr_set = true;
+  }
+  if (!g_num_sms) {
+    int dev;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
+  }
+  Params p{};
+  p.El = gp.El;
+  p.h = gp.h;
+  p.g = gp.g;
+  p.rows_cap = gp.rows_cap;
+  p.seg = gp.seg;
+  p.info = gp.info;
+  p.GU = gp.GU;
+  p.A = gp.A;
+  p.O = gp.O;
+  p.w_row = gp.w_row;
+  p.dw_row = gp.dw_row;
+  p.store_a = gp.store_a;
+  p.store_gu = gp.store_gu;
+  const uint64_t R = (uint64_t)gp.rows_cap, h = gp.h, g = gp.g, El = gp.El;
+  if (R == 0) return 0;
+  CUtensorMap mA, mB0, mB1;
+  bool ok = true;
+  int64_t max_tiles;
+  switch (KIND) {
+    case GK_GATEUP:
+      p.N = gp.g; p.K = gp.h;
+      ok &= map2d(&mA, gp.X, h, R, BK, BM);
+      ok &= map3d(&mB0, gp.Wg, h, g, El, BK, BN);
+      ok &= map3d(&mB1, gp.Wu, h, g, El, BK, BN);
+      break;
+    case GK_DOWN:
+      p.N = gp.h; p.K = gp.g;
+      ok &= map2d(&mA, gp.A, g, R, BK, BM);
+      ok &= map3d(&mB0, gp.Wd, g, h, El, BK, BN);
+      mB1 = mB0;
+      break;
+    case GK_DACT:
+      p.N = gp.g; p.K = gp.h;
+      ok &= map2d(&mA, gp.DY, h, R, BK, BM);
+      ok &= map3d(&mB0, gp.Wd, g, h, El, 64, BK);   // B(n,k) = W_down[e][k][n]
+      mB1 = mB0;
+      break;
+    case GK_DX:
+      p.N = gp.h; p.K = 2 * gp.g;
+      ok &= map2d(&mA, gp.GU, 2 * g, R, BK, BM);
+      ok &= map3d(&mB0, gp.Wg, h, g, El, 64, BK);   // B(n,k) = W_gate[e][k][n]
+      ok &= map3d(&mB1, gp.Wu, h, g, El, 64, BK);
+      break;
+    case GK_WGRAD_DOWN:
+      p.M = gp.h; p.N = gp.g;
+      ok &= map2d(&mA, gp.DY, h, R, 64, BK);        // A(m,k) = dY[s0+k][m]
+      ok &= map2d(&mB0, gp.A, g, R, 64, BK);        // B(n,k) = a_w[s0+k][n]
+      mB1 = mB0;
+      p.dW0 = gp.dWd;
+      break;
+    default:
+      p.M = 2 * gp.g; p.N = gp.h;
+      ok &= map2d(&mA, gp.GU, 2 * g, R, 64, BK);    // A(m,k) = dGU[s0+k][m]
+      ok &= map2d(&mB0, gp.X, h, R, 64, BK);        // B(n,k) = X[s0+k][n]
+      mB1 = mB0;
+      p.dW0 = gp.dWg;
+      p.dW1 = gp.dWu;
+      break;
+  }
+  if (!ok) return -1;
+  int nt = (p.N + BN - 1) / BN;
+  if (KIND >= GK_WGRAD_DOWN) {
+    p.num_mt_w = (p.M + BM - 1) / BM;
+    max_tiles = (int64_t)p.El * p.num_mt_w * nt;
+  } else {
+    max_tiles = (int64_t)(R / BM) * nt;
+  }
+  int grid = (int)std::min<int64_t>(max_tiles, g_num_sms);
+  if (grid <= 0) return 0;
+  gemm_kernel<KIND><<<grid, THREADS, SMEM, st>>>(p, mA, mB0, mB1);
+  return 1;
+}
+
+}  // namespace sm100
+
+int launch_gemm_sm100(const GemmProblem<__nv_bfloat16>& p, cudaStream_t st) {
+  switch (p.kind) {
+    case GK_GATEUP: return sm100::launch<GK_GATEUP>(p, st);
+    case GK_DOWN: return sm100::launch<GK_DOWN>(p, st);
+    case GK_DACT: return sm100::launch<GK_DACT>(p, st);
+    case GK_DX: return sm100::launch<GK_DX>(p, st);
+    case GK_WGRAD_DOWN: return sm100::launch<GK_WGRAD_DOWN>(p, st);
+    case GK_WGRAD_GU: return sm100::launch<GK_WGRAD_GU>(p, st);
+  }
+  return -1;
+}
+
+int sm100_num_sms() { return sm100::g_num_sms ? sm100::g_num_sms : 148; }
+
 }  // namespace memfine
