@@ -1,0 +1,415 @@
+"""bench.py — MemFine chunked MoE layer, forward + backward tokens/s on B200.
+
+Contract (driver): ``python bench.py --gpus N --steps K --warmup W`` (torchrun for N > 1,
+one rank per GPU, EP = N) prints ONE JSON line on rank 0.
+
+Workload (BASELINE.json configs[1], the config its metric is quoted on): the Mixtral-8x7B-
+style layer — 8 experts, top-2, h = 4096, SwiGLU FFN 14336, 16K tokens per GPU, bf16
+storage / fp32 accumulation — with Zipf(1.2)-skewed synthetic routing (random popularity
+placement).  At N GPUs the experts are split EP = N ways and every rank holds its own 16K
+tokens (weak scaling).  One step = memfine_route_counts -> memfine_plan (device tuner) ->
+memfine_moe_fwd -> memfine_moe_bwd at the chunk count C the tuner picks for the budget.
+
+``--impl reference`` times the CPU oracle (oracle/, fp64, the method's reference
+definition) on a bounded sample of the same workload — the reference arm of this tier.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+import synth  # noqa: E402
+
+METRIC = "MoE layer fwd+bwd tokens/s"
+# Algorithmic FLOPs per routed copy and kernel class, in units of h*g:
+# gate/up runs in the forward and again as the backward recompute (4+4), down 2, dA 2,
+# dX 4, dW_down 2, dW_gate||dW_up 4  -> 22 h g per copy.
+FLOP_COEF = {"gemm_gateup_swiglu": 8, "gemm_down": 2, "gemm_dact_epilogue": 2, "gemm_dx": 4,
+             "gemm_wgrad_down": 2, "gemm_wgrad_gateup": 4}
+
+
+def load_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return {"hbm_gbs": d["hbm_gbs"], "bf16_tflops": d["bf16_tflops"],
+                "bf16_tflops_sustained": d.get("bf16_tflops_sustained", d["bf16_tflops"]), "source": "measured"}
+    return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0, "source": "fallback"}
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled DURING the timed region."""
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except FileNotFoundError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 7:
+                continue
+            try:
+                sm.append(float(f[0]))
+                mx = float(f[1])
+            except ValueError:
+                continue
+            for n, v in zip(names, f[3:7]):
+                if v.lower() == "active":
+                    reasons.add(n)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def dist_setup():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        import torch.distributed as dist
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    else:
+        torch.cuda.set_device(local)
+    return world, rank, local
+
+
+def barrier(world):
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+
+
+def max_over_ranks(v: float, world: int) -> float:
+    if world == 1:
+        return v
+    import torch.distributed as dist
+    t = torch.tensor([v], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def device_weights(experts, h, g, dev):
+    """Seeded per-global-expert weights generated on the device (same recipe as synth)."""
+    out = []
+    for e in experts:
+        gen = torch.Generator(device=dev).manual_seed(7000 + int(e))
+        wg = (torch.randn(g, h, generator=gen, device=dev) / math.sqrt(h)).to(torch.bfloat16)
+        wu = (torch.randn(g, h, generator=gen, device=dev) / math.sqrt(h)).to(torch.bfloat16)
+        wd = (torch.randn(h, g, generator=gen, device=dev) / math.sqrt(g)).to(torch.bfloat16)
+        out.append((wg, wu, wd))
+    return tuple(torch.stack([o[i] for o in out]).contiguous() for i in range(3))
+
+
+# ------------------------------------------------------------------------------------ oracle legs
+def oracle_sample_time(cfg, ntok: int, rank: int = 0):
+    """Oracle (fp64, unchunked Eq. 4 + Eq. 5) fwd + bwd on ntok tokens of the workload; seconds."""
+    import oracle
+    oracle.build()
+    x = synth.make_x(ntok, cfg.h, rank=rank)
+    dy = synth.make_dy(ntok, cfg.h, rank=rank)
+    ids, w = synth.make_routing(ntok, cfg.E, cfg.k, rank=rank, zipf_s=cfg.zipf_s, placement=cfg.placement)
+    wg, wu, wd = synth.make_experts(range(cfg.E), cfg.h, cfg.g)
+    b = lambda a: a.contiguous().view(torch.int16).numpy().view(np.uint16)
+    d = oracle.Dims(T=ntok, h=cfg.h, g=cfg.g, E=cfg.E, k=cfg.k, in_dtype="bf16")
+    args = (b(x), ids, w.astype(np.float64), b(wg), b(wu), b(wd))
+    t0 = time.perf_counter()
+    oracle.moe_forward(d, *args)
+    oracle.moe_backward(d, b(dy), *args)
+    return time.perf_counter() - t0, int(oracle.lib().oracle_num_threads())
+
+
+def cpu_baseline(cfg, ntok: int):
+    dt, cores = oracle_sample_time(cfg, ntok)
+    return {"value": ntok / dt, "unit": "tokens/s", "cores": cores, "kind": "oracle",
+            "sample": f"{ntok} tokens of the {cfg.name} layer (all {cfg.E} experts, full h={cfg.h}, g={cfg.g}), "
+                      f"oracle fwd (Eq. 4) + bwd (Eq. 5) incl. dW, fp64, {dt:.1f} s; cost linear in tokens "
+                      f"plus a fixed dW zeroing term"}
+
+
+def run_reference(args):
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    cfg = synth.CONFIGS[args.config]
+    ntok = args.ref_tokens
+    times = []
+    cores = None
+    for i in range(args.warmup + args.steps):
+        dt, cores = oracle_sample_time(cfg, ntok, rank=i % 8)
+        if i >= args.warmup:
+            times.append(dt)
+    ms = 1000.0 * statistics.mean(times)
+    value = ntok / (ms / 1000.0)
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": f"{cfg.name}: E={cfg.E} top-{cfg.k} h={cfg.h} ffn={cfg.g}, oracle sample "
+                                   f"{ntok} tokens/step, Zipf({cfg.zipf_s}) routing"},
+            "cpu_baseline": {"value": value, "unit": "tokens/s", "cores": cores, "kind": "oracle",
+                             "sample": f"{ntok} tokens per step, fwd+bwd, fp64"},
+            "e2e": {"value": value, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------------------------------ GPU arm
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="memfine", choices=["memfine", "reference"])
+    ap.add_argument("--config", default="mixtral", choices=sorted(synth.CONFIGS))
+    ap.add_argument("--tokens", type=int, default=0, help="tokens per GPU (default: the config's)")
+    ap.add_argument("--budget-gb", type=float, default=0.0, help="M^GPU for MACT (default: this GPU's HBM)")
+    ap.add_argument("--alpha", type=float, default=0.9)
+    ap.add_argument("--chunks", type=int, default=0, help="override the tuner's C")
+    ap.add_argument("--sweep", type=int, default=1, help="also time every bin C (N=1 only)")
+    ap.add_argument("--cpu-tokens", type=int, default=6)
+    ap.add_argument("--ref-tokens", type=int, default=4)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--placement", default=None)
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return run_reference(args)
+
+    from paper_2511_21431_b200 import capi, layer
+    world, rank, local = dist_setup()
+    assert world == args.gpus or args.gpus == 1 and world == 1, "run N>1 under torchrun"
+    dev = torch.device("cuda", local)
+    cfg = synth.CONFIGS[args.config]
+    placement = args.placement or cfg.placement
+    T = args.tokens or cfg.T
+    EP = world
+    assert cfg.E % EP == 0
+    El = cfg.E // EP
+    h, g, E, k = cfg.h, cfg.g, cfg.E, cfg.k
+    pg = None
+    if world > 1:
+        import torch.distributed as dist
+        pg = dist.group.WORLD
+
+    # ---------------------------------------------------------------- inputs (seeded, synthetic)
+    x_h = synth.make_x(T, h, rank=rank)
+    dy_h = synth.make_dy(T, h, rank=rank)
+    ids_np, w_np = synth.make_routing(T, E, k, rank=rank, zipf_s=cfg.zipf_s, placement=placement)
+    ids_h = torch.from_numpy(ids_np)
+    w_h = torch.from_numpy(w_np)
+    x, dy, ids, w = (t.to(dev) for t in (x_h, dy_h, ids_h, w_h))
+    wg, wu, wd = device_weights(synth.local_experts(E, EP, rank), h, g, dev)
+    f32 = dict(dtype=torch.float32, device=dev)
+    dwg, dwu, dwd = torch.empty(wg.shape, **f32), torch.empty(wu.shape, **f32), torch.empty(wd.shape, **f32)
+    y, dx = torch.empty_like(x), torch.empty_like(x)
+    dscore = torch.empty(w.shape, **f32)
+
+    mf = layer.MemFine(T, h, g, E, k, ep_size=EP, ep_rank=rank, dtype=torch.bfloat16, process_group=pg)
+    bins = (1, 2, 4, 8)
+
+    # ---------------------------------------------------------------- MACT: counts -> C (device tuner)
+    counts = mf.route_counts(ids, nsub=8)
+    torch.cuda.synchronize()
+    counts_h = counts.cpu()
+    cap = int(args.budget_gb * 1e9) if args.budget_gb else torch.cuda.get_device_properties(dev).total_memory
+    static = sum(t.numel() * t.element_size() for t in (wg, wu, wd, dwg, dwu, dwd, x, dy, y, dx, ids, w, dscore))
+    budget = capi.make_budget(cap, args.alpha, static, 0, bins=bins)
+    plan = layer.plan(counts, mf.dims, budget)
+    assert plan["status"] == 0, plan
+    C = args.chunks or plan["C"]
+
+    def ws_for(Cc):
+        fwd = layer.workspace_bytes(counts_h, mf.dims, Cc, capi.FWD)
+        bwd = layer.workspace_bytes(counts_h, mf.dims, Cc, capi.BWD)
+        return fwd, bwd
+
+    def make_step(Cc, ws):
+        def step(xx=x, dyy=dy, idss=ids, ww=w):
+            mf.moe_fwd(xx, idss, ww, wg, wu, wd, Cc, ws, y=y)
+            mf.moe_bwd(dyy, xx, idss, ww, wg, wu, wd, Cc, ws, dx=dx, dw_gate=dwg, dw_up=dwu, dw_down=dwd,
+                       dscore=dscore)
+        return step
+
+    def timed(step, K, W, prof=False):
+        for _ in range(W):
+            step()
+        torch.cuda.synchronize()
+        st = mf.sync()
+        assert st == 0, capi.status_str(st)
+        if prof:
+            mf.profile_read()
+            mf.profile_enable(True)
+        barrier(world)
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(K):
+            step()
+        e1.record()
+        torch.cuda.synchronize()
+        barrier(world)
+        ms = e0.elapsed_time(e1) / K
+        profd = None
+        if prof:
+            profd = mf.profile_read()
+            mf.profile_enable(False)
+        st = mf.sync()
+        assert st == 0, capi.status_str(st)
+        return max_over_ranks(ms, world), profd
+
+    fwd_b, bwd_b = ws_for(C)
+    ws = torch.empty(max(fwd_b, bwd_b), dtype=torch.uint8, device=dev)
+    step = make_step(C, ws)
+
+    # launches per step (the library's own kernels)
+    step()
+    torch.cuda.synchronize()
+    mf.sync()
+    launches_fwd_bwd = None
+    mf.moe_fwd(x, ids, w, wg, wu, wd, C, ws, y=y)
+    mf.sync()
+    lf = mf.last_stats()["kernel_launches"]
+    mf.moe_bwd(dy, x, ids, w, wg, wu, wd, C, ws, dx=dx, dw_gate=dwg, dw_up=dwu, dw_down=dwd, dscore=dscore)
+    mf.sync()
+    bstats = mf.last_stats()
+    launches_fwd_bwd = lf + bstats["kernel_launches"]
+    rows_total = sum(bstats["rows"])  # s''_r: copies this rank's experts processed per step
+
+    with ClockSampler(local) as clk:
+        ms, prof = timed(step, args.steps, args.warmup, prof=True)
+        # the same timed region again without event bracketing (the headline number)
+        ms_plain, _ = timed(step, args.steps, 1, prof=False)
+    ms = ms_plain
+    value = EP * T / (ms / 1000.0)
+
+    # ---------------------------------------------------------------- roofline of the dominant kernel
+    peaks = load_peaks()
+    dom = max(prof, key=lambda s: prof[s]["ms"])
+    tot_ms = sum(v["ms"] for v in prof.values())
+    roof = None
+    if dom in FLOP_COEF and prof[dom]["launches"]:
+        flops_step = FLOP_COEF[dom] * h * g * rows_total
+        per_launch_flops = flops_step * args.steps / prof[dom]["launches"]
+        avg_ms = prof[dom]["ms"] / prof[dom]["launches"]
+        achieved = per_launch_flops / (avg_ms / 1000.0) / 1e12
+        peak = peaks["bf16_tflops_sustained"]
+        roof = {"bound": "tensor", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+                "frac": achieved / peak, "traffic": None,
+                "peak_source": f"{peaks['source']} bf16_tflops_sustained (kernel timed inside a long step)",
+                "share_of_step": prof[dom]["ms"] / tot_ms if tot_ms else None}
+    gemm_ms = sum(prof[s]["ms"] for s in FLOP_COEF) / args.steps
+    all_gemm_tflops = 22 * h * g * rows_total / (gemm_ms / 1000.0) / 1e12 if gemm_ms else None
+    step_tflops = 22 * h * g * rows_total / (ms / 1000.0) / 1e12
+
+    # ---------------------------------------------------------------- e2e through the public API
+    pin = lambda t: t.pin_memory()
+    xh, dyh, idsh, wh = pin(x_h), pin(dy_h), pin(ids_h), pin(w_h)
+    yh = torch.empty(y.shape, dtype=y.dtype).pin_memory()
+    dxh = torch.empty(dx.shape, dtype=dx.dtype).pin_memory()
+    xd, dyd, idsd, wdv = torch.empty_like(x), torch.empty_like(dy), torch.empty_like(ids), torch.empty_like(w)
+
+    def e2e_step():
+        xd.copy_(xh, non_blocking=True)
+        dyd.copy_(dyh, non_blocking=True)
+        idsd.copy_(idsh, non_blocking=True)
+        wdv.copy_(wh, non_blocking=True)
+        step(xd, dyd, idsd, wdv)
+        yh.copy_(y, non_blocking=True)
+        dxh.copy_(dx, non_blocking=True)
+
+    ms_e2e, _ = timed(e2e_step, args.steps, 1)
+    h2d = sum(t.numel() * t.element_size() for t in (xh, dyh, idsh, wh))
+    d2h = sum(t.numel() * t.element_size() for t in (yh, dxh))
+
+    # ---------------------------------------------------------------- memory: peak activation vs unchunked
+    def peak_gb(Cc):
+        f, b = ws_for(Cc)
+        return max(f, b) / 1e9
+
+    per_C = {}
+    if args.sweep and world == 1:
+        for Cc in bins:
+            if Cc == C:
+                per_C[Cc] = {"ms_per_step": ms, "tokens_per_s": value, "peak_act_gb": peak_gb(Cc)}
+                continue
+            wsc = torch.empty(int(peak_gb(Cc) * 1e9) + 1, dtype=torch.uint8, device=dev)
+            msc, _ = timed(make_step(Cc, wsc), max(3, args.steps // 2), 1)
+            per_C[Cc] = {"ms_per_step": msc, "tokens_per_s": EP * T / (msc / 1000.0), "peak_act_gb": peak_gb(Cc)}
+            del wsc
+    peak_c = peak_gb(C)
+    peak_1 = peak_gb(1)
+    beta = 2 * (2 * h + 2 * g)
+    paper_model = {Cc: beta * max(int(counts_h[:, j * (8 // Cc):(j + 1) * (8 // Cc), rank * El:(rank + 1) * El].sum())
+                                  for j in range(Cc)) / 1e9 for Cc in bins}
+
+    if rank != 0:
+        return
+    line = {
+        "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
+        "config": {"workload": f"{cfg.name}-style MoE layer: E={E} top-{k} h={h} SwiGLU ffn={g}, {T} tokens/GPU, "
+                               f"Zipf({cfg.zipf_s}) routing ({placement} placement), EP={EP}",
+                   "tokens_per_gpu": T, "ep": EP, "chunks": C, "tuner": plan,
+                   "budget": {"gpu_capacity_bytes": cap, "alpha": args.alpha, "static_bytes": static},
+                   "l2": "no flush: every step streams > 126 MB (weights 2.8 GB at EP=1, activations GBs)"},
+        "peak_act_gb": peak_c, "peak_act_gb_unchunked": peak_1,
+        "peak_act_paper_model_gb": paper_model,
+        "per_C": per_C,
+        "roofline": roof,
+        "gemm_tflops_all_kernels": all_gemm_tflops, "step_tflops": step_tflops,
+        "kernel_ms_per_step": {s: v["ms"] / args.steps for s, v in prof.items() if v["launches"]},
+        "clocks": clk.summary(),
+        "e2e": {"value": EP * T / (ms_e2e / 1000.0), "unit": "tokens/s", "h2d_bytes_per_step": h2d,
+                "d2h_bytes_per_step": d2h, "ms_per_step": ms_e2e},
+        "gpu_launches": launches_fwd_bwd * args.steps,
+    }
+    if world == 1 and not args.no_cpu_baseline:
+        line["cpu_baseline"] = cpu_baseline(cfg, args.cpu_tokens)
+    print(json.dumps(line), flush=True)
+
+
+if __name__ == "__main__":
+    main()

@@ -206,6 +206,20 @@ memfine_status memfine_sync(memfine_handle_t h, void* stream);
 /* Statistics of the last fwd/bwd (call memfine_sync first). */
 memfine_status memfine_last_stats(memfine_handle_t h, memfine_stats* out);
 
+/* Measurement: when enabled, the library brackets each of its launches with CUDA events
+ * recorded on the launch stream and accumulates per-kernel-class device time.  Slots:
+ * 0..5 the expert GEMMs (0 gate/up+SwiGLU, 1 down, 2 dA+fused epilogue, 3 dX,
+ * 4 dW_down, 5 dW_gate||dW_up), 6 dispatch (histogram, scan, permute, padding), 7 combine /
+ * unpermute-reduce, 8 memsets, 9 NCCL exchanges.  memfine_profile_read synchronises on the
+ * recorded events, returns the totals since the last read, and resets them. */
+#define MEMFINE_PROF_SLOTS 10
+typedef struct {
+    int32_t launches[MEMFINE_PROF_SLOTS];
+    double  ms[MEMFINE_PROF_SLOTS];
+} memfine_profile;
+memfine_status memfine_profile_enable(memfine_handle_t h, int32_t enable);
+memfine_status memfine_profile_read(memfine_handle_t h, memfine_profile* out);
+
 /* Debug: when enabled, fwd records each chunk's canonical dispatch order
  * (reading R3: ascending local expert, src rank, token, slot; padding rows
  * dropped) as src*T*k + i*k + slot.  memfine_debug_perm copies chunk `chunk`

@@ -650,3 +650,16 @@ void oracle_moe_tokens(const oracle_dims* d, int64_t ntok, const int64_t* toks,
 }
 
 int32_t oracle_version(void) { return 1; }
+
+#ifdef _OPENMP
+#include <omp.h>
+#endif
+/* Threads the OpenMP loops above use (reported as cpu_baseline.cores). */
+int32_t oracle_num_threads(void)
+{
+#ifdef _OPENMP
+    return omp_get_max_threads();
+#else
+    return 1;
+#endif
+}

@@ -18,7 +18,10 @@ FWD, BWD = 0, 1
 SYMBOLS = ("memfine_abi_version", "memfine_status_str", "memfine_nccl_unique_id", "memfine_create",
            "memfine_destroy", "memfine_route_counts", "memfine_plan", "memfine_workspace_bytes",
            "memfine_moe_fwd", "memfine_moe_bwd", "memfine_sync", "memfine_last_stats",
-           "memfine_set_debug", "memfine_debug_perm")
+           "memfine_profile_enable", "memfine_profile_read", "memfine_set_debug", "memfine_debug_perm")
+
+PROF_SLOTS = ("gemm_gateup_swiglu", "gemm_down", "gemm_dact_epilogue", "gemm_dx", "gemm_wgrad_down",
+              "gemm_wgrad_gateup", "dispatch_permute", "combine_unpermute", "memset", "nccl_exchange")
 
 
 class MemfineError(RuntimeError):
@@ -62,6 +65,13 @@ class Stats(C.Structure):
                 "gemm_launches": self.gemm_launches, "kernel_launches": self.kernel_launches}
 
 
+class Profile(C.Structure):
+    _fields_ = [("launches", C.c_int32 * 10), ("ms", C.c_double * 10)]
+
+    def as_dict(self):
+        return {PROF_SLOTS[i]: {"launches": self.launches[i], "ms": self.ms[i]} for i in range(10)}
+
+
 _lib = None
 
 
@@ -89,6 +99,8 @@ def lib():
         L.memfine_moe_bwd.argtypes = [vp, vp, vp, vp, vp, vp, vp, vp, i32, vp, vp, vp, vp, vp, i32, vp, u64, vp]
         L.memfine_sync.argtypes = [vp, vp]
         L.memfine_last_stats.argtypes = [vp, C.POINTER(Stats)]
+        L.memfine_profile_enable.argtypes = [vp, i32]
+        L.memfine_profile_read.argtypes = [vp, C.POINTER(Profile)]
         L.memfine_set_debug.argtypes = [vp, i32]
         L.memfine_debug_perm.argtypes = [vp, i32, vp, i64, C.POINTER(i64)]
         if L.memfine_abi_version() != 1:

@@ -32,7 +32,40 @@ struct memfine_handle_s {
   int* counts_h = nullptr;     // pinned mirror
   size_t counts_cap = 0;
   cudaEvent_t ev = nullptr;
+  // measurement (memfine_profile_enable)
+  int prof = 0;
+  struct Rec { int slot; cudaEvent_t a, b; };
+  std::vector<Rec> recs;
+  std::vector<cudaEvent_t> pool;
+  size_t pool_used = 0;
+  int open_slot = -1;
+  cudaEvent_t open_ev = nullptr;
 };
+
+namespace {
+cudaEvent_t pool_event(memfine_handle_s* h) {
+  if (h->pool_used == h->pool.size()) {
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    h->pool.push_back(e);
+  }
+  return h->pool[h->pool_used++];
+}
+// Bracket a launch (or a group of launches) of class `slot` with events on stream st.
+void prof_begin(memfine_handle_s* h, int slot, cudaStream_t st) {
+  if (!h->prof) return;
+  h->open_slot = slot;
+  h->open_ev = pool_event(h);
+  cudaEventRecord(h->open_ev, st);
+}
+void prof_end(memfine_handle_s* h, cudaStream_t st) {
+  if (!h->prof || h->open_slot < 0) return;
+  cudaEvent_t b = pool_event(h);
+  cudaEventRecord(b, st);
+  h->recs.push_back({h->open_slot, h->open_ev, b});
+  h->open_slot = -1;
+}
+}  // namespace
 
 namespace {
 
@@ -231,12 +264,14 @@ bool bf16_use_simt() {
 template <typename T>
 int run_gemm(memfine_handle_s* h, const GemmProblem<T>& p, cudaStream_t st) {
   int n;
+  prof_begin(h, p.kind, st);
   if constexpr (std::is_same<T, __nv_bfloat16>::value) {
     if (bf16_use_simt()) n = launch_gemm_simt<T>(p, st);
     else n = launch_gemm_sm100(p, st);
   } else {
     n = launch_gemm_simt<T>(p, st);
   }
+  prof_end(h, st);
   if (n < 0) return MEMFINE_ERR_UNSUPPORTED;
   h->last.gemm_launches += n;
   h->last.kernel_launches += n;
@@ -265,10 +300,12 @@ memfine_status fwd_ep1(memfine_handle_s* h, const T* x, const int32_t* ids, cons
     int64_t t0 = chunk_begin(d.tokens, C, j), t1 = chunk_begin(d.tokens, C, j + 1);
     if (t1 == t0) continue;
     int NB = (int)ceil_div64(t1 - t0, kTokPerBlk);
+    prof_begin(h, 6, st);
     launch_dispatch_hist(ids, t0, t1, k, E, L.m, h->status_d, st);
     launch_dispatch_scan(NB, E, El, 1, R, L.m, h->rows_d, h->rows_d + kMaxSub, j, st);
     launch_dispatch_scatter<T>(x, nullptr, ids, w, t0, t1, k, E, hd, L.m, (T*)L.X, nullptr, st);
     launch_zero_padding<T>(El, hd, L.m, (T*)L.X, nullptr, st);
+    prof_end(h, st);
     h->last.kernel_launches += 4;
     if (h->debug) {
       cudaStreamSynchronize(st);
@@ -284,7 +321,9 @@ memfine_status fwd_ep1(memfine_handle_s* h, const T* x, const int32_t* ids, cons
     if (int rc = run_gemm<T>(h, p, st)) return (memfine_status)rc;
     p.kind = GK_DOWN;
     if (int rc = run_gemm<T>(h, p, st)) return (memfine_status)rc;
+    prof_begin(h, 7, st);
     launch_combine<T>((const T*)L.O, w, t0, t1, k, hd, L.m, y, st);
+    prof_end(h, st);
     h->last.kernel_launches += 1;
   }
   return latch_cuda(h);
@@ -301,6 +340,7 @@ memfine_status bwd_ep1(memfine_handle_s* h, const T* dy, const T* x, const int32
   int E = d.num_experts, El = E, k = d.topk, hd = d.hidden, g = d.ffn;
   h->last_meta = L.meta_bytes;
   h->last_row_bytes = L.row_bytes;
+  prof_begin(h, 8, st);
   if (!accumulate) {
     size_t wb = sizeof(float) * (size_t)El * g * hd;
     MF_CUDA_OK(cudaMemsetAsync(dwg, 0, wb, st));
@@ -308,15 +348,18 @@ memfine_status bwd_ep1(memfine_handle_s* h, const T* dy, const T* x, const int32
     MF_CUDA_OK(cudaMemsetAsync(dwd, 0, wb, st));
   }
   if (dscore && d.tokens > 0) MF_CUDA_OK(cudaMemsetAsync(dscore, 0, sizeof(float) * d.tokens * k, st));
+  prof_end(h, st);
   for (int j = 0; j < C; j++) {
     int64_t t0 = chunk_begin(d.tokens, C, j), t1 = chunk_begin(d.tokens, C, j + 1);
     if (t1 == t0) continue;
     int NB = (int)ceil_div64(t1 - t0, kTokPerBlk);
     // B1: re-dispatch x and dy of the chunk (the recompute of Eq. 7 starts from X_j)
+    prof_begin(h, 6, st);
     launch_dispatch_hist(ids, t0, t1, k, E, L.m, h->status_d, st);
     launch_dispatch_scan(NB, E, El, 1, R, L.m, h->rows_d, h->rows_d + kMaxSub, j, st);
     launch_dispatch_scatter<T>(x, dy, ids, w, t0, t1, k, E, hd, L.m, (T*)L.X, (T*)L.DY, st);
     launch_zero_padding<T>(El, hd, L.m, (T*)L.X, (T*)L.DY, st);
+    prof_end(h, st);
     h->last.kernel_launches += 4;
     GemmProblem<T> p = base_problem<T>(h, L, wg, wu, wd);
     p.dWg = dwg;
@@ -339,7 +382,9 @@ memfine_status bwd_ep1(memfine_handle_s* h, const T* dy, const T* x, const int32
     p.kind = GK_DX;
     if (int rc = run_gemm<T>(h, p, st)) return (memfine_status)rc;
     // B7: dX_i = sum_slot dX_disp[pos], d_score
+    prof_begin(h, 7, st);
     launch_unpermute_reduce<T>((const T*)L.O, t0, t1, k, hd, L.m, dx, dscore, st);
+    prof_end(h, st);
     h->last.kernel_launches += 1;
   }
   return latch_cuda(h);
@@ -491,6 +536,7 @@ memfine_status ep_run(memfine_handle_s* h, int pass, const T* dy, const T* x, co
     launch_ep_recv_seg(h->counts_d, C, j, E, El, d.ep_rank, d.ep_size, L.rows_cap, L.m, h->rows_d,
                        h->rows_d + kMaxSub, st);
     // A6/B1: dispatch all-to-allv
+    prof_begin(h, 9, st);
     if (ep_exchange(h, t, h->counts_h, C, j, true, (char*)L.send, (char*)L.X, rb, st)) return MEMFINE_ERR_NCCL;
     if (pass == MEMFINE_BWD) {
       if (ep_exchange(h, t, h->counts_h, C, j, true, (char*)L.send_dy, (char*)L.DY, rb, st)) return MEMFINE_ERR_NCCL;
@@ -498,6 +544,7 @@ memfine_status ep_run(memfine_handle_s* h, int pass, const T* dy, const T* x, co
         return MEMFINE_ERR_NCCL;
       if (t.rows_pad) MF_CUDA_OK(cudaMemsetAsync(L.m.dw_row, 0, sizeof(float) * t.rows_pad, st));
     }
+    prof_end(h, st);
     launch_zero_padding<T>(El, hd, L.m, (T*)L.X, pass == MEMFINE_BWD ? (T*)L.DY : nullptr, st);
     h->last.kernel_launches += 2;
     GemmProblem<T> p = base_problem<T>(h, L, wg, wu, wd);
@@ -636,6 +683,7 @@ memfine_status memfine_destroy(memfine_handle_t h) {
   if (h->counts_d) cudaFree(h->counts_d);
   if (h->counts_h) cudaFreeHost(h->counts_h);
   if (h->ev) cudaEventDestroy(h->ev);
+  for (auto e : h->pool) cudaEventDestroy(e);
   delete h;
   return MEMFINE_OK;
 }
@@ -775,6 +823,27 @@ memfine_status memfine_sync(memfine_handle_t h, void* stream) {
 memfine_status memfine_last_stats(memfine_handle_t h, memfine_stats* out) {
   if (!h || !out) return MEMFINE_ERR_INVALID_ARG;
   *out = h->last;
+  return MEMFINE_OK;
+}
+
+memfine_status memfine_profile_enable(memfine_handle_t h, int32_t enable) {
+  if (!h) return MEMFINE_ERR_INVALID_ARG;
+  h->prof = enable ? 1 : 0;
+  return MEMFINE_OK;
+}
+
+memfine_status memfine_profile_read(memfine_handle_t h, memfine_profile* out) {
+  if (!h || !out) return MEMFINE_ERR_INVALID_ARG;
+  memset(out, 0, sizeof *out);
+  for (auto& r : h->recs) {
+    if (cudaEventSynchronize(r.b) != cudaSuccess) { cudaGetLastError(); return MEMFINE_ERR_CUDA; }
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, r.a, r.b);
+    out->launches[r.slot] += 1;
+    out->ms[r.slot] += ms;
+  }
+  h->recs.clear();
+  h->pool_used = 0;
   return MEMFINE_OK;
 }
 

@@ -137,6 +137,14 @@ class MemFine:
         capi.check(capi.lib().memfine_last_stats(self.h, C.byref(s)), "memfine_last_stats")
         return s.as_dict()
 
+    def profile_enable(self, on: bool = True):
+        capi.check(capi.lib().memfine_profile_enable(self.h, int(on)), "memfine_profile_enable")
+
+    def profile_read(self) -> dict:
+        pr = capi.Profile()
+        capi.check(capi.lib().memfine_profile_read(self.h, C.byref(pr)), "memfine_profile_read")
+        return pr.as_dict()
+
     def set_debug(self, on: bool = True):
         capi.check(capi.lib().memfine_set_debug(self.h, int(on)), "memfine_set_debug")
 

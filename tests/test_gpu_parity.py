@@ -173,3 +173,12 @@ def test_mixtral_full_size_sampled():
     assert rel_err(dx.float().cpu().numpy()[toks], rdx) <= 2e-2
     assert rel_err(ds.cpu().numpy()[toks], rds) <= 2e-2
     assert torch.isfinite(dwg).all() and torch.isfinite(dwu).all() and torch.isfinite(dwd).all()
+
+
+@pytest.mark.parametrize("C", [1, 2])
+def test_many_tiles_per_cta(C):
+    """8192 tokens x top-2 over 4 experts: ~512 gate/up tiles and 4096-deep weight-gradient K
+    loops, so every persistent CTA runs several tiles through both TMEM accumulator stages."""
+    p = make_problem(8192, 256, 512, 4, 2, zipf_s=1.2, seed=6)
+    run = GpuRun(p)
+    _check_all(p, run, C, oracle_fwd_bwd(p, C))
