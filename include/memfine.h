@@ -170,6 +170,20 @@ memfine_status memfine_workspace_bytes(const int32_t* counts_host, int32_t nsub,
                                        const memfine_dims* dims, int32_t C, int32_t pass,
                                        uint64_t* bytes);
 
+/* A6 (EP > 1), host only: the all-to-allv the layer performs for chunk `chunk` of C on
+ * rank dims->ep_rank.  counts_host: int32 [EP][nsub][E] (the all-gathered routing counts),
+ * C | nsub.  Outputs (host):
+ *   send_rows[EP]        rows this rank sends to each peer (its chunk copies, by dest rank)
+ *   recv_rows[EP]        rows it receives from each source rank
+ *   recv_offsets[EP*E_l] first row of (src, local expert) in the padded expert-major receive
+ *                        buffer: local expert major, src rank minor (reading R3), each local
+ *                        expert's segment padded to 128 rows
+ *   rows_padded          total padded receive rows of the chunk (nullable)
+ * Pure; no GPU, no communication. */
+memfine_status memfine_a2a_plan(const int32_t* counts_host, int32_t nsub, const memfine_dims* dims, int32_t C,
+                                int32_t chunk, int64_t* send_rows, int64_t* recv_rows, int64_t* recv_offsets,
+                                int64_t* rows_padded);
+
 /* FCDA forward (Eq. 6): Y = concat_j combine(expert(dispatch(X_j))).
  *   x       dev [T][h]        bf16 or fp32 (dims.dtype)
  *   ids     dev [T][k]        int32 global expert ids

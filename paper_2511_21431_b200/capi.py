@@ -16,7 +16,7 @@ FWD, BWD = 0, 1
 
 # Every symbol include/memfine.h declares (checked by tests/test_abi.py).
 SYMBOLS = ("memfine_abi_version", "memfine_status_str", "memfine_nccl_unique_id", "memfine_create",
-           "memfine_destroy", "memfine_route_counts", "memfine_plan", "memfine_workspace_bytes",
+           "memfine_destroy", "memfine_route_counts", "memfine_plan", "memfine_workspace_bytes", "memfine_a2a_plan",
            "memfine_moe_fwd", "memfine_moe_bwd", "memfine_sync", "memfine_last_stats",
            "memfine_profile_enable", "memfine_profile_read", "memfine_set_debug", "memfine_debug_perm")
 
@@ -95,6 +95,7 @@ def lib():
         L.memfine_route_counts.argtypes = [vp, vp, i32, vp, vp]
         L.memfine_plan.argtypes = [vp, i32, C.POINTER(Dims), C.POINTER(Budget), C.POINTER(PlanInfo)]
         L.memfine_workspace_bytes.argtypes = [vp, i32, C.POINTER(Dims), i32, i32, C.POINTER(u64)]
+        L.memfine_a2a_plan.argtypes = [vp, i32, C.POINTER(Dims), i32, i32, vp, vp, vp, vp]
         L.memfine_moe_fwd.argtypes = [vp, vp, vp, vp, vp, vp, vp, i32, vp, vp, u64, vp]
         L.memfine_moe_bwd.argtypes = [vp, vp, vp, vp, vp, vp, vp, vp, i32, vp, vp, vp, vp, vp, i32, vp, u64, vp]
         L.memfine_sync.argtypes = [vp, vp]

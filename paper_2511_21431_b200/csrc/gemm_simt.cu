@@ -56,7 +56,8 @@ __global__ void __launch_bounds__(256) gemm_simt_kernel(GemmProblem<T> p, int M,
     row0 = p.seg[e];
     Kc = p.seg[e + 1] - row0;
     m0 = blockIdx.y * SB;
-    if (p.info[kInfoSkip] || Kc == 0) return;
+    if (p.info[kInfoSkip]) return;
+    if (Kc == 0 && p.wgrad_beta) return;
   } else {
     int rows = p.info[kInfoRowsPad];
     m0 = blockIdx.y * SB;
@@ -138,13 +139,17 @@ __global__ void __launch_bounds__(256) gemm_simt_kernel(GemmProblem<T> p, int M,
           p.A[row * p.g + n] = Elt<T>::from_f(ws * a);
           break;
         }
-        case GK_WGRAD_DOWN:
-          p.dWd[((int64_t)e * p.h + m) * p.g + n] += v;
+        case GK_WGRAD_DOWN: {
+          float* d = p.dWd + ((int64_t)e * p.h + m) * p.g + n;
+          *d = p.wgrad_beta ? *d + v : v;
           break;
-        default:
-          if (m < p.g) p.dWg[((int64_t)e * p.g + m) * p.h + n] += v;
-          else p.dWu[((int64_t)e * p.g + (m - p.g)) * p.h + n] += v;
+        }
+        default: {
+          float* d = (m < p.g) ? p.dWg + ((int64_t)e * p.g + m) * p.h + n
+                               : p.dWu + ((int64_t)e * p.g + (m - p.g)) * p.h + n;
+          *d = p.wgrad_beta ? *d + v : v;
           break;
+        }
       }
     }
     if (p.kind == GK_DACT) atomicAdd(p.dw_row + row, dwp);

@@ -5,7 +5,8 @@
 //   warp 0      TMA producer: cp.async.bulk.tensor 2D/3D loads, 128B swizzle, mbarrier tx
 //   warp 1      TMEM allocator + MMA issuer: tcgen05.mma.cta_group::1.kind::f16, BF16 in,
 //               FP32 accumulators in TMEM, tcgen05.commit -> mbarriers
-//   warps 2..5  epilogue: tcgen05.ld 32x32b -> registers -> fused MoE epilogue -> global
+//   warps 2..9  epilogue: tcgen05.ld 32x32b -> registers -> fused MoE epilogue -> global;
+//               two warps per TMEM lane quarter (warp % 4), each taking half of the columns
 // A 4-stage smem ring (48 KB/stage) feeds the MMA; two TMEM accumulator stages (512 cols)
 // let the epilogue of tile i overlap the mainloop of tile i+1.
 //
@@ -21,7 +22,7 @@
 namespace memfine {
 namespace sm100 {
 
-constexpr int BM = 128, BK = 64, STAGES = 4, THREADS = 192;
+constexpr int BM = 128, BK = 64, STAGES = 4, EPI_WARPS = 8, THREADS = 64 + 32 * EPI_WARPS;
 constexpr int A_BYTES = BM * BK * 2;  // 16 KB
 
 // ------------------------------------------------------------------ PTX wrappers
@@ -133,7 +134,8 @@ __device__ __forceinline__ void load32_bf16(const __nv_bfloat16* src, float* v) 
 // ------------------------------------------------------------------ per-kind configuration
 template <int KIND>
 struct Cfg;
-// A7/B2: X[R,h] x W_gate/W_up[g,h]^T, two accumulators (G, U) of 128 columns.
+// A7/B2: X[R,h] x W_gate/W_up[g,h]^T: the W_gate and W_up tiles land back to back in smem and
+// form one 256-row B operand, so a single N=256 MMA produces G (cols 0..127) and U (128..255).
 template <> struct Cfg<GK_GATEUP> { static constexpr int BN = 128, NACC = 2, A_MN = 0, B_MN = 0; };
 // A8: a[R,g] x W_down[h,g]^T.
 template <> struct Cfg<GK_DOWN> { static constexpr int BN = 256, NACC = 1, A_MN = 0, B_MN = 0; };
@@ -160,13 +162,13 @@ struct Params {
   float* dW0;        // WGRAD_DOWN: dW_down; WGRAD_GU: dW_gate
   float* dW1;        // WGRAD_GU: dW_up
   int store_a, store_gu;
+  int beta;          // WGRAD: 1 = dW += acc (accumulate), 0 = dW = acc (first chunk, overwrite)
+  int group_m;       // M tiles per raster group (host-sized so a wave's operands stay in L2)
 };
 
 struct Tile {
   int e, m0, n0, k0, nkb;  // expert, first row (M-tiled: padded row; WGRAD: dW row), first column, K origin, K blocks
 };
-
-constexpr int GROUP_M = 8;
 
 template <int KIND>
 __device__ __forceinline__ int num_tiles(const Params& p) {
@@ -185,18 +187,22 @@ __device__ __forceinline__ Tile tile_of(const Params& p, int t) {
   if (KIND >= GK_WGRAD_DOWN) {
     int per = p.num_mt_w * nt;
     T.e = t / per;
-    int r = t % per;
-    T.m0 = (r % p.num_mt_w) * BM;
-    T.n0 = (r / p.num_mt_w) * BN;
+    int r0 = t % per;
+    int gsz = p.group_m * nt;
+    int gi = r0 / gsz, first = gi * p.group_m;
+    int gm = min(p.num_mt_w - first, p.group_m);
+    int r = r0 % gsz;
+    T.m0 = (first + r % gm) * BM;
+    T.n0 = (r / gm) * BN;
     int s0 = __ldg(p.seg + T.e), s1 = __ldg(p.seg + T.e + 1);
     T.k0 = s0;
     T.nkb = (s1 - s0) / BK;
     return T;
   }
   int num_mt = p.info[kInfoRowsPad] / BM;
-  int gsz = GROUP_M * nt;
-  int gi = t / gsz, first = gi * GROUP_M;
-  int gm = min(num_mt - first, GROUP_M);
+  int gsz = p.group_m * nt;
+  int gi = t / gsz, first = gi * p.group_m;
+  int gm = min(num_mt - first, p.group_m);
   int r = t % gsz;
   int mt = first + r % gm;
   T.m0 = mt * BM;
@@ -220,7 +226,9 @@ __global__ void __launch_bounds__(THREADS, 1)
   constexpr int ACC_COLS = NACC * BN;                                 // per accumulator stage
   constexpr uint32_t TMEM_COLS = 2 * ACC_COLS;                         // double-buffered
   static_assert(TMEM_COLS <= 512, "TMEM");
-  constexpr uint32_t IDESC = idesc_bf16(BM, BN, CF::A_MN, CF::B_MN);
+  constexpr int MMA_N = NACC * BN;                                    // GATEUP: G||U in one MMA
+  static_assert(MMA_N <= 256, "MMA N");
+  constexpr uint32_t IDESC = idesc_bf16(BM, MMA_N, CF::A_MN, CF::B_MN);
 
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
@@ -236,7 +244,7 @@ __global__ void __launch_bounds__(THREADS, 1)
     prefetch_tmap(&tmB0);
     if (NB_OPS == 2 || KIND == GK_DX) prefetch_tmap(&tmB1);
     for (int s = 0; s < STAGES; s++) { mbar_init(full + s, 1); mbar_init(empty + s, 1); }
-    for (int a = 0; a < 2; a++) { mbar_init(tfull + a, 1); mbar_init(tempty + a, 4); }
+    for (int a = 0; a < 2; a++) { mbar_init(tfull + a, 1); mbar_init(tempty + a, EPI_WARPS); }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   }
@@ -315,12 +323,8 @@ __global__ void __launch_bounds__(THREADS, 1)
 #pragma unroll
           for (int k = 0; k < BK / 16; k++) {
             uint64_t ad = CF::A_MN ? sdesc(sa + k * 2048, 8192, 1024) : sdesc(sa + k * 32, 16, 1024);
-#pragma unroll
-            for (int q = 0; q < NACC; q++) {
-              uint32_t bq = sb + q * B_BYTES;
-              uint64_t bd = CF::B_MN ? sdesc(bq + k * 2048, 8192, 1024) : sdesc(bq + k * 32, 16, 1024);
-              mma_bf16(dbase + q * BN, ad, bd, IDESC, (kb | k) != 0);
-            }
+            uint64_t bd = CF::B_MN ? sdesc(sb + k * 2048, 8192, 1024) : sdesc(sb + k * 32, 16, 1024);
+            mma_bf16(dbase, ad, bd, IDESC, (kb | k) != 0);
           }
           mma_commit(empty + stage);
           if (++stage == STAGES) { stage = 0; phase ^= 1; }
@@ -330,13 +334,31 @@ __global__ void __launch_bounds__(THREADS, 1)
       }
     }
   } else {
-    // ================================================================ epilogue (warps 2..5)
+    // ================================================================ epilogue (warps 2..9)
     const int q = warp & 3;               // TMEM lane quarter this warp may access
+    const int half = (warp - 2) >> 2;     // which half of the tile's columns
     const int rloc = q * 32 + lane;       // row within the 128-row tile
+    constexpr int CPW = BN / 2;           // columns per epilogue warp
     int it = 0;
     for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
       Tile T = tile_of<KIND>(p, t);
-      if (T.nkb == 0) continue;
+      if (T.nkb == 0) {
+        if (KIND >= GK_WGRAD_DOWN && !p.beta) {
+          // an expert without rows in the first chunk: its dW tile is zero
+          const int m = T.m0 + rloc;
+          if (m < p.M)
+            for (int c = half * CPW; c < (half + 1) * CPW; c += 4) {
+              const int n = T.n0 + c;
+              if (n >= p.N) break;
+              float* dst;
+              if (KIND == GK_WGRAD_DOWN) dst = p.dW0 + ((int64_t)T.e * p.h + m) * p.g + n;
+              else dst = (m < p.g) ? p.dW0 + ((int64_t)T.e * p.g + m) * p.h + n
+                                   : p.dW1 + ((int64_t)T.e * p.g + (m - p.g)) * p.h + n;
+              *reinterpret_cast<float4*>(dst) = make_float4(0.f, 0.f, 0.f, 0.f);
+            }
+        }
+        continue;
+      }
       int as = it & 1;
       uint32_t aph = (it >> 1) & 1;
       mbar_wait(tfull + as, aph);
@@ -347,7 +369,7 @@ __global__ void __launch_bounds__(THREADS, 1)
       float wrow = 0.f;
       if (KIND == GK_DACT) wrow = p.w_row[row];
 #pragma unroll 1
-      for (int c = 0; c < BN; c += 32) {
+      for (int c = half * CPW; c < (half + 1) * CPW; c += 32) {
         const int n = T.n0 + c;
         uint32_t r[32];
         tmem_ld32(tb + c, r);
@@ -403,14 +425,19 @@ __global__ void __launch_bounds__(THREADS, 1)
             else dst = (m < p.g) ? p.dW0 + ((int64_t)T.e * p.g + m) * p.h + n
                                  : p.dW1 + ((int64_t)T.e * p.g + (m - p.g)) * p.h + n;
             float4* d4 = reinterpret_cast<float4*>(dst);
+            if (p.beta) {
 #pragma unroll
-            for (int i = 0; i < 8; i++) {
-              float4 o = d4[i];
-              o.x += v[4 * i];
-              o.y += v[4 * i + 1];
-              o.z += v[4 * i + 2];
-              o.w += v[4 * i + 3];
-              d4[i] = o;
+              for (int i = 0; i < 8; i++) {
+                float4 o = d4[i];
+                o.x += v[4 * i];
+                o.y += v[4 * i + 1];
+                o.z += v[4 * i + 2];
+                o.w += v[4 * i + 3];
+                d4[i] = o;
+              }
+            } else {
+#pragma unroll
+              for (int i = 0; i < 8; i++) d4[i] = make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
             }
           }
         }
@@ -503,6 +530,7 @@ int launch(const GemmProblem<__nv_bfloat16>& gp, cudaStream_t st) {
   p.dw_row = gp.dw_row;
   p.store_a = gp.store_a;
   p.store_gu = gp.store_gu;
+  p.beta = gp.wgrad_beta;
   const uint64_t R = (uint64_t)gp.rows_cap, h = gp.h, g = gp.g, El = gp.El;
   if (R == 0) return 0;
   CUtensorMap mA, mB0, mB1;
@@ -551,6 +579,12 @@ int launch(const GemmProblem<__nv_bfloat16>& gp, cudaStream_t st) {
   }
   if (!ok) return -1;
   int nt = (p.N + BN - 1) / BN;
+  {
+    // raster group: keep the group's A strips (GROUP_M x 128 rows x K) within ~48 MB of L2
+    int64_t kdim = (KIND >= GK_WGRAD_DOWN) ? (int64_t)std::max<int64_t>(1, R / std::max(1, (int)El)) : p.K;
+    int64_t strip = (int64_t)BM * kdim * 2;
+    p.group_m = (int)std::max<int64_t>(1, std::min<int64_t>(64, (48ll << 20) / std::max<int64_t>(1, strip)));
+  }
   if (KIND >= GK_WGRAD_DOWN) {
     p.num_mt_w = (p.M + BM - 1) / BM;
     max_tiles = (int64_t)p.El * p.num_mt_w * nt;

@@ -84,6 +84,7 @@ struct GemmProblem {
   float* dWd;        // [El][h][g]
   int store_a;       // GATEUP: store a
   int store_gu;      // GATEUP: store G||U
+  int wgrad_beta;    // WGRAD: 1 accumulate into dW, 0 overwrite (zero tiles for experts without rows)
 };
 
 // CUDA-core FFMA path (MEMFINE_FP32 mode; K12 of SURVEY §2.4).

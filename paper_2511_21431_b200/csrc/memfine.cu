@@ -340,8 +340,11 @@ memfine_status bwd_ep1(memfine_handle_s* h, const T* dy, const T* x, const int32
   int E = d.num_experts, El = E, k = d.topk, hd = d.hidden, g = d.ffn;
   h->last_meta = L.meta_bytes;
   h->last_row_bytes = L.row_bytes;
+  // dW is overwritten by the first non-empty chunk's weight-gradient GEMMs (beta = 0) and
+  // accumulated by the later ones; only a call with no tokens at all needs a memset.
+  int beta = accumulate ? 1 : 0;
   prof_begin(h, 8, st);
-  if (!accumulate) {
+  if (!accumulate && d.tokens == 0) {
     size_t wb = sizeof(float) * (size_t)El * g * hd;
     MF_CUDA_OK(cudaMemsetAsync(dwg, 0, wb, st));
     MF_CUDA_OK(cudaMemsetAsync(dwu, 0, wb, st));
@@ -374,10 +377,12 @@ memfine_status bwd_ep1(memfine_handle_s* h, const T* dy, const T* x, const int32
     p.kind = GK_DACT;
     if (int rc = run_gemm<T>(h, p, st)) return (memfine_status)rc;
     // B5: weight gradients accumulate across chunks (reading R18)
+    p.wgrad_beta = beta;
     p.kind = GK_WGRAD_DOWN;
     if (int rc = run_gemm<T>(h, p, st)) return (memfine_status)rc;
     p.kind = GK_WGRAD_GU;
     if (int rc = run_gemm<T>(h, p, st)) return (memfine_status)rc;
+    beta = 1;
     // B4: dX_disp = dG W_gate + dU W_up (overwrites X_disp, dead after B5)
     p.kind = GK_DX;
     if (int rc = run_gemm<T>(h, p, st)) return (memfine_status)rc;
@@ -508,13 +513,8 @@ memfine_status ep_run(memfine_handle_s* h, int pass, const T* dy, const T* x, co
   h->last_meta = L.meta_bytes;
   h->last_row_bytes = L.row_bytes;
   size_t rb = (size_t)hd * sizeof(T);
+  int beta = accumulate ? 1 : 0;  // first chunk overwrites dW, later chunks accumulate
   if (pass == MEMFINE_BWD) {
-    if (!accumulate) {
-      size_t wb = sizeof(float) * (size_t)El * g * hd;
-      MF_CUDA_OK(cudaMemsetAsync(dwg, 0, wb, st));
-      MF_CUDA_OK(cudaMemsetAsync(dwu, 0, wb, st));
-      MF_CUDA_OK(cudaMemsetAsync(dwd, 0, wb, st));
-    }
     if (dscore && d.tokens > 0) MF_CUDA_OK(cudaMemsetAsync(dscore, 0, sizeof(float) * d.tokens * k, st));
   }
   for (int j = 0; j < C; j++) {
@@ -567,10 +567,12 @@ memfine_status ep_run(memfine_handle_s* h, int pass, const T* dy, const T* x, co
       if (int rc = run_gemm<T>(h, p, st)) return (memfine_status)rc;
       p.kind = GK_DACT;
       if (int rc = run_gemm<T>(h, p, st)) return (memfine_status)rc;
+      p.wgrad_beta = beta;
       p.kind = GK_WGRAD_DOWN;
       if (int rc = run_gemm<T>(h, p, st)) return (memfine_status)rc;
       p.kind = GK_WGRAD_GU;
       if (int rc = run_gemm<T>(h, p, st)) return (memfine_status)rc;
+      beta = 1;
       p.kind = GK_DX;
       if (int rc = run_gemm<T>(h, p, st)) return (memfine_status)rc;
       // B6: dX rows and d_w back to the source ranks, then B7
@@ -765,6 +767,32 @@ memfine_status memfine_workspace_bytes(const int32_t* counts_host, int32_t nsub,
   }
   Layout L = carve(d, C, pass, nullptr, rows_pad_max, d.ep_size > 1 ? send_max : 0);
   *bytes = L.total;
+  return MEMFINE_OK;
+}
+
+memfine_status memfine_a2a_plan(const int32_t* counts_host, int32_t nsub, const memfine_dims* dims, int32_t C,
+                                int32_t chunk, int64_t* send_rows, int64_t* recv_rows, int64_t* recv_offsets,
+                                int64_t* rows_padded) {
+  if (!counts_host || !dims_ok(dims) || C < 1 || C > kMaxSub || nsub < 1 || nsub > kMaxSub || nsub % C ||
+      chunk < 0 || chunk >= C || !send_rows || !recv_rows || !recv_offsets)
+    return MEMFINE_ERR_INVALID_ARG;
+  const memfine_dims& d = *dims;
+  int E = d.num_experts, EP = d.ep_size, El = E / EP, per = nsub / C;
+  std::vector<int> agg((size_t)EP * C * E, 0);  // [EP][C][E]
+  for (int src = 0; src < EP; src++)
+    for (int j = 0; j < nsub; j++)
+      for (int e = 0; e < E; e++) agg[((size_t)src * C + j / per) * E + e] += counts_host[((int64_t)src * nsub + j) * E + e];
+  EpChunk t = ep_chunk_table(d, agg.data(), C, chunk);
+  for (int peer = 0; peer < EP; peer++) {
+    send_rows[peer] = t.send_off[(peer + 1) * El] - t.send_off[peer * El];
+    int64_t r = 0;
+    for (int el = 0; el < El; el++) {
+      r += t.recv_cnt[(size_t)peer * El + el];
+      recv_offsets[(size_t)peer * El + el] = t.recv_off[(size_t)peer * El + el];
+    }
+    recv_rows[peer] = r;
+  }
+  if (rows_padded) *rows_padded = t.rows_pad;
   return MEMFINE_OK;
 }
 

@@ -52,6 +52,21 @@ def workspace_bytes(counts_host: Optional[torch.Tensor], dims: capi.Dims, C_: in
     return int(out.value)
 
 
+def a2a_plan(counts_host: torch.Tensor, dims: capi.Dims, C_: int, chunk: int):
+    """memfine_a2a_plan: (send_rows [EP], recv_rows [EP], recv_offsets [EP, E_l], rows_padded)."""
+    import numpy as np
+    assert counts_host.device.type == "cpu" and counts_host.dtype == torch.int32 and counts_host.is_contiguous()
+    EP, El = dims.ep_size, dims.num_experts // dims.ep_size
+    send = np.zeros(EP, np.int64)
+    recv = np.zeros(EP, np.int64)
+    off = np.zeros((EP, El), np.int64)
+    rp = C.c_int64()
+    vp = lambda a: a.ctypes.data_as(C.c_void_p)
+    capi.check(capi.lib().memfine_a2a_plan(_ptr(counts_host), counts_host.shape[1], C.byref(dims), C_, chunk,
+                                           vp(send), vp(recv), vp(off), C.byref(rp)), "memfine_a2a_plan")
+    return send, recv, off, int(rp.value)
+
+
 class MemFine:
     """One handle = one EP rank of one MoE layer shape.  ``process_group``: the EP group
     (torch.distributed) used only to broadcast the NCCL unique id when ep_size > 1."""
