@@ -17,6 +17,7 @@ enum InfoWord {
   kInfoRowsPad = 1,    // padded rows (multiple of 128)
   kInfoSend = 2,       // copies of this rank's chunk tokens (valid ids)
   kInfoSkip = 3,       // 1 => capacity exceeded, every kernel of the chunk is a no-op
+  kInfoPairs = 4,      // 256-row tile pairs (two 128-row m-tiles of one expert) for 2-CTA GEMMs
   kInfoWords = 8
 };
 
@@ -55,6 +56,11 @@ __device__ __forceinline__ int expert_of_row(const int* __restrict__ seg, int El
     if (__ldg(seg + mid) <= row) lo = mid; else hi = mid;
   }
   return lo;
+}
+
+// The local expert owning 256-row pair `pair` (pseg: prefix of ceil(m_tiles_e / 2)).
+__device__ __forceinline__ int expert_of_pair(const int* __restrict__ pseg, int El, int pair) {
+  return expert_of_row(pseg, El, pair);
 }
 
 }  // namespace memfine

@@ -17,12 +17,14 @@
 #include <cuda.h>
 #include <cudaTypedefs.h>
 #include <mutex>
+#include <cstdlib>
+#include <algorithm>
 #include "kernels.h"
 
 namespace memfine {
 namespace sm100 {
 
-constexpr int BM = 128, BK = 64, STAGES = 4, EPI_WARPS = 8, THREADS = 64 + 32 * EPI_WARPS;
+constexpr int BM = 128, BK = 64, EPI_WARPS = 8, THREADS = 64 + 32 * EPI_WARPS;
 constexpr int A_BYTES = BM * BK * 2;  // 16 KB
 
 // ------------------------------------------------------------------ PTX wrappers
@@ -150,9 +152,10 @@ template <> struct Cfg<GK_WGRAD_GU> { static constexpr int BN = 256, NACC = 1, A
 struct Params {
   int El, h, g;
   int M, N, K;       // M: rows of dW for WGRAD kinds; N: output columns; K: reduction (M-tiled kinds)
-  int num_mt_w;      // WGRAD: M tiles per expert
+  int num_mt_w;      // WGRAD: M tiles (of 128 or 256 rows) per expert
   int64_t rows_cap;
   const int* seg;
+  const int* pseg;
   const int* info;
   __nv_bfloat16* GU;
   __nv_bfloat16* A;
@@ -167,21 +170,70 @@ struct Params {
 };
 
 struct Tile {
-  int e, m0, n0, k0, nkb;  // expert, first row (M-tiled: padded row; WGRAD: dW row), first column, K origin, K blocks
+  int e;      // local expert
+  int m0;     // first row of the (pair) tile: padded row (M-tiled kinds) or dW row (WGRAD)
+  int m_end;  // rows >= m_end are not stored (expert segment end / M)
+  int n0, k0, nkb;
 };
 
-template <int KIND>
+// 2-CTA helpers (cta_group::2): the pair's leader is the even CTA of the cluster.
+constexpr uint32_t kPeerMask = 0xFEFFFFFFu;  // clears the CTA-in-pair bit of a shared::cluster address
+__device__ __forceinline__ uint32_t cta_rank_in_cluster() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void tma_2d_pair(void* dst, const CUtensorMap* m, uint64_t* bar, int c0, int c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, "
+      "%4}], [%2];" ::"r"(su32(dst)),
+      "l"(m), "r"(su32(bar) & kPeerMask), "r"(c0), "r"(c1)
+      : "memory");
+}
+__device__ __forceinline__ void tma_3d_pair(void* dst, const CUtensorMap* m, uint64_t* bar, int c0, int c1, int c2) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, "
+      "%4, %5}], [%2];" ::"r"(su32(dst)),
+      "l"(m), "r"(su32(bar) & kPeerMask), "r"(c0), "r"(c1), "r"(c2)
+      : "memory");
+}
+__device__ __forceinline__ void mma_bf16_pair(uint32_t d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n}" ::"r"(d),
+      "l"(a), "l"(b), "r"(idesc), "r"(acc)
+      : "memory");
+}
+// commit -> arrive on the barrier at the same smem offset in both CTAs of the pair
+__device__ __forceinline__ void mma_commit_pair(uint64_t* bar) {
+  asm volatile(
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+          su32(bar)),
+      "h"((uint16_t)3)
+      : "memory");
+}
+// arrive on the leader CTA's copy of a barrier (own copy when this is the leader)
+__device__ __forceinline__ void mbar_arrive_leader(uint64_t* b) {
+  asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(su32(b) & kPeerMask) : "memory");
+}
+
+template <int KIND, bool PAIR>
 __device__ __forceinline__ int num_tiles(const Params& p) {
   constexpr int BN = Cfg<KIND>::BN;
   int nt = (p.N + BN - 1) / BN;
   if (KIND >= GK_WGRAD_DOWN) return p.El * p.num_mt_w * nt;
   if (p.info[kInfoSkip]) return 0;
-  return (p.info[kInfoRowsPad] / BM) * nt;
+  return (PAIR ? p.info[kInfoPairs] : p.info[kInfoRowsPad] / BM) * nt;
 }
 
-template <int KIND>
+template <int KIND, bool PAIR>
 __device__ __forceinline__ Tile tile_of(const Params& p, int t) {
   constexpr int BN = Cfg<KIND>::BN;
+  constexpr int TM = PAIR ? 2 * BM : BM;  // rows per (pair) tile
   int nt = (p.N + BN - 1) / BN;
   Tile T;
   if (KIND >= GK_WGRAD_DOWN) {
@@ -192,123 +244,160 @@ __device__ __forceinline__ Tile tile_of(const Params& p, int t) {
     int gi = r0 / gsz, first = gi * p.group_m;
     int gm = min(p.num_mt_w - first, p.group_m);
     int r = r0 % gsz;
-    T.m0 = (first + r % gm) * BM;
+    T.m0 = (first + r % gm) * TM;
+    T.m_end = p.M;
     T.n0 = (r / gm) * BN;
     int s0 = __ldg(p.seg + T.e), s1 = __ldg(p.seg + T.e + 1);
     T.k0 = s0;
     T.nkb = (s1 - s0) / BK;
     return T;
   }
-  int num_mt = p.info[kInfoRowsPad] / BM;
+  int num_mt = PAIR ? p.info[kInfoPairs] : p.info[kInfoRowsPad] / BM;
   int gsz = p.group_m * nt;
   int gi = t / gsz, first = gi * p.group_m;
   int gm = min(num_mt - first, p.group_m);
   int r = t % gsz;
   int mt = first + r % gm;
-  T.m0 = mt * BM;
   T.n0 = (r / gm) * BN;
-  T.e = expert_of_row(p.seg, p.El, T.m0);
+  if (PAIR) {
+    T.e = expert_of_pair(p.pseg, p.El, mt);
+    T.m0 = __ldg(p.seg + T.e) + (mt - __ldg(p.pseg + T.e)) * TM;
+    T.m_end = __ldg(p.seg + T.e + 1);
+  } else {
+    T.m0 = mt * BM;
+    T.e = expert_of_row(p.seg, p.El, T.m0);
+    T.m_end = T.m0 + BM;
+  }
   T.k0 = 0;
   T.nkb = p.K / BK;
   return T;
 }
 
 // ------------------------------------------------------------------ the kernel
-template <int KIND>
+// PAIR = false: one CTA per 128-row tile, tcgen05.mma.cta_group::1 (M=128).
+// PAIR = true : a 2-CTA cluster per 256-row tile, tcgen05.mma.cta_group::2 (M=256) issued by the
+//               even CTA; each CTA stages 128 rows of A and half of B's columns, each CTA's TMEM
+//               holds its 128 rows x N accumulator.  Per-CTA operand traffic drops by a third.
+template <int KIND, bool PAIR>
 __global__ void __launch_bounds__(THREADS, 1)
     gemm_kernel(const __grid_constant__ Params p, const __grid_constant__ CUtensorMap tmA,
                 const __grid_constant__ CUtensorMap tmB0, const __grid_constant__ CUtensorMap tmB1) {
   using CF = Cfg<KIND>;
   constexpr int BN = CF::BN, NACC = CF::NACC;
-  constexpr int B_BYTES = BN * BK * 2;
-  constexpr int NB_OPS = (KIND == GK_GATEUP) ? 2 : 1;                 // B tiles per stage
-  constexpr int STAGE_BYTES = A_BYTES + NB_OPS * B_BYTES;
-  constexpr int ACC_COLS = NACC * BN;                                 // per accumulator stage
-  constexpr uint32_t TMEM_COLS = 2 * ACC_COLS;                         // double-buffered
-  static_assert(TMEM_COLS <= 512, "TMEM");
-  constexpr int MMA_N = NACC * BN;                                    // GATEUP: G||U in one MMA
+  constexpr int MMA_N = NACC * BN;                      // GATEUP: G||U in one MMA (N = 256)
   static_assert(MMA_N <= 256, "MMA N");
-  constexpr uint32_t IDESC = idesc_bf16(BM, MMA_N, CF::A_MN, CF::B_MN);
+  constexpr int B_ROWS = PAIR ? MMA_N / 2 : MMA_N;      // B rows (N) staged per CTA
+  constexpr int B_BYTES = B_ROWS * BK * 2;
+  constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+  constexpr int NSTAGE = PAIR ? 6 : 4;
+  constexpr int ACC_COLS = MMA_N;                       // per accumulator stage
+  constexpr uint32_t TMEM_COLS = 2 * ACC_COLS;          // double-buffered
+  static_assert(TMEM_COLS <= 512, "TMEM");
+  constexpr uint32_t IDESC = idesc_bf16(PAIR ? 2 * BM : BM, MMA_N, CF::A_MN, CF::B_MN);
 
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
-  uint64_t* full = (uint64_t*)(smem + STAGES * STAGE_BYTES);
-  uint64_t* empty = full + STAGES;
-  uint64_t* tfull = empty + STAGES;
+  uint64_t* full = (uint64_t*)(smem + NSTAGE * STAGE_BYTES);
+  uint64_t* empty = full + NSTAGE;
+  uint64_t* tfull = empty + NSTAGE;
   uint64_t* tempty = tfull + 2;
   uint32_t* tmem_slot = (uint32_t*)(tempty + 2);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t rank = PAIR ? cta_rank_in_cluster() : 0;
+  const bool leader = rank == 0;
+  const int cid = PAIR ? (int)(blockIdx.x >> 1) : (int)blockIdx.x;     // tile-loop index
+  const int ncid = PAIR ? (int)(gridDim.x >> 1) : (int)gridDim.x;
   if (warp == 0 && lane == 0) {
     prefetch_tmap(&tmA);
     prefetch_tmap(&tmB0);
-    if (NB_OPS == 2 || KIND == GK_DX) prefetch_tmap(&tmB1);
-    for (int s = 0; s < STAGES; s++) { mbar_init(full + s, 1); mbar_init(empty + s, 1); }
-    for (int a = 0; a < 2; a++) { mbar_init(tfull + a, 1); mbar_init(tempty + a, EPI_WARPS); }
+    if (KIND == GK_GATEUP || KIND == GK_DX) prefetch_tmap(&tmB1);
+    for (int s = 0; s < NSTAGE; s++) { mbar_init(full + s, 1); mbar_init(empty + s, 1); }
+    for (int a = 0; a < 2; a++) { mbar_init(tfull + a, 1); mbar_init(tempty + a, (PAIR ? 2 : 1) * EPI_WARPS); }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   }
   if (warp == 1) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(su32(tmem_slot)),
-                 "r"(TMEM_COLS)
-                 : "memory");
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    if (PAIR) {
+      asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(su32(tmem_slot)),
+                   "r"(TMEM_COLS)
+                   : "memory");
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+    } else {
+      asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(su32(tmem_slot)),
+                   "r"(TMEM_COLS)
+                   : "memory");
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    }
   }
   fence_before();
-  __syncthreads();
+  if (PAIR) cluster_sync(); else __syncthreads();
   fence_after();
   const uint32_t tmem_base = *tmem_slot;
-  const int ntiles = num_tiles<KIND>(p);
+  const int ntiles = num_tiles<KIND, PAIR>(p);
 
   if (warp == 0) {
-    // ================================================================ TMA producer
+    // ================================================================ TMA producer (both CTAs)
     if (lane == 0) {
       int stage = 0;
       uint32_t phase = 0;
-      for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
-        Tile T = tile_of<KIND>(p, t);
+      for (int t = cid; t < ntiles; t += ncid) {
+        Tile T = tile_of<KIND, PAIR>(p, t);
+        const int am0 = T.m0 + (int)rank * BM;              // this CTA's A rows
         for (int kb = 0; kb < T.nkb; kb++) {
           mbar_wait(empty + stage, phase ^ 1);
           uint8_t* sa = smem + stage * STAGE_BYTES;
           uint8_t* sb = sa + A_BYTES;
-          mbar_expect_tx(full + stage, STAGE_BYTES);
+          if (leader) mbar_expect_tx(full + stage, (PAIR ? 2 : 1) * STAGE_BYTES);
           int kc = T.k0 + kb * BK;
+          auto L2 = [&](void* dst, const CUtensorMap* m, int c0, int c1) {
+            if (PAIR) tma_2d_pair(dst, m, full + stage, c0, c1); else tma_2d(dst, m, full + stage, c0, c1);
+          };
+          auto L3 = [&](void* dst, const CUtensorMap* m, int c0, int c1, int c2) {
+            if (PAIR) tma_3d_pair(dst, m, full + stage, c0, c1, c2); else tma_3d(dst, m, full + stage, c0, c1, c2);
+          };
           if (CF::A_MN) {
-            // A(m,k) = rows[kc + k][m0 + m]: two 64-wide MN atoms of 64 K rows
-            tma_2d(sa, &tmA, full + stage, T.m0, kc);
-            tma_2d(sa + 8192, &tmA, full + stage, T.m0 + 64, kc);
+            // A(m,k) = rows[kc + k][am0 + m]: two 64-wide MN atoms of 64 K rows
+            L2(sa, &tmA, am0, kc);
+            L2(sa + 8192, &tmA, am0 + 64, kc);
           } else {
-            tma_2d(sa, &tmA, full + stage, kc, T.m0);
+            L2(sa, &tmA, kc, am0);
           }
+          // B: this CTA's share of the N columns
+          const int bn0 = T.n0 + (PAIR ? (int)rank * B_ROWS : 0);
           if (KIND == GK_GATEUP) {
-            tma_3d(sb, &tmB0, full + stage, kc, T.n0, T.e);
-            tma_3d(sb + B_BYTES, &tmB1, full + stage, kc, T.n0, T.e);
+            if (PAIR) {
+              L3(sb, rank ? &tmB1 : &tmB0, kc, T.n0, T.e);      // CTA0: W_gate rows, CTA1: W_up rows
+            } else {
+              L3(sb, &tmB0, kc, T.n0, T.e);
+              L3(sb + B_BYTES / 2, &tmB1, kc, T.n0, T.e);
+            }
           } else if (KIND == GK_DOWN) {
-            tma_3d(sb, &tmB0, full + stage, kc, T.n0, T.e);
+            L3(sb, &tmB0, kc, bn0, T.e);
           } else if (KIND == GK_DACT) {
 #pragma unroll
-            for (int i = 0; i < BN / 64; i++) tma_3d(sb + i * 8192, &tmB0, full + stage, T.n0 + 64 * i, kc, T.e);
+            for (int i = 0; i < B_ROWS / 64; i++) L3(sb + i * 8192, &tmB0, bn0 + 64 * i, kc, T.e);
           } else if (KIND == GK_DX) {
             const CUtensorMap* mb = kc < p.g ? &tmB0 : &tmB1;
             int kk = kc < p.g ? kc : kc - p.g;
 #pragma unroll
-            for (int i = 0; i < BN / 64; i++) tma_3d(sb + i * 8192, mb, full + stage, T.n0 + 64 * i, kk, T.e);
+            for (int i = 0; i < B_ROWS / 64; i++) L3(sb + i * 8192, mb, bn0 + 64 * i, kk, T.e);
           } else {
 #pragma unroll
-            for (int i = 0; i < BN / 64; i++) tma_2d(sb + i * 8192, &tmB0, full + stage, T.n0 + 64 * i, kc);
+            for (int i = 0; i < B_ROWS / 64; i++) L2(sb + i * 8192, &tmB0, bn0 + 64 * i, kc);
           }
-          if (++stage == STAGES) { stage = 0; phase ^= 1; }
+          if (++stage == NSTAGE) { stage = 0; phase ^= 1; }
         }
       }
     }
   } else if (warp == 1) {
-    // ================================================================ MMA issuer
-    if (lane == 0) {
+    // ================================================================ MMA issuer (leader CTA only)
+    if (lane == 0 && leader) {
       int stage = 0;
       uint32_t phase = 0;
       int it = 0;
-      for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
-        Tile T = tile_of<KIND>(p, t);
+      for (int t = cid; t < ntiles; t += ncid) {
+        Tile T = tile_of<KIND, PAIR>(p, t);
         if (T.nkb == 0) continue;
         int as = it & 1;
         uint32_t aph = (it >> 1) & 1;
@@ -324,38 +413,40 @@ __global__ void __launch_bounds__(THREADS, 1)
           for (int k = 0; k < BK / 16; k++) {
             uint64_t ad = CF::A_MN ? sdesc(sa + k * 2048, 8192, 1024) : sdesc(sa + k * 32, 16, 1024);
             uint64_t bd = CF::B_MN ? sdesc(sb + k * 2048, 8192, 1024) : sdesc(sb + k * 32, 16, 1024);
-            mma_bf16(dbase, ad, bd, IDESC, (kb | k) != 0);
+            if (PAIR) mma_bf16_pair(dbase, ad, bd, IDESC, (kb | k) != 0);
+            else mma_bf16(dbase, ad, bd, IDESC, (kb | k) != 0);
           }
-          mma_commit(empty + stage);
-          if (++stage == STAGES) { stage = 0; phase ^= 1; }
+          if (PAIR) mma_commit_pair(empty + stage); else mma_commit(empty + stage);
+          if (++stage == NSTAGE) { stage = 0; phase ^= 1; }
         }
-        mma_commit(tfull + as);
+        if (PAIR) mma_commit_pair(tfull + as); else mma_commit(tfull + as);
         it++;
       }
     }
   } else {
-    // ================================================================ epilogue (warps 2..9)
+    // ================================================================ epilogue (warps 2..9, both CTAs)
     const int q = warp & 3;               // TMEM lane quarter this warp may access
     const int half = (warp - 2) >> 2;     // which half of the tile's columns
-    const int rloc = q * 32 + lane;       // row within the 128-row tile
+    const int rloc = q * 32 + lane;       // row within this CTA's 128 rows
     constexpr int CPW = BN / 2;           // columns per epilogue warp
     int it = 0;
-    for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
-      Tile T = tile_of<KIND>(p, t);
+    for (int t = cid; t < ntiles; t += ncid) {
+      Tile T = tile_of<KIND, PAIR>(p, t);
+      const int rowi = T.m0 + (int)rank * BM + rloc;
+      const bool row_ok = rowi < T.m_end;
       if (T.nkb == 0) {
-        if (KIND >= GK_WGRAD_DOWN && !p.beta) {
+        if (KIND >= GK_WGRAD_DOWN && !p.beta && row_ok) {
           // an expert without rows in the first chunk: its dW tile is zero
-          const int m = T.m0 + rloc;
-          if (m < p.M)
-            for (int c = half * CPW; c < (half + 1) * CPW; c += 4) {
-              const int n = T.n0 + c;
-              if (n >= p.N) break;
-              float* dst;
-              if (KIND == GK_WGRAD_DOWN) dst = p.dW0 + ((int64_t)T.e * p.h + m) * p.g + n;
-              else dst = (m < p.g) ? p.dW0 + ((int64_t)T.e * p.g + m) * p.h + n
-                                   : p.dW1 + ((int64_t)T.e * p.g + (m - p.g)) * p.h + n;
-              *reinterpret_cast<float4*>(dst) = make_float4(0.f, 0.f, 0.f, 0.f);
-            }
+          const int m = rowi;
+          for (int c = half * CPW; c < (half + 1) * CPW; c += 4) {
+            const int n = T.n0 + c;
+            if (n >= p.N) break;
+            float* dst;
+            if (KIND == GK_WGRAD_DOWN) dst = p.dW0 + ((int64_t)T.e * p.h + m) * p.g + n;
+            else dst = (m < p.g) ? p.dW0 + ((int64_t)T.e * p.g + m) * p.h + n
+                                 : p.dW1 + ((int64_t)T.e * p.g + (m - p.g)) * p.h + n;
+            *reinterpret_cast<float4*>(dst) = make_float4(0.f, 0.f, 0.f, 0.f);
+          }
         }
         continue;
       }
@@ -364,10 +455,10 @@ __global__ void __launch_bounds__(THREADS, 1)
       mbar_wait(tfull + as, aph);
       fence_after();
       uint32_t tb = tmem_base + as * ACC_COLS + ((uint32_t)(q * 32) << 16);
-      const int64_t row = (int64_t)T.m0 + rloc;
+      const int64_t row = rowi;
       float dwp = 0.f;
       float wrow = 0.f;
-      if (KIND == GK_DACT) wrow = p.w_row[row];
+      if (KIND == GK_DACT && row_ok) wrow = p.w_row[row];
 #pragma unroll 1
       for (int c = half * CPW; c < (half + 1) * CPW; c += 32) {
         const int n = T.n0 + c;
@@ -382,7 +473,7 @@ __global__ void __launch_bounds__(THREADS, 1)
           float u[32];
 #pragma unroll
           for (int i = 0; i < 32; i++) u[i] = __uint_as_float(r2[i]);
-          if (n < p.g) {
+          if (row_ok && n < p.g) {
             if (p.store_gu) {
               store32_bf16(p.GU + row * 2 * p.g + n, v);
               store32_bf16(p.GU + row * 2 * p.g + p.g + n, u);
@@ -395,9 +486,9 @@ __global__ void __launch_bounds__(THREADS, 1)
             }
           }
         } else if (KIND == GK_DOWN || KIND == GK_DX) {
-          if (n < p.h) store32_bf16(p.O + row * p.h + n, v);
+          if (row_ok && n < p.h) store32_bf16(p.O + row * p.h + n, v);
         } else if (KIND == GK_DACT) {
-          if (n < p.g) {
+          if (row_ok && n < p.g) {
             float G[32], U[32], dG[32], dU[32], aw[32];
             load32_bf16(p.GU + row * 2 * p.g + n, G);
             load32_bf16(p.GU + row * 2 * p.g + p.g + n, U);
@@ -416,10 +507,9 @@ __global__ void __launch_bounds__(THREADS, 1)
             store32_bf16(p.A + row * p.g + n, aw);
           }
         } else {
-          // WGRAD: fp32 read-modify-write of dW (each element owned by one tile; accumulates
-          // across chunks, reading R18)
-          const int m = T.m0 + rloc;
-          if (m < p.M && n < p.N) {
+          // WGRAD: fp32 dW tile, overwrite (first chunk) or read-modify-write (later chunks)
+          const int m = rowi;
+          if (row_ok && n < p.N) {
             float* dst;
             if (KIND == GK_WGRAD_DOWN) dst = p.dW0 + ((int64_t)T.e * p.h + m) * p.g + n;
             else dst = (m < p.g) ? p.dW0 + ((int64_t)T.e * p.g + m) * p.h + n
@@ -442,19 +532,26 @@ __global__ void __launch_bounds__(THREADS, 1)
           }
         }
       }
-      if (KIND == GK_DACT) atomicAdd(p.dw_row + row, dwp);
+      if (KIND == GK_DACT && row_ok) atomicAdd(p.dw_row + row, dwp);
       fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(tempty + as);
+      if (lane == 0) {
+        if (PAIR) mbar_arrive_leader(tempty + as); else mbar_arrive(tempty + as);
+      }
       it++;
     }
   }
   fence_before();
-  __syncthreads();
+  if (PAIR) cluster_sync(); else __syncthreads();
   fence_after();
-  if (warp == 1)
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(TMEM_COLS)
-                 : "memory");
+  if (warp == 1) {
+    if (PAIR)
+      asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(TMEM_COLS)
+                   : "memory");
+    else
+      asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(TMEM_COLS)
+                   : "memory");
+  }
 }
 
 // ------------------------------------------------------------------ host side
@@ -499,15 +596,27 @@ bool map3d(CUtensorMap* m, const void* base, uint64_t d0, uint64_t d1, uint64_t 
 
 int g_num_sms = 0;
 
-template <int KIND>
+bool use_pairs() {
+  static int v = -1;
+  if (v < 0) {
+    const char* s = getenv("MEMFINE_GEMM_CTA");
+    v = (s && s[0] == '1') ? 0 : 1;  // default: 2-CTA pairs (cta_group::2); MEMFINE_GEMM_CTA=1 for 1-CTA
+  }
+  return v == 1;
+}
+
+template <int KIND, bool PAIR>
 int launch(const GemmProblem<__nv_bfloat16>& gp, cudaStream_t st) {
   using CF = Cfg<KIND>;
   constexpr int BN = CF::BN;
-  constexpr int NB_OPS = (KIND == GK_GATEUP) ? 2 : 1;
-  constexpr int SMEM = STAGES * (A_BYTES + NB_OPS * BN * BK * 2) + 1024 + 256;
+  constexpr int MMA_N = CF::NACC * BN;
+  constexpr int B_ROWS = PAIR ? MMA_N / 2 : MMA_N;
+  constexpr int NSTAGE = PAIR ? 6 : 4;
+  constexpr int SMEM = NSTAGE * (A_BYTES + B_ROWS * BK * 2) + 1024 + 256;
   static bool attr_set = false;
   if (!attr_set) {
-    if (cudaFuncSetAttribute(gemm_kernel<KIND>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM) != cudaSuccess)
+    if (cudaFuncSetAttribute(gemm_kernel<KIND, PAIR>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM) !=
+        cudaSuccess)
       return -1;
     attr_set = true;
   }
@@ -522,6 +631,7 @@ int launch(const GemmProblem<__nv_bfloat16>& gp, cudaStream_t st) {
   p.g = gp.g;
   p.rows_cap = gp.rows_cap;
   p.seg = gp.seg;
+  p.pseg = gp.pseg;
   p.info = gp.info;
   p.GU = gp.GU;
   p.A = gp.A;
@@ -535,18 +645,18 @@ int launch(const GemmProblem<__nv_bfloat16>& gp, cudaStream_t st) {
   if (R == 0) return 0;
   CUtensorMap mA, mB0, mB1;
   bool ok = true;
-  int64_t max_tiles;
+  const uint32_t gu_rows = PAIR ? BN : BN;  // per-CTA B box rows for GATEUP (one of W_gate / W_up)
   switch (KIND) {
     case GK_GATEUP:
       p.N = gp.g; p.K = gp.h;
       ok &= map2d(&mA, gp.X, h, R, BK, BM);
-      ok &= map3d(&mB0, gp.Wg, h, g, El, BK, BN);
-      ok &= map3d(&mB1, gp.Wu, h, g, El, BK, BN);
+      ok &= map3d(&mB0, gp.Wg, h, g, El, BK, gu_rows);
+      ok &= map3d(&mB1, gp.Wu, h, g, El, BK, gu_rows);
       break;
     case GK_DOWN:
       p.N = gp.h; p.K = gp.g;
       ok &= map2d(&mA, gp.A, g, R, BK, BM);
-      ok &= map3d(&mB0, gp.Wd, g, h, El, BK, BN);
+      ok &= map3d(&mB0, gp.Wd, g, h, El, BK, B_ROWS);
       mB1 = mB0;
       break;
     case GK_DACT:
@@ -578,35 +688,55 @@ int launch(const GemmProblem<__nv_bfloat16>& gp, cudaStream_t st) {
       break;
   }
   if (!ok) return -1;
+  constexpr int TM = PAIR ? 2 * BM : BM;
   int nt = (p.N + BN - 1) / BN;
   {
-    // raster group: keep the group's A strips (GROUP_M x 128 rows x K) within ~48 MB of L2
-    int64_t kdim = (KIND >= GK_WGRAD_DOWN) ? (int64_t)std::max<int64_t>(1, R / std::max(1, (int)El)) : p.K;
-    int64_t strip = (int64_t)BM * kdim * 2;
+    // raster group: keep the group's A strips (GROUP_M x TM rows x K) within ~48 MB of L2
+    int64_t kdim = (KIND >= GK_WGRAD_DOWN) ? (int64_t)std::max<int64_t>(1, R / std::max<uint64_t>(1, El)) : p.K;
+    int64_t strip = (int64_t)TM * kdim * 2;
     p.group_m = (int)std::max<int64_t>(1, std::min<int64_t>(64, (48ll << 20) / std::max<int64_t>(1, strip)));
   }
+  int64_t max_tiles;
   if (KIND >= GK_WGRAD_DOWN) {
-    p.num_mt_w = (p.M + BM - 1) / BM;
+    p.num_mt_w = (p.M + TM - 1) / TM;
     max_tiles = (int64_t)p.El * p.num_mt_w * nt;
   } else {
-    max_tiles = (int64_t)(R / BM) * nt;
+    max_tiles = (int64_t)((R / BM + (PAIR ? El : 0)) / (PAIR ? 2 : 1) + 1) * nt;
   }
-  int grid = (int)std::min<int64_t>(max_tiles, g_num_sms);
-  if (grid <= 0) return 0;
-  gemm_kernel<KIND><<<grid, THREADS, SMEM, st>>>(p, mA, mB0, mB1);
+  const int per_unit = PAIR ? 2 : 1;
+  int units = (int)std::min<int64_t>(max_tiles, g_num_sms / per_unit);
+  if (units <= 0) return 0;
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(units * per_unit);
+  cfg.blockDim = dim3(THREADS);
+  cfg.dynamicSmemBytes = SMEM;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = per_unit;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  if (cudaLaunchKernelEx(&cfg, gemm_kernel<KIND, PAIR>, p, mA, mB0, mB1) != cudaSuccess) return -1;
   return 1;
+}
+
+template <int KIND>
+int launch_kind(const GemmProblem<__nv_bfloat16>& gp, cudaStream_t st) {
+  return use_pairs() ? launch<KIND, true>(gp, st) : launch<KIND, false>(gp, st);
 }
 
 }  // namespace sm100
 
 int launch_gemm_sm100(const GemmProblem<__nv_bfloat16>& p, cudaStream_t st) {
   switch (p.kind) {
-    case GK_GATEUP: return sm100::launch<GK_GATEUP>(p, st);
-    case GK_DOWN: return sm100::launch<GK_DOWN>(p, st);
-    case GK_DACT: return sm100::launch<GK_DACT>(p, st);
-    case GK_DX: return sm100::launch<GK_DX>(p, st);
-    case GK_WGRAD_DOWN: return sm100::launch<GK_WGRAD_DOWN>(p, st);
-    case GK_WGRAD_GU: return sm100::launch<GK_WGRAD_GU>(p, st);
+    case GK_GATEUP: return sm100::launch_kind<GK_GATEUP>(p, st);
+    case GK_DOWN: return sm100::launch_kind<GK_DOWN>(p, st);
+    case GK_DACT: return sm100::launch_kind<GK_DACT>(p, st);
+    case GK_DX: return sm100::launch_kind<GK_DX>(p, st);
+    case GK_WGRAD_DOWN: return sm100::launch_kind<GK_WGRAD_DOWN>(p, st);
+    case GK_WGRAD_GU: return sm100::launch_kind<GK_WGRAD_GU>(p, st);
   }
   return -1;
 }

@@ -10,6 +10,7 @@ struct ChunkMeta {
   int* exp_cnt;    // [E]          this rank's chunk copies per global expert
   int* recv_cnt;   // [E_l]        rows received per local expert (EP>1; == exp_cnt slice at EP=1)
   int* seg;        // [E_l+1]      padded row segment starts of the local experts
+  int* pseg;       // [E_l+1]      prefix of 256-row tile pairs per local expert (2-CTA GEMMs)
   int* info;       // [kInfoWords]
   int* dest_of;    // [Tmax*k]     position of copy (i,slot): expert-major row (EP=1) or send row
   int* src_of;     // [rows_cap]   copy index feeding each row (EP=1, debug/gather), -1 padding
@@ -68,6 +69,7 @@ struct GemmProblem {
   int El, h, g;
   int64_t rows_cap;
   const int* seg;    // [El+1]
+  const int* pseg;   // [El+1]  pair prefix
   const int* info;   // chunk info words
   const T* X;        // X_disp [R][h]
   const T* DY;       // dY_disp [R][h]

@@ -132,6 +132,7 @@ Layout carve(const memfine_dims& d, int C, int pass, void* ws, int64_t rows_cap,
   L.m.exp_cnt = b.take<int>(E);
   L.m.recv_cnt = b.take<int>(El);
   L.m.seg = b.take<int>(El + 1);
+  L.m.pseg = b.take<int>(El + 1);
   L.m.info = b.take<int>(kInfoWords);
   L.m.dest_of = b.take<int>((uint64_t)Tm * d.topk);
   if (d.ep_size > 1) {
@@ -242,6 +243,7 @@ GemmProblem<T> base_problem(const memfine_handle_s* h, const Layout& L, const vo
   p.g = h->d.ffn;
   p.rows_cap = L.rows_cap;
   p.seg = L.m.seg;
+  p.pseg = L.m.pseg;
   p.info = L.m.info;
   p.X = (const T*)L.X;
   p.DY = (const T*)L.DY;

@@ -83,7 +83,7 @@ void launch_dispatch_hist(const int32_t* ids, int64_t t0, int64_t t1, int k, int
 // ------------------------------------------------------------------------------------------
 __global__ void dispatch_scan_kernel(int NB, int E, int El, int ep_size, int64_t rows_cap,
                                      int* __restrict__ blk, int* __restrict__ exp_cnt, int* __restrict__ recv_cnt,
-                                     int* __restrict__ seg, int* __restrict__ info,
+                                     int* __restrict__ seg, int* __restrict__ pseg, int* __restrict__ info,
                                      int64_t* stats_rows, int64_t* stats_rows_pad, int chunk) {
   __shared__ int base[1024];
   for (int e = threadIdx.x; e < E; e += blockDim.x) {
@@ -97,15 +97,18 @@ __global__ void dispatch_scan_kernel(int NB, int E, int El, int ep_size, int64_t
   }
   __syncthreads();
   if (threadIdx.x == 0) {
-    int acc = 0, send = 0;
+    int acc = 0, send = 0, pairs = 0;
     for (int e = 0; e < E; e++) {
       int c = exp_cnt[e];
       send += c;
       if (ep_size == 1) {
         base[e] = acc;
         seg[e] = acc;
+        pseg[e] = pairs;
         recv_cnt[e] = c;
-        acc += (int)round_up64(c, kRowAlign);
+        int pad = (int)round_up64(c, kRowAlign);
+        acc += pad;
+        pairs += (pad / kRowAlign + 1) / 2;
       } else {
         base[e] = acc;
         acc += c;
@@ -113,6 +116,8 @@ __global__ void dispatch_scan_kernel(int NB, int E, int El, int ep_size, int64_t
     }
     if (ep_size == 1) {
       seg[El] = acc;
+      pseg[El] = pairs;
+      info[kInfoPairs] = pairs;
       info[kInfoRows] = send;
       info[kInfoRowsPad] = acc;
       info[kInfoSkip] = (acc > rows_cap) ? 1 : 0;
@@ -129,7 +134,7 @@ __global__ void dispatch_scan_kernel(int NB, int E, int El, int ep_size, int64_t
 void launch_dispatch_scan(int NB, int E, int El, int ep_size, int64_t rows_cap, const ChunkMeta& m,
                           int64_t* stats_rows, int64_t* stats_rows_pad, int chunk, cudaStream_t st) {
   dispatch_scan_kernel<<<1, 1024, 0, st>>>(NB, E, El, ep_size, rows_cap, m.blk_cnt, m.exp_cnt, m.recv_cnt,
-                                           m.seg, m.info, stats_rows, stats_rows_pad, chunk);
+                                           m.seg, m.pseg, m.info, stats_rows, stats_rows_pad, chunk);
 }
 
 // ------------------------------------------------------------------------------------------
@@ -334,19 +339,25 @@ void launch_unpermute_reduce(const T* dXd, int64_t t0, int64_t t1, int k, int h,
 // EP > 1: received rows per local expert for chunk j from the all-gathered counts
 // [EP][C][E]; padded segment starts (expert-major: local expert, then src rank, reading R3).
 __global__ void ep_recv_seg_kernel(const int* __restrict__ counts, int C, int j, int E, int El, int me, int EP,
-                                   int64_t rows_cap, int* __restrict__ seg, int* __restrict__ recv_cnt,
-                                   int* __restrict__ info, int64_t* stats_rows, int64_t* stats_rows_pad) {
+                                   int64_t rows_cap, int* __restrict__ seg, int* __restrict__ pseg,
+                                   int* __restrict__ recv_cnt, int* __restrict__ info, int64_t* stats_rows,
+                                   int64_t* stats_rows_pad) {
   if (threadIdx.x != 0) return;
-  int acc = 0, rows = 0;
+  int acc = 0, rows = 0, pairs = 0;
   for (int el = 0; el < El; el++) {
     int c = 0;
     for (int src = 0; src < EP; src++) c += counts[((int64_t)src * C + j) * E + me * El + el];
     recv_cnt[el] = c;
     seg[el] = acc;
-    acc += (int)round_up64(c, kRowAlign);
+    pseg[el] = pairs;
+    int pad = (int)round_up64(c, kRowAlign);
+    acc += pad;
+    pairs += (pad / kRowAlign + 1) / 2;
     rows += c;
   }
   seg[El] = acc;
+  pseg[El] = pairs;
+  info[kInfoPairs] = pairs;
   info[kInfoRows] = rows;
   info[kInfoRowsPad] = acc;
   info[kInfoSkip] = acc > rows_cap ? 1 : 0;
@@ -355,8 +366,8 @@ __global__ void ep_recv_seg_kernel(const int* __restrict__ counts, int C, int j,
 
 void launch_ep_recv_seg(const int* counts, int C, int j, int E, int El, int me, int EP, int64_t rows_cap,
                         const ChunkMeta& m, int64_t* stats_rows, int64_t* stats_rows_pad, cudaStream_t st) {
-  ep_recv_seg_kernel<<<1, 32, 0, st>>>(counts, C, j, E, El, me, EP, rows_cap, m.seg, m.recv_cnt, m.info, stats_rows,
-                                       stats_rows_pad);
+  ep_recv_seg_kernel<<<1, 32, 0, st>>>(counts, C, j, E, El, me, EP, rows_cap, m.seg, m.pseg, m.recv_cnt, m.info,
+                                       stats_rows, stats_rows_pad);
 }
 
 // ------------------------------------------------------------------------------------------
