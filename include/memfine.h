@@ -56,6 +56,7 @@ typedef enum {
 enum { MEMFINE_BF16 = 0, MEMFINE_FP32 = 1 };         /* memfine_dims.dtype  */
 enum { MEMFINE_RULE_EQ9 = 0, MEMFINE_RULE_EXACT = 1 }; /* memfine_budget.rule */
 enum { MEMFINE_FWD = 0, MEMFINE_BWD = 1 };           /* workspace pass      */
+enum { MEMFINE_MODEL_PAPER = 0, MEMFINE_MODEL_IMPL = 1 }; /* memfine_budget.model */
 
 typedef struct memfine_handle_s* memfine_handle_t;
 
@@ -89,6 +90,14 @@ typedef struct {
                                     (Eq. 9 + "the large bin closest to c", reading R8);
                                     MEMFINE_RULE_EXACT: smallest bin whose true per-chunk
                                     maximum fits s'_max (every bin must divide nsub)        */
+    int32_t  model;              /* MEMFINE_MODEL_PAPER: the paper's per-copy activation
+                                    beta = D_t(2h+2g) (Table 2 rows 11-13; Eqs. 8-9 as above).
+                                    MEMFINE_MODEL_IMPL: C = smallest bin whose EXACT workspace
+                                    high-water (memfine_workspace_bytes, backward pass, max over
+                                    EP ranks) fits B - static - other; every bin must divide
+                                    nsub; s'_max / c_theory are still reported per Eqs. 8-9 and
+                                    predicted_peak_bytes is that exact workspace.  Evaluated on
+                                    the host (device counts are copied, 4*EP*nsub*E bytes).    */
 } memfine_budget;
 
 /* Result of memfine_plan. */

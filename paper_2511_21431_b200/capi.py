@@ -12,6 +12,7 @@ LIB_PATH = os.path.join(_PKG, "libmemfine.so")
 OK, ERR_INVALID_ARG, ERR_INFEASIBLE, ERR_ROUTING, ERR_CUDA, ERR_NCCL, ERR_WORKSPACE, ERR_UNSUPPORTED = range(8)
 BF16, FP32 = 0, 1
 RULE_EQ9, RULE_EXACT = 0, 1
+MODEL_PAPER, MODEL_IMPL = 0, 1
 FWD, BWD = 0, 1
 
 # Every symbol include/memfine.h declares (checked by tests/test_abi.py).
@@ -40,7 +41,7 @@ class Budget(C.Structure):
     _fields_ = [("gpu_capacity_bytes", C.c_uint64), ("alpha", C.c_double), ("static_bytes", C.c_uint64),
                 ("other_act_bytes", C.c_uint64), ("m_g", C.c_uint32), ("tp", C.c_uint32), ("cp", C.c_uint32),
                 ("micro_batch", C.c_uint32), ("bins", C.POINTER(C.c_int32)), ("nbins", C.c_int32),
-                ("rule", C.c_int32)]
+                ("rule", C.c_int32), ("model", C.c_int32)]
 
 
 class PlanInfo(C.Structure):
@@ -121,10 +122,10 @@ def check(status: int, where: str) -> None:
 
 def make_budget(gpu_capacity_bytes: int, alpha: float = 1.0, static_bytes: int = 0, other_act_bytes: int = 0,
                 m_g: int = 1, tp: int = 1, cp: int = 1, micro_batch: int = 1, bins=(1, 2, 4, 8),
-                rule: int = RULE_EQ9):
+                rule: int = RULE_EQ9, model: int = MODEL_PAPER):
     arr = (C.c_int32 * len(bins))(*bins) if bins is not None else None
     b = Budget(int(gpu_capacity_bytes), float(alpha), int(static_bytes), int(other_act_bytes), m_g, tp, cp,
                micro_batch, C.cast(arr, C.POINTER(C.c_int32)) if arr is not None else None,
-               len(bins) if bins is not None else 0, rule)
+               len(bins) if bins is not None else 0, rule, model)
     b._keep = arr  # keep the bins array alive
     return b

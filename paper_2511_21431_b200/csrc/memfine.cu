@@ -214,6 +214,7 @@ int budget_to_params(const memfine_dims* d, const memfine_budget* b, int nsub, P
   if (!(b->alpha > 0.0) || !std::isfinite(b->alpha)) return MEMFINE_ERR_INVALID_ARG;
   if (b->m_g < 1 || b->tp < 1 || b->cp < 1 || b->micro_batch < 1) return MEMFINE_ERR_INVALID_ARG;
   if (b->rule != MEMFINE_RULE_EQ9 && b->rule != MEMFINE_RULE_EXACT) return MEMFINE_ERR_INVALID_ARG;
+  if (b->model != MEMFINE_MODEL_PAPER && b->model != MEMFINE_MODEL_IMPL) return MEMFINE_ERR_INVALID_ARG;
   long double B = (long double)b->alpha * (long double)b->gpu_capacity_bytes;
   if (B >= 18446744073709551615.0L) B = 18446744073709551615.0L;
   p->budget = (uint64_t)floorl(B);
@@ -707,12 +708,27 @@ memfine_status memfine_route_counts(memfine_handle_t h, const int32_t* ids_dev, 
   return MEMFINE_OK;
 }
 
+memfine_status plan_host(const int32_t* counts, int32_t nsub, const memfine_dims* dims, const memfine_budget* budget,
+                         memfine_plan_info* info);
+memfine_status plan_impl(const int32_t* counts_host, int32_t nsub, const memfine_dims* dims,
+                         const memfine_budget* budget, memfine_plan_info* info);
+
 memfine_status memfine_plan(const int32_t* counts, int32_t nsub, const memfine_dims* dims, const memfine_budget* budget,
                             memfine_plan_info* info) {
   if (!counts || !info) return MEMFINE_ERR_INVALID_ARG;
   PlanParams p;
   if (int rc = budget_to_params(dims, budget, nsub, &p)) return (memfine_status)rc;
   memset(info, 0, sizeof *info);
+  if (budget->model == MEMFINE_MODEL_IMPL) {
+    if (is_device_ptr(counts)) {
+      std::vector<int32_t> hc((size_t)p.EP * nsub * p.E);
+      cudaDeviceSynchronize();
+      if (cudaMemcpy(hc.data(), counts, hc.size() * sizeof(int32_t), cudaMemcpyDeviceToHost) != cudaSuccess)
+        return MEMFINE_ERR_CUDA;
+      return plan_impl(hc.data(), nsub, dims, budget, info);
+    }
+    return plan_impl(counts, nsub, dims, budget, info);
+  }
   if (is_device_ptr(counts)) {
     // A3 on the device: the single-CTA tuner kernel reads the (all-gathered) counts in HBM.
     memfine_plan_info* out_h = nullptr;
@@ -737,6 +753,13 @@ memfine_status memfine_plan(const int32_t* counts, int32_t nsub, const memfine_d
     if (e != cudaSuccess) return MEMFINE_ERR_CUDA;
     return (memfine_status)rc;
   }
+  return plan_host(counts, nsub, dims, budget, info);
+}
+
+memfine_status plan_host(const int32_t* counts, int32_t nsub, const memfine_dims* dims, const memfine_budget* budget,
+                         memfine_plan_info* info) {
+  PlanParams p;
+  if (int rc = budget_to_params(dims, budget, nsub, &p)) return (memfine_status)rc;
   // Host counts: same evaluation on the CPU.
   std::vector<int64_t> sub((size_t)p.EP * nsub, 0);
   int El = p.E / p.EP;
@@ -744,6 +767,67 @@ memfine_status memfine_plan(const int32_t* counts, int32_t nsub, const memfine_d
     for (int j = 0; j < nsub; j++)
       for (int e = 0; e < p.E; e++) sub[(size_t)(e / El) * nsub + j] += counts[((int64_t)src * nsub + j) * p.E + e];
   return (memfine_status)plan_from_subsums(sub.data(), p, info);
+}
+
+// MEMFINE_MODEL_IMPL: smallest bin whose exact workspace high-water fits the budget (host).
+memfine_status plan_impl(const int32_t* counts_host, int32_t nsub, const memfine_dims* dims,
+                         const memfine_budget* budget, memfine_plan_info* info) {
+  memfine_budget paper = *budget;
+  paper.model = MEMFINE_MODEL_PAPER;
+  paper.rule = MEMFINE_RULE_EQ9;
+  memfine_status st = plan_host(counts_host, nsub, dims, &paper, info);
+  if (st != MEMFINE_OK && st != MEMFINE_ERR_INFEASIBLE) return st;
+  static const int32_t kDefaultBins[4] = {1, 2, 4, 8};
+  const int32_t* bins = budget->bins ? budget->bins : kDefaultBins;
+  int nb = budget->bins ? budget->nbins : 4;
+  for (int i = 0; i < nb; i++)
+    if (nsub % bins[i]) return MEMFINE_ERR_INVALID_ARG;
+  long double Bl = (long double)budget->alpha * (long double)budget->gpu_capacity_bytes;
+  uint64_t B = Bl >= 18446744073709551615.0L ? ~0ull : (uint64_t)floorl(Bl);
+  uint64_t used = budget->static_bytes + budget->other_act_bytes;
+  if (B <= used) return MEMFINE_ERR_INFEASIBLE;
+  uint64_t room = B - used;
+  auto ws_of = [&](int Cb) {
+    uint64_t mx = 0;
+    memfine_dims d = *dims;
+    for (int r = 0; r < dims->ep_size; r++) {
+      d.ep_rank = r;
+      uint64_t w = 0;
+      memfine_workspace_bytes(counts_host, nsub, &d, Cb, MEMFINE_BWD, &w);
+      mx = std::max(mx, w);
+    }
+    return mx;
+  };
+  int C = -1;
+  uint64_t wsC = 0;
+  for (int i = 0; i < nb && C < 0; i++) {
+    uint64_t w = ws_of(bins[i]);
+    if (w <= room) { C = bins[i]; wsC = w; }
+  }
+  info->clamped = 0;
+  info->feasible = 1;
+  if (C < 0) {
+    C = bins[nb - 1];
+    wsC = ws_of(C);
+    info->clamped = 1;
+    info->feasible = 0;
+  }
+  info->C = C;
+  info->exact_peak = 1;
+  info->predicted_peak_bytes = wsC;
+  // s_chunk_max for the chosen C (paper quantity, exact because C | nsub)
+  int El = dims->num_experts / dims->ep_size, per = nsub / C, E = dims->num_experts;
+  int64_t mx = 0;
+  for (int r = 0; r < dims->ep_size; r++)
+    for (int jc = 0; jc < C; jc++) {
+      int64_t sum = 0;
+      for (int src = 0; src < dims->ep_size; src++)
+        for (int j = jc * per; j < (jc + 1) * per; j++)
+          for (int e = r * El; e < (r + 1) * El; e++) sum += counts_host[((int64_t)src * nsub + j) * E + e];
+      mx = std::max(mx, sum);
+    }
+  info->s_chunk_max = mx;
+  return MEMFINE_OK;
 }
 
 memfine_status memfine_workspace_bytes(const int32_t* counts_host, int32_t nsub, const memfine_dims* dims, int32_t C,

@@ -76,10 +76,25 @@ def make_expert(e: int, h: int, g: int, seed: int = 7000, dtype=torch.bfloat16):
 
 
 def make_experts(experts, h: int, g: int, seed: int = 7000, dtype=torch.bfloat16):
-    """Stacked weights for the listed global experts: [n,g,h], [n,g,h], [n,h,g]."""
-    ws = [make_expert(int(e), h, g, seed, dtype) for e in experts]
-    return (torch.stack([w[0] for w in ws]), torch.stack([w[1] for w in ws]),
-            torch.stack([w[2] for w in ws]))
+    """Stacked weights for the listed global experts: [n,g,h], [n,g,h], [n,h,g].
+    Experts are drawn in parallel threads (each from its own seeded generator, so the
+    values do not depend on the thread count)."""
+    from concurrent.futures import ThreadPoolExecutor
+    experts = [int(e) for e in experts]
+    n = len(experts)
+    wg = torch.empty((n, g, h), dtype=dtype)
+    wu = torch.empty((n, g, h), dtype=dtype)
+    wd = torch.empty((n, h, g), dtype=dtype)
+
+    def one(i):
+        a, b, c = make_expert(experts[i], h, g, seed, dtype)
+        wg[i].copy_(a)
+        wu[i].copy_(b)
+        wd[i].copy_(c)
+
+    with ThreadPoolExecutor(max_workers=min(16, max(1, n))) as ex:
+        list(ex.map(one, range(n)))
+    return wg, wu, wd
 
 
 def popularity_rank(E: int, placement: str, seed: int = 4242) -> np.ndarray:

@@ -124,3 +124,27 @@ def test_workspace_bytes_formula_and_scaling():
         assert 0 < meta < 2 * 1024 * 1024
     wsb = {C_: layer.workspace_bytes(ct, d, C_, capi.BWD) for C_ in (1, 8)}
     assert wsb[1] > ws[1] and wsb[8] < wsb[1] / 4
+
+
+def test_impl_model_picks_smallest_fitting_bin():
+    """MEMFINE_MODEL_IMPL: C = smallest bin whose exact backward workspace (max over EP ranks)
+    fits B - static - other; checked against memfine_workspace_bytes directly."""
+    rng = np.random.default_rng(5)
+    T, h, g, E, k, EP = 2048, 256, 512, 16, 4, 4
+    ids = [np.stack([rng.permutation(E)[:k] for _ in range(T)]).astype(np.int32) for _ in range(EP)]
+    od = oracle.Dims(T=T, h=h, g=g, E=E, k=k)
+    counts = torch.from_numpy(np.stack([oracle.route_counts(od, i, 8)[0] for i in ids]).astype(np.int32))
+    dims0 = layer.make_dims(T, h, g, E, k, ep_size=EP, ep_rank=0)
+    ws = {}
+    for C_ in (1, 2, 4, 8):
+        ws[C_] = max(layer.workspace_bytes(counts, layer.make_dims(T, h, g, E, k, ep_size=EP, ep_rank=r), C_,
+                                           capi.BWD) for r in range(EP))
+    assert ws[1] > ws[2] > ws[4] > ws[8]
+    static = 10**6
+    for C_ in (1, 2, 4, 8):
+        b = capi.make_budget(static + ws[C_], 1.0, static, 0, model=capi.MODEL_IMPL)
+        p = layer.plan(counts, dims0, b)
+        assert p["status"] == 0 and p["C"] == C_ and p["feasible"] and p["predicted_peak_bytes"] == ws[C_]
+        b = capi.make_budget(static + ws[C_] - 1, 1.0, static, 0, model=capi.MODEL_IMPL)
+        p = layer.plan(counts, dims0, b)
+        assert p["C"] == (C_ * 2 if C_ < 8 else 8) and (p["clamped"] == (C_ == 8))

@@ -1,0 +1,119 @@
+"""BASELINE.json configs 3-5 at full size on one GPU (run with -m gpu; slow).
+
+Y / dX / d_score on sampled tokens vs the oracle, integer outputs in full, and the
+memory-budget sweep with every budget enforced physically (a ballast allocation leaves only
+the budget), so a tuner that under-chunks runs out of memory."""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+from paper_2511_21431_b200 import capi, layer
+from tests.harness import GpuRun, make_problem, oracle_dims, oracle_tokens, rel_err
+
+pytestmark = [pytest.mark.gpu, pytest.mark.slow]
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _need_gpu():
+    if not torch.cuda.is_available():
+        pytest.skip("needs a CUDA device")
+
+
+def _sampled_parity(p, run, C, ntok=6, seed=0):
+    y, st, fstats, wsb = run.fwd(C)
+    assert st == 0, capi.status_str(st)
+    assert fstats["workspace_used_bytes"] == wsb
+    (dx, dwg, dwu, dwd, ds), st, bstats, wsbb = run.bwd(C)
+    assert st == 0, capi.status_str(st)
+    assert bstats["workspace_used_bytes"] == wsbb
+    toks = np.random.default_rng(seed).choice(p.T, ntok, replace=False)
+    ry, rdx, rds = oracle_tokens(p, toks)
+    errs = {"y": rel_err(y.float().cpu().numpy()[toks], ry), "dx": rel_err(dx.float().cpu().numpy()[toks], rdx),
+            "dscore": rel_err(ds.cpu().numpy()[toks], rds)}
+    assert all(v <= 2e-2 for v in errs.values()), errs
+    for t in (dwg, dwu, dwd):
+        assert torch.isfinite(t).all()
+    return fstats, bstats
+
+
+def test_dsv3_layer_full_size():
+    """Config 3: 256 experts, top-8, h=7168, FFN=2048, 8K tokens, Zipf(1.2) routing, C=2."""
+    p = make_problem(8192, 7168, 2048, 256, 8, zipf_s=1.2, seed=11)
+    run = GpuRun(p)
+    c = run.counts(8).cpu().numpy()[0]
+    ref, bad = oracle.route_counts(oracle_dims(p), p.ids.numpy(), 8)
+    assert bad == 0
+    np.testing.assert_array_equal(c, ref)
+    _sampled_parity(p, run, 2)
+
+
+def test_qwen3_layer_extreme_imbalance():
+    """Config 4: 64 experts, top-6, h=4096, FFN=1536, 16K tokens, Zipf(1.2) with the hot
+    experts contiguous; the hottest expert receives > 8x the mean; C=4."""
+    p = make_problem(16384, 4096, 1536, 64, 6, zipf_s=1.2, placement="contiguous", seed=12)
+    per_expert = np.bincount(p.ids.numpy().ravel(), minlength=64)
+    assert per_expert.max() > 8 * per_expert.mean()
+    run = GpuRun(p)
+    c = run.counts(8)
+    # at EP=8 the contiguous placement puts the hot experts on rank 0: the tuner's s''_max
+    d8 = layer.make_dims(16384, 4096, 1536, 64, 6, ep_size=8)
+    c8 = torch.zeros((8, 8, 64), dtype=torch.int32)
+    c8[0] = c[0].cpu()
+    info = layer.plan(c8, d8, capi.make_budget(180 * 10**9, 0.9))
+    assert info["status"] == 0 and info["hot_rank"] == 0
+    _sampled_parity(p, run, 4)
+
+
+def test_memory_budget_sweep_physical():
+    """Config 5: the DeepSeek-V3-style layer's per-rank load at EP=8 (32 local experts, 8K tokens
+    x top-8 = 65536 copies, ~2048 rows per expert) under activation budgets from 180 GB down to
+    where C steps.  At every budget: device tuner == host planner (== oracle for the paper model),
+    and the run at the chosen C fits under a ballast allocation that leaves only the budget."""
+    T, h, g, E, k = 8192, 7168, 2048, 32, 8
+    p = make_problem(T, h, g, E, k, zipf_s=1.2, seed=13)
+    run = GpuRun(p)
+    counts_d = run.counts(8)
+    counts_h = counts_d.cpu()
+    dims = run.mf.dims
+    f32 = dict(dtype=torch.float32, device=run.dev)
+    grads = (torch.empty(run.wg.shape, **f32), torch.empty(run.wu.shape, **f32), torch.empty(run.wd.shape, **f32))
+    torch.cuda.synchronize()
+    static = sum(t.numel() * t.element_size() for t in (run.x, run.dy, run.ids, run.w, run.wg, run.wu, run.wd)
+                 + grads) + 3 * run.x.numel() * 2
+    ws = {C_: layer.workspace_bytes(counts_h, dims, C_, capi.BWD) for C_ in (1, 2, 4, 8)}
+    assert ws[1] > ws[2] > ws[4] > ws[8]
+    budgets = [180e9, 100e9, 40e9] + [static + ws[C_] + (1 << 20) for C_ in (1, 2, 4, 8)]
+    od = oracle_dims(p)
+    seen = set()
+    for B in budgets:
+        B = int(B)
+        bp = capi.make_budget(B, 1.0, static, 0)
+        pd, ph = layer.plan(counts_d, dims, bp), layer.plan(counts_h, dims, bp)
+        assert pd == ph
+        st, ro = oracle.plan(counts_h.numpy().astype(np.int64), od, budget_bytes=B, static_bytes=static)
+        assert st == pd["status"] and (st != 0 or ro["C"] == pd["C"])
+        bi = capi.make_budget(B, 1.0, static, 0, model=capi.MODEL_IMPL)
+        pi = layer.plan(counts_d, dims, bi)
+        assert pi["status"] == 0 and pi["feasible"], pi
+        C_ = pi["C"]
+        assert ws[C_] <= B - static
+        # enforce the budget physically: leave only B - (bytes in use) free
+        torch.cuda.synchronize()
+        free, total = torch.cuda.mem_get_info()
+        in_use = total - free
+        ballast_bytes = max(0, free - max(0, B - in_use) - (64 << 20))
+        ballast = torch.empty(ballast_bytes, dtype=torch.uint8, device=run.dev) if ballast_bytes else None
+        try:
+            (dx, *_), st, bstats, _ = run.bwd(C_, ws_bytes=ws[C_], grads=grads)
+            assert st == 0
+            assert bstats["workspace_used_bytes"] <= ws[C_]
+            if C_ not in seen:
+                seen.add(C_)
+                toks = np.random.default_rng(C_).choice(T, 3, replace=False)
+                _, rdx, _ = oracle_tokens(p, toks)
+                assert rel_err(dx.float().cpu().numpy()[toks], rdx) <= 2e-2
+        finally:
+            del ballast
+            torch.cuda.empty_cache()
+    assert {1, 2, 4, 8} <= seen
