@@ -111,25 +111,59 @@ __device__ __forceinline__ uint32_t pack_bf16(float a, float b) {
   __nv_bfloat162 v = __floats2bfloat162_rn(a, b);
   return *reinterpret_cast<uint32_t*>(&v);
 }
-__device__ __forceinline__ void store32_bf16(__nv_bfloat16* dst, const float* v) {
-  uint4* d = reinterpret_cast<uint4*>(dst);
-#pragma unroll
-  for (int i = 0; i < 4; i++)
-    d[i] = make_uint4(pack_bf16(v[8 * i], v[8 * i + 1]), pack_bf16(v[8 * i + 2], v[8 * i + 3]),
-                      pack_bf16(v[8 * i + 4], v[8 * i + 5]), pack_bf16(v[8 * i + 6], v[8 * i + 7]));
+// 32-byte global accesses (LDG/STG.E.ENL2.256 on sm_100): one thread moves half a 64-B row
+// chunk per instruction, halving the L1 wavefronts of the row-per-thread epilogue.
+__device__ __forceinline__ void st256(void* p, const uint32_t (&v)[8]) {
+  asm volatile("st.global.v8.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};" ::"l"(p), "r"(v[0]), "r"(v[1]), "r"(v[2]),
+               "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7])
+               : "memory");
 }
-__device__ __forceinline__ void load32_bf16(const __nv_bfloat16* src, float* v) {
-  const uint4* s = reinterpret_cast<const uint4*>(src);
+__device__ __forceinline__ void ld256(const void* p, uint32_t (&v)[8]) {
+  asm volatile("ld.global.v8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+               : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7])
+               : "l"(p));
+}
+__device__ __forceinline__ void store32_bf16(__nv_bfloat16* dst, const float* v) {
+#pragma unroll
+  for (int i = 0; i < 2; i++) {
+    uint32_t u[8];
+#pragma unroll
+    for (int j = 0; j < 8; j++) u[j] = pack_bf16(v[16 * i + 2 * j], v[16 * i + 2 * j + 1]);
+    st256(dst + 16 * i, u);
+  }
+}
+// raw bf16 pairs of a 32-element row chunk (two 32-byte loads)
+__device__ __forceinline__ void load32_raw(const __nv_bfloat16* src, uint32_t (&u)[16]) {
+  uint32_t a[8], b[8];
+  ld256(src, a);
+  ld256(src + 16, b);
+#pragma unroll
+  for (int j = 0; j < 8; j++) { u[j] = a[j]; u[8 + j] = b[j]; }
+}
+__device__ __forceinline__ void unpack32(const uint32_t (&u)[16], float* v) {
+#pragma unroll
+  for (int j = 0; j < 16; j++) {
+    v[2 * j] = __uint_as_float(u[j] << 16);
+    v[2 * j + 1] = __uint_as_float(u[j] & 0xFFFF0000u);
+  }
+}
+__device__ __forceinline__ void store32_f32(float* dst, const float* v) {
 #pragma unroll
   for (int i = 0; i < 4; i++) {
-    uint4 u = s[i];
-    const __nv_bfloat162* b = reinterpret_cast<const __nv_bfloat162*>(&u);
+    uint32_t u[8];
 #pragma unroll
-    for (int j = 0; j < 4; j++) {
-      float2 f = __bfloat1622float2(b[j]);
-      v[8 * i + 2 * j] = f.x;
-      v[8 * i + 2 * j + 1] = f.y;
-    }
+    for (int j = 0; j < 8; j++) u[j] = __float_as_uint(v[8 * i + j]);
+    st256(dst + 8 * i, u);
+  }
+}
+__device__ __forceinline__ void add32_f32(float* dst, const float* v) {
+#pragma unroll
+  for (int i = 0; i < 4; i++) {
+    uint32_t u[8];
+    ld256(dst + 8 * i, u);
+#pragma unroll
+    for (int j = 0; j < 8; j++) u[j] = __float_as_uint(__uint_as_float(u[j]) + v[8 * i + j]);
+    st256(dst + 8 * i, u);
   }
 }
 
@@ -458,7 +492,15 @@ __global__ void __launch_bounds__(THREADS, 1)
       const int64_t row = rowi;
       float dwp = 0.f;
       float wrow = 0.f;
-      if (KIND == GK_DACT && row_ok) wrow = p.w_row[row];
+      uint32_t gpre[16], upre[16];
+      if (KIND == GK_DACT && row_ok) {
+        wrow = p.w_row[row];
+        const int n0c = T.n0 + half * CPW;
+        if (n0c < p.g) {
+          load32_raw(p.GU + row * 2 * p.g + n0c, gpre);
+          load32_raw(p.GU + row * 2 * p.g + p.g + n0c, upre);
+        }
+      }
 #pragma unroll 1
       for (int c = half * CPW; c < (half + 1) * CPW; c += 32) {
         const int n = T.n0 + c;
@@ -489,22 +531,42 @@ __global__ void __launch_bounds__(THREADS, 1)
           if (row_ok && n < p.h) store32_bf16(p.O + row * p.h + n, v);
         } else if (KIND == GK_DACT) {
           if (row_ok && n < p.g) {
-            float G[32], U[32], dG[32], dU[32], aw[32];
-            load32_bf16(p.GU + row * 2 * p.g + n, G);
-            load32_bf16(p.GU + row * 2 * p.g + p.g + n, U);
+            uint32_t gcur[16], ucur[16];
 #pragma unroll
-            for (int i = 0; i < 32; i++) {
-              float sg = sigmoid_f(G[i]);
-              float a = G[i] * sg * U[i];
-              dwp = fmaf(v[i], a, dwp);
-              float dA = wrow * v[i];
-              dG[i] = dA * U[i] * sg * (1.f + G[i] * (1.f - sg));
-              dU[i] = dA * G[i] * sg;
-              aw[i] = wrow * a;
+            for (int j = 0; j < 16; j++) { gcur[j] = gpre[j]; ucur[j] = upre[j]; }
+            // prefetch the next chunk's G||U while this one computes
+            if (c + 32 < (half + 1) * CPW && n + 32 < p.g) {
+              load32_raw(p.GU + row * 2 * p.g + n + 32, gpre);
+              load32_raw(p.GU + row * 2 * p.g + p.g + n + 32, upre);
             }
-            store32_bf16(p.GU + row * 2 * p.g + n, dG);
-            store32_bf16(p.GU + row * 2 * p.g + p.g + n, dU);
-            store32_bf16(p.A + row * p.g + n, aw);
+#pragma unroll
+            for (int hh = 0; hh < 2; hh++) {
+              uint32_t og[8], ou[8], oa[8];
+#pragma unroll
+              for (int j = 0; j < 8; j++) {
+                float r2[2][3];
+#pragma unroll
+                for (int q2 = 0; q2 < 2; q2++) {
+                  const int i = 16 * hh + 2 * j + q2;
+                  const uint32_t gw = gcur[8 * hh + j], uw = ucur[8 * hh + j];
+                  const float G = __uint_as_float(q2 ? (gw & 0xFFFF0000u) : (gw << 16));
+                  const float U = __uint_as_float(q2 ? (uw & 0xFFFF0000u) : (uw << 16));
+                  const float sg = sigmoid_f(G);
+                  const float a = G * sg * U;
+                  dwp = fmaf(v[i], a, dwp);
+                  const float dA = wrow * v[i];
+                  r2[q2][0] = dA * U * sg * (1.f + G * (1.f - sg));
+                  r2[q2][1] = dA * G * sg;
+                  r2[q2][2] = wrow * a;
+                }
+                og[j] = pack_bf16(r2[0][0], r2[1][0]);
+                ou[j] = pack_bf16(r2[0][1], r2[1][1]);
+                oa[j] = pack_bf16(r2[0][2], r2[1][2]);
+              }
+              st256(p.GU + row * 2 * p.g + n + 16 * hh, og);
+              st256(p.GU + row * 2 * p.g + p.g + n + 16 * hh, ou);
+              st256(p.A + row * p.g + n + 16 * hh, oa);
+            }
           }
         } else {
           // WGRAD: fp32 dW tile, overwrite (first chunk) or read-modify-write (later chunks)
@@ -514,21 +576,8 @@ __global__ void __launch_bounds__(THREADS, 1)
             if (KIND == GK_WGRAD_DOWN) dst = p.dW0 + ((int64_t)T.e * p.h + m) * p.g + n;
             else dst = (m < p.g) ? p.dW0 + ((int64_t)T.e * p.g + m) * p.h + n
                                  : p.dW1 + ((int64_t)T.e * p.g + (m - p.g)) * p.h + n;
-            float4* d4 = reinterpret_cast<float4*>(dst);
-            if (p.beta) {
-#pragma unroll
-              for (int i = 0; i < 8; i++) {
-                float4 o = d4[i];
-                o.x += v[4 * i];
-                o.y += v[4 * i + 1];
-                o.z += v[4 * i + 2];
-                o.w += v[4 * i + 3];
-                d4[i] = o;
-              }
-            } else {
-#pragma unroll
-              for (int i = 0; i < 8; i++) d4[i] = make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
-            }
+            if (p.beta) add32_f32(dst, v);
+            else store32_f32(dst, v);
           }
         }
       }
