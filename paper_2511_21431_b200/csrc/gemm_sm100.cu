@@ -19,6 +19,7 @@
 #include <mutex>
 #include <cstdlib>
 #include <algorithm>
+#include <cstring>
 #include "kernels.h"
 
 namespace memfine {
@@ -167,6 +168,57 @@ __device__ __forceinline__ void add32_f32(float* dst, const float* v) {
   }
 }
 
+// TMA stores from shared memory (bulk async groups).  reduce = 1: element-wise add into global.
+__device__ __forceinline__ void tma_store_2d(const CUtensorMap* m, const void* src, int c0, int c1) {
+  asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];" ::"l"(m),
+               "r"(su32(src)), "r"(c0), "r"(c1)
+               : "memory");
+}
+__device__ __forceinline__ void tma_store_3d(const CUtensorMap* m, const void* src, int c0, int c1, int c2,
+                                             bool reduce) {
+  if (reduce)
+    asm volatile("cp.reduce.async.bulk.tensor.3d.global.shared::cta.add.tile.bulk_group [%0, {%2, %3, %4}], [%1];" ::
+                     "l"(m),
+                 "r"(su32(src)), "r"(c0), "r"(c1), "r"(c2)
+                 : "memory");
+  else
+    asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%2, %3, %4}], [%1];" ::"l"(m),
+                 "r"(su32(src)), "r"(c0), "r"(c1), "r"(c2)
+                 : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void bulk_wait_read() { asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory"); }
+__device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+__device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+
+// Staging writes in the TMA swizzle layouts.  bf16: 32 rows x 64 B, SWIZZLE_64B (16-B chunk c of
+// row r at chunk c ^ ((r >> 1) & 3)); fp32: 32 rows x 128 B, SWIZZLE_128B (chunk c ^ (r & 7)).
+// Both are bank-conflict-free for the row-per-thread writes of the 32x32b TMEM layout.
+__device__ __forceinline__ void stage_bf16_row(uint8_t* buf, int r, const float* v) {
+  uint8_t* row = buf + r * 64;
+#pragma unroll
+  for (int c = 0; c < 4; c++) {
+    uint4 u = make_uint4(pack_bf16(v[8 * c], v[8 * c + 1]), pack_bf16(v[8 * c + 2], v[8 * c + 3]),
+                         pack_bf16(v[8 * c + 4], v[8 * c + 5]), pack_bf16(v[8 * c + 6], v[8 * c + 7]));
+    *reinterpret_cast<uint4*>(row + ((c ^ ((r >> 1) & 3)) << 4)) = u;
+  }
+}
+__device__ __forceinline__ void stage_bf16_row_packed(uint8_t* buf, int r, const uint32_t (&u)[16]) {
+  uint8_t* row = buf + r * 64;
+#pragma unroll
+  for (int c = 0; c < 4; c++)
+    *reinterpret_cast<uint4*>(row + ((c ^ ((r >> 1) & 3)) << 4)) =
+        make_uint4(u[4 * c], u[4 * c + 1], u[4 * c + 2], u[4 * c + 3]);
+}
+__device__ __forceinline__ void stage_f32_row(uint8_t* buf, int r, const float* v) {
+  uint8_t* row = buf + r * 128;
+#pragma unroll
+  for (int c = 0; c < 8; c++)
+    *reinterpret_cast<float4*>(row + ((c ^ (r & 7)) << 4)) =
+        make_float4(v[4 * c], v[4 * c + 1], v[4 * c + 2], v[4 * c + 3]);
+}
+
 // ------------------------------------------------------------------ per-kind configuration
 template <int KIND>
 struct Cfg;
@@ -182,6 +234,17 @@ template <> struct Cfg<GK_DX> { static constexpr int BN = 256, NACC = 1, A_MN = 
 // B5: dW[e] += rows^T rows  (A(m,k) = rows[s0+k][m], B(n,k) = rows[s0+k][n]; both MN-major).
 template <> struct Cfg<GK_WGRAD_DOWN> { static constexpr int BN = 256, NACC = 1, A_MN = 1, B_MN = 1; };
 template <> struct Cfg<GK_WGRAD_GU> { static constexpr int BN = 256, NACC = 1, A_MN = 1, B_MN = 1; };
+
+// Epilogue staging per epilogue warp and chunk of 32 columns: output slots x slot bytes,
+// double-buffered across chunks.
+template <int KIND>
+struct Epi {
+  static constexpr int SLOTS = KIND == GK_DACT ? 3 : (KIND == GK_GATEUP ? 2 : 1);
+  static constexpr int SLOT_BYTES = KIND >= GK_WGRAD_DOWN ? 4096 : 2048;
+  static constexpr int CHUNK_BYTES = SLOTS * SLOT_BYTES;
+  static constexpr int WARP_BYTES = 2 * CHUNK_BYTES;
+  static constexpr int TOTAL = EPI_WARPS * WARP_BYTES;
+};
 
 struct Params {
   int El, h, g;
@@ -307,6 +370,22 @@ __device__ __forceinline__ Tile tile_of(const Params& p, int t) {
   return T;
 }
 
+template <int KIND, bool PAIR>
+__host__ __device__ constexpr int stage_bytes() {
+  return A_BYTES + (PAIR ? Cfg<KIND>::NACC * Cfg<KIND>::BN / 2 : Cfg<KIND>::NACC * Cfg<KIND>::BN) * BK * 2;
+}
+// as many 1024-aligned stages as fit next to the epilogue staging (227 KB per CTA)
+template <int KIND, bool PAIR>
+__host__ __device__ constexpr int nstage() {
+  return (232448 - 1024 - 256 - Epi<KIND>::TOTAL) / stage_bytes<KIND, PAIR>() > 6
+             ? 6
+             : (232448 - 1024 - 256 - Epi<KIND>::TOTAL) / stage_bytes<KIND, PAIR>();
+}
+template <int KIND, bool PAIR>
+__host__ __device__ constexpr int smem_bytes() {
+  return nstage<KIND, PAIR>() * stage_bytes<KIND, PAIR>() + Epi<KIND>::TOTAL + 1024 + 256;
+}
+
 // ------------------------------------------------------------------ the kernel
 // PAIR = false: one CTA per 128-row tile, tcgen05.mma.cta_group::1 (M=128).
 // PAIR = true : a 2-CTA cluster per 256-row tile, tcgen05.mma.cta_group::2 (M=256) issued by the
@@ -315,7 +394,8 @@ __device__ __forceinline__ Tile tile_of(const Params& p, int t) {
 template <int KIND, bool PAIR>
 __global__ void __launch_bounds__(THREADS, 1)
     gemm_kernel(const __grid_constant__ Params p, const __grid_constant__ CUtensorMap tmA,
-                const __grid_constant__ CUtensorMap tmB0, const __grid_constant__ CUtensorMap tmB1) {
+                const __grid_constant__ CUtensorMap tmB0, const __grid_constant__ CUtensorMap tmB1,
+                const __grid_constant__ CUtensorMap tmO0, const __grid_constant__ CUtensorMap tmO1) {
   using CF = Cfg<KIND>;
   constexpr int BN = CF::BN, NACC = CF::NACC;
   constexpr int MMA_N = NACC * BN;                      // GATEUP: G||U in one MMA (N = 256)
@@ -323,7 +403,7 @@ __global__ void __launch_bounds__(THREADS, 1)
   constexpr int B_ROWS = PAIR ? MMA_N / 2 : MMA_N;      // B rows (N) staged per CTA
   constexpr int B_BYTES = B_ROWS * BK * 2;
   constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
-  constexpr int NSTAGE = PAIR ? 6 : 4;
+  constexpr int NSTAGE = nstage<KIND, PAIR>();
   constexpr int ACC_COLS = MMA_N;                       // per accumulator stage
   constexpr uint32_t TMEM_COLS = 2 * ACC_COLS;          // double-buffered
   static_assert(TMEM_COLS <= 512, "TMEM");
@@ -331,7 +411,8 @@ __global__ void __launch_bounds__(THREADS, 1)
 
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
-  uint64_t* full = (uint64_t*)(smem + NSTAGE * STAGE_BYTES);
+  uint8_t* epi_smem = smem + NSTAGE * STAGE_BYTES;      // 1024-aligned (STAGE_BYTES is)
+  uint64_t* full = (uint64_t*)(epi_smem + Epi<KIND>::TOTAL);
   uint64_t* empty = full + NSTAGE;
   uint64_t* tfull = empty + NSTAGE;
   uint64_t* tempty = tfull + 2;
@@ -346,6 +427,8 @@ __global__ void __launch_bounds__(THREADS, 1)
     prefetch_tmap(&tmA);
     prefetch_tmap(&tmB0);
     if (KIND == GK_GATEUP || KIND == GK_DX) prefetch_tmap(&tmB1);
+    prefetch_tmap(&tmO0);
+    if (KIND == GK_GATEUP || KIND == GK_DACT || KIND == GK_WGRAD_GU) prefetch_tmap(&tmO1);
     for (int s = 0; s < NSTAGE; s++) { mbar_init(full + s, 1); mbar_init(empty + s, 1); }
     for (int a = 0; a < 2; a++) { mbar_init(tfull + a, 1); mbar_init(tempty + a, (PAIR ? 2 : 1) * EPI_WARPS); }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -459,27 +542,49 @@ __global__ void __launch_bounds__(THREADS, 1)
     }
   } else {
     // ================================================================ epilogue (warps 2..9, both CTAs)
+    // TMEM -> registers (tcgen05.ld 32x32b: lane = row) -> fused MoE math -> swizzled smem
+    // staging -> TMA store (or TMA reduce-add for accumulated dW), one bulk group per chunk,
+    // double-buffered per warp.
     const int q = warp & 3;               // TMEM lane quarter this warp may access
     const int half = (warp - 2) >> 2;     // which half of the tile's columns
+    const int ew = warp - 2;              // epilogue warp index 0..7
     const int rloc = q * 32 + lane;       // row within this CTA's 128 rows
     constexpr int CPW = BN / 2;           // columns per epilogue warp
+    using EP = Epi<KIND>;
+    uint8_t* wbuf = epi_smem + ew * EP::WARP_BYTES;
+    int sbuf = 0;
     int it = 0;
+    auto next_buf = [&]() -> uint8_t* {
+      // the group that last used this buffer (two chunks ago) must have finished reading it
+      if (lane == 0) bulk_wait_read<1>();
+      __syncwarp();
+      uint8_t* b = wbuf + sbuf * EP::CHUNK_BYTES;
+      sbuf ^= 1;
+      return b;
+    };
     for (int t = cid; t < ntiles; t += ncid) {
       Tile T = tile_of<KIND, PAIR>(p, t);
-      const int rowi = T.m0 + (int)rank * BM + rloc;
-      const bool row_ok = rowi < T.m_end;
+      const int row0 = T.m0 + (int)rank * BM + q * 32;     // first row of this warp's 32 rows
+      const int rowi = row0 + lane;
+      const bool rows_ok = row0 < T.m_end;                 // warp-uniform (halves are 128-row aligned)
       if (T.nkb == 0) {
-        if (KIND >= GK_WGRAD_DOWN && !p.beta && row_ok) {
+        if (KIND >= GK_WGRAD_DOWN && !p.beta && rows_ok) {
           // an expert without rows in the first chunk: its dW tile is zero
-          const int m = rowi;
-          for (int c = half * CPW; c < (half + 1) * CPW; c += 4) {
-            const int n = T.n0 + c;
-            if (n >= p.N) break;
-            float* dst;
-            if (KIND == GK_WGRAD_DOWN) dst = p.dW0 + ((int64_t)T.e * p.h + m) * p.g + n;
-            else dst = (m < p.g) ? p.dW0 + ((int64_t)T.e * p.g + m) * p.h + n
-                                 : p.dW1 + ((int64_t)T.e * p.g + (m - p.g)) * p.h + n;
-            *reinterpret_cast<float4*>(dst) = make_float4(0.f, 0.f, 0.f, 0.f);
+          float z[32];
+#pragma unroll
+          for (int i = 0; i < 32; i++) z[i] = 0.f;
+          for (int c = half * CPW; c < (half + 1) * CPW; c += 32) {
+            uint8_t* buf = next_buf();
+            stage_f32_row(buf, lane, z);
+            fence_async_smem();
+            __syncwarp();
+            if (lane == 0) {
+              const int n = T.n0 + c;
+              if (KIND == GK_WGRAD_DOWN) tma_store_3d(&tmO0, buf, n, row0, T.e, false);
+              else if (row0 < p.g) tma_store_3d(&tmO0, buf, n, row0, T.e, false);
+              else tma_store_3d(&tmO1, buf, n, row0 - p.g, T.e, false);
+              bulk_commit();
+            }
           }
         }
         continue;
@@ -493,7 +598,7 @@ __global__ void __launch_bounds__(THREADS, 1)
       float dwp = 0.f;
       float wrow = 0.f;
       uint32_t gpre[16], upre[16];
-      if (KIND == GK_DACT && row_ok) {
+      if (KIND == GK_DACT && rows_ok) {
         wrow = p.w_row[row];
         const int n0c = T.n0 + half * CPW;
         if (n0c < p.g) {
@@ -512,25 +617,45 @@ __global__ void __launch_bounds__(THREADS, 1)
         if (KIND == GK_GATEUP) {
           uint32_t r2[32];
           tmem_ld32(tb + BN + c, r2);
-          float u[32];
+          if (rows_ok && n < p.g) {
+            uint8_t* buf = next_buf();
+            float u[32];
 #pragma unroll
-          for (int i = 0; i < 32; i++) u[i] = __uint_as_float(r2[i]);
-          if (row_ok && n < p.g) {
+            for (int i = 0; i < 32; i++) u[i] = __uint_as_float(r2[i]);
             if (p.store_gu) {
-              store32_bf16(p.GU + row * 2 * p.g + n, v);
-              store32_bf16(p.GU + row * 2 * p.g + p.g + n, u);
-            }
-            if (p.store_a) {
+              stage_bf16_row(buf, lane, v);
+              stage_bf16_row(buf + 2048, lane, u);
+            } else {
               float a[32];
 #pragma unroll
               for (int i = 0; i < 32; i++) a[i] = silu_f(v[i]) * u[i];
-              store32_bf16(p.A + row * p.g + n, a);
+              stage_bf16_row(buf, lane, a);
+            }
+            fence_async_smem();
+            __syncwarp();
+            if (lane == 0) {
+              if (p.store_gu) {
+                tma_store_2d(&tmO0, buf, n, row0);               // G -> GU[:, n]
+                tma_store_2d(&tmO0, buf + 2048, p.g + n, row0);  // U -> GU[:, g + n]
+              } else {
+                tma_store_2d(&tmO1, buf, n, row0);               // a -> A[:, n]
+              }
+              bulk_commit();
             }
           }
         } else if (KIND == GK_DOWN || KIND == GK_DX) {
-          if (row_ok && n < p.h) store32_bf16(p.O + row * p.h + n, v);
+          if (rows_ok && n < p.h) {
+            uint8_t* buf = next_buf();
+            stage_bf16_row(buf, lane, v);
+            fence_async_smem();
+            __syncwarp();
+            if (lane == 0) {
+              tma_store_2d(&tmO0, buf, n, row0);
+              bulk_commit();
+            }
+          }
         } else if (KIND == GK_DACT) {
-          if (row_ok && n < p.g) {
+          if (rows_ok && n < p.g) {
             uint32_t gcur[16], ucur[16];
 #pragma unroll
             for (int j = 0; j < 16; j++) { gcur[j] = gpre[j]; ucur[j] = upre[j]; }
@@ -539,49 +664,58 @@ __global__ void __launch_bounds__(THREADS, 1)
               load32_raw(p.GU + row * 2 * p.g + n + 32, gpre);
               load32_raw(p.GU + row * 2 * p.g + p.g + n + 32, upre);
             }
+            uint8_t* buf = next_buf();
+            uint32_t og[16], ou[16], oa[16];
 #pragma unroll
-            for (int hh = 0; hh < 2; hh++) {
-              uint32_t og[8], ou[8], oa[8];
+            for (int j = 0; j < 16; j++) {
+              float r2v[2][3];
 #pragma unroll
-              for (int j = 0; j < 8; j++) {
-                float r2[2][3];
-#pragma unroll
-                for (int q2 = 0; q2 < 2; q2++) {
-                  const int i = 16 * hh + 2 * j + q2;
-                  const uint32_t gw = gcur[8 * hh + j], uw = ucur[8 * hh + j];
-                  const float G = __uint_as_float(q2 ? (gw & 0xFFFF0000u) : (gw << 16));
-                  const float U = __uint_as_float(q2 ? (uw & 0xFFFF0000u) : (uw << 16));
-                  const float sg = sigmoid_f(G);
-                  const float a = G * sg * U;
-                  dwp = fmaf(v[i], a, dwp);
-                  const float dA = wrow * v[i];
-                  r2[q2][0] = dA * U * sg * (1.f + G * (1.f - sg));
-                  r2[q2][1] = dA * G * sg;
-                  r2[q2][2] = wrow * a;
-                }
-                og[j] = pack_bf16(r2[0][0], r2[1][0]);
-                ou[j] = pack_bf16(r2[0][1], r2[1][1]);
-                oa[j] = pack_bf16(r2[0][2], r2[1][2]);
+              for (int q2 = 0; q2 < 2; q2++) {
+                const int i = 2 * j + q2;
+                const uint32_t gw = gcur[j], uw = ucur[j];
+                const float G = __uint_as_float(q2 ? (gw & 0xFFFF0000u) : (gw << 16));
+                const float U = __uint_as_float(q2 ? (uw & 0xFFFF0000u) : (uw << 16));
+                const float sg = sigmoid_f(G);
+                const float a = G * sg * U;
+                dwp = fmaf(v[i], a, dwp);
+                const float dA = wrow * v[i];
+                r2v[q2][0] = dA * U * sg * (1.f + G * (1.f - sg));
+                r2v[q2][1] = dA * G * sg;
+                r2v[q2][2] = wrow * a;
               }
-              st256(p.GU + row * 2 * p.g + n + 16 * hh, og);
-              st256(p.GU + row * 2 * p.g + p.g + n + 16 * hh, ou);
-              st256(p.A + row * p.g + n + 16 * hh, oa);
+              og[j] = pack_bf16(r2v[0][0], r2v[1][0]);
+              ou[j] = pack_bf16(r2v[0][1], r2v[1][1]);
+              oa[j] = pack_bf16(r2v[0][2], r2v[1][2]);
+            }
+            stage_bf16_row_packed(buf, lane, og);
+            stage_bf16_row_packed(buf + 2048, lane, ou);
+            stage_bf16_row_packed(buf + 4096, lane, oa);
+            fence_async_smem();
+            __syncwarp();
+            if (lane == 0) {
+              tma_store_2d(&tmO0, buf, n, row0);               // dG over G
+              tma_store_2d(&tmO0, buf + 2048, p.g + n, row0);  // dU over U
+              tma_store_2d(&tmO1, buf + 4096, n, row0);        // a_w
+              bulk_commit();
             }
           }
         } else {
-          // WGRAD: fp32 dW tile, overwrite (first chunk) or read-modify-write (later chunks)
-          const int m = rowi;
-          if (row_ok && n < p.N) {
-            float* dst;
-            if (KIND == GK_WGRAD_DOWN) dst = p.dW0 + ((int64_t)T.e * p.h + m) * p.g + n;
-            else dst = (m < p.g) ? p.dW0 + ((int64_t)T.e * p.g + m) * p.h + n
-                                 : p.dW1 + ((int64_t)T.e * p.g + (m - p.g)) * p.h + n;
-            if (p.beta) add32_f32(dst, v);
-            else store32_f32(dst, v);
+          // WGRAD: fp32 dW tile: TMA store (first chunk) or TMA reduce-add (later chunks)
+          if (rows_ok && n < p.N) {
+            uint8_t* buf = next_buf();
+            stage_f32_row(buf, lane, v);
+            fence_async_smem();
+            __syncwarp();
+            if (lane == 0) {
+              if (KIND == GK_WGRAD_DOWN) tma_store_3d(&tmO0, buf, n, row0, T.e, p.beta != 0);
+              else if (row0 < p.g) tma_store_3d(&tmO0, buf, n, row0, T.e, p.beta != 0);
+              else tma_store_3d(&tmO1, buf, n, row0 - p.g, T.e, p.beta != 0);
+              bulk_commit();
+            }
           }
         }
       }
-      if (KIND == GK_DACT && row_ok) atomicAdd(p.dw_row + row, dwp);
+      if (KIND == GK_DACT && rows_ok) atomicAdd(p.dw_row + row, dwp);
       fence_before();
       __syncwarp();
       if (lane == 0) {
@@ -589,6 +723,8 @@ __global__ void __launch_bounds__(THREADS, 1)
       }
       it++;
     }
+    if (lane == 0) bulk_wait_all();
+    __syncwarp();
   }
   fence_before();
   if (PAIR) cluster_sync(); else __syncthreads();
@@ -632,6 +768,35 @@ bool make_map(CUtensorMap* m, const void* base, int rank, const uint64_t* dims, 
   return r == CUDA_SUCCESS;
 }
 
+bool make_map_t(CUtensorMap* m, CUtensorMapDataType dt, int esize, CUtensorMapSwizzle sw, const void* base, int rank,
+                const uint64_t* dims, const uint32_t* box) {
+  auto fn = encode_fn();
+  if (!fn) return false;
+  cuuint64_t gd[3], gs[2];
+  cuuint32_t bx[3], es[3] = {1, 1, 1};
+  uint64_t stride = esize;
+  for (int i = 0; i < rank; i++) {
+    gd[i] = dims[i];
+    bx[i] = box[i];
+    if (i < rank - 1) { stride *= dims[i]; gs[i] = stride; }
+  }
+  return fn(m, dt, rank, const_cast<void*>(base), gd, gs, bx, es, CU_TENSOR_MAP_INTERLEAVE_NONE, sw,
+            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+// epilogue store maps: bf16 [outer][inner] boxes of 32 x 32 (SWIZZLE_64B); fp32 dW [El][rows][cols]
+// boxes of 32 x 32 x 1 (SWIZZLE_128B); out-of-range rows / columns are clipped by the TMA unit.
+bool map2d_st(CUtensorMap* m, const void* base, uint64_t inner, uint64_t outer) {
+  if (!base) { memset(m, 0, sizeof *m); return true; }
+  uint64_t d[2] = {inner, outer};
+  uint32_t b[2] = {32, 32};
+  return make_map_t(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, CU_TENSOR_MAP_SWIZZLE_64B, base, 2, d, b);
+}
+bool map3d_f32(CUtensorMap* m, const void* base, uint64_t d0, uint64_t d1, uint64_t d2) {
+  uint64_t d[3] = {d0, d1, d2};
+  uint32_t b[3] = {32, 32, 1};
+  return make_map_t(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, CU_TENSOR_MAP_SWIZZLE_128B, base, 3, d, b);
+}
+
 bool map2d(CUtensorMap* m, const void* base, uint64_t inner, uint64_t outer, uint32_t box_in, uint32_t box_out) {
   uint64_t d[2] = {inner, outer}, s[1] = {inner * 2};
   uint32_t b[2] = {box_in, box_out};
@@ -660,8 +825,8 @@ int launch(const GemmProblem<__nv_bfloat16>& gp, cudaStream_t st) {
   constexpr int BN = CF::BN;
   constexpr int MMA_N = CF::NACC * BN;
   constexpr int B_ROWS = PAIR ? MMA_N / 2 : MMA_N;
-  constexpr int NSTAGE = PAIR ? 6 : 4;
-  constexpr int SMEM = NSTAGE * (A_BYTES + B_ROWS * BK * 2) + 1024 + 256;
+  constexpr int SMEM = smem_bytes<KIND, PAIR>();
+  static_assert(SMEM <= 232448, "smem");
   static bool attr_set = false;
   if (!attr_set) {
     if (cudaFuncSetAttribute(gemm_kernel<KIND, PAIR>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM) !=
@@ -692,7 +857,7 @@ int launch(const GemmProblem<__nv_bfloat16>& gp, cudaStream_t st) {
   p.beta = gp.wgrad_beta;
   const uint64_t R = (uint64_t)gp.rows_cap, h = gp.h, g = gp.g, El = gp.El;
   if (R == 0) return 0;
-  CUtensorMap mA, mB0, mB1;
+  CUtensorMap mA, mB0, mB1, mO0, mO1;
   bool ok = true;
   const uint32_t gu_rows = PAIR ? BN : BN;  // per-CTA B box rows for GATEUP (one of W_gate / W_up)
   switch (KIND) {
@@ -701,24 +866,32 @@ int launch(const GemmProblem<__nv_bfloat16>& gp, cudaStream_t st) {
       ok &= map2d(&mA, gp.X, h, R, BK, BM);
       ok &= map3d(&mB0, gp.Wg, h, g, El, BK, gu_rows);
       ok &= map3d(&mB1, gp.Wu, h, g, El, BK, gu_rows);
+      ok &= map2d_st(&mO0, gp.GU ? (const void*)gp.GU : (const void*)gp.A, gp.GU ? 2 * g : g, R);
+      ok &= map2d_st(&mO1, gp.A ? (const void*)gp.A : (const void*)gp.GU, gp.A ? g : 2 * g, R);
       break;
     case GK_DOWN:
       p.N = gp.h; p.K = gp.g;
       ok &= map2d(&mA, gp.A, g, R, BK, BM);
       ok &= map3d(&mB0, gp.Wd, g, h, El, BK, B_ROWS);
       mB1 = mB0;
+      ok &= map2d_st(&mO0, gp.O, h, R);
+      mO1 = mO0;
       break;
     case GK_DACT:
       p.N = gp.g; p.K = gp.h;
       ok &= map2d(&mA, gp.DY, h, R, BK, BM);
       ok &= map3d(&mB0, gp.Wd, g, h, El, 64, BK);   // B(n,k) = W_down[e][k][n]
       mB1 = mB0;
+      ok &= map2d_st(&mO0, gp.GU, 2 * g, R);
+      ok &= map2d_st(&mO1, gp.A, g, R);
       break;
     case GK_DX:
       p.N = gp.h; p.K = 2 * gp.g;
       ok &= map2d(&mA, gp.GU, 2 * g, R, BK, BM);
       ok &= map3d(&mB0, gp.Wg, h, g, El, 64, BK);   // B(n,k) = W_gate[e][k][n]
       ok &= map3d(&mB1, gp.Wu, h, g, El, 64, BK);
+      ok &= map2d_st(&mO0, gp.O, h, R);
+      mO1 = mO0;
       break;
     case GK_WGRAD_DOWN:
       p.M = gp.h; p.N = gp.g;
@@ -726,6 +899,8 @@ int launch(const GemmProblem<__nv_bfloat16>& gp, cudaStream_t st) {
       ok &= map2d(&mB0, gp.A, g, R, 64, BK);        // B(n,k) = a_w[s0+k][n]
       mB1 = mB0;
       p.dW0 = gp.dWd;
+      ok &= map3d_f32(&mO0, gp.dWd, g, h, El);
+      mO1 = mO0;
       break;
     default:
       p.M = 2 * gp.g; p.N = gp.h;
@@ -734,6 +909,8 @@ int launch(const GemmProblem<__nv_bfloat16>& gp, cudaStream_t st) {
       mB1 = mB0;
       p.dW0 = gp.dWg;
       p.dW1 = gp.dWu;
+      ok &= map3d_f32(&mO0, gp.dWg, h, g, El);
+      ok &= map3d_f32(&mO1, gp.dWu, h, g, El);
       break;
   }
   if (!ok) return -1;
@@ -767,7 +944,7 @@ int launch(const GemmProblem<__nv_bfloat16>& gp, cudaStream_t st) {
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  if (cudaLaunchKernelEx(&cfg, gemm_kernel<KIND, PAIR>, p, mA, mB0, mB1) != cudaSuccess) return -1;
+  if (cudaLaunchKernelEx(&cfg, gemm_kernel<KIND, PAIR>, p, mA, mB0, mB1, mO0, mO1) != cudaSuccess) return -1;
   return 1;
 }
 
