@@ -146,6 +146,17 @@ memfine_status memfine_create(const memfine_dims* dims, const uint8_t* nccl_uniq
                               memfine_handle_t* out);
 memfine_status memfine_destroy(memfine_handle_t h);
 
+/* In-process EP group: ep_size ranks of one layer in ONE process on ONE device, one host
+ * thread per rank, exchanging rows with stream-ordered device copies instead of NCCL (the
+ * same send layout, per-(peer, local expert) segments and receive offsets as the NCCL path).
+ * For validating the expert-parallel data path on a single GPU; every rank's calls must be
+ * made concurrently from its own thread (they rendezvous like collectives).  The group must
+ * outlive its handles. */
+typedef struct memfine_group_s* memfine_group_t;
+memfine_status memfine_local_group_create(int32_t nranks, memfine_group_t* out);
+memfine_status memfine_local_group_destroy(memfine_group_t g);
+memfine_status memfine_create_local(const memfine_dims* dims, memfine_group_t group, memfine_handle_t* out);
+
 /* A1 + A2: per-sub-chunk expert histogram of this rank's routing,
  * then the all-gather of every rank's histogram ("the first notification",
  * PAPER.md:200).  ids_dev: int32 [T][k] row-major.  counts_dev: int32

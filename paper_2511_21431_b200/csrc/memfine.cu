@@ -8,14 +8,40 @@
 #include <string>
 #include <algorithm>
 #include <type_traits>
+#include <mutex>
+#include <condition_variable>
+#include <array>
 
 #include "kernels.h"
 #include "nccl_shim.h"
 
 using namespace memfine;
 
+// In-process EP group (memfine_local_group_create): a host barrier plus per-rank events and
+// published buffer pointers; exchanges are pull-based device copies.
+struct memfine_group_s {
+  int n = 0;
+  std::mutex m;
+  std::condition_variable cv;
+  int arrived = 0, gen = 0;
+  std::vector<cudaEvent_t> ready, done;
+  std::vector<std::array<char*, 8>> ptrs;   // per rank: buffers of the current call
+  void barrier() {
+    std::unique_lock<std::mutex> lk(m);
+    int g = gen;
+    if (++arrived == n) {
+      arrived = 0;
+      gen++;
+      cv.notify_all();
+    } else {
+      cv.wait(lk, [&] { return gen != g; });
+    }
+  }
+};
+
 struct memfine_handle_s {
   memfine_dims d;
+  memfine_group_s* lg = nullptr;   // in-process EP group (instead of NCCL)
   int device = 0;
   int num_sms = 148;
   int* status_h = nullptr;     // pinned, mapped: device-latched error word
@@ -434,6 +460,58 @@ EpChunk ep_chunk_table(const memfine_dims& d, const int* counts, int C, int j) {
   return t;
 }
 
+// ---- in-process group transport
+enum { kPtrSend = 0, kPtrSendDy = 1, kPtrSendW = 2, kPtrX = 3, kPtrDY = 4, kPtrO = 5, kPtrWRow = 6, kPtrDWRow = 7 };
+
+// all ranks' device work before this point is visible to every rank's stream after it
+void local_fence(memfine_handle_s* h, cudaStream_t st, std::vector<cudaEvent_t>& evs) {
+  memfine_group_s* g = h->lg;
+  cudaEventRecord(evs[h->d.ep_rank], st);
+  g->barrier();
+  for (int r = 0; r < g->n; r++)
+    if (r != h->d.ep_rank) cudaStreamWaitEvent(st, evs[r], 0);
+}
+
+EpChunk ep_chunk_table(const memfine_dims& d, const int* counts, int C, int j);
+
+// Pull-based exchange.  forward: copy the rows peers send me (their send layout) into my
+// expert-major buffer; reverse: copy the rows peers computed for my tokens (their expert-major
+// buffer) into my send layout.  Both tables are derived from the shared counts.
+int local_exchange(memfine_handle_s* h, const int* counts, int C, int j, bool forward, int kind_send,
+                   int kind_expert, size_t row_bytes, cudaStream_t st) {
+  memfine_group_s* g = h->lg;
+  const memfine_dims& d = h->d;
+  int E = d.num_experts, EP = d.ep_size, El = E / EP, me = d.ep_rank;
+  local_fence(h, st, g->ready);
+  EpChunk mine = ep_chunk_table(d, counts, C, j);
+  for (int p = 0; p < EP; p++) {
+    memfine_dims dp = d;
+    dp.ep_rank = p;
+    EpChunk theirs = ep_chunk_table(dp, counts, C, j);
+    for (int el = 0; el < El; el++) {
+      if (forward) {
+        // p's copies for my expert (me, el) -> my rows recv_off[p][el]
+        int eg = me * El + el;
+        int64_t s0 = theirs.send_off[eg], n = theirs.send_off[eg + 1] - s0;
+        if (!n) continue;
+        char* src = g->ptrs[p][kind_send] + s0 * row_bytes;
+        char* dst = g->ptrs[me][kind_expert] + mine.recv_off[(size_t)p * El + el] * row_bytes;
+        if (cudaMemcpyAsync(dst, src, n * row_bytes, cudaMemcpyDeviceToDevice, st)) return 1;
+      } else {
+        // rows p computed for my copies of its expert (p, el) -> my send layout
+        int eg = p * El + el;
+        int64_t s0 = mine.send_off[eg], n = mine.send_off[eg + 1] - s0;
+        if (!n) continue;
+        char* src = g->ptrs[p][kind_expert] + theirs.recv_off[(size_t)me * El + el] * row_bytes;
+        char* dst = g->ptrs[me][kind_send] + s0 * row_bytes;
+        if (cudaMemcpyAsync(dst, src, n * row_bytes, cudaMemcpyDeviceToDevice, st)) return 1;
+      }
+    }
+  }
+  local_fence(h, st, g->done);  // nobody reuses a buffer until every rank's copies are done
+  return 0;
+}
+
 // One grouped exchange.  forward=true: send-layout rows -> receiver's expert-major rows;
 // forward=false: expert-major rows -> the source's send layout.  width = elements per row,
 // esize = bytes per element (row payload moved as bytes; NCCL dtype uint8) or 4 for fp32 scalars.
@@ -441,6 +519,16 @@ int ep_exchange(memfine_handle_s* h, const EpChunk& t, const int* counts, int C,
                 char* expert_buf, size_t row_bytes, cudaStream_t st) {
   const memfine_dims& d = h->d;
   int E = d.num_experts, EP = d.ep_size, El = E / EP, me = d.ep_rank;
+  if (h->lg) {
+    // the buffer kinds are identified from the published pointer table
+    int ks = -1, ke = -1;
+    for (int k = 0; k < 8; k++) {
+      if (h->lg->ptrs[me][k] == send_buf) ks = k;
+      if (h->lg->ptrs[me][k] == expert_buf) ke = k;
+    }
+    if (ks < 0 || ke < 0) return 1;
+    return local_exchange(h, counts, C, j, forward, ks, ke, row_bytes, st);
+  }
   if (nccl_group_start()) return 1;
   int rc = 0;
   for (int peer = 0; peer < EP && !rc; peer++) {
@@ -490,7 +578,18 @@ int ep_gather_counts(memfine_handle_s* h, const int32_t* ids, int C, cudaStream_
   }
   int* mine = h->counts_d + (int64_t)d.ep_rank * C * d.num_experts;
   launch_route_hist(ids, d.tokens, d.topk, d.num_experts, C, mine, h->status_d, st);
-  if (nccl_all_gather_int(&h->comm, mine, h->counts_d, (size_t)C * d.num_experts, st)) return MEMFINE_ERR_NCCL;
+  if (h->lg) {
+    h->lg->ptrs[d.ep_rank][0] = (char*)mine;
+    local_fence(h, st, h->lg->ready);
+    size_t nb = sizeof(int) * (size_t)C * d.num_experts;
+    for (int r = 0; r < d.ep_size; r++)
+      if (r != d.ep_rank)
+        MF_CUDA_OK(cudaMemcpyAsync(h->counts_d + (int64_t)r * C * d.num_experts, h->lg->ptrs[r][0], nb,
+                                   cudaMemcpyDeviceToDevice, st));
+    local_fence(h, st, h->lg->done);
+  } else if (nccl_all_gather_int(&h->comm, mine, h->counts_d, (size_t)C * d.num_experts, st)) {
+    return MEMFINE_ERR_NCCL;
+  }
   MF_CUDA_OK(cudaMemcpyAsync(h->counts_h, h->counts_d, need * sizeof(int), cudaMemcpyDeviceToHost, st));
   MF_CUDA_OK(cudaStreamSynchronize(st));
   if (*h->status_h) return __atomic_exchange_n(h->status_h, 0, __ATOMIC_SEQ_CST);
@@ -513,6 +612,18 @@ memfine_status ep_run(memfine_handle_s* h, int pass, const T* dy, const T* x, co
   }
   Layout L = carve(d, C, pass, ws, rows_max, send_max);
   if (L.total > ws_bytes) return MEMFINE_ERR_WORKSPACE;
+  if (h->lg) {
+    auto& P = h->lg->ptrs[d.ep_rank];
+    P[kPtrSend] = (char*)L.send;
+    P[kPtrSendDy] = (char*)L.send_dy;
+    P[kPtrSendW] = (char*)L.send_w;
+    P[kPtrX] = (char*)L.X;
+    P[kPtrDY] = (char*)L.DY;
+    P[kPtrO] = (char*)L.O;
+    P[kPtrWRow] = (char*)L.m.w_row;
+    P[kPtrDWRow] = (char*)L.m.dw_row;
+    if (pass == MEMFINE_BWD) P[kPtrO] = nullptr;  // O aliases X in the backward
+  }
   h->last_meta = L.meta_bytes;
   h->last_row_bytes = L.row_bytes;
   size_t rb = (size_t)hd * sizeof(T);
@@ -680,6 +791,48 @@ memfine_status memfine_create(const memfine_dims* dims, const uint8_t* nccl_uniq
   return MEMFINE_OK;
 }
 
+memfine_status memfine_local_group_create(int32_t nranks, memfine_group_t* out) {
+  if (!out || nranks < 1 || nranks > 64) return MEMFINE_ERR_INVALID_ARG;
+  memfine_group_s* g = new memfine_group_s();
+  g->n = nranks;
+  g->ready.resize(nranks);
+  g->done.resize(nranks);
+  g->ptrs.assign(nranks, {});
+  for (int r = 0; r < nranks; r++) {
+    if (cudaEventCreateWithFlags(&g->ready[r], cudaEventDisableTiming) ||
+        cudaEventCreateWithFlags(&g->done[r], cudaEventDisableTiming)) {
+      cudaGetLastError();
+      memfine_local_group_destroy(g);
+      return MEMFINE_ERR_CUDA;
+    }
+  }
+  *out = g;
+  return MEMFINE_OK;
+}
+
+memfine_status memfine_local_group_destroy(memfine_group_t g) {
+  if (!g) return MEMFINE_ERR_INVALID_ARG;
+  for (auto e : g->ready) if (e) cudaEventDestroy(e);
+  for (auto e : g->done) if (e) cudaEventDestroy(e);
+  delete g;
+  return MEMFINE_OK;
+}
+
+memfine_status memfine_create_local(const memfine_dims* dims, memfine_group_t group, memfine_handle_t* out) {
+  if (!group || !dims || !out || dims->ep_size != group->n) return MEMFINE_ERR_INVALID_ARG;
+  memfine_dims d1 = *dims;
+  int ep = d1.ep_size, rk = d1.ep_rank;
+  d1.ep_size = 1;   // create with the single-rank path, then switch to the group
+  d1.ep_rank = 0;
+  if (!dims_ok(dims)) return MEMFINE_ERR_INVALID_ARG;
+  memfine_status st = memfine_create(&d1, nullptr, out);
+  if (st != MEMFINE_OK) return st;
+  (*out)->d.ep_size = ep;
+  (*out)->d.ep_rank = rk;
+  (*out)->lg = group;
+  return MEMFINE_OK;
+}
+
 memfine_status memfine_destroy(memfine_handle_t h) {
   if (!h) return MEMFINE_ERR_INVALID_ARG;
   if (h->comm.comm) nccl_comm_destroy(&h->comm);
@@ -702,7 +855,16 @@ memfine_status memfine_route_counts(memfine_handle_t h, const int32_t* ids_dev, 
   int* mine = counts_dev + (int64_t)d.ep_rank * nsub * d.num_experts;
   launch_route_hist(ids_dev, d.tokens, d.topk, d.num_experts, nsub, mine, h->status_d, st);
   if (cudaGetLastError() != cudaSuccess) return MEMFINE_ERR_CUDA;
-  if (d.ep_size > 1) {
+  if (d.ep_size > 1 && h->lg) {
+    h->lg->ptrs[d.ep_rank][0] = (char*)mine;
+    local_fence(h, st, h->lg->ready);
+    size_t nb = sizeof(int) * (size_t)nsub * d.num_experts;
+    for (int r = 0; r < d.ep_size; r++)
+      if (r != d.ep_rank)
+        MF_CUDA_OK(cudaMemcpyAsync(counts_dev + (int64_t)r * nsub * d.num_experts, h->lg->ptrs[r][0], nb,
+                                   cudaMemcpyDeviceToDevice, st));
+    local_fence(h, st, h->lg->done);
+  } else if (d.ep_size > 1) {
     if (nccl_all_gather_int(&h->comm, mine, counts_dev, (size_t)nsub * d.num_experts, st)) return MEMFINE_ERR_NCCL;
   }
   return MEMFINE_OK;

@@ -67,15 +67,37 @@ def a2a_plan(counts_host: torch.Tensor, dims: capi.Dims, C_: int, chunk: int):
     return send, recv, off, int(rp.value)
 
 
+class LocalGroup:
+    """memfine_local_group_create: ep_size ranks of one layer in this process on one device
+    (one host thread per rank); used to validate the EP data path on a single GPU."""
+
+    def __init__(self, nranks: int):
+        g = C.c_void_p()
+        capi.check(capi.lib().memfine_local_group_create(nranks, C.byref(g)), "memfine_local_group_create")
+        self.g = g
+
+    def close(self):
+        if getattr(self, "g", None):
+            capi.lib().memfine_local_group_destroy(self.g)
+            self.g = None
+
+
 class MemFine:
     """One handle = one EP rank of one MoE layer shape.  ``process_group``: the EP group
     (torch.distributed) used only to broadcast the NCCL unique id when ep_size > 1."""
 
     def __init__(self, tokens, hidden, ffn, num_experts, topk, ep_size=1, ep_rank=0, dtype=torch.bfloat16,
-                 process_group=None):
+                 process_group=None, local_group=None):
         self.dims = make_dims(tokens, hidden, ffn, num_experts, topk, ep_size, ep_rank, dtype)
         self.dtype = dtype
         self.E_l = num_experts // ep_size
+        self._ws = None
+        if local_group is not None:
+            h = C.c_void_p()
+            capi.check(capi.lib().memfine_create_local(C.byref(self.dims), local_group.g, C.byref(h)),
+                       "memfine_create_local")
+            self.h = h
+            return
         uid = None
         if ep_size > 1:
             import torch.distributed as dist

@@ -1,0 +1,99 @@
+"""The expert-parallel data path on ONE GPU (run with -m gpu): EP = 2 / 4 ranks as host threads
+of one process (memfine_local_group_create), exchanging rows with device copies in exactly the
+NCCL path's layouts.  Every rank's Y, dX, d_score and its local experts' dW are compared with
+the oracle's EP emulation (all ranks, canonical chunk-major dW order)."""
+import threading
+
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import synth
+from paper_2511_21431_b200 import capi, layer
+from tests.harness import rel_err, tol
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _need_gpu():
+    if not torch.cuda.is_available():
+        pytest.skip("needs a CUDA device")
+
+
+def _bits(t, dtype):
+    return t.contiguous().view(torch.int16).numpy().view(np.uint16) if dtype == torch.bfloat16 else \
+        t.contiguous().numpy().astype(np.float32)
+
+
+@pytest.mark.parametrize("EP,C,dtype", [(2, 1, torch.bfloat16), (2, 3, torch.bfloat16), (4, 2, torch.bfloat16),
+                                        (4, 1, torch.float32), (2, 2, torch.float32)])
+def test_ep_local_group_matches_oracle(EP, C, dtype):
+    T, h, g, E, k = 300, 128, 256, 8, 2
+    El = E // EP
+    xs = [synth.make_x(T, h, rank=r, dtype=dtype) for r in range(EP)]
+    dys = [synth.make_dy(T, h, rank=r, dtype=dtype) for r in range(EP)]
+    routes = [synth.make_routing(T, E, k, rank=r, zipf_s=1.2, placement="contiguous") for r in range(EP)]
+    wg, wu, wd = synth.make_experts(range(E), h, g, dtype=dtype)
+    group = layer.LocalGroup(EP)
+    results, errors = [None] * EP, []
+    counts_seen = [None] * EP
+
+    def rank_main(r):
+        try:
+            torch.cuda.set_device(0)
+            st = torch.cuda.Stream()
+            with torch.cuda.stream(st):
+                mf = layer.MemFine(T, h, g, E, k, ep_size=EP, ep_rank=r, dtype=dtype, local_group=group)
+                dev = "cuda:0"
+                x, dy = xs[r].to(dev), dys[r].to(dev)
+                ids = torch.from_numpy(routes[r][0]).to(dev)
+                w = torch.from_numpy(routes[r][1]).to(dev)
+                lwg, lwu, lwd = (t[r * El:(r + 1) * El].contiguous().to(dev) for t in (wg, wu, wd))
+                counts = mf.route_counts(ids, nsub=C, stream=st)
+                st.synchronize()
+                ch = counts.cpu()
+                counts_seen[r] = ch.numpy().copy()
+                wsb = max(layer.workspace_bytes(ch, mf.dims, C, capi.FWD), layer.workspace_bytes(ch, mf.dims, C, capi.BWD))
+                ws = torch.empty(wsb, dtype=torch.uint8, device=dev)
+                y = mf.moe_fwd(x, ids, w, lwg, lwu, lwd, C, ws, stream=st)
+                dx, dwg, dwu, dwd, ds = mf.moe_bwd(dy, x, ids, w, lwg, lwu, lwd, C, ws, stream=st)
+                s_ = mf.sync(stream=st)
+                assert s_ == 0, capi.status_str(s_)
+                results[r] = [t.float().cpu().numpy() for t in (y, dx, ds, dwg, dwu, dwd)]
+                mf.close()
+        except BaseException as e:  # noqa: BLE001
+            import traceback
+            errors.append(f"rank {r}: {traceback.format_exc()}")
+
+    ths = [threading.Thread(target=rank_main, args=(r,)) for r in range(EP)]
+    for t in ths:
+        t.start()
+    for t in ths:
+        t.join(timeout=300)
+    group.close()
+    assert not errors, "\n".join(errors)
+    # every rank saw the same all-gathered counts, equal to the oracle's per-rank histograms
+    od1 = oracle.Dims(T=T, h=h, g=g, E=E, k=k)
+    ref_counts = np.stack([oracle.route_counts(od1, routes[r][0], C)[0] for r in range(EP)])
+    for r in range(EP):
+        np.testing.assert_array_equal(counts_seen[r], ref_counts)
+    # oracle EP emulation
+    d = oracle.Dims(T=T, h=h, g=g, E=E, k=k, EP=EP, in_dtype="bf16" if dtype == torch.bfloat16 else "f32")
+    xa = np.concatenate([_bits(x, dtype) for x in xs])
+    dya = np.concatenate([_bits(x, dtype) for x in dys])
+    ida = np.concatenate([r[0] for r in routes])
+    wa = np.concatenate([r[1] for r in routes]).astype(np.float64)
+    W = [_bits(t, dtype) for t in (wg, wu, wd)]
+    y_ref, _, _ = oracle.fcda_forward(d, C, xa, ida, wa, *W)
+    dx_ref, ds_ref, dwg_ref, dwu_ref, dwd_ref, _, _ = oracle.fcda_backward(d, C, dya, xa, ida, wa, *W)
+    t_ = tol(dtype)
+    for r in range(EP):
+        y, dx, ds, dwg, dwu, dwd = results[r]
+        sl = slice(r * T, (r + 1) * T)
+        es = slice(r * El, (r + 1) * El)
+        errs = {"y": rel_err(y, y_ref[sl]), "dx": rel_err(dx, dx_ref[sl]), "dscore": rel_err(ds, ds_ref[sl]),
+                "dw_gate": rel_err(dwg, dwg_ref[es]), "dw_up": rel_err(dwu, dwu_ref[es]),
+                "dw_down": rel_err(dwd, dwd_ref[es])}
+        assert all(v <= t_ for v in errs.values()), (r, errs)
