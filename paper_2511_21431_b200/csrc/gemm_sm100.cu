@@ -20,6 +20,7 @@
 #include <cstdlib>
 #include <algorithm>
 #include <cstring>
+#include <cmath>
 #include "kernels.h"
 
 namespace memfine {
@@ -916,11 +917,25 @@ int launch(const GemmProblem<__nv_bfloat16>& gp, cudaStream_t st) {
   if (!ok) return -1;
   constexpr int TM = PAIR ? 2 * BM : BM;
   int nt = (p.N + BN - 1) / BN;
+  const int per_unit = PAIR ? 2 : 1;
+  const int units_hw = g_num_sms / per_unit;
   {
-    // raster group: keep the group's A strips (GROUP_M x TM rows x K) within ~48 MB of L2
+    // Raster group: gm M tiles x all N tiles, gm sized so the group's A strips take ~24 MB of L2
+    // (measured best on the Mixtral-size step: less DRAM traffic -> less power -> higher clocks
+    // under the 1 kW cap; 48 and 96 MB were slower).  MEMFINE_L2_GROUP_MB=0 selects a square-ish
+    // wave block (gm ~ sqrt(units * B_strip / A_strip)) instead; other values set the budget.
+    static int64_t budget = [] {
+      const char* s = getenv("MEMFINE_L2_GROUP_MB");
+      return (int64_t)(s ? atoi(s) : 24) << 20;
+    }();
     int64_t kdim = (KIND >= GK_WGRAD_DOWN) ? (int64_t)std::max<int64_t>(1, R / std::max<uint64_t>(1, El)) : p.K;
-    int64_t strip = (int64_t)TM * kdim * 2;
-    p.group_m = (int)std::max<int64_t>(1, std::min<int64_t>(64, (48ll << 20) / std::max<int64_t>(1, strip)));
+    int64_t a_strip = (int64_t)TM * kdim * 2, b_strip = (int64_t)BN * kdim * 2;
+    if (budget) {
+      p.group_m = (int)std::max<int64_t>(1, std::min<int64_t>(64, budget / std::max<int64_t>(1, a_strip)));
+    } else {
+      double gm = std::sqrt((double)units_hw * (double)b_strip / (double)a_strip);
+      p.group_m = (int)std::max<double>(1.0, std::min<double>(64.0, std::floor(gm + 0.5)));
+    }
   }
   int64_t max_tiles;
   if (KIND >= GK_WGRAD_DOWN) {
@@ -929,8 +944,7 @@ int launch(const GemmProblem<__nv_bfloat16>& gp, cudaStream_t st) {
   } else {
     max_tiles = (int64_t)((R / BM + (PAIR ? El : 0)) / (PAIR ? 2 : 1) + 1) * nt;
   }
-  const int per_unit = PAIR ? 2 : 1;
-  int units = (int)std::min<int64_t>(max_tiles, g_num_sms / per_unit);
+  int units = (int)std::min<int64_t>(max_tiles, units_hw);
   if (units <= 0) return 0;
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(units * per_unit);
