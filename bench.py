@@ -41,6 +41,15 @@ FLOP_COEF = {"gemm_gateup_swiglu": 8, "gemm_down": 2, "gemm_dact_epilogue": 2, "
              "gemm_wgrad_down": 2, "gemm_wgrad_gateup": 4}
 
 
+def load_traffic():
+    """DRAM bytes per launch per kernel class from the committed ncu capture (tools/ncu_traffic.py)."""
+    import glob
+    files = sorted(glob.glob(os.path.join(ROOT, "profiles", "*_ncu_traffic.json")))
+    if not files:
+        return None, None
+    return json.load(open(files[-1])), os.path.relpath(files[-1], ROOT)
+
+
 def load_peaks():
     p = os.path.join(ROOT, "MEASURED_PEAKS.json")
     if os.path.exists(p):
@@ -335,8 +344,13 @@ def main():
         avg_ms = prof[dom]["ms"] / prof[dom]["launches"]
         achieved = per_launch_flops / (avg_ms / 1000.0) / 1e12
         peak = peaks["bf16_tflops_sustained"]
+        traffic, tsrc = load_traffic()
+        tb = traffic.get(dom, {}).get("bytes_per_launch") if traffic else None
         roof = {"bound": "tensor", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
-                "frac": achieved / peak, "traffic": None,
+                "frac": achieved / peak, "traffic": tb,
+                "traffic_source": f"{tsrc}: ncu --set full dram__bytes_read.sum + dram__bytes_write.sum per launch"
+                if tb else None,
+                "algorithmic_flops_per_launch": per_launch_flops,
                 "peak_source": f"{peaks['source']} bf16_tflops_sustained (kernel timed inside a long step)",
                 "share_of_step": prof[dom]["ms"] / tot_ms if tot_ms else None}
     gemm_ms = sum(prof[s]["ms"] for s in FLOP_COEF) / args.steps
