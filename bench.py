@@ -358,24 +358,61 @@ def main():
     step_tflops = 22 * h * g * rows_total / (ms / 1000.0) / 1e12
 
     # ---------------------------------------------------------------- e2e through the public API
+    # Every step copies its inputs (x, dY, ids, scores) host->device from pinned memory and reads
+    # its results (y, dX) device->host, inside the timed region.  Copies run on a second stream,
+    # double-buffered: step i+1's inputs and step i-1's results move while step i computes.
     pin = lambda t: t.pin_memory()
     xh, dyh, idsh, wh = pin(x_h), pin(dy_h), pin(ids_h), pin(w_h)
-    yh = torch.empty(y.shape, dtype=y.dtype).pin_memory()
-    dxh = torch.empty(dx.shape, dtype=dx.dtype).pin_memory()
-    xd, dyd, idsd, wdv = torch.empty_like(x), torch.empty_like(dy), torch.empty_like(ids), torch.empty_like(w)
+    out_h = [(torch.empty(y.shape, dtype=y.dtype).pin_memory(), torch.empty(dx.shape, dtype=dx.dtype).pin_memory())
+             for _ in range(2)]
+    ins = [tuple(torch.empty_like(t) for t in (x, dy, ids, w)) for _ in range(2)]
+    outs = [(y, dx), (torch.empty_like(y), torch.empty_like(dx))]
+    cs = torch.cuda.Stream()
+    comp = torch.cuda.current_stream()
 
-    def e2e_step():
-        xd.copy_(xh, non_blocking=True)
-        dyd.copy_(dyh, non_blocking=True)
-        idsd.copy_(idsh, non_blocking=True)
-        wdv.copy_(wh, non_blocking=True)
-        step(xd, dyd, idsd, wdv)
-        yh.copy_(y, non_blocking=True)
-        dxh.copy_(dx, non_blocking=True)
+    def e2e_run(K):
+        in_ready = [torch.cuda.Event() for _ in range(2)]
+        done = [torch.cuda.Event() for _ in range(2)]
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(comp)
+        cs.wait_stream(comp)
 
-    ms_e2e, _ = timed(e2e_step, args.steps, 1)
+        def h2d(b):
+            with torch.cuda.stream(cs):
+                for dst, src in zip(ins[b], (xh, dyh, idsh, wh)):
+                    dst.copy_(src, non_blocking=True)
+                in_ready[b].record(cs)
+
+        h2d(0)
+        if K > 1:
+            h2d(1)
+        for i in range(K):
+            b = i % 2
+            comp.wait_event(in_ready[b])
+            xx, dyy, idd, ww = ins[b]
+            yy, dxx = outs[b]
+            mf.moe_fwd(xx, idd, ww, wg, wu, wd, C, ws, y=yy)
+            mf.moe_bwd(dyy, xx, idd, ww, wg, wu, wd, C, ws, dx=dxx, dw_gate=dwg, dw_up=dwu, dw_down=dwd,
+                       dscore=dscore)
+            done[b].record(comp)
+            with torch.cuda.stream(cs):
+                cs.wait_event(done[b])
+                out_h[b][0].copy_(yy, non_blocking=True)
+                out_h[b][1].copy_(dxx, non_blocking=True)
+            if i + 2 < K:
+                h2d(b)   # waits (stream order on cs) for the D2H above, which waited for step i
+        comp.wait_stream(cs)
+        e1.record(comp)
+        torch.cuda.synchronize()
+        return e0.elapsed_time(e1) / K
+
+    e2e_run(2)
+    mf.sync()
+    barrier(world)
+    ms_e2e = max_over_ranks(e2e_run(args.steps), world)
+    assert mf.sync() == 0
     h2d = sum(t.numel() * t.element_size() for t in (xh, dyh, idsh, wh))
-    d2h = sum(t.numel() * t.element_size() for t in (yh, dxh))
+    d2h = sum(t.numel() * t.element_size() for t in out_h[0])
 
     # ---------------------------------------------------------------- memory: peak activation vs unchunked
     def peak_gb(Cc):

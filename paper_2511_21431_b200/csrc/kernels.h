@@ -14,6 +14,7 @@ struct ChunkMeta {
   int* info;       // [kInfoWords]
   int* dest_of;    // [Tmax*k]     position of copy (i,slot): expert-major row (EP=1) or send row
   int* src_of;     // [rows_cap]   copy index feeding each row (EP=1, debug/gather), -1 padding
+  int* send_src;   // [Tmax*k]     copy index feeding each send row (EP>1)
   float* w_row;    // [rows_cap]   top-k score of each row (0 on padding)
   float* dw_row;   // [rows_cap]   d_score of each row (bwd)
 };
@@ -28,10 +29,12 @@ void launch_dispatch_scan(int NB, int E, int El, int ep_size, int64_t rows_cap, 
                           int64_t* stats_rows, int64_t* stats_rows_pad, int chunk, cudaStream_t st);
 void launch_ep_recv_seg(const int* counts, int C, int j, int E, int El, int me, int EP, int64_t rows_cap,
                         const ChunkMeta& m, int64_t* stats_rows, int64_t* stats_rows_pad, cudaStream_t st);
+// Index pass (stable ranks) + row gather.  expert_major: EP=1 padded layout (padding rows zeroed,
+// rows_cap bounds the grid); otherwise the EP send layout.
 template <typename T>
 void launch_dispatch_scatter(const T* x, const T* dy, const int32_t* ids, const float* w, int64_t t0,
-                             int64_t t1, int k, int E, int h, const ChunkMeta& m, T* xd, T* dyd,
-                             cudaStream_t st);
+                             int64_t t1, int k, int E, int h, const ChunkMeta& m, T* xd, T* dyd, int El,
+                             bool expert_major, int64_t rows_cap, cudaStream_t st);
 template <typename T>
 void launch_zero_padding(int El, int h, const ChunkMeta& m, T* xd, T* dyd, cudaStream_t st);
 template <typename T>

@@ -162,6 +162,7 @@ Layout carve(const memfine_dims& d, int C, int pass, void* ws, int64_t rows_cap,
   L.m.info = b.take<int>(kInfoWords);
   L.m.dest_of = b.take<int>((uint64_t)Tm * d.topk);
   if (d.ep_size > 1) {
+    L.m.send_src = b.take<int>((uint64_t)Tm * d.topk);
     L.send = b.take<char>((uint64_t)send_rows * d.hidden * D);
     if (pass == MEMFINE_BWD) L.send_dy = b.take<char>((uint64_t)send_rows * d.hidden * D);
     L.send_w = b.take<float>((uint64_t)send_rows);
@@ -332,8 +333,7 @@ memfine_status fwd_ep1(memfine_handle_s* h, const T* x, const int32_t* ids, cons
     prof_begin(h, 6, st);
     launch_dispatch_hist(ids, t0, t1, k, E, L.m, h->status_d, st);
     launch_dispatch_scan(NB, E, El, 1, R, L.m, h->rows_d, h->rows_d + kMaxSub, j, st);
-    launch_dispatch_scatter<T>(x, nullptr, ids, w, t0, t1, k, E, hd, L.m, (T*)L.X, nullptr, st);
-    launch_zero_padding<T>(El, hd, L.m, (T*)L.X, nullptr, st);
+    launch_dispatch_scatter<T>(x, nullptr, ids, w, t0, t1, k, E, hd, L.m, (T*)L.X, nullptr, El, true, R, st);
     prof_end(h, st);
     h->last.kernel_launches += 4;
     if (h->debug) {
@@ -389,8 +389,7 @@ memfine_status bwd_ep1(memfine_handle_s* h, const T* dy, const T* x, const int32
     prof_begin(h, 6, st);
     launch_dispatch_hist(ids, t0, t1, k, E, L.m, h->status_d, st);
     launch_dispatch_scan(NB, E, El, 1, R, L.m, h->rows_d, h->rows_d + kMaxSub, j, st);
-    launch_dispatch_scatter<T>(x, dy, ids, w, t0, t1, k, E, hd, L.m, (T*)L.X, (T*)L.DY, st);
-    launch_zero_padding<T>(El, hd, L.m, (T*)L.X, (T*)L.DY, st);
+    launch_dispatch_scatter<T>(x, dy, ids, w, t0, t1, k, E, hd, L.m, (T*)L.X, (T*)L.DY, El, true, R, st);
     prof_end(h, st);
     h->last.kernel_launches += 4;
     GemmProblem<T> p = base_problem<T>(h, L, wg, wu, wd);
@@ -644,8 +643,8 @@ memfine_status ep_run(memfine_handle_s* h, int pass, const T* dy, const T* x, co
       launch_dispatch_hist(ids, t0, t1, k, E, L.m, h->status_d, st);
       launch_dispatch_scan(NB, E, El, d.ep_size, L.rows_cap, L.m, nullptr, nullptr, j, st);
       launch_dispatch_scatter<T>(x, pass == MEMFINE_BWD ? dy : nullptr, ids, w, t0, t1, k, E, hd, ms, (T*)L.send,
-                                 pass == MEMFINE_BWD ? (T*)L.send_dy : nullptr, st);
-      h->last.kernel_launches += 3;
+                                 pass == MEMFINE_BWD ? (T*)L.send_dy : nullptr, El, false, 0, st);
+      h->last.kernel_launches += 4;
     }
     launch_ep_recv_seg(h->counts_d, C, j, E, El, d.ep_rank, d.ep_size, L.rows_cap, L.m, h->rows_d,
                        h->rows_d + kMaxSub, st);

@@ -1,6 +1,7 @@
 // route.cu — routing histogram, stable dispatch permute, combine, unpermute-reduce and the
 // MACT tuner kernel.  HBM-bound data movement:
 // 16-byte vector loads/stores along contiguous rows, one warp per routed copy / token.
+#include <algorithm>
 #include "kernels.h"
 
 namespace memfine {
@@ -155,12 +156,11 @@ __device__ __forceinline__ void copy_row(T* __restrict__ dst, const T* __restric
   for (; i < nv; i += 32) d[i] = __ldg(s + i);
 }
 
-template <typename T>
-__global__ void __launch_bounds__(256) dispatch_scatter_kernel(
-    const T* __restrict__ x, const T* __restrict__ dy, const int32_t* __restrict__ ids, const float* __restrict__ w,
-    int64_t t0, int64_t t1, int k, int E, int h, const int* __restrict__ blk_off, int* __restrict__ dest_of,
-    int* __restrict__ src_of, float* __restrict__ w_row, float* __restrict__ dw_row, const int* __restrict__ info,
-    T* __restrict__ xd, T* __restrict__ dyd) {
+// Pass 3a: stable in-block rank -> dest_of[copy], row_src[row] = copy index, row scores.
+__global__ void __launch_bounds__(256) dispatch_index_kernel(
+    const int32_t* __restrict__ ids, const float* __restrict__ w, int64_t t0, int64_t t1, int k, int E,
+    const int* __restrict__ blk_off, int* __restrict__ dest_of, int* __restrict__ row_src,
+    float* __restrict__ w_row, float* __restrict__ dw_row, const int* __restrict__ info) {
   if (info[kInfoSkip]) return;
   extern __shared__ int smem[];
   int* run = smem;        // [E]
@@ -191,31 +191,85 @@ __global__ void __launch_bounds__(256) dispatch_scatter_kernel(
     }
   }
   __syncthreads();
-  int nw = blockDim.x >> 5;
-  for (int q = warp; q < ncp; q += nw) {
+  for (int q = threadIdx.x; q < ncp; q += blockDim.x) {
     int p = spos[q];
     int64_t qg = b0 * k + q;  // global copy index i*k + slot
-    if (lane == 0) dest_of[qg - t0 * k] = p;
+    dest_of[qg - t0 * k] = p;
     if (p < 0) continue;
-    if (lane == 0) {
-      if (src_of) src_of[p] = (int)qg;
-      if (w_row) w_row[p] = __ldg(w + qg);
-      if (dw_row) dw_row[p] = 0.0f;
+    row_src[p] = (int)qg;
+    if (w_row) w_row[p] = __ldg(w + qg);
+    if (dw_row) dw_row[p] = 0.0f;
+  }
+}
+
+// Pass 3b: one warp per destination row copies the token row(s) with 16-byte vectors, 4 loads in
+// flight per lane.  With `seg` (EP=1 expert-major layout) rows past a local expert's count are
+// padding: zero-filled, row_src = -1, scores 0.  Row count from info (device-side).
+template <typename T>
+__global__ void __launch_bounds__(256) dispatch_gather_kernel(
+    const T* __restrict__ x, const T* __restrict__ dy, int k, int h, const int* __restrict__ row_src_in,
+    int* __restrict__ row_src, const int* __restrict__ seg, const int* __restrict__ cnt, int El,
+    float* __restrict__ w_row, float* __restrict__ dw_row, const int* __restrict__ info, int rows_word,
+    T* __restrict__ xd, T* __restrict__ dyd) {
+  if (info[kInfoSkip]) return;
+  const int rows = info[rows_word];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int nwarps = gridDim.x * (blockDim.x >> 5);
+  constexpr int V = 16 / sizeof(T);
+  const int nv = h / V;
+  for (int r = blockIdx.x * (blockDim.x >> 5) + warp; r < rows; r += nwarps) {
+    bool pad = false;
+    if (seg) {
+      int e = expert_of_row(seg, El, r);
+      pad = r >= __ldg(seg + e) + __ldg(cnt + e);
     }
-    int64_t i = qg / k;
-    copy_row<T>(xd + (int64_t)p * h, x + i * h, h, lane);
-    if (dy) copy_row<T>(dyd + (int64_t)p * h, dy + i * h, h, lane);
+    uint4* d = reinterpret_cast<uint4*>(xd + (int64_t)r * h);
+    uint4* d2 = dy ? reinterpret_cast<uint4*>(dyd + (int64_t)r * h) : nullptr;
+    if (pad) {
+      uint4 z = make_uint4(0, 0, 0, 0);
+      for (int i = lane; i < nv; i += 32) { d[i] = z; if (d2) d2[i] = z; }
+      if (lane == 0) {
+        row_src[r] = -1;
+        if (w_row) w_row[r] = 0.f;
+        if (dw_row) dw_row[r] = 0.f;
+      }
+      continue;
+    }
+    const int64_t tok = __ldg(row_src_in + r) / k;
+    const uint4* s = reinterpret_cast<const uint4*>(x + tok * h);
+    const uint4* s2 = dy ? reinterpret_cast<const uint4*>(dy + tok * h) : nullptr;
+    int i = lane;
+    for (; i + 96 < nv; i += 128) {
+      uint4 a0 = __ldg(s + i), a1 = __ldg(s + i + 32), a2 = __ldg(s + i + 64), a3 = __ldg(s + i + 96);
+      if (s2) {
+        uint4 b0 = __ldg(s2 + i), b1 = __ldg(s2 + i + 32), b2 = __ldg(s2 + i + 64), b3 = __ldg(s2 + i + 96);
+        d2[i] = b0; d2[i + 32] = b1; d2[i + 64] = b2; d2[i + 96] = b3;
+      }
+      d[i] = a0; d[i + 32] = a1; d[i + 64] = a2; d[i + 96] = a3;
+    }
+    for (; i < nv; i += 32) {
+      d[i] = __ldg(s + i);
+      if (s2) d2[i] = __ldg(s2 + i);
+    }
   }
 }
 
 template <typename T>
 void launch_dispatch_scatter(const T* x, const T* dy, const int32_t* ids, const float* w, int64_t t0, int64_t t1,
-                             int k, int E, int h, const ChunkMeta& m, T* xd, T* dyd, cudaStream_t st) {
+                             int k, int E, int h, const ChunkMeta& m, T* xd, T* dyd, int El, bool expert_major,
+                             int64_t rows_cap, cudaStream_t st) {
   int NB = (int)ceil_div64(t1 - t0, kTokPerBlk);
   if (NB == 0) return;
   size_t smem = sizeof(int) * ((size_t)E + (size_t)kTokPerBlk * k);
-  dispatch_scatter_kernel<T><<<NB, 256, smem, st>>>(x, dy, ids, w, t0, t1, k, E, h, m.blk_cnt, m.dest_of,
-                                                    m.src_of, m.w_row, dy ? m.dw_row : nullptr, m.info, xd, dyd);
+  int* row_src = expert_major ? m.src_of : m.send_src;
+  dispatch_index_kernel<<<NB, 256, smem, st>>>(ids, w, t0, t1, k, E, m.blk_cnt, m.dest_of, row_src, m.w_row,
+                                               dy ? m.dw_row : nullptr, m.info);
+  int64_t rows_ub = expert_major ? rows_cap : (t1 - t0) * k;
+  int blocks = (int)std::min<int64_t>(ceil_div64(std::max<int64_t>(rows_ub, 1), 8), 148 * 16);
+  dispatch_gather_kernel<T><<<blocks, 256, 0, st>>>(x, dy, k, h, row_src, row_src, expert_major ? m.seg : nullptr,
+                                                    m.recv_cnt, El, expert_major ? m.w_row : nullptr,
+                                                    (expert_major && dy) ? m.dw_row : nullptr, m.info,
+                                                    expert_major ? kInfoRowsPad : kInfoSend, xd, dyd);
 }
 
 // Zero the padding rows of each local expert segment (so padded rows contribute exact
@@ -305,6 +359,8 @@ __global__ void __launch_bounds__(256) gather_reduce_kernel(
     int p = dest_of[(i - t0) * k + lane];
     dscore[i * k + lane] = p >= 0 ? dw_row[p] : 0.0f;
   }
+  // 4 column chunks per iteration: 4*k independent 16-byte loads in flight per lane
+#pragma unroll 4
   for (int c = lane * 8; c < h; c += 256) {
     float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
     for (int s = 0; s < kk; s++) {
@@ -479,9 +535,10 @@ void launch_plan_kernel(const int32_t* counts_dev, const PlanParams& p, memfine_
 // ------------------------------------------------------------------------------------------
 template void launch_dispatch_scatter<__nv_bfloat16>(const __nv_bfloat16*, const __nv_bfloat16*, const int32_t*,
                                                      const float*, int64_t, int64_t, int, int, int, const ChunkMeta&,
-                                                     __nv_bfloat16*, __nv_bfloat16*, cudaStream_t);
+                                                     __nv_bfloat16*, __nv_bfloat16*, int, bool, int64_t, cudaStream_t);
 template void launch_dispatch_scatter<float>(const float*, const float*, const int32_t*, const float*, int64_t,
-                                             int64_t, int, int, int, const ChunkMeta&, float*, float*, cudaStream_t);
+                                             int64_t, int, int, int, const ChunkMeta&, float*, float*, int, bool,
+                                             int64_t, cudaStream_t);
 template void launch_zero_padding<__nv_bfloat16>(int, int, const ChunkMeta&, __nv_bfloat16*, __nv_bfloat16*,
                                                  cudaStream_t);
 template void launch_zero_padding<float>(int, int, const ChunkMeta&, float*, float*, cudaStream_t);
