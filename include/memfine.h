@@ -157,6 +157,19 @@ memfine_status memfine_local_group_create(int32_t nranks, memfine_group_t* out);
 memfine_status memfine_local_group_destroy(memfine_group_t g);
 memfine_status memfine_create_local(const memfine_dims* dims, memfine_group_t group, memfine_handle_t* out);
 
+/* EP transport of a handle (ep_size > 1).
+ *  MEMFINE_EP_COPY (default): the permute writes a send buffer; the dispatch / combine
+ *    all-to-allv move rows between ranks (ncclSend/Recv per (peer, local expert) segment, or
+ *    stream-ordered device copies inside an in-process group).
+ *  MEMFINE_EP_P2P: the exchange is fused into the kernels over peer memory:
+ *    the permute kernel stores each token row straight into the receiving rank's expert-major
+ *    buffer, and the down / dX GEMM epilogues store each output row straight into its source
+ *    rank's combine buffer as the tile is produced; ranks fence with events (in-process group).
+ *    Requires an in-process group for now (MEMFINE_ERR_UNSUPPORTED otherwise); ep_size <= 16.
+ * The workspace layout and size are the same for both. */
+enum { MEMFINE_EP_COPY = 0, MEMFINE_EP_P2P = 1 };
+memfine_status memfine_set_ep_transport(memfine_handle_t h, int32_t transport);
+
 /* A1 + A2: per-sub-chunk expert histogram of this rank's routing,
  * then the all-gather of every rank's histogram ("the first notification",
  * PAPER.md:200).  ids_dev: int32 [T][k] row-major.  counts_dev: int32

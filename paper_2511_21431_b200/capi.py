@@ -13,11 +13,12 @@ OK, ERR_INVALID_ARG, ERR_INFEASIBLE, ERR_ROUTING, ERR_CUDA, ERR_NCCL, ERR_WORKSP
 BF16, FP32 = 0, 1
 RULE_EQ9, RULE_EXACT = 0, 1
 MODEL_PAPER, MODEL_IMPL = 0, 1
+EP_COPY, EP_P2P = 0, 1
 FWD, BWD = 0, 1
 
 # Every symbol include/memfine.h declares (checked by tests/test_abi.py).
 SYMBOLS = ("memfine_abi_version", "memfine_status_str", "memfine_nccl_unique_id", "memfine_create",
-           "memfine_destroy", "memfine_local_group_create", "memfine_local_group_destroy", "memfine_create_local", "memfine_route_counts", "memfine_plan", "memfine_workspace_bytes", "memfine_a2a_plan",
+           "memfine_destroy", "memfine_local_group_create", "memfine_local_group_destroy", "memfine_create_local", "memfine_set_ep_transport", "memfine_route_counts", "memfine_plan", "memfine_workspace_bytes", "memfine_a2a_plan",
            "memfine_moe_fwd", "memfine_moe_bwd", "memfine_sync", "memfine_last_stats",
            "memfine_profile_enable", "memfine_profile_read", "memfine_set_debug", "memfine_debug_perm")
 
@@ -96,6 +97,7 @@ def lib():
         L.memfine_local_group_create.argtypes = [i32, C.POINTER(vp)]
         L.memfine_local_group_destroy.argtypes = [vp]
         L.memfine_create_local.argtypes = [C.POINTER(Dims), vp, C.POINTER(vp)]
+        L.memfine_set_ep_transport.argtypes = [vp, i32]
         L.memfine_route_counts.argtypes = [vp, vp, i32, vp, vp]
         L.memfine_plan.argtypes = [vp, i32, C.POINTER(Dims), C.POINTER(Budget), C.POINTER(PlanInfo)]
         L.memfine_workspace_bytes.argtypes = [vp, i32, C.POINTER(Dims), i32, i32, C.POINTER(u64)]

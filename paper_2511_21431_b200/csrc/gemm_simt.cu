@@ -124,7 +124,12 @@ __global__ void __launch_bounds__(256) gemm_simt_kernel(GemmProblem<T> p, int M,
         }
         case GK_DOWN:
         case GK_DX:
-          p.O[row * p.h + n] = Elt<T>::from_f(v);
+          if (p.row_addr) {
+            const uint64_t a = p.row_addr[row];
+            if (a) reinterpret_cast<T*>(a)[n] = Elt<T>::from_f(v);
+          } else {
+            p.O[row * p.h + n] = Elt<T>::from_f(v);
+          }
           break;
         case GK_DACT: {
           float G = Elt<T>::to_f(p.GU[row * 2 * p.g + n]);

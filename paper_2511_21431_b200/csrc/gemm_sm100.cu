@@ -264,6 +264,7 @@ struct Params {
   float* dW1;        // WGRAD_GU: dW_up
   int store_a, store_gu;
   int beta;          // WGRAD: 1 = dW += acc (accumulate), 0 = dW = acc (first chunk, overwrite)
+  const uint64_t* row_addr;  // DOWN / DX fused EP combine: per-row peer destination (0 = padding)
   int group_m;       // M tiles per raster group (host-sized so a wave's operands stay in L2)
 };
 
@@ -644,6 +645,13 @@ __global__ void __launch_bounds__(THREADS, 1)
               bulk_commit();
             }
           }
+        } else if ((KIND == GK_DOWN || KIND == GK_DX) && p.row_addr) {
+          // fused combine exchange: the row goes straight into its source rank's send buffer
+          // (peer memory) as the tile is produced
+          if (rows_ok && n < p.h) {
+            const uint64_t a = __ldg(p.row_addr + row);
+            if (a) store32_bf16(reinterpret_cast<__nv_bfloat16*>(a) + n, v);
+          }
         } else if (KIND == GK_DOWN || KIND == GK_DX) {
           if (rows_ok && n < p.h) {
             uint8_t* buf = next_buf();
@@ -856,6 +864,7 @@ int launch(const GemmProblem<__nv_bfloat16>& gp, cudaStream_t st) {
   p.store_a = gp.store_a;
   p.store_gu = gp.store_gu;
   p.beta = gp.wgrad_beta;
+  p.row_addr = gp.row_addr;
   const uint64_t R = (uint64_t)gp.rows_cap, h = gp.h, g = gp.g, El = gp.El;
   if (R == 0) return 0;
   CUtensorMap mA, mB0, mB1, mO0, mO1;

@@ -15,6 +15,9 @@ struct ChunkMeta {
   int* dest_of;    // [Tmax*k]     position of copy (i,slot): expert-major row (EP=1) or send row
   int* src_of;     // [rows_cap]   copy index feeding each row (EP=1, debug/gather), -1 padding
   int* send_src;   // [Tmax*k]     copy index feeding each send row (EP>1)
+  int* p2p_tab;    // [C][4E+1]    fused-exchange tables (EP>1, see PeerTable)
+  uint64_t* row_addr;    // [rows_cap] fused combine: destination of each row in its source's send buffer
+  uint64_t* row_addr_w;  // [rows_cap] ... and of its d_score slot
   float* w_row;    // [rows_cap]   top-k score of each row (0 on padding)
   float* dw_row;   // [rows_cap]   d_score of each row (bwd)
 };
@@ -35,6 +38,9 @@ template <typename T>
 void launch_dispatch_scatter(const T* x, const T* dy, const int32_t* ids, const float* w, int64_t t0,
                              int64_t t1, int k, int E, int h, const ChunkMeta& m, T* xd, T* dyd, int El,
                              bool expert_major, int64_t rows_cap, cudaStream_t st);
+// Index pass only (stable ranks -> dest_of, row_src, scores), for the fused P2P dispatch.
+void launch_dispatch_index(const int32_t* ids, const float* w, int64_t t0, int64_t t1, int k, int E,
+                           const ChunkMeta& m, int* row_src, float* w_row, cudaStream_t st);
 template <typename T>
 void launch_zero_padding(int El, int h, const ChunkMeta& m, T* xd, T* dyd, cudaStream_t st);
 template <typename T>
@@ -43,6 +49,36 @@ void launch_combine(const T* O, const float* w, int64_t t0, int64_t t1, int k, i
 template <typename T>
 void launch_unpermute_reduce(const T* dXd, int64_t t0, int64_t t1, int k, int h, const ChunkMeta& m,
                              T* dx, float* dscore, cudaStream_t st);
+
+// ---------------------------------------------------------------- fused EP exchange over peer memory
+// Peer buffers of every EP rank, mapped into this process (in-process group: other ranks'
+// workspaces on the same device; multi-process: CUDA IPC mappings).
+constexpr int kMaxPeers = 16;
+struct PeerTable {
+  char* X[kMaxPeers];       // expert-major token rows [R][h]
+  char* DY[kMaxPeers];      // expert-major dY rows (bwd)
+  char* w_row[kMaxPeers];   // per-row scores
+  char* send[kMaxPeers];    // send-layout rows: where o / dX rows come back
+  char* send_w[kMaxPeers];  // send-layout d_score slots (bwd)
+  int n;
+};
+// Per-chunk table (ints): send_off[E+1] | land[EP*El] | recv_off[EP*El] | ret[EP*El]
+//   send_off: prefix of this rank's chunk copies over global experts (its send layout)
+//   land[p*El+el]: first row of this rank's copies in rank p's expert-major buffer, expert (p, el)
+//   recv_off[s*El+el]: first row of rank s's copies in THIS rank's buffer, local expert el
+//   ret[s*El+el]: rank s's send-layout position of its copies of expert (this rank, el)
+// A5+A6 fused: one warp per send row writes the token row straight into the receiver's buffer.
+template <typename T>
+void launch_p2p_push(const T* x, const T* dy, const float* w, int k, int h, int E, int El, int EP,
+                     const int* tab, const int* send_src, const int* info, const PeerTable& pt, int64_t rows_ub,
+                     cudaStream_t st);
+// Row -> destination addresses for the combine direction (0 for padding rows).
+void launch_p2p_row_addr(const int* seg, const int* recv_cnt, int El, int EP, const int* tab, int E,
+                         const int* info, const PeerTable& pt, int row_bytes, uint64_t* row_addr,
+                         uint64_t* row_addr_w, int64_t rows_cap, cudaStream_t st);
+// B6 for d_score: each received row's d_w straight into its source rank's send_w slot.
+void launch_p2p_push_dw(const float* dw_row, const uint64_t* row_addr_w, const int* info, int64_t rows_cap,
+                        cudaStream_t st);
 
 // ---------------------------------------------------------------- MACT tuner (A3)
 struct PlanParams {
@@ -90,6 +126,8 @@ struct GemmProblem {
   int store_a;       // GATEUP: store a
   int store_gu;      // GATEUP: store G||U
   int wgrad_beta;    // WGRAD: 1 accumulate into dW, 0 overwrite (zero tiles for experts without rows)
+  const uint64_t* row_addr;  // DOWN / DX (fused EP combine): per-row destination address in the
+                             // source rank's send buffer (peer memory), 0 = padding; null = local O
 };
 
 // CUDA-core FFMA path (MEMFINE_FP32 mode; K12 of SURVEY §2.4).

@@ -25,7 +25,7 @@ struct memfine_group_s {
   std::condition_variable cv;
   int arrived = 0, gen = 0;
   std::vector<cudaEvent_t> ready, done;
-  std::vector<std::array<char*, 8>> ptrs;   // per rank: buffers of the current call
+  std::vector<std::array<char*, 12>> ptrs;  // per rank: buffers of the current call (slot 8: workspace)
   void barrier() {
     std::unique_lock<std::mutex> lk(m);
     int g = gen;
@@ -42,6 +42,10 @@ struct memfine_group_s {
 struct memfine_handle_s {
   memfine_dims d;
   memfine_group_s* lg = nullptr;   // in-process EP group (instead of NCCL)
+  int p2p = 0;                     // fused exchange over peer memory (MEMFINE_EP_P2P)
+  int fence_ctr = 0;
+  int* tab_h = nullptr;            // pinned staging of the per-chunk P2P tables
+  size_t tab_cap = 0;
   int device = 0;
   int num_sms = 148;
   int* status_h = nullptr;     // pinned, mapped: device-latched error word
@@ -140,8 +144,9 @@ struct Layout {
 
 uint64_t row_bytes_of(const memfine_dims& d, int pass) {
   uint64_t D = elt_bytes(d), h = d.hidden, g = d.ffn;
-  if (pass == MEMFINE_FWD) return 4 + 4 + D * (h + g + h);        // src_of, w_row, X, A, O
-  return 4 + 4 + 4 + D * (h + h + 2 * g + g);                      // + dw_row, DY, GU; O aliases X
+  uint64_t ep = d.ep_size > 1 ? 16 : 0;                            // row_addr, row_addr_w (EP>1)
+  if (pass == MEMFINE_FWD) return ep + 4 + 4 + D * (h + g + h);   // src_of, w_row, X, A, O
+  return ep + 4 + 4 + 4 + D * (h + h + 2 * g + g);                 // + dw_row, DY, GU; O aliases X
 }
 
 int64_t tmax_chunk(const memfine_dims& d, int C) { return ceil_div64(d.tokens, C); }
@@ -163,6 +168,7 @@ Layout carve(const memfine_dims& d, int C, int pass, void* ws, int64_t rows_cap,
   L.m.dest_of = b.take<int>((uint64_t)Tm * d.topk);
   if (d.ep_size > 1) {
     L.m.send_src = b.take<int>((uint64_t)Tm * d.topk);
+    L.m.p2p_tab = b.take<int>((uint64_t)C * (4 * (uint64_t)E + 1));
     L.send = b.take<char>((uint64_t)send_rows * d.hidden * D);
     if (pass == MEMFINE_BWD) L.send_dy = b.take<char>((uint64_t)send_rows * d.hidden * D);
     L.send_w = b.take<float>((uint64_t)send_rows);
@@ -174,6 +180,10 @@ Layout carve(const memfine_dims& d, int C, int pass, void* ws, int64_t rows_cap,
   int64_t R = rows_cap;
   L.m.src_of = b.take<int>(R);
   L.m.w_row = b.take<float>(R);
+  if (d.ep_size > 1) {
+    L.m.row_addr = b.take<uint64_t>(R);
+    L.m.row_addr_w = b.take<uint64_t>(R);
+  }
   if (pass == MEMFINE_BWD) L.m.dw_row = b.take<float>(R);
   L.X = b.take<char>((uint64_t)R * d.hidden * D);
   if (pass == MEMFINE_BWD) {
@@ -595,10 +605,150 @@ int ep_gather_counts(memfine_handle_s* h, const int32_t* ids, int C, cudaStream_
   return MEMFINE_OK;
 }
 
+// Alternating event sets so consecutive fences never re-record an event a peer may still wait on.
+void p2p_fence(memfine_handle_s* h, cudaStream_t st) {
+  local_fence(h, st, (h->fence_ctr++ & 1) ? h->lg->done : h->lg->ready);
+}
+
+// EP with the exchange fused into the kernels over peer memory: the permute
+// pushes each token row straight into the receiver's expert-major buffer, and the down / dX GEMM
+// epilogues store each output row straight into its source rank's send buffer, tile by tile.
+template <typename T>
+memfine_status ep_run_p2p(memfine_handle_s* h, int pass, const T* dy, const T* x, const int32_t* ids, const float* w,
+                          const void* wg, const void* wu, const void* wd, int C, T* out, float* dwg, float* dwu,
+                          float* dwd, float* dscore, int accumulate, void* ws, uint64_t ws_bytes, cudaStream_t st) {
+  const memfine_dims& d = h->d;
+  const int E = d.num_experts, EP = d.ep_size, El = E / EP, k = d.topk, hd = d.hidden, me = d.ep_rank;
+  if (EP > kMaxPeers) return MEMFINE_ERR_UNSUPPORTED;
+  if (int rc = ep_gather_counts(h, ids, C, st)) return (memfine_status)rc;
+  // every rank's chunk tables and workspace layout, from the shared counts
+  std::vector<std::vector<EpChunk>> tabs(EP);
+  std::vector<int64_t> rows_max(EP, 0), send_max(EP, 0);
+  for (int r = 0; r < EP; r++) {
+    memfine_dims dr = d;
+    dr.ep_rank = r;
+    for (int j = 0; j < C; j++) {
+      tabs[r].push_back(ep_chunk_table(dr, h->counts_h, C, j));
+      rows_max[r] = std::max(rows_max[r], tabs[r][j].rows_pad);
+      send_max[r] = std::max(send_max[r], tabs[r][j].send);
+    }
+  }
+  Layout L = carve(d, C, pass, ws, rows_max[me], send_max[me]);
+  if (L.total > ws_bytes) return MEMFINE_ERR_WORKSPACE;
+  h->last_meta = L.meta_bytes;
+  h->last_row_bytes = L.row_bytes;
+  h->lg->ptrs[me][8] = (char*)ws;
+  h->lg->barrier();  // every rank published its workspace
+  PeerTable pt{};
+  pt.n = EP;
+  for (int r = 0; r < EP; r++) {
+    memfine_dims dr = d;
+    dr.ep_rank = r;
+    Layout Lr = carve(dr, C, pass, h->lg->ptrs[r][8], rows_max[r], send_max[r]);
+    pt.X[r] = (char*)Lr.X;
+    pt.DY[r] = (char*)Lr.DY;
+    pt.w_row[r] = (char*)Lr.m.w_row;
+    pt.send[r] = (char*)Lr.send;
+    pt.send_w[r] = pass == MEMFINE_BWD ? (char*)Lr.send_w : nullptr;
+  }
+  // per-chunk tables -> device (one H2D from pinned staging; the call already synchronised once)
+  const size_t per = 4 * (size_t)E + 1;
+  if (h->tab_cap < per * C) {
+    if (h->tab_h) cudaFreeHost(h->tab_h);
+    h->tab_h = nullptr;
+    h->tab_cap = 0;
+    MF_CUDA_OK(cudaHostAlloc((void**)&h->tab_h, sizeof(int) * per * C, cudaHostAllocDefault));
+    h->tab_cap = per * C;
+  }
+  for (int j = 0; j < C; j++) {
+    int* tj = h->tab_h + per * j;
+    for (int e = 0; e <= E; e++) tj[e] = (int)tabs[me][j].send_off[e];
+    int* land = tj + E + 1;
+    int* roff = land + EP * El;
+    int* ret = roff + EP * El;
+    for (int p = 0; p < EP; p++)
+      for (int el = 0; el < El; el++) {
+        land[p * El + el] = (int)tabs[p][j].recv_off[(size_t)me * El + el];
+        roff[p * El + el] = (int)tabs[me][j].recv_off[(size_t)p * El + el];
+        ret[p * El + el] = (int)tabs[p][j].send_off[me * El + el];
+      }
+  }
+  MF_CUDA_OK(cudaMemcpyAsync(L.m.p2p_tab, h->tab_h, sizeof(int) * per * C, cudaMemcpyHostToDevice, st));
+  int beta = accumulate ? 1 : 0;
+  if (pass == MEMFINE_BWD && dscore && d.tokens > 0)
+    MF_CUDA_OK(cudaMemsetAsync(dscore, 0, sizeof(float) * d.tokens * k, st));
+  const int rb = hd * (int)sizeof(T);
+  for (int j = 0; j < C; j++) {
+    const EpChunk& t = tabs[me][j];
+    const int* tab_j = L.m.p2p_tab + per * j;
+    int64_t t0 = chunk_begin(d.tokens, C, j), t1 = chunk_begin(d.tokens, C, j + 1);
+    int NB = (int)ceil_div64(t1 - t0, kTokPerBlk);
+    if (NB) {
+      launch_dispatch_hist(ids, t0, t1, k, E, L.m, h->status_d, st);
+      launch_dispatch_scan(NB, E, El, EP, L.rows_cap, L.m, nullptr, nullptr, j, st);
+      launch_dispatch_index(ids, w, t0, t1, k, E, L.m, L.m.send_src, nullptr, st);
+      h->last.kernel_launches += 3;
+    }
+    launch_ep_recv_seg(h->counts_d, C, j, E, El, me, EP, L.rows_cap, L.m, h->rows_d, h->rows_d + kMaxSub, st);
+    prof_begin(h, 9, st);
+    p2p_fence(h, st);  // (A) every rank is done with its buffers of the previous chunk
+    if (NB)
+      launch_p2p_push<T>(x, pass == MEMFINE_BWD ? dy : nullptr, w, k, hd, E, El, EP, tab_j, L.m.send_src, L.m.info,
+                         pt, t.send, st);
+    p2p_fence(h, st);  // (B) every row pushed into this rank has landed
+    prof_end(h, st);
+    launch_zero_padding<T>(El, hd, L.m, (T*)L.X, pass == MEMFINE_BWD ? (T*)L.DY : nullptr, st);
+    if (pass == MEMFINE_BWD && t.rows_pad) MF_CUDA_OK(cudaMemsetAsync(L.m.dw_row, 0, sizeof(float) * t.rows_pad, st));
+    launch_p2p_row_addr(L.m.seg, L.m.recv_cnt, El, EP, tab_j, E, L.m.info, pt, rb, L.m.row_addr,
+                        pass == MEMFINE_BWD ? L.m.row_addr_w : nullptr, L.rows_cap, st);
+    h->last.kernel_launches += 3;
+    GemmProblem<T> p = base_problem<T>(h, L, wg, wu, wd);
+    p.dWg = dwg;
+    p.dWu = dwu;
+    p.dWd = dwd;
+    if (pass == MEMFINE_FWD) {
+      p.kind = GK_GATEUP;
+      p.store_a = 1;
+      if (int rc = run_gemm<T>(h, p, st)) return (memfine_status)rc;
+      p.kind = GK_DOWN;
+      p.row_addr = L.m.row_addr;   // A8 + A9 fused: o rows stored into their source's send buffer
+      if (int rc = run_gemm<T>(h, p, st)) return (memfine_status)rc;
+      p2p_fence(h, st);  // (C) every o row for this rank's tokens has landed
+      if (t1 > t0) launch_combine<T>((const T*)L.send, w, t0, t1, k, hd, L.m, out, st);
+    } else {
+      p.kind = GK_GATEUP;
+      p.store_a = 0;
+      p.store_gu = 1;
+      if (int rc = run_gemm<T>(h, p, st)) return (memfine_status)rc;
+      p.kind = GK_DACT;
+      if (int rc = run_gemm<T>(h, p, st)) return (memfine_status)rc;
+      p.wgrad_beta = beta;
+      p.kind = GK_WGRAD_DOWN;
+      if (int rc = run_gemm<T>(h, p, st)) return (memfine_status)rc;
+      p.kind = GK_WGRAD_GU;
+      if (int rc = run_gemm<T>(h, p, st)) return (memfine_status)rc;
+      beta = 1;
+      p.kind = GK_DX;
+      p.row_addr = L.m.row_addr;   // B4 + B6 fused: dX rows stored into their source's send buffer
+      if (int rc = run_gemm<T>(h, p, st)) return (memfine_status)rc;
+      launch_p2p_push_dw(L.m.dw_row, L.m.row_addr_w, L.m.info, L.rows_cap, st);
+      p2p_fence(h, st);  // (C)
+      ChunkMeta mb = L.m;
+      mb.dw_row = L.send_w;
+      if (t1 > t0) launch_unpermute_reduce<T>((const T*)L.send, t0, t1, k, hd, mb, out, dscore, st);
+    }
+    h->last.kernel_launches += 2;
+  }
+  return latch_cuda(h);
+}
+
 template <typename T>
 memfine_status ep_run(memfine_handle_s* h, int pass, const T* dy, const T* x, const int32_t* ids, const float* w,
                       const void* wg, const void* wu, const void* wd, int C, T* out, float* dwg, float* dwu,
                       float* dwd, float* dscore, int accumulate, void* ws, uint64_t ws_bytes, cudaStream_t st) {
+  if (h->p2p)
+    return ep_run_p2p<T>(h, pass, dy, x, ids, w, wg, wu, wd, C, out, dwg, dwu, dwd, dscore, accumulate, ws, ws_bytes,
+                         st);
   const memfine_dims& d = h->d;
   int E = d.num_experts, El = E / d.ep_size, k = d.topk, hd = d.hidden, g = d.ffn;
   if (int rc = ep_gather_counts(h, ids, C, st)) return (memfine_status)rc;
@@ -832,8 +982,16 @@ memfine_status memfine_create_local(const memfine_dims* dims, memfine_group_t gr
   return MEMFINE_OK;
 }
 
+memfine_status memfine_set_ep_transport(memfine_handle_t h, int32_t transport) {
+  if (!h || (transport != MEMFINE_EP_COPY && transport != MEMFINE_EP_P2P)) return MEMFINE_ERR_INVALID_ARG;
+  if (transport == MEMFINE_EP_P2P && !h->lg) return MEMFINE_ERR_UNSUPPORTED;  // peers mapped in-process only
+  h->p2p = transport == MEMFINE_EP_P2P;
+  return MEMFINE_OK;
+}
+
 memfine_status memfine_destroy(memfine_handle_t h) {
   if (!h) return MEMFINE_ERR_INVALID_ARG;
+  if (h->tab_h) cudaFreeHost(h->tab_h);
   if (h->comm.comm) nccl_comm_destroy(&h->comm);
   if (h->status_h) cudaFreeHost(h->status_h);
   if (h->rows_h) cudaFreeHost(h->rows_h);

@@ -254,6 +254,15 @@ __global__ void __launch_bounds__(256) dispatch_gather_kernel(
   }
 }
 
+void launch_dispatch_index(const int32_t* ids, const float* w, int64_t t0, int64_t t1, int k, int E,
+                           const ChunkMeta& m, int* row_src, float* w_row, cudaStream_t st) {
+  int NB = (int)ceil_div64(t1 - t0, kTokPerBlk);
+  if (NB == 0) return;
+  size_t smem = sizeof(int) * ((size_t)E + (size_t)kTokPerBlk * k);
+  dispatch_index_kernel<<<NB, 256, smem, st>>>(ids, w, t0, t1, k, E, m.blk_cnt, m.dest_of, row_src, w_row, nullptr,
+                                               m.info);
+}
+
 template <typename T>
 void launch_dispatch_scatter(const T* x, const T* dy, const int32_t* ids, const float* w, int64_t t0, int64_t t1,
                              int k, int E, int h, const ChunkMeta& m, T* xd, T* dyd, int El, bool expert_major,
@@ -427,6 +436,110 @@ void launch_ep_recv_seg(const int* counts, int C, int j, int E, int El, int me, 
 }
 
 // ------------------------------------------------------------------------------------------
+// Fused EP exchange over peer memory.
+// ------------------------------------------------------------------------------------------
+template <typename T>
+__global__ void __launch_bounds__(256) p2p_push_kernel(const T* __restrict__ x, const T* __restrict__ dy,
+                                                       const float* __restrict__ w, int k, int h, int E, int El,
+                                                       const int* __restrict__ tab, const int* __restrict__ send_src,
+                                                       const int* __restrict__ info, PeerTable pt) {
+  const int rows = info[kInfoSend];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int nwarps = gridDim.x * (blockDim.x >> 5);
+  const int* send_off = tab;
+  const int* land = tab + E + 1;
+  constexpr int V = 16 / sizeof(T);
+  const int nv = h / V;
+  for (int r = blockIdx.x * (blockDim.x >> 5) + warp; r < rows; r += nwarps) {
+    // expert of send row r: last e with send_off[e] <= r
+    int lo = 0, hi = E;
+    while (hi - lo > 1) {
+      int mid = (lo + hi) >> 1;
+      if (__ldg(send_off + mid) <= r) lo = mid; else hi = mid;
+    }
+    const int e = lo, dst = e / El, el = e % El;
+    const int64_t drow = (int64_t)__ldg(land + dst * El + el) + (r - __ldg(send_off + e));
+    const int q = __ldg(send_src + r);
+    const int64_t tok = q / k;
+    const uint4* s = reinterpret_cast<const uint4*>(x + tok * h);
+    uint4* d = reinterpret_cast<uint4*>(pt.X[dst] + drow * h * (int64_t)sizeof(T));
+    const uint4* s2 = dy ? reinterpret_cast<const uint4*>(dy + tok * h) : nullptr;
+    uint4* d2 = dy ? reinterpret_cast<uint4*>(pt.DY[dst] + drow * h * (int64_t)sizeof(T)) : nullptr;
+    int i = lane;
+    for (; i + 96 < nv; i += 128) {
+      uint4 a0 = __ldg(s + i), a1 = __ldg(s + i + 32), a2 = __ldg(s + i + 64), a3 = __ldg(s + i + 96);
+      if (s2) {
+        uint4 b0 = __ldg(s2 + i), b1 = __ldg(s2 + i + 32), b2 = __ldg(s2 + i + 64), b3 = __ldg(s2 + i + 96);
+        d2[i] = b0; d2[i + 32] = b1; d2[i + 64] = b2; d2[i + 96] = b3;
+      }
+      d[i] = a0; d[i + 32] = a1; d[i + 64] = a2; d[i + 96] = a3;
+    }
+    for (; i < nv; i += 32) {
+      d[i] = __ldg(s + i);
+      if (s2) d2[i] = __ldg(s2 + i);
+    }
+    if (lane == 0) reinterpret_cast<float*>(pt.w_row[dst])[drow] = __ldg(w + q);
+  }
+}
+
+template <typename T>
+void launch_p2p_push(const T* x, const T* dy, const float* w, int k, int h, int E, int El, int EP, const int* tab,
+                     const int* send_src, const int* info, const PeerTable& pt, int64_t rows_ub, cudaStream_t st) {
+  (void)EP;
+  if (rows_ub <= 0) return;
+  int blocks = (int)std::min<int64_t>(ceil_div64(rows_ub, 8), 148 * 16);
+  p2p_push_kernel<T><<<blocks, 256, 0, st>>>(x, dy, w, k, h, E, El, tab, send_src, info, pt);
+}
+
+__global__ void p2p_row_addr_kernel(const int* __restrict__ seg, const int* __restrict__ recv_cnt, int El, int EP,
+                                    const int* __restrict__ tab, int E, const int* __restrict__ info, PeerTable pt,
+                                    int row_bytes, uint64_t* __restrict__ row_addr, uint64_t* __restrict__ row_addr_w) {
+  const int rows = info[kInfoRowsPad];
+  const int* recv_off = tab + E + 1 + EP * El;
+  const int* ret = recv_off + EP * El;
+  for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < rows; r += gridDim.x * blockDim.x) {
+    const int el = expert_of_row(seg, El, r);
+    uint64_t a = 0, aw = 0;
+    if (r < __ldg(seg + el) + __ldg(recv_cnt + el)) {
+      // source rank: last s with recv_off[s][el] <= r (segments of one expert are src-ordered)
+      int s = 0;
+      for (int s2 = 1; s2 < EP; s2++)
+        if (__ldg(recv_off + s2 * El + el) <= r) s = s2;
+      const int64_t pos = (int64_t)__ldg(ret + s * El + el) + (r - __ldg(recv_off + s * El + el));
+      a = (uint64_t)(pt.send[s] + pos * row_bytes);
+      aw = pt.send_w[s] ? (uint64_t)(pt.send_w[s] + pos * 4) : 0;
+    }
+    row_addr[r] = a;
+    if (row_addr_w) row_addr_w[r] = aw;
+  }
+}
+
+void launch_p2p_row_addr(const int* seg, const int* recv_cnt, int El, int EP, const int* tab, int E, const int* info,
+                         const PeerTable& pt, int row_bytes, uint64_t* row_addr, uint64_t* row_addr_w,
+                         int64_t rows_cap, cudaStream_t st) {
+  if (rows_cap <= 0) return;
+  int blocks = (int)std::min<int64_t>(ceil_div64(rows_cap, 256), 148 * 8);
+  p2p_row_addr_kernel<<<blocks, 256, 0, st>>>(seg, recv_cnt, El, EP, tab, E, info, pt, row_bytes, row_addr,
+                                               row_addr_w);
+}
+
+__global__ void p2p_push_dw_kernel(const float* __restrict__ dw_row, const uint64_t* __restrict__ row_addr_w,
+                                   const int* __restrict__ info) {
+  const int rows = info[kInfoRowsPad];
+  for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < rows; r += gridDim.x * blockDim.x) {
+    uint64_t a = row_addr_w[r];
+    if (a) *reinterpret_cast<float*>(a) = dw_row[r];
+  }
+}
+
+void launch_p2p_push_dw(const float* dw_row, const uint64_t* row_addr_w, const int* info, int64_t rows_cap,
+                        cudaStream_t st) {
+  if (rows_cap <= 0) return;
+  int blocks = (int)std::min<int64_t>(ceil_div64(rows_cap, 256), 148 * 8);
+  p2p_push_dw_kernel<<<blocks, 256, 0, st>>>(dw_row, row_addr_w, info);
+}
+
+// ------------------------------------------------------------------------------------------
 // A3: MACT tuner.  plan_from_subsums is the one evaluation used by both the host path and
 // the device kernel (same integer arithmetic, so both are bit-identical by construction).
 // ------------------------------------------------------------------------------------------
@@ -539,6 +652,11 @@ template void launch_dispatch_scatter<__nv_bfloat16>(const __nv_bfloat16*, const
 template void launch_dispatch_scatter<float>(const float*, const float*, const int32_t*, const float*, int64_t,
                                              int64_t, int, int, int, const ChunkMeta&, float*, float*, int, bool,
                                              int64_t, cudaStream_t);
+template void launch_p2p_push<__nv_bfloat16>(const __nv_bfloat16*, const __nv_bfloat16*, const float*, int, int, int,
+                                             int, int, const int*, const int*, const int*, const PeerTable&,
+                                             int64_t, cudaStream_t);
+template void launch_p2p_push<float>(const float*, const float*, const float*, int, int, int, int, int, const int*,
+                                     const int*, const int*, const PeerTable&, int64_t, cudaStream_t);
 template void launch_zero_padding<__nv_bfloat16>(int, int, const ChunkMeta&, __nv_bfloat16*, __nv_bfloat16*,
                                                  cudaStream_t);
 template void launch_zero_padding<float>(int, int, const ChunkMeta&, float*, float*, cudaStream_t);

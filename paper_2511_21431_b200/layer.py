@@ -182,6 +182,9 @@ class MemFine:
         capi.check(capi.lib().memfine_profile_read(self.h, C.byref(pr)), "memfine_profile_read")
         return pr.as_dict()
 
+    def set_ep_transport(self, transport: int):
+        capi.check(capi.lib().memfine_set_ep_transport(self.h, int(transport)), "memfine_set_ep_transport")
+
     def set_debug(self, on: bool = True):
         capi.check(capi.lib().memfine_set_debug(self.h, int(on)), "memfine_set_debug")
 

@@ -27,9 +27,13 @@ def _bits(t, dtype):
         t.contiguous().numpy().astype(np.float32)
 
 
+@pytest.mark.parametrize("transport", [capi.EP_COPY, capi.EP_P2P])
 @pytest.mark.parametrize("EP,C,dtype", [(2, 1, torch.bfloat16), (2, 3, torch.bfloat16), (4, 2, torch.bfloat16),
                                         (4, 1, torch.float32), (2, 2, torch.float32)])
-def test_ep_local_group_matches_oracle(EP, C, dtype):
+def test_ep_local_group_matches_oracle(EP, C, dtype, transport):
+    """transport EP_COPY: send buffers + stream-ordered copies (the NCCL path's layouts);
+    EP_P2P: dispatch and combine fused into the permute kernel and the down/dX GEMM epilogues,
+    storing rows straight into peer buffers."""
     T, h, g, E, k = 300, 128, 256, 8, 2
     El = E // EP
     xs = [synth.make_x(T, h, rank=r, dtype=dtype) for r in range(EP)]
@@ -46,6 +50,7 @@ def test_ep_local_group_matches_oracle(EP, C, dtype):
             st = torch.cuda.Stream()
             with torch.cuda.stream(st):
                 mf = layer.MemFine(T, h, g, E, k, ep_size=EP, ep_rank=r, dtype=dtype, local_group=group)
+                mf.set_ep_transport(transport)
                 dev = "cuda:0"
                 x, dy = xs[r].to(dev), dys[r].to(dev)
                 ids = torch.from_numpy(routes[r][0]).to(dev)
