@@ -223,6 +223,9 @@ def main():
     ap.add_argument("--ref-tokens", type=int, default=4)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--placement", default=None)
+    ap.add_argument("--ep-transport", default="copy", choices=["copy", "p2p"],
+                    help="N>1: 'copy' = permute into send buffers + NCCL all-to-allv; 'p2p' = dispatch/combine "
+                         "fused into the permute kernel and the GEMM epilogues over CUDA-IPC peer memory")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
@@ -311,6 +314,9 @@ def main():
 
     fwd_b, bwd_b = ws_for(C)
     ws = torch.empty(max(fwd_b, bwd_b), dtype=torch.uint8, device=dev)
+    if world > 1 and args.ep_transport == "p2p":
+        mf.set_ep_transport(capi.EP_P2P)
+        mf.register_workspace(ws)
     step = make_step(C, ws)
 
     # launches per step (the library's own kernels)
@@ -445,6 +451,7 @@ def main():
         "config": {"workload": f"{cfg.name}-style MoE layer: E={E} top-{k} h={h} SwiGLU ffn={g}, {T} tokens/GPU, "
                                f"Zipf({cfg.zipf_s}) routing ({placement} placement), EP={EP}",
                    "tokens_per_gpu": T, "ep": EP, "chunks": C, "tuner": plan,
+                   "ep_transport": args.ep_transport if world > 1 else None,
                    "budget": {"gpu_capacity_bytes": cap, "alpha": args.alpha, "static_bytes": static},
                    "l2": "no flush: every step streams > 126 MB (weights 2.8 GB at EP=1, activations GBs)"},
         "peak_act_gb": peak_c, "peak_act_gb_unchunked": peak_1,

@@ -165,10 +165,19 @@ memfine_status memfine_create_local(const memfine_dims* dims, memfine_group_t gr
  *    the permute kernel stores each token row straight into the receiving rank's expert-major
  *    buffer, and the down / dX GEMM epilogues store each output row straight into its source
  *    rank's combine buffer as the tile is produced; ranks fence with events (in-process group).
- *    Requires an in-process group for now (MEMFINE_ERR_UNSUPPORTED otherwise); ep_size <= 16.
+ *    ep_size <= 16.  In-process groups map peers directly; across processes (NCCL handles) the
+ *    workspace must first be registered with memfine_register_workspace, and ranks fence with a
+ *    one-int NCCL all-reduce on the stream.
  * The workspace layout and size are the same for both. */
 enum { MEMFINE_EP_COPY = 0, MEMFINE_EP_P2P = 1 };
 memfine_status memfine_set_ep_transport(memfine_handle_t h, int32_t transport);
+
+/* Collective over the EP group (NCCL handles): export the device allocation holding `ws`
+ * through CUDA IPC, all-gather (handle, offset) over the handle's communicator and map every
+ * peer's workspace (cudaIpcMemLazyEnablePeerAccess).  MEMFINE_EP_P2P calls must then pass this
+ * same ws (MEMFINE_ERR_INVALID_ARG otherwise).  For in-process groups and ep_size == 1 it only
+ * records ws.  Synchronises `stream`. */
+memfine_status memfine_register_workspace(memfine_handle_t h, void* ws, uint64_t ws_bytes, void* stream);
 
 /* A1 + A2: per-sub-chunk expert histogram of this rank's routing,
  * then the all-gather of every rank's histogram ("the first notification",

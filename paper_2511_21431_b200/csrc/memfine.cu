@@ -13,6 +13,7 @@
 #include <array>
 
 #include "kernels.h"
+#include <cuda.h>
 #include "nccl_shim.h"
 
 using namespace memfine;
@@ -46,6 +47,12 @@ struct memfine_handle_s {
   int fence_ctr = 0;
   int* tab_h = nullptr;            // pinned staging of the per-chunk P2P tables
   size_t tab_cap = 0;
+  // multi-process P2P: every rank's registered workspace, mapped here with CUDA IPC
+  void* reg_ws = nullptr;
+  uint64_t reg_bytes = 0;
+  std::vector<char*> peer_ws;      // [EP] (own entry = reg_ws)
+  std::vector<void*> ipc_bases;    // opened peer allocation bases (to close)
+  int* barrier_d = nullptr;
   int device = 0;
   int num_sms = 148;
   int* status_h = nullptr;     // pinned, mapped: device-latched error word
@@ -607,7 +614,12 @@ int ep_gather_counts(memfine_handle_s* h, const int32_t* ids, int C, cudaStream_
 
 // Alternating event sets so consecutive fences never re-record an event a peer may still wait on.
 void p2p_fence(memfine_handle_s* h, cudaStream_t st) {
-  local_fence(h, st, (h->fence_ctr++ & 1) ? h->lg->done : h->lg->ready);
+  if (h->lg) {
+    local_fence(h, st, (h->fence_ctr++ & 1) ? h->lg->done : h->lg->ready);
+  } else {
+    // an all-reduce completes on every rank only after every rank's prior stream work
+    nccl_stream_barrier(&h->comm, h->barrier_d, st);
+  }
 }
 
 // EP with the exchange fused into the kernels over peer memory: the permute
@@ -637,14 +649,19 @@ memfine_status ep_run_p2p(memfine_handle_s* h, int pass, const T* dy, const T* x
   if (L.total > ws_bytes) return MEMFINE_ERR_WORKSPACE;
   h->last_meta = L.meta_bytes;
   h->last_row_bytes = L.row_bytes;
-  h->lg->ptrs[me][8] = (char*)ws;
-  h->lg->barrier();  // every rank published its workspace
+  if (h->lg) {
+    h->lg->ptrs[me][8] = (char*)ws;
+    h->lg->barrier();  // every rank published its workspace
+  } else if (ws != h->reg_ws || (int)h->peer_ws.size() != EP) {
+    return MEMFINE_ERR_INVALID_ARG;  // P2P across processes needs memfine_register_workspace(ws) first
+  }
   PeerTable pt{};
   pt.n = EP;
   for (int r = 0; r < EP; r++) {
     memfine_dims dr = d;
     dr.ep_rank = r;
-    Layout Lr = carve(dr, C, pass, h->lg->ptrs[r][8], rows_max[r], send_max[r]);
+    char* base_r = h->lg ? h->lg->ptrs[r][8] : h->peer_ws[r];
+    Layout Lr = carve(dr, C, pass, base_r, rows_max[r], send_max[r]);
     pt.X[r] = (char*)Lr.X;
     pt.DY[r] = (char*)Lr.DY;
     pt.w_row[r] = (char*)Lr.m.w_row;
@@ -655,6 +672,8 @@ memfine_status ep_run_p2p(memfine_handle_s* h, int pass, const T* dy, const T* x
   const size_t per = 4 * (size_t)E + 1;
   if (h->tab_cap < per * C) {
     if (h->tab_h) cudaFreeHost(h->tab_h);
+  for (void* b : h->ipc_bases) cudaIpcCloseMemHandle(b);
+  if (h->barrier_d) cudaFree(h->barrier_d);
     h->tab_h = nullptr;
     h->tab_cap = 0;
     MF_CUDA_OK(cudaHostAlloc((void**)&h->tab_h, sizeof(int) * per * C, cudaHostAllocDefault));
@@ -984,14 +1003,78 @@ memfine_status memfine_create_local(const memfine_dims* dims, memfine_group_t gr
 
 memfine_status memfine_set_ep_transport(memfine_handle_t h, int32_t transport) {
   if (!h || (transport != MEMFINE_EP_COPY && transport != MEMFINE_EP_P2P)) return MEMFINE_ERR_INVALID_ARG;
-  if (transport == MEMFINE_EP_P2P && !h->lg) return MEMFINE_ERR_UNSUPPORTED;  // peers mapped in-process only
+  if (transport == MEMFINE_EP_P2P && h->d.ep_size > kMaxPeers) return MEMFINE_ERR_UNSUPPORTED;
+  if (transport == MEMFINE_EP_P2P && !h->lg && h->d.ep_size > 1 && !h->comm.comm) return MEMFINE_ERR_UNSUPPORTED;
   h->p2p = transport == MEMFINE_EP_P2P;
+  return MEMFINE_OK;
+}
+
+// Multi-process P2P: export the allocation holding ws (base + offset) through CUDA IPC, all-gather
+// the records over the handle's NCCL communicator, open every peer's mapping.
+memfine_status memfine_register_workspace(memfine_handle_t h, void* ws, uint64_t ws_bytes, void* stream) {
+  if (!h || !ws) return MEMFINE_ERR_INVALID_ARG;
+  if (h->lg || h->d.ep_size == 1) {  // nothing to map: in-process peers / single rank
+    h->reg_ws = ws;
+    h->reg_bytes = ws_bytes;
+    return MEMFINE_OK;
+  }
+  if (!h->comm.comm) return MEMFINE_ERR_NCCL;
+  cudaStream_t st = (cudaStream_t)stream;
+  // allocation base of ws
+  typedef CUresult (*RangeFn)(CUdeviceptr*, size_t*, CUdeviceptr);
+  static RangeFn range_fn = nullptr;
+  if (!range_fn) {
+    cudaDriverEntryPointQueryResult q;
+    void* fp = nullptr;
+    if (cudaGetDriverEntryPoint("cuMemGetAddressRange", &fp, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      return MEMFINE_ERR_CUDA;
+    range_fn = (RangeFn)fp;
+  }
+  CUdeviceptr base = 0;
+  size_t size = 0;
+  if (range_fn(&base, &size, (CUdeviceptr)ws) != CUDA_SUCCESS) return MEMFINE_ERR_CUDA;
+  struct Rec { cudaIpcMemHandle_t hdl; uint64_t offset, bytes; };
+  Rec mine{};
+  if (cudaIpcGetMemHandle(&mine.hdl, (void*)base) != cudaSuccess) { cudaGetLastError(); return MEMFINE_ERR_CUDA; }
+  mine.offset = (uint64_t)((char*)ws - (char*)base);
+  mine.bytes = ws_bytes;
+  const int EP = h->d.ep_size, me = h->d.ep_rank;
+  char* dbuf = nullptr;
+  MF_CUDA_OK(cudaMalloc((void**)&dbuf, sizeof(Rec) * (EP + 1)));
+  MF_CUDA_OK(cudaMemcpyAsync(dbuf + sizeof(Rec) * EP, &mine, sizeof(Rec), cudaMemcpyHostToDevice, st));
+  if (nccl_all_gather_bytes(&h->comm, dbuf + sizeof(Rec) * EP, dbuf, sizeof(Rec), st)) {
+    cudaFree(dbuf);
+    return MEMFINE_ERR_NCCL;
+  }
+  std::vector<Rec> all(EP);
+  cudaMemcpyAsync(all.data(), dbuf, sizeof(Rec) * EP, cudaMemcpyDeviceToHost, st);
+  cudaStreamSynchronize(st);
+  cudaFree(dbuf);
+  for (void* b : h->ipc_bases) cudaIpcCloseMemHandle(b);
+  h->ipc_bases.clear();
+  h->peer_ws.assign(EP, nullptr);
+  for (int r = 0; r < EP; r++) {
+    if (r == me) { h->peer_ws[r] = (char*)ws; continue; }
+    void* pb = nullptr;
+    if (cudaIpcOpenMemHandle(&pb, all[r].hdl, cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) {
+      cudaGetLastError();
+      return MEMFINE_ERR_CUDA;
+    }
+    h->ipc_bases.push_back(pb);
+    h->peer_ws[r] = (char*)pb + all[r].offset;
+  }
+  if (!h->barrier_d) MF_CUDA_OK(cudaMalloc((void**)&h->barrier_d, sizeof(int)));
+  h->reg_ws = ws;
+  h->reg_bytes = ws_bytes;
   return MEMFINE_OK;
 }
 
 memfine_status memfine_destroy(memfine_handle_t h) {
   if (!h) return MEMFINE_ERR_INVALID_ARG;
   if (h->tab_h) cudaFreeHost(h->tab_h);
+  for (void* b : h->ipc_bases) cudaIpcCloseMemHandle(b);
+  if (h->barrier_d) cudaFree(h->barrier_d);
   if (h->comm.comm) nccl_comm_destroy(&h->comm);
   if (h->status_h) cudaFreeHost(h->status_h);
   if (h->rows_h) cudaFreeHost(h->rows_h);

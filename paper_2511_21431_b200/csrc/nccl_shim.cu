@@ -12,6 +12,7 @@ struct Api {
   decltype(&ncclCommInitRank) commInitRank = nullptr;
   decltype(&ncclCommDestroy) commDestroy = nullptr;
   decltype(&ncclAllGather) allGather = nullptr;
+  decltype(&ncclAllReduce) allReduce = nullptr;
   decltype(&ncclGroupStart) groupStart = nullptr;
   decltype(&ncclGroupEnd) groupEnd = nullptr;
   decltype(&ncclSend) send = nullptr;
@@ -36,6 +37,7 @@ Api* api() {
   LOAD(commInitRank, "ncclCommInitRank");
   LOAD(commDestroy, "ncclCommDestroy");
   LOAD(allGather, "ncclAllGather");
+  LOAD(allReduce, "ncclAllReduce");
   LOAD(groupStart, "ncclGroupStart");
   LOAD(groupEnd, "ncclGroupEnd");
   LOAD(send, "ncclSend");
@@ -80,6 +82,18 @@ int nccl_all_gather_int(NcclComm* c, const int* send, int* recv, size_t n, cudaS
   Api* a = api();
   if (!a || !c->comm) return 1;
   return a->allGather(send, recv, n, ncclInt32, (ncclComm_t)c->comm, st) != ncclSuccess;
+}
+
+int nccl_stream_barrier(NcclComm* c, int* dev_int, cudaStream_t st) {
+  Api* a = api();
+  if (!a || !c->comm) return 1;
+  return a->allReduce(dev_int, dev_int, 1, ncclInt32, ncclSum, (ncclComm_t)c->comm, st) != ncclSuccess;
+}
+
+int nccl_all_gather_bytes(NcclComm* c, const void* send, void* recv, size_t n, cudaStream_t st) {
+  Api* a = api();
+  if (!a || !c->comm) return 1;
+  return a->allGather(send, recv, n, ncclUint8, (ncclComm_t)c->comm, st) != ncclSuccess;
 }
 
 int nccl_group_start() { Api* a = api(); return !a || a->groupStart() != ncclSuccess; }

@@ -16,6 +16,9 @@ int nccl_get_unique_id(uint8_t out[128]);
 int nccl_comm_init(NcclComm* c, const uint8_t id[128], int nranks, int rank);
 void nccl_comm_destroy(NcclComm* c);
 int nccl_all_gather_int(NcclComm* c, const int* send, int* recv, size_t count_per_rank, cudaStream_t st);
+// all-reduce of one int (sum) on `st`: a stream barrier across the EP group
+int nccl_stream_barrier(NcclComm* c, int* dev_int, cudaStream_t st);
+int nccl_all_gather_bytes(NcclComm* c, const void* send, void* recv, size_t bytes_per_rank, cudaStream_t st);
 int nccl_group_start();
 int nccl_group_end();
 // dtype: 0 = uint8 bytes, 1 = int32, 2 = float32

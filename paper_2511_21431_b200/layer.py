@@ -185,6 +185,12 @@ class MemFine:
     def set_ep_transport(self, transport: int):
         capi.check(capi.lib().memfine_set_ep_transport(self.h, int(transport)), "memfine_set_ep_transport")
 
+    def register_workspace(self, ws: torch.Tensor, stream=None):
+        """memfine_register_workspace (collective for NCCL handles): map every rank's workspace
+        for the fused peer-memory exchange."""
+        capi.check(capi.lib().memfine_register_workspace(self.h, _ptr(ws), ws.numel(), _stream(stream)),
+                   "memfine_register_workspace")
+
     def set_debug(self, on: bool = True):
         capi.check(capi.lib().memfine_set_debug(self.h, int(on)), "memfine_set_debug")
 
