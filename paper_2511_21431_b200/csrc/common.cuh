@@ -45,8 +45,12 @@ template <> struct Elt<float> {
   static __device__ __forceinline__ float from_f(float v) { return v; }
 };
 
-__device__ __forceinline__ float silu_f(float z) { return z / (1.0f + __expf(-z)); }
-__device__ __forceinline__ float sigmoid_f(float z) { return 1.0f / (1.0f + __expf(-z)); }
+// MUFU-based (ex2 + rcp, ~2 ulp): ample for bf16 outputs; the fp32-mode FFMA path uses the
+// IEEE-exact forms (1e-5 parity).
+__device__ __forceinline__ float silu_f(float z) { return __fdividef(z, 1.0f + __expf(-z)); }
+__device__ __forceinline__ float sigmoid_f(float z) { return __fdividef(1.0f, 1.0f + __expf(-z)); }
+__device__ __forceinline__ float silu_exact(float z) { return z / (1.0f + expf(-z)); }
+__device__ __forceinline__ float sigmoid_exact(float z) { return 1.0f / (1.0f + expf(-z)); }
 
 // Binary search: the local expert owning padded row `row` (seg has El+1 entries).
 __device__ __forceinline__ int expert_of_row(const int* __restrict__ seg, int El, int row) {

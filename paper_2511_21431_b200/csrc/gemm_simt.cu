@@ -115,7 +115,7 @@ __global__ void __launch_bounds__(256) gemm_simt_kernel(GemmProblem<T> p, int M,
       switch (p.kind) {
         case GK_GATEUP: {
           float G = v, U = DUAL ? acc2[i][j] : 0.f;
-          if (p.store_a) p.A[row * p.g + n] = Elt<T>::from_f(silu_f(G) * U);
+          if (p.store_a) p.A[row * p.g + n] = Elt<T>::from_f(silu_exact(G) * U);
           if (p.store_gu) {
             p.GU[row * 2 * p.g + n] = Elt<T>::from_f(G);
             p.GU[row * 2 * p.g + p.g + n] = Elt<T>::from_f(U);
@@ -135,7 +135,7 @@ __global__ void __launch_bounds__(256) gemm_simt_kernel(GemmProblem<T> p, int M,
           float G = Elt<T>::to_f(p.GU[row * 2 * p.g + n]);
           float U = Elt<T>::to_f(p.GU[row * 2 * p.g + p.g + n]);
           float ws = p.w_row[row];
-          float sg = sigmoid_f(G);
+          float sg = sigmoid_exact(G);
           float a = G * sg * U;
           dwp = fmaf(v, a, dwp);
           float dA = ws * v;

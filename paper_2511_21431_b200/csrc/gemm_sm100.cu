@@ -109,6 +109,16 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
   asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }
 
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&r)[16]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, "
+      "%15}, [%16];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+
 __device__ __forceinline__ uint32_t pack_bf16(float a, float b) {
   __nv_bfloat162 v = __floats2bfloat162_rn(a, b);
   return *reinterpret_cast<uint32_t*>(&v);
@@ -241,9 +251,13 @@ template <> struct Cfg<GK_WGRAD_GU> { static constexpr int BN = 256, NACC = 1, A
 template <int KIND>
 struct Epi {
   static constexpr int SLOTS = KIND == GK_DACT ? 3 : (KIND == GK_GATEUP ? 2 : 1);
-  static constexpr int SLOT_BYTES = KIND >= GK_WGRAD_DOWN ? 4096 : 2048;
+  // dA works in 16-column sub-chunks (32 rows x 32 B, SWIZZLE_32B) so its staging is 24 KB
+  static constexpr int SLOT_BYTES = KIND >= GK_WGRAD_DOWN ? 4096 : (KIND == GK_DACT ? 1024 : 2048);
   static constexpr int CHUNK_BYTES = SLOTS * SLOT_BYTES;
-  static constexpr int WARP_BYTES = 2 * CHUNK_BYTES;
+  // dA and dW: single-buffered staging so the mainloop keeps one more stage of operands in flight
+  // (measured: dA 72% -> 82% tensor-active going from 4 to 5 stages); the others double-buffer.
+  static constexpr int BUFS = (KIND == GK_DACT || KIND >= GK_WGRAD_DOWN) ? 1 : 2;
+  static constexpr int WARP_BYTES = BUFS * CHUNK_BYTES;
   static constexpr int TOTAL = EPI_WARPS * WARP_BYTES;
 };
 
@@ -379,13 +393,13 @@ __host__ __device__ constexpr int stage_bytes() {
 // as many 1024-aligned stages as fit next to the epilogue staging (227 KB per CTA)
 template <int KIND, bool PAIR>
 __host__ __device__ constexpr int nstage() {
-  return (232448 - 1024 - 256 - Epi<KIND>::TOTAL) / stage_bytes<KIND, PAIR>() > 6
+  return (232448 - 1024 - 512 - Epi<KIND>::TOTAL) / stage_bytes<KIND, PAIR>() > 6
              ? 6
-             : (232448 - 1024 - 256 - Epi<KIND>::TOTAL) / stage_bytes<KIND, PAIR>();
+             : (232448 - 1024 - 512 - Epi<KIND>::TOTAL) / stage_bytes<KIND, PAIR>();
 }
 template <int KIND, bool PAIR>
 __host__ __device__ constexpr int smem_bytes() {
-  return nstage<KIND, PAIR>() * stage_bytes<KIND, PAIR>() + Epi<KIND>::TOTAL + 1024 + 256;
+  return nstage<KIND, PAIR>() * stage_bytes<KIND, PAIR>() + Epi<KIND>::TOTAL + 1024 + 512;
 }
 
 // ------------------------------------------------------------------ the kernel
@@ -418,7 +432,8 @@ __global__ void __launch_bounds__(THREADS, 1)
   uint64_t* empty = full + NSTAGE;
   uint64_t* tfull = empty + NSTAGE;
   uint64_t* tempty = tfull + 2;
-  uint32_t* tmem_slot = (uint32_t*)(tempty + 2);
+  uint64_t* ebar = tempty + 2;                          // [EPI_WARPS][2] epilogue TMA-load barriers (dA)
+  uint32_t* tmem_slot = (uint32_t*)(ebar + 2 * EPI_WARPS);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t rank = PAIR ? cta_rank_in_cluster() : 0;
@@ -433,6 +448,7 @@ __global__ void __launch_bounds__(THREADS, 1)
     if (KIND == GK_GATEUP || KIND == GK_DACT || KIND == GK_WGRAD_GU) prefetch_tmap(&tmO1);
     for (int s = 0; s < NSTAGE; s++) { mbar_init(full + s, 1); mbar_init(empty + s, 1); }
     for (int a = 0; a < 2; a++) { mbar_init(tfull + a, 1); mbar_init(tempty + a, (PAIR ? 2 : 1) * EPI_WARPS); }
+    for (int i = 0; i < 2 * EPI_WARPS; i++) mbar_init(ebar + i, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   }
@@ -556,12 +572,26 @@ __global__ void __launch_bounds__(THREADS, 1)
     uint8_t* wbuf = epi_smem + ew * EP::WARP_BYTES;
     int sbuf = 0;
     int it = 0;
+    uint32_t ephase[2] = {0, 0};   // dA: phase of this warp's two G||U load barriers
+    // dA: TMA-load the G||U sub-tile (32 rows x 32 cols each) of chunk column n into buffer b
+    auto dact_load = [&](int b, int n, int row0) {
+      if (lane == 0) {
+        bulk_wait_read<0>();   // the buffer's previous stores have read it
+        uint8_t* buf = wbuf + b * EP::CHUNK_BYTES;
+        mbar_expect_tx(ebar + 2 * ew + b, 2 * EP::SLOT_BYTES);
+        tma_2d(buf, &tmO0, ebar + 2 * ew + b, n, row0);
+        tma_2d(buf + EP::SLOT_BYTES, &tmO0, ebar + 2 * ew + b, p.g + n, row0);
+      }
+      __syncwarp();
+    };
     auto next_buf = [&]() -> uint8_t* {
-      // the group that last used this buffer (two chunks ago) must have finished reading it
-      if (lane == 0) bulk_wait_read<1>();
+      // the group that last used this buffer must have finished reading it
+      if (lane == 0) {
+        if (EP::BUFS == 2) bulk_wait_read<1>(); else bulk_wait_read<0>();
+      }
       __syncwarp();
       uint8_t* b = wbuf + sbuf * EP::CHUNK_BYTES;
-      sbuf ^= 1;
+      if (EP::BUFS == 2) sbuf ^= 1;
       return b;
     };
     for (int t = cid; t < ntiles; t += ncid) {
@@ -593,21 +623,17 @@ __global__ void __launch_bounds__(THREADS, 1)
       }
       int as = it & 1;
       uint32_t aph = (it >> 1) & 1;
-      mbar_wait(tfull + as, aph);
-      fence_after();
-      uint32_t tb = tmem_base + as * ACC_COLS + ((uint32_t)(q * 32) << 16);
       const int64_t row = rowi;
       float dwp = 0.f;
       float wrow = 0.f;
-      uint32_t gpre[16], upre[16];
       if (KIND == GK_DACT && rows_ok) {
         wrow = p.w_row[row];
         const int n0c = T.n0 + half * CPW;
-        if (n0c < p.g) {
-          load32_raw(p.GU + row * 2 * p.g + n0c, gpre);
-          load32_raw(p.GU + row * 2 * p.g + p.g + n0c, upre);
-        }
+        if (n0c < p.g) dact_load(0, n0c, row0);   // first chunk's G||U, overlapping the MMA
       }
+      mbar_wait(tfull + as, aph);
+      fence_after();
+      uint32_t tb = tmem_base + as * ACC_COLS + ((uint32_t)(q * 32) << 16);
 #pragma unroll 1
       for (int c = half * CPW; c < (half + 1) * CPW; c += 32) {
         const int n = T.n0 + c;
@@ -665,47 +691,63 @@ __global__ void __launch_bounds__(THREADS, 1)
           }
         } else if (KIND == GK_DACT) {
           if (rows_ok && n < p.g) {
-            uint32_t gcur[16], ucur[16];
+            uint8_t* buf = wbuf;
 #pragma unroll
-            for (int j = 0; j < 16; j++) { gcur[j] = gpre[j]; ucur[j] = upre[j]; }
-            // prefetch the next chunk's G||U while this one computes
-            if (c + 32 < (half + 1) * CPW && n + 32 < p.g) {
-              load32_raw(p.GU + row * 2 * p.g + n + 32, gpre);
-              load32_raw(p.GU + row * 2 * p.g + p.g + n + 32, upre);
-            }
-            uint8_t* buf = next_buf();
-            uint32_t og[16], ou[16], oa[16];
+            for (int h2 = 0; h2 < 2; h2++) {
+              const int n2 = n + 16 * h2;
+              if (c != half * CPW || h2) dact_load(0, n2, row0);   // (the first load was issued early)
+              mbar_wait(ebar + 2 * ew, ephase[0]);
+              ephase[0] ^= 1;
+              // this row's 16 G and 16 U (bf16) from the SWIZZLE_32B staging rows (32 B each)
+              uint32_t gcur[8], ucur[8];
 #pragma unroll
-            for (int j = 0; j < 16; j++) {
-              float r2v[2][3];
-#pragma unroll
-              for (int q2 = 0; q2 < 2; q2++) {
-                const int i = 2 * j + q2;
-                const uint32_t gw = gcur[j], uw = ucur[j];
-                const float G = __uint_as_float(q2 ? (gw & 0xFFFF0000u) : (gw << 16));
-                const float U = __uint_as_float(q2 ? (uw & 0xFFFF0000u) : (uw << 16));
-                const float sg = sigmoid_f(G);
-                const float a = G * sg * U;
-                dwp = fmaf(v[i], a, dwp);
-                const float dA = wrow * v[i];
-                r2v[q2][0] = dA * U * sg * (1.f + G * (1.f - sg));
-                r2v[q2][1] = dA * G * sg;
-                r2v[q2][2] = wrow * a;
+              for (int cc = 0; cc < 2; cc++) {
+                const int off = lane * 32 + ((cc ^ ((lane >> 2) & 1)) << 4);
+                const uint4 gv = *reinterpret_cast<const uint4*>(buf + off);
+                const uint4 uv = *reinterpret_cast<const uint4*>(buf + 1024 + off);
+                gcur[4 * cc] = gv.x; gcur[4 * cc + 1] = gv.y; gcur[4 * cc + 2] = gv.z; gcur[4 * cc + 3] = gv.w;
+                ucur[4 * cc] = uv.x; ucur[4 * cc + 1] = uv.y; ucur[4 * cc + 2] = uv.z; ucur[4 * cc + 3] = uv.w;
               }
-              og[j] = pack_bf16(r2v[0][0], r2v[1][0]);
-              ou[j] = pack_bf16(r2v[0][1], r2v[1][1]);
-              oa[j] = pack_bf16(r2v[0][2], r2v[1][2]);
-            }
-            stage_bf16_row_packed(buf, lane, og);
-            stage_bf16_row_packed(buf + 2048, lane, ou);
-            stage_bf16_row_packed(buf + 4096, lane, oa);
-            fence_async_smem();
-            __syncwarp();
-            if (lane == 0) {
-              tma_store_2d(&tmO0, buf, n, row0);               // dG over G
-              tma_store_2d(&tmO0, buf + 2048, p.g + n, row0);  // dU over U
-              tma_store_2d(&tmO1, buf + 4096, n, row0);        // a_w
-              bulk_commit();
+              __syncwarp();
+              uint32_t og[8], ou[8], oa[8];
+#pragma unroll
+              for (int j = 0; j < 8; j++) {
+                float r2v[2][3];
+#pragma unroll
+                for (int q2 = 0; q2 < 2; q2++) {
+                  const int i = 16 * h2 + 2 * j + q2;
+                  const uint32_t gw = gcur[j], uw = ucur[j];
+                  const float G = __uint_as_float(q2 ? (gw & 0xFFFF0000u) : (gw << 16));
+                  const float U = __uint_as_float(q2 ? (uw & 0xFFFF0000u) : (uw << 16));
+                  const float sg = sigmoid_f(G);
+                  const float a = G * sg * U;
+                  dwp = fmaf(v[i], a, dwp);
+                  const float dA = wrow * v[i];
+                  r2v[q2][0] = dA * U * sg * (1.f + G * (1.f - sg));
+                  r2v[q2][1] = dA * G * sg;
+                  r2v[q2][2] = wrow * a;
+                }
+                og[j] = pack_bf16(r2v[0][0], r2v[1][0]);
+                ou[j] = pack_bf16(r2v[0][1], r2v[1][1]);
+                oa[j] = pack_bf16(r2v[0][2], r2v[1][2]);
+              }
+#pragma unroll
+              for (int cc = 0; cc < 2; cc++) {
+                const int off = lane * 32 + ((cc ^ ((lane >> 2) & 1)) << 4);
+                *reinterpret_cast<uint4*>(buf + off) = make_uint4(og[4 * cc], og[4 * cc + 1], og[4 * cc + 2], og[4 * cc + 3]);
+                *reinterpret_cast<uint4*>(buf + 1024 + off) =
+                    make_uint4(ou[4 * cc], ou[4 * cc + 1], ou[4 * cc + 2], ou[4 * cc + 3]);
+                *reinterpret_cast<uint4*>(buf + 2048 + off) =
+                    make_uint4(oa[4 * cc], oa[4 * cc + 1], oa[4 * cc + 2], oa[4 * cc + 3]);
+              }
+              fence_async_smem();
+              __syncwarp();
+              if (lane == 0) {
+                tma_store_2d(&tmO0, buf, n2, row0);               // dG over G
+                tma_store_2d(&tmO0, buf + 1024, p.g + n2, row0);  // dU over U
+                tma_store_2d(&tmO1, buf + 2048, n2, row0);        // a_w
+                bulk_commit();
+              }
             }
           }
         } else {
@@ -800,6 +842,11 @@ bool map2d_st(CUtensorMap* m, const void* base, uint64_t inner, uint64_t outer) 
   uint32_t b[2] = {32, 32};
   return make_map_t(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, CU_TENSOR_MAP_SWIZZLE_64B, base, 2, d, b);
 }
+bool map2d_st16(CUtensorMap* m, const void* base, uint64_t inner, uint64_t outer) {
+  uint64_t d[2] = {inner, outer};
+  uint32_t b[2] = {16, 32};
+  return make_map_t(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, CU_TENSOR_MAP_SWIZZLE_32B, base, 2, d, b);
+}
 bool map3d_f32(CUtensorMap* m, const void* base, uint64_t d0, uint64_t d1, uint64_t d2) {
   uint64_t d[3] = {d0, d1, d2};
   uint32_t b[3] = {32, 32, 1};
@@ -892,8 +939,8 @@ int launch(const GemmProblem<__nv_bfloat16>& gp, cudaStream_t st) {
       ok &= map2d(&mA, gp.DY, h, R, BK, BM);
       ok &= map3d(&mB0, gp.Wd, g, h, El, 64, BK);   // B(n,k) = W_down[e][k][n]
       mB1 = mB0;
-      ok &= map2d_st(&mO0, gp.GU, 2 * g, R);
-      ok &= map2d_st(&mO1, gp.A, g, R);
+      ok &= map2d_st16(&mO0, gp.GU, 2 * g, R);
+      ok &= map2d_st16(&mO1, gp.A, g, R);
       break;
     case GK_DX:
       p.N = gp.h; p.K = 2 * gp.g;
