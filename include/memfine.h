@@ -98,6 +98,8 @@ typedef struct {
                                     nsub; s'_max / c_theory are still reported per Eqs. 8-9 and
                                     predicted_peak_bytes is that exact workspace.  Evaluated on
                                     the host (device counts are copied, 4*EP*nsub*E bytes).    */
+    int32_t  pass;               /* MEMFINE_MODEL_IMPL only: size for MEMFINE_BWD (default, the
+                                    larger live set) or MEMFINE_FWD (a forward-only C)          */
 } memfine_budget;
 
 /* Result of memfine_plan. */

@@ -42,7 +42,7 @@ class Budget(C.Structure):
     _fields_ = [("gpu_capacity_bytes", C.c_uint64), ("alpha", C.c_double), ("static_bytes", C.c_uint64),
                 ("other_act_bytes", C.c_uint64), ("m_g", C.c_uint32), ("tp", C.c_uint32), ("cp", C.c_uint32),
                 ("micro_batch", C.c_uint32), ("bins", C.POINTER(C.c_int32)), ("nbins", C.c_int32),
-                ("rule", C.c_int32), ("model", C.c_int32)]
+                ("rule", C.c_int32), ("model", C.c_int32), ("pass_", C.c_int32)]
 
 
 class PlanInfo(C.Structure):
@@ -128,10 +128,10 @@ def check(status: int, where: str) -> None:
 
 def make_budget(gpu_capacity_bytes: int, alpha: float = 1.0, static_bytes: int = 0, other_act_bytes: int = 0,
                 m_g: int = 1, tp: int = 1, cp: int = 1, micro_batch: int = 1, bins=(1, 2, 4, 8),
-                rule: int = RULE_EQ9, model: int = MODEL_PAPER):
+                rule: int = RULE_EQ9, model: int = MODEL_PAPER, pass_: int = BWD):
     arr = (C.c_int32 * len(bins))(*bins) if bins is not None else None
     b = Budget(int(gpu_capacity_bytes), float(alpha), int(static_bytes), int(other_act_bytes), m_g, tp, cp,
                micro_batch, C.cast(arr, C.POINTER(C.c_int32)) if arr is not None else None,
-               len(bins) if bins is not None else 0, rule, model)
+               len(bins) if bins is not None else 0, rule, model, pass_)
     b._keep = arr  # keep the bins array alive
     return b

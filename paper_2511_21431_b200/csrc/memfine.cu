@@ -259,6 +259,7 @@ int budget_to_params(const memfine_dims* d, const memfine_budget* b, int nsub, P
   if (b->m_g < 1 || b->tp < 1 || b->cp < 1 || b->micro_batch < 1) return MEMFINE_ERR_INVALID_ARG;
   if (b->rule != MEMFINE_RULE_EQ9 && b->rule != MEMFINE_RULE_EXACT) return MEMFINE_ERR_INVALID_ARG;
   if (b->model != MEMFINE_MODEL_PAPER && b->model != MEMFINE_MODEL_IMPL) return MEMFINE_ERR_INVALID_ARG;
+  if (b->pass != MEMFINE_FWD && b->pass != MEMFINE_BWD) return MEMFINE_ERR_INVALID_ARG;
   long double B = (long double)b->alpha * (long double)b->gpu_capacity_bytes;
   if (B >= 18446744073709551615.0L) B = 18446744073709551615.0L;
   p->budget = (uint64_t)floorl(B);
@@ -1195,7 +1196,7 @@ memfine_status plan_impl(const int32_t* counts_host, int32_t nsub, const memfine
     for (int r = 0; r < dims->ep_size; r++) {
       d.ep_rank = r;
       uint64_t w = 0;
-      memfine_workspace_bytes(counts_host, nsub, &d, Cb, MEMFINE_BWD, &w);
+      memfine_workspace_bytes(counts_host, nsub, &d, Cb, budget->pass == MEMFINE_FWD ? MEMFINE_FWD : MEMFINE_BWD, &w);
       mx = std::max(mx, w);
     }
     return mx;
