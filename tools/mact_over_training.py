@@ -23,7 +23,6 @@ import time
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 
-import numpy as np  # noqa: E402
 import torch  # noqa: E402
 
 import synth  # noqa: E402
@@ -40,7 +39,7 @@ def main():
     ap.add_argument("--layers", type=int, default=8)
     ap.add_argument("--iters", type=int, default=12)
     ap.add_argument("--ep", type=int, default=4)
-    ap.add_argument("--budget-mb", type=float, default=700.0, help="per-GPU activation budget")
+    ap.add_argument("--budget-mb", type=float, default=1300.0, help="per-GPU activation budget")
     args = ap.parse_args()
     EP, L, I = args.ep, args.layers, args.iters
     T, h, g, E, k = 4096, 2048, 4096, 16, 4
@@ -122,7 +121,6 @@ def main():
     heat = [[cells[(i, l)]["C_mact"] for l in range(L)] for i in range(I)]
     summ = {}
     for name in ("method1_c1", "method2_c8", "method3_mact"):
-        ok = [c for c in cells.values() if name != "method1_c1" or c["feasible_C1"]]
         summ[name] = {"total_ms_all_cells": sum(c[name + "_ms"] for c in cells.values()),
                       "cells_over_budget": sum(1 for c in cells.values() if name == "method1_c1"
                                                and not c["feasible_C1"]),
