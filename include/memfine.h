@@ -258,6 +258,21 @@ memfine_status memfine_moe_bwd(memfine_handle_t h, const void* dy, const void* x
                                float* dscore, int32_t accumulate_dw, void* ws, uint64_t ws_bytes,
                                void* stream);
 
+/* N3: the router step before the layer (Table 2 rows 9-10).
+ *   logits = x W_r^T (fp32 accumulation), ids = the k largest logits (ties: lower expert id),
+ *   scores = softmax over the k selected logits (the renormalised top-k convention).
+ *   x dev [T][h], w_router dev [E][h] (dims.dtype, replicated on every EP rank), ids dev int32
+ *   [T][k], scores dev fp32 [T][k], logits dev fp32 [T][E] (nullable: library scratch). */
+memfine_status memfine_router_fwd(memfine_handle_t h, const void* x, const void* w_router, int32_t* ids,
+                                  float* scores, float* logits, void* stream);
+/* Router backward from the layer's d_score (memfine_moe_bwd's dscore):
+ *   d_logit = s (ds - <s, ds>) on the selected slots (0 elsewhere);
+ *   dx (dev [T][h]) = d_logits W_r, added to dx when accumulate_dx (the router shares the layer input);
+ *   dw_router (dev fp32 [E][h]) = d_logits^T x, accumulated when accumulate_dw. */
+memfine_status memfine_router_bwd(memfine_handle_t h, const void* x, const void* w_router, const int32_t* ids,
+                                  const float* scores, const float* dscore, void* dx, int32_t accumulate_dx,
+                                  float* dw_router, int32_t accumulate_dw, void* stream);
+
 /* Synchronise `stream` and return (and clear) any device-latched error. */
 memfine_status memfine_sync(memfine_handle_t h, void* stream);
 

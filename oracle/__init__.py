@@ -231,3 +231,28 @@ def moe_tokens(d: Dims, toks, dy, x, ids, w, wg, wu, wd):
     lib().oracle_moe_tokens(C.byref(d.c()), C.c_int64(n), _p(toks), _p(dy), _p(x), _p(ids), _p(w),
                             _p(wg), _p(wu), _p(wd), _p(y), _p(dx), _p(ds))
     return y, dx, ds
+
+
+def router_forward(d: Dims, x, wr):
+    """Router: logits = x W_r^T, top-k (ties -> lower id), softmax over the k selected."""
+    x, wr = _wt(x, d.in_dtype), _wt(wr, d.in_dtype)
+    n = x.shape[0]
+    logits = np.zeros((n, d.E))
+    ids = np.zeros((n, d.k), np.int32)
+    scores = np.zeros((n, d.k))
+    lib().oracle_router_forward(C.byref(d.c()), C.c_int64(n), _p(x), _p(wr), _p(logits), _p(ids), _p(scores))
+    return logits, ids, scores
+
+
+def router_backward(d: Dims, x, wr, ids, scores, dscore):
+    """d_logits (softmax Jacobian on the selected slots), dx = d_logits W_r, dW_r = d_logits^T x."""
+    x, wr = _wt(x, d.in_dtype), _wt(wr, d.in_dtype)
+    n = x.shape[0]
+    ids = np.ascontiguousarray(ids, np.int32)
+    scores = np.ascontiguousarray(scores, np.float64)
+    dscore = np.ascontiguousarray(dscore, np.float64)
+    dx = np.zeros((n, d.h))
+    dwr = np.zeros((d.E, d.h))
+    lib().oracle_router_backward(C.byref(d.c()), C.c_int64(n), _p(x), _p(wr), _p(ids), _p(scores), _p(dscore),
+                                 _p(dx), _p(dwr))
+    return dx, dwr

@@ -649,6 +649,71 @@ void oracle_moe_tokens(const oracle_dims* d, int64_t ntok, const int64_t* toks,
     }
 }
 
+/* ------------------------------------------------------------------------- */
+/* Router (Table 2 rows 9-10: the router stores its input and  */
+/* its e_n logits).  logits = x W_r^T; the k largest logits (ties: lower expert id first);        */
+/* scores = softmax over the k selected logits (the renormalised top-k convention).               */
+/* x [ntok][h] and W_r [E][h] as in_dtype; logits, scores double; ids int32.                     */
+/* ------------------------------------------------------------------------- */
+void oracle_router_forward(const oracle_dims* d, int64_t ntok, const void* x, const void* wr,
+                           double* logits, int32_t* ids, double* scores)
+{
+    int64_t h = d->h, E = d->E, k = d->k;
+    #pragma omp parallel for schedule(dynamic, 16)
+    for (int64_t t = 0; t < ntok; t++) {
+        double* lg = logits + t * E;
+        for (int64_t e = 0; e < E; e++) {
+            double s = 0.0;
+            for (int64_t c = 0; c < h; c++) s += load(x, t * h + c, d->in_dtype) * load(wr, e * h + c, d->in_dtype);
+            lg[e] = s;
+        }
+        /* selection: k passes of argmax over the not-yet-chosen experts */
+        for (int64_t j = 0; j < k; j++) {
+            int64_t best = -1;
+            for (int64_t e = 0; e < E; e++) {
+                int taken = 0;
+                for (int64_t q = 0; q < j; q++) if (ids[t * k + q] == e) taken = 1;
+                if (taken) continue;
+                if (best < 0 || lg[e] > lg[best]) best = e;
+            }
+            ids[t * k + j] = (int32_t)best;
+        }
+        double mx = lg[ids[t * k]], z = 0.0;
+        for (int64_t j = 0; j < k; j++) z += exp(lg[ids[t * k + j]] - mx);
+        for (int64_t j = 0; j < k; j++) scores[t * k + j] = exp(lg[ids[t * k + j]] - mx) / z;
+    }
+}
+
+/* Router backward given d_score (the MoE layer's dL/dw) for the selected slots:
+ *   d_logit[e_j] = s_j (ds_j - sum_q s_q ds_q) for the selected e_j, 0 elsewhere (softmax Jacobian);
+ *   dx = d_logits W_r,  dW_r = d_logits^T x. */
+void oracle_router_backward(const oracle_dims* d, int64_t ntok, const void* x, const void* wr, const int32_t* ids,
+                            const double* scores, const double* dscore, double* dx, double* dwr)
+{
+    int64_t h = d->h, E = d->E, k = d->k;
+    double* dl = (double*)calloc((size_t)(ntok > 0 ? ntok : 1) * E, sizeof(double));
+    for (int64_t t = 0; t < ntok; t++) {
+        double dot = 0.0;
+        for (int64_t j = 0; j < k; j++) dot += scores[t * k + j] * dscore[t * k + j];
+        for (int64_t j = 0; j < k; j++) dl[t * E + ids[t * k + j]] += scores[t * k + j] * (dscore[t * k + j] - dot);
+    }
+    #pragma omp parallel for schedule(static)
+    for (int64_t t = 0; t < ntok; t++)
+        for (int64_t c = 0; c < h; c++) {
+            double s = 0.0;
+            for (int64_t e = 0; e < E; e++) s += dl[t * E + e] * load(wr, e * h + c, d->in_dtype);
+            dx[t * h + c] = s;
+        }
+    #pragma omp parallel for schedule(static)
+    for (int64_t e = 0; e < E; e++)
+        for (int64_t c = 0; c < h; c++) {
+            double s = 0.0;
+            for (int64_t t = 0; t < ntok; t++) s += dl[t * E + e] * load(x, t * h + c, d->in_dtype);
+            dwr[e * h + c] = s;
+        }
+    free(dl);
+}
+
 int32_t oracle_version(void) { return 1; }
 
 #ifdef _OPENMP

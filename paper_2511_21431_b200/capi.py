@@ -19,7 +19,7 @@ FWD, BWD = 0, 1
 # Every symbol include/memfine.h declares (checked by tests/test_abi.py).
 SYMBOLS = ("memfine_abi_version", "memfine_status_str", "memfine_nccl_unique_id", "memfine_create",
            "memfine_destroy", "memfine_local_group_create", "memfine_local_group_destroy", "memfine_create_local", "memfine_set_ep_transport", "memfine_register_workspace", "memfine_route_counts", "memfine_plan", "memfine_workspace_bytes", "memfine_a2a_plan",
-           "memfine_moe_fwd", "memfine_moe_bwd", "memfine_sync", "memfine_last_stats",
+           "memfine_moe_fwd", "memfine_moe_bwd", "memfine_router_fwd", "memfine_router_bwd", "memfine_sync", "memfine_last_stats",
            "memfine_profile_enable", "memfine_profile_read", "memfine_set_debug", "memfine_debug_perm")
 
 PROF_SLOTS = ("gemm_gateup_swiglu", "gemm_down", "gemm_dact_epilogue", "gemm_dx", "gemm_wgrad_down",
@@ -105,6 +105,8 @@ def lib():
         L.memfine_a2a_plan.argtypes = [vp, i32, C.POINTER(Dims), i32, i32, vp, vp, vp, vp]
         L.memfine_moe_fwd.argtypes = [vp, vp, vp, vp, vp, vp, vp, i32, vp, vp, u64, vp]
         L.memfine_moe_bwd.argtypes = [vp, vp, vp, vp, vp, vp, vp, vp, i32, vp, vp, vp, vp, vp, i32, vp, u64, vp]
+        L.memfine_router_fwd.argtypes = [vp, vp, vp, vp, vp, vp, vp]
+        L.memfine_router_bwd.argtypes = [vp, vp, vp, vp, vp, vp, vp, i32, vp, i32, vp]
         L.memfine_sync.argtypes = [vp, vp]
         L.memfine_last_stats.argtypes = [vp, C.POINTER(Stats)]
         L.memfine_profile_enable.argtypes = [vp, i32]

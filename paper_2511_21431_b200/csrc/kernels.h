@@ -80,6 +80,16 @@ void launch_p2p_row_addr(const int* seg, const int* recv_cnt, int El, int EP, co
 void launch_p2p_push_dw(const float* dw_row, const uint64_t* row_addr_w, const int* info, int64_t rows_cap,
                         cudaStream_t st);
 
+// ---------------------------------------------------------------- router (N3)
+template <typename T>
+void launch_router_fwd(const T* x, const T* wr, int64_t ntok, int E, int h, int k, float* logits, int32_t* ids,
+                       float* scores, cudaStream_t st);
+// m: a counting sort of ids by expert (dispatch_hist/scan/index with ep_size 1): seg, recv_cnt, src_of
+template <typename T>
+void launch_router_bwd(const T* x, const T* wr, const int32_t* ids, const float* scores, const float* dscore,
+                       int64_t ntok, int E, int h, int k, float* dlog, T* dx, int acc_dx, float* dwr, int acc_dw,
+                       const ChunkMeta& m, cudaStream_t st);
+
 // ---------------------------------------------------------------- MACT tuner (A3)
 struct PlanParams {
   int32_t EP, nsub, E, h, g, D_t, nbins, rule;

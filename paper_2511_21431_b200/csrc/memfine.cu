@@ -53,6 +53,9 @@ struct memfine_handle_s {
   std::vector<char*> peer_ws;      // [EP] (own entry = reg_ws)
   std::vector<void*> ipc_bases;    // opened peer allocation bases (to close)
   int* barrier_d = nullptr;
+  // router scratch (lazily allocated): logits, d_logits, counting sort of ids by expert
+  char* router_scratch = nullptr;
+  size_t router_bytes = 0;
   int device = 0;
   int num_sms = 148;
   int* status_h = nullptr;     // pinned, mapped: device-latched error word
@@ -673,6 +676,7 @@ memfine_status ep_run_p2p(memfine_handle_s* h, int pass, const T* dy, const T* x
   const size_t per = 4 * (size_t)E + 1;
   if (h->tab_cap < per * C) {
     if (h->tab_h) cudaFreeHost(h->tab_h);
+  if (h->router_scratch) cudaFree(h->router_scratch);
   for (void* b : h->ipc_bases) cudaIpcCloseMemHandle(b);
   if (h->barrier_d) cudaFree(h->barrier_d);
     h->tab_h = nullptr;
@@ -1074,6 +1078,7 @@ memfine_status memfine_register_workspace(memfine_handle_t h, void* ws, uint64_t
 memfine_status memfine_destroy(memfine_handle_t h) {
   if (!h) return MEMFINE_ERR_INVALID_ARG;
   if (h->tab_h) cudaFreeHost(h->tab_h);
+  if (h->router_scratch) cudaFree(h->router_scratch);
   for (void* b : h->ipc_bases) cudaIpcCloseMemHandle(b);
   if (h->barrier_d) cudaFree(h->barrier_d);
   if (h->comm.comm) nccl_comm_destroy(&h->comm);
@@ -1318,6 +1323,99 @@ memfine_status memfine_moe_bwd(memfine_handle_t h, const void* dy, const void* x
                                   st);
   return bwd_ep1<float>(h, (const float*)dy, (const float*)x, ids, w, w_gate, w_up, w_down, C, (float*)dx, dw_gate,
                         dw_up, dw_down, dscore, accumulate_dw, ws, ws_bytes, st);
+}
+
+// ---------------------------------------------------------------- router (N3)
+namespace {
+struct RouterScratch {
+  float* logits;
+  float* dlog;
+  ChunkMeta m;
+  int64_t rows_cap;
+};
+memfine_status router_scratch(memfine_handle_s* h, RouterScratch* rs) {
+  const memfine_dims& d = h->d;
+  const int E = d.num_experts, k = d.topk;
+  const int64_t T = d.tokens, NB = std::max<int64_t>(1, ceil_div64(T, kTokPerBlk));
+  const int64_t rows_cap = round_up64(T * k + (int64_t)E * (kRowAlign - 1), kRowAlign);
+  Bump b(nullptr);
+  b.take<float>((uint64_t)T * E);
+  b.take<float>((uint64_t)T * k);
+  b.take<int>((uint64_t)NB * E);
+  for (int i = 0; i < 3; i++) b.take<int>(E + 1);
+  b.take<int>(E + 1);
+  b.take<int>(kInfoWords);
+  b.take<int>((uint64_t)T * k);
+  b.take<int>((uint64_t)rows_cap);
+  if (b.off > h->router_bytes) {
+    if (h->router_scratch) cudaFree(h->router_scratch);
+    h->router_scratch = nullptr;
+    h->router_bytes = 0;
+    MF_CUDA_OK(cudaMalloc((void**)&h->router_scratch, b.off));
+    h->router_bytes = b.off;
+  }
+  Bump c(h->router_scratch);
+  rs->logits = c.take<float>((uint64_t)T * E);
+  rs->dlog = c.take<float>((uint64_t)T * k);
+  rs->m = ChunkMeta{};
+  rs->m.blk_cnt = c.take<int>((uint64_t)NB * E);
+  rs->m.exp_cnt = c.take<int>(E + 1);
+  rs->m.recv_cnt = c.take<int>(E + 1);
+  rs->m.seg = c.take<int>(E + 1);
+  rs->m.pseg = c.take<int>(E + 1);
+  rs->m.info = c.take<int>(kInfoWords);
+  rs->m.dest_of = c.take<int>((uint64_t)T * k);
+  rs->m.src_of = c.take<int>((uint64_t)rows_cap);
+  rs->rows_cap = rows_cap;
+  return MEMFINE_OK;
+}
+}  // namespace
+
+memfine_status memfine_router_fwd(memfine_handle_t h, const void* x, const void* w_router, int32_t* ids,
+                                  float* scores, float* logits, void* stream) {
+  if (!h || !w_router || (h->d.tokens > 0 && (!x || !ids || !scores))) return MEMFINE_ERR_INVALID_ARG;
+  const memfine_dims& d = h->d;
+  cudaStream_t st = (cudaStream_t)stream;
+  RouterScratch rs;
+  if (int rc = router_scratch(h, &rs)) return (memfine_status)rc;
+  float* lg = logits ? logits : rs.logits;
+  if (d.dtype == MEMFINE_BF16)
+    launch_router_fwd<__nv_bfloat16>((const __nv_bfloat16*)x, (const __nv_bfloat16*)w_router, d.tokens,
+                                     d.num_experts, d.hidden, d.topk, lg, ids, scores, st);
+  else
+    launch_router_fwd<float>((const float*)x, (const float*)w_router, d.tokens, d.num_experts, d.hidden, d.topk, lg,
+                             ids, scores, st);
+  return latch_cuda(h);
+}
+
+memfine_status memfine_router_bwd(memfine_handle_t h, const void* x, const void* w_router, const int32_t* ids,
+                                  const float* scores, const float* dscore, void* dx, int32_t accumulate_dx,
+                                  float* dw_router, int32_t accumulate_dw, void* stream) {
+  if (!h || !w_router || !dw_router || (h->d.tokens > 0 && (!x || !ids || !scores || !dscore || !dx)))
+    return MEMFINE_ERR_INVALID_ARG;
+  const memfine_dims& d = h->d;
+  cudaStream_t st = (cudaStream_t)stream;
+  RouterScratch rs;
+  if (int rc = router_scratch(h, &rs)) return (memfine_status)rc;
+  const int E = d.num_experts, k = d.topk;
+  // counting sort of the copies by expert (stable): segment e = rows [seg[e], seg[e] + cnt[e])
+  int NB = (int)ceil_div64(d.tokens, kTokPerBlk);
+  if (NB) {
+    launch_dispatch_hist(ids, 0, d.tokens, k, E, rs.m, h->status_d, st);
+    launch_dispatch_scan(NB, E, E, 1, rs.rows_cap, rs.m, nullptr, nullptr, 0, st);
+    launch_dispatch_index(ids, nullptr, 0, d.tokens, k, E, rs.m, rs.m.src_of, nullptr, st);
+  } else {
+    MF_CUDA_OK(cudaMemsetAsync(rs.m.seg, 0, sizeof(int) * (E + 1), st));
+    MF_CUDA_OK(cudaMemsetAsync(rs.m.recv_cnt, 0, sizeof(int) * (E + 1), st));
+  }
+  if (d.dtype == MEMFINE_BF16)
+    launch_router_bwd<__nv_bfloat16>((const __nv_bfloat16*)x, (const __nv_bfloat16*)w_router, ids, scores, dscore,
+                                     d.tokens, E, d.hidden, k, rs.dlog, (__nv_bfloat16*)dx, accumulate_dx, dw_router,
+                                     accumulate_dw, rs.m, st);
+  else
+    launch_router_bwd<float>((const float*)x, (const float*)w_router, ids, scores, dscore, d.tokens, E, d.hidden, k,
+                             rs.dlog, (float*)dx, accumulate_dx, dw_router, accumulate_dw, rs.m, st);
+  return latch_cuda(h);
 }
 
 memfine_status memfine_sync(memfine_handle_t h, void* stream) {

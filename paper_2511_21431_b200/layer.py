@@ -166,6 +166,26 @@ class MemFine:
                    "memfine_moe_bwd")
         return dx, dw_gate, dw_up, dw_down, dscore
 
+    # ------------------------------------------------------------------ router (N3)
+    def router_fwd(self, x, w_router, logits=None, stream=None):
+        T, k = x.shape[0], self.dims.topk
+        ids = torch.empty((T, k), dtype=torch.int32, device=x.device)
+        scores = torch.empty((T, k), dtype=torch.float32, device=x.device)
+        capi.check(capi.lib().memfine_router_fwd(self.h, _ptr(x), _ptr(w_router), _ptr(ids), _ptr(scores),
+                                                 _ptr(logits), _stream(stream)), "memfine_router_fwd")
+        return ids, scores
+
+    def router_bwd(self, x, w_router, ids, scores, dscore, dx=None, accumulate_dx=False, dw_router=None,
+                   accumulate_dw=False, stream=None):
+        if dx is None:
+            dx = torch.empty_like(x)
+        if dw_router is None:
+            dw_router = torch.empty(w_router.shape, dtype=torch.float32, device=x.device)
+        capi.check(capi.lib().memfine_router_bwd(self.h, _ptr(x), _ptr(w_router), _ptr(ids), _ptr(scores),
+                                                 _ptr(dscore), _ptr(dx), int(bool(accumulate_dx)), _ptr(dw_router),
+                                                 int(bool(accumulate_dw)), _stream(stream)), "memfine_router_bwd")
+        return dx, dw_router
+
     def sync(self, stream=None) -> int:
         return int(capi.lib().memfine_sync(self.h, _stream(stream)))
 

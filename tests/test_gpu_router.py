@@ -1,0 +1,76 @@
+"""Router step on the GPU vs the oracle (run with -m gpu).
+
+Top-k is an integer decision taken on floating-point logits: the GPU's selected set must be a valid
+top-k of the oracle's fp64 logits up to the fp32 accumulation error (the unique part), scores are
+compared with the oracle's softmax over the GPU-selected experts, and the backward is compared on
+the GPU's own ids / scores."""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import synth
+from paper_2511_21431_b200 import layer
+from tests.harness import rel_err, tol
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _need_gpu():
+    if not torch.cuda.is_available():
+        pytest.skip("needs a CUDA device")
+
+
+def _np(t, dtype):
+    return t.contiguous().view(torch.int16).numpy().view(np.uint16) if dtype == torch.bfloat16 else \
+        t.contiguous().numpy().astype(np.float32)
+
+
+@pytest.mark.parametrize("dtype", [torch.bfloat16, torch.float32])
+@pytest.mark.parametrize("T,h,E,k", [(300, 64, 8, 2), (1000, 512, 256, 8), (77, 128, 64, 6)])
+def test_router_fwd_bwd(dtype, T, h, E, k):
+    dev = "cuda:0"
+    x = synth.make_x(T, h, rank=3, dtype=dtype)
+    gen = torch.Generator().manual_seed(11)
+    wr = (torch.randn(E, h, generator=gen) / h ** 0.5).to(dtype)
+    mf = layer.MemFine(T, h, 64, E, k, dtype=dtype)
+    logits = torch.empty((T, E), dtype=torch.float32, device=dev)
+    xd, wd = x.to(dev), wr.to(dev)
+    ids, scores = mf.router_fwd(xd, wd, logits=logits)
+    assert mf.sync() == 0
+    d = oracle.Dims(T=T, h=h, g=1, E=E, k=k, in_dtype="bf16" if dtype == torch.bfloat16 else "f32")
+    ref_logits, ref_ids, ref_scores = oracle.router_forward(d, _np(x, dtype), _np(wr, dtype))
+    assert rel_err(logits.cpu().numpy(), ref_logits) <= 1e-5
+    g_ids = ids.cpu().numpy()
+    # the unique part: a valid top-k of the exact logits (up to the fp32 accumulation error)
+    eps = 1e-5 * np.abs(ref_logits).max()
+    for t in range(T):
+        sel = g_ids[t]
+        assert len(set(sel.tolist())) == k and sel.min() >= 0 and sel.max() < E
+        rest = np.setdiff1d(np.arange(E), sel)
+        if len(rest):
+            assert ref_logits[t, sel].min() >= ref_logits[t, rest].max() - eps
+    assert (g_ids == ref_ids).mean() > 0.99
+    # scores: softmax over the GPU-selected experts of the exact logits
+    sl = np.take_along_axis(ref_logits, g_ids.astype(np.int64), 1)
+    sl = np.exp(sl - sl.max(1, keepdims=True))
+    sref = sl / sl.sum(1, keepdims=True)
+    assert rel_err(scores.cpu().numpy(), sref) <= 1e-5
+    # backward on the GPU's ids / scores
+    ds = torch.from_numpy(np.random.default_rng(2).standard_normal((T, k)).astype(np.float32))
+    dx0 = synth.make_dy(T, h, rank=4, dtype=dtype).to(dev)
+    dwr0 = torch.randn(E, h, generator=gen).to(dev)
+    dx, dwr = mf.router_bwd(xd, wd, ids, scores, ds.to(dev), dx=dx0.clone(), accumulate_dx=True,
+                            dw_router=dwr0.clone(), accumulate_dw=True)
+    assert mf.sync() == 0
+    rdx, rdw = oracle.router_backward(d, _np(x, dtype), _np(wr, dtype), g_ids, scores.cpu().numpy().astype(np.float64),
+                                      ds.numpy().astype(np.float64))
+    t_ = tol(dtype)
+    assert rel_err(dx.float().cpu().numpy() - dx0.float().cpu().numpy(), rdx) <= max(t_, 1e-2 if dtype == torch.bfloat16 else 0)
+    assert rel_err(dwr.cpu().numpy() - dwr0.cpu().numpy(), rdw) <= t_
+    # overwrite mode
+    dx2, dwr2 = mf.router_bwd(xd, wd, ids, scores, ds.to(dev))
+    assert mf.sync() == 0
+    assert rel_err(dwr2.cpu().numpy(), rdw) <= t_
+    assert rel_err(dx2.float().cpu().numpy(), rdx) <= t_

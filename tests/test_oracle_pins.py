@@ -402,3 +402,59 @@ def test_meter_peak_scales_as_one_over_c(oracle_lib):
         assert int(pkb[0]) == int(pk[0])
     assert all(peaks[i + 1] <= peaks[i] for i in range(7))
     assert peaks[3] * 4 == peaks[0]
+
+
+# ----------------------------------------------------------------------------- router (N3)
+def test_router_matches_torch_topk_softmax_and_autograd(oracle_lib):
+    """Router forward == torch.topk + softmax over the selected logits; backward == torch.autograd
+    of that composition (library routines), fp64, with an upstream d_score."""
+    rng = np.random.default_rng(31)
+    n, h, E, k = 23, 16, 12, 3
+    x = rng.standard_normal((n, h))
+    wr = rng.standard_normal((E, h))
+    d = Dims(T=n, h=h, g=1, E=E, k=k, in_dtype="f64")
+    logits, ids, scores = oracle.router_forward(d, x, wr)
+    X = torch.tensor(x, requires_grad=True)
+    W = torch.tensor(wr, requires_grad=True)
+    L = X @ W.T
+    top = torch.topk(L, k, dim=1)
+    np.testing.assert_allclose(logits, L.detach().numpy(), rtol=1e-13, atol=1e-13)
+    np.testing.assert_array_equal(ids, top.indices.numpy())
+    S = torch.softmax(top.values, dim=1)
+    np.testing.assert_allclose(scores, S.detach().numpy(), rtol=1e-13, atol=1e-14)
+    ds = rng.standard_normal((n, k))
+    S.backward(torch.tensor(ds))
+    dx, dwr = oracle.router_backward(d, x, wr, ids, scores, ds)
+    np.testing.assert_allclose(dx, X.grad.numpy(), rtol=1e-11, atol=1e-12)
+    np.testing.assert_allclose(dwr, W.grad.numpy(), rtol=1e-11, atol=1e-12)
+
+
+def test_router_ties_and_finite_differences(oracle_lib):
+    """Ties resolve to the lower expert id; the backward matches central differences of
+    sum(ds * scores) away from ties (fp64, step 1e-6)."""
+    d = Dims(T=1, h=2, g=1, E=4, k=2, in_dtype="f64")
+    x = np.array([[1.0, 0.0]])
+    wr = np.array([[1.0, 0.0], [2.0, 0.0], [2.0, 0.0], [0.5, 0.0]])   # logits 1, 2, 2, 0.5
+    _, ids, sc = oracle.router_forward(d, x, wr)
+    assert ids.tolist() == [[1, 2]] and np.allclose(sc, 0.5)
+    rng = np.random.default_rng(5)
+    n, h, E, k = 6, 5, 7, 3
+    x = rng.standard_normal((n, h))
+    wr = rng.standard_normal((E, h))
+    ds = rng.standard_normal((n, k))
+    d = Dims(T=n, h=h, g=1, E=E, k=k, in_dtype="f64")
+    _, ids, sc = oracle.router_forward(d, x, wr)
+    dx, dwr = oracle.router_backward(d, x, wr, ids, sc, ds)
+
+    def f(x_, w_):
+        _, i2, s2 = oracle.router_forward(d, x_, w_)
+        assert np.array_equal(i2, ids)
+        return float((s2 * ds).sum())
+    eps = 1e-6
+    for arr, an in ((x, dx), (wr, dwr)):
+        for idx in list(np.ndindex(arr.shape))[:15]:
+            ap, am = arr.copy(), arr.copy()
+            ap[idx] += eps
+            am[idx] -= eps
+            num = (f(ap, wr) - f(am, wr)) / (2 * eps) if arr is x else (f(x, ap) - f(x, am)) / (2 * eps)
+            assert abs(num - an[idx]) <= 1e-6 * max(1.0, abs(an[idx]))
