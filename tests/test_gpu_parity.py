@@ -182,3 +182,42 @@ def test_many_tiles_per_cta(C):
     p = make_problem(8192, 256, 512, 4, 2, zipf_s=1.2, seed=6)
     run = GpuRun(p)
     _check_all(p, run, C, oracle_fwd_bwd(p, C))
+
+
+def test_cuda_graph_capture_replays_identically():
+    """At EP=1 memfine_moe_fwd / memfine_moe_bwd do no host synchronisation, so a whole fwd+bwd
+    step can be captured into a CUDA graph and replayed; the replay is bit-identical to eager, except
+    d_score, whose per-row partial dots over the N-tiles are added with atomics (order not fixed)."""
+    p = make_problem(1000, 256, 384, 8, 2, zipf_s=1.2, seed=21)
+    run = GpuRun(p)
+    C = 2
+    wsb = max(layer.workspace_bytes(run.counts(C).cpu(), run.mf.dims, C, capi.FWD),
+              layer.workspace_bytes(run.counts(C).cpu(), run.mf.dims, C, capi.BWD))
+    ws = torch.empty(wsb, dtype=torch.uint8, device=run.dev)
+    f32 = dict(dtype=torch.float32, device=run.dev)
+    y, dx = torch.empty_like(run.x), torch.empty_like(run.x)
+    g3 = [torch.empty(t.shape, **f32) for t in (run.wg, run.wu, run.wd)]
+    ds = torch.empty(run.w.shape, **f32)
+
+    def step():
+        run.mf.moe_fwd(run.x, run.ids, run.w, run.wg, run.wu, run.wd, C, ws, y=y)
+        run.mf.moe_bwd(run.dy, run.x, run.ids, run.w, run.wg, run.wu, run.wd, C, ws, dx=dx, dw_gate=g3[0],
+                       dw_up=g3[1], dw_down=g3[2], dscore=ds)
+
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s):
+        step()                      # warm-up: kernel attributes / modules loaded outside capture
+        torch.cuda.synchronize()
+        ref = [t.clone() for t in (y, dx, *g3, ds)]
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph, stream=s):
+            step()
+    for t in (y, dx, *g3, ds):
+        t.zero_()
+    graph.replay()
+    torch.cuda.synchronize()
+    assert run.mf.sync() == 0
+    for a, b in zip((y, dx, *g3), ref[:5]):
+        assert torch.equal(a, b)
+    assert (ds - ref[5]).abs().max().item() <= 1e-5 * ref[5].abs().max().item()
