@@ -75,6 +75,13 @@ def lib():
         _lib.oracle_moe_backward.restype = C.c_int32
         _lib.oracle_moe_fcda_forward.restype = C.c_int32
         _lib.oracle_moe_fcda_backward.restype = C.c_int32
+        _lib.oracle_e4m3_decode.restype = C.c_double
+        _lib.oracle_e4m3_decode.argtypes = [C.c_uint8]
+        _lib.oracle_e4m3_encode.restype = C.c_uint8
+        _lib.oracle_e4m3_encode.argtypes = [C.c_double]
+        _lib.oracle_mx_scale_exp.restype = C.c_int32
+        _lib.oracle_mx_scale_exp.argtypes = [C.c_double]
+        _lib.oracle_moe_mx.restype = C.c_int32
     return _lib
 
 
@@ -256,3 +263,64 @@ def router_backward(d: Dims, x, wr, ids, scores, dscore):
     lib().oracle_router_backward(C.byref(d.c()), C.c_int64(n), _p(x), _p(wr), _p(ids), _p(scores), _p(dscore),
                                  _p(dx), _p(dwr))
     return dx, dwr
+
+
+# ---------------------------------------------------------------- MXFP8 variant (reading R28)
+def e4m3_decode(code: int) -> float:
+    return float(lib().oracle_e4m3_decode(code))
+
+
+def e4m3_encode(v: float) -> int:
+    """Round-to-nearest-even onto the FP8 E4M3 grid, saturating at +-448."""
+    return int(lib().oracle_e4m3_encode(float(v)))
+
+
+def mx_scale_exp(amax: float) -> int:
+    """Smallest E with amax <= 448 * 2^E (E = 0 for amax = 0), clamped to [-127, 127]."""
+    return int(lib().oracle_mx_scale_exp(float(amax)))
+
+
+def mx_quantize(v, in_dtype: str = "f32"):
+    """Blocks of 32 consecutive values of v (flattened): (E4M3 codes uint8 [n], scale codes E+127 uint8 [n/32])."""
+    v = _wt(v, in_dtype)
+    n = v.size
+    assert n % 32 == 0
+    codes = np.zeros(n, np.uint8)
+    scales = np.zeros(n // 32, np.uint8)
+    lib().oracle_mx_quantize(_p(v), C.c_int32({"f32": 0, "bf16": 1, "f64": 2}[in_dtype]), C.c_int64(n),
+                             _p(codes), _p(scales))
+    return codes.reshape(v.shape), scales
+
+
+def mx_weights(d: Dims, wg, wu, wd, mode: int = 1):
+    """Dequantised weights (fp64): gate/up rows along h, down rows along g, gate/up columns along g,
+    down columns along h (the six operand layouts of the MX variant)."""
+    wg, wu, wd = (_wt(a, d.in_dtype) for a in (wg, wu, wd))
+    out = [np.zeros((d.E, d.g, d.h)), np.zeros((d.E, d.g, d.h)), np.zeros((d.E, d.h, d.g)),
+           np.zeros((d.E, d.g, d.h)), np.zeros((d.E, d.g, d.h)), np.zeros((d.E, d.h, d.g))]
+    arr = (C.POINTER(C.c_double) * 6)(*[a.ctypes.data_as(C.POINTER(C.c_double)) for a in out])
+    lib().oracle_mx_weights(C.byref(d.c()), C.c_int32(mode), _p(wg), _p(wu), _p(wd), arr)
+    return out
+
+
+def moe_mx(d: Dims, x, ids, w, wq, dy=None, mode: int = 1):
+    """MX variant of the layer (mode 0: quantisers off).  wq from mx_weights(mode).
+    Returns y, or (y, dx, dscore, dwg, dwu, dwd) when dy is given."""
+    x = _wt(x, d.in_dtype)
+    ids = np.ascontiguousarray(ids, dtype=np.int32)
+    w = np.ascontiguousarray(w, dtype=np.float64)
+    n = d.EP * d.T
+    y = np.zeros((n, d.h))
+    arr = (C.POINTER(C.c_double) * 6)(*[np.ascontiguousarray(a).ctypes.data_as(C.POINTER(C.c_double)) for a in wq])
+    if dy is None:
+        st = lib().oracle_moe_mx(C.byref(d.c()), C.c_int32(mode), None, _p(x), _p(ids), _p(w), arr, _p(y),
+                                 None, None, None, None, None)
+        assert st == 0
+        return y
+    dy = _wt(dy, d.in_dtype)
+    dx = np.zeros((n, d.h)); ds = np.zeros((n, d.k))
+    dwg = np.zeros((d.E, d.g, d.h)); dwu = np.zeros((d.E, d.g, d.h)); dwd = np.zeros((d.E, d.h, d.g))
+    st = lib().oracle_moe_mx(C.byref(d.c()), C.c_int32(mode), _p(dy), _p(x), _p(ids), _p(w), arr, _p(y), _p(dx),
+                             _p(ds), _p(dwg), _p(dwu), _p(dwd))
+    assert st == 0
+    return y, dx, ds, dwg, dwu, dwd

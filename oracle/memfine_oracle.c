@@ -714,6 +714,240 @@ void oracle_router_backward(const oracle_dims* d, int64_t ntok, const void* x, c
     free(dl);
 }
 
+/* ------------------------------------------------------------------------- */
+/* MXFP8 variant of the expert GEMMs (reading R28). */
+/* The paper trains in BF16 and says nothing about FP8; this    */
+/* variant is this build's extension, defined here as:                          */
+/*  - blocks of 32 consecutive elements along each GEMM's contraction dim K;    */
+/*  - one shared power-of-two scale X = 2^E per block (E8M0), E the smallest    */
+/*    integer with amax <= 448 * 2^E (no element clips), E clamped to [-127,127]*/
+/*    and E = 0 for an all-zero block;                                          */
+/*  - elements v / X rounded to FP8 E4M3 (bias 7, max 448, no inf) by          */
+/*    round-to-nearest-even, saturating at +-448;  dequant = e4m3(code) * X.    */
+/* Quantised operands: forward/recompute x and W_gate/W_up rows along h, a and */
+/* W_down rows along g; backward dY and W_down columns along h, dG/dU and      */
+/* W_gate/W_up columns along g.  Weight gradients keep unquantised operands.   */
+/* mode 0 replaces every quantiser by the identity (then these functions equal */
+/* oracle_moe_forward / oracle_moe_tokens exactly) - a structural pin.          */
+/* ------------------------------------------------------------------------- */
+double oracle_e4m3_decode(uint8_t c)
+{
+    int sgn = c >> 7, ex = (c >> 3) & 15, m = c & 7;
+    if (ex == 15 && m == 7) return NAN;
+    double v = ex == 0 ? ldexp((double)m / 8.0, -6) : ldexp(1.0 + (double)m / 8.0, ex - 7);
+    return sgn ? -v : v;
+}
+
+/* round-to-nearest-even onto the E4M3 grid, saturating at 448 */
+uint8_t oracle_e4m3_encode(double v)
+{
+    uint8_t sgn = (v < 0.0 || (v == 0.0 && signbit(v))) ? 0x80 : 0;
+    double a = fabs(v);
+    if (!(a == a)) return 0x7F;                           /* NaN */
+    if (a >= 448.0) return (uint8_t)(sgn | 0x7E);
+    int e = a > 0.0 ? ilogb(a) : -6;                      /* binade of a */
+    if (e < -6) e = -6;                                   /* subnormal quantum 2^-9 */
+    double q = ldexp(1.0, e - 3);                         /* spacing in this binade */
+    double r = nearbyint(a / q);                          /* ties to even (default rounding mode) */
+    double val = r * q;                                   /* may step up into the next binade */
+    if (val > 448.0) val = 448.0;
+    /* encode val exactly */
+    if (val == 0.0) return sgn;
+    int ev = ilogb(val);
+    if (ev < -6) return (uint8_t)(sgn | (uint8_t)(val / ldexp(1.0, -9)));   /* subnormal: m * 2^-9 */
+    int m = (int)(ldexp(val, -ev) * 8.0 - 8.0);
+    return (uint8_t)(sgn | (uint8_t)((ev + 7) << 3) | (uint8_t)m);
+}
+
+/* E of one block from its amax: smallest integer E with amax <= 448 * 2^E */
+int32_t oracle_mx_scale_exp(double amax)
+{
+    if (amax == 0.0) return 0;
+    int e0 = ilogb(amax);
+    double mant = ldexp(amax, -e0);                       /* [1, 2) */
+    int e = e0 - 8 + (mant > 1.75 ? 1 : 0);
+    if (e < -127) e = -127;
+    if (e > 127) e = 127;
+    return e;
+}
+
+/* Quantise n values (n % 32 == 0, consecutive = one block per 32) from in_dtype
+ * storage: codes[n], scale codes[n / 32] (E + 127). */
+void oracle_mx_quantize(const void* v, int32_t in_dtype, int64_t n, uint8_t* codes, uint8_t* scales)
+{
+    for (int64_t b = 0; b < n / 32; b++) {
+        double amax = 0.0;
+        for (int i = 0; i < 32; i++) amax = fmax(amax, fabs(load(v, b * 32 + i, in_dtype)));
+        int32_t E = oracle_mx_scale_exp(amax);
+        scales[b] = (uint8_t)(E + 127);
+        for (int i = 0; i < 32; i++) codes[b * 32 + i] = oracle_e4m3_encode(ldexp(load(v, b * 32 + i, in_dtype), -E));
+    }
+}
+
+/* quantise-dequantise n strided doubles in place (blocks of 32 along the stride) */
+static void mx_qdq(double* v, int64_t n, int64_t stride, int mode)
+{
+    if (!mode) return;
+    for (int64_t b = 0; b < n / 32; b++) {
+        double amax = 0.0;
+        for (int i = 0; i < 32; i++) amax = fmax(amax, fabs(v[(b * 32 + i) * stride]));
+        int32_t E = oracle_mx_scale_exp(amax);
+        for (int i = 0; i < 32; i++) {
+            double* p = v + (b * 32 + i) * stride;
+            *p = ldexp(oracle_e4m3_decode(oracle_e4m3_encode(ldexp(*p, -E))), E);
+        }
+    }
+}
+
+/* Dequantised weights of all E experts, fp64, 6 arrays:
+ *  wq[0] W_gate rows along h [E][g][h]   wq[3] W_gate columns along g [E][g][h]
+ *  wq[1] W_up   rows along h              wq[4] W_up columns along g
+ *  wq[2] W_down rows along g [E][h][g]   wq[5] W_down columns along h [E][h][g] */
+void oracle_mx_weights(const oracle_dims* d, int32_t mode, const void* wg, const void* wu, const void* wd,
+                       double* const* wq)
+{
+    int64_t h = d->h, g = d->g, E = d->E, n = E * g * h;
+    for (int64_t i = 0; i < n; i++) {
+        wq[0][i] = wq[3][i] = load(wg, i, d->in_dtype);
+        wq[1][i] = wq[4][i] = load(wu, i, d->in_dtype);
+        wq[2][i] = wq[5][i] = load(wd, i, d->in_dtype);
+    }
+    for (int64_t e = 0; e < E; e++) {
+        for (int64_t r = 0; r < g; r++) {       /* gate/up rows: contiguous h */
+            mx_qdq(wq[0] + (e * g + r) * h, h, 1, mode);
+            mx_qdq(wq[1] + (e * g + r) * h, h, 1, mode);
+        }
+        for (int64_t c = 0; c < h; c++) {       /* gate/up columns: stride h over g */
+            mx_qdq(wq[3] + e * g * h + c, g, h, mode);
+            mx_qdq(wq[4] + e * g * h + c, g, h, mode);
+        }
+        for (int64_t r = 0; r < h; r++) mx_qdq(wq[2] + (e * h + r) * g, g, 1, mode);   /* down rows */
+        for (int64_t c = 0; c < g; c++) mx_qdq(wq[5] + e * h * g + c, h, g, mode);     /* down columns */
+    }
+}
+
+/* One copy, MX variant: forward (y term), backward (dx term, d_score, and the
+ * unquantised dW operands a, dO, dG, dU).  Same loop orders as expert_forward /
+ * expert_backward, quantisers inserted. */
+static void expert_mx(const oracle_dims* d, int mode, const void* x, int64_t xoff, const void* dy, int64_t dyoff,
+                      double ws, double* const* wq, int32_t e, double* scratch,
+                      double* O, double* a_out, double* dO_out, double* dG_out, double* dU_out, double* dxc,
+                      double* dscore)
+{
+    int64_t h = d->h, g = d->g;
+    double *xq = scratch, *G = xq + h, *U = G + g, *A = U + g, *Aq = A + g, *dyq = Aq + g, *dA = dyq + h;
+    double *dGq = dA + g, *dUq = dGq + g;
+    for (int64_t c = 0; c < h; c++) xq[c] = load(x, xoff + c, d->in_dtype);
+    mx_qdq(xq, h, 1, mode);
+    for (int64_t n = 0; n < g; n++) {
+        double sg = 0.0, su = 0.0;
+        for (int64_t c = 0; c < h; c++) {
+            sg += wq[0][((int64_t)e * g + n) * h + c] * xq[c];
+            su += wq[1][((int64_t)e * g + n) * h + c] * xq[c];
+        }
+        G[n] = sg; U[n] = su;
+        A[n] = sg * sigmoid(sg) * su;
+        Aq[n] = A[n];
+    }
+    mx_qdq(Aq, g, 1, mode);
+    for (int64_t m = 0; m < h; m++) {
+        double so = 0.0;
+        for (int64_t n = 0; n < g; n++) so += wq[2][((int64_t)e * h + m) * g + n] * Aq[n];
+        O[m] = so;
+    }
+    if (!dy) return;
+    for (int64_t m = 0; m < h; m++) dyq[m] = load(dy, dyoff + m, d->in_dtype);
+    mx_qdq(dyq, h, 1, mode);
+    /* u = W_down^T dY_q (columns along h);  d_score = <u, a>;  dA = w u (reading R15) */
+    double dwv = 0.0;
+    for (int64_t n = 0; n < g; n++) {
+        double s = 0.0;
+        for (int64_t m = 0; m < h; m++) s += wq[5][((int64_t)e * h + m) * g + n] * dyq[m];
+        dwv += s * A[n];
+        dA[n] = ws * s;
+    }
+    *dscore = dwv;
+    for (int64_t m = 0; m < h; m++) dO_out[m] = ws * load(dy, dyoff + m, d->in_dtype);
+    for (int64_t n = 0; n < g; n++) {
+        double sg = sigmoid(G[n]);
+        dG_out[n] = dA[n] * U[n] * sg * (1.0 + G[n] * (1.0 - sg));
+        dU_out[n] = dA[n] * G[n] * sg;
+        dGq[n] = dG_out[n];
+        dUq[n] = dU_out[n];
+        a_out[n] = A[n];
+    }
+    mx_qdq(dGq, g, 1, mode);
+    mx_qdq(dUq, g, 1, mode);
+    for (int64_t c = 0; c < h; c++) {
+        double s1 = 0.0, s2 = 0.0;
+        for (int64_t n = 0; n < g; n++) {
+            s1 += wq[3][((int64_t)e * g + n) * h + c] * dGq[n];
+            s2 += wq[4][((int64_t)e * g + n) * h + c] * dUq[n];
+        }
+        dxc[c] = s1 + s2;
+    }
+}
+
+/* MX variant of the whole layer: y, and (dy != NULL) dx, dscore and dW (dW in the
+ * canonical copy order, unquantised operands).  Outputs as oracle_moe_forward /
+ * oracle_moe_backward.  wq from oracle_mx_weights with the same mode. */
+int32_t oracle_moe_mx(const oracle_dims* d, int32_t mode, const void* dy, const void* x, const int32_t* ids,
+                      const double* w, double* const* wq, double* y, double* dx, double* dscore,
+                      double* dwg, double* dwu, double* dwd)
+{
+    int64_t h = d->h, g = d->g, ntok = (int64_t)d->EP * d->T, nq = ntok * d->k;
+    double *a_all = NULL, *dG_all = NULL, *dU_all = NULL, *dO_all = NULL;
+    int64_t* order = NULL;
+    if (dy) {
+        a_all = (double*)malloc(sizeof(double) * (size_t)(nq > 0 ? nq : 1) * g);
+        dG_all = (double*)malloc(sizeof(double) * (size_t)(nq > 0 ? nq : 1) * g);
+        dU_all = (double*)malloc(sizeof(double) * (size_t)(nq > 0 ? nq : 1) * g);
+        dO_all = (double*)malloc(sizeof(double) * (size_t)(nq > 0 ? nq : 1) * h);
+        order = (int64_t*)malloc(sizeof(int64_t) * (size_t)(nq > 0 ? nq : 1));
+        if (!a_all || !dG_all || !dU_all || !dO_all || !order) {
+            free(a_all); free(dG_all); free(dU_all); free(dO_all); free(order);
+            return 1;
+        }
+    }
+    #pragma omp parallel
+    {
+        double* scratch = (double*)malloc(sizeof(double) * (size_t)(8 * g + 2 * h));
+        double* O = (double*)malloc(sizeof(double) * (size_t)(2 * h + 3 * g + h));
+        double *dxc = O + h, *a1 = dxc + h, *dG1 = a1 + g, *dU1 = dG1 + g, *dO1 = dU1 + g;
+        #pragma omp for schedule(dynamic, 1)
+        for (int64_t t = 0; t < ntok; t++) {
+            for (int64_t c = 0; c < h; c++) { y[t * h + c] = 0.0; if (dy) dx[t * h + c] = 0.0; }
+            for (int32_t s = 0; s < d->k; s++) {
+                int64_t q = t * d->k + s;
+                int32_t e = ids[q];
+                if (dy) dscore[q] = 0.0;
+                double *aq = dy ? a_all + q * g : a1, *dGq = dy ? dG_all + q * g : dG1;
+                double *dUq = dy ? dU_all + q * g : dU1, *dOq = dy ? dO_all + q * h : dO1;
+                if (e < 0 || e >= d->E) {
+                    if (dy) {
+                        memset(aq, 0, sizeof(double) * (size_t)g); memset(dGq, 0, sizeof(double) * (size_t)g);
+                        memset(dUq, 0, sizeof(double) * (size_t)g); memset(dOq, 0, sizeof(double) * (size_t)h);
+                    }
+                    continue;
+                }
+                expert_mx(d, mode, x, t * h, dy, t * h, w[q], wq, e, scratch, O, aq, dOq, dGq, dUq, dxc,
+                          dy ? dscore + q : NULL);
+                for (int64_t c = 0; c < h; c++) {
+                    y[t * h + c] += w[q] * O[c];
+                    if (dy) dx[t * h + c] += dxc[c];
+                }
+            }
+        }
+        free(scratch); free(O);
+    }
+    if (dy) {
+        for (int64_t q = 0; q < nq; q++) order[q] = q;
+        accumulate_dw(d, x, ids, order, nq, a_all, dO_all, dG_all, dU_all, dwg, dwu, dwd);
+        free(a_all); free(dG_all); free(dU_all); free(dO_all); free(order);
+    }
+    return 0;
+}
+
 int32_t oracle_version(void) { return 1; }
 
 #ifdef _OPENMP

@@ -1,0 +1,149 @@
+"""Pins for the oracle's MXFP8 variant (reading R28), CPU only.
+
+The oracle's E4M3 codec is pinned to torch's float8_e4m3fn conversion (an independent library
+routine) and to brute force over all 256 codes; the scale rule to its closed-form property; the
+MX layer to the exact oracle with quantisers off, and — for the operand layouts (which tensors are
+quantised along which axis) — to an independent numpy/torch re-derivation of one token."""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import synth
+
+
+def _dec_all():
+    return np.array([oracle.e4m3_decode(c) for c in range(256)])
+
+
+def test_e4m3_decode_matches_torch_all_codes():
+    ref = torch.arange(256, dtype=torch.uint8).view(torch.float8_e4m3fn).to(torch.float64).numpy()
+    got = _dec_all()
+    nan = np.isnan(ref)
+    assert (np.isnan(got) == nan).all() and nan.sum() == 2          # 0x7F and 0xFF
+    assert (got[~nan] == ref[~nan]).all()
+    assert np.nanmax(got) == 448.0 and got[1] == 2.0 ** -9               # max normal, min subnormal
+
+
+def test_e4m3_encode_matches_torch_and_brute_force():
+    rng = np.random.default_rng(5)
+    mag = 2.0 ** rng.uniform(-12, np.log2(448), 4000)
+    v = (mag * rng.choice([-1, 1], 4000)).astype(np.float32)
+    # torch: float32 -> float8_e4m3fn, round to nearest even
+    ref = torch.from_numpy(v).to(torch.float8_e4m3fn).view(torch.uint8).numpy()
+    got = np.array([oracle.e4m3_encode(float(x)) for x in v], np.uint8)
+    assert (got == ref).all()
+    # exact midpoints between neighbouring codes tie to the even code (brute force over the grid)
+    vals = _dec_all()
+    pos = np.array(sorted({(float(vals[c]), c) for c in range(0x7F)}))
+    for (a, ca), (b, cb) in zip(pos[:-1], pos[1:]):
+        mid = (a + b) / 2
+        want = int(ca) if int(ca) % 2 == 0 else int(cb)
+        assert oracle.e4m3_encode(mid) == want
+        assert oracle.e4m3_encode(-mid) == want | 0x80
+    assert oracle.e4m3_encode(1e6) == 0x7E and oracle.e4m3_encode(-1e6) == 0xFE   # saturating
+    assert oracle.e4m3_encode(0.0) == 0
+
+
+def test_mx_scale_rule_closed_form():
+    rng = np.random.default_rng(6)
+    for amax in np.concatenate([2.0 ** rng.uniform(-100, 100, 2000), [448.0, 449.0, 1.75, 1.0, 896.0, 897.0]]):
+        E = oracle.mx_scale_exp(amax)
+        assert amax <= 448.0 * 2.0 ** E                 # nothing clips
+        assert amax > 448.0 * 2.0 ** (E - 1)            # and E is the smallest such
+    assert oracle.mx_scale_exp(0.0) == 0
+    assert oracle.mx_scale_exp(1e-300) == -127 and oracle.mx_scale_exp(1e300) == 127
+
+
+def test_mx_quantize_block_error_bound():
+    rng = np.random.default_rng(7)
+    v = (rng.standard_normal(32 * 64) * 2.0 ** rng.integers(-20, 20, 32 * 64)).astype(np.float32)
+    v[:32] = 0.0                                                          # an all-zero block
+    codes, sc = oracle.mx_quantize(v)
+    vals = _dec_all()
+    E = sc.astype(np.int64) - 127
+    deq = vals[codes] * 2.0 ** np.repeat(E, 32)
+    assert (deq[:32] == 0).all() and E[0] == 0
+    for b in range(64):
+        blk = v[b * 32:(b + 1) * 32].astype(np.float64)
+        if not blk.any():
+            continue
+        assert E[b] == oracle.mx_scale_exp(np.abs(blk).max())
+        # half an E4M3 spacing of each element (3 mantissa bits; subnormal spacing 2^-9 * 2^E)
+        sp = np.maximum(2.0 ** (np.floor(np.log2(np.maximum(np.abs(blk) / 2.0 ** E[b], 2.0 ** -6))) - 3),
+                        2.0 ** -9) * 2.0 ** E[b]
+        assert (np.abs(deq[b * 32:(b + 1) * 32] - blk) <= sp / 2 + 1e-300).all()
+
+
+def _problem(T=6, h=64, g=96, E=4, k=2, seed=3):
+    d = oracle.Dims(T=T, h=h, g=g, E=E, k=k, in_dtype="f32")
+    rng = np.random.default_rng(seed)
+    x = rng.standard_normal((T, h)).astype(np.float32)
+    dy = rng.standard_normal((T, h)).astype(np.float32)
+    wg = (rng.standard_normal((E, g, h)) / np.sqrt(h)).astype(np.float32)
+    wu = (rng.standard_normal((E, g, h)) / np.sqrt(h)).astype(np.float32)
+    wd = (rng.standard_normal((E, h, g)) / np.sqrt(g)).astype(np.float32)
+    wd[1, 5, :] *= 300.0                         # an outlier row: row vs column blocking differ
+    ids = np.stack([rng.choice(E, k, replace=False) for _ in range(T)]).astype(np.int32)
+    w = rng.dirichlet(np.ones(k), T)
+    return d, x, dy, wg, wu, wd, ids, w
+
+
+def test_mx_layer_mode0_equals_exact_oracle():
+    d, x, dy, wg, wu, wd, ids, w = _problem()
+    wq = oracle.mx_weights(d, wg, wu, wd, mode=0)
+    y0 = oracle.moe_mx(d, x, ids, w, wq, mode=0)
+    assert np.array_equal(y0, oracle.moe_forward(d, x, ids, w, wg, wu, wd))
+    y, dx, ds, dwg, dwu, dwd = oracle.moe_mx(d, x, ids, w, wq, dy=dy, mode=0)
+    ref = oracle.moe_backward(d, dy, x, ids, w, wg, wu, wd)
+    for a, b in zip((dx, ds, dwg, dwu, dwd), ref):
+        assert np.abs(a - b).max() <= 1e-12 * max(1.0, np.abs(b).max())
+
+
+def _mxq(v, axis):
+    """Independent MX quantise-dequantise along `axis` (numpy frexp + torch float8 conversion)."""
+    v = np.moveaxis(np.asarray(v, np.float64), axis, -1)
+    sh = v.shape
+    b = v.reshape(-1, 32)
+    amax = np.abs(b).max(1)
+    m, ex = np.frexp(amax)                       # amax = m 2^ex, m in [0.5, 1)
+    E = np.where(amax > 0, ex - 1 - 8 + (2 * m > 1.75), 0)
+    s = b / 2.0 ** E[:, None]
+    q = torch.from_numpy(s.astype(np.float32)).to(torch.float8_e4m3fn).to(torch.float64).numpy()
+    return np.moveaxis((q * 2.0 ** E[:, None]).reshape(sh), -1, axis)
+
+
+def test_mx_layer_one_token_brute_force():
+    d, x, dy, wg, wu, wd, ids, w = _problem()
+    wq = oracle.mx_weights(d, wg, wu, wd)
+    y, dx, ds, *_ = oracle.moe_mx(d, x, ids, w, wq, dy=dy)
+    t = 2
+    sig = lambda z: 1 / (1 + np.exp(-z))
+    xq, dyq = _mxq(x[t], 0), _mxq(dy[t], 0)
+    y_ref = np.zeros(d.h); dx_ref = np.zeros(d.h); ds_ref = np.zeros(d.k)
+    for s in range(d.k):
+        e = ids[t, s]
+        G = _mxq(wg[e], 1) @ xq                  # W_gate rows blocked along h
+        U = _mxq(wu[e], 1) @ xq
+        a = G * sig(G) * U
+        o = _mxq(wd[e], 1) @ _mxq(a, 0)          # W_down rows and a blocked along g
+        y_ref += w[t, s] * o
+        u = _mxq(wd[e], 0).T @ dyq               # W_down columns blocked along h
+        ds_ref[s] = u @ a
+        dA = w[t, s] * u
+        dG = dA * U * sig(G) * (1 + G * (1 - sig(G)))
+        dU = dA * G * sig(G)
+        dx_ref += _mxq(wg[e], 0).T @ _mxq(dG, 0) + _mxq(wu[e], 0).T @ _mxq(dU, 0)   # columns along g
+    for got, ref in ((y[t], y_ref), (dx[t], dx_ref), (ds[t], ds_ref)):
+        assert np.abs(got - ref).max() <= 1e-10 * np.abs(ref).max()
+
+
+def test_mx_layer_quantisation_error_is_small_but_present():
+    d = oracle.Dims(T=64, h=128, g=192, E=4, k=2, in_dtype="bf16")
+    x = synth.make_x(64, 128, rank=0).view(torch.int16).numpy().view(np.uint16)
+    wg, wu, wd = (t.view(torch.int16).numpy().view(np.uint16) for t in synth.make_experts(range(4), 128, 192))
+    ids, w = synth.make_routing(64, 4, 2, rank=0, zipf_s=1.2)
+    y_mx = oracle.moe_mx(d, x, ids, w, oracle.mx_weights(d, wg, wu, wd))
+    y = oracle.moe_forward(d, x, ids, w, wg, wu, wd)
+    err = np.abs(y_mx - y).max() / np.abs(y).max()
+    assert 1e-4 < err < 0.1          # E4M3 keeps 3 mantissa bits: a few % at most, never zero
