@@ -784,6 +784,21 @@ void oracle_mx_quantize(const void* v, int32_t in_dtype, int64_t n, uint8_t* cod
     }
 }
 
+/* Decision precision (reading R28b): a quantised code is decided on the value as the
+ * kernel holds it - a in fp32 (from the fp32 accumulators), dG / dU in bf16 (as stored for the
+ * weight gradients) - so these are rounded (to nearest even) before their blocks are quantised. */
+static double round_f32(double v) { return (double)(float)v; }
+static double round_bf16(double v)
+{
+    float f = (float)v;
+    uint32_t u;
+    memcpy(&u, &f, sizeof u);
+    if ((u & 0x7F800000u) != 0x7F800000u) u += 0x7FFFu + ((u >> 16) & 1u);
+    u &= 0xFFFF0000u;
+    memcpy(&f, &u, sizeof f);
+    return (double)f;
+}
+
 /* quantise-dequantise n strided doubles in place (blocks of 32 along the stride) */
 static void mx_qdq(double* v, int64_t n, int64_t stride, int mode)
 {
@@ -847,7 +862,7 @@ static void expert_mx(const oracle_dims* d, int mode, const void* x, int64_t xof
         }
         G[n] = sg; U[n] = su;
         A[n] = sg * sigmoid(sg) * su;
-        Aq[n] = A[n];
+        Aq[n] = mode ? round_f32(A[n]) : A[n];
     }
     mx_qdq(Aq, g, 1, mode);
     for (int64_t m = 0; m < h; m++) {
@@ -872,8 +887,8 @@ static void expert_mx(const oracle_dims* d, int mode, const void* x, int64_t xof
         double sg = sigmoid(G[n]);
         dG_out[n] = dA[n] * U[n] * sg * (1.0 + G[n] * (1.0 - sg));
         dU_out[n] = dA[n] * G[n] * sg;
-        dGq[n] = dG_out[n];
-        dUq[n] = dU_out[n];
+        dGq[n] = mode ? round_bf16(dG_out[n]) : dG_out[n];
+        dUq[n] = mode ? round_bf16(dU_out[n]) : dU_out[n];
         a_out[n] = A[n];
     }
     mx_qdq(dGq, g, 1, mode);
