@@ -786,7 +786,9 @@ void oracle_mx_quantize(const void* v, int32_t in_dtype, int64_t n, uint8_t* cod
 
 /* Decision precision (reading R28b): a quantised code is decided on the value as the
  * kernel holds it - a in fp32 (from the fp32 accumulators), dG / dU in bf16 (as stored for the
- * weight gradients) - so these are rounded (to nearest even) before their blocks are quantised. */
+ * weight gradients) - so these are rounded (to nearest even) before their blocks are quantised;
+ * and the backward's dA step works from the recomputed G || U as stored (bf16), since a code
+ * flip amplifies that 2^-9 difference to a 2^-4 E4M3 step. */
 static double round_f32(double v) { return (double)(float)v; }
 static double round_bf16(double v)
 {
@@ -874,6 +876,14 @@ static void expert_mx(const oracle_dims* d, int mode, const void* x, int64_t xof
     for (int64_t m = 0; m < h; m++) dyq[m] = load(dy, dyoff + m, d->in_dtype);
     mx_qdq(dyq, h, 1, mode);
     /* u = W_down^T dY_q (columns along h);  d_score = <u, a>;  dA = w u (reading R15) */
+    /* G, U, a as the dA step sees them (mode 1: recomputed G || U stored as bf16) */
+    for (int64_t n = 0; n < g; n++) {
+        if (mode) {
+            G[n] = round_bf16(G[n]);
+            U[n] = round_bf16(U[n]);
+            A[n] = G[n] * sigmoid(G[n]) * U[n];
+        }
+    }
     double dwv = 0.0;
     for (int64_t n = 0; n < g; n++) {
         double s = 0.0;

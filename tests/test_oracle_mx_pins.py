@@ -128,12 +128,14 @@ def test_mx_layer_one_token_brute_force():
         a = G * sig(G) * U
         o = _mxq(wd[e], 1) @ _mxq(a.astype(np.float32), 0)   # W_down rows and a (as fp32) along g
         y_ref += w[t, s] * o
+        bf = lambda v: torch.from_numpy(v).to(torch.bfloat16).to(torch.float64).numpy()
+        G, U = bf(G), bf(U)                      # the dA step reads the recomputed G || U as bf16
+        a = G * sig(G) * U
         u = _mxq(wd[e], 0).T @ dyq               # W_down columns blocked along h
         ds_ref[s] = u @ a
         dA = w[t, s] * u
         dG = dA * U * sig(G) * (1 + G * (1 - sig(G)))
         dU = dA * G * sig(G)
-        bf = lambda v: torch.from_numpy(v).to(torch.bfloat16).to(torch.float64).numpy()   # dG, dU as bf16
         dx_ref += _mxq(wg[e], 0).T @ _mxq(bf(dG), 0) + _mxq(wu[e], 0).T @ _mxq(bf(dU), 0)   # columns along g
     for got, ref in ((y[t], y_ref), (dx[t], dx_ref), (ds[t], ds_ref)):
         assert np.abs(got - ref).max() <= 1e-10 * np.abs(ref).max()
