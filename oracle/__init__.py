@@ -293,34 +293,36 @@ def mx_quantize(v, in_dtype: str = "f32"):
 
 
 def mx_weights(d: Dims, wg, wu, wd, mode: int = 1):
-    """Dequantised weights (fp64): gate/up rows along h, down rows along g, gate/up columns along g,
-    down columns along h (the six operand layouts of the MX variant)."""
+    """Dequantised weights (fp64): gate/up rows along h, down rows along g, gate/up columns along g
+    (the five weight operand layouts of the MX variant)."""
     wg, wu, wd = (_wt(a, d.in_dtype) for a in (wg, wu, wd))
     out = [np.zeros((d.E, d.g, d.h)), np.zeros((d.E, d.g, d.h)), np.zeros((d.E, d.h, d.g)),
-           np.zeros((d.E, d.g, d.h)), np.zeros((d.E, d.g, d.h)), np.zeros((d.E, d.h, d.g))]
-    arr = (C.POINTER(C.c_double) * 6)(*[a.ctypes.data_as(C.POINTER(C.c_double)) for a in out])
+           np.zeros((d.E, d.g, d.h)), np.zeros((d.E, d.g, d.h))]
+    arr = (C.POINTER(C.c_double) * 5)(*[a.ctypes.data_as(C.POINTER(C.c_double)) for a in out])
     lib().oracle_mx_weights(C.byref(d.c()), C.c_int32(mode), _p(wg), _p(wu), _p(wd), arr)
     return out
 
 
-def moe_mx(d: Dims, x, ids, w, wq, dy=None, mode: int = 1):
-    """MX variant of the layer (mode 0: quantisers off).  wq from mx_weights(mode).
+def moe_mx(d: Dims, x, ids, w, wq, dy=None, mode: int = 1, wd=None):
+    """MX variant of the layer (mode 0: quantisers off).  wq from mx_weights(mode); wd the unquantised
+    W_down (needed with dy: the dA step keeps BF16 operands).
     Returns y, or (y, dx, dscore, dwg, dwu, dwd) when dy is given."""
     x = _wt(x, d.in_dtype)
     ids = np.ascontiguousarray(ids, dtype=np.int32)
     w = np.ascontiguousarray(w, dtype=np.float64)
     n = d.EP * d.T
     y = np.zeros((n, d.h))
-    arr = (C.POINTER(C.c_double) * 6)(*[np.ascontiguousarray(a).ctypes.data_as(C.POINTER(C.c_double)) for a in wq])
+    arr = (C.POINTER(C.c_double) * 5)(*[np.ascontiguousarray(a).ctypes.data_as(C.POINTER(C.c_double)) for a in wq])
     if dy is None:
-        st = lib().oracle_moe_mx(C.byref(d.c()), C.c_int32(mode), None, _p(x), _p(ids), _p(w), arr, _p(y),
+        st = lib().oracle_moe_mx(C.byref(d.c()), C.c_int32(mode), None, _p(x), _p(ids), _p(w), arr, None, _p(y),
                                  None, None, None, None, None)
         assert st == 0
         return y
     dy = _wt(dy, d.in_dtype)
+    wd = _wt(wd, d.in_dtype)
     dx = np.zeros((n, d.h)); ds = np.zeros((n, d.k))
     dwg = np.zeros((d.E, d.g, d.h)); dwu = np.zeros((d.E, d.g, d.h)); dwd = np.zeros((d.E, d.h, d.g))
-    st = lib().oracle_moe_mx(C.byref(d.c()), C.c_int32(mode), _p(dy), _p(x), _p(ids), _p(w), arr, _p(y), _p(dx),
+    st = lib().oracle_moe_mx(C.byref(d.c()), C.c_int32(mode), _p(dy), _p(x), _p(ids), _p(w), arr, _p(wd), _p(y), _p(dx),
                              _p(ds), _p(dwg), _p(dwu), _p(dwd))
     assert st == 0
     return y, dx, ds, dwg, dwu, dwd

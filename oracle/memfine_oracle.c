@@ -725,8 +725,9 @@ void oracle_router_backward(const oracle_dims* d, int64_t ntok, const void* x, c
 /*  - elements v / X rounded to FP8 E4M3 (bias 7, max 448, no inf) by          */
 /*    round-to-nearest-even, saturating at +-448;  dequant = e4m3(code) * X.    */
 /* Quantised operands: forward/recompute x and W_gate/W_up rows along h, a and */
-/* W_down rows along g; backward dY and W_down columns along h, dG/dU and      */
-/* W_gate/W_up columns along g.  Weight gradients keep unquantised operands.   */
+/* W_down rows along g; backward dX: dG/dU and W_gate/W_up columns along g.    */
+/* The dA GEMM (dY W_down, epilogue-bound) and the weight gradients keep       */
+/* unquantised operands.                                                        */
 /* mode 0 replaces every quantiser by the identity (then these functions equal */
 /* oracle_moe_forward / oracle_moe_tokens exactly) - a structural pin.          */
 /* ------------------------------------------------------------------------- */
@@ -816,10 +817,10 @@ static void mx_qdq(double* v, int64_t n, int64_t stride, int mode)
     }
 }
 
-/* Dequantised weights of all E experts, fp64, 6 arrays:
+/* Dequantised weights of all E experts, fp64, 5 arrays:
  *  wq[0] W_gate rows along h [E][g][h]   wq[3] W_gate columns along g [E][g][h]
  *  wq[1] W_up   rows along h              wq[4] W_up columns along g
- *  wq[2] W_down rows along g [E][h][g]   wq[5] W_down columns along h [E][h][g] */
+ *  wq[2] W_down rows along g [E][h][g] */
 void oracle_mx_weights(const oracle_dims* d, int32_t mode, const void* wg, const void* wu, const void* wd,
                        double* const* wq)
 {
@@ -827,7 +828,7 @@ void oracle_mx_weights(const oracle_dims* d, int32_t mode, const void* wg, const
     for (int64_t i = 0; i < n; i++) {
         wq[0][i] = wq[3][i] = load(wg, i, d->in_dtype);
         wq[1][i] = wq[4][i] = load(wu, i, d->in_dtype);
-        wq[2][i] = wq[5][i] = load(wd, i, d->in_dtype);
+        wq[2][i] = load(wd, i, d->in_dtype);
     }
     for (int64_t e = 0; e < E; e++) {
         for (int64_t r = 0; r < g; r++) {       /* gate/up rows: contiguous h */
@@ -839,7 +840,6 @@ void oracle_mx_weights(const oracle_dims* d, int32_t mode, const void* wg, const
             mx_qdq(wq[4] + e * g * h + c, g, h, mode);
         }
         for (int64_t r = 0; r < h; r++) mx_qdq(wq[2] + (e * h + r) * g, g, 1, mode);   /* down rows */
-        for (int64_t c = 0; c < g; c++) mx_qdq(wq[5] + e * h * g + c, h, g, mode);     /* down columns */
     }
 }
 
@@ -847,7 +847,7 @@ void oracle_mx_weights(const oracle_dims* d, int32_t mode, const void* wg, const
  * unquantised dW operands a, dO, dG, dU).  Same loop orders as expert_forward /
  * expert_backward, quantisers inserted. */
 static void expert_mx(const oracle_dims* d, int mode, const void* x, int64_t xoff, const void* dy, int64_t dyoff,
-                      double ws, double* const* wq, int32_t e, double* scratch,
+                      double ws, double* const* wq, const void* wd, int32_t e, double* scratch,
                       double* O, double* a_out, double* dO_out, double* dG_out, double* dU_out, double* dxc,
                       double* dscore)
 {
@@ -873,9 +873,8 @@ static void expert_mx(const oracle_dims* d, int mode, const void* x, int64_t xof
         O[m] = so;
     }
     if (!dy) return;
-    for (int64_t m = 0; m < h; m++) dyq[m] = load(dy, dyoff + m, d->in_dtype);
-    mx_qdq(dyq, h, 1, mode);
-    /* u = W_down^T dY_q (columns along h);  d_score = <u, a>;  dA = w u (reading R15) */
+    for (int64_t m = 0; m < h; m++) dyq[m] = load(dy, dyoff + m, d->in_dtype);   /* dA: unquantised */
+    /* u = W_down^T dY (BF16 operands);  d_score = <u, a>;  dA = w u (reading R15) */
     /* G, U, a as the dA step sees them (mode 1: recomputed G || U stored as bf16) */
     for (int64_t n = 0; n < g; n++) {
         if (mode) {
@@ -887,7 +886,7 @@ static void expert_mx(const oracle_dims* d, int mode, const void* x, int64_t xof
     double dwv = 0.0;
     for (int64_t n = 0; n < g; n++) {
         double s = 0.0;
-        for (int64_t m = 0; m < h; m++) s += wq[5][((int64_t)e * h + m) * g + n] * dyq[m];
+        for (int64_t m = 0; m < h; m++) s += load(wd, ((int64_t)e * h + m) * g + n, d->in_dtype) * dyq[m];
         dwv += s * A[n];
         dA[n] = ws * s;
     }
@@ -915,9 +914,10 @@ static void expert_mx(const oracle_dims* d, int mode, const void* x, int64_t xof
 
 /* MX variant of the whole layer: y, and (dy != NULL) dx, dscore and dW (dW in the
  * canonical copy order, unquantised operands).  Outputs as oracle_moe_forward /
- * oracle_moe_backward.  wq from oracle_mx_weights with the same mode. */
+ * oracle_moe_backward.  wq from oracle_mx_weights with the same mode; wd the
+ * unquantised W_down (in_dtype) for the dA step. */
 int32_t oracle_moe_mx(const oracle_dims* d, int32_t mode, const void* dy, const void* x, const int32_t* ids,
-                      const double* w, double* const* wq, double* y, double* dx, double* dscore,
+                      const double* w, double* const* wq, const void* wd, double* y, double* dx, double* dscore,
                       double* dwg, double* dwu, double* dwd)
 {
     int64_t h = d->h, g = d->g, ntok = (int64_t)d->EP * d->T, nq = ntok * d->k;
@@ -955,7 +955,7 @@ int32_t oracle_moe_mx(const oracle_dims* d, int32_t mode, const void* dy, const 
                     }
                     continue;
                 }
-                expert_mx(d, mode, x, t * h, dy, t * h, w[q], wq, e, scratch, O, aq, dOq, dGq, dUq, dxc,
+                expert_mx(d, mode, x, t * h, dy, t * h, w[q], wq, wd, e, scratch, O, aq, dOq, dGq, dUq, dxc,
                           dy ? dscore + q : NULL);
                 for (int64_t c = 0; c < h; c++) {
                     y[t * h + c] += w[q] * O[c];

@@ -94,7 +94,7 @@ def test_mx_layer_mode0_equals_exact_oracle():
     wq = oracle.mx_weights(d, wg, wu, wd, mode=0)
     y0 = oracle.moe_mx(d, x, ids, w, wq, mode=0)
     assert np.array_equal(y0, oracle.moe_forward(d, x, ids, w, wg, wu, wd))
-    y, dx, ds, dwg, dwu, dwd = oracle.moe_mx(d, x, ids, w, wq, dy=dy, mode=0)
+    y, dx, ds, dwg, dwu, dwd = oracle.moe_mx(d, x, ids, w, wq, dy=dy, mode=0, wd=wd)
     ref = oracle.moe_backward(d, dy, x, ids, w, wg, wu, wd)
     for a, b in zip((dx, ds, dwg, dwu, dwd), ref):
         assert np.abs(a - b).max() <= 1e-12 * max(1.0, np.abs(b).max())
@@ -116,10 +116,10 @@ def _mxq(v, axis):
 def test_mx_layer_one_token_brute_force():
     d, x, dy, wg, wu, wd, ids, w = _problem()
     wq = oracle.mx_weights(d, wg, wu, wd)
-    y, dx, ds, *_ = oracle.moe_mx(d, x, ids, w, wq, dy=dy)
+    y, dx, ds, *_ = oracle.moe_mx(d, x, ids, w, wq, dy=dy, wd=wd)
     t = 2
     sig = lambda z: 1 / (1 + np.exp(-z))
-    xq, dyq = _mxq(x[t], 0), _mxq(dy[t], 0)
+    xq = _mxq(x[t], 0)
     y_ref = np.zeros(d.h); dx_ref = np.zeros(d.h); ds_ref = np.zeros(d.k)
     for s in range(d.k):
         e = ids[t, s]
@@ -131,7 +131,7 @@ def test_mx_layer_one_token_brute_force():
         bf = lambda v: torch.from_numpy(v).to(torch.bfloat16).to(torch.float64).numpy()
         G, U = bf(G), bf(U)                      # the dA step reads the recomputed G || U as bf16
         a = G * sig(G) * U
-        u = _mxq(wd[e], 0).T @ dyq               # W_down columns blocked along h
+        u = wd[e].astype(np.float64).T @ dy[t].astype(np.float64)   # dA: BF16 operands, not quantised
         ds_ref[s] = u @ a
         dA = w[t, s] * u
         dG = dA * U * sig(G) * (1 + G * (1 - sig(G)))
