@@ -53,7 +53,7 @@ typedef enum {
     MEMFINE_ERR_UNSUPPORTED = 7    /* shape outside what the kernels support (see below)  */
 } memfine_status;
 
-enum { MEMFINE_BF16 = 0, MEMFINE_FP32 = 1 };         /* memfine_dims.dtype  */
+enum { MEMFINE_BF16 = 0, MEMFINE_FP32 = 1, MEMFINE_MXFP8 = 2 }; /* memfine_dims.dtype */
 enum { MEMFINE_RULE_EQ9 = 0, MEMFINE_RULE_EXACT = 1 }; /* memfine_budget.rule */
 enum { MEMFINE_FWD = 0, MEMFINE_BWD = 1 };           /* workspace pass      */
 enum { MEMFINE_MODEL_PAPER = 0, MEMFINE_MODEL_IMPL = 1 }; /* memfine_budget.model */
@@ -71,7 +71,10 @@ typedef struct {
     int32_t ep_size;      /* EP; ranks hold contiguous expert blocks (reading R4)    */
     int32_t ep_rank;      /* this rank                                               */
     int32_t dtype;        /* MEMFINE_BF16 (bf16 storage, fp32 accumulate, tcgen05)    *
-                           * MEMFINE_FP32 (fp32 everywhere, CUDA-core FFMA; <=1e-5)   */
+                           * MEMFINE_FP32 (fp32 everywhere, CUDA-core FFMA; <=1e-5)   *
+                           * MEMFINE_MXFP8 (bf16 storage; the gate/up, down and dX   *
+                           *   GEMMs on MXFP8 operands, see memfine_mx_*; EP = 1,     *
+                           *   hidden, ffn % 128 == 0)                                 */
 } memfine_dims;
 
 /* Memory budget for MACT (Eq. 3; Eq. 8). */
@@ -272,6 +275,30 @@ memfine_status memfine_router_fwd(memfine_handle_t h, const void* x, const void*
 memfine_status memfine_router_bwd(memfine_handle_t h, const void* x, const void* w_router, const int32_t* ids,
                                   const float* scores, const float* dscore, void* dx, int32_t accumulate_dx,
                                   float* dw_router, int32_t accumulate_dw, void* stream);
+
+/* ---- MXFP8 variant of the expert GEMMs (reading R28) ----
+ * The paper trains in BF16; this variant is the build's extension.  Block format:
+ * 32 consecutive elements along a GEMM's K share one E8M0 scale 2^E, E the smallest integer with
+ * amax <= 448 * 2^E (no element clips; E = 0 for an all-zero block); elements are E4M3,
+ * round-to-nearest-even.  Quantised operands: x and W_gate/W_up rows along h, a and W_down rows
+ * along g (forward and recompute); dG||dU and W_gate/W_up columns along g (dX).  The dA GEMM
+ * (bound by its fused epilogue) and the weight gradients stay BF16 x BF16 -> fp32.
+ *
+ * memfine_mx_weights_bytes: bytes of the quantised-weights buffer for dims (dtype MXFP8).
+ * memfine_mx_quantize_weights: quantise the handle's local experts' bf16 weights (dev, the
+ *   layouts of memfine_moe_fwd) into wq (dev, caller-owned, >= memfine_mx_weights_bytes;
+ *   MEMFINE_ERR_WORKSPACE if smaller) and bind wq to the handle: every later fwd/bwd of an
+ *   MXFP8 handle reads it (call again after each weight update; fwd/bwd before the first call
+ *   return MEMFINE_ERR_INVALID_ARG).  Stream-ordered.
+ * memfine_mx_quantize: the block format on its own: src dev bf16 [rows][K] -> codes dev uint8
+ *   [rows][K] (E4M3) and scales dev uint8 [rows*K/32] (E + 127) in the tcgen05 scale-chunk
+ *   layout (byte of row r, block b: ((r/128)*(K/128) + b/4)*512 + (r%32)*16 + ((r%128)/32)*4
+ *   + b%4).  rows % 128 == 0, K % 128 == 0. */
+memfine_status memfine_mx_weights_bytes(const memfine_dims* dims, uint64_t* bytes);
+memfine_status memfine_mx_quantize_weights(memfine_handle_t h, const void* w_gate, const void* w_up,
+                                           const void* w_down, void* wq, uint64_t wq_bytes, void* stream);
+memfine_status memfine_mx_quantize(const void* src, int64_t rows, int32_t K, void* codes, void* scales,
+                                   void* stream);
 
 /* Synchronise `stream` and return (and clear) any device-latched error. */
 memfine_status memfine_sync(memfine_handle_t h, void* stream);

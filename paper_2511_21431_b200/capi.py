@@ -10,7 +10,7 @@ _PKG = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_PKG, "libmemfine.so")
 
 OK, ERR_INVALID_ARG, ERR_INFEASIBLE, ERR_ROUTING, ERR_CUDA, ERR_NCCL, ERR_WORKSPACE, ERR_UNSUPPORTED = range(8)
-BF16, FP32 = 0, 1
+BF16, FP32, MXFP8 = 0, 1, 2
 RULE_EQ9, RULE_EXACT = 0, 1
 MODEL_PAPER, MODEL_IMPL = 0, 1
 EP_COPY, EP_P2P = 0, 1
@@ -20,7 +20,8 @@ FWD, BWD = 0, 1
 SYMBOLS = ("memfine_abi_version", "memfine_status_str", "memfine_nccl_unique_id", "memfine_create",
            "memfine_destroy", "memfine_local_group_create", "memfine_local_group_destroy", "memfine_create_local", "memfine_set_ep_transport", "memfine_register_workspace", "memfine_route_counts", "memfine_plan", "memfine_workspace_bytes", "memfine_a2a_plan",
            "memfine_moe_fwd", "memfine_moe_bwd", "memfine_router_fwd", "memfine_router_bwd", "memfine_sync", "memfine_last_stats",
-           "memfine_profile_enable", "memfine_profile_read", "memfine_set_debug", "memfine_debug_perm")
+           "memfine_profile_enable", "memfine_profile_read", "memfine_set_debug", "memfine_debug_perm",
+           "memfine_mx_weights_bytes", "memfine_mx_quantize_weights", "memfine_mx_quantize")
 
 PROF_SLOTS = ("gemm_gateup_swiglu", "gemm_down", "gemm_dact_epilogue", "gemm_dx", "gemm_wgrad_down",
               "gemm_wgrad_gateup", "dispatch_permute", "combine_unpermute", "memset", "nccl_exchange")
@@ -113,6 +114,9 @@ def lib():
         L.memfine_profile_read.argtypes = [vp, C.POINTER(Profile)]
         L.memfine_set_debug.argtypes = [vp, i32]
         L.memfine_debug_perm.argtypes = [vp, i32, vp, i64, C.POINTER(i64)]
+        L.memfine_mx_weights_bytes.argtypes = [C.POINTER(Dims), C.POINTER(u64)]
+        L.memfine_mx_quantize_weights.argtypes = [vp, vp, vp, vp, vp, u64, vp]
+        L.memfine_mx_quantize.argtypes = [vp, i64, i32, vp, vp, vp]
         if L.memfine_abi_version() != 1:
             raise RuntimeError("libmemfine.so ABI mismatch")
         _lib = L

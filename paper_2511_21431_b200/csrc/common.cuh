@@ -2,6 +2,7 @@
 #pragma once
 #include <cuda_runtime.h>
 #include <cuda_bf16.h>
+#include <cuda_fp8.h>
 #include <stdint.h>
 #include "../../include/memfine.h"
 
@@ -65,6 +66,30 @@ __device__ __forceinline__ int expert_of_row(const int* __restrict__ seg, int El
 // The local expert owning 256-row pair `pair` (pseg: prefix of ceil(m_tiles_e / 2)).
 __device__ __forceinline__ int expert_of_pair(const int* __restrict__ pseg, int El, int pair) {
   return expert_of_row(pseg, El, pair);
+}
+
+// ------------------------------------------------------------------ MXFP8 (DESIGN reading R28)
+// Block of 32 consecutive elements along K, one E8M0 scale 2^E: E is the smallest integer with
+// amax <= 448 * 2^E (448 = E4M3 max, so no element clips), E = 0 for an all-zero block, clamped
+// to [-127, 126]; elements v * 2^-E rounded to E4M3 (round-to-nearest-even, satfinite).
+__device__ __forceinline__ int mx_exp(float amax) {
+  if (!(amax > 0.f)) return 0;
+  int e;
+  const float m = frexpf(amax, &e);              // amax = m 2^e, m in [0.5, 1): exact
+  int E = e - 9 + (m > 0.875f ? 1 : 0);          // floor(log2 amax) - 8 (+1 if mantissa > 1.75)
+  return E < -127 ? -127 : (E > 126 ? 126 : E);
+}
+// 2^-E as a float (exact: 127 - E in [1, 254])
+__device__ __forceinline__ float mx_inv_scale(int E) { return __uint_as_float((uint32_t)(127 - E) << 23); }
+// two floats -> packed E4M3 pair (lo byte = a)
+__device__ __forceinline__ uint32_t mx_e4m3x2(float a, float b) {
+  return (uint32_t)__nv_cvt_float2_to_fp8x2(make_float2(a, b), __NV_SATFINITE, __NV_E4M3);
+}
+// Scale-factor chunk layout read by tcgen05.cp 32x128b.warpx4 + the block-scaled MMA: a 512-byte
+// chunk per 128 rows x 128 K (4 blocks); chunk (r/128, k/128) at ((r/128) * (K/128) + k/128) * 512,
+// row r, block kb (= k/32) at byte (r % 32) * 16 + ((r % 128) / 32) * 4 + kb % 4.
+__host__ __device__ __forceinline__ int64_t mx_sf_off(int64_t r, int64_t kb, int64_t K) {
+  return ((r >> 7) * (K >> 7) + (kb >> 2)) * 512 + (r & 31) * 16 + ((r & 127) >> 5) * 4 + (kb & 3);
 }
 
 }  // namespace memfine

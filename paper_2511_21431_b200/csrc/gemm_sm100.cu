@@ -109,6 +109,19 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
   asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }
 
+// the same without the wait (issue several, then one tmem_wait_ld)
+__device__ __forceinline__ void tmem_ld32_nw(uint32_t taddr, uint32_t (&r)[32]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, "
+      "%15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31}, [%32];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]),
+        "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]),
+        "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      : "r"(taddr));
+}
+__device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+
 __device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&r)[16]) {
   asm volatile(
       "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, "
@@ -230,6 +243,59 @@ __device__ __forceinline__ void stage_f32_row(uint8_t* buf, int r, const float* 
         make_float4(v[4 * c], v[4 * c + 1], v[4 * c + 2], v[4 * c + 3]);
 }
 
+// ------------------------------------------------------------------ MXFP8 (block-scaled) helpers
+// Instruction descriptor, kind::mxf8f6f4.block_scale: A/B E4M3 (format 0), K-major, N>>3 at 17,
+// scale format E8M0 (bit 23), M>>4 at 24; the scale-factor byte ids (which of the 4 blocks of a
+// 128-K chunk) of B at [4,6) and of A at [29,31).
+__host__ __device__ constexpr uint32_t idesc_mx(int M, int N) {
+  return ((uint32_t)(N >> 3) << 17) | (1u << 23) | ((uint32_t)(M >> 4) << 24);
+}
+__device__ __forceinline__ void mma_mx(uint32_t d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc,
+                                       uint32_t tsfa, uint32_t tsfb) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::mxf8f6f4.block_scale [%0], %1, %2, %3, [%5], [%6], p;\n}" ::"r"(d),
+      "l"(a), "l"(b), "r"(idesc), "r"(acc), "r"(tsfa), "r"(tsfb)
+      : "memory");
+}
+// SMEM descriptor of one 512-byte scale chunk (32 rows x 16 B, no swizzle; 8-row groups 128 B apart)
+__device__ __forceinline__ uint64_t sdesc_sf(uint32_t saddr) {
+  uint64_t d = (uint64_t)((saddr & 0x3FFFFu) >> 4);
+  d |= (uint64_t)(128 >> 4) << 16;
+  d |= (uint64_t)(128 >> 4) << 32;
+  d |= (uint64_t)1 << 46;
+  return d;
+}
+// smem chunk -> TMEM: 32 lanes x 128 bits, replicated to the 4 lane quarters (4 columns)
+__device__ __forceinline__ void utccp_sf(uint32_t taddr, uint64_t sd) {
+  asm volatile("tcgen05.cp.cta_group::1.32x128b.warpx4 [%0], %1;" ::"r"(taddr), "l"(sd) : "memory");
+}
+// plain bulk copy global -> shared, completing on an mbarrier
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   su32(dst)),
+               "l"(src), "r"(bytes), "r"(su32(bar))
+               : "memory");
+}
+// cta_group::2 variants (MX pairs): the leader issues for both CTAs; each CTA's scale chunk goes
+// from its own smem to its own TMEM.
+__device__ __forceinline__ void mma_mx_pair(uint32_t d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc,
+                                            uint32_t tsfa, uint32_t tsfb) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::2.kind::mxf8f6f4.block_scale [%0], %1, %2, %3, [%5], [%6], p;\n}" ::"r"(d),
+      "l"(a), "l"(b), "r"(idesc), "r"(acc), "r"(tsfa), "r"(tsfb)
+      : "memory");
+}
+__device__ __forceinline__ void utccp_sf_pair(uint32_t taddr, uint64_t sd) {
+  asm volatile("tcgen05.cp.cta_group::2.32x128b.warpx4 [%0], %1;" ::"r"(taddr), "l"(sd) : "memory");
+}
+// 0: one N=256 block-scaled MMA (B scales of rows 128..255 four TMEM columns after rows 0..127);
+// 1: two N=128 MMAs (each with its own B scale chunk).  MEMFINE_MX_SPLITN selects 1 at launch.
+constexpr int kMxSf = 12;   // TMEM columns of scale factors: A 4, B 2 x 4
+
 // ------------------------------------------------------------------ per-kind configuration
 template <int KIND>
 struct Cfg;
@@ -246,9 +312,18 @@ template <> struct Cfg<GK_DX> { static constexpr int BN = 256, NACC = 1, A_MN = 
 template <> struct Cfg<GK_WGRAD_DOWN> { static constexpr int BN = 256, NACC = 1, A_MN = 1, B_MN = 1; };
 template <> struct Cfg<GK_WGRAD_GU> { static constexpr int BN = 256, NACC = 1, A_MN = 1, B_MN = 1; };
 
+// MX kernels (gate/up, down, dX): the same tiles, both operands K-major.
+template <int KIND, bool MX>
+struct CfgX {
+  static constexpr int BN = Cfg<KIND>::BN;
+  static constexpr int NACC = Cfg<KIND>::NACC;
+  static constexpr int A_MN = MX ? 0 : Cfg<KIND>::A_MN;
+  static constexpr int B_MN = MX ? 0 : Cfg<KIND>::B_MN;
+};
+
 // Epilogue staging per epilogue warp and chunk of 32 columns: output slots x slot bytes,
 // double-buffered across chunks.
-template <int KIND>
+template <int KIND, bool MX = false>
 struct Epi {
   static constexpr int SLOTS = KIND == GK_DACT ? 3 : (KIND == GK_GATEUP ? 2 : 1);
   // dA works in 16-column sub-chunks (32 rows x 32 B, SWIZZLE_32B) so its staging is 24 KB
@@ -258,7 +333,9 @@ struct Epi {
   // (measured: dA 72% -> 82% tensor-active going from 4 to 5 stages); the others double-buffer.
   static constexpr int BUFS = (KIND == GK_DACT || KIND >= GK_WGRAD_DOWN) ? 1 : 2;
   static constexpr int WARP_BYTES = BUFS * CHUNK_BYTES;
-  static constexpr int TOTAL = EPI_WARPS * WARP_BYTES;
+  // MX N=256 kinds store straight from registers (early accumulator release): no staging, so the
+  // mainloop gets the smem for more stages.
+  static constexpr int TOTAL = MX ? 0 : EPI_WARPS * WARP_BYTES;
 };
 
 struct Params {
@@ -280,6 +357,13 @@ struct Params {
   int beta;          // WGRAD: 1 = dW += acc (accumulate), 0 = dW = acc (first chunk, overwrite)
   const uint64_t* row_addr;  // DOWN / DX fused EP combine: per-row peer destination (0 = padding)
   int group_m;       // M tiles per raster group (host-sized so a wave's operands stay in L2)
+  // MXFP8 (MX kernels): scale chunks of A and B, GATEUP forward's quantised a
+  const uint8_t* mx_a_sf;
+  const uint8_t* mx_b0_sf;
+  const uint8_t* mx_b1_sf;
+  uint8_t* mx_aq;
+  uint8_t* mx_aq_sf;
+  int mx_split_n;
 };
 
 struct Tile {
@@ -334,18 +418,18 @@ __device__ __forceinline__ void mbar_arrive_leader(uint64_t* b) {
   asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(su32(b) & kPeerMask) : "memory");
 }
 
-template <int KIND, bool PAIR>
+template <int KIND, bool PAIR, bool MX = false>
 __device__ __forceinline__ int num_tiles(const Params& p) {
-  constexpr int BN = Cfg<KIND>::BN;
+  constexpr int BN = CfgX<KIND, MX>::BN;
   int nt = (p.N + BN - 1) / BN;
   if (KIND >= GK_WGRAD_DOWN) return p.El * p.num_mt_w * nt;
   if (p.info[kInfoSkip]) return 0;
   return (PAIR ? p.info[kInfoPairs] : p.info[kInfoRowsPad] / BM) * nt;
 }
 
-template <int KIND, bool PAIR>
+template <int KIND, bool PAIR, bool MX = false>
 __device__ __forceinline__ Tile tile_of(const Params& p, int t) {
-  constexpr int BN = Cfg<KIND>::BN;
+  constexpr int BN = CfgX<KIND, MX>::BN;
   constexpr int TM = PAIR ? 2 * BM : BM;  // rows per (pair) tile
   int nt = (p.N + BN - 1) / BN;
   Tile T;
@@ -382,24 +466,26 @@ __device__ __forceinline__ Tile tile_of(const Params& p, int t) {
     T.m_end = T.m0 + BM;
   }
   T.k0 = 0;
-  T.nkb = p.K / BK;
+  T.nkb = p.K / (MX ? 128 : BK);
   return T;
 }
 
-template <int KIND, bool PAIR>
+// MX stage: A 128 x 128 B + B (N rows) x 128 B (E4M3, 128 K per stage) + 1.5 KB scale chunks, 1 KB aligned
+template <int KIND, bool PAIR, bool MX = false>
 __host__ __device__ constexpr int stage_bytes() {
-  return A_BYTES + (PAIR ? Cfg<KIND>::NACC * Cfg<KIND>::BN / 2 : Cfg<KIND>::NACC * Cfg<KIND>::BN) * BK * 2;
+  return MX ? (A_BYTES + CfgX<KIND, MX>::NACC * CfgX<KIND, MX>::BN * 128 / (PAIR ? 2 : 1) + 1536 + 1023) / 1024 * 1024
+            : A_BYTES + (PAIR ? Cfg<KIND>::NACC * Cfg<KIND>::BN / 2 : Cfg<KIND>::NACC * Cfg<KIND>::BN) * BK * 2;
 }
 // as many 1024-aligned stages as fit next to the epilogue staging (227 KB per CTA)
-template <int KIND, bool PAIR>
+template <int KIND, bool PAIR, bool MX = false>
 __host__ __device__ constexpr int nstage() {
-  return (232448 - 1024 - 512 - Epi<KIND>::TOTAL) / stage_bytes<KIND, PAIR>() > 6
+  return (232448 - 1024 - 512 - Epi<KIND, MX>::TOTAL) / stage_bytes<KIND, PAIR, MX>() > 6
              ? 6
-             : (232448 - 1024 - 512 - Epi<KIND>::TOTAL) / stage_bytes<KIND, PAIR>();
+             : (232448 - 1024 - 512 - Epi<KIND, MX>::TOTAL) / stage_bytes<KIND, PAIR, MX>();
 }
-template <int KIND, bool PAIR>
+template <int KIND, bool PAIR, bool MX = false>
 __host__ __device__ constexpr int smem_bytes() {
-  return nstage<KIND, PAIR>() * stage_bytes<KIND, PAIR>() + Epi<KIND>::TOTAL + 1024 + 512;
+  return nstage<KIND, PAIR, MX>() * stage_bytes<KIND, PAIR, MX>() + Epi<KIND, MX>::TOTAL + 1024 + 512;
 }
 
 // ------------------------------------------------------------------ the kernel
@@ -407,28 +493,40 @@ __host__ __device__ constexpr int smem_bytes() {
 // PAIR = true : a 2-CTA cluster per 256-row tile, tcgen05.mma.cta_group::2 (M=256) issued by the
 //               even CTA; each CTA stages 128 rows of A and half of B's columns, each CTA's TMEM
 //               holds its 128 rows x N accumulator.  Per-CTA operand traffic drops by a third.
-template <int KIND, bool PAIR>
+// MX = true: MXFP8 operands (kind::mxf8f6f4.block_scale, cta_group::1, K-major A and B, 128 K
+//            per stage, N=256 tiles with one accumulator stage + 12 scale-factor columns in TMEM,
+//            drained early into registers by the epilogue).  MX && PAIR: cta_group::2 (M = 256) like the BF16 pairs - each CTA
+//            stages its 128 A rows and half of B, so the tensor core's smem reads per CTA halve;
+//            scale chunks come by TMA (uint32 rows of 512 B): each CTA holds its own A scales and
+//            the full B tile's scales.
+template <int KIND, bool PAIR, bool MX = false>
 __global__ void __launch_bounds__(THREADS, 1)
     gemm_kernel(const __grid_constant__ Params p, const __grid_constant__ CUtensorMap tmA,
                 const __grid_constant__ CUtensorMap tmB0, const __grid_constant__ CUtensorMap tmB1,
-                const __grid_constant__ CUtensorMap tmO0, const __grid_constant__ CUtensorMap tmO1) {
-  using CF = Cfg<KIND>;
+                const __grid_constant__ CUtensorMap tmO0, const __grid_constant__ CUtensorMap tmO1,
+                const __grid_constant__ CUtensorMap tmSA, const __grid_constant__ CUtensorMap tmSB0,
+                const __grid_constant__ CUtensorMap tmSB1) {
+  using CF = CfgX<KIND, MX>;
   constexpr int BN = CF::BN, NACC = CF::NACC;
   constexpr int MMA_N = NACC * BN;                      // GATEUP: G||U in one MMA (N = 256)
   static_assert(MMA_N <= 256, "MMA N");
-  constexpr int B_ROWS = PAIR ? MMA_N / 2 : MMA_N;      // B rows (N) staged per CTA
-  constexpr int B_BYTES = B_ROWS * BK * 2;
-  constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
-  constexpr int NSTAGE = nstage<KIND, PAIR>();
+  constexpr bool G2 = PAIR;                             // cta_group::2 pair
+  constexpr int B_ROWS = G2 ? MMA_N / 2 : MMA_N;        // B rows (N) staged per CTA
+  constexpr int B_BYTES = B_ROWS * BK * 2;               // (MX: B_ROWS x 128 E4M3 = the same bytes)
+  constexpr int STAGE_BYTES = stage_bytes<KIND, PAIR, MX>();
+  constexpr int NSTAGE = nstage<KIND, PAIR, MX>();
   constexpr int ACC_COLS = MMA_N;                       // per accumulator stage
-  constexpr uint32_t TMEM_COLS = 2 * ACC_COLS;          // double-buffered
-  static_assert(TMEM_COLS <= 512, "TMEM");
+  constexpr int ACC_ST = (MX && MMA_N == 256) ? 1 : 2;  // accumulator stages (MX N=256: scales take TMEM)
+  constexpr uint32_t TMEM_COLS = MX ? 512 : 2 * ACC_COLS;
+  constexpr uint32_t SF_COL = ACC_ST * ACC_COLS;        // MX: A scales at +0..3, B at +4..11
+  static_assert(TMEM_COLS <= 512 && (!MX || ACC_ST * ACC_COLS + kMxSf <= 512), "TMEM");
+  static_assert(!MX || KIND == GK_GATEUP || KIND == GK_DOWN || KIND == GK_DX, "MX: gate/up, down, dX");
   constexpr uint32_t IDESC = idesc_bf16(PAIR ? 2 * BM : BM, MMA_N, CF::A_MN, CF::B_MN);
 
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   uint8_t* epi_smem = smem + NSTAGE * STAGE_BYTES;      // 1024-aligned (STAGE_BYTES is)
-  uint64_t* full = (uint64_t*)(epi_smem + Epi<KIND>::TOTAL);
+  uint64_t* full = (uint64_t*)(epi_smem + Epi<KIND, MX>::TOTAL);
   uint64_t* empty = full + NSTAGE;
   uint64_t* tfull = empty + NSTAGE;
   uint64_t* tempty = tfull + 2;
@@ -446,14 +544,19 @@ __global__ void __launch_bounds__(THREADS, 1)
     if (KIND == GK_GATEUP || KIND == GK_DX) prefetch_tmap(&tmB1);
     prefetch_tmap(&tmO0);
     if (KIND == GK_GATEUP || KIND == GK_DACT || KIND == GK_WGRAD_GU) prefetch_tmap(&tmO1);
+    if (MX) {
+      prefetch_tmap(&tmSA);
+      prefetch_tmap(&tmSB0);
+      if (KIND == GK_GATEUP || KIND == GK_DX) prefetch_tmap(&tmSB1);
+    }
     for (int s = 0; s < NSTAGE; s++) { mbar_init(full + s, 1); mbar_init(empty + s, 1); }
-    for (int a = 0; a < 2; a++) { mbar_init(tfull + a, 1); mbar_init(tempty + a, (PAIR ? 2 : 1) * EPI_WARPS); }
+    for (int a = 0; a < 2; a++) { mbar_init(tfull + a, 1); mbar_init(tempty + a, (G2 ? 2 : 1) * EPI_WARPS); }
     for (int i = 0; i < 2 * EPI_WARPS; i++) mbar_init(ebar + i, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   }
   if (warp == 1) {
-    if (PAIR) {
+    if (G2) {
       asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(su32(tmem_slot)),
                    "r"(TMEM_COLS)
                    : "memory");
@@ -469,7 +572,8 @@ __global__ void __launch_bounds__(THREADS, 1)
   if (PAIR) cluster_sync(); else __syncthreads();
   fence_after();
   const uint32_t tmem_base = *tmem_slot;
-  const int ntiles = num_tiles<KIND, PAIR>(p);
+  const int ntiles = num_tiles<KIND, PAIR, MX>(p);
+  (void)SF_COL;
 
   if (warp == 0) {
     // ================================================================ TMA producer (both CTAs)
@@ -477,12 +581,54 @@ __global__ void __launch_bounds__(THREADS, 1)
       int stage = 0;
       uint32_t phase = 0;
       for (int t = cid; t < ntiles; t += ncid) {
-        Tile T = tile_of<KIND, PAIR>(p, t);
+        Tile T = tile_of<KIND, PAIR, MX>(p, t);
         const int am0 = T.m0 + (int)rank * BM;              // this CTA's A rows
         for (int kb = 0; kb < T.nkb; kb++) {
           mbar_wait(empty + stage, phase ^ 1);
           uint8_t* sa = smem + stage * STAGE_BYTES;
           uint8_t* sb = sa + A_BYTES;
+          if constexpr (MX) {
+            // E4M3 A [128 rows x 128 K], this CTA's B rows (all, or its half in a pair) and the scale
+            // chunks: own A rows' chunk, the whole B tile's chunks (TMA zero-fills chunks and rows
+            // past the end - ragged N tiles, a pair's second m-tile past the buffer)
+            const int kc = kb * 128;
+            uint8_t* ssf = sb + B_BYTES;
+            const int KB = p.K >> 7;
+            constexpr int SFB_CH = MMA_N / 128;
+            if (leader) mbar_expect_tx(full + stage, (PAIR ? 2 : 1) * (A_BYTES + B_BYTES + 512 + 512 * SFB_CH));
+            auto L2 = [&](void* dst, const CUtensorMap* m, int c0, int c1) {
+              if (PAIR) tma_2d_pair(dst, m, full + stage, c0, c1); else tma_2d(dst, m, full + stage, c0, c1);
+            };
+            auto L3 = [&](void* dst, const CUtensorMap* m, int c0, int c1, int c2) {
+              if (PAIR) tma_3d_pair(dst, m, full + stage, c0, c1, c2); else tma_3d(dst, m, full + stage, c0, c1, c2);
+            };
+            L2(sa, &tmA, kc, am0);
+            L2(ssf, &tmSA, 0, (am0 >> 7) * KB + kb);
+            if (KIND == GK_GATEUP) {
+              if (PAIR) {
+                L3(sb, rank ? &tmB1 : &tmB0, kc, T.n0, T.e);       // CTA0: W_gate rows, CTA1: W_up rows
+              } else {
+                L3(sb, &tmB0, kc, T.n0, T.e);
+                L3(sb + B_BYTES / 2, &tmB1, kc, T.n0, T.e);
+              }
+              const int ci = (T.e * (p.N >> 7) + (T.n0 >> 7)) * KB + kb;
+              L2(ssf + 512, &tmSB0, 0, ci);
+              L2(ssf + 1024, &tmSB1, 0, ci);
+            } else {
+              // DOWN: W_down rows; DACT: W_down^T rows; DX: W_gate^T (k < g) / W_up^T rows
+              const bool lo = KIND != GK_DX || kc < p.g;
+              const int kk = lo ? kc : kc - p.g;
+              const int KW = KIND == GK_DX ? (p.g >> 7) : KB;       // K chunks of the weight
+              L3(sb, lo ? &tmB0 : &tmB1, kk, T.n0 + (PAIR ? (int)rank * B_ROWS : 0), T.e);
+              const int ci = (T.e * (p.N >> 7) + (T.n0 >> 7)) * KW + (kk >> 7);
+              const int nvalid = (p.N - T.n0 + 127) >> 7;           // B chunks inside this expert
+#pragma unroll
+              for (int i = 0; i < SFB_CH; i++)
+                L2(ssf + 512 + 512 * i, lo ? &tmSB0 : &tmSB1, 0, i < nvalid ? ci + i * KW : ci);
+            }
+            if (++stage == NSTAGE) { stage = 0; phase ^= 1; }
+            continue;
+          }
           if (leader) mbar_expect_tx(full + stage, (PAIR ? 2 : 1) * STAGE_BYTES);
           int kc = T.k0 + kb * BK;
           auto L2 = [&](void* dst, const CUtensorMap* m, int c0, int c1) {
@@ -532,10 +678,10 @@ __global__ void __launch_bounds__(THREADS, 1)
       uint32_t phase = 0;
       int it = 0;
       for (int t = cid; t < ntiles; t += ncid) {
-        Tile T = tile_of<KIND, PAIR>(p, t);
+        Tile T = tile_of<KIND, PAIR, MX>(p, t);
         if (T.nkb == 0) continue;
-        int as = it & 1;
-        uint32_t aph = (it >> 1) & 1;
+        int as = it % ACC_ST;
+        uint32_t aph = (it / ACC_ST) & 1;
         mbar_wait(tempty + as, aph ^ 1);
         fence_after();
         uint32_t dbase = tmem_base + as * ACC_COLS;
@@ -544,6 +690,40 @@ __global__ void __launch_bounds__(THREADS, 1)
           fence_after();
           uint32_t sa = su32(smem + stage * STAGE_BYTES);
           uint32_t sb = sa + A_BYTES;
+          if constexpr (MX) {
+            // scales smem -> TMEM (executes in order with the MMAs: the previous stage's MMAs
+            // have read the columns before these copies land)
+            const uint32_t ssf = sb + B_BYTES;
+            const uint32_t tsf = tmem_base + SF_COL;
+            constexpr int SFB_CH = MMA_N / 128;
+#pragma unroll
+            for (int i = 0; i <= SFB_CH; i++) {
+              if (PAIR) utccp_sf_pair(tsf + 4 * i, sdesc_sf(ssf + 512 * i));
+              else utccp_sf(tsf + 4 * i, sdesc_sf(ssf + 512 * i));
+            }
+#pragma unroll
+            for (int k = 0; k < 4; k++) {
+              const uint64_t ad = sdesc(sa + k * 32, 16, 1024);
+              const uint32_t ids = ((uint32_t)k << 29) | ((uint32_t)k << 4);
+              if (PAIR) {
+                const uint64_t bd = sdesc(sb + k * 32, 16, 1024);
+                mma_mx_pair(dbase, ad, bd, idesc_mx(2 * BM, MMA_N) | ids, (kb | k) != 0, tsf, tsf + 4);
+              } else if (MMA_N == 128 || !(p.mx_split_n & 1)) {
+                const uint64_t bd = sdesc(sb + k * 32, 16, 1024);
+                mma_mx(dbase, ad, bd, idesc_mx(BM, MMA_N) | ids, (kb | k) != 0, tsf, tsf + 4);
+              } else {
+#pragma unroll
+                for (int hn = 0; hn < 2; hn++) {
+                  const uint64_t bd = sdesc(sb + hn * (B_BYTES / 2) + k * 32, 16, 1024);
+                  mma_mx(dbase + hn * (MMA_N / 2), ad, bd, idesc_mx(BM, MMA_N >= 256 ? 128 : MMA_N) | ids,
+                         (kb | k) != 0, tsf, tsf + 4 + 4 * hn);
+                }
+              }
+            }
+            if (PAIR) mma_commit_pair(empty + stage); else mma_commit(empty + stage);
+            if (++stage == NSTAGE) { stage = 0; phase ^= 1; }
+            continue;
+          }
 #pragma unroll
           for (int k = 0; k < BK / 16; k++) {
             uint64_t ad = CF::A_MN ? sdesc(sa + k * 2048, 8192, 1024) : sdesc(sa + k * 32, 16, 1024);
@@ -554,7 +734,7 @@ __global__ void __launch_bounds__(THREADS, 1)
           if (PAIR) mma_commit_pair(empty + stage); else mma_commit(empty + stage);
           if (++stage == NSTAGE) { stage = 0; phase ^= 1; }
         }
-        if (PAIR) mma_commit_pair(tfull + as); else mma_commit(tfull + as);
+        if (G2) mma_commit_pair(tfull + as); else mma_commit(tfull + as);
         it++;
       }
     }
@@ -568,7 +748,7 @@ __global__ void __launch_bounds__(THREADS, 1)
     const int ew = warp - 2;              // epilogue warp index 0..7
     const int rloc = q * 32 + lane;       // row within this CTA's 128 rows
     constexpr int CPW = BN / 2;           // columns per epilogue warp
-    using EP = Epi<KIND>;
+    using EP = Epi<KIND, MX>;
     uint8_t* wbuf = epi_smem + ew * EP::WARP_BYTES;
     int sbuf = 0;
     int it = 0;
@@ -595,7 +775,7 @@ __global__ void __launch_bounds__(THREADS, 1)
       return b;
     };
     for (int t = cid; t < ntiles; t += ncid) {
-      Tile T = tile_of<KIND, PAIR>(p, t);
+      Tile T = tile_of<KIND, PAIR, MX>(p, t);
       const int row0 = T.m0 + (int)rank * BM + q * 32;     // first row of this warp's 32 rows
       const int rowi = row0 + lane;
       const bool rows_ok = row0 < T.m_end;                 // warp-uniform (halves are 128-row aligned)
@@ -621,9 +801,73 @@ __global__ void __launch_bounds__(THREADS, 1)
         }
         continue;
       }
-      int as = it & 1;
-      uint32_t aph = (it >> 1) & 1;
+      int as = it % ACC_ST;
+      uint32_t aph = (it / ACC_ST) & 1;
       const int64_t row = rowi;
+      if constexpr (MX && ACC_ST == 1) {
+        // One accumulator stage (the scales take the rest of TMEM): drain this warp's slice of
+        // the tile into registers, free TMEM for the next tile's MMAs, then run the epilogue from
+        // registers - the mainloop of tile i+1 overlaps the math and stores of tile i.
+        constexpr int NCH = CPW / 32;
+        uint32_t acc[NCH][32];
+        uint32_t acc2[KIND == GK_GATEUP ? NCH : 1][32];
+        mbar_wait(tfull + as, aph);
+        fence_after();
+        const uint32_t tb = tmem_base + ((uint32_t)(q * 32) << 16);
+#pragma unroll
+        for (int i = 0; i < NCH; i++) {
+          tmem_ld32_nw(tb + half * CPW + 32 * i, acc[i]);
+          if constexpr (KIND == GK_GATEUP) tmem_ld32_nw(tb + BN + half * CPW + 32 * i, acc2[i]);
+        }
+        tmem_wait_ld();
+        fence_before();
+        __syncwarp();
+        if (lane == 0) {
+          if (PAIR) mbar_arrive_leader(tempty + as); else mbar_arrive(tempty + as);
+        }
+#pragma unroll
+        for (int i = 0; i < NCH; i++) {
+          const int n = T.n0 + half * CPW + 32 * i;
+          float v[32];
+#pragma unroll
+          for (int j = 0; j < 32; j++) v[j] = __uint_as_float(acc[i][j]);
+          if constexpr (KIND == GK_GATEUP) {
+            if (!rows_ok || n >= p.g) continue;
+            if (!p.store_gu) {
+              // a = silu(G) U straight to MXFP8: this thread's 32 columns are one block
+              float a[32];
+              float amax = 0.f;
+#pragma unroll
+              for (int j = 0; j < 32; j++) {
+                a[j] = silu_f(v[j]) * __uint_as_float(acc2[i][j]);
+                amax = fmaxf(amax, fabsf(a[j]));
+              }
+              const int E = mx_exp(amax);
+              const float inv = mx_inv_scale(E);
+              uint32_t o[8];
+#pragma unroll
+              for (int j = 0; j < 8; j++)
+                o[j] = mx_e4m3x2(a[4 * j] * inv, a[4 * j + 1] * inv) |
+                       (mx_e4m3x2(a[4 * j + 2] * inv, a[4 * j + 3] * inv) << 16);
+              st256(p.mx_aq + row * p.g + n, o);
+              p.mx_aq_sf[mx_sf_off(row, n >> 5, p.g)] = (uint8_t)(E + 127);
+            } else {
+              // G -> GU[row, n..n+31], U -> GU[row, g + n..]: 64 B each, straight from registers
+              float u[32];
+#pragma unroll
+              for (int j = 0; j < 32; j++) u[j] = __uint_as_float(acc2[i][j]);
+              __nv_bfloat16* gu = p.GU + row * (2 * (int64_t)p.g);
+              store32_bf16(gu + n, v);
+              store32_bf16(gu + p.g + n, u);
+            }
+          } else {
+            if (!rows_ok || n >= p.h) continue;                 // DOWN / DX: N = h
+            store32_bf16(p.O + row * (int64_t)p.h + n, v);
+          }
+        }
+        it++;
+        continue;
+      }
       float dwp = 0.f;
       float wrow = 0.f;
       if (KIND == GK_DACT && rows_ok) {
@@ -770,7 +1014,7 @@ __global__ void __launch_bounds__(THREADS, 1)
       fence_before();
       __syncwarp();
       if (lane == 0) {
-        if (PAIR) mbar_arrive_leader(tempty + as); else mbar_arrive(tempty + as);
+        if (G2) mbar_arrive_leader(tempty + as); else mbar_arrive(tempty + as);
       }
       it++;
     }
@@ -781,7 +1025,7 @@ __global__ void __launch_bounds__(THREADS, 1)
   if (PAIR) cluster_sync(); else __syncthreads();
   fence_after();
   if (warp == 1) {
-    if (PAIR)
+    if (G2)
       asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(TMEM_COLS)
                    : "memory");
     else
@@ -1014,7 +1258,10 @@ int launch(const GemmProblem<__nv_bfloat16>& gp, cudaStream_t st) {
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  if (cudaLaunchKernelEx(&cfg, gemm_kernel<KIND, PAIR>, p, mA, mB0, mB1, mO0, mO1) != cudaSuccess) return -1;
+  CUtensorMap none;
+  memset(&none, 0, sizeof none);
+  if (cudaLaunchKernelEx(&cfg, gemm_kernel<KIND, PAIR>, p, mA, mB0, mB1, mO0, mO1, none, none, none) != cudaSuccess)
+    return -1;
   return 1;
 }
 
@@ -1023,9 +1270,177 @@ int launch_kind(const GemmProblem<__nv_bfloat16>& gp, cudaStream_t st) {
   return use_pairs() ? launch<KIND, true>(gp, st) : launch<KIND, false>(gp, st);
 }
 
+// E4M3 maps: K-major rows, 128 K (bytes) x box rows, 128B swizzle
+bool map_fp8_2d(CUtensorMap* m, const void* base, uint64_t K, uint64_t rows) {
+  uint64_t d[2] = {K, rows};
+  uint32_t b[2] = {128, 128};
+  return make_map_t(m, CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, CU_TENSOR_MAP_SWIZZLE_128B, base, 2, d, b);
+}
+bool map_fp8_3d(CUtensorMap* m, const void* base, uint64_t K, uint64_t rows, uint64_t El, uint32_t box_rows) {
+  uint64_t d[3] = {K, rows, El};
+  uint32_t b[3] = {128, box_rows, 1};
+  return make_map_t(m, CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, CU_TENSOR_MAP_SWIZZLE_128B, base, 3, d, b);
+}
+
+// MEMFINE_MX_SPLITN=1 (1-CTA only): two N=128 block-scaled MMAs instead of one N=256
+int mx_flags() {
+  static int v = -1;
+  if (v < 0) {
+    const char* s = getenv("MEMFINE_MX_SPLITN");
+    v = (s && s[0] == '1') ? 1 : 0;
+  }
+  return v;
+}
+
+bool mx_pairs() {
+  static int v = -1;
+  if (v < 0) {
+    const char* s = getenv("MEMFINE_MX_CTA");
+    v = (s && s[0] == '1') ? 0 : 1;   // default: cta_group::2 pairs; MEMFINE_MX_CTA=1 for 1-CTA
+  }
+  return v == 1;
+}
+// scale chunks as uint32 rows of 128 words (512 B), one TMA box per chunk
+bool map_sf(CUtensorMap* m, const void* base, uint64_t nchunks) {
+  uint64_t d[2] = {128, nchunks};
+  uint32_t b[2] = {128, 1};
+  return make_map_t(m, CU_TENSOR_MAP_DATA_TYPE_UINT32, 4, CU_TENSOR_MAP_SWIZZLE_NONE, base, 2, d, b);
+}
+
+// MXFP8 launch (K-major E4M3 operands, block scales): the four M-tiled kinds; PAIR = cta_group::2.
+template <int KIND, bool PAIR>
+int launch_mx(const GemmProblem<__nv_bfloat16>& gp, cudaStream_t st) {
+  constexpr int SMEM = smem_bytes<KIND, PAIR, true>();
+  static_assert(SMEM <= 232448, "smem");
+  constexpr int BROWS = CfgX<KIND, true>::NACC * CfgX<KIND, true>::BN;     // B tile rows
+  constexpr uint32_t BOX = KIND == GK_GATEUP ? 128 : (PAIR ? BROWS / 2 : BROWS);  // B rows per TMA load
+  static bool attr_set = false;
+  if (!attr_set) {
+    if (cudaFuncSetAttribute(gemm_kernel<KIND, PAIR, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM) !=
+        cudaSuccess)
+      return -1;
+    attr_set = true;
+  }
+  if (!g_num_sms) {
+    int dev;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
+  }
+  Params p{};
+  p.El = gp.El;
+  p.h = gp.h;
+  p.g = gp.g;
+  p.rows_cap = gp.rows_cap;
+  p.seg = gp.seg;
+  p.pseg = gp.pseg;
+  p.info = gp.info;
+  p.GU = gp.GU;
+  p.A = gp.A;
+  p.O = gp.O;
+  p.w_row = gp.w_row;
+  p.dw_row = gp.dw_row;
+  p.store_a = gp.store_a;
+  p.store_gu = gp.store_gu;
+  p.row_addr = gp.row_addr;
+  p.mx_a_sf = gp.mx_a.sf;
+  p.mx_b0_sf = gp.mx_b0.sf;
+  p.mx_b1_sf = gp.mx_b1.sf;
+  p.mx_aq = gp.mx_aq;
+  p.mx_aq_sf = gp.mx_aq_sf;
+  p.mx_split_n = mx_flags();
+  const uint64_t R = (uint64_t)gp.rows_cap, h = gp.h, g = gp.g, El = gp.El;
+  if (R == 0) return 0;
+  if (h % 128 || g % 128 || R % 128) return -1;
+  CUtensorMap mA, mB0, mB1, mO0, mO1, mSA, mSB0, mSB1;
+  bool ok = true;
+  const uint64_t wch = El * (h / 128) * (g / 128);   // scale chunks of one weight operand
+  switch (KIND) {
+    case GK_GATEUP:
+      p.N = gp.g; p.K = gp.h;
+      ok &= map_sf(&mSB0, gp.mx_b0.sf, wch);
+      ok &= map_sf(&mSB1, gp.mx_b1.sf, wch);
+      ok &= map_fp8_2d(&mA, gp.mx_a.q, h, R);
+      ok &= map_fp8_3d(&mB0, gp.mx_b0.q, h, g, El, 128);
+      ok &= map_fp8_3d(&mB1, gp.mx_b1.q, h, g, El, 128);
+      if (gp.store_gu) {
+        ok &= map2d_st(&mO0, gp.GU, 2 * g, R);
+        mO1 = mO0;
+      } else {
+        memset(&mO0, 0, sizeof mO0);
+        memset(&mO1, 0, sizeof mO1);
+      }
+      break;
+    case GK_DOWN:
+      p.N = gp.h; p.K = gp.g;
+      ok &= map_fp8_2d(&mA, gp.mx_a.q, g, R);
+      ok &= map_fp8_3d(&mB0, gp.mx_b0.q, g, h, El, BOX);
+      mB1 = mB0;
+      ok &= map_sf(&mSB0, gp.mx_b0.sf, wch);
+      mSB1 = mSB0;
+      ok &= map2d_st(&mO0, gp.O, h, R);
+      mO1 = mO0;
+      break;
+    default:  // GK_DX
+      p.N = gp.h; p.K = 2 * gp.g;
+      ok &= map_fp8_2d(&mA, gp.mx_a.q, 2 * g, R);
+      ok &= map_fp8_3d(&mB0, gp.mx_b0.q, g, h, El, BOX);    // W_gate^T [El][h][g]
+      ok &= map_fp8_3d(&mB1, gp.mx_b1.q, g, h, El, BOX);    // W_up^T
+      ok &= map_sf(&mSB0, gp.mx_b0.sf, wch);
+      ok &= map_sf(&mSB1, gp.mx_b1.sf, wch);
+      ok &= map2d_st(&mO0, gp.O, h, R);
+      mO1 = mO0;
+      break;
+  }
+  ok &= map_sf(&mSA, gp.mx_a.sf, (R / 128) * (uint64_t)(p.K / 128));
+  if (!ok) return -1;
+  constexpr int BN = CfgX<KIND, true>::BN;
+  int nt = (p.N + BN - 1) / BN;
+  {
+    static int64_t budget = [] {
+      const char* s = getenv("MEMFINE_L2_GROUP_MB");
+      return (int64_t)(s ? atoi(s) : 24) << 20;
+    }();
+    int64_t a_strip = (int64_t)(PAIR ? 2 : 1) * BM * p.K;   // E4M3: one byte per element
+    p.group_m = (int)std::max<int64_t>(1, std::min<int64_t>(64, (budget ? budget : (24 << 20)) / a_strip));
+  }
+  const int per_unit = PAIR ? 2 : 1;
+  int64_t max_tiles = (int64_t)((R / BM + (PAIR ? El : 0)) / per_unit + 1) * nt;
+  int units = (int)std::min<int64_t>(max_tiles, g_num_sms / per_unit);
+  if (units <= 0) return 0;
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(units * per_unit);
+  cfg.blockDim = dim3(THREADS);
+  cfg.dynamicSmemBytes = SMEM;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = per_unit;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  if (cudaLaunchKernelEx(&cfg, gemm_kernel<KIND, PAIR, true>, p, mA, mB0, mB1, mO0, mO1, mSA, mSB0, mSB1) !=
+      cudaSuccess)
+    return -1;
+  return 1;
+}
+
+template <int KIND>
+int launch_mx_kind(const GemmProblem<__nv_bfloat16>& gp, cudaStream_t st) {
+  return mx_pairs() ? launch_mx<KIND, true>(gp, st) : launch_mx<KIND, false>(gp, st);
+}
+
 }  // namespace sm100
 
 int launch_gemm_sm100(const GemmProblem<__nv_bfloat16>& p, cudaStream_t st) {
+  if (p.mx) {
+    switch (p.kind) {
+      case GK_GATEUP: return sm100::launch_mx_kind<GK_GATEUP>(p, st);
+      case GK_DOWN: return sm100::launch_mx_kind<GK_DOWN>(p, st);
+      case GK_DX: return sm100::launch_mx_kind<GK_DX>(p, st);
+      default: break;   // dA and the weight gradients stay BF16 (reading R28)
+    }
+  }
   switch (p.kind) {
     case GK_GATEUP: return sm100::launch_kind<GK_GATEUP>(p, st);
     case GK_DOWN: return sm100::launch_kind<GK_DOWN>(p, st);

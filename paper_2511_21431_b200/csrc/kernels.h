@@ -112,6 +112,12 @@ enum GemmKind {
   GK_WGRAD_GU = 5     // B5:    dW_gate[e] || dW_up[e] += dGU^T X
 };
 
+// One MXFP8 operand: E4M3 codes (K-major rows) and its scale-factor chunks.
+struct MxOp {
+  const uint8_t* q;
+  const uint8_t* sf;
+};
+
 template <typename T>
 struct GemmProblem {
   int kind;
@@ -138,6 +144,13 @@ struct GemmProblem {
   int wgrad_beta;    // WGRAD: 1 accumulate into dW, 0 overwrite (zero tiles for experts without rows)
   const uint64_t* row_addr;  // DOWN / DX (fused EP combine): per-row destination address in the
                              // source rank's send buffer (peer memory), 0 = padding; null = local O
+  // MXFP8 variant (mx = 1, sm100 path only): E4M3 operands + E8M0 block scales (mx_sf_off layout)
+  int mx;
+  MxOp mx_a;                 // A operand: Xq (GATEUP), Aq (DOWN), DYq (DACT), dGUq (DX)
+  MxOp mx_b0, mx_b1;         // B: W_gate / W_up rows (GATEUP), W_down rows (DOWN), W_down^T (DACT),
+                             //    W_gate^T / W_up^T (DX; K split at g)
+  uint8_t* mx_aq;            // GATEUP forward output: a quantised (codes [R][g]) ...
+  uint8_t* mx_aq_sf;         // ... and its block scales
 };
 
 // CUDA-core FFMA path (MEMFINE_FP32 mode; K12 of SURVEY §2.4).
@@ -146,5 +159,14 @@ int launch_gemm_simt(const GemmProblem<T>& p, cudaStream_t st);
 // tcgen05 / TMEM / TMA path (MEMFINE_BF16).  Returns number of launches or <0 on error.
 int launch_gemm_sm100(const GemmProblem<__nv_bfloat16>& p, cudaStream_t st);
 int sm100_num_sms();
+
+// ---------------------------------------------------------------- MXFP8 quantisation (mx.cu)
+// info != null: rows = the chunk's padded rows (0 if skipped), capped at rows_max; else rows_max.
+// Rows and K multiples of 128 (scale chunks).
+void launch_mx_quant_rows(const __nv_bfloat16* src, int64_t ld, int64_t rows_max, const int* info, int K,
+                          uint8_t* q, uint8_t* sf, cudaStream_t st);
+// src [B][R][Cc] -> q [B][Cc][R] blocked along R (R % 128 == 0, Cc % 128 == 0)
+void launch_mx_quant_transpose(const __nv_bfloat16* src, int B, int R, int Cc, uint8_t* q, uint8_t* sf,
+                               cudaStream_t st);
 
 }  // namespace memfine

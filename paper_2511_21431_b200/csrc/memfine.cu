@@ -53,6 +53,8 @@ struct memfine_handle_s {
   std::vector<char*> peer_ws;      // [EP] (own entry = reg_ws)
   std::vector<void*> ipc_bases;    // opened peer allocation bases (to close)
   int* barrier_d = nullptr;
+  // MXFP8: the bound quantised weights (memfine_mx_quantize_weights)
+  const uint8_t* mx_w = nullptr;
   // router scratch (lazily allocated): logits, d_logits, counting sort of ids by expert
   char* router_scratch = nullptr;
   size_t router_bytes = 0;
@@ -116,11 +118,12 @@ bool dims_ok(const memfine_dims* d) {
   if (d->num_experts < 1 || d->topk < 1 || d->topk > d->num_experts || d->topk > 16) return false;
   if (d->ep_size < 1 || d->num_experts % d->ep_size || d->ep_rank < 0 || d->ep_rank >= d->ep_size) return false;
   if (d->num_experts > 1024) return false;
-  if (d->dtype != MEMFINE_BF16 && d->dtype != MEMFINE_FP32) return false;
+  if (d->dtype != MEMFINE_BF16 && d->dtype != MEMFINE_FP32 && d->dtype != MEMFINE_MXFP8) return false;
+  if (d->dtype == MEMFINE_MXFP8 && (d->hidden % 128 || d->ffn % 128)) return false;
   return true;
 }
 
-int elt_bytes(const memfine_dims& d) { return d.dtype == MEMFINE_BF16 ? 2 : 4; }
+int elt_bytes(const memfine_dims& d) { return d.dtype == MEMFINE_FP32 ? 4 : 2; }  // MXFP8: bf16 storage
 
 // ------------------------------------------------------------------ workspace carving
 // One bump allocator (256-byte aligned) defines the layout; the byte count it reaches is
@@ -148,6 +151,9 @@ struct Layout {
   void* send = nullptr;      // [S][h]   EP>1 staging (x out / o back)
   void* send_dy = nullptr;   // [S][h]   EP>1 bwd
   float* send_w = nullptr;   // [S]      EP>1 scores out / d_score back
+  // MXFP8 operands (E4M3 codes + scale chunks): X, a (fwd) / X, dG||dU (bwd)
+  uint8_t *Xq = nullptr, *Xsf = nullptr, *Aq = nullptr, *Asf = nullptr;
+  uint8_t *GUq = nullptr, *GUsf = nullptr;
   int64_t rows_cap = 0;
   uint64_t meta_bytes = 0, row_bytes = 0, total = 0;
 };
@@ -155,6 +161,13 @@ struct Layout {
 uint64_t row_bytes_of(const memfine_dims& d, int pass) {
   uint64_t D = elt_bytes(d), h = d.hidden, g = d.ffn;
   uint64_t ep = d.ep_size > 1 ? 16 : 0;                            // row_addr, row_addr_w (EP>1)
+  if (d.dtype == MEMFINE_MXFP8) {
+    // fwd: X (bf16) -> Xq + scales, a straight to Aq + scales, O (bf16)
+    if (pass == MEMFINE_FWD) return ep + 8 + D * h + (h + h / 32) + (g + g / 32) + D * h;
+    // bwd: bf16 X, dY, G||U, a_w (dA and the weight gradients stay BF16) + Xq, dGUq with scales;
+    // O aliases X
+    return ep + 12 + D * (h + h + 2 * g + g) + (h + h / 32) + (2 * g + 2 * g / 32);
+  }
   if (pass == MEMFINE_FWD) return ep + 4 + 4 + D * (h + g + h);   // src_of, w_row, X, A, O
   return ep + 4 + 4 + 4 + D * (h + h + 2 * g + g);                 // + dw_row, DY, GU; O aliases X
 }
@@ -196,7 +209,23 @@ Layout carve(const memfine_dims& d, int C, int pass, void* ws, int64_t rows_cap,
   }
   if (pass == MEMFINE_BWD) L.m.dw_row = b.take<float>(R);
   L.X = b.take<char>((uint64_t)R * d.hidden * D);
-  if (pass == MEMFINE_BWD) {
+  if (d.dtype == MEMFINE_MXFP8) {
+    const uint64_t hh = d.hidden, gg = d.ffn;
+    L.Xq = b.take<uint8_t>((uint64_t)R * hh);
+    L.Xsf = b.take<uint8_t>((uint64_t)R * hh / 32);
+    if (pass == MEMFINE_BWD) {
+      L.DY = b.take<char>((uint64_t)R * hh * D);
+      L.GU = b.take<char>((uint64_t)R * 2 * gg * D);
+      L.A = b.take<char>((uint64_t)R * gg * D);
+      L.GUq = b.take<uint8_t>((uint64_t)R * 2 * gg);
+      L.GUsf = b.take<uint8_t>((uint64_t)R * 2 * gg / 32);
+      L.O = L.X;
+    } else {
+      L.Aq = b.take<uint8_t>((uint64_t)R * gg);
+      L.Asf = b.take<uint8_t>((uint64_t)R * gg / 32);
+      L.O = b.take<char>((uint64_t)R * hh * D);
+    }
+  } else if (pass == MEMFINE_BWD) {
     L.DY = b.take<char>((uint64_t)R * d.hidden * D);
     L.GU = b.take<char>((uint64_t)R * 2 * d.ffn * D);
     L.A = b.take<char>((uint64_t)R * d.ffn * D);
@@ -335,6 +364,34 @@ memfine_status latch_cuda(memfine_handle_s* h) {
   return e == cudaSuccess ? MEMFINE_OK : MEMFINE_ERR_CUDA;
 }
 
+// ------------------------------------------------------------------ MXFP8 weights (N4, reading R28)
+// Five E4M3 operands of E_l*g*h codes each, then their scale chunks (E_l*g*h/32 each), 256-aligned:
+//   0 W_gate rows (K = h)  1 W_up rows (K = h)  2 W_down rows (K = g)
+//   3 W_gate^T [E_l][h][g] (K = g, dX)   4 W_up^T (K = g, dX)
+constexpr int kMxW = 5;
+struct MxWeightsLayout {
+  MxOp op[kMxW];
+  uint64_t total = 0;
+};
+MxWeightsLayout mx_weights_layout(const memfine_dims& d, const void* base) {
+  MxWeightsLayout W;
+  Bump b(const_cast<void*>(base));
+  const uint64_t n = (uint64_t)(d.num_experts / d.ep_size) * d.hidden * d.ffn;
+  uint8_t* q[kMxW];
+  for (int i = 0; i < kMxW; i++) q[i] = b.take<uint8_t>(n);
+  for (int i = 0; i < kMxW; i++) W.op[i] = {q[i], b.take<uint8_t>(n / 32)};
+  b.off = (b.off + 255) & ~uint64_t(255);
+  W.total = b.off;
+  return W;
+}
+
+void set_mx(GemmProblem<__nv_bfloat16>& p, const MxOp& a, const MxOp& b0, const MxOp& b1) {
+  p.mx = 1;
+  p.mx_a = a;
+  p.mx_b0 = b0;
+  p.mx_b1 = b1;
+}
+
 // ------------------------------------------------------------------ the FCDA chunk loops (EP = 1)
 template <typename T>
 memfine_status fwd_ep1(memfine_handle_s* h, const T* x, const int32_t* ids, const float* w, const void* wg,
@@ -344,6 +401,9 @@ memfine_status fwd_ep1(memfine_handle_s* h, const T* x, const int32_t* ids, cons
   if (R < 0) return MEMFINE_ERR_WORKSPACE;
   Layout L = carve(d, C, MEMFINE_FWD, ws, R, 0);
   int E = d.num_experts, El = E, k = d.topk, hd = d.hidden;
+  const bool mx = d.dtype == MEMFINE_MXFP8;
+  if (mx && !h->mx_w) return MEMFINE_ERR_INVALID_ARG;   // memfine_mx_quantize_weights first
+  MxWeightsLayout W = mx_weights_layout(d, h->mx_w);
   h->last_meta = L.meta_bytes;
   h->last_row_bytes = L.row_bytes;
   if (h->debug) h->debug_perm.assign(C, {});
@@ -355,8 +415,10 @@ memfine_status fwd_ep1(memfine_handle_s* h, const T* x, const int32_t* ids, cons
     launch_dispatch_hist(ids, t0, t1, k, E, L.m, h->status_d, st);
     launch_dispatch_scan(NB, E, El, 1, R, L.m, h->rows_d, h->rows_d + kMaxSub, j, st);
     launch_dispatch_scatter<T>(x, nullptr, ids, w, t0, t1, k, E, hd, L.m, (T*)L.X, nullptr, El, true, R, st);
+    if constexpr (std::is_same<T, __nv_bfloat16>::value)
+      if (mx) launch_mx_quant_rows((const __nv_bfloat16*)L.X, hd, R, L.m.info, hd, L.Xq, L.Xsf, st);
     prof_end(h, st);
-    h->last.kernel_launches += 4;
+    h->last.kernel_launches += mx ? 5 : 4;
     if (h->debug) {
       cudaStreamSynchronize(st);
       int rp = (int)h->rows_h[kMaxSub + j];
@@ -368,8 +430,16 @@ memfine_status fwd_ep1(memfine_handle_s* h, const T* x, const int32_t* ids, cons
     GemmProblem<T> p = base_problem<T>(h, L, wg, wu, wd);
     p.kind = GK_GATEUP;
     p.store_a = 1;
+    if constexpr (std::is_same<T, __nv_bfloat16>::value)
+      if (mx) {
+        set_mx(p, {L.Xq, L.Xsf}, W.op[0], W.op[1]);
+        p.mx_aq = L.Aq;
+        p.mx_aq_sf = L.Asf;
+      }
     if (int rc = run_gemm<T>(h, p, st)) return (memfine_status)rc;
     p.kind = GK_DOWN;
+    if constexpr (std::is_same<T, __nv_bfloat16>::value)
+      if (mx) set_mx(p, {L.Aq, L.Asf}, W.op[2], W.op[2]);
     if (int rc = run_gemm<T>(h, p, st)) return (memfine_status)rc;
     prof_begin(h, 7, st);
     launch_combine<T>((const T*)L.O, w, t0, t1, k, hd, L.m, y, st);
@@ -388,6 +458,9 @@ memfine_status bwd_ep1(memfine_handle_s* h, const T* dy, const T* x, const int32
   if (R < 0) return MEMFINE_ERR_WORKSPACE;
   Layout L = carve(d, C, MEMFINE_BWD, ws, R, 0);
   int E = d.num_experts, El = E, k = d.topk, hd = d.hidden, g = d.ffn;
+  const bool mx = d.dtype == MEMFINE_MXFP8;
+  if (mx && !h->mx_w) return MEMFINE_ERR_INVALID_ARG;   // memfine_mx_quantize_weights first
+  MxWeightsLayout W = mx_weights_layout(d, h->mx_w);
   h->last_meta = L.meta_bytes;
   h->last_row_bytes = L.row_bytes;
   // dW is overwritten by the first non-empty chunk's weight-gradient GEMMs (beta = 0) and
@@ -411,8 +484,10 @@ memfine_status bwd_ep1(memfine_handle_s* h, const T* dy, const T* x, const int32
     launch_dispatch_hist(ids, t0, t1, k, E, L.m, h->status_d, st);
     launch_dispatch_scan(NB, E, El, 1, R, L.m, h->rows_d, h->rows_d + kMaxSub, j, st);
     launch_dispatch_scatter<T>(x, dy, ids, w, t0, t1, k, E, hd, L.m, (T*)L.X, (T*)L.DY, El, true, R, st);
+    if constexpr (std::is_same<T, __nv_bfloat16>::value)
+      if (mx) launch_mx_quant_rows((const __nv_bfloat16*)L.X, hd, R, L.m.info, hd, L.Xq, L.Xsf, st);
     prof_end(h, st);
-    h->last.kernel_launches += 4;
+    h->last.kernel_launches += mx ? 5 : 4;
     GemmProblem<T> p = base_problem<T>(h, L, wg, wu, wd);
     p.dWg = dwg;
     p.dWu = dwu;
@@ -421,10 +496,22 @@ memfine_status bwd_ep1(memfine_handle_s* h, const T* dy, const T* x, const int32
     p.kind = GK_GATEUP;
     p.store_a = 0;
     p.store_gu = 1;
+    if constexpr (std::is_same<T, __nv_bfloat16>::value)
+      if (mx) set_mx(p, {L.Xq, L.Xsf}, W.op[0], W.op[1]);
     if (int rc = run_gemm<T>(h, p, st)) return (memfine_status)rc;
-    // B3: u = dY W_down, fused d_w / dG / dU / a_w epilogue
+    // B3: u = dY W_down, fused d_w / dG / dU / a_w epilogue (BF16 operands in the MX variant too:
+    // the GEMM is bound by its epilogue - reading R28)
     p.kind = GK_DACT;
+    p.mx = 0;
     if (int rc = run_gemm<T>(h, p, st)) return (memfine_status)rc;
+    if constexpr (std::is_same<T, __nv_bfloat16>::value)
+      if (mx) {
+        // dG || dU rows -> E4M3 for the dX GEMM (blocks along 2g never straddle: g % 32 == 0)
+        prof_begin(h, 6, st);
+        launch_mx_quant_rows((const __nv_bfloat16*)L.GU, 2 * (int64_t)g, R, L.m.info, 2 * g, L.GUq, L.GUsf, st);
+        prof_end(h, st);
+        h->last.kernel_launches += 1;
+      }
     // B5: weight gradients accumulate across chunks (reading R18)
     p.wgrad_beta = beta;
     p.kind = GK_WGRAD_DOWN;
@@ -434,6 +521,8 @@ memfine_status bwd_ep1(memfine_handle_s* h, const T* dy, const T* x, const int32
     beta = 1;
     // B4: dX_disp = dG W_gate + dU W_up (overwrites X_disp, dead after B5)
     p.kind = GK_DX;
+    if constexpr (std::is_same<T, __nv_bfloat16>::value)
+      if (mx) set_mx(p, {L.GUq, L.GUsf}, W.op[3], W.op[4]);
     if (int rc = run_gemm<T>(h, p, st)) return (memfine_status)rc;
     // B7: dX_i = sum_slot dX_disp[pos], d_score
     prof_begin(h, 7, st);
@@ -676,9 +765,6 @@ memfine_status ep_run_p2p(memfine_handle_s* h, int pass, const T* dy, const T* x
   const size_t per = 4 * (size_t)E + 1;
   if (h->tab_cap < per * C) {
     if (h->tab_h) cudaFreeHost(h->tab_h);
-  if (h->router_scratch) cudaFree(h->router_scratch);
-  for (void* b : h->ipc_bases) cudaIpcCloseMemHandle(b);
-  if (h->barrier_d) cudaFree(h->barrier_d);
     h->tab_h = nullptr;
     h->tab_cap = 0;
     MF_CUDA_OK(cudaHostAlloc((void**)&h->tab_h, sizeof(int) * per * C, cudaHostAllocDefault));
@@ -1298,8 +1384,9 @@ memfine_status memfine_moe_fwd(memfine_handle_t h, const void* x, const int32_t*
   if (!w_gate || !w_up || !w_down || !ws) return MEMFINE_ERR_INVALID_ARG;
   cudaStream_t st = (cudaStream_t)stream;
   begin_call(h, C, MEMFINE_FWD, ws_bytes, st);
+  if (h->d.ep_size > 1 && h->d.dtype == MEMFINE_MXFP8) return MEMFINE_ERR_UNSUPPORTED;
   if (h->d.ep_size > 1) return memfine_ep_fwd(h, x, ids, w, w_gate, w_up, w_down, C, y, ws, ws_bytes, st);
-  if (h->d.dtype == MEMFINE_BF16)
+  if (h->d.dtype != MEMFINE_FP32)
     return fwd_ep1<__nv_bfloat16>(h, (const __nv_bfloat16*)x, ids, w, w_gate, w_up, w_down, C, (__nv_bfloat16*)y, ws,
                                   ws_bytes, st);
   return fwd_ep1<float>(h, (const float*)x, ids, w, w_gate, w_up, w_down, C, (float*)y, ws, ws_bytes, st);
@@ -1314,15 +1401,51 @@ memfine_status memfine_moe_bwd(memfine_handle_t h, const void* dy, const void* x
   if (!w_gate || !w_up || !w_down || !dw_gate || !dw_up || !dw_down || !ws) return MEMFINE_ERR_INVALID_ARG;
   cudaStream_t st = (cudaStream_t)stream;
   begin_call(h, C, MEMFINE_BWD, ws_bytes, st);
+  if (h->d.ep_size > 1 && h->d.dtype == MEMFINE_MXFP8) return MEMFINE_ERR_UNSUPPORTED;
   if (h->d.ep_size > 1)
     return memfine_ep_bwd(h, dy, x, ids, w, w_gate, w_up, w_down, C, dx, dw_gate, dw_up, dw_down, dscore,
                           accumulate_dw, ws, ws_bytes, st);
-  if (h->d.dtype == MEMFINE_BF16)
+  if (h->d.dtype != MEMFINE_FP32)
     return bwd_ep1<__nv_bfloat16>(h, (const __nv_bfloat16*)dy, (const __nv_bfloat16*)x, ids, w, w_gate, w_up, w_down,
                                   C, (__nv_bfloat16*)dx, dw_gate, dw_up, dw_down, dscore, accumulate_dw, ws, ws_bytes,
                                   st);
   return bwd_ep1<float>(h, (const float*)dy, (const float*)x, ids, w, w_gate, w_up, w_down, C, (float*)dx, dw_gate,
                         dw_up, dw_down, dscore, accumulate_dw, ws, ws_bytes, st);
+}
+
+// ---------------------------------------------------------------- MXFP8 (N4, reading R28)
+memfine_status memfine_mx_weights_bytes(const memfine_dims* dims, uint64_t* bytes) {
+  if (!dims_ok(dims) || !bytes || dims->dtype != MEMFINE_MXFP8) return MEMFINE_ERR_INVALID_ARG;
+  *bytes = mx_weights_layout(*dims, nullptr).total;
+  return MEMFINE_OK;
+}
+
+memfine_status memfine_mx_quantize_weights(memfine_handle_t h, const void* w_gate, const void* w_up,
+                                           const void* w_down, void* wq, uint64_t wq_bytes, void* stream) {
+  if (!h || h->d.dtype != MEMFINE_MXFP8 || !w_gate || !w_up || !w_down || !wq) return MEMFINE_ERR_INVALID_ARG;
+  const memfine_dims& d = h->d;
+  MxWeightsLayout W = mx_weights_layout(d, wq);
+  if (wq_bytes < W.total) return MEMFINE_ERR_WORKSPACE;
+  cudaStream_t st = (cudaStream_t)stream;
+  const int El = d.num_experts / d.ep_size, hd = d.hidden, g = d.ffn;
+  auto q = [&](int i) { return const_cast<uint8_t*>(W.op[i].q); };
+  auto sf = [&](int i) { return const_cast<uint8_t*>(W.op[i].sf); };
+  const __nv_bfloat16 *wg = (const __nv_bfloat16*)w_gate, *wu = (const __nv_bfloat16*)w_up,
+                      *wd = (const __nv_bfloat16*)w_down;
+  launch_mx_quant_rows(wg, hd, (int64_t)El * g, nullptr, hd, q(0), sf(0), st);
+  launch_mx_quant_rows(wu, hd, (int64_t)El * g, nullptr, hd, q(1), sf(1), st);
+  launch_mx_quant_rows(wd, g, (int64_t)El * hd, nullptr, g, q(2), sf(2), st);
+  launch_mx_quant_transpose(wg, El, g, hd, q(3), sf(3), st);   // [El][g][h] -> [El][h][g], blocks along g
+  launch_mx_quant_transpose(wu, El, g, hd, q(4), sf(4), st);
+  h->mx_w = (const uint8_t*)wq;
+  return latch_cuda(h);
+}
+
+memfine_status memfine_mx_quantize(const void* src, int64_t rows, int32_t K, void* codes, void* scales, void* stream) {
+  if (!src || !codes || !scales || rows < 0 || rows % 128 || K <= 0 || K % 128) return MEMFINE_ERR_INVALID_ARG;
+  launch_mx_quant_rows((const __nv_bfloat16*)src, K, rows, nullptr, K, (uint8_t*)codes, (uint8_t*)scales,
+                       (cudaStream_t)stream);
+  return cudaGetLastError() == cudaSuccess ? MEMFINE_OK : MEMFINE_ERR_CUDA;
 }
 
 // ---------------------------------------------------------------- router (N3)
@@ -1379,7 +1502,7 @@ memfine_status memfine_router_fwd(memfine_handle_t h, const void* x, const void*
   RouterScratch rs;
   if (int rc = router_scratch(h, &rs)) return (memfine_status)rc;
   float* lg = logits ? logits : rs.logits;
-  if (d.dtype == MEMFINE_BF16)
+  if (d.dtype != MEMFINE_FP32)
     launch_router_fwd<__nv_bfloat16>((const __nv_bfloat16*)x, (const __nv_bfloat16*)w_router, d.tokens,
                                      d.num_experts, d.hidden, d.topk, lg, ids, scores, st);
   else
@@ -1408,7 +1531,7 @@ memfine_status memfine_router_bwd(memfine_handle_t h, const void* x, const void*
     MF_CUDA_OK(cudaMemsetAsync(rs.m.seg, 0, sizeof(int) * (E + 1), st));
     MF_CUDA_OK(cudaMemsetAsync(rs.m.recv_cnt, 0, sizeof(int) * (E + 1), st));
   }
-  if (d.dtype == MEMFINE_BF16)
+  if (d.dtype != MEMFINE_FP32)
     launch_router_bwd<__nv_bfloat16>((const __nv_bfloat16*)x, (const __nv_bfloat16*)w_router, ids, scores, dscore,
                                      d.tokens, E, d.hidden, k, rs.dlog, (__nv_bfloat16*)dx, accumulate_dx, dw_router,
                                      accumulate_dw, rs.m, st);

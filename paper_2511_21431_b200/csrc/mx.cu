@@ -1,0 +1,110 @@
+// mx.cu — MXFP8 operand quantisation for the block-scaled expert GEMMs (
+// DESIGN.md reading R28): E4M3 codes, K-major, with E8M0 block scales written straight into the
+// tcgen05 scale-factor chunk layout (common.cuh mx_sf_off), so the GEMM producer moves them with
+// one 512-byte bulk copy per 128 rows x 128 K.
+#include <algorithm>
+#include "kernels.h"
+
+namespace memfine {
+
+// Row-wise: src [rows][K] bf16 (row stride ld) -> q [rows][K] E4M3, sf chunks.  One thread per 8
+// consecutive elements (one 16-B load), 4 threads per 32-element block (amax by two shuffles).
+// With a chunk's info words: rows = its padded rows (0 when the chunk is skipped), at most rows_max.
+__global__ void __launch_bounds__(256) mx_quant_rows_kernel(const __nv_bfloat16* __restrict__ src, int64_t ld,
+                                                            int64_t rows_max, const int* __restrict__ info,
+                                                            int K, uint8_t* __restrict__ q,
+                                                            uint8_t* __restrict__ sf) {
+  int64_t rows = rows_max;
+  if (info) rows = __ldg(info + kInfoSkip) ? 0 : min(rows_max, (int64_t)__ldg(info + kInfoRowsPad));
+  const int per_row = K >> 3;
+  const int64_t n = rows * per_row;
+  // whole warps iterate together (full-mask shuffles); the 4 threads of a block share ok
+  // (n and per_row are multiples of 4)
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i - (threadIdx.x & 31) < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const bool ok = i < n;
+    const int64_t r = ok ? i / per_row : 0;
+    const int s = ok ? (int)(i % per_row) : 0;
+    uint4 u = ok ? *reinterpret_cast<const uint4*>(src + r * ld + (int64_t)s * 8) : make_uint4(0, 0, 0, 0);
+    float v[8];
+    const uint32_t w[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+    for (int j = 0; j < 4; j++) {
+      v[2 * j] = __uint_as_float(w[j] << 16);
+      v[2 * j + 1] = __uint_as_float(w[j] & 0xFFFF0000u);
+    }
+    float amax = 0.f;
+#pragma unroll
+    for (int j = 0; j < 8; j++) amax = fmaxf(amax, fabsf(v[j]));
+    amax = fmaxf(amax, __shfl_xor_sync(0xffffffffu, amax, 1));
+    amax = fmaxf(amax, __shfl_xor_sync(0xffffffffu, amax, 2));
+    const int E = mx_exp(amax);
+    const float inv = mx_inv_scale(E);
+    uint2 o;
+    o.x = mx_e4m3x2(v[0] * inv, v[1] * inv) | (mx_e4m3x2(v[2] * inv, v[3] * inv) << 16);
+    o.y = mx_e4m3x2(v[4] * inv, v[5] * inv) | (mx_e4m3x2(v[6] * inv, v[7] * inv) << 16);
+    if (ok) {
+      *reinterpret_cast<uint2*>(q + r * K + (int64_t)s * 8) = o;
+      if ((s & 3) == 0) sf[mx_sf_off(r, s >> 2, K)] = (uint8_t)(E + 127);
+    }
+  }
+}
+
+// Transposing, for the backward weight operands: src [B][R][Cc] bf16 -> q [B][Cc][R] E4M3 blocked
+// along R (the GEMM's K), sf chunks per b at b * Cc * R / 32.  Tile: 128 R x 32 Cc through smem.
+__global__ void __launch_bounds__(256) mx_quant_transpose_kernel(const __nv_bfloat16* __restrict__ src, int R, int Cc,
+                                                                 uint8_t* __restrict__ q, uint8_t* __restrict__ sf) {
+  __shared__ float t[128][33];
+  const int b = blockIdx.z, r0 = blockIdx.y * 128, c0 = blockIdx.x * 32;
+  const __nv_bfloat16* s = src + (int64_t)b * R * Cc;
+  // load 128 x 32 (4 threads x 8 elements per row, 64 rows per pass)
+#pragma unroll
+  for (int pass = 0; pass < 2; pass++) {
+    const int rr = pass * 64 + (threadIdx.x >> 2), cc = (threadIdx.x & 3) * 8;
+    const uint4 u = *reinterpret_cast<const uint4*>(s + (int64_t)(r0 + rr) * Cc + c0 + cc);
+    const uint32_t w[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+    for (int j = 0; j < 4; j++) {
+      t[rr][cc + 2 * j] = __uint_as_float(w[j] << 16);
+      t[rr][cc + 2 * j + 1] = __uint_as_float(w[j] & 0xFFFF0000u);
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x >= 128) return;
+  const int c = threadIdx.x >> 2, kb = threadIdx.x & 3;   // output row c0 + c, block kb of 4
+  float v[32];
+  float amax = 0.f;
+#pragma unroll
+  for (int i = 0; i < 32; i++) {
+    v[i] = t[kb * 32 + i][c];
+    amax = fmaxf(amax, fabsf(v[i]));
+  }
+  const int E = mx_exp(amax);
+  const float inv = mx_inv_scale(E);
+  uint32_t o[8];
+#pragma unroll
+  for (int j = 0; j < 8; j++)
+    o[j] = mx_e4m3x2(v[4 * j] * inv, v[4 * j + 1] * inv) | (mx_e4m3x2(v[4 * j + 2] * inv, v[4 * j + 3] * inv) << 16);
+  const int64_t orow = c0 + c;
+  uint8_t* dst = q + ((int64_t)b * Cc + orow) * R + r0 + kb * 32;
+  reinterpret_cast<uint4*>(dst)[0] = make_uint4(o[0], o[1], o[2], o[3]);
+  reinterpret_cast<uint4*>(dst)[1] = make_uint4(o[4], o[5], o[6], o[7]);
+  sf[(int64_t)b * Cc * (R / 32) + mx_sf_off(orow, (r0 >> 5) + kb, R)] = (uint8_t)(E + 127);
+}
+
+void launch_mx_quant_rows(const __nv_bfloat16* src, int64_t ld, int64_t rows_max, const int* info, int K,
+                          uint8_t* q, uint8_t* sf, cudaStream_t st) {
+  const int64_t n = rows_max * (K / 8);
+  if (n <= 0) return;
+  const int64_t blocks = std::min<int64_t>(ceil_div64(n, 256), (int64_t)sm100_num_sms() * 16);
+  mx_quant_rows_kernel<<<(unsigned)blocks, 256, 0, st>>>(src, ld, rows_max, info, K, q, sf);
+}
+
+void launch_mx_quant_transpose(const __nv_bfloat16* src, int B, int R, int Cc, uint8_t* q, uint8_t* sf,
+                               cudaStream_t st) {
+  if (B <= 0 || R <= 0 || Cc <= 0) return;
+  dim3 grid((unsigned)(Cc / 32), (unsigned)(R / 128), (unsigned)B);
+  mx_quant_transpose_kernel<<<grid, 256, 0, st>>>(src, R, Cc, q, sf);
+}
+
+}  // namespace memfine

@@ -25,9 +25,28 @@ def _stream(stream=None):
     return C.c_void_p(s.cuda_stream)
 
 
-def make_dims(tokens, hidden, ffn, num_experts, topk, ep_size=1, ep_rank=0, dtype=torch.bfloat16) -> capi.Dims:
+def make_dims(tokens, hidden, ffn, num_experts, topk, ep_size=1, ep_rank=0, dtype=torch.bfloat16,
+              mx: bool = False) -> capi.Dims:
+    """mx=True: MEMFINE_MXFP8 (bf16 storage, MXFP8 expert-GEMM operands; dtype must be bf16)."""
+    assert not mx or dtype == torch.bfloat16
     return capi.Dims(int(tokens), int(hidden), int(ffn), int(num_experts), int(topk), int(ep_size), int(ep_rank),
-                     _DT[dtype])
+                     capi.MXFP8 if mx else _DT[dtype])
+
+
+def mx_weights_bytes(dims: capi.Dims) -> int:
+    out = C.c_uint64()
+    capi.check(capi.lib().memfine_mx_weights_bytes(C.byref(dims), C.byref(out)), "memfine_mx_weights_bytes")
+    return int(out.value)
+
+
+def mx_quantize(src: torch.Tensor, stream=None):
+    """memfine_mx_quantize: bf16 [rows][K] -> (E4M3 codes uint8 [rows][K], scale codes uint8 [rows*K/32])."""
+    assert src.dtype == torch.bfloat16 and src.is_cuda and src.is_contiguous() and src.dim() == 2
+    codes = torch.empty(src.shape, dtype=torch.uint8, device=src.device)
+    scales = torch.empty(src.numel() // 32, dtype=torch.uint8, device=src.device)
+    capi.check(capi.lib().memfine_mx_quantize(_ptr(src), src.shape[0], src.shape[1], _ptr(codes), _ptr(scales),
+                                              _stream(stream)), "memfine_mx_quantize")
+    return codes, scales
 
 
 def plan(counts: torch.Tensor, dims: capi.Dims, budget: capi.Budget) -> dict:
@@ -87,9 +106,11 @@ class MemFine:
     (torch.distributed) used only to broadcast the NCCL unique id when ep_size > 1."""
 
     def __init__(self, tokens, hidden, ffn, num_experts, topk, ep_size=1, ep_rank=0, dtype=torch.bfloat16,
-                 process_group=None, local_group=None):
-        self.dims = make_dims(tokens, hidden, ffn, num_experts, topk, ep_size, ep_rank, dtype)
+                 process_group=None, local_group=None, mx: bool = False):
+        self.dims = make_dims(tokens, hidden, ffn, num_experts, topk, ep_size, ep_rank, dtype, mx)
         self.dtype = dtype
+        self.mx = mx
+        self._wq = None
         self.E_l = num_experts // ep_size
         self._ws = None
         if local_group is not None:
@@ -136,6 +157,17 @@ class MemFine:
     def workspace(self, counts_host, C_: int, pass_: int, device=None) -> torch.Tensor:
         n = workspace_bytes(counts_host, self.dims, C_, pass_)
         return torch.empty(n, dtype=torch.uint8, device=device or torch.cuda.current_device())
+
+    # ------------------------------------------------------------------ MXFP8 variant (N4)
+    def mx_quantize_weights(self, w_gate, w_up, w_down, wq: Optional[torch.Tensor] = None, stream=None):
+        """memfine_mx_quantize_weights: quantise and bind the local experts' weights (again after
+        every weight update).  Returns the (kept-alive) quantised-weights buffer."""
+        if wq is None:
+            wq = torch.empty(mx_weights_bytes(self.dims), dtype=torch.uint8, device=w_gate.device)
+        capi.check(capi.lib().memfine_mx_quantize_weights(self.h, _ptr(w_gate), _ptr(w_up), _ptr(w_down), _ptr(wq),
+                                                          wq.numel(), _stream(stream)), "memfine_mx_quantize_weights")
+        self._wq = wq
+        return wq
 
     # ------------------------------------------------------------------ FCDA forward / backward
     def moe_fwd(self, x, ids, w, w_gate, w_up, w_down, C_: int, ws: torch.Tensor, y=None, stream=None):
