@@ -1,6 +1,6 @@
 """Summarise ncu reports into markdown for profiles/ (run here, on the CPU box).
 
-  python tools/ncu_summary.py full   gpurun_out/prof_gemm.ncu-rep   > profiles/...md
+  python tools/ncu_summary.py full   gpurun_out/prof_gemm.ncu-rep   > profiles/...md   (or a raw .csv)
   python tools/ncu_summary.py launches gpurun_out/launches.csv       > profiles/...md
 """
 import csv
@@ -29,7 +29,10 @@ def short(name):
 
 
 def full(path):
-    raw = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    if path.endswith(".csv"):   # `ncu -i rep --page raw --csv` exported on the GPU box
+        raw = open(path).read()
+    else:
+        raw = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
     rows = list(csv.reader(io.StringIO(raw)))
     hdr, units, data = rows[0], rows[1], rows[2:]
     cols = [(hdr.index(m), lab, units[hdr.index(m)]) for m, lab in METRICS if m in hdr]
