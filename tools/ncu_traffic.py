@@ -2,6 +2,7 @@
 an `ncu --set full` capture, as JSON for bench.py's roofline.traffic field.
 
   python tools/ncu_traffic.py gpurun_out/prof.ncu-rep > profiles/r01_ncu_traffic.json
+  python tools/ncu_traffic.py gpurun_out/prof_raw.csv  (ncu -i prof.ncu-rep --page raw --csv, exported on the box)
 """
 import csv
 import io
@@ -17,7 +18,10 @@ UNIT = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
 
 
 def main(path):
-    raw = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    if path.endswith(".csv"):
+        raw = open(path).read()
+    else:
+        raw = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
     rows = list(csv.reader(io.StringIO(raw)))
     hdr, units, data = rows[0], rows[1], rows[2:]
     ir, iw = hdr.index("dram__bytes_read.sum"), hdr.index("dram__bytes_write.sum")
