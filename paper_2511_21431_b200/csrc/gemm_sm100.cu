@@ -1220,14 +1220,19 @@ int launch(const GemmProblem<__nv_bfloat16>& gp, cudaStream_t st) {
   const int per_unit = PAIR ? 2 : 1;
   const int units_hw = g_num_sms / per_unit;
   {
-    // Raster group: gm M tiles x all N tiles, gm sized so the group's A strips take ~24 MB of L2
-    // (measured best on the Mixtral-size step: less DRAM traffic -> less power -> higher clocks
-    // under the 1 kW cap; 48 and 96 MB were slower).  MEMFINE_L2_GROUP_MB=0 selects a square-ish
-    // wave block (gm ~ sqrt(units * B_strip / A_strip)) instead; other values set the budget.
-    static int64_t budget = [] {
+    // Raster group: gm M tiles x all N tiles, gm sized so the group's A strips take a per-kind L2
+    // budget.  Cycles do not depend on it, DRAM traffic does - and under the power cap DRAM energy
+    // costs SM clock (profiles/r01_l2_group_sweep.md: 8..96 MB, same cycles, 72..123 GB per step,
+    // 1.10..1.30 GHz).  Per-kind minima of the Mixtral step: gate/up and dA 24 MB, down, dX and
+    // dW_gate/up 8 MB, dW_down 48 MB.  MEMFINE_L2_GROUP_MB overrides every kind (0 = square-ish
+    // wave block, gm ~ sqrt(units * B_strip / A_strip)).
+    static const int64_t env_budget = [] {
       const char* s = getenv("MEMFINE_L2_GROUP_MB");
-      return (int64_t)(s ? atoi(s) : 24) << 20;
+      return s ? (int64_t)atoi(s) << 20 : (int64_t)-1;
     }();
+    constexpr int64_t kind_mb = (KIND == GK_DOWN || KIND == GK_DX || KIND == GK_WGRAD_GU) ? 8
+                                : KIND == GK_WGRAD_DOWN ? 48 : 24;
+    const int64_t budget = env_budget >= 0 ? env_budget : kind_mb << 20;
     int64_t kdim = (KIND >= GK_WGRAD_DOWN) ? (int64_t)std::max<int64_t>(1, R / std::max<uint64_t>(1, El)) : p.K;
     int64_t a_strip = (int64_t)TM * kdim * 2, b_strip = (int64_t)BN * kdim * 2;
     if (budget) {
@@ -1396,12 +1401,15 @@ int launch_mx(const GemmProblem<__nv_bfloat16>& gp, cudaStream_t st) {
   constexpr int BN = CfgX<KIND, true>::BN;
   int nt = (p.N + BN - 1) / BN;
   {
-    static int64_t budget = [] {
+    // the same per-kind raster budgets as the BF16 kernels (launch<>); MEMFINE_L2_GROUP_MB overrides
+    static const int64_t env_budget = [] {
       const char* s = getenv("MEMFINE_L2_GROUP_MB");
-      return (int64_t)(s ? atoi(s) : 24) << 20;
+      return s ? (int64_t)atoi(s) << 20 : (int64_t)-1;
     }();
+    constexpr int64_t kind_mb = (KIND == GK_DOWN || KIND == GK_DX) ? 8 : 24;
+    const int64_t budget = env_budget > 0 ? env_budget : kind_mb << 20;
     int64_t a_strip = (int64_t)(PAIR ? 2 : 1) * BM * p.K;   // E4M3: one byte per element
-    p.group_m = (int)std::max<int64_t>(1, std::min<int64_t>(64, (budget ? budget : (24 << 20)) / a_strip));
+    p.group_m = (int)std::max<int64_t>(1, std::min<int64_t>(64, budget / a_strip));
   }
   const int per_unit = PAIR ? 2 : 1;
   int64_t max_tiles = (int64_t)((R / BM + (PAIR ? El : 0)) / per_unit + 1) * nt;
