@@ -180,6 +180,15 @@ def cpu_baseline(cfg, ntok: int):
                       f"plus a fixed dW zeroing term"}
 
 
+def workload_config(cfg, args, world: int) -> dict:
+    """The workload both arms are measured on (config.workload of the JSON line)."""
+    T = args.tokens or cfg.T
+    placement = args.placement or cfg.placement
+    return {"workload": f"{cfg.name}-style MoE layer: E={cfg.E} top-{cfg.k} h={cfg.h} SwiGLU ffn={cfg.g}, {T} "
+                        f"tokens/GPU, Zipf({cfg.zipf_s}) routing ({placement} placement), EP={world}",
+            "tokens_per_gpu": T, "ep": world}
+
+
 def run_reference(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -198,10 +207,11 @@ def run_reference(args):
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": f"{cfg.name}: E={cfg.E} top-{cfg.k} h={cfg.h} ffn={cfg.g}, oracle sample "
-                                   f"{ntok} tokens/step, Zipf({cfg.zipf_s}) routing"},
+            "config": workload_config(cfg, args, world),
             "cpu_baseline": {"value": value, "unit": "tokens/s", "cores": cores, "kind": "oracle",
-                             "sample": f"{ntok} tokens per step, fwd+bwd, fp64"},
+                             "sample": f"{ntok} tokens of the workload per step (all {cfg.E} experts, full "
+                                       f"h={cfg.h}, g={cfg.g}), oracle fwd (Eq. 4) + bwd (Eq. 5) incl. dW, fp64; "
+                                       f"cost linear in tokens"},
             "e2e": {"value": value, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
@@ -501,9 +511,7 @@ def main():
         "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
-        "config": {"workload": f"{cfg.name}-style MoE layer: E={E} top-{k} h={h} SwiGLU ffn={g}, {T} tokens/GPU, "
-                               f"Zipf({cfg.zipf_s}) routing ({placement} placement), EP={EP}",
-                   "tokens_per_gpu": T, "ep": EP, "chunks": C, "tuner": plan,
+        "config": {**workload_config(cfg, args, world), "chunks": C, "tuner": plan,
                    "ep_transport": args.ep_transport if world > 1 else None,
                    "budget": {"gpu_capacity_bytes": cap, "alpha": args.alpha, "static_bytes": static},
                    "l2": "no flush: every step streams > 126 MB (weights 2.8 GB at EP=1, activations GBs)"},
