@@ -192,6 +192,31 @@ __device__ __forceinline__ void add32_f32(float* dst, const float* v) {
   }
 }
 
+// One MXFP8 block from 32 bf16 values (two packed halves of 8 words): E4M3 codes (32 B, one
+// 256-bit store) and the E8M0 scale byte (reading R28; the values are the stored bf16 ones, R28b).
+__device__ __forceinline__ void mx_store_block_bf16(const uint32_t (&lo)[8], const uint32_t (&hi)[8], uint8_t* q,
+                                                    uint8_t* sf) {
+  float f[32];
+  float amax = 0.f;
+#pragma unroll
+  for (int j = 0; j < 8; j++) {
+    f[2 * j] = __uint_as_float(lo[j] << 16);
+    f[2 * j + 1] = __uint_as_float(lo[j] & 0xFFFF0000u);
+    f[16 + 2 * j] = __uint_as_float(hi[j] << 16);
+    f[16 + 2 * j + 1] = __uint_as_float(hi[j] & 0xFFFF0000u);
+  }
+#pragma unroll
+  for (int j = 0; j < 32; j++) amax = fmaxf(amax, fabsf(f[j]));
+  const int E = mx_exp(amax);
+  const float inv = mx_inv_scale(E);
+  uint32_t o[8];
+#pragma unroll
+  for (int j = 0; j < 8; j++)
+    o[j] = mx_e4m3x2(f[4 * j] * inv, f[4 * j + 1] * inv) | (mx_e4m3x2(f[4 * j + 2] * inv, f[4 * j + 3] * inv) << 16);
+  st256(q, o);
+  *sf = (uint8_t)(E + 127);
+}
+
 // TMA stores from shared memory (bulk async groups).  reduce = 1: element-wise add into global.
 __device__ __forceinline__ void tma_store_2d(const CUtensorMap* m, const void* src, int c0, int c1) {
   asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];" ::"l"(m),
@@ -363,6 +388,8 @@ struct Params {
   const uint8_t* mx_b1_sf;
   uint8_t* mx_aq;
   uint8_t* mx_aq_sf;
+  uint8_t* mx_gq;      // dA (BF16 GEMM) in the MX variant: dG||dU also quantised for the dX GEMM
+  uint8_t* mx_gq_sf;
   int mx_split_n;
 };
 
@@ -936,6 +963,7 @@ __global__ void __launch_bounds__(THREADS, 1)
         } else if (KIND == GK_DACT) {
           if (rows_ok && n < p.g) {
             uint8_t* buf = wbuf;
+            uint32_t qg[8], qu[8];   // MX: the first 16 columns' dG / dU (bf16 pairs) of this block
 #pragma unroll
             for (int h2 = 0; h2 < 2; h2++) {
               const int n2 = n + 16 * h2;
@@ -974,6 +1002,18 @@ __global__ void __launch_bounds__(THREADS, 1)
                 og[j] = pack_bf16(r2v[0][0], r2v[1][0]);
                 ou[j] = pack_bf16(r2v[0][1], r2v[1][1]);
                 oa[j] = pack_bf16(r2v[0][2], r2v[1][2]);
+              }
+              if (p.mx_gq) {
+                // MX variant: dG and dU of this 32-column block -> E4M3 + scale for the dX GEMM
+                if (h2 == 0) {
+#pragma unroll
+                  for (int j = 0; j < 8; j++) { qg[j] = og[j]; qu[j] = ou[j]; }
+                } else {
+                  const int64_t K2 = 2 * (int64_t)p.g;
+                  mx_store_block_bf16(qg, og, p.mx_gq + row * K2 + n, p.mx_gq_sf + mx_sf_off(row, n >> 5, K2));
+                  mx_store_block_bf16(qu, ou, p.mx_gq + row * K2 + p.g + n,
+                                      p.mx_gq_sf + mx_sf_off(row, (p.g + n) >> 5, K2));
+                }
               }
 #pragma unroll
               for (int cc = 0; cc < 2; cc++) {
@@ -1156,6 +1196,8 @@ int launch(const GemmProblem<__nv_bfloat16>& gp, cudaStream_t st) {
   p.store_gu = gp.store_gu;
   p.beta = gp.wgrad_beta;
   p.row_addr = gp.row_addr;
+  p.mx_gq = gp.mx_gq;
+  p.mx_gq_sf = gp.mx_gq_sf;
   const uint64_t R = (uint64_t)gp.rows_cap, h = gp.h, g = gp.g, El = gp.El;
   if (R == 0) return 0;
   CUtensorMap mA, mB0, mB1, mO0, mO1;

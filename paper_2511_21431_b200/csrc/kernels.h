@@ -37,7 +37,8 @@ void launch_ep_recv_seg(const int* counts, int C, int j, int E, int El, int me, 
 template <typename T>
 void launch_dispatch_scatter(const T* x, const T* dy, const int32_t* ids, const float* w, int64_t t0,
                              int64_t t1, int k, int E, int h, const ChunkMeta& m, T* xd, T* dyd, int El,
-                             bool expert_major, int64_t rows_cap, cudaStream_t st);
+                             bool expert_major, int64_t rows_cap, cudaStream_t st,
+                             uint8_t* xq = nullptr, uint8_t* xsf = nullptr, bool write_x = true);
 // Index pass only (stable ranks -> dest_of, row_src, scores), for the fused P2P dispatch.
 void launch_dispatch_index(const int32_t* ids, const float* w, int64_t t0, int64_t t1, int k, int E,
                            const ChunkMeta& m, int* row_src, float* w_row, cudaStream_t st);
@@ -151,6 +152,8 @@ struct GemmProblem {
                              //    W_gate^T / W_up^T (DX; K split at g)
   uint8_t* mx_aq;            // GATEUP forward output: a quantised (codes [R][g]) ...
   uint8_t* mx_aq_sf;         // ... and its block scales
+  uint8_t* mx_gq;            // DACT (BF16) in the MX variant: dG||dU also quantised ([R][2g]) ...
+  uint8_t* mx_gq_sf;         // ... with scales (non-null = on)
 };
 
 // CUDA-core FFMA path (MEMFINE_FP32 mode; K12 of SURVEY §2.4).
@@ -165,8 +168,9 @@ int sm100_num_sms();
 // Rows and K multiples of 128 (scale chunks).
 void launch_mx_quant_rows(const __nv_bfloat16* src, int64_t ld, int64_t rows_max, const int* info, int K,
                           uint8_t* q, uint8_t* sf, cudaStream_t st);
-// src [B][R][Cc] -> q [B][Cc][R] blocked along R (R % 128 == 0, Cc % 128 == 0)
-void launch_mx_quant_transpose(const __nv_bfloat16* src, int B, int R, int Cc, uint8_t* q, uint8_t* sf,
-                               cudaStream_t st);
+// src [B][R][Cc] -> q_rows [B][R][Cc] blocked along Cc and q_t [B][Cc][R] blocked along R, one read
+void launch_mx_quant_dual(const __nv_bfloat16* src, int B, int R, int Cc, uint8_t* q_rows, uint8_t* sf_rows,
+                          uint8_t* q_t, uint8_t* sf_t, cudaStream_t st);
+
 
 }  // namespace memfine

@@ -162,8 +162,8 @@ uint64_t row_bytes_of(const memfine_dims& d, int pass) {
   uint64_t D = elt_bytes(d), h = d.hidden, g = d.ffn;
   uint64_t ep = d.ep_size > 1 ? 16 : 0;                            // row_addr, row_addr_w (EP>1)
   if (d.dtype == MEMFINE_MXFP8) {
-    // fwd: X (bf16) -> Xq + scales, a straight to Aq + scales, O (bf16)
-    if (pass == MEMFINE_FWD) return ep + 8 + D * h + (h + h / 32) + (g + g / 32) + D * h;
+    // fwd: x gathered straight to Xq + scales, a straight to Aq + scales, O (bf16)
+    if (pass == MEMFINE_FWD) return ep + 8 + (h + h / 32) + (g + g / 32) + D * h;
     // bwd: bf16 X, dY, G||U, a_w (dA and the weight gradients stay BF16) + Xq, dGUq with scales;
     // O aliases X
     return ep + 12 + D * (h + h + 2 * g + g) + (h + h / 32) + (2 * g + 2 * g / 32);
@@ -208,7 +208,8 @@ Layout carve(const memfine_dims& d, int C, int pass, void* ws, int64_t rows_cap,
     L.m.row_addr_w = b.take<uint64_t>(R);
   }
   if (pass == MEMFINE_BWD) L.m.dw_row = b.take<float>(R);
-  L.X = b.take<char>((uint64_t)R * d.hidden * D);
+  // (the MX forward keeps no bf16 copy of the dispatched rows: the gather writes E4M3 only)
+  if (!(d.dtype == MEMFINE_MXFP8 && pass == MEMFINE_FWD)) L.X = b.take<char>((uint64_t)R * d.hidden * D);
   if (d.dtype == MEMFINE_MXFP8) {
     const uint64_t hh = d.hidden, gg = d.ffn;
     L.Xq = b.take<uint8_t>((uint64_t)R * hh);
@@ -414,11 +415,11 @@ memfine_status fwd_ep1(memfine_handle_s* h, const T* x, const int32_t* ids, cons
     prof_begin(h, 6, st);
     launch_dispatch_hist(ids, t0, t1, k, E, L.m, h->status_d, st);
     launch_dispatch_scan(NB, E, El, 1, R, L.m, h->rows_d, h->rows_d + kMaxSub, j, st);
-    launch_dispatch_scatter<T>(x, nullptr, ids, w, t0, t1, k, E, hd, L.m, (T*)L.X, nullptr, El, true, R, st);
-    if constexpr (std::is_same<T, __nv_bfloat16>::value)
-      if (mx) launch_mx_quant_rows((const __nv_bfloat16*)L.X, hd, R, L.m.info, hd, L.Xq, L.Xsf, st);
+    // (MX: the gather writes x's E4M3 codes + scales only - the forward needs no bf16 copy)
+    launch_dispatch_scatter<T>(x, nullptr, ids, w, t0, t1, k, E, hd, L.m, (T*)L.X, nullptr, El, true, R, st,
+                               mx ? L.Xq : nullptr, mx ? L.Xsf : nullptr, !mx);
     prof_end(h, st);
-    h->last.kernel_launches += mx ? 5 : 4;
+    h->last.kernel_launches += 4;
     if (h->debug) {
       cudaStreamSynchronize(st);
       int rp = (int)h->rows_h[kMaxSub + j];
@@ -483,11 +484,10 @@ memfine_status bwd_ep1(memfine_handle_s* h, const T* dy, const T* x, const int32
     prof_begin(h, 6, st);
     launch_dispatch_hist(ids, t0, t1, k, E, L.m, h->status_d, st);
     launch_dispatch_scan(NB, E, El, 1, R, L.m, h->rows_d, h->rows_d + kMaxSub, j, st);
-    launch_dispatch_scatter<T>(x, dy, ids, w, t0, t1, k, E, hd, L.m, (T*)L.X, (T*)L.DY, El, true, R, st);
-    if constexpr (std::is_same<T, __nv_bfloat16>::value)
-      if (mx) launch_mx_quant_rows((const __nv_bfloat16*)L.X, hd, R, L.m.info, hd, L.Xq, L.Xsf, st);
+    launch_dispatch_scatter<T>(x, dy, ids, w, t0, t1, k, E, hd, L.m, (T*)L.X, (T*)L.DY, El, true, R, st,
+                               mx ? L.Xq : nullptr, mx ? L.Xsf : nullptr, true);
     prof_end(h, st);
-    h->last.kernel_launches += mx ? 5 : 4;
+    h->last.kernel_launches += 4;
     GemmProblem<T> p = base_problem<T>(h, L, wg, wu, wd);
     p.dWg = dwg;
     p.dWu = dwu;
@@ -503,15 +503,13 @@ memfine_status bwd_ep1(memfine_handle_s* h, const T* dy, const T* x, const int32
     // the GEMM is bound by its epilogue - reading R28)
     p.kind = GK_DACT;
     p.mx = 0;
+    if (mx) {   // ... whose epilogue also writes dG || dU as E4M3 + scales for the dX GEMM
+      p.mx_gq = L.GUq;
+      p.mx_gq_sf = L.GUsf;
+    }
     if (int rc = run_gemm<T>(h, p, st)) return (memfine_status)rc;
-    if constexpr (std::is_same<T, __nv_bfloat16>::value)
-      if (mx) {
-        // dG || dU rows -> E4M3 for the dX GEMM (blocks along 2g never straddle: g % 32 == 0)
-        prof_begin(h, 6, st);
-        launch_mx_quant_rows((const __nv_bfloat16*)L.GU, 2 * (int64_t)g, R, L.m.info, 2 * g, L.GUq, L.GUsf, st);
-        prof_end(h, st);
-        h->last.kernel_launches += 1;
-      }
+    p.mx_gq = nullptr;
+    p.mx_gq_sf = nullptr;
     // B5: weight gradients accumulate across chunks (reading R18)
     p.wgrad_beta = beta;
     p.kind = GK_WGRAD_DOWN;
@@ -1432,11 +1430,10 @@ memfine_status memfine_mx_quantize_weights(memfine_handle_t h, const void* w_gat
   auto sf = [&](int i) { return const_cast<uint8_t*>(W.op[i].sf); };
   const __nv_bfloat16 *wg = (const __nv_bfloat16*)w_gate, *wu = (const __nv_bfloat16*)w_up,
                       *wd = (const __nv_bfloat16*)w_down;
-  launch_mx_quant_rows(wg, hd, (int64_t)El * g, nullptr, hd, q(0), sf(0), st);
-  launch_mx_quant_rows(wu, hd, (int64_t)El * g, nullptr, hd, q(1), sf(1), st);
+  // W_gate / W_up: rows (blocks along h) and transposed (blocks along g) from one read each
+  launch_mx_quant_dual(wg, El, g, hd, q(0), sf(0), q(3), sf(3), st);
+  launch_mx_quant_dual(wu, El, g, hd, q(1), sf(1), q(4), sf(4), st);
   launch_mx_quant_rows(wd, g, (int64_t)El * hd, nullptr, g, q(2), sf(2), st);
-  launch_mx_quant_transpose(wg, El, g, hd, q(3), sf(3), st);   // [El][g][h] -> [El][h][g], blocks along g
-  launch_mx_quant_transpose(wu, El, g, hd, q(4), sf(4), st);
   h->mx_w = (const uint8_t*)wq;
   return latch_cuda(h);
 }

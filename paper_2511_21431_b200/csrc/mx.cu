@@ -50,46 +50,60 @@ __global__ void __launch_bounds__(256) mx_quant_rows_kernel(const __nv_bfloat16*
   }
 }
 
-// Transposing, for the backward weight operands: src [B][R][Cc] bf16 -> q [B][Cc][R] E4M3 blocked
-// along R (the GEMM's K), sf chunks per b at b * Cc * R / 32.  Tile: 128 R x 32 Cc through smem.
-__global__ void __launch_bounds__(256) mx_quant_transpose_kernel(const __nv_bfloat16* __restrict__ src, int R, int Cc,
-                                                                 uint8_t* __restrict__ q, uint8_t* __restrict__ sf) {
-  __shared__ float t[128][33];
-  const int b = blockIdx.z, r0 = blockIdx.y * 128, c0 = blockIdx.x * 32;
+// Both layouts of one weight in one pass (W_gate, W_up): src [B][R][Cc] bf16 ->
+//   q_rows [B][R][Cc] blocked along Cc (the forward's K = h) and q_t [B][Cc][R] blocked along R
+//   (dX's K = g), each with its scale chunks.  Tile 128 x 128 through smem, read once.
+__global__ void __launch_bounds__(256) mx_quant_dual_kernel(const __nv_bfloat16* __restrict__ src, int R, int Cc,
+                                                            uint8_t* __restrict__ q_rows, uint8_t* __restrict__ sf_rows,
+                                                            uint8_t* __restrict__ q_t, uint8_t* __restrict__ sf_t) {
+  __shared__ __nv_bfloat16 t[128][128 + 8];
+  const int b = blockIdx.z, r0 = blockIdx.y * 128, c0 = blockIdx.x * 128;
   const __nv_bfloat16* s = src + (int64_t)b * R * Cc;
-  // load 128 x 32 (4 threads x 8 elements per row, 64 rows per pass)
 #pragma unroll
-  for (int pass = 0; pass < 2; pass++) {
-    const int rr = pass * 64 + (threadIdx.x >> 2), cc = (threadIdx.x & 3) * 8;
-    const uint4 u = *reinterpret_cast<const uint4*>(s + (int64_t)(r0 + rr) * Cc + c0 + cc);
-    const uint32_t w[4] = {u.x, u.y, u.z, u.w};
-#pragma unroll
-    for (int j = 0; j < 4; j++) {
-      t[rr][cc + 2 * j] = __uint_as_float(w[j] << 16);
-      t[rr][cc + 2 * j + 1] = __uint_as_float(w[j] & 0xFFFF0000u);
-    }
+  for (int pass = 0; pass < 8; pass++) {
+    const int idx = pass * 256 + threadIdx.x;    // 16 x uint4 per row
+    const int rr = idx >> 4, cc = (idx & 15) * 8;
+    *reinterpret_cast<uint4*>(&t[rr][cc]) = *reinterpret_cast<const uint4*>(s + (int64_t)(r0 + rr) * Cc + c0 + cc);
   }
   __syncthreads();
-  if (threadIdx.x >= 128) return;
-  const int c = threadIdx.x >> 2, kb = threadIdx.x & 3;   // output row c0 + c, block kb of 4
-  float v[32];
-  float amax = 0.f;
+  auto quant32 = [](const float (&v)[32], uint8_t* q, uint8_t* sf) {
+    float amax = 0.f;
 #pragma unroll
-  for (int i = 0; i < 32; i++) {
-    v[i] = t[kb * 32 + i][c];
-    amax = fmaxf(amax, fabsf(v[i]));
+    for (int i = 0; i < 32; i++) amax = fmaxf(amax, fabsf(v[i]));
+    const int E = mx_exp(amax);
+    const float inv = mx_inv_scale(E);
+    uint32_t o[8];
+#pragma unroll
+    for (int j = 0; j < 8; j++)
+      o[j] = mx_e4m3x2(v[4 * j] * inv, v[4 * j + 1] * inv) | (mx_e4m3x2(v[4 * j + 2] * inv, v[4 * j + 3] * inv) << 16);
+    reinterpret_cast<uint4*>(q)[0] = make_uint4(o[0], o[1], o[2], o[3]);
+    reinterpret_cast<uint4*>(q)[1] = make_uint4(o[4], o[5], o[6], o[7]);
+    *sf = (uint8_t)(E + 127);
+  };
+  const int line = threadIdx.x >> 1;             // 0..127: a row (pass 1) / a column (pass 2)
+#pragma unroll
+  for (int k2 = 0; k2 < 2; k2++) {
+    const int kb = (threadIdx.x & 1) * 2 + k2;   // block 0..3 along the 128
+    float v[32];
+    // row-wise: row r0 + line, columns c0 + 32 kb ..
+#pragma unroll
+    for (int i = 0; i < 32; i++) v[i] = __bfloat162float(t[line][32 * kb + i]);
+    const int64_t gr = (int64_t)b * R + r0 + line;
+    quant32(v, q_rows + gr * Cc + c0 + 32 * kb, sf_rows + mx_sf_off(gr, (c0 >> 5) + kb, Cc));
+    // column-wise: column c0 + line, rows r0 + 32 kb .. (output row of q_t)
+#pragma unroll
+    for (int i = 0; i < 32; i++) v[i] = __bfloat162float(t[32 * kb + i][line]);
+    const int64_t gc = c0 + line;
+    quant32(v, q_t + ((int64_t)b * Cc + gc) * R + r0 + 32 * kb,
+            sf_t + (int64_t)b * Cc * (R / 32) + mx_sf_off(gc, (r0 >> 5) + kb, R));
   }
-  const int E = mx_exp(amax);
-  const float inv = mx_inv_scale(E);
-  uint32_t o[8];
-#pragma unroll
-  for (int j = 0; j < 8; j++)
-    o[j] = mx_e4m3x2(v[4 * j] * inv, v[4 * j + 1] * inv) | (mx_e4m3x2(v[4 * j + 2] * inv, v[4 * j + 3] * inv) << 16);
-  const int64_t orow = c0 + c;
-  uint8_t* dst = q + ((int64_t)b * Cc + orow) * R + r0 + kb * 32;
-  reinterpret_cast<uint4*>(dst)[0] = make_uint4(o[0], o[1], o[2], o[3]);
-  reinterpret_cast<uint4*>(dst)[1] = make_uint4(o[4], o[5], o[6], o[7]);
-  sf[(int64_t)b * Cc * (R / 32) + mx_sf_off(orow, (r0 >> 5) + kb, R)] = (uint8_t)(E + 127);
+}
+
+void launch_mx_quant_dual(const __nv_bfloat16* src, int B, int R, int Cc, uint8_t* q_rows, uint8_t* sf_rows,
+                          uint8_t* q_t, uint8_t* sf_t, cudaStream_t st) {
+  if (B <= 0 || R <= 0 || Cc <= 0) return;
+  dim3 grid((unsigned)(Cc / 128), (unsigned)(R / 128), (unsigned)B);
+  mx_quant_dual_kernel<<<grid, 256, 0, st>>>(src, R, Cc, q_rows, sf_rows, q_t, sf_t);
 }
 
 void launch_mx_quant_rows(const __nv_bfloat16* src, int64_t ld, int64_t rows_max, const int* info, int K,
@@ -100,11 +114,5 @@ void launch_mx_quant_rows(const __nv_bfloat16* src, int64_t ld, int64_t rows_max
   mx_quant_rows_kernel<<<(unsigned)blocks, 256, 0, st>>>(src, ld, rows_max, info, K, q, sf);
 }
 
-void launch_mx_quant_transpose(const __nv_bfloat16* src, int B, int R, int Cc, uint8_t* q, uint8_t* sf,
-                               cudaStream_t st) {
-  if (B <= 0 || R <= 0 || Cc <= 0) return;
-  dim3 grid((unsigned)(Cc / 32), (unsigned)(R / 128), (unsigned)B);
-  mx_quant_transpose_kernel<<<grid, 256, 0, st>>>(src, R, Cc, q, sf);
-}
 
 }  // namespace memfine

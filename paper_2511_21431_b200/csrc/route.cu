@@ -2,6 +2,7 @@
 // MACT tuner kernel.  HBM-bound data movement:
 // 16-byte vector loads/stores along contiguous rows, one warp per routed copy / token.
 #include <algorithm>
+#include <type_traits>
 #include "kernels.h"
 
 namespace memfine {
@@ -254,6 +255,66 @@ __global__ void __launch_bounds__(256) dispatch_gather_kernel(
   }
 }
 
+// MXFP8 variant (N4): the same gather, also quantising each x row into E4M3 codes + E8M0 block
+// scales (common.cuh mx_sf_off layout) on the fly: lanes 4j..4j+3 hold one 32-element block, the
+// block amax takes two shuffles.  write_x = 0 (the forward): only the quantised row is written.
+// Padding rows: zero codes, scale code 127 (E = 0), zero bf16 rows.
+__global__ void __launch_bounds__(256) dispatch_gather_mx_kernel(
+    const __nv_bfloat16* __restrict__ x, const __nv_bfloat16* __restrict__ dy, int k, int h,
+    int* __restrict__ row_src, const int* __restrict__ seg, const int* __restrict__ cnt, int El,
+    float* __restrict__ w_row, float* __restrict__ dw_row, const int* __restrict__ info, int write_x,
+    __nv_bfloat16* __restrict__ xd, __nv_bfloat16* __restrict__ dyd, uint8_t* __restrict__ xq,
+    uint8_t* __restrict__ xsf) {
+  if (info[kInfoSkip]) return;
+  const int rows = info[kInfoRowsPad];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int nwarps = gridDim.x * (blockDim.x >> 5);
+  const int nv = h / 8;   // uint4 per row (h % 32 == 0: blocks never straddle a quad of lanes)
+  for (int r = blockIdx.x * (blockDim.x >> 5) + warp; r < rows; r += nwarps) {
+    const int e = expert_of_row(seg, El, r);
+    const bool pad = r >= __ldg(seg + e) + __ldg(cnt + e);
+    int64_t tok = 0;
+    if (!pad) tok = row_src[r] / k;
+    else if (lane == 0) {
+      row_src[r] = -1;
+      w_row[r] = 0.f;
+      if (dw_row) dw_row[r] = 0.f;
+    }
+    const uint4* s = reinterpret_cast<const uint4*>(x + tok * h);
+    const uint4* s2 = dy ? reinterpret_cast<const uint4*>(dy + tok * h) : nullptr;
+    uint4* d = reinterpret_cast<uint4*>(xd + (int64_t)r * h);
+    uint4* d2 = dy ? reinterpret_cast<uint4*>(dyd + (int64_t)r * h) : nullptr;
+    for (int base = 0; base < nv; base += 32) {
+      const int i = base + lane;
+      const bool ok = i < nv;   // whole quads (nv % 4 == 0)
+      uint4 a = make_uint4(0, 0, 0, 0);
+      if (ok && !pad) a = __ldg(s + i);
+      if (ok && write_x) d[i] = a;
+      if (ok && dy) d2[i] = pad ? make_uint4(0, 0, 0, 0) : __ldg(s2 + i);
+      const uint32_t wv[4] = {a.x, a.y, a.z, a.w};
+      float v[8];
+      float amax = 0.f;
+#pragma unroll
+      for (int j = 0; j < 4; j++) {
+        v[2 * j] = __uint_as_float(wv[j] << 16);
+        v[2 * j + 1] = __uint_as_float(wv[j] & 0xFFFF0000u);
+        amax = fmaxf(amax, fmaxf(fabsf(v[2 * j]), fabsf(v[2 * j + 1])));
+      }
+      amax = fmaxf(amax, __shfl_xor_sync(0xffffffffu, amax, 1));
+      amax = fmaxf(amax, __shfl_xor_sync(0xffffffffu, amax, 2));
+      const int E = mx_exp(amax);
+      const float inv = mx_inv_scale(E);
+      uint2 o;
+      o.x = mx_e4m3x2(v[0] * inv, v[1] * inv) | (mx_e4m3x2(v[2] * inv, v[3] * inv) << 16);
+      o.y = mx_e4m3x2(v[4] * inv, v[5] * inv) | (mx_e4m3x2(v[6] * inv, v[7] * inv) << 16);
+      if (ok) {
+        *reinterpret_cast<uint2*>(xq + (int64_t)r * h + (int64_t)i * 8) = o;
+        if ((i & 3) == 0) xsf[mx_sf_off(r, i >> 2, h)] = (uint8_t)(E + 127);
+      }
+    }
+  }
+}
+
 void launch_dispatch_index(const int32_t* ids, const float* w, int64_t t0, int64_t t1, int k, int E,
                            const ChunkMeta& m, int* row_src, float* w_row, cudaStream_t st) {
   int NB = (int)ceil_div64(t1 - t0, kTokPerBlk);
@@ -266,7 +327,7 @@ void launch_dispatch_index(const int32_t* ids, const float* w, int64_t t0, int64
 template <typename T>
 void launch_dispatch_scatter(const T* x, const T* dy, const int32_t* ids, const float* w, int64_t t0, int64_t t1,
                              int k, int E, int h, const ChunkMeta& m, T* xd, T* dyd, int El, bool expert_major,
-                             int64_t rows_cap, cudaStream_t st) {
+                             int64_t rows_cap, cudaStream_t st, uint8_t* xq, uint8_t* xsf, bool write_x) {
   int NB = (int)ceil_div64(t1 - t0, kTokPerBlk);
   if (NB == 0) return;
   size_t smem = sizeof(int) * ((size_t)E + (size_t)kTokPerBlk * k);
@@ -275,6 +336,14 @@ void launch_dispatch_scatter(const T* x, const T* dy, const int32_t* ids, const 
                                                dy ? m.dw_row : nullptr, m.info);
   int64_t rows_ub = expert_major ? rows_cap : (t1 - t0) * k;
   int blocks = (int)std::min<int64_t>(ceil_div64(std::max<int64_t>(rows_ub, 1), 8), 148 * 16);
+  if constexpr (std::is_same<T, __nv_bfloat16>::value) {
+    if (xq && expert_major) {
+      dispatch_gather_mx_kernel<<<blocks, 256, 0, st>>>(x, dy, k, h, row_src, m.seg, m.recv_cnt, El, m.w_row,
+                                                         dy ? m.dw_row : nullptr, m.info, write_x ? 1 : 0, xd, dyd,
+                                                         xq, xsf);
+      return;
+    }
+  }
   dispatch_gather_kernel<T><<<blocks, 256, 0, st>>>(x, dy, k, h, row_src, row_src, expert_major ? m.seg : nullptr,
                                                     m.recv_cnt, El, expert_major ? m.w_row : nullptr,
                                                     (expert_major && dy) ? m.dw_row : nullptr, m.info,
@@ -648,10 +717,11 @@ void launch_plan_kernel(const int32_t* counts_dev, const PlanParams& p, memfine_
 // ------------------------------------------------------------------------------------------
 template void launch_dispatch_scatter<__nv_bfloat16>(const __nv_bfloat16*, const __nv_bfloat16*, const int32_t*,
                                                      const float*, int64_t, int64_t, int, int, int, const ChunkMeta&,
-                                                     __nv_bfloat16*, __nv_bfloat16*, int, bool, int64_t, cudaStream_t);
+                                                     __nv_bfloat16*, __nv_bfloat16*, int, bool, int64_t, cudaStream_t,
+                                                     uint8_t*, uint8_t*, bool);
 template void launch_dispatch_scatter<float>(const float*, const float*, const int32_t*, const float*, int64_t,
                                              int64_t, int, int, int, const ChunkMeta&, float*, float*, int, bool,
-                                             int64_t, cudaStream_t);
+                                             int64_t, cudaStream_t, uint8_t*, uint8_t*, bool);
 template void launch_p2p_push<__nv_bfloat16>(const __nv_bfloat16*, const __nv_bfloat16*, const float*, int, int, int,
                                              int, int, const int*, const int*, const int*, const PeerTable&,
                                              int64_t, cudaStream_t);
