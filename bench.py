@@ -234,6 +234,9 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--placement", default=None)
     ap.add_argument("--mx", type=int, default=1, help="also time the MXFP8 variant (SURVEY N4; N=1 only)")
+    ap.add_argument("--overlap", type=int, default=1,
+                    help="N>1, C>1: MEMFINE_FLAG_OVERLAP (chunk j+-1's exchange on a comm stream under chunk j's GEMMs)")
+    ap.add_argument("--comm-sms", type=int, default=0, help="with --overlap: SMs the GEMMs leave to the comm stream")
     ap.add_argument("--ep-transport", default="copy", choices=["copy", "p2p"],
                     help="N>1: 'copy' = permute into send buffers + NCCL all-to-allv; 'p2p' = dispatch/combine "
                          "fused into the permute kernel and the GEMM epilogues over CUDA-IPC peer memory")
@@ -270,7 +273,11 @@ def main():
     y, dx = torch.empty_like(x), torch.empty_like(x)
     dscore = torch.empty(w.shape, **f32)
 
-    mf = layer.MemFine(T, h, g, E, k, ep_size=EP, ep_rank=rank, dtype=torch.bfloat16, process_group=pg)
+    overlap = bool(args.overlap) and world > 1 and args.ep_transport == "copy"
+    mf = layer.MemFine(T, h, g, E, k, ep_size=EP, ep_rank=rank, dtype=torch.bfloat16, process_group=pg,
+                       overlap=overlap)
+    if overlap and args.comm_sms:
+        mf.set_comm_sms(args.comm_sms)
     bins = (1, 2, 4, 8)
 
     # ---------------------------------------------------------------- MACT: counts -> C (device tuner)
@@ -513,6 +520,7 @@ def main():
         "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
         "config": {**workload_config(cfg, args, world), "chunks": C, "tuner": plan,
                    "ep_transport": args.ep_transport if world > 1 else None,
+                   "overlap": overlap and C > 1,
                    "budget": {"gpu_capacity_bytes": cap, "alpha": args.alpha, "static_bytes": static},
                    "l2": "no flush: every step streams > 126 MB (weights 2.8 GB at EP=1, activations GBs)"},
         "peak_act_gb": peak_c, "peak_act_gb_unchunked": peak_1,

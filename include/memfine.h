@@ -75,7 +75,22 @@ typedef struct {
                            * MEMFINE_MXFP8 (bf16 storage; the gate/up, down and dX   *
                            *   GEMMs on MXFP8 operands, see memfine_mx_*; EP = 1,     *
                            *   hidden, ffn % 128 == 0)                                 */
+    int32_t flags;        /* MEMFINE_FLAG_* (0 = none).  Part of the workspace layout:  *
+                           * memfine_workspace_bytes and the fwd/bwd calls must see the *
+                           * same flags.                                                */
 } memfine_dims;
+
+/* memfine_dims.flags
+ *  MEMFINE_FLAG_OVERLAP (ep_size > 1, C > 1, EP_COPY transport): pipeline the FCDA chunk loop
+ *    over two streams, "the per-chunk dispatch and combine overlapped chunk by chunk with the
+ *    grouped GEMM" (north star; Eq. 6 / 7 order is unchanged): chunk j+1's
+ *    permute + dispatch all-to-allv and chunk j-1's combine all-to-allv + unpermute run on the
+ *    handle's high-priority comm stream while chunk j's GEMMs run on the caller's stream.  The
+ *    workspace holds two slots of the exchanged rows (send staging, X_disp, dY_disp, per-row
+ *    scores and metadata); G||U and a stay single (compute-only).  In the forward o is written
+ *    over X_disp, so the forward's per-row bytes do not grow; the backward's grow by 2h*D_t.
+ *    Ignored (layout and bytes identical to flags = 0) when ep_size == 1, C == 1 or MXFP8. */
+enum { MEMFINE_FLAG_OVERLAP = 1 };
 
 /* Memory budget for MACT (Eq. 3; Eq. 8). */
 typedef struct {
@@ -176,6 +191,12 @@ memfine_status memfine_create_local(const memfine_dims* dims, memfine_group_t gr
  * The workspace layout and size are the same for both. */
 enum { MEMFINE_EP_COPY = 0, MEMFINE_EP_P2P = 1 };
 memfine_status memfine_set_ep_transport(memfine_handle_t h, int32_t transport);
+
+/* MEMFINE_FLAG_OVERLAP only: number of SMs the expert GEMMs leave free for the comm stream's
+ * kernels (NCCL send/recv, permute, unpermute) while chunks overlap; 0 (default) = the GEMMs
+ * take every SM and the comm kernels interleave at kernel boundaries (the comm stream has the
+ * highest priority).  0 <= n < SM count, else MEMFINE_ERR_INVALID_ARG. */
+memfine_status memfine_set_comm_sms(memfine_handle_t h, int32_t n);
 
 /* Collective over the EP group (NCCL handles): export the device allocation holding `ws`
  * through CUDA IPC, all-gather (handle, offset) over the handle's communicator and map every

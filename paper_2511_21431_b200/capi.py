@@ -14,11 +14,12 @@ BF16, FP32, MXFP8 = 0, 1, 2
 RULE_EQ9, RULE_EXACT = 0, 1
 MODEL_PAPER, MODEL_IMPL = 0, 1
 EP_COPY, EP_P2P = 0, 1
+FLAG_OVERLAP = 1
 FWD, BWD = 0, 1
 
 # Every symbol include/memfine.h declares (checked by tests/test_abi.py).
 SYMBOLS = ("memfine_abi_version", "memfine_status_str", "memfine_nccl_unique_id", "memfine_create",
-           "memfine_destroy", "memfine_local_group_create", "memfine_local_group_destroy", "memfine_create_local", "memfine_set_ep_transport", "memfine_register_workspace", "memfine_route_counts", "memfine_plan", "memfine_workspace_bytes", "memfine_a2a_plan",
+           "memfine_destroy", "memfine_local_group_create", "memfine_local_group_destroy", "memfine_create_local", "memfine_set_ep_transport", "memfine_set_comm_sms", "memfine_register_workspace", "memfine_route_counts", "memfine_plan", "memfine_workspace_bytes", "memfine_a2a_plan",
            "memfine_moe_fwd", "memfine_moe_bwd", "memfine_router_fwd", "memfine_router_bwd", "memfine_sync", "memfine_last_stats",
            "memfine_profile_enable", "memfine_profile_read", "memfine_set_debug", "memfine_debug_perm",
            "memfine_mx_weights_bytes", "memfine_mx_quantize_weights", "memfine_mx_quantize")
@@ -36,7 +37,7 @@ class MemfineError(RuntimeError):
 class Dims(C.Structure):
     _fields_ = [("tokens", C.c_int64), ("hidden", C.c_int32), ("ffn", C.c_int32),
                 ("num_experts", C.c_int32), ("topk", C.c_int32), ("ep_size", C.c_int32),
-                ("ep_rank", C.c_int32), ("dtype", C.c_int32)]
+                ("ep_rank", C.c_int32), ("dtype", C.c_int32), ("flags", C.c_int32)]
 
 
 class Budget(C.Structure):
@@ -99,6 +100,7 @@ def lib():
         L.memfine_local_group_destroy.argtypes = [vp]
         L.memfine_create_local.argtypes = [C.POINTER(Dims), vp, C.POINTER(vp)]
         L.memfine_set_ep_transport.argtypes = [vp, i32]
+        L.memfine_set_comm_sms.argtypes = [vp, i32]
         L.memfine_register_workspace.argtypes = [vp, vp, u64, vp]
         L.memfine_route_counts.argtypes = [vp, vp, i32, vp, vp]
         L.memfine_plan.argtypes = [vp, i32, C.POINTER(Dims), C.POINTER(Budget), C.POINTER(PlanInfo)]

@@ -1260,7 +1260,7 @@ int launch(const GemmProblem<__nv_bfloat16>& gp, cudaStream_t st) {
   constexpr int TM = PAIR ? 2 * BM : BM;
   int nt = (p.N + BN - 1) / BN;
   const int per_unit = PAIR ? 2 : 1;
-  const int units_hw = g_num_sms / per_unit;
+  const int units_hw = (gp.sm_limit > 0 ? std::min(gp.sm_limit, g_num_sms) : g_num_sms) / per_unit;
   {
     // Raster group: gm M tiles x all N tiles, gm sized so the group's A strips take a per-kind L2
     // budget.  Cycles do not depend on it, DRAM traffic does - and under the power cap DRAM energy
@@ -1455,7 +1455,8 @@ int launch_mx(const GemmProblem<__nv_bfloat16>& gp, cudaStream_t st) {
   }
   const int per_unit = PAIR ? 2 : 1;
   int64_t max_tiles = (int64_t)((R / BM + (PAIR ? El : 0)) / per_unit + 1) * nt;
-  int units = (int)std::min<int64_t>(max_tiles, g_num_sms / per_unit);
+  const int sms = gp.sm_limit > 0 ? std::min(gp.sm_limit, g_num_sms) : g_num_sms;
+  int units = (int)std::min<int64_t>(max_tiles, sms / per_unit);
   if (units <= 0) return 0;
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(units * per_unit);

@@ -26,7 +26,8 @@ struct memfine_group_s {
   std::condition_variable cv;
   int arrived = 0, gen = 0;
   std::vector<cudaEvent_t> ready, done;
-  std::vector<std::array<char*, 12>> ptrs;  // per rank: buffers of the current call (slot 8: workspace)
+  std::vector<std::array<char*, 20>> ptrs;  // per rank: buffers of the current call ([slot*8 + kind];
+                                            // kPtrWs: workspace)
   void barrier() {
     std::unique_lock<std::mutex> lk(m);
     int g = gen;
@@ -74,6 +75,11 @@ struct memfine_handle_s {
   int* counts_h = nullptr;     // pinned mirror
   size_t counts_cap = 0;
   cudaEvent_t ev = nullptr;
+  // MEMFINE_FLAG_OVERLAP: the comm stream (highest priority) and its fork/join events
+  cudaStream_t cs = nullptr;
+  cudaEvent_t ev_disp[2] = {nullptr, nullptr}, ev_gemm[2] = {nullptr, nullptr};
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  int comm_sms = 0;
   // measurement (memfine_profile_enable)
   int prof = 0;
   struct Rec { int slot; cudaEvent_t a, b; };
@@ -120,6 +126,7 @@ bool dims_ok(const memfine_dims* d) {
   if (d->num_experts > 1024) return false;
   if (d->dtype != MEMFINE_BF16 && d->dtype != MEMFINE_FP32 && d->dtype != MEMFINE_MXFP8) return false;
   if (d->dtype == MEMFINE_MXFP8 && (d->hidden % 128 || d->ffn % 128)) return false;
+  if (d->flags & ~MEMFINE_FLAG_OVERLAP) return false;
   return true;
 }
 
@@ -158,7 +165,12 @@ struct Layout {
   uint64_t meta_bytes = 0, row_bytes = 0, total = 0;
 };
 
-uint64_t row_bytes_of(const memfine_dims& d, int pass) {
+// MEMFINE_FLAG_OVERLAP: two slots of the exchanged rows (chunk j+1 lands while chunk j computes).
+int ep_slots(const memfine_dims& d, int C) {
+  return (d.flags & MEMFINE_FLAG_OVERLAP) && d.ep_size > 1 && C > 1 && d.dtype != MEMFINE_MXFP8 ? 2 : 1;
+}
+
+uint64_t row_bytes_of(const memfine_dims& d, int pass, int slots = 1) {
   uint64_t D = elt_bytes(d), h = d.hidden, g = d.ffn;
   uint64_t ep = d.ep_size > 1 ? 16 : 0;                            // row_addr, row_addr_w (EP>1)
   if (d.dtype == MEMFINE_MXFP8) {
@@ -168,76 +180,120 @@ uint64_t row_bytes_of(const memfine_dims& d, int pass) {
     // O aliases X
     return ep + 12 + D * (h + h + 2 * g + g) + (h + h / 32) + (2 * g + 2 * g / 32);
   }
+  if (slots == 2) {
+    // per slot: src_of, w_row, row addresses, (bwd: dw_row, dY_disp), X_disp (o / dX_disp written
+    // over it); shared: a (fwd) / G||U + a_w (bwd)
+    if (pass == MEMFINE_FWD) return 2 * (ep + 8 + D * h) + D * g;
+    return 2 * (ep + 12 + D * 2 * h) + D * 3 * g;
+  }
   if (pass == MEMFINE_FWD) return ep + 4 + 4 + D * (h + g + h);   // src_of, w_row, X, A, O
   return ep + 4 + 4 + 4 + D * (h + h + 2 * g + g);                 // + dw_row, DY, GU; O aliases X
 }
 
 int64_t tmax_chunk(const memfine_dims& d, int C) { return ceil_div64(d.tokens, C); }
 
-// Carve: metadata, optional EP send staging (send_rows), then rows_cap rows.
-Layout carve(const memfine_dims& d, int C, int pass, void* ws, int64_t rows_cap, int64_t send_rows) {
-  Layout L;
+// Carve: metadata, optional EP send staging (send_rows), then rows_cap rows.  With two slots
+// (ep_slots) the metadata + staging and the exchanged row arrays are carved twice; slot s is
+// returned in L2[s] (L2 may be null when slots == 1).  The returned Layout is slot 0 and carries
+// the totals.
+Layout carve(const memfine_dims& d, int C, int pass, void* ws, int64_t rows_cap, int64_t send_rows,
+             Layout* L2 = nullptr) {
+  const int S = ep_slots(d, C);
+  Layout Ls[2];
   Bump b(ws);
   int E = d.num_experts, El = E / d.ep_size;
   int64_t Tm = tmax_chunk(d, C);
   int64_t NB = ceil_div64(Tm, kTokPerBlk);
   uint64_t D = elt_bytes(d);
-  L.m.blk_cnt = b.take<int>((uint64_t)NB * E);
-  L.m.exp_cnt = b.take<int>(E);
-  L.m.recv_cnt = b.take<int>(El);
-  L.m.seg = b.take<int>(El + 1);
-  L.m.pseg = b.take<int>(El + 1);
-  L.m.info = b.take<int>(kInfoWords);
-  L.m.dest_of = b.take<int>((uint64_t)Tm * d.topk);
-  if (d.ep_size > 1) {
-    L.m.send_src = b.take<int>((uint64_t)Tm * d.topk);
-    L.m.p2p_tab = b.take<int>((uint64_t)C * (4 * (uint64_t)E + 1));
-    L.send = b.take<char>((uint64_t)send_rows * d.hidden * D);
-    if (pass == MEMFINE_BWD) L.send_dy = b.take<char>((uint64_t)send_rows * d.hidden * D);
-    L.send_w = b.take<float>((uint64_t)send_rows);
+  for (int s = 0; s < S; s++) {
+    Layout& L = Ls[s];
+    L.m.blk_cnt = b.take<int>((uint64_t)NB * E);
+    L.m.exp_cnt = b.take<int>(E);
+    L.m.recv_cnt = b.take<int>(El);
+    L.m.seg = b.take<int>(El + 1);
+    L.m.pseg = b.take<int>(El + 1);
+    L.m.info = b.take<int>(kInfoWords);
+    L.m.dest_of = b.take<int>((uint64_t)Tm * d.topk);
+    if (d.ep_size > 1) {
+      L.m.send_src = b.take<int>((uint64_t)Tm * d.topk);
+      L.m.p2p_tab = b.take<int>((uint64_t)C * (4 * (uint64_t)E + 1));
+      L.send = b.take<char>((uint64_t)send_rows * d.hidden * D);
+      if (pass == MEMFINE_BWD) L.send_dy = b.take<char>((uint64_t)send_rows * d.hidden * D);
+      L.send_w = b.take<float>((uint64_t)send_rows);
+    }
   }
   b.off = (b.off + 255) & ~uint64_t(255);
-  L.meta_bytes = b.off;
-  L.row_bytes = row_bytes_of(d, pass);
-  L.rows_cap = rows_cap;
+  const uint64_t meta_bytes = b.off;
   int64_t R = rows_cap;
-  L.m.src_of = b.take<int>(R);
-  L.m.w_row = b.take<float>(R);
-  if (d.ep_size > 1) {
-    L.m.row_addr = b.take<uint64_t>(R);
-    L.m.row_addr_w = b.take<uint64_t>(R);
-  }
-  if (pass == MEMFINE_BWD) L.m.dw_row = b.take<float>(R);
-  // (the MX forward keeps no bf16 copy of the dispatched rows: the gather writes E4M3 only)
-  if (!(d.dtype == MEMFINE_MXFP8 && pass == MEMFINE_FWD)) L.X = b.take<char>((uint64_t)R * d.hidden * D);
-  if (d.dtype == MEMFINE_MXFP8) {
-    const uint64_t hh = d.hidden, gg = d.ffn;
-    L.Xq = b.take<uint8_t>((uint64_t)R * hh);
-    L.Xsf = b.take<uint8_t>((uint64_t)R * hh / 32);
-    if (pass == MEMFINE_BWD) {
-      L.DY = b.take<char>((uint64_t)R * hh * D);
-      L.GU = b.take<char>((uint64_t)R * 2 * gg * D);
-      L.A = b.take<char>((uint64_t)R * gg * D);
-      L.GUq = b.take<uint8_t>((uint64_t)R * 2 * gg);
-      L.GUsf = b.take<uint8_t>((uint64_t)R * 2 * gg / 32);
+  if (S == 2) {
+    for (int s = 0; s < 2; s++) {
+      Layout& L = Ls[s];
+      L.m.src_of = b.take<int>(R);
+      L.m.w_row = b.take<float>(R);
+      L.m.row_addr = b.take<uint64_t>(R);
+      L.m.row_addr_w = b.take<uint64_t>(R);
+      if (pass == MEMFINE_BWD) {
+        L.m.dw_row = b.take<float>(R);
+        L.DY = b.take<char>((uint64_t)R * d.hidden * D);
+      }
+      L.X = b.take<char>((uint64_t)R * d.hidden * D);
+      L.O = L.X;
+    }
+    void* GU = pass == MEMFINE_BWD ? b.take<char>((uint64_t)R * 2 * d.ffn * D) : nullptr;
+    void* A = b.take<char>((uint64_t)R * d.ffn * D);
+    for (int s = 0; s < 2; s++) {
+      Ls[s].GU = GU;
+      Ls[s].A = A;
+    }
+  } else {
+    Layout& L = Ls[0];
+    L.m.src_of = b.take<int>(R);
+    L.m.w_row = b.take<float>(R);
+    if (d.ep_size > 1) {
+      L.m.row_addr = b.take<uint64_t>(R);
+      L.m.row_addr_w = b.take<uint64_t>(R);
+    }
+    if (pass == MEMFINE_BWD) L.m.dw_row = b.take<float>(R);
+    // (the MX forward keeps no bf16 copy of the dispatched rows: the gather writes E4M3 only)
+    if (!(d.dtype == MEMFINE_MXFP8 && pass == MEMFINE_FWD)) L.X = b.take<char>((uint64_t)R * d.hidden * D);
+    if (d.dtype == MEMFINE_MXFP8) {
+      const uint64_t hh = d.hidden, gg = d.ffn;
+      L.Xq = b.take<uint8_t>((uint64_t)R * hh);
+      L.Xsf = b.take<uint8_t>((uint64_t)R * hh / 32);
+      if (pass == MEMFINE_BWD) {
+        L.DY = b.take<char>((uint64_t)R * hh * D);
+        L.GU = b.take<char>((uint64_t)R * 2 * gg * D);
+        L.A = b.take<char>((uint64_t)R * gg * D);
+        L.GUq = b.take<uint8_t>((uint64_t)R * 2 * gg);
+        L.GUsf = b.take<uint8_t>((uint64_t)R * 2 * gg / 32);
+        L.O = L.X;
+      } else {
+        L.Aq = b.take<uint8_t>((uint64_t)R * gg);
+        L.Asf = b.take<uint8_t>((uint64_t)R * gg / 32);
+        L.O = b.take<char>((uint64_t)R * hh * D);
+      }
+    } else if (pass == MEMFINE_BWD) {
+      L.DY = b.take<char>((uint64_t)R * d.hidden * D);
+      L.GU = b.take<char>((uint64_t)R * 2 * d.ffn * D);
+      L.A = b.take<char>((uint64_t)R * d.ffn * D);
       L.O = L.X;
     } else {
-      L.Aq = b.take<uint8_t>((uint64_t)R * gg);
-      L.Asf = b.take<uint8_t>((uint64_t)R * gg / 32);
-      L.O = b.take<char>((uint64_t)R * hh * D);
+      L.A = b.take<char>((uint64_t)R * d.ffn * D);
+      L.O = b.take<char>((uint64_t)R * d.hidden * D);
     }
-  } else if (pass == MEMFINE_BWD) {
-    L.DY = b.take<char>((uint64_t)R * d.hidden * D);
-    L.GU = b.take<char>((uint64_t)R * 2 * d.ffn * D);
-    L.A = b.take<char>((uint64_t)R * d.ffn * D);
-    L.O = L.X;
-  } else {
-    L.A = b.take<char>((uint64_t)R * d.ffn * D);
-    L.O = b.take<char>((uint64_t)R * d.hidden * D);
   }
   b.off = (b.off + 255) & ~uint64_t(255);
-  L.total = b.off;
-  return L;
+  for (int s = 0; s < S; s++) {
+    Ls[s].meta_bytes = meta_bytes;
+    Ls[s].row_bytes = row_bytes_of(d, pass, S);
+    Ls[s].rows_cap = rows_cap;
+    Ls[s].total = b.off;
+  }
+  if (L2) {
+    L2[0] = Ls[0];
+    L2[1] = Ls[S - 1];
+  }
+  return Ls[0];
 }
 
 // rows_cap that fits ws_bytes (multiple of 128; each row array then stays 256-aligned).
@@ -568,7 +624,8 @@ EpChunk ep_chunk_table(const memfine_dims& d, const int* counts, int C, int j) {
 }
 
 // ---- in-process group transport
-enum { kPtrSend = 0, kPtrSendDy = 1, kPtrSendW = 2, kPtrX = 3, kPtrDY = 4, kPtrO = 5, kPtrWRow = 6, kPtrDWRow = 7 };
+enum { kPtrSend = 0, kPtrSendDy = 1, kPtrSendW = 2, kPtrX = 3, kPtrDY = 4, kPtrO = 5, kPtrWRow = 6, kPtrDWRow = 7,
+       kPtrWs = 16 };
 
 // all ranks' device work before this point is visible to every rank's stream after it
 void local_fence(memfine_handle_s* h, cudaStream_t st, std::vector<cudaEvent_t>& evs) {
@@ -629,9 +686,9 @@ int ep_exchange(memfine_handle_s* h, const EpChunk& t, const int* counts, int C,
   if (h->lg) {
     // the buffer kinds are identified from the published pointer table
     int ks = -1, ke = -1;
-    for (int k = 0; k < 8; k++) {
-      if (h->lg->ptrs[me][k] == send_buf) ks = k;
-      if (h->lg->ptrs[me][k] == expert_buf) ke = k;
+    for (int k = 0; k < 16; k++) {
+      if (ks < 0 && h->lg->ptrs[me][k] == send_buf) ks = k;
+      if (ke < 0 && h->lg->ptrs[me][k] == expert_buf) ke = k;
     }
     if (ks < 0 || ke < 0) return 1;
     return local_exchange(h, counts, C, j, forward, ks, ke, row_bytes, st);
@@ -741,7 +798,7 @@ memfine_status ep_run_p2p(memfine_handle_s* h, int pass, const T* dy, const T* x
   h->last_meta = L.meta_bytes;
   h->last_row_bytes = L.row_bytes;
   if (h->lg) {
-    h->lg->ptrs[me][8] = (char*)ws;
+    h->lg->ptrs[me][kPtrWs] = (char*)ws;
     h->lg->barrier();  // every rank published its workspace
   } else if (ws != h->reg_ws || (int)h->peer_ws.size() != EP) {
     return MEMFINE_ERR_INVALID_ARG;  // P2P across processes needs memfine_register_workspace(ws) first
@@ -751,7 +808,7 @@ memfine_status ep_run_p2p(memfine_handle_s* h, int pass, const T* dy, const T* x
   for (int r = 0; r < EP; r++) {
     memfine_dims dr = d;
     dr.ep_rank = r;
-    char* base_r = h->lg ? h->lg->ptrs[r][8] : h->peer_ws[r];
+    char* base_r = h->lg ? h->lg->ptrs[r][kPtrWs] : h->peer_ws[r];
     Layout Lr = carve(dr, C, pass, base_r, rows_max[r], send_max[r]);
     pt.X[r] = (char*)Lr.X;
     pt.DY[r] = (char*)Lr.DY;
@@ -850,6 +907,28 @@ memfine_status ep_run_p2p(memfine_handle_s* h, int pass, const T* dy, const T* x
   return latch_cuda(h);
 }
 
+// The comm stream of MEMFINE_FLAG_OVERLAP (created on first use, highest priority).
+int ensure_comm_stream(memfine_handle_s* h) {
+  if (h->cs) return 0;
+  int lo = 0, hi = 0;
+  cudaDeviceGetStreamPriorityRange(&lo, &hi);
+  if (cudaStreamCreateWithPriority(&h->cs, cudaStreamNonBlocking, hi)) return 1;
+  for (cudaEvent_t* e : {&h->ev_disp[0], &h->ev_disp[1], &h->ev_gemm[0], &h->ev_gemm[1], &h->ev_fork, &h->ev_join})
+    if (cudaEventCreateWithFlags(e, cudaEventDisableTiming)) return 1;
+  return 0;
+}
+
+// The FCDA chunk loop with EP > 1 over send buffers + all-to-allv (MEMFINE_EP_COPY).
+// One slot: every step of chunk j on the caller's stream, in the order of Eq. 6 / Eq. 7.
+// Two slots (MEMFINE_FLAG_OVERLAP): the exchange side of each chunk - permute, dispatch
+// all-to-allv, (after the chunk's GEMMs) combine all-to-allv and unpermute - runs on the comm
+// stream cs, the GEMMs on st; chunk j uses slot j % 2.  Issue order on cs is
+//   dispatch(0) dispatch(1) combine(0) dispatch(2) combine(1) dispatch(3) ...
+// so chunk j+1's rows move while chunk j multiplies, and chunk j's results return while chunk
+// j+1 multiplies.  Hazards: GEMMs(j) wait ev_disp[j%2] (their rows and metadata arrived);
+// combine(j) waits ev_gemm[j%2] (o / dX_disp, d_w written); dispatch(j+2) reuses slot j%2 after
+// combine(j) in cs order; G||U and a are touched by st only.  Results are bit-identical to the
+// one-slot order: every kernel sees the same inputs.
 template <typename T>
 memfine_status ep_run(memfine_handle_s* h, int pass, const T* dy, const T* x, const int32_t* ids, const float* w,
                       const void* wg, const void* wu, const void* wd, int C, T* out, float* dwg, float* dwu,
@@ -858,7 +937,7 @@ memfine_status ep_run(memfine_handle_s* h, int pass, const T* dy, const T* x, co
     return ep_run_p2p<T>(h, pass, dy, x, ids, w, wg, wu, wd, C, out, dwg, dwu, dwd, dscore, accumulate, ws, ws_bytes,
                          st);
   const memfine_dims& d = h->d;
-  int E = d.num_experts, El = E / d.ep_size, k = d.topk, hd = d.hidden, g = d.ffn;
+  int E = d.num_experts, El = E / d.ep_size, k = d.topk, hd = d.hidden;
   if (int rc = ep_gather_counts(h, ids, C, st)) return (memfine_status)rc;
   std::vector<EpChunk> tab;
   int64_t rows_max = 0, send_max = 0;
@@ -867,70 +946,106 @@ memfine_status ep_run(memfine_handle_s* h, int pass, const T* dy, const T* x, co
     rows_max = std::max(rows_max, tab[j].rows_pad);
     send_max = std::max(send_max, tab[j].send);
   }
-  Layout L = carve(d, C, pass, ws, rows_max, send_max);
-  if (L.total > ws_bytes) return MEMFINE_ERR_WORKSPACE;
+  Layout Ls[2];
+  carve(d, C, pass, ws, rows_max, send_max, Ls);
+  if (Ls[0].total > ws_bytes) return MEMFINE_ERR_WORKSPACE;
+  const int S = ep_slots(d, C);
   if (h->lg) {
     auto& P = h->lg->ptrs[d.ep_rank];
-    P[kPtrSend] = (char*)L.send;
-    P[kPtrSendDy] = (char*)L.send_dy;
-    P[kPtrSendW] = (char*)L.send_w;
-    P[kPtrX] = (char*)L.X;
-    P[kPtrDY] = (char*)L.DY;
-    P[kPtrO] = (char*)L.O;
-    P[kPtrWRow] = (char*)L.m.w_row;
-    P[kPtrDWRow] = (char*)L.m.dw_row;
-    if (pass == MEMFINE_BWD) P[kPtrO] = nullptr;  // O aliases X in the backward
+    for (int s = 0; s < S; s++) {
+      const Layout& L = Ls[s];
+      char** Q = P.data() + 8 * s;
+      Q[kPtrSend] = (char*)L.send;
+      Q[kPtrSendDy] = (char*)L.send_dy;
+      Q[kPtrSendW] = (char*)L.send_w;
+      Q[kPtrX] = (char*)L.X;
+      Q[kPtrDY] = (char*)L.DY;
+      Q[kPtrO] = L.O == L.X ? nullptr : (char*)L.O;  // O aliases X in the backward and with two slots
+      Q[kPtrWRow] = (char*)L.m.w_row;
+      Q[kPtrDWRow] = (char*)L.m.dw_row;
+    }
   }
-  h->last_meta = L.meta_bytes;
-  h->last_row_bytes = L.row_bytes;
+  h->last_meta = Ls[0].meta_bytes;
+  h->last_row_bytes = Ls[0].row_bytes;
   size_t rb = (size_t)hd * sizeof(T);
-  int beta = accumulate ? 1 : 0;  // first chunk overwrites dW, later chunks accumulate
-  if (pass == MEMFINE_BWD) {
-    if (dscore && d.tokens > 0) MF_CUDA_OK(cudaMemsetAsync(dscore, 0, sizeof(float) * d.tokens * k, st));
+  if (pass == MEMFINE_BWD && dscore && d.tokens > 0)
+    MF_CUDA_OK(cudaMemsetAsync(dscore, 0, sizeof(float) * d.tokens * k, st));
+  cudaStream_t cs = st;
+  if (S == 2) {
+    if (ensure_comm_stream(h)) return MEMFINE_ERR_CUDA;
+    cs = h->cs;
+    MF_CUDA_OK(cudaEventRecord(h->ev_fork, st));   // inputs, dscore zeroing, counts
+    MF_CUDA_OK(cudaStreamWaitEvent(cs, h->ev_fork, 0));
   }
-  for (int j = 0; j < C; j++) {
+
+  // A5/B1 permute + A6 dispatch all-to-allv of chunk j into slot j % S (on cs)
+  auto dispatch = [&](int j) -> memfine_status {
+    const Layout& L = Ls[j % S];
     const EpChunk& t = tab[j];
     int64_t t0 = chunk_begin(d.tokens, C, j), t1 = chunk_begin(d.tokens, C, j + 1);
     int NB = (int)ceil_div64(t1 - t0, kTokPerBlk);
-    // A5/B1: permute my chunk into the send layout
     ChunkMeta ms = L.m;
     ms.src_of = nullptr;
     ms.w_row = L.send_w;
     ms.dw_row = nullptr;
     if (NB) {
-      launch_dispatch_hist(ids, t0, t1, k, E, L.m, h->status_d, st);
-      launch_dispatch_scan(NB, E, El, d.ep_size, L.rows_cap, L.m, nullptr, nullptr, j, st);
+      launch_dispatch_hist(ids, t0, t1, k, E, L.m, h->status_d, cs);
+      launch_dispatch_scan(NB, E, El, d.ep_size, L.rows_cap, L.m, nullptr, nullptr, j, cs);
       launch_dispatch_scatter<T>(x, pass == MEMFINE_BWD ? dy : nullptr, ids, w, t0, t1, k, E, hd, ms, (T*)L.send,
-                                 pass == MEMFINE_BWD ? (T*)L.send_dy : nullptr, El, false, 0, st);
+                                 pass == MEMFINE_BWD ? (T*)L.send_dy : nullptr, El, false, 0, cs);
       h->last.kernel_launches += 4;
     }
     launch_ep_recv_seg(h->counts_d, C, j, E, El, d.ep_rank, d.ep_size, L.rows_cap, L.m, h->rows_d,
-                       h->rows_d + kMaxSub, st);
-    // A6/B1: dispatch all-to-allv
-    prof_begin(h, 9, st);
-    if (ep_exchange(h, t, h->counts_h, C, j, true, (char*)L.send, (char*)L.X, rb, st)) return MEMFINE_ERR_NCCL;
+                       h->rows_d + kMaxSub, cs);
+    prof_begin(h, 9, cs);
+    if (ep_exchange(h, t, h->counts_h, C, j, true, (char*)L.send, (char*)L.X, rb, cs)) return MEMFINE_ERR_NCCL;
     if (pass == MEMFINE_BWD) {
-      if (ep_exchange(h, t, h->counts_h, C, j, true, (char*)L.send_dy, (char*)L.DY, rb, st)) return MEMFINE_ERR_NCCL;
-      if (ep_exchange(h, t, h->counts_h, C, j, true, (char*)L.send_w, (char*)L.m.w_row, 4, st))
+      if (ep_exchange(h, t, h->counts_h, C, j, true, (char*)L.send_dy, (char*)L.DY, rb, cs)) return MEMFINE_ERR_NCCL;
+      if (ep_exchange(h, t, h->counts_h, C, j, true, (char*)L.send_w, (char*)L.m.w_row, 4, cs))
         return MEMFINE_ERR_NCCL;
-      if (t.rows_pad) MF_CUDA_OK(cudaMemsetAsync(L.m.dw_row, 0, sizeof(float) * t.rows_pad, st));
+      if (t.rows_pad) MF_CUDA_OK(cudaMemsetAsync(L.m.dw_row, 0, sizeof(float) * t.rows_pad, cs));
     }
-    prof_end(h, st);
-    launch_zero_padding<T>(El, hd, L.m, (T*)L.X, pass == MEMFINE_BWD ? (T*)L.DY : nullptr, st);
+    prof_end(h, cs);
+    launch_zero_padding<T>(El, hd, L.m, (T*)L.X, pass == MEMFINE_BWD ? (T*)L.DY : nullptr, cs);
     h->last.kernel_launches += 2;
+    if (S == 2) MF_CUDA_OK(cudaEventRecord(h->ev_disp[j % 2], cs));
+    return MEMFINE_OK;
+  };
+  // A9/B6 combine all-to-allv + A10/B7 unpermute of chunk j (on cs)
+  auto combine = [&](int j) -> memfine_status {
+    const Layout& L = Ls[j % S];
+    const EpChunk& t = tab[j];
+    int64_t t0 = chunk_begin(d.tokens, C, j), t1 = chunk_begin(d.tokens, C, j + 1);
+    if (S == 2) MF_CUDA_OK(cudaStreamWaitEvent(cs, h->ev_gemm[j % 2], 0));
+    if (ep_exchange(h, t, h->counts_h, C, j, false, (char*)L.send, (char*)L.O, rb, cs)) return MEMFINE_ERR_NCCL;
+    if (pass == MEMFINE_FWD) {
+      if (t1 > t0) launch_combine<T>((const T*)L.send, w, t0, t1, k, hd, L.m, out, cs);
+    } else {
+      if (ep_exchange(h, t, h->counts_h, C, j, false, (char*)L.send_w, (char*)L.m.dw_row, 4, cs))
+        return MEMFINE_ERR_NCCL;
+      ChunkMeta mb = L.m;
+      mb.dw_row = L.send_w;
+      if (t1 > t0) launch_unpermute_reduce<T>((const T*)L.send, t0, t1, k, hd, mb, out, dscore, cs);
+    }
+    h->last.kernel_launches += 1;
+    return MEMFINE_OK;
+  };
+  int beta = accumulate ? 1 : 0;  // first chunk overwrites dW, later chunks accumulate
+  // A7-A8 / B2-B5 expert GEMMs of chunk j (on st)
+  auto compute = [&](int j) -> memfine_status {
+    const Layout& L = Ls[j % S];
+    if (S == 2) MF_CUDA_OK(cudaStreamWaitEvent(st, h->ev_disp[j % 2], 0));
     GemmProblem<T> p = base_problem<T>(h, L, wg, wu, wd);
     p.dWg = dwg;
     p.dWu = dwu;
     p.dWd = dwd;
+    if (S == 2) p.sm_limit = h->num_sms - h->comm_sms;
     if (pass == MEMFINE_FWD) {
       p.kind = GK_GATEUP;
       p.store_a = 1;
       if (int rc = run_gemm<T>(h, p, st)) return (memfine_status)rc;
-      p.kind = GK_DOWN;
+      p.kind = GK_DOWN;   // (two slots: o written over X_disp, dead after gate/up)
       if (int rc = run_gemm<T>(h, p, st)) return (memfine_status)rc;
-      // A9: combine all-to-allv back into my send layout, then A10
-      if (ep_exchange(h, t, h->counts_h, C, j, false, (char*)L.send, (char*)L.O, rb, st)) return MEMFINE_ERR_NCCL;
-      if (t1 > t0) launch_combine<T>((const T*)L.send, w, t0, t1, k, hd, L.m, out, st);
     } else {
       p.kind = GK_GATEUP;
       p.store_a = 0;
@@ -946,15 +1061,27 @@ memfine_status ep_run(memfine_handle_s* h, int pass, const T* dy, const T* x, co
       beta = 1;
       p.kind = GK_DX;
       if (int rc = run_gemm<T>(h, p, st)) return (memfine_status)rc;
-      // B6: dX rows and d_w back to the source ranks, then B7
-      if (ep_exchange(h, t, h->counts_h, C, j, false, (char*)L.send, (char*)L.O, rb, st)) return MEMFINE_ERR_NCCL;
-      if (ep_exchange(h, t, h->counts_h, C, j, false, (char*)L.send_w, (char*)L.m.dw_row, 4, st))
-        return MEMFINE_ERR_NCCL;
-      ChunkMeta mb = L.m;
-      mb.dw_row = L.send_w;
-      if (t1 > t0) launch_unpermute_reduce<T>((const T*)L.send, t0, t1, k, hd, mb, out, dscore, st);
     }
-    h->last.kernel_launches += 1;
+    if (S == 2) MF_CUDA_OK(cudaEventRecord(h->ev_gemm[j % 2], st));
+    return MEMFINE_OK;
+  };
+
+  if (S == 1) {
+    for (int j = 0; j < C; j++) {
+      if (memfine_status rc = dispatch(j)) return rc;
+      if (memfine_status rc = compute(j)) return rc;
+      if (memfine_status rc = combine(j)) return rc;
+    }
+  } else {
+    if (memfine_status rc = dispatch(0)) return rc;
+    for (int j = 0; j < C; j++) {
+      if (j + 1 < C)
+        if (memfine_status rc = dispatch(j + 1)) return rc;
+      if (memfine_status rc = compute(j)) return rc;
+      if (memfine_status rc = combine(j)) return rc;
+    }
+    MF_CUDA_OK(cudaEventRecord(h->ev_join, cs));
+    MF_CUDA_OK(cudaStreamWaitEvent(st, h->ev_join, 0));
   }
   return latch_cuda(h);
 }
@@ -1090,6 +1217,12 @@ memfine_status memfine_create_local(const memfine_dims* dims, memfine_group_t gr
   return MEMFINE_OK;
 }
 
+memfine_status memfine_set_comm_sms(memfine_handle_t h, int32_t n) {
+  if (!h || n < 0 || n >= h->num_sms) return MEMFINE_ERR_INVALID_ARG;
+  h->comm_sms = n;
+  return MEMFINE_OK;
+}
+
 memfine_status memfine_set_ep_transport(memfine_handle_t h, int32_t transport) {
   if (!h || (transport != MEMFINE_EP_COPY && transport != MEMFINE_EP_P2P)) return MEMFINE_ERR_INVALID_ARG;
   if (transport == MEMFINE_EP_P2P && h->d.ep_size > kMaxPeers) return MEMFINE_ERR_UNSUPPORTED;
@@ -1171,6 +1304,9 @@ memfine_status memfine_destroy(memfine_handle_t h) {
   if (h->counts_d) cudaFree(h->counts_d);
   if (h->counts_h) cudaFreeHost(h->counts_h);
   if (h->ev) cudaEventDestroy(h->ev);
+  for (cudaEvent_t e : {h->ev_disp[0], h->ev_disp[1], h->ev_gemm[0], h->ev_gemm[1], h->ev_fork, h->ev_join})
+    if (e) cudaEventDestroy(e);
+  if (h->cs) cudaStreamDestroy(h->cs);
   for (auto e : h->pool) cudaEventDestroy(e);
   delete h;
   return MEMFINE_OK;

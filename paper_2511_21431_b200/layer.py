@@ -26,11 +26,13 @@ def _stream(stream=None):
 
 
 def make_dims(tokens, hidden, ffn, num_experts, topk, ep_size=1, ep_rank=0, dtype=torch.bfloat16,
-              mx: bool = False) -> capi.Dims:
-    """mx=True: MEMFINE_MXFP8 (bf16 storage, MXFP8 expert-GEMM operands; dtype must be bf16)."""
+              mx: bool = False, overlap: bool = False) -> capi.Dims:
+    """mx=True: MEMFINE_MXFP8 (bf16 storage, MXFP8 expert-GEMM operands; dtype must be bf16).
+    overlap=True: MEMFINE_FLAG_OVERLAP (EP > 1, C > 1: exchange of chunk j+-1 on a comm stream
+    while chunk j's GEMMs run; two slots of exchanged rows in the workspace)."""
     assert not mx or dtype == torch.bfloat16
     return capi.Dims(int(tokens), int(hidden), int(ffn), int(num_experts), int(topk), int(ep_size), int(ep_rank),
-                     capi.MXFP8 if mx else _DT[dtype])
+                     capi.MXFP8 if mx else _DT[dtype], capi.FLAG_OVERLAP if overlap else 0)
 
 
 def mx_weights_bytes(dims: capi.Dims) -> int:
@@ -106,8 +108,8 @@ class MemFine:
     (torch.distributed) used only to broadcast the NCCL unique id when ep_size > 1."""
 
     def __init__(self, tokens, hidden, ffn, num_experts, topk, ep_size=1, ep_rank=0, dtype=torch.bfloat16,
-                 process_group=None, local_group=None, mx: bool = False):
-        self.dims = make_dims(tokens, hidden, ffn, num_experts, topk, ep_size, ep_rank, dtype, mx)
+                 process_group=None, local_group=None, mx: bool = False, overlap: bool = False):
+        self.dims = make_dims(tokens, hidden, ffn, num_experts, topk, ep_size, ep_rank, dtype, mx, overlap)
         self.dtype = dtype
         self.mx = mx
         self._wq = None
@@ -236,6 +238,10 @@ class MemFine:
 
     def set_ep_transport(self, transport: int):
         capi.check(capi.lib().memfine_set_ep_transport(self.h, int(transport)), "memfine_set_ep_transport")
+
+    def set_comm_sms(self, n: int):
+        """memfine_set_comm_sms: SMs the GEMMs leave to the comm stream while chunks overlap."""
+        capi.check(capi.lib().memfine_set_comm_sms(self.h, int(n)), "memfine_set_comm_sms")
 
     def register_workspace(self, ws: torch.Tensor, stream=None):
         """memfine_register_workspace (collective for NCCL handles): map every rank's workspace

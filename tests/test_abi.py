@@ -126,6 +126,45 @@ def test_workspace_bytes_formula_and_scaling():
     assert wsb[1] > ws[1] and wsb[8] < wsb[1] / 4
 
 
+def test_workspace_bytes_overlap_slots():
+    """MEMFINE_FLAG_OVERLAP: identical bytes where it does not apply (EP = 1, C = 1); with EP > 1
+    and C > 1 exactly two slots of the exchanged rows - forward per-row bytes 2(16+8+2h) + 2g
+    (o over X_disp), backward 2(16+12+4h) + 6g - on top of the hottest chunk's padded rows."""
+    rng = np.random.default_rng(11)
+    T, h, g, E, k, EP = 1024, 256, 512, 8, 2, 2
+    ids = [np.stack([rng.permutation(E)[:k] for _ in range(T)]).astype(np.int32) for _ in range(EP)]
+    od = oracle.Dims(T=T, h=h, g=g, E=E, k=k)
+    counts = np.stack([oracle.route_counts(od, i, 8)[0] for i in ids]).astype(np.int32)
+    ct = torch.from_numpy(counts)
+    ct1 = ct[:1].contiguous()
+    for C_ in (1, 2, 4):
+        for pass_ in (capi.FWD, capi.BWD):
+            # EP = 1: the flag is ignored
+            a = layer.workspace_bytes(ct1, layer.make_dims(T, h, g, E, k), C_, pass_)
+            b = layer.workspace_bytes(ct1, layer.make_dims(T, h, g, E, k, overlap=True), C_, pass_)
+            assert a == b
+            for r in range(EP):
+                d0 = layer.make_dims(T, h, g, E, k, ep_size=EP, ep_rank=r)
+                d1 = layer.make_dims(T, h, g, E, k, ep_size=EP, ep_rank=r, overlap=True)
+                w0 = layer.workspace_bytes(ct, d0, C_, pass_)
+                w1 = layer.workspace_bytes(ct, d1, C_, pass_)
+                if C_ == 1:
+                    assert w0 == w1
+                    continue
+                El, per = E // EP, 8 // C_
+                pad = max(sum(-(-int(counts[:, j * per:(j + 1) * per, e].sum()) // 128) * 128
+                              for e in range(r * El, (r + 1) * El)) for j in range(C_))
+                rb0 = 16 + 8 + 2 * (2 * h + g) if pass_ == capi.FWD else 16 + 12 + 2 * (2 * h + 3 * g)
+                rb1 = 2 * (16 + 8 + 2 * h) + 2 * g if pass_ == capi.FWD else 2 * (16 + 12 + 4 * h) + 6 * g
+                meta0, meta1 = w0 - pad * rb0, w1 - pad * rb1
+                # two copies of the metadata + send staging (256-byte aligned pieces)
+                assert 0 < meta0 < meta1 <= 2 * meta0 + 256, (C_, pass_, r, meta0, meta1)
+    bad = layer.make_dims(T, h, g, E, k)
+    bad.flags = 2
+    out = C.c_uint64()
+    assert capi.lib().memfine_workspace_bytes(None, 0, C.byref(bad), 1, 0, C.byref(out)) == capi.ERR_INVALID_ARG
+
+
 def test_impl_model_picks_smallest_fitting_bin():
     """MEMFINE_MODEL_IMPL: C = smallest bin whose exact backward workspace (max over EP ranks)
     fits B - static - other; checked against memfine_workspace_bytes directly."""

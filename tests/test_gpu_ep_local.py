@@ -27,19 +27,9 @@ def _bits(t, dtype):
         t.contiguous().numpy().astype(np.float32)
 
 
-@pytest.mark.parametrize("transport", [capi.EP_COPY, capi.EP_P2P])
-@pytest.mark.parametrize("EP,C,dtype", [(2, 1, torch.bfloat16), (2, 3, torch.bfloat16), (4, 2, torch.bfloat16),
-                                        (4, 1, torch.float32), (2, 2, torch.float32)])
-def test_ep_local_group_matches_oracle(EP, C, dtype, transport):
-    """transport EP_COPY: send buffers + stream-ordered copies (the NCCL path's layouts);
-    EP_P2P: dispatch and combine fused into the permute kernel and the down/dX GEMM epilogues,
-    storing rows straight into peer buffers."""
-    T, h, g, E, k = 300, 128, 256, 8, 2
+def _run_group(EP, C, dtype, transport, xs, dys, routes, wg, wu, wd, T, h, g, E, k):
+    """Every rank of an in-process EP group: fwd + bwd; returns (per-rank outputs, counts seen)."""
     El = E // EP
-    xs = [synth.make_x(T, h, rank=r, dtype=dtype) for r in range(EP)]
-    dys = [synth.make_dy(T, h, rank=r, dtype=dtype) for r in range(EP)]
-    routes = [synth.make_routing(T, E, k, rank=r, zipf_s=1.2, placement="contiguous") for r in range(EP)]
-    wg, wu, wd = synth.make_experts(range(E), h, g, dtype=dtype)
     group = layer.LocalGroup(EP)
     results, errors = [None] * EP, []
     counts_seen = [None] * EP
@@ -49,8 +39,11 @@ def test_ep_local_group_matches_oracle(EP, C, dtype, transport):
             torch.cuda.set_device(0)
             st = torch.cuda.Stream()
             with torch.cuda.stream(st):
-                mf = layer.MemFine(T, h, g, E, k, ep_size=EP, ep_rank=r, dtype=dtype, local_group=group)
-                mf.set_ep_transport(transport)
+                ov = transport == "overlap"
+                mf = layer.MemFine(T, h, g, E, k, ep_size=EP, ep_rank=r, dtype=dtype, local_group=group, overlap=ov)
+                mf.set_ep_transport(capi.EP_COPY if ov else transport)
+                if ov:
+                    mf.set_comm_sms(16)
                 dev = "cuda:0"
                 x, dy = xs[r].to(dev), dys[r].to(dev)
                 ids = torch.from_numpy(routes[r][0]).to(dev)
@@ -68,7 +61,7 @@ def test_ep_local_group_matches_oracle(EP, C, dtype, transport):
                 assert s_ == 0, capi.status_str(s_)
                 results[r] = [t.float().cpu().numpy() for t in (y, dx, ds, dwg, dwu, dwd)]
                 mf.close()
-        except BaseException as e:  # noqa: BLE001
+        except BaseException:  # noqa: BLE001
             import traceback
             errors.append(f"rank {r}: {traceback.format_exc()}")
 
@@ -79,6 +72,24 @@ def test_ep_local_group_matches_oracle(EP, C, dtype, transport):
         t.join(timeout=300)
     group.close()
     assert not errors, "\n".join(errors)
+    return results, counts_seen
+
+
+@pytest.mark.parametrize("transport", [capi.EP_COPY, capi.EP_P2P, "overlap"])
+@pytest.mark.parametrize("EP,C,dtype", [(2, 1, torch.bfloat16), (2, 3, torch.bfloat16), (4, 2, torch.bfloat16),
+                                        (4, 1, torch.float32), (2, 2, torch.float32)])
+def test_ep_local_group_matches_oracle(EP, C, dtype, transport):
+    """transport EP_COPY: send buffers + stream-ordered copies (the NCCL path's layouts);
+    EP_P2P: dispatch and combine fused into the permute kernel and the down/dX GEMM epilogues,
+    storing rows straight into peer buffers; "overlap": EP_COPY with MEMFINE_FLAG_OVERLAP (chunk
+    j+-1's exchange on the comm stream while chunk j's GEMMs run; GEMMs leave 16 SMs free)."""
+    T, h, g, E, k = 300, 128, 256, 8, 2
+    El = E // EP
+    xs = [synth.make_x(T, h, rank=r, dtype=dtype) for r in range(EP)]
+    dys = [synth.make_dy(T, h, rank=r, dtype=dtype) for r in range(EP)]
+    routes = [synth.make_routing(T, E, k, rank=r, zipf_s=1.2, placement="contiguous") for r in range(EP)]
+    wg, wu, wd = synth.make_experts(range(E), h, g, dtype=dtype)
+    results, counts_seen = _run_group(EP, C, dtype, transport, xs, dys, routes, wg, wu, wd, T, h, g, E, k)
     # every rank saw the same all-gathered counts, equal to the oracle's per-rank histograms
     od1 = oracle.Dims(T=T, h=h, g=g, E=E, k=k)
     ref_counts = np.stack([oracle.route_counts(od1, routes[r][0], C)[0] for r in range(EP)])
@@ -102,3 +113,20 @@ def test_ep_local_group_matches_oracle(EP, C, dtype, transport):
                 "dw_gate": rel_err(dwg, dwg_ref[es]), "dw_up": rel_err(dwu, dwu_ref[es]),
                 "dw_down": rel_err(dwd, dwd_ref[es])}
         assert all(v <= t_ for v in errs.values()), (r, errs)
+
+
+@pytest.mark.parametrize("EP,C", [(2, 3), (4, 4)])
+def test_ep_overlap_bit_identical(EP, C):
+    """MEMFINE_FLAG_OVERLAP changes when the exchange runs, not what any kernel reads: every
+    output is bit-identical to the one-stream order (the dW first-chunk overwrite included)."""
+    T, h, g, E, k = 700, 128, 256, 8, 2
+    dtype = torch.bfloat16
+    xs = [synth.make_x(T, h, rank=r, dtype=dtype) for r in range(EP)]
+    dys = [synth.make_dy(T, h, rank=r, dtype=dtype) for r in range(EP)]
+    routes = [synth.make_routing(T, E, k, rank=r, zipf_s=1.2, placement="random") for r in range(EP)]
+    wg, wu, wd = synth.make_experts(range(E), h, g, dtype=dtype)
+    a, _ = _run_group(EP, C, dtype, capi.EP_COPY, xs, dys, routes, wg, wu, wd, T, h, g, E, k)
+    b, _ = _run_group(EP, C, dtype, "overlap", xs, dys, routes, wg, wu, wd, T, h, g, E, k)
+    for r in range(EP):
+        for name, u, v in zip(("y", "dx", "dscore", "dw_gate", "dw_up", "dw_down"), a[r], b[r]):
+            np.testing.assert_array_equal(u, v, err_msg=f"rank {r} {name}")
