@@ -89,8 +89,14 @@ typedef struct {
  *    workspace holds two slots of the exchanged rows (send staging, X_disp, dY_disp, per-row
  *    scores and metadata); G||U and a stay single (compute-only).  In the forward o is written
  *    over X_disp, so the forward's per-row bytes do not grow; the backward's grow by 2h*D_t.
- *    Ignored (layout and bytes identical to flags = 0) when ep_size == 1, C == 1 or MXFP8. */
-enum { MEMFINE_FLAG_OVERLAP = 1 };
+ *    Ignored (layout and bytes identical to flags = 0) when ep_size == 1 (without EP_PATH), C == 1
+ *    or MXFP8.
+ *  MEMFINE_FLAG_EP_PATH (ep_size == 1 only, not MXFP8): run the expert-parallel data path - count
+ *    all-gather, send staging, per-(peer, local expert) all-to-allv, combine exchange - over a
+ *    1-rank NCCL communicator, every segment (including the self segment) through ncclSend /
+ *    ncclRecv.  memfine_create then takes a unique id.  Results equal the EP = 1 path; this is
+ *    how the NCCL transport is exercised on a single GPU (NCCL refuses two ranks on one device). */
+enum { MEMFINE_FLAG_OVERLAP = 1, MEMFINE_FLAG_EP_PATH = 2 };
 
 /* Memory budget for MACT (Eq. 3; Eq. 8). */
 typedef struct {
@@ -159,7 +165,8 @@ const char* memfine_status_str(memfine_status s);
 memfine_status memfine_nccl_unique_id(uint8_t out_id[128]);
 
 /* Create a handle on the CURRENT CUDA device.  nccl_unique_id: host, 128 bytes from
- * memfine_nccl_unique_id(), NULL iff dims->ep_size == 1.  Collective over the EP
+ * memfine_nccl_unique_id(), NULL iff dims->ep_size == 1 and MEMFINE_FLAG_EP_PATH is not
+ * set.  Collective over the EP
  * group when ep_size > 1 (ncclCommInitRank).  Fails with MEMFINE_ERR_CUDA if the
  * current device is not sm_100. */
 memfine_status memfine_create(const memfine_dims* dims, const uint8_t* nccl_unique_id,

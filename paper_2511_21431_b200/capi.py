@@ -14,7 +14,7 @@ BF16, FP32, MXFP8 = 0, 1, 2
 RULE_EQ9, RULE_EXACT = 0, 1
 MODEL_PAPER, MODEL_IMPL = 0, 1
 EP_COPY, EP_P2P = 0, 1
-FLAG_OVERLAP = 1
+FLAG_OVERLAP, FLAG_EP_PATH = 1, 2
 FWD, BWD = 0, 1
 
 # Every symbol include/memfine.h declares (checked by tests/test_abi.py).

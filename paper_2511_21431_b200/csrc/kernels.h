@@ -27,8 +27,8 @@ void launch_route_hist(const int32_t* ids, int64_t T, int k, int E, int nsub, in
                        int* status, cudaStream_t st);
 void launch_dispatch_hist(const int32_t* ids, int64_t t0, int64_t t1, int k, int E, const ChunkMeta& m,
                           int* status, cudaStream_t st);
-// ep_size == 1: expert-major padded layout; ep_size > 1: send layout (global expert order).
-void launch_dispatch_scan(int NB, int E, int El, int ep_size, int64_t rows_cap, const ChunkMeta& m,
+// send_layout 0: EP=1 expert-major padded layout; 1: EP send layout (global expert order).
+void launch_dispatch_scan(int NB, int E, int El, int send_layout, int64_t rows_cap, const ChunkMeta& m,
                           int64_t* stats_rows, int64_t* stats_rows_pad, int chunk, cudaStream_t st);
 void launch_ep_recv_seg(const int* counts, int C, int j, int E, int El, int me, int EP, int64_t rows_cap,
                         const ChunkMeta& m, int64_t* stats_rows, int64_t* stats_rows_pad, cudaStream_t st);

@@ -126,9 +126,14 @@ bool dims_ok(const memfine_dims* d) {
   if (d->num_experts > 1024) return false;
   if (d->dtype != MEMFINE_BF16 && d->dtype != MEMFINE_FP32 && d->dtype != MEMFINE_MXFP8) return false;
   if (d->dtype == MEMFINE_MXFP8 && (d->hidden % 128 || d->ffn % 128)) return false;
-  if (d->flags & ~MEMFINE_FLAG_OVERLAP) return false;
+  if (d->flags & ~(MEMFINE_FLAG_OVERLAP | MEMFINE_FLAG_EP_PATH)) return false;
+  if ((d->flags & MEMFINE_FLAG_EP_PATH) && (d->ep_size != 1 || d->dtype == MEMFINE_MXFP8)) return false;
   return true;
 }
+
+// The expert-parallel data path runs for ep_size > 1, or at ep_size == 1 over a 1-rank NCCL
+// communicator with MEMFINE_FLAG_EP_PATH (the NCCL transport exercised on one GPU).
+bool ep_path(const memfine_dims& d) { return d.ep_size > 1 || (d.flags & MEMFINE_FLAG_EP_PATH); }
 
 int elt_bytes(const memfine_dims& d) { return d.dtype == MEMFINE_FP32 ? 4 : 2; }  // MXFP8: bf16 storage
 
@@ -167,12 +172,12 @@ struct Layout {
 
 // MEMFINE_FLAG_OVERLAP: two slots of the exchanged rows (chunk j+1 lands while chunk j computes).
 int ep_slots(const memfine_dims& d, int C) {
-  return (d.flags & MEMFINE_FLAG_OVERLAP) && d.ep_size > 1 && C > 1 && d.dtype != MEMFINE_MXFP8 ? 2 : 1;
+  return (d.flags & MEMFINE_FLAG_OVERLAP) && ep_path(d) && C > 1 && d.dtype != MEMFINE_MXFP8 ? 2 : 1;
 }
 
 uint64_t row_bytes_of(const memfine_dims& d, int pass, int slots = 1) {
   uint64_t D = elt_bytes(d), h = d.hidden, g = d.ffn;
-  uint64_t ep = d.ep_size > 1 ? 16 : 0;                            // row_addr, row_addr_w (EP>1)
+  uint64_t ep = ep_path(d) ? 16 : 0;                               // row_addr, row_addr_w (EP>1)
   if (d.dtype == MEMFINE_MXFP8) {
     // fwd: x gathered straight to Xq + scales, a straight to Aq + scales, O (bf16)
     if (pass == MEMFINE_FWD) return ep + 8 + (h + h / 32) + (g + g / 32) + D * h;
@@ -214,7 +219,7 @@ Layout carve(const memfine_dims& d, int C, int pass, void* ws, int64_t rows_cap,
     L.m.pseg = b.take<int>(El + 1);
     L.m.info = b.take<int>(kInfoWords);
     L.m.dest_of = b.take<int>((uint64_t)Tm * d.topk);
-    if (d.ep_size > 1) {
+    if (ep_path(d)) {
       L.m.send_src = b.take<int>((uint64_t)Tm * d.topk);
       L.m.p2p_tab = b.take<int>((uint64_t)C * (4 * (uint64_t)E + 1));
       L.send = b.take<char>((uint64_t)send_rows * d.hidden * D);
@@ -249,7 +254,7 @@ Layout carve(const memfine_dims& d, int C, int pass, void* ws, int64_t rows_cap,
     Layout& L = Ls[0];
     L.m.src_of = b.take<int>(R);
     L.m.w_row = b.take<float>(R);
-    if (d.ep_size > 1) {
+    if (ep_path(d)) {
       L.m.row_addr = b.take<uint64_t>(R);
       L.m.row_addr_w = b.take<uint64_t>(R);
     }
@@ -470,7 +475,7 @@ memfine_status fwd_ep1(memfine_handle_s* h, const T* x, const int32_t* ids, cons
     int NB = (int)ceil_div64(t1 - t0, kTokPerBlk);
     prof_begin(h, 6, st);
     launch_dispatch_hist(ids, t0, t1, k, E, L.m, h->status_d, st);
-    launch_dispatch_scan(NB, E, El, 1, R, L.m, h->rows_d, h->rows_d + kMaxSub, j, st);
+    launch_dispatch_scan(NB, E, El, 0, R, L.m, h->rows_d, h->rows_d + kMaxSub, j, st);
     // (MX: the gather writes x's E4M3 codes + scales only - the forward needs no bf16 copy)
     launch_dispatch_scatter<T>(x, nullptr, ids, w, t0, t1, k, E, hd, L.m, (T*)L.X, nullptr, El, true, R, st,
                                mx ? L.Xq : nullptr, mx ? L.Xsf : nullptr, !mx);
@@ -539,7 +544,7 @@ memfine_status bwd_ep1(memfine_handle_s* h, const T* dy, const T* x, const int32
     // B1: re-dispatch x and dy of the chunk (the recompute of Eq. 7 starts from X_j)
     prof_begin(h, 6, st);
     launch_dispatch_hist(ids, t0, t1, k, E, L.m, h->status_d, st);
-    launch_dispatch_scan(NB, E, El, 1, R, L.m, h->rows_d, h->rows_d + kMaxSub, j, st);
+    launch_dispatch_scan(NB, E, El, 0, R, L.m, h->rows_d, h->rows_d + kMaxSub, j, st);
     launch_dispatch_scatter<T>(x, dy, ids, w, t0, t1, k, E, hd, L.m, (T*)L.X, (T*)L.DY, El, true, R, st,
                                mx ? L.Xq : nullptr, mx ? L.Xsf : nullptr, true);
     prof_end(h, st);
@@ -702,7 +707,7 @@ int ep_exchange(memfine_handle_s* h, const EpChunk& t, const int* counts, int C,
       int64_t s0 = t.send_off[eg], sn = t.send_off[eg + 1] - s0;
       // rows of src=peer for my local expert el in my expert-major buffer
       int64_t r0 = t.recv_off[(size_t)peer * El + el], rn = t.recv_cnt[(size_t)peer * El + el];
-      if (peer == me) {
+      if (peer == me && !(d.flags & MEMFINE_FLAG_EP_PATH)) {
         if (sn) {
           char* a = send_buf + s0 * row_bytes;
           char* b = expert_buf + r0 * row_bytes;
@@ -850,7 +855,7 @@ memfine_status ep_run_p2p(memfine_handle_s* h, int pass, const T* dy, const T* x
     int NB = (int)ceil_div64(t1 - t0, kTokPerBlk);
     if (NB) {
       launch_dispatch_hist(ids, t0, t1, k, E, L.m, h->status_d, st);
-      launch_dispatch_scan(NB, E, El, EP, L.rows_cap, L.m, nullptr, nullptr, j, st);
+      launch_dispatch_scan(NB, E, El, 1, L.rows_cap, L.m, nullptr, nullptr, j, st);
       launch_dispatch_index(ids, w, t0, t1, k, E, L.m, L.m.send_src, nullptr, st);
       h->last.kernel_launches += 3;
     }
@@ -990,7 +995,7 @@ memfine_status ep_run(memfine_handle_s* h, int pass, const T* dy, const T* x, co
     ms.dw_row = nullptr;
     if (NB) {
       launch_dispatch_hist(ids, t0, t1, k, E, L.m, h->status_d, cs);
-      launch_dispatch_scan(NB, E, El, d.ep_size, L.rows_cap, L.m, nullptr, nullptr, j, cs);
+      launch_dispatch_scan(NB, E, El, 1, L.rows_cap, L.m, nullptr, nullptr, j, cs);
       launch_dispatch_scatter<T>(x, pass == MEMFINE_BWD ? dy : nullptr, ids, w, t0, t1, k, E, hd, ms, (T*)L.send,
                                  pass == MEMFINE_BWD ? (T*)L.send_dy : nullptr, El, false, 0, cs);
       h->last.kernel_launches += 4;
@@ -1144,7 +1149,7 @@ memfine_status memfine_nccl_unique_id(uint8_t out_id[128]) {
 
 memfine_status memfine_create(const memfine_dims* dims, const uint8_t* nccl_unique_id, memfine_handle_t* out) {
   if (!out || !dims_ok(dims)) return MEMFINE_ERR_INVALID_ARG;
-  if ((dims->ep_size > 1) != (nccl_unique_id != nullptr)) return MEMFINE_ERR_INVALID_ARG;
+  if (ep_path(*dims) != (nccl_unique_id != nullptr)) return MEMFINE_ERR_INVALID_ARG;
   *out = nullptr;
   int dev;
   if (cudaGetDevice(&dev) != cudaSuccess) { cudaGetLastError(); return MEMFINE_ERR_CUDA; }
@@ -1165,7 +1170,7 @@ memfine_status memfine_create(const memfine_dims* dims, const uint8_t* nccl_uniq
   cudaHostGetDevicePointer((void**)&h->status_d, h->status_h, 0);
   cudaHostGetDevicePointer((void**)&h->rows_d, h->rows_h, 0);
   cudaEventCreateWithFlags(&h->ev, cudaEventDisableTiming);
-  if (dims->ep_size > 1) {
+  if (ep_path(*dims)) {
     if (nccl_comm_init(&h->comm, nccl_unique_id, dims->ep_size, dims->ep_rank)) {
       memfine_destroy(h);
       return MEMFINE_ERR_NCCL;
@@ -1330,7 +1335,7 @@ memfine_status memfine_route_counts(memfine_handle_t h, const int32_t* ids_dev, 
         MF_CUDA_OK(cudaMemcpyAsync(counts_dev + (int64_t)r * nsub * d.num_experts, h->lg->ptrs[r][0], nb,
                                    cudaMemcpyDeviceToDevice, st));
     local_fence(h, st, h->lg->done);
-  } else if (d.ep_size > 1) {
+  } else if (ep_path(d)) {
     if (nccl_all_gather_int(&h->comm, mine, counts_dev, (size_t)nsub * d.num_experts, st)) return MEMFINE_ERR_NCCL;
   }
   return MEMFINE_OK;
@@ -1479,7 +1484,7 @@ memfine_status memfine_workspace_bytes(const int32_t* counts_host, int32_t nsub,
     rows_pad_max = round_up64(total + (int64_t)El * (kRowAlign - 1), kRowAlign);
     send_max = Tm * d.topk;
   }
-  Layout L = carve(d, C, pass, nullptr, rows_pad_max, d.ep_size > 1 ? send_max : 0);
+  Layout L = carve(d, C, pass, nullptr, rows_pad_max, ep_path(d) ? send_max : 0);
   *bytes = L.total;
   return MEMFINE_OK;
 }
@@ -1519,7 +1524,7 @@ memfine_status memfine_moe_fwd(memfine_handle_t h, const void* x, const int32_t*
   cudaStream_t st = (cudaStream_t)stream;
   begin_call(h, C, MEMFINE_FWD, ws_bytes, st);
   if (h->d.ep_size > 1 && h->d.dtype == MEMFINE_MXFP8) return MEMFINE_ERR_UNSUPPORTED;
-  if (h->d.ep_size > 1) return memfine_ep_fwd(h, x, ids, w, w_gate, w_up, w_down, C, y, ws, ws_bytes, st);
+  if (ep_path(h->d)) return memfine_ep_fwd(h, x, ids, w, w_gate, w_up, w_down, C, y, ws, ws_bytes, st);
   if (h->d.dtype != MEMFINE_FP32)
     return fwd_ep1<__nv_bfloat16>(h, (const __nv_bfloat16*)x, ids, w, w_gate, w_up, w_down, C, (__nv_bfloat16*)y, ws,
                                   ws_bytes, st);
@@ -1536,7 +1541,7 @@ memfine_status memfine_moe_bwd(memfine_handle_t h, const void* dy, const void* x
   cudaStream_t st = (cudaStream_t)stream;
   begin_call(h, C, MEMFINE_BWD, ws_bytes, st);
   if (h->d.ep_size > 1 && h->d.dtype == MEMFINE_MXFP8) return MEMFINE_ERR_UNSUPPORTED;
-  if (h->d.ep_size > 1)
+  if (ep_path(h->d))
     return memfine_ep_bwd(h, dy, x, ids, w, w_gate, w_up, w_down, C, dx, dw_gate, dw_up, dw_down, dscore,
                           accumulate_dw, ws, ws_bytes, st);
   if (h->d.dtype != MEMFINE_FP32)
@@ -1658,7 +1663,7 @@ memfine_status memfine_router_bwd(memfine_handle_t h, const void* x, const void*
   int NB = (int)ceil_div64(d.tokens, kTokPerBlk);
   if (NB) {
     launch_dispatch_hist(ids, 0, d.tokens, k, E, rs.m, h->status_d, st);
-    launch_dispatch_scan(NB, E, E, 1, rs.rows_cap, rs.m, nullptr, nullptr, 0, st);
+    launch_dispatch_scan(NB, E, E, 0, rs.rows_cap, rs.m, nullptr, nullptr, 0, st);
     launch_dispatch_index(ids, nullptr, 0, d.tokens, k, E, rs.m, rs.m.src_of, nullptr, st);
   } else {
     MF_CUDA_OK(cudaMemsetAsync(rs.m.seg, 0, sizeof(int) * (E + 1), st));

@@ -79,11 +79,12 @@ void launch_dispatch_hist(const int32_t* ids, int64_t t0, int64_t t1, int k, int
 
 // ------------------------------------------------------------------------------------------
 // A5 dispatch, pass 2 (one CTA): exclusive scan over blocks per expert, expert bases, info.
-//  ep_size == 1: base[e] = padded prefix (every local expert's segment padded to 128 rows);
-//  ep_size  > 1: base[e] = unpadded prefix over global experts (the NCCL send layout:
-//                dest rank major because ranks hold contiguous expert blocks).
+//  send_layout == 0 (EP = 1): base[e] = padded prefix (every local expert's segment padded to
+//                128 rows);
+//  send_layout == 1 (the EP path): base[e] = unpadded prefix over global experts (the NCCL send
+//                layout: dest rank major because ranks hold contiguous expert blocks).
 // ------------------------------------------------------------------------------------------
-__global__ void dispatch_scan_kernel(int NB, int E, int El, int ep_size, int64_t rows_cap,
+__global__ void dispatch_scan_kernel(int NB, int E, int El, int send_layout, int64_t rows_cap,
                                      int* __restrict__ blk, int* __restrict__ exp_cnt, int* __restrict__ recv_cnt,
                                      int* __restrict__ seg, int* __restrict__ pseg, int* __restrict__ info,
                                      int64_t* stats_rows, int64_t* stats_rows_pad, int chunk) {
@@ -103,7 +104,7 @@ __global__ void dispatch_scan_kernel(int NB, int E, int El, int ep_size, int64_t
     for (int e = 0; e < E; e++) {
       int c = exp_cnt[e];
       send += c;
-      if (ep_size == 1) {
+      if (!send_layout) {
         base[e] = acc;
         seg[e] = acc;
         pseg[e] = pairs;
@@ -116,7 +117,7 @@ __global__ void dispatch_scan_kernel(int NB, int E, int El, int ep_size, int64_t
         acc += c;
       }
     }
-    if (ep_size == 1) {
+    if (!send_layout) {
       seg[El] = acc;
       pseg[El] = pairs;
       info[kInfoPairs] = pairs;
@@ -133,9 +134,9 @@ __global__ void dispatch_scan_kernel(int NB, int E, int El, int ep_size, int64_t
   for (int64_t i = threadIdx.x; i < (int64_t)NB * E; i += blockDim.x) blk[i] += base[i % E];
 }
 
-void launch_dispatch_scan(int NB, int E, int El, int ep_size, int64_t rows_cap, const ChunkMeta& m,
+void launch_dispatch_scan(int NB, int E, int El, int send_layout, int64_t rows_cap, const ChunkMeta& m,
                           int64_t* stats_rows, int64_t* stats_rows_pad, int chunk, cudaStream_t st) {
-  dispatch_scan_kernel<<<1, 1024, 0, st>>>(NB, E, El, ep_size, rows_cap, m.blk_cnt, m.exp_cnt, m.recv_cnt,
+  dispatch_scan_kernel<<<1, 1024, 0, st>>>(NB, E, El, send_layout, rows_cap, m.blk_cnt, m.exp_cnt, m.recv_cnt,
                                            m.seg, m.pseg, m.info, stats_rows, stats_rows_pad, chunk);
 }
 

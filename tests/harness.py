@@ -71,10 +71,10 @@ def oracle_tokens(p: Problem, toks):
 class GpuRun:
     """Runs route_counts -> plan -> fwd -> bwd on cuda:0 through the C ABI."""
 
-    def __init__(self, p: Problem, dev="cuda:0"):
+    def __init__(self, p: Problem, dev="cuda:0", **mf_kw):
         self.p = p
         self.dev = dev
-        self.mf = layer.MemFine(p.T, p.h, p.g, p.E, p.k, dtype=p.dtype)
+        self.mf = layer.MemFine(p.T, p.h, p.g, p.E, p.k, dtype=p.dtype, **mf_kw)
         g = lambda t: t.to(dev).contiguous()
         self.x, self.dy, self.ids, self.w = g(p.x), g(p.dy), g(p.ids), g(p.w)
         self.wg, self.wu, self.wd = g(p.wg), g(p.wu), g(p.wd)

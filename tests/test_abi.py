@@ -159,10 +159,18 @@ def test_workspace_bytes_overlap_slots():
                 meta0, meta1 = w0 - pad * rb0, w1 - pad * rb1
                 # two copies of the metadata + send staging (256-byte aligned pieces)
                 assert 0 < meta0 < meta1 <= 2 * meta0 + 256, (C_, pass_, r, meta0, meta1)
-    bad = layer.make_dims(T, h, g, E, k)
-    bad.flags = 2
     out = C.c_uint64()
+    bad = layer.make_dims(T, h, g, E, k)
+    bad.flags = 4   # unknown flag
     assert capi.lib().memfine_workspace_bytes(None, 0, C.byref(bad), 1, 0, C.byref(out)) == capi.ERR_INVALID_ARG
+    bad = layer.make_dims(T, h, g, E, k, ep_size=2, ep_path=True)   # EP_PATH is for ep_size == 1
+    assert capi.lib().memfine_workspace_bytes(None, 0, C.byref(bad), 1, 0, C.byref(out)) == capi.ERR_INVALID_ARG
+    # EP_PATH at ep_size == 1: the EP layout (send staging, row addresses), overlap slots apply
+    for pass_ in (capi.FWD, capi.BWD):
+        e1 = layer.workspace_bytes(ct1, layer.make_dims(T, h, g, E, k), 2, pass_)
+        ep = layer.workspace_bytes(ct1, layer.make_dims(T, h, g, E, k, ep_path=True), 2, pass_)
+        epo = layer.workspace_bytes(ct1, layer.make_dims(T, h, g, E, k, ep_path=True, overlap=True), 2, pass_)
+        assert e1 < ep < epo
 
 
 def test_impl_model_picks_smallest_fitting_bin():
