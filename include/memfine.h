@@ -73,8 +73,9 @@ typedef struct {
     int32_t dtype;        /* MEMFINE_BF16 (bf16 storage, fp32 accumulate, tcgen05)    *
                            * MEMFINE_FP32 (fp32 everywhere, CUDA-core FFMA; <=1e-5)   *
                            * MEMFINE_MXFP8 (bf16 storage; the gate/up, down and dX   *
-                           *   GEMMs on MXFP8 operands, see memfine_mx_*; EP = 1,     *
-                           *   hidden, ffn % 128 == 0)                                 */
+                           *   GEMMs on MXFP8 operands, see memfine_mx_*; hidden,     *
+                           *   ffn % 128 == 0; with EP the rows travel in bf16 and are *
+                           *   quantised on arrival; EP_COPY transport only)           */
     int32_t flags;        /* MEMFINE_FLAG_* (0 = none).  Part of the workspace layout:  *
                            * memfine_workspace_bytes and the fwd/bwd calls must see the *
                            * same flags.                                                */
@@ -91,7 +92,7 @@ typedef struct {
  *    over X_disp, so the forward's per-row bytes do not grow; the backward's grow by 2h*D_t.
  *    Ignored (layout and bytes identical to flags = 0) when ep_size == 1 (without EP_PATH), C == 1
  *    or MXFP8.
- *  MEMFINE_FLAG_EP_PATH (ep_size == 1 only, not MXFP8): run the expert-parallel data path - count
+ *  MEMFINE_FLAG_EP_PATH (ep_size == 1 only): run the expert-parallel data path - count
  *    all-gather, send staging, per-(peer, local expert) all-to-allv, combine exchange - over a
  *    1-rank NCCL communicator, every segment (including the self segment) through ncclSend /
  *    ncclRecv.  memfine_create then takes a unique id.  Results equal the EP = 1 path; this is
@@ -310,7 +311,9 @@ memfine_status memfine_router_bwd(memfine_handle_t h, const void* x, const void*
  * amax <= 448 * 2^E (no element clips; E = 0 for an all-zero block); elements are E4M3,
  * round-to-nearest-even.  Quantised operands: x and W_gate/W_up rows along h, a and W_down rows
  * along g (forward and recompute); dG||dU and W_gate/W_up columns along g (dX).  The dA GEMM
- * (bound by its fused epilogue) and the weight gradients stay BF16 x BF16 -> fp32.
+ * (bound by its fused epilogue) and the weight gradients stay BF16 x BF16 -> fp32.  With EP > 1
+ * (EP_COPY transport) the dispatched rows travel in bf16 and each rank quantises the rows it
+ * received (the same codes: x is blocked along h, per row); EP_P2P returns MEMFINE_ERR_UNSUPPORTED.
  *
  * memfine_mx_weights_bytes: bytes of the quantised-weights buffer for dims (dtype MXFP8).
  * memfine_mx_quantize_weights: quantise the handle's local experts' bf16 weights (dev, the

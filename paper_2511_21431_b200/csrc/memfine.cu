@@ -127,7 +127,7 @@ bool dims_ok(const memfine_dims* d) {
   if (d->dtype != MEMFINE_BF16 && d->dtype != MEMFINE_FP32 && d->dtype != MEMFINE_MXFP8) return false;
   if (d->dtype == MEMFINE_MXFP8 && (d->hidden % 128 || d->ffn % 128)) return false;
   if (d->flags & ~(MEMFINE_FLAG_OVERLAP | MEMFINE_FLAG_EP_PATH)) return false;
-  if ((d->flags & MEMFINE_FLAG_EP_PATH) && (d->ep_size != 1 || d->dtype == MEMFINE_MXFP8)) return false;
+  if ((d->flags & MEMFINE_FLAG_EP_PATH) && d->ep_size != 1) return false;
   return true;
 }
 
@@ -259,8 +259,10 @@ Layout carve(const memfine_dims& d, int C, int pass, void* ws, int64_t rows_cap,
       L.m.row_addr_w = b.take<uint64_t>(R);
     }
     if (pass == MEMFINE_BWD) L.m.dw_row = b.take<float>(R);
-    // (the MX forward keeps no bf16 copy of the dispatched rows: the gather writes E4M3 only)
-    if (!(d.dtype == MEMFINE_MXFP8 && pass == MEMFINE_FWD)) L.X = b.take<char>((uint64_t)R * d.hidden * D);
+    // (the MX forward at EP = 1 keeps no bf16 copy of the dispatched rows: the gather writes E4M3
+    // only; on the EP path X_disp receives the bf16 rows and o is later written over it)
+    if (!(d.dtype == MEMFINE_MXFP8 && pass == MEMFINE_FWD) || ep_path(d))
+      L.X = b.take<char>((uint64_t)R * d.hidden * D);
     if (d.dtype == MEMFINE_MXFP8) {
       const uint64_t hh = d.hidden, gg = d.ffn;
       L.Xq = b.take<uint8_t>((uint64_t)R * hh);
@@ -275,7 +277,7 @@ Layout carve(const memfine_dims& d, int C, int pass, void* ws, int64_t rows_cap,
       } else {
         L.Aq = b.take<uint8_t>((uint64_t)R * gg);
         L.Asf = b.take<uint8_t>((uint64_t)R * gg / 32);
-        L.O = b.take<char>((uint64_t)R * hh * D);
+        L.O = ep_path(d) ? L.X : b.take<char>((uint64_t)R * hh * D);
       }
     } else if (pass == MEMFINE_BWD) {
       L.DY = b.take<char>((uint64_t)R * d.hidden * D);
@@ -784,7 +786,7 @@ memfine_status ep_run_p2p(memfine_handle_s* h, int pass, const T* dy, const T* x
                           float* dwd, float* dscore, int accumulate, void* ws, uint64_t ws_bytes, cudaStream_t st) {
   const memfine_dims& d = h->d;
   const int E = d.num_experts, EP = d.ep_size, El = E / EP, k = d.topk, hd = d.hidden, me = d.ep_rank;
-  if (EP > kMaxPeers) return MEMFINE_ERR_UNSUPPORTED;
+  if (EP > kMaxPeers || d.dtype == MEMFINE_MXFP8) return MEMFINE_ERR_UNSUPPORTED;
   if (int rc = ep_gather_counts(h, ids, C, st)) return (memfine_status)rc;
   // every rank's chunk tables and workspace layout, from the shared counts
   std::vector<std::vector<EpChunk>> tabs(EP);
@@ -943,6 +945,9 @@ memfine_status ep_run(memfine_handle_s* h, int pass, const T* dy, const T* x, co
                          st);
   const memfine_dims& d = h->d;
   int E = d.num_experts, El = E / d.ep_size, k = d.topk, hd = d.hidden;
+  const bool mx = d.dtype == MEMFINE_MXFP8;
+  if (mx && !h->mx_w) return MEMFINE_ERR_INVALID_ARG;   // memfine_mx_quantize_weights first
+  MxWeightsLayout W = mx_weights_layout(d, h->mx_w);
   if (int rc = ep_gather_counts(h, ids, C, st)) return (memfine_status)rc;
   std::vector<EpChunk> tab;
   int64_t rows_max = 0, send_max = 0;
@@ -1045,19 +1050,43 @@ memfine_status ep_run(memfine_handle_s* h, int pass, const T* dy, const T* x, co
     p.dWu = dwu;
     p.dWd = dwd;
     if (S == 2) p.sm_limit = h->num_sms - h->comm_sms;
+    if constexpr (std::is_same<T, __nv_bfloat16>::value)
+      if (mx) {   // MXFP8 (reading R28): the received bf16 rows -> E4M3 + scale chunks
+        prof_begin(h, 6, st);
+        launch_mx_quant_rows((const __nv_bfloat16*)L.X, hd, L.rows_cap, L.m.info, hd, L.Xq, L.Xsf, st);
+        prof_end(h, st);
+        h->last.kernel_launches += 1;
+      }
     if (pass == MEMFINE_FWD) {
       p.kind = GK_GATEUP;
       p.store_a = 1;
+      if constexpr (std::is_same<T, __nv_bfloat16>::value)
+        if (mx) {
+          set_mx(p, {L.Xq, L.Xsf}, W.op[0], W.op[1]);
+          p.mx_aq = L.Aq;
+          p.mx_aq_sf = L.Asf;
+        }
       if (int rc = run_gemm<T>(h, p, st)) return (memfine_status)rc;
-      p.kind = GK_DOWN;   // (two slots: o written over X_disp, dead after gate/up)
+      p.kind = GK_DOWN;   // (two slots / MX: o written over X_disp, dead after gate/up)
+      if constexpr (std::is_same<T, __nv_bfloat16>::value)
+        if (mx) set_mx(p, {L.Aq, L.Asf}, W.op[2], W.op[2]);
       if (int rc = run_gemm<T>(h, p, st)) return (memfine_status)rc;
     } else {
       p.kind = GK_GATEUP;
       p.store_a = 0;
       p.store_gu = 1;
+      if constexpr (std::is_same<T, __nv_bfloat16>::value)
+        if (mx) set_mx(p, {L.Xq, L.Xsf}, W.op[0], W.op[1]);
       if (int rc = run_gemm<T>(h, p, st)) return (memfine_status)rc;
       p.kind = GK_DACT;
+      p.mx = 0;
+      if (mx) {   // BF16 dA GEMM whose epilogue also writes dG || dU as E4M3 + scales
+        p.mx_gq = L.GUq;
+        p.mx_gq_sf = L.GUsf;
+      }
       if (int rc = run_gemm<T>(h, p, st)) return (memfine_status)rc;
+      p.mx_gq = nullptr;
+      p.mx_gq_sf = nullptr;
       p.wgrad_beta = beta;
       p.kind = GK_WGRAD_DOWN;
       if (int rc = run_gemm<T>(h, p, st)) return (memfine_status)rc;
@@ -1065,6 +1094,8 @@ memfine_status ep_run(memfine_handle_s* h, int pass, const T* dy, const T* x, co
       if (int rc = run_gemm<T>(h, p, st)) return (memfine_status)rc;
       beta = 1;
       p.kind = GK_DX;
+      if constexpr (std::is_same<T, __nv_bfloat16>::value)
+        if (mx) set_mx(p, {L.GUq, L.GUsf}, W.op[3], W.op[4]);
       if (int rc = run_gemm<T>(h, p, st)) return (memfine_status)rc;
     }
     if (S == 2) MF_CUDA_OK(cudaEventRecord(h->ev_gemm[j % 2], st));
@@ -1094,7 +1125,7 @@ memfine_status ep_run(memfine_handle_s* h, int pass, const T* dy, const T* x, co
 memfine_status memfine_ep_fwd(memfine_handle_s* h, const void* x, const int32_t* ids, const float* w, const void* wg,
                               const void* wu, const void* wd, int C, void* y, void* ws, uint64_t ws_bytes,
                               cudaStream_t st) {
-  if (h->d.dtype == MEMFINE_BF16)
+  if (h->d.dtype != MEMFINE_FP32)   // BF16 and MXFP8 (bf16 storage)
     return ep_run<__nv_bfloat16>(h, MEMFINE_FWD, nullptr, (const __nv_bfloat16*)x, ids, w, wg, wu, wd, C,
                                  (__nv_bfloat16*)y, nullptr, nullptr, nullptr, nullptr, 0, ws, ws_bytes, st);
   return ep_run<float>(h, MEMFINE_FWD, nullptr, (const float*)x, ids, w, wg, wu, wd, C, (float*)y, nullptr, nullptr,
@@ -1105,7 +1136,7 @@ memfine_status memfine_ep_bwd(memfine_handle_s* h, const void* dy, const void* x
                               const void* wg, const void* wu, const void* wd, int C, void* dx, float* dwg, float* dwu,
                               float* dwd, float* dscore, int accumulate, void* ws, uint64_t ws_bytes,
                               cudaStream_t st) {
-  if (h->d.dtype == MEMFINE_BF16)
+  if (h->d.dtype != MEMFINE_FP32)   // BF16 and MXFP8 (bf16 storage)
     return ep_run<__nv_bfloat16>(h, MEMFINE_BWD, (const __nv_bfloat16*)dy, (const __nv_bfloat16*)x, ids, w, wg, wu,
                                  wd, C, (__nv_bfloat16*)dx, dwg, dwu, dwd, dscore, accumulate, ws, ws_bytes, st);
   return ep_run<float>(h, MEMFINE_BWD, (const float*)dy, (const float*)x, ids, w, wg, wu, wd, C, (float*)dx, dwg,
@@ -1523,7 +1554,6 @@ memfine_status memfine_moe_fwd(memfine_handle_t h, const void* x, const int32_t*
   if (!w_gate || !w_up || !w_down || !ws) return MEMFINE_ERR_INVALID_ARG;
   cudaStream_t st = (cudaStream_t)stream;
   begin_call(h, C, MEMFINE_FWD, ws_bytes, st);
-  if (h->d.ep_size > 1 && h->d.dtype == MEMFINE_MXFP8) return MEMFINE_ERR_UNSUPPORTED;
   if (ep_path(h->d)) return memfine_ep_fwd(h, x, ids, w, w_gate, w_up, w_down, C, y, ws, ws_bytes, st);
   if (h->d.dtype != MEMFINE_FP32)
     return fwd_ep1<__nv_bfloat16>(h, (const __nv_bfloat16*)x, ids, w, w_gate, w_up, w_down, C, (__nv_bfloat16*)y, ws,
@@ -1540,7 +1570,6 @@ memfine_status memfine_moe_bwd(memfine_handle_t h, const void* dy, const void* x
   if (!w_gate || !w_up || !w_down || !dw_gate || !dw_up || !dw_down || !ws) return MEMFINE_ERR_INVALID_ARG;
   cudaStream_t st = (cudaStream_t)stream;
   begin_call(h, C, MEMFINE_BWD, ws_bytes, st);
-  if (h->d.ep_size > 1 && h->d.dtype == MEMFINE_MXFP8) return MEMFINE_ERR_UNSUPPORTED;
   if (ep_path(h->d))
     return memfine_ep_bwd(h, dy, x, ids, w, w_gate, w_up, w_down, C, dx, dw_gate, dw_up, dw_down, dscore,
                           accumulate_dw, ws, ws_bytes, st);

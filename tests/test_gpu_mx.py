@@ -48,10 +48,10 @@ def test_mx_quantize_bit_exact():
     assert np.array_equal(_sf_rows(scales.cpu().numpy(), rows, K), ref_scales.reshape(rows, K // 32))
 
 
-def _mx_run(p, C):
+def _mx_run(p, C, **mf_kw):
     run = GpuRun(p)
     run.mf.close()
-    run.mf = layer.MemFine(p.T, p.h, p.g, p.E, p.k, mx=True)
+    run.mf = layer.MemFine(p.T, p.h, p.g, p.E, p.k, mx=True, **mf_kw)
     run.mf.mx_quantize_weights(run.wg, run.wu, run.wd)
     y, st, _, _ = run.fwd(C)
     assert st == 0
@@ -102,3 +102,19 @@ def test_mx_errors():
     small = torch.empty(16, dtype=torch.uint8, device="cuda:0")
     with pytest.raises(capi.MemfineError):
         mf.mx_quantize_weights(g(p.wg), g(p.wu), g(p.wd), wq=small)
+
+
+@pytest.mark.parametrize("C", [1, 3])
+def test_mx_nccl_ep_path_bit_identical(C):
+    """MXFP8 over the NCCL transport (MEMFINE_FLAG_EP_PATH, 1-rank communicator): the rows travel
+    in bf16 and are quantised on arrival - the same codes the EP = 1 gather writes - so every
+    output equals the EP = 1 MX path bit for bit - except d_score, whose per-row partials from
+    the dA GEMM's N tiles (g = 384: two) meet in an fp32 atomicAdd of run-dependent order."""
+    p = make_problem(700, 256, 384, 8, 2, zipf_s=1.2, seed=5)
+    a = _mx_run(p, C)
+    b = _mx_run(p, C, ep_path=True)
+    for key in a:
+        if key == "dscore":
+            assert rel_err(b[key], a[key]) <= 1e-6
+        else:
+            np.testing.assert_array_equal(a[key], b[key], err_msg=key)
