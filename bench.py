@@ -180,12 +180,26 @@ def cpu_baseline(cfg, ntok: int):
                       f"plus a fixed dW zeroing term"}
 
 
+def emulated_config(args):
+    """The config, or with --ep-emulate R one rank's expert load at EP=R: the same T tokens x top-k
+    copies routed over E/R experts (the GEMM shapes of a uniform EP=R share; the skew differs)."""
+    cfg = synth.CONFIGS[args.config]
+    if args.ep_emulate > 1:
+        import dataclasses
+        assert cfg.E % args.ep_emulate == 0 and cfg.k <= cfg.E // args.ep_emulate
+        cfg = dataclasses.replace(cfg, E=cfg.E // args.ep_emulate)
+    return cfg
+
+
 def workload_config(cfg, args, world: int) -> dict:
     """The workload both arms are measured on (config.workload of the JSON line)."""
     T = args.tokens or cfg.T
     placement = args.placement or cfg.placement
-    return {"workload": f"{cfg.name}-style MoE layer: E={cfg.E} top-{cfg.k} h={cfg.h} SwiGLU ffn={cfg.g}, {T} "
-                        f"tokens/GPU, Zipf({cfg.zipf_s}) routing ({placement} placement), EP={world}",
+    emu = (f" [one rank's load at EP={args.ep_emulate}: {T}x{cfg.k} copies over E/{args.ep_emulate}="
+           f"{cfg.E} local experts, run at EP=1]") if args.ep_emulate > 1 else ""
+    return {"workload": f"{cfg.name}-style MoE layer: E={cfg.E * args.ep_emulate} top-{cfg.k} h={cfg.h} SwiGLU "
+                        f"ffn={cfg.g}, {T} tokens/GPU, Zipf({cfg.zipf_s}) routing ({placement} placement), "
+                        f"EP={world}{emu}",
             "tokens_per_gpu": T, "ep": world}
 
 
@@ -194,7 +208,7 @@ def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
-    cfg = synth.CONFIGS[args.config]
+    cfg = emulated_config(args)
     ntok = args.ref_tokens
     times = []
     cores = None
@@ -233,6 +247,9 @@ def main():
     ap.add_argument("--ref-tokens", type=int, default=4)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--placement", default=None)
+    ap.add_argument("--ep-emulate", type=int, default=1,
+                    help="N=1 only: one rank's expert load at EP=R (T*k copies over E/R local experts); "
+                         "labelled in config.workload, never the headline")
     ap.add_argument("--mx", type=int, default=1, help="also time the MXFP8 variant (SURVEY N4; N=1 only)")
     ap.add_argument("--overlap", type=int, default=1,
                     help="N>1, C>1: MEMFINE_FLAG_OVERLAP (chunk j+-1's exchange on a comm stream under chunk j's GEMMs)")
@@ -248,7 +265,7 @@ def main():
     world, rank, local = dist_setup()
     assert world == args.gpus or args.gpus == 1 and world == 1, "run N>1 under torchrun"
     dev = torch.device("cuda", local)
-    cfg = synth.CONFIGS[args.config]
+    cfg = emulated_config(args)
     placement = args.placement or cfg.placement
     T = args.tokens or cfg.T
     EP = world

@@ -9,7 +9,7 @@
 namespace memfine {
 
 constexpr int kRowAlign = 128;   // every local expert's row segment is padded to 128 rows
-constexpr int kTokPerBlk = 128;  // tokens per dispatch block
+constexpr int kTokPerBlk = 32;   // tokens per dispatch block (ranking pass: 32*k copies per CTA)
 constexpr int kMaxSub = 64;      // max sub-chunks / chunks per call (memfine_stats.rows)
 
 // info[] words written by the dispatch scan kernel, read by the GEMM schedulers.

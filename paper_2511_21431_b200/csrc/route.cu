@@ -84,54 +84,97 @@ void launch_dispatch_hist(const int32_t* ids, int64_t t0, int64_t t1, int k, int
 //  send_layout == 1 (the EP path): base[e] = unpadded prefix over global experts (the NCCL send
 //                layout: dest rank major because ranks hold contiguous expert blocks).
 // ------------------------------------------------------------------------------------------
-__global__ void dispatch_scan_kernel(int NB, int E, int El, int send_layout, int64_t rows_cap,
+__device__ __forceinline__ int warp_incl_scan(int v, int lane) {
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    int n = __shfl_up_sync(0xffffffffu, v, o);
+    if (lane >= o) v += n;
+  }
+  return v;
+}
+
+__global__ void __launch_bounds__(1024) dispatch_scan_kernel(int NB, int E, int El, int send_layout, int64_t rows_cap,
                                      int* __restrict__ blk, int* __restrict__ exp_cnt, int* __restrict__ recv_cnt,
                                      int* __restrict__ seg, int* __restrict__ pseg, int* __restrict__ info,
                                      int64_t* stats_rows, int64_t* stats_rows_pad, int chunk) {
   __shared__ int base[1024];
-  for (int e = threadIdx.x; e < E; e += blockDim.x) {
-    int run = 0;
-    for (int b = 0; b < NB; b++) {
-      int c = blk[(int64_t)b * E + e];
-      blk[(int64_t)b * E + e] = run;
-      run += c;
-    }
-    exp_cnt[e] = run;
-  }
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    int acc = 0, send = 0, pairs = 0;
-    for (int e = 0; e < E; e++) {
-      int c = exp_cnt[e];
-      send += c;
-      if (!send_layout) {
-        base[e] = acc;
-        seg[e] = acc;
-        pseg[e] = pairs;
-        recv_cnt[e] = c;
-        int pad = (int)round_up64(c, kRowAlign);
-        acc += pad;
-        pairs += (pad / kRowAlign + 1) / 2;
-      } else {
-        base[e] = acc;
-        acc += c;
+  __shared__ int cnt_s[1024];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+  // per expert (one warp each): exclusive scan over the token blocks, 32 blocks per step
+  for (int e = warp; e < E; e += nw) {
+    int carry = 0;
+    for (int b0 = 0; b0 < NB; b0 += 256) {  // 8 independent loads per lane per round trip
+      int c[8];
+#pragma unroll
+      for (int u = 0; u < 8; u++) {
+        const int b = b0 + u * 32 + lane;
+        c[u] = b < NB ? blk[(int64_t)b * E + e] : 0;
+      }
+#pragma unroll
+      for (int u = 0; u < 8; u++) {
+        const int b = b0 + u * 32 + lane;
+        const int incl = warp_incl_scan(c[u], lane);
+        if (b < NB) blk[(int64_t)b * E + e] = carry + incl - c[u];
+        carry += __shfl_sync(0xffffffffu, incl, 31);
       }
     }
-    if (!send_layout) {
-      seg[El] = acc;
-      pseg[El] = pairs;
-      info[kInfoPairs] = pairs;
-      info[kInfoRows] = send;
-      info[kInfoRowsPad] = acc;
-      info[kInfoSkip] = (acc > rows_cap) ? 1 : 0;
-      if (stats_rows) { stats_rows[chunk] = send; stats_rows_pad[chunk] = acc; }
-    } else {
-      info[kInfoSkip] = 0;  // EP>1: the host checked the capacity exactly (it knows the counts)
-    }
-    info[kInfoSend] = send;
+    if (lane == 0) { exp_cnt[e] = carry; cnt_s[e] = carry; }
   }
   __syncthreads();
-  for (int64_t i = threadIdx.x; i < (int64_t)NB * E; i += blockDim.x) blk[i] += base[i % E];
+  // expert bases (warp 0, 32 experts per step)
+  if (warp == 0) {
+    int acc = 0, send = 0, pairs = 0;
+    for (int e0 = 0; e0 < E; e0 += 32) {
+      const int e = e0 + lane;
+      const int c = e < E ? cnt_s[e] : 0;
+      const int ic = warp_incl_scan(c, lane);
+      if (!send_layout) {
+        const int pad = (int)round_up64(c, kRowAlign);
+        const int pr = e < E ? (pad / kRowAlign + 1) / 2 : 0;
+        const int ipad = warp_incl_scan(pad, lane), ipr = warp_incl_scan(pr, lane);
+        if (e < E) {
+          base[e] = acc + ipad - pad;
+          seg[e] = acc + ipad - pad;
+          pseg[e] = pairs + ipr - pr;
+          recv_cnt[e] = c;
+        }
+        acc += __shfl_sync(0xffffffffu, ipad, 31);
+        pairs += __shfl_sync(0xffffffffu, ipr, 31);
+      } else {
+        if (e < E) base[e] = acc + ic - c;
+        acc += __shfl_sync(0xffffffffu, ic, 31);
+      }
+      send += __shfl_sync(0xffffffffu, ic, 31);
+    }
+    if (lane == 0) {
+      if (!send_layout) {
+        seg[El] = acc;
+        pseg[El] = pairs;
+        info[kInfoPairs] = pairs;
+        info[kInfoRows] = send;
+        info[kInfoRowsPad] = acc;
+        info[kInfoSkip] = (acc > rows_cap) ? 1 : 0;
+        if (stats_rows) { stats_rows[chunk] = send; stats_rows_pad[chunk] = acc; }
+      } else {
+        info[kInfoSkip] = 0;  // EP>1: the host checked the capacity exactly (it knows the counts)
+      }
+      info[kInfoSend] = send;
+    }
+  }
+  __syncthreads();
+  const int64_t n = (int64_t)NB * E;
+  if ((E & 3) == 0) {
+    int4* b4 = reinterpret_cast<int4*>(blk);
+#pragma unroll 4
+    for (int64_t i = threadIdx.x; i < n / 4; i += blockDim.x) {
+      int4 v = b4[i];
+      const int e = (int)((i * 4) % E);
+      v.x += base[e]; v.y += base[e + 1]; v.z += base[e + 2]; v.w += base[e + 3];
+      b4[i] = v;
+    }
+  } else {
+    for (int64_t i = threadIdx.x; i < n; i += blockDim.x) blk[i] += base[i % E];
+  }
 }
 
 void launch_dispatch_scan(int NB, int E, int El, int send_layout, int64_t rows_cap, const ChunkMeta& m,
@@ -171,6 +214,7 @@ __global__ void __launch_bounds__(256) dispatch_index_kernel(
   int64_t b1 = min(b0 + kTokPerBlk, t1);
   int ncp = (int)(b1 - b0) * k;
   for (int e = threadIdx.x; e < E; e += blockDim.x) run[e] = blk_off[(int64_t)blockIdx.x * E + e];
+  for (int q = threadIdx.x; q < ncp; q += blockDim.x) spos[q] = __ldg(ids + b0 * k + q);  // ids, coalesced
   __syncthreads();
   int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (warp == 0) {
@@ -179,7 +223,7 @@ __global__ void __launch_bounds__(256) dispatch_index_kernel(
       int q = base + lane;
       int e = -1;
       if (q < ncp) {
-        e = __ldg(ids + b0 * k + q);
+        e = spos[q];
         if (e < 0 || e >= E) e = -1;
       }
       unsigned peers = __match_any_sync(0xffffffffu, e);
@@ -256,6 +300,83 @@ __global__ void __launch_bounds__(256) dispatch_gather_kernel(
   }
 }
 
+// Pass 3b': one warp per SOURCE token reads its row(s) once and writes them to the token's k
+// destination rows (dest_of from pass 3a).  Every token row crosses HBM once instead of once per
+// copy (the destination-order gather re-reads it k times: 6.2x x's bytes at DeepSeek-V3's k = 8),
+// so the kernel moves the algorithmic bytes, T_j*h read + T_j*k*h written per tensor.  Padding rows
+// of the expert-major layout are zeroed by zero_padding_kernel.
+template <typename T>
+__global__ void __launch_bounds__(256) dispatch_scatter_kernel(
+    const T* __restrict__ x, const T* __restrict__ dy, int64_t t0, int64_t t1, int k, int h,
+    const int* __restrict__ dest_of, const int* __restrict__ info, T* __restrict__ xd, T* __restrict__ dyd,
+    const int* __restrict__ seg, const int* __restrict__ cnt, int El, int* __restrict__ src_of,
+    float* __restrict__ w_row, float* __restrict__ dw_row) {
+  if (info[kInfoSkip]) return;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t nwarps = (int64_t)gridDim.x * (blockDim.x >> 5);
+  constexpr int V = 16 / sizeof(T);
+  const int nv = h / V;
+  for (int64_t i = t0 + (int64_t)blockIdx.x * (blockDim.x >> 5) + warp; i < t1; i += nwarps) {
+    __shared__ int pos_s[8][16];
+    int* pos = pos_s[warp];
+    const int kk = k < 16 ? k : 16;
+    __syncwarp();
+    if (lane < 16) pos[lane] = lane < kk ? __ldg(dest_of + (i - t0) * k + lane) : -1;
+    __syncwarp();
+    const uint4* s1 = reinterpret_cast<const uint4*>(x + i * h);
+    const uint4* s2 = dy ? reinterpret_cast<const uint4*>(dy + i * h) : nullptr;
+    int c = lane;
+    for (; c + 96 < nv; c += 128) {
+      uint4 a0 = __ldg(s1 + c), a1 = __ldg(s1 + c + 32), a2 = __ldg(s1 + c + 64), a3 = __ldg(s1 + c + 96);
+      uint4 b0, b1, b2, b3;
+      if (s2) { b0 = __ldg(s2 + c); b1 = __ldg(s2 + c + 32); b2 = __ldg(s2 + c + 64); b3 = __ldg(s2 + c + 96); }
+#pragma unroll
+      for (int s = 0; s < 16; s++) {
+        if (s >= kk) break;
+        if (pos[s] < 0) continue;
+        uint4* d = reinterpret_cast<uint4*>(xd + (int64_t)pos[s] * h) + c;
+        d[0] = a0; d[32] = a1; d[64] = a2; d[96] = a3;
+        if (s2) {
+          uint4* d2 = reinterpret_cast<uint4*>(dyd + (int64_t)pos[s] * h) + c;
+          d2[0] = b0; d2[32] = b1; d2[64] = b2; d2[96] = b3;
+        }
+      }
+    }
+    for (; c < nv; c += 32) {
+      uint4 a = __ldg(s1 + c), b;
+      if (s2) b = __ldg(s2 + c);
+#pragma unroll
+      for (int s = 0; s < 16; s++) {
+        if (s >= kk) break;
+        if (pos[s] < 0) continue;
+        reinterpret_cast<uint4*>(xd + (int64_t)pos[s] * h)[c] = a;
+        if (s2) reinterpret_cast<uint4*>(dyd + (int64_t)pos[s] * h)[c] = b;
+      }
+    }
+  }
+  if (!seg) return;
+  // expert-major layout: zero the padding rows [seg[e] + cnt[e], seg[e+1]) (<= 127 per expert),
+  // one warp per (expert, padding slot), so padded rows add exact zeros to the dW reductions
+  const int64_t gw = (int64_t)blockIdx.x * (blockDim.x >> 5) + warp;
+  for (int64_t q = gw; q < (int64_t)El * kRowAlign; q += nwarps) {
+    const int e = (int)(q / kRowAlign);
+    const int r = __ldg(seg + e) + __ldg(cnt + e) + (int)(q % kRowAlign);
+    if (r >= __ldg(seg + e + 1)) continue;
+    const uint4 z = make_uint4(0, 0, 0, 0);
+    uint4* a = reinterpret_cast<uint4*>(xd + (int64_t)r * h);
+    for (int i = lane; i < nv; i += 32) a[i] = z;
+    if (dyd) {
+      uint4* b = reinterpret_cast<uint4*>(dyd + (int64_t)r * h);
+      for (int i = lane; i < nv; i += 32) b[i] = z;
+    }
+    if (lane == 0) {
+      src_of[r] = -1;
+      w_row[r] = 0.0f;
+      if (dw_row) dw_row[r] = 0.0f;
+    }
+  }
+}
+
 // MXFP8 variant (N4): the same gather, also quantising each x row into E4M3 codes + E8M0 block
 // scales (common.cuh mx_sf_off layout) on the fly: lanes 4j..4j+3 hold one 32-element block, the
 // block amax takes two shuffles.  write_x = 0 (the forward): only the quantised row is written.
@@ -316,6 +437,11 @@ __global__ void __launch_bounds__(256) dispatch_gather_mx_kernel(
   }
 }
 
+template <typename T>
+__global__ void zero_padding_kernel(const int* __restrict__ seg, const int* __restrict__ recv_cnt, int h,
+                                    const int* __restrict__ info, T* __restrict__ xd, T* __restrict__ dyd,
+                                    int* __restrict__ src_of, float* __restrict__ w_row, float* __restrict__ dw_row);
+
 void launch_dispatch_index(const int32_t* ids, const float* w, int64_t t0, int64_t t1, int k, int E,
                            const ChunkMeta& m, int* row_src, float* w_row, cudaStream_t st) {
   int NB = (int)ceil_div64(t1 - t0, kTokPerBlk);
@@ -345,6 +471,14 @@ void launch_dispatch_scatter(const T* x, const T* dy, const int32_t* ids, const 
       return;
     }
   }
+  if (k <= 16) {
+    // token-order scatter (each source row read once) + padding rows zeroed per expert
+    int sblocks = (int)std::min<int64_t>(std::max<int64_t>(ceil_div64(t1 - t0, 8), expert_major ? El * 16 : 1), 148 * 16);
+    dispatch_scatter_kernel<T><<<sblocks, 256, 0, st>>>(
+        x, dy, t0, t1, k, h, m.dest_of, m.info, xd, dyd, expert_major ? m.seg : nullptr, m.recv_cnt, El, m.src_of,
+        m.w_row, dy ? m.dw_row : nullptr);
+    return;
+  }
   dispatch_gather_kernel<T><<<blocks, 256, 0, st>>>(x, dy, k, h, row_src, row_src, expert_major ? m.seg : nullptr,
                                                     m.recv_cnt, El, expert_major ? m.w_row : nullptr,
                                                     (expert_major && dy) ? m.dw_row : nullptr, m.info,
@@ -362,7 +496,7 @@ __global__ void zero_padding_kernel(const int* __restrict__ seg, const int* __re
   int r0 = seg[e] + recv_cnt[e], r1 = seg[e + 1];
   int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
   constexpr int V = 16 / sizeof(T);
-  for (int r = r0 + warp; r < r1; r += nw) {
+  for (int r = r0 + blockIdx.y * nw + warp; r < r1; r += nw * gridDim.y) {
     uint4 z = make_uint4(0, 0, 0, 0);
     uint4* a = reinterpret_cast<uint4*>(xd + (int64_t)r * h);
     for (int i = lane; i < h / V; i += 32) a[i] = z;
@@ -380,8 +514,8 @@ __global__ void zero_padding_kernel(const int* __restrict__ seg, const int* __re
 
 template <typename T>
 void launch_zero_padding(int El, int h, const ChunkMeta& m, T* xd, T* dyd, cudaStream_t st) {
-  zero_padding_kernel<T><<<El, 256, 0, st>>>(m.seg, m.recv_cnt, h, m.info, xd, dyd, m.src_of, m.w_row,
-                                              dyd ? m.dw_row : nullptr);
+  zero_padding_kernel<T><<<dim3(El, kRowAlign / 8), 256, 0, st>>>(m.seg, m.recv_cnt, h, m.info, xd, dyd, m.src_of,
+                                                                 m.w_row, dyd ? m.dw_row : nullptr);
 }
 
 // ------------------------------------------------------------------------------------------
@@ -418,38 +552,92 @@ __device__ __forceinline__ void store8<float>(float* p, const float v[8]) {
   reinterpret_cast<float4*>(p)[1] = make_float4(v[4], v[5], v[6], v[7]);
 }
 
+// Raw 8-element vectors: all k rows of a column chunk are loaded before any FMA, so a lane keeps
+// k (x NC column chunks) independent 16-byte loads in flight - the loop over slots would otherwise
+// issue one load, wait for it at the FMA, then issue the next.
+template <typename T> struct Raw8;
+template <> struct Raw8<__nv_bfloat16> {
+  uint4 u;
+  __device__ __forceinline__ void load(const __nv_bfloat16* p) { u = __ldg(reinterpret_cast<const uint4*>(p)); }
+  __device__ __forceinline__ void zero() { u = make_uint4(0, 0, 0, 0); }
+  __device__ __forceinline__ void to_float(float v[8]) const {
+    const __nv_bfloat162* b = reinterpret_cast<const __nv_bfloat162*>(&u);
+#pragma unroll
+    for (int i = 0; i < 4; i++) { float2 f = __bfloat1622float2(b[i]); v[2 * i] = f.x; v[2 * i + 1] = f.y; }
+  }
+};
+template <> struct Raw8<float> {
+  float4 a, b;
+  __device__ __forceinline__ void load(const float* p) {
+    a = __ldg(reinterpret_cast<const float4*>(p)); b = __ldg(reinterpret_cast<const float4*>(p) + 1);
+  }
+  __device__ __forceinline__ void zero() { a = b = make_float4(0, 0, 0, 0); }
+  __device__ __forceinline__ void to_float(float v[8]) const {
+    v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w; v[4] = b.x; v[5] = b.y; v[6] = b.z; v[7] = b.w;
+  }
+};
+
+// One warp per token; per iteration NC column chunks of 8 elements per lane.  Slots are
+// accumulated in ascending order from 0 (fma(w_s, v, acc)), exactly as before the loads were
+// hoisted, so results are bit-identical; slots with pos < 0 (invalid ids) contribute nothing.
 template <typename T, bool WEIGHTED>
-__global__ void __launch_bounds__(256) gather_reduce_kernel(
+__global__ void __launch_bounds__(256, 2) gather_reduce_kernel(
     const T* __restrict__ rows, const float* __restrict__ w, int64_t t0, int64_t t1, int k, int h,
     const int* __restrict__ dest_of, const int* __restrict__ info, T* __restrict__ out,
     const float* __restrict__ dw_row, float* __restrict__ dscore) {
   if (info[kInfoSkip]) return;
+  constexpr int SG = 8;                       // slots loaded per group
+  constexpr int NC = sizeof(T) == 2 ? 2 : 1;  // column chunks per iteration
   int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   int64_t i = t0 + (int64_t)blockIdx.x * (blockDim.x >> 5) + warp;
   if (i >= t1) return;
-  int pos[16];
-  float ws[16];
-  int kk = k < 16 ? k : 16;
-  for (int s = 0; s < kk; s++) {
-    pos[s] = dest_of[(i - t0) * k + s];
-    ws[s] = WEIGHTED ? __ldg(w + i * k + s) : 1.0f;
+  __shared__ int pos_s[8][16];   // per warp: destination row and score of each slot
+  __shared__ float ws_s[8][16];
+  int* pos = pos_s[warp];
+  float* ws = ws_s[warp];
+  const int kk = k < 16 ? k : 16;
+  if (lane < 16) {
+    pos[lane] = lane < kk ? dest_of[(i - t0) * k + lane] : -1;
+    ws[lane] = (WEIGHTED && lane < kk) ? __ldg(w + i * k + lane) : 1.0f;
   }
+  __syncwarp();
   if (dscore && lane < k) {
     int p = dest_of[(i - t0) * k + lane];
     dscore[i * k + lane] = p >= 0 ? dw_row[p] : 0.0f;
   }
-  // 4 column chunks per iteration: 4*k independent 16-byte loads in flight per lane
-#pragma unroll 4
-  for (int c = lane * 8; c < h; c += 256) {
-    float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-    for (int s = 0; s < kk; s++) {
-      if (pos[s] < 0) continue;
-      float v[8];
-      load8<T>(rows + (int64_t)pos[s] * h + c, v);
+  for (int c0 = lane * 8; c0 < h; c0 += 256 * NC) {
+    float acc[NC][8];
 #pragma unroll
-      for (int u = 0; u < 8; u++) acc[u] = fmaf(ws[s], v[u], acc[u]);
+    for (int q = 0; q < NC; q++)
+#pragma unroll
+      for (int u = 0; u < 8; u++) acc[q][u] = 0.f;
+#pragma unroll
+    for (int g0 = 0; g0 < 16; g0 += SG) {
+      if (g0 >= kk) break;
+      Raw8<T> raw[SG][NC];
+#pragma unroll
+      for (int s = 0; s < SG; s++)
+#pragma unroll
+        for (int q = 0; q < NC; q++) {
+          const int c = c0 + q * 256;
+          if (g0 + s < kk && pos[g0 + s] >= 0 && c < h) raw[s][q].load(rows + (int64_t)pos[g0 + s] * h + c);
+          else raw[s][q].zero();
+        }
+#pragma unroll
+      for (int s = 0; s < SG; s++) {
+        if (g0 + s >= kk || pos[g0 + s] < 0) continue;
+#pragma unroll
+        for (int q = 0; q < NC; q++) {
+          float v[8];
+          raw[s][q].to_float(v);
+#pragma unroll
+          for (int u = 0; u < 8; u++) acc[q][u] = fmaf(ws[g0 + s], v[u], acc[q][u]);
+        }
+      }
     }
-    store8<T>(out + i * h + c, acc);
+#pragma unroll
+    for (int q = 0; q < NC; q++)
+      if (c0 + q * 256 < h) store8<T>(out + i * h + c0 + q * 256, acc[q]);
   }
 }
 
