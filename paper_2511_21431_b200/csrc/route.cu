@@ -437,6 +437,101 @@ __global__ void __launch_bounds__(256) dispatch_gather_mx_kernel(
   }
 }
 
+// The MX gather as a token-order scatter: one warp per source token quantises its x row ONCE
+// (codes are per row along h, so every copy of a token has the same codes and scales) and writes
+// the codes, scale bytes (tcgen05 chunk layout at each destination row) and, when asked, the bf16
+// x / dY rows to the token's k destinations.  Padding rows: zero codes, scale code 127 (E = 0),
+// zero bf16 rows.
+__device__ __forceinline__ void mx_quant8(const uint4& a, uint2& o, int& E) {
+  const uint32_t wv[4] = {a.x, a.y, a.z, a.w};
+  float v[8];
+  float amax = 0.f;
+#pragma unroll
+  for (int j = 0; j < 4; j++) {
+    v[2 * j] = __uint_as_float(wv[j] << 16);
+    v[2 * j + 1] = __uint_as_float(wv[j] & 0xFFFF0000u);
+    amax = fmaxf(amax, fmaxf(fabsf(v[2 * j]), fabsf(v[2 * j + 1])));
+  }
+  amax = fmaxf(amax, __shfl_xor_sync(0xffffffffu, amax, 1));
+  amax = fmaxf(amax, __shfl_xor_sync(0xffffffffu, amax, 2));
+  E = mx_exp(amax);
+  const float inv = mx_inv_scale(E);
+  o.x = mx_e4m3x2(v[0] * inv, v[1] * inv) | (mx_e4m3x2(v[2] * inv, v[3] * inv) << 16);
+  o.y = mx_e4m3x2(v[4] * inv, v[5] * inv) | (mx_e4m3x2(v[6] * inv, v[7] * inv) << 16);
+}
+
+__global__ void __launch_bounds__(256) dispatch_scatter_mx_kernel(
+    const __nv_bfloat16* __restrict__ x, const __nv_bfloat16* __restrict__ dy, int64_t t0, int64_t t1, int k, int h,
+    const int* __restrict__ dest_of, const int* __restrict__ seg, const int* __restrict__ cnt, int El,
+    int* __restrict__ src_of, float* __restrict__ w_row, float* __restrict__ dw_row, const int* __restrict__ info,
+    int write_x, __nv_bfloat16* __restrict__ xd, __nv_bfloat16* __restrict__ dyd, uint8_t* __restrict__ xq,
+    uint8_t* __restrict__ xsf) {
+  if (info[kInfoSkip]) return;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t nwarps = (int64_t)gridDim.x * (blockDim.x >> 5);
+  const int nv = h / 8;   // uint4 per row (h % 32 == 0: blocks never straddle a quad of lanes)
+  __shared__ int pos_s[8][16];
+  int* pos = pos_s[warp];
+  const int kk = k < 16 ? k : 16;
+  for (int64_t t = t0 + (int64_t)blockIdx.x * (blockDim.x >> 5) + warp; t < t1; t += nwarps) {
+    __syncwarp();
+    if (lane < 16) pos[lane] = lane < kk ? __ldg(dest_of + (t - t0) * k + lane) : -1;
+    __syncwarp();
+    const uint4* s = reinterpret_cast<const uint4*>(x + t * h);
+    const uint4* s2 = dy ? reinterpret_cast<const uint4*>(dy + t * h) : nullptr;
+    for (int base = 0; base < nv; base += 64) {
+      const int i0 = base + lane, i1 = base + 32 + lane;
+      const bool ok0 = i0 < nv, ok1 = i1 < nv;   // whole quads (nv % 4 == 0)
+      uint4 a0 = make_uint4(0, 0, 0, 0), a1 = a0, b0 = a0, b1 = a0;
+      if (ok0) a0 = __ldg(s + i0);
+      if (ok1) a1 = __ldg(s + i1);
+      if (s2 && ok0) b0 = __ldg(s2 + i0);
+      if (s2 && ok1) b1 = __ldg(s2 + i1);
+      uint2 o0, o1;
+      int E0, E1;
+      mx_quant8(a0, o0, E0);
+      mx_quant8(a1, o1, E1);
+#pragma unroll
+      for (int q = 0; q < 16; q++) {
+        if (q >= kk) break;
+        const int64_t r = pos[q];
+        if (r < 0) continue;
+        if (ok0) {
+          *reinterpret_cast<uint2*>(xq + r * h + (int64_t)i0 * 8) = o0;
+          if ((i0 & 3) == 0) xsf[mx_sf_off(r, i0 >> 2, h)] = (uint8_t)(E0 + 127);
+          if (write_x) reinterpret_cast<uint4*>(xd + r * h)[i0] = a0;
+          if (s2) reinterpret_cast<uint4*>(dyd + r * h)[i0] = b0;
+        }
+        if (ok1) {
+          *reinterpret_cast<uint2*>(xq + r * h + (int64_t)i1 * 8) = o1;
+          if ((i1 & 3) == 0) xsf[mx_sf_off(r, i1 >> 2, h)] = (uint8_t)(E1 + 127);
+          if (write_x) reinterpret_cast<uint4*>(xd + r * h)[i1] = a1;
+          if (s2) reinterpret_cast<uint4*>(dyd + r * h)[i1] = b1;
+        }
+      }
+    }
+  }
+  // padding rows of each local expert segment
+  const int64_t gw = (int64_t)blockIdx.x * (blockDim.x >> 5) + warp;
+  for (int64_t q = gw; q < (int64_t)El * kRowAlign; q += nwarps) {
+    const int e = (int)(q / kRowAlign);
+    const int64_t r = __ldg(seg + e) + __ldg(cnt + e) + (int)(q % kRowAlign);
+    if (r >= __ldg(seg + e + 1)) continue;
+    const uint4 z = make_uint4(0, 0, 0, 0);
+    for (int i = lane; i < nv; i += 32) {
+      *reinterpret_cast<uint2*>(xq + r * h + (int64_t)i * 8) = make_uint2(0, 0);
+      if ((i & 3) == 0) xsf[mx_sf_off(r, i >> 2, h)] = (uint8_t)127;
+      if (write_x) reinterpret_cast<uint4*>(xd + r * h)[i] = z;
+      if (dy) reinterpret_cast<uint4*>(dyd + r * h)[i] = z;
+    }
+    if (lane == 0) {
+      src_of[r] = -1;
+      w_row[r] = 0.0f;
+      if (dw_row) dw_row[r] = 0.0f;
+    }
+  }
+}
+
 template <typename T>
 __global__ void zero_padding_kernel(const int* __restrict__ seg, const int* __restrict__ recv_cnt, int h,
                                     const int* __restrict__ info, T* __restrict__ xd, T* __restrict__ dyd,
@@ -464,6 +559,13 @@ void launch_dispatch_scatter(const T* x, const T* dy, const int32_t* ids, const 
   int64_t rows_ub = expert_major ? rows_cap : (t1 - t0) * k;
   int blocks = (int)std::min<int64_t>(ceil_div64(std::max<int64_t>(rows_ub, 1), 8), 148 * 16);
   if constexpr (std::is_same<T, __nv_bfloat16>::value) {
+    if (xq && expert_major && k <= 16) {
+      int sblocks = (int)std::min<int64_t>(std::max<int64_t>(ceil_div64(t1 - t0, 8), El * 16), 148 * 16);
+      dispatch_scatter_mx_kernel<<<sblocks, 256, 0, st>>>(x, dy, t0, t1, k, h, m.dest_of, m.seg, m.recv_cnt, El,
+                                                           m.src_of, m.w_row, dy ? m.dw_row : nullptr, m.info,
+                                                           write_x ? 1 : 0, xd, dyd, xq, xsf);
+      return;
+    }
     if (xq && expert_major) {
       dispatch_gather_mx_kernel<<<blocks, 256, 0, st>>>(x, dy, k, h, row_src, m.seg, m.recv_cnt, El, m.w_row,
                                                          dy ? m.dw_row : nullptr, m.info, write_x ? 1 : 0, xd, dyd,
