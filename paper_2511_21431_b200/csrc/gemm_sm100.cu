@@ -382,6 +382,7 @@ struct Params {
   int beta;          // WGRAD: 1 = dW += acc (accumulate), 0 = dW = acc (first chunk, overwrite)
   const uint64_t* row_addr;  // DOWN / DX fused EP combine: per-row peer destination (0 = padding)
   int group_m;       // M tiles per raster group (host-sized so a wave's operands stay in L2)
+  int* wave_ctr;     // wave pacing: tiles started by all units, zeroed per launch (null = off)
   // MXFP8 (MX kernels): scale chunks of A and B, GATEUP forward's quantised a
   const uint8_t* mx_a_sf;
   const uint8_t* mx_b0_sf;
@@ -607,7 +608,22 @@ __global__ void __launch_bounds__(THREADS, 1)
     if (lane == 0) {
       int stage = 0;
       uint32_t phase = 0;
-      for (int t = cid; t < ntiles; t += ncid) {
+      int li = 0;   // local tile index of this unit
+      for (int t = cid; t < ntiles; t += ncid, li++) {
+        if (p.wave_ctr && leader && li > 0) {
+          // Wave pacing: a unit starts its tile li only once every unit has started tile li - 1, so
+          // the units of one wave (which share A strips along n and B strips along m) stay within a
+          // tile of each other and their operand loads meet in L2 instead of each missing to DRAM.
+          // Spin bounded (~100 us): pacing is a hint, a unit that is not resident cannot deadlock.
+          const int target = ncid * li;
+          for (int spin = 0; spin < 1000; spin++) {
+            int v;
+            asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p.wave_ctr) : "memory");
+            if (v >= target) break;
+            __nanosleep(64);
+          }
+        }
+        if (p.wave_ctr && leader) atomicAdd(p.wave_ctr, 1);
         Tile T = tile_of<KIND, PAIR, MX>(p, t);
         const int am0 = T.m0 + (int)rank * BM;              // this CTA's A rows
         for (int kb = 0; kb < T.nkb; kb++) {
@@ -658,18 +674,19 @@ __global__ void __launch_bounds__(THREADS, 1)
           }
           if (leader) mbar_expect_tx(full + stage, (PAIR ? 2 : 1) * STAGE_BYTES);
           int kc = T.k0 + kb * BK;
-          auto L2 = [&](void* dst, const CUtensorMap* m, int c0, int c1) {
+          auto LA = [&](void* dst, const CUtensorMap* m, int c0, int c1) {
             if (PAIR) tma_2d_pair(dst, m, full + stage, c0, c1); else tma_2d(dst, m, full + stage, c0, c1);
           };
+          auto L2 = LA;
           auto L3 = [&](void* dst, const CUtensorMap* m, int c0, int c1, int c2) {
             if (PAIR) tma_3d_pair(dst, m, full + stage, c0, c1, c2); else tma_3d(dst, m, full + stage, c0, c1, c2);
           };
           if (CF::A_MN) {
             // A(m,k) = rows[kc + k][am0 + m]: two 64-wide MN atoms of 64 K rows
-            L2(sa, &tmA, am0, kc);
-            L2(sa + 8192, &tmA, am0 + 64, kc);
+            LA(sa, &tmA, am0, kc);
+            LA(sa + 8192, &tmA, am0 + 64, kc);
           } else {
-            L2(sa, &tmA, kc, am0);
+            LA(sa, &tmA, kc, am0);
           }
           // B: this CTA's share of the N columns
           const int bn0 = T.n0 + (PAIR ? (int)rank * B_ROWS : 0);
@@ -1282,6 +1299,22 @@ int launch(const GemmProblem<__nv_bfloat16>& gp, cudaStream_t st) {
     } else {
       double gm = std::sqrt((double)units_hw * (double)b_strip / (double)a_strip);
       p.group_m = (int)std::max<double>(1.0, std::min<double>(64.0, std::floor(gm + 0.5)));
+    }
+  }
+  {
+    // Wave pacing (opt-in, MEMFINE_WAVE_SYNC=1): -2..-15 % DRAM traffic, +0..3 % step
+    // on the boxes measured.  Off by default: with SMs lent to a concurrent comm kernel (overlap, the
+    // in-process EP group) some units are not resident and the others would sit out the spin bound.
+    static const int env_wave = [] {
+      const char* s = getenv("MEMFINE_WAVE_SYNC");
+      return s ? atoi(s) : 0;
+    }();
+    static int* ctr_ring = nullptr;
+    static int ctr_next = 0;
+    if (env_wave) {
+      if (!ctr_ring && cudaMalloc(&ctr_ring, 4096 * sizeof(int)) != cudaSuccess) return -1;
+      p.wave_ctr = ctr_ring + (ctr_next++ & 4095);
+      if (cudaMemsetAsync(p.wave_ctr, 0, sizeof(int), st) != cudaSuccess) return -1;
     }
   }
   int64_t max_tiles;
