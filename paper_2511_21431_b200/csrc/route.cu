@@ -248,63 +248,11 @@ __global__ void __launch_bounds__(256) dispatch_index_kernel(
   }
 }
 
-// Pass 3b: one warp per destination row copies the token row(s) with 16-byte vectors, 4 loads in
-// flight per lane.  With `seg` (EP=1 expert-major layout) rows past a local expert's count are
-// padding: zero-filled, row_src = -1, scores 0.  Row count from info (device-side).
-template <typename T>
-__global__ void __launch_bounds__(256) dispatch_gather_kernel(
-    const T* __restrict__ x, const T* __restrict__ dy, int k, int h, const int* __restrict__ row_src_in,
-    int* __restrict__ row_src, const int* __restrict__ seg, const int* __restrict__ cnt, int El,
-    float* __restrict__ w_row, float* __restrict__ dw_row, const int* __restrict__ info, int rows_word,
-    T* __restrict__ xd, T* __restrict__ dyd) {
-  if (info[kInfoSkip]) return;
-  const int rows = info[rows_word];
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int nwarps = gridDim.x * (blockDim.x >> 5);
-  constexpr int V = 16 / sizeof(T);
-  const int nv = h / V;
-  for (int r = blockIdx.x * (blockDim.x >> 5) + warp; r < rows; r += nwarps) {
-    bool pad = false;
-    if (seg) {
-      int e = expert_of_row(seg, El, r);
-      pad = r >= __ldg(seg + e) + __ldg(cnt + e);
-    }
-    uint4* d = reinterpret_cast<uint4*>(xd + (int64_t)r * h);
-    uint4* d2 = dy ? reinterpret_cast<uint4*>(dyd + (int64_t)r * h) : nullptr;
-    if (pad) {
-      uint4 z = make_uint4(0, 0, 0, 0);
-      for (int i = lane; i < nv; i += 32) { d[i] = z; if (d2) d2[i] = z; }
-      if (lane == 0) {
-        row_src[r] = -1;
-        if (w_row) w_row[r] = 0.f;
-        if (dw_row) dw_row[r] = 0.f;
-      }
-      continue;
-    }
-    const int64_t tok = __ldg(row_src_in + r) / k;
-    const uint4* s = reinterpret_cast<const uint4*>(x + tok * h);
-    const uint4* s2 = dy ? reinterpret_cast<const uint4*>(dy + tok * h) : nullptr;
-    int i = lane;
-    for (; i + 96 < nv; i += 128) {
-      uint4 a0 = __ldg(s + i), a1 = __ldg(s + i + 32), a2 = __ldg(s + i + 64), a3 = __ldg(s + i + 96);
-      if (s2) {
-        uint4 b0 = __ldg(s2 + i), b1 = __ldg(s2 + i + 32), b2 = __ldg(s2 + i + 64), b3 = __ldg(s2 + i + 96);
-        d2[i] = b0; d2[i + 32] = b1; d2[i + 64] = b2; d2[i + 96] = b3;
-      }
-      d[i] = a0; d[i + 32] = a1; d[i + 64] = a2; d[i + 96] = a3;
-    }
-    for (; i < nv; i += 32) {
-      d[i] = __ldg(s + i);
-      if (s2) d2[i] = __ldg(s2 + i);
-    }
-  }
-}
-
 // Pass 3b': one warp per SOURCE token reads its row(s) once and writes them to the token's k
 // destination rows (dest_of from pass 3a).  Every token row crosses HBM once instead of once per
 // copy (the destination-order gather re-reads it k times: 6.2x x's bytes at DeepSeek-V3's k = 8),
-// so the kernel moves the algorithmic bytes, T_j*h read + T_j*k*h written per tensor.  Padding rows
-// of the expert-major layout are zeroed by zero_padding_kernel.
+// so the kernel moves the algorithmic bytes, T_j*h read + T_j*k*h written per tensor.  With `seg`
+// (the expert-major layout) the same launch then zeroes the padding rows.
 template <typename T>
 __global__ void __launch_bounds__(256) dispatch_scatter_kernel(
     const T* __restrict__ x, const T* __restrict__ dy, int64_t t0, int64_t t1, int k, int h,
@@ -373,66 +321,6 @@ __global__ void __launch_bounds__(256) dispatch_scatter_kernel(
       src_of[r] = -1;
       w_row[r] = 0.0f;
       if (dw_row) dw_row[r] = 0.0f;
-    }
-  }
-}
-
-// MXFP8 variant (N4): the same gather, also quantising each x row into E4M3 codes + E8M0 block
-// scales (common.cuh mx_sf_off layout) on the fly: lanes 4j..4j+3 hold one 32-element block, the
-// block amax takes two shuffles.  write_x = 0 (the forward): only the quantised row is written.
-// Padding rows: zero codes, scale code 127 (E = 0), zero bf16 rows.
-__global__ void __launch_bounds__(256) dispatch_gather_mx_kernel(
-    const __nv_bfloat16* __restrict__ x, const __nv_bfloat16* __restrict__ dy, int k, int h,
-    int* __restrict__ row_src, const int* __restrict__ seg, const int* __restrict__ cnt, int El,
-    float* __restrict__ w_row, float* __restrict__ dw_row, const int* __restrict__ info, int write_x,
-    __nv_bfloat16* __restrict__ xd, __nv_bfloat16* __restrict__ dyd, uint8_t* __restrict__ xq,
-    uint8_t* __restrict__ xsf) {
-  if (info[kInfoSkip]) return;
-  const int rows = info[kInfoRowsPad];
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int nwarps = gridDim.x * (blockDim.x >> 5);
-  const int nv = h / 8;   // uint4 per row (h % 32 == 0: blocks never straddle a quad of lanes)
-  for (int r = blockIdx.x * (blockDim.x >> 5) + warp; r < rows; r += nwarps) {
-    const int e = expert_of_row(seg, El, r);
-    const bool pad = r >= __ldg(seg + e) + __ldg(cnt + e);
-    int64_t tok = 0;
-    if (!pad) tok = row_src[r] / k;
-    else if (lane == 0) {
-      row_src[r] = -1;
-      w_row[r] = 0.f;
-      if (dw_row) dw_row[r] = 0.f;
-    }
-    const uint4* s = reinterpret_cast<const uint4*>(x + tok * h);
-    const uint4* s2 = dy ? reinterpret_cast<const uint4*>(dy + tok * h) : nullptr;
-    uint4* d = reinterpret_cast<uint4*>(xd + (int64_t)r * h);
-    uint4* d2 = dy ? reinterpret_cast<uint4*>(dyd + (int64_t)r * h) : nullptr;
-    for (int base = 0; base < nv; base += 32) {
-      const int i = base + lane;
-      const bool ok = i < nv;   // whole quads (nv % 4 == 0)
-      uint4 a = make_uint4(0, 0, 0, 0);
-      if (ok && !pad) a = __ldg(s + i);
-      if (ok && write_x) d[i] = a;
-      if (ok && dy) d2[i] = pad ? make_uint4(0, 0, 0, 0) : __ldg(s2 + i);
-      const uint32_t wv[4] = {a.x, a.y, a.z, a.w};
-      float v[8];
-      float amax = 0.f;
-#pragma unroll
-      for (int j = 0; j < 4; j++) {
-        v[2 * j] = __uint_as_float(wv[j] << 16);
-        v[2 * j + 1] = __uint_as_float(wv[j] & 0xFFFF0000u);
-        amax = fmaxf(amax, fmaxf(fabsf(v[2 * j]), fabsf(v[2 * j + 1])));
-      }
-      amax = fmaxf(amax, __shfl_xor_sync(0xffffffffu, amax, 1));
-      amax = fmaxf(amax, __shfl_xor_sync(0xffffffffu, amax, 2));
-      const int E = mx_exp(amax);
-      const float inv = mx_inv_scale(E);
-      uint2 o;
-      o.x = mx_e4m3x2(v[0] * inv, v[1] * inv) | (mx_e4m3x2(v[2] * inv, v[3] * inv) << 16);
-      o.y = mx_e4m3x2(v[4] * inv, v[5] * inv) | (mx_e4m3x2(v[6] * inv, v[7] * inv) << 16);
-      if (ok) {
-        *reinterpret_cast<uint2*>(xq + (int64_t)r * h + (int64_t)i * 8) = o;
-        if ((i & 3) == 0) xsf[mx_sf_off(r, i >> 2, h)] = (uint8_t)(E + 127);
-      }
     }
   }
 }
@@ -532,11 +420,6 @@ __global__ void __launch_bounds__(256) dispatch_scatter_mx_kernel(
   }
 }
 
-template <typename T>
-__global__ void zero_padding_kernel(const int* __restrict__ seg, const int* __restrict__ recv_cnt, int h,
-                                    const int* __restrict__ info, T* __restrict__ xd, T* __restrict__ dyd,
-                                    int* __restrict__ src_of, float* __restrict__ w_row, float* __restrict__ dw_row);
-
 void launch_dispatch_index(const int32_t* ids, const float* w, int64_t t0, int64_t t1, int k, int E,
                            const ChunkMeta& m, int* row_src, float* w_row, cudaStream_t st) {
   int NB = (int)ceil_div64(t1 - t0, kTokPerBlk);
@@ -550,41 +433,28 @@ template <typename T>
 void launch_dispatch_scatter(const T* x, const T* dy, const int32_t* ids, const float* w, int64_t t0, int64_t t1,
                              int k, int E, int h, const ChunkMeta& m, T* xd, T* dyd, int El, bool expert_major,
                              int64_t rows_cap, cudaStream_t st, uint8_t* xq, uint8_t* xsf, bool write_x) {
+  (void)rows_cap;
   int NB = (int)ceil_div64(t1 - t0, kTokPerBlk);
   if (NB == 0) return;
   size_t smem = sizeof(int) * ((size_t)E + (size_t)kTokPerBlk * k);
   int* row_src = expert_major ? m.src_of : m.send_src;
   dispatch_index_kernel<<<NB, 256, smem, st>>>(ids, w, t0, t1, k, E, m.blk_cnt, m.dest_of, row_src, m.w_row,
                                                dy ? m.dw_row : nullptr, m.info);
-  int64_t rows_ub = expert_major ? rows_cap : (t1 - t0) * k;
-  int blocks = (int)std::min<int64_t>(ceil_div64(std::max<int64_t>(rows_ub, 1), 8), 148 * 16);
+  // token-order scatter (each source row read once; k <= 16, memfine_create checks) + the padding
+  // rows of the expert-major layout zeroed in the same launch
+  const int blocks = (int)std::min<int64_t>(std::max<int64_t>(ceil_div64(t1 - t0, 8), expert_major ? El * 16 : 1),
+                                            148 * 16);
   if constexpr (std::is_same<T, __nv_bfloat16>::value) {
-    if (xq && expert_major && k <= 16) {
-      int sblocks = (int)std::min<int64_t>(std::max<int64_t>(ceil_div64(t1 - t0, 8), El * 16), 148 * 16);
-      dispatch_scatter_mx_kernel<<<sblocks, 256, 0, st>>>(x, dy, t0, t1, k, h, m.dest_of, m.seg, m.recv_cnt, El,
-                                                           m.src_of, m.w_row, dy ? m.dw_row : nullptr, m.info,
-                                                           write_x ? 1 : 0, xd, dyd, xq, xsf);
-      return;
-    }
     if (xq && expert_major) {
-      dispatch_gather_mx_kernel<<<blocks, 256, 0, st>>>(x, dy, k, h, row_src, m.seg, m.recv_cnt, El, m.w_row,
-                                                         dy ? m.dw_row : nullptr, m.info, write_x ? 1 : 0, xd, dyd,
-                                                         xq, xsf);
+      dispatch_scatter_mx_kernel<<<blocks, 256, 0, st>>>(x, dy, t0, t1, k, h, m.dest_of, m.seg, m.recv_cnt, El,
+                                                          m.src_of, m.w_row, dy ? m.dw_row : nullptr, m.info,
+                                                          write_x ? 1 : 0, xd, dyd, xq, xsf);
       return;
     }
   }
-  if (k <= 16) {
-    // token-order scatter (each source row read once) + padding rows zeroed per expert
-    int sblocks = (int)std::min<int64_t>(std::max<int64_t>(ceil_div64(t1 - t0, 8), expert_major ? El * 16 : 1), 148 * 16);
-    dispatch_scatter_kernel<T><<<sblocks, 256, 0, st>>>(
-        x, dy, t0, t1, k, h, m.dest_of, m.info, xd, dyd, expert_major ? m.seg : nullptr, m.recv_cnt, El, m.src_of,
-        m.w_row, dy ? m.dw_row : nullptr);
-    return;
-  }
-  dispatch_gather_kernel<T><<<blocks, 256, 0, st>>>(x, dy, k, h, row_src, row_src, expert_major ? m.seg : nullptr,
-                                                    m.recv_cnt, El, expert_major ? m.w_row : nullptr,
-                                                    (expert_major && dy) ? m.dw_row : nullptr, m.info,
-                                                    expert_major ? kInfoRowsPad : kInfoSend, xd, dyd);
+  dispatch_scatter_kernel<T><<<blocks, 256, 0, st>>>(x, dy, t0, t1, k, h, m.dest_of, m.info, xd, dyd,
+                                                     expert_major ? m.seg : nullptr, m.recv_cnt, El, m.src_of,
+                                                     m.w_row, dy ? m.dw_row : nullptr);
 }
 
 // Zero the padding rows of each local expert segment (so padded rows contribute exact
