@@ -608,17 +608,19 @@ __global__ void __launch_bounds__(THREADS, 1)
     if (lane == 0) {
       int stage = 0;
       uint32_t phase = 0;
-      int li = 0;   // local tile index of this unit
+      int li = 0;    // local tile index of this unit
+      int seen = 0;  // pacing counter as loaded mid-way through the previous tile
       for (int t = cid; t < ntiles; t += ncid, li++) {
-        if (p.wave_ctr && leader && li > 0) {
+        if (p.wave_ctr && leader && li > 0 && seen < ncid * li) {
           // Wave pacing: a unit starts its tile li only once every unit has started tile li - 1, so
           // the units of one wave (which share A strips along n and B strips along m) stay within a
           // tile of each other and their operand loads meet in L2 instead of each missing to DRAM.
-          // Spin bounded (~100 us): pacing is a hint, a unit that is not resident cannot deadlock.
+          // The counter was loaded half a tile ago, so a unit that is not behind never waits on the
+          // load.  Spin bounded (~1 ms): pacing is a hint, a non-resident unit cannot deadlock.
           const int target = ncid * li;
           for (int spin = 0; spin < 1000; spin++) {
             int v;
-            asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p.wave_ctr) : "memory");
+            asm volatile("ld.relaxed.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p.wave_ctr) : "memory");
             if (v >= target) break;
             __nanosleep(64);
           }
@@ -627,6 +629,8 @@ __global__ void __launch_bounds__(THREADS, 1)
         Tile T = tile_of<KIND, PAIR, MX>(p, t);
         const int am0 = T.m0 + (int)rank * BM;              // this CTA's A rows
         for (int kb = 0; kb < T.nkb; kb++) {
+          if (p.wave_ctr && leader && kb == (T.nkb >> 1))
+            asm volatile("ld.relaxed.gpu.global.b32 %0, [%1];" : "=r"(seen) : "l"(p.wave_ctr) : "memory");
           mbar_wait(empty + stage, phase ^ 1);
           uint8_t* sa = smem + stage * STAGE_BYTES;
           uint8_t* sb = sa + A_BYTES;
@@ -1302,16 +1306,16 @@ int launch(const GemmProblem<__nv_bfloat16>& gp, cudaStream_t st) {
     }
   }
   {
-    // Wave pacing (opt-in, MEMFINE_WAVE_SYNC=1): -2..-15 % DRAM traffic, +0..3 % step
-    // on the boxes measured.  Off by default: with SMs lent to a concurrent comm kernel (overlap, the
-    // in-process EP group) some units are not resident and the others would sit out the spin bound.
+    // Wave pacing (profiles/r01_gemm_dram_pacing.md: -2..-15 % DRAM traffic, +0..3 % step).  On where
+    // the caller guarantees no concurrent kernel holds SMs (gp.pace: EP = 1, one stream) - elsewhere a
+    // non-resident unit would make the others sit out the spin bound.  MEMFINE_WAVE_SYNC=0/1 forces it.
     static const int env_wave = [] {
       const char* s = getenv("MEMFINE_WAVE_SYNC");
-      return s ? atoi(s) : 0;
+      return s ? atoi(s) : -1;
     }();
     static int* ctr_ring = nullptr;
     static int ctr_next = 0;
-    if (env_wave) {
+    if (env_wave == 1 || (env_wave < 0 && gp.pace && gp.sm_limit <= 0)) {
       if (!ctr_ring && cudaMalloc(&ctr_ring, 4096 * sizeof(int)) != cudaSuccess) return -1;
       p.wave_ctr = ctr_ring + (ctr_next++ & 4095);
       if (cudaMemsetAsync(p.wave_ctr, 0, sizeof(int), st) != cudaSuccess) return -1;

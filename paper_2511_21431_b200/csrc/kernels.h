@@ -155,6 +155,7 @@ struct GemmProblem {
   uint8_t* mx_gq;            // DACT (BF16) in the MX variant: dG||dU also quantised ([R][2g]) ...
   uint8_t* mx_gq_sf;         // ... with scales (non-null = on)
   int sm_limit;              // > 0: launch on at most this many SMs (MEMFINE_FLAG_OVERLAP comm reserve)
+  int pace;                  // 1: no other kernel shares the SMs (EP = 1, one stream): wave pacing is safe
 };
 
 // CUDA-core FFMA path (MEMFINE_FP32 mode; K12 of SURVEY §2.4).

@@ -397,6 +397,9 @@ GemmProblem<T> base_problem(const memfine_handle_s* h, const Layout& L, const vo
   p.Wd = (const T*)wd;
   p.w_row = L.m.w_row;
   p.dw_row = L.m.dw_row;
+  // wave pacing of the persistent GEMM units needs every unit resident: not when GEMMs of other
+  // ranks (in-process group) or comm kernels (EP path) may hold SMs concurrently
+  p.pace = (h->d.ep_size == 1 && !(h->d.flags & MEMFINE_FLAG_EP_PATH) && !h->lg) ? 1 : 0;
   return p;
 }
 
