@@ -382,7 +382,8 @@ struct Params {
   int beta;          // WGRAD: 1 = dW += acc (accumulate), 0 = dW = acc (first chunk, overwrite)
   const uint64_t* row_addr;  // DOWN / DX fused EP combine: per-row peer destination (0 = padding)
   int group_m;       // M tiles per raster group (host-sized so a wave's operands stay in L2)
-  int* wave_ctr;     // wave pacing: tiles started by all units, zeroed per launch (null = off)
+  int* wave_ctr;     // wave pacing: steps started by all units, zeroed per launch (null = off)
+  int pace_kb;       // k-blocks per pacing step of M-tiled kinds (<= 0: one step per tile)
   // MXFP8 (MX kernels): scale chunks of A and B, GATEUP forward's quantised a
   const uint8_t* mx_a_sf;
   const uint8_t* mx_b0_sf;
@@ -608,16 +609,19 @@ __global__ void __launch_bounds__(THREADS, 1)
     if (lane == 0) {
       int stage = 0;
       uint32_t phase = 0;
-      int li = 0;    // local tile index of this unit
-      int seen = 0;  // pacing counter as loaded mid-way through the previous tile
-      for (int t = cid; t < ntiles; t += ncid, li++) {
-        if (p.wave_ctr && leader && li > 0 && seen < ncid * li) {
-          // Wave pacing: a unit starts its tile li only once every unit has started tile li - 1, so
-          // the units of one wave (which share A strips along n and B strips along m) stay within a
-          // tile of each other and their operand loads meet in L2 instead of each missing to DRAM.
-          // The counter was loaded half a tile ago, so a unit that is not behind never waits on the
-          // load.  Spin bounded (~1 ms): pacing is a hint, a non-resident unit cannot deadlock.
-          const int target = ncid * li;
+      int step = 0;  // pacing steps this unit has started
+      int seen = 0;  // pacing counter as loaded half a step ago
+      // Wave pacing: a unit starts its pacing step s only once every unit has started step s - 1, so
+      // the units of one wave (which share A strips along n and B strips along m) stay within a step
+      // of each other and their operand loads meet in L2 instead of each missing to DRAM.  A step is
+      // a tile, or PACE_KB k-blocks of a long-K tile (every tile of an M-tiled launch has the same K,
+      // so the steps line up across units; weight-gradient tiles pace per tile).  The counter is
+      // loaded half a step ahead, so a unit that is not ahead never waits on the load.  Spin bounded
+      // (~1 ms): pacing is a hint, a non-resident unit cannot deadlock the others.
+      const int PACE_KB = (KIND >= GK_WGRAD_DOWN || p.pace_kb <= 0) ? (1 << 30) : p.pace_kb;
+      auto pace = [&]() {
+        if (step > 0 && seen < ncid * step) {
+          const int target = ncid * step;
           for (int spin = 0; spin < 1000; spin++) {
             int v;
             asm volatile("ld.relaxed.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p.wave_ctr) : "memory");
@@ -625,12 +629,25 @@ __global__ void __launch_bounds__(THREADS, 1)
             __nanosleep(64);
           }
         }
-        if (p.wave_ctr && leader) atomicAdd(p.wave_ctr, 1);
+        atomicAdd(p.wave_ctr, 1);
+        step++;
+      };
+      for (int t = cid; t < ntiles; t += ncid) {
         Tile T = tile_of<KIND, PAIR, MX>(p, t);
         const int am0 = T.m0 + (int)rank * BM;              // this CTA's A rows
-        for (int kb = 0; kb < T.nkb; kb++) {
-          if (p.wave_ctr && leader && kb == (T.nkb >> 1))
+        if (KIND >= GK_WGRAD_DOWN && p.wave_ctr && leader) {
+          // weight gradients: one step per tile, taken even by tiles without rows (nkb = 0)
+          pace();
+          if (T.nkb == 0)
             asm volatile("ld.relaxed.gpu.global.b32 %0, [%1];" : "=r"(seen) : "l"(p.wave_ctr) : "memory");
+        }
+        for (int kb = 0; kb < T.nkb; kb++) {
+          if (p.wave_ctr && leader) {
+            const int ks = kb % PACE_KB, slen = min(PACE_KB, T.nkb - (kb - ks));
+            if (ks == 0 && KIND < GK_WGRAD_DOWN) pace();
+            if (ks == (slen >> 1))
+              asm volatile("ld.relaxed.gpu.global.b32 %0, [%1];" : "=r"(seen) : "l"(p.wave_ctr) : "memory");
+          }
           mbar_wait(empty + stage, phase ^ 1);
           uint8_t* sa = smem + stage * STAGE_BYTES;
           uint8_t* sb = sa + A_BYTES;
@@ -1319,6 +1336,11 @@ int launch(const GemmProblem<__nv_bfloat16>& gp, cudaStream_t st) {
       if (!ctr_ring && cudaMalloc(&ctr_ring, 4096 * sizeof(int)) != cudaSuccess) return -1;
       p.wave_ctr = ctr_ring + (ctr_next++ & 4095);
       if (cudaMemsetAsync(p.wave_ctr, 0, sizeof(int), st) != cudaSuccess) return -1;
+      static const int env_kb = [] {
+        const char* s = getenv("MEMFINE_PACE_KB");
+        return s ? atoi(s) : 0;   // sub-tile steps measured worse (dX 7.3 -> 9.3 ms at 64)
+      }();
+      p.pace_kb = env_kb;
     }
   }
   int64_t max_tiles;
