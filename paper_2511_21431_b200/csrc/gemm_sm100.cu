@@ -17,6 +17,7 @@
 #include <cuda.h>
 #include <cudaTypedefs.h>
 #include <mutex>
+#include <atomic>
 #include <cstdlib>
 #include <algorithm>
 #include <cstring>
@@ -384,6 +385,7 @@ struct Params {
   int group_m;       // M tiles per raster group (host-sized so a wave's operands stay in L2)
   int* wave_ctr;     // wave pacing: steps started by all units, zeroed per launch (null = off)
   int pace_kb;       // k-blocks per pacing step of M-tiled kinds (<= 0: one step per tile)
+  int pace_slack;    // steps a unit may run ahead of the slowest unit (>= 1)
   // MXFP8 (MX kernels): scale chunks of A and B, GATEUP forward's quantised a
   const uint8_t* mx_a_sf;
   const uint8_t* mx_b0_sf;
@@ -620,8 +622,8 @@ __global__ void __launch_bounds__(THREADS, 1)
       // (~1 ms): pacing is a hint, a non-resident unit cannot deadlock the others.
       const int PACE_KB = (KIND >= GK_WGRAD_DOWN || p.pace_kb <= 0) ? (1 << 30) : p.pace_kb;
       auto pace = [&]() {
-        if (step > 0 && seen < ncid * step) {
-          const int target = ncid * step;
+        const int target = ncid * (step + 1 - p.pace_slack);   // every unit started step - slack
+        if (step >= p.pace_slack && seen < target) {
           for (int spin = 0; spin < 1000; spin++) {
             int v;
             asm volatile("ld.relaxed.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p.wave_ctr) : "memory");
@@ -1186,6 +1188,38 @@ bool map3d(CUtensorMap* m, const void* base, uint64_t d0, uint64_t d1, uint64_t 
   return make_map(m, base, 3, d, s, b);
 }
 
+// Wave pacing (profiles/r01_gemm_dram_pacing.md): opt-in, MEMFINE_WAVE_SYNC=1.  It cuts DRAM traffic
+// 2-15 %, but the step time moved -5 % on two boxes and +3..6 % on another (lock-stepped units hit
+// the same L2 lines at once), so it is not the default.  Even when asked for, it is used only where
+// the caller guarantees no concurrent kernel holds SMs (gp.pace: EP = 1, one stream) - elsewhere a
+// non-resident unit would make the others sit out the spin bound.  One counter per launch from a
+// ring, zeroed on the launch's stream.
+int setup_pacing(Params& p, const GemmProblem<__nv_bfloat16>& gp, cudaStream_t st) {
+  static const int env_wave = [] {
+    const char* s = getenv("MEMFINE_WAVE_SYNC");
+    return s ? atoi(s) : -1;
+  }();
+  static const int env_kb = [] {
+    const char* s = getenv("MEMFINE_PACE_KB");
+    return s ? atoi(s) : 0;   // sub-tile steps measured worse (dX 7.3 -> 9.3 ms at 64)
+  }();
+  static int* ctr_ring = nullptr;
+  static std::atomic<unsigned> ctr_next{0};
+  p.wave_ctr = nullptr;
+  if (!(env_wave == 1 && gp.pace && gp.sm_limit <= 0)) return 0;
+  static std::once_flag once;
+  std::call_once(once, [] { if (cudaMalloc(&ctr_ring, 4096 * sizeof(int)) != cudaSuccess) ctr_ring = nullptr; });
+  if (!ctr_ring) return -1;
+  p.wave_ctr = ctr_ring + (ctr_next++ & 4095u);
+  p.pace_kb = env_kb;
+  static const int env_slack = [] {
+    const char* s = getenv("MEMFINE_PACE_SLACK");
+    return s ? std::max(1, atoi(s)) : 1;
+  }();
+  p.pace_slack = env_slack;
+  return cudaMemsetAsync(p.wave_ctr, 0, sizeof(int), st) == cudaSuccess ? 0 : -1;
+}
+
 int g_num_sms = 0;
 
 bool use_pairs() {
@@ -1322,27 +1356,7 @@ int launch(const GemmProblem<__nv_bfloat16>& gp, cudaStream_t st) {
       p.group_m = (int)std::max<double>(1.0, std::min<double>(64.0, std::floor(gm + 0.5)));
     }
   }
-  {
-    // Wave pacing (profiles/r01_gemm_dram_pacing.md: -2..-15 % DRAM traffic, +0..3 % step).  On where
-    // the caller guarantees no concurrent kernel holds SMs (gp.pace: EP = 1, one stream) - elsewhere a
-    // non-resident unit would make the others sit out the spin bound.  MEMFINE_WAVE_SYNC=0/1 forces it.
-    static const int env_wave = [] {
-      const char* s = getenv("MEMFINE_WAVE_SYNC");
-      return s ? atoi(s) : -1;
-    }();
-    static int* ctr_ring = nullptr;
-    static int ctr_next = 0;
-    if (env_wave == 1 || (env_wave < 0 && gp.pace && gp.sm_limit <= 0)) {
-      if (!ctr_ring && cudaMalloc(&ctr_ring, 4096 * sizeof(int)) != cudaSuccess) return -1;
-      p.wave_ctr = ctr_ring + (ctr_next++ & 4095);
-      if (cudaMemsetAsync(p.wave_ctr, 0, sizeof(int), st) != cudaSuccess) return -1;
-      static const int env_kb = [] {
-        const char* s = getenv("MEMFINE_PACE_KB");
-        return s ? atoi(s) : 0;   // sub-tile steps measured worse (dX 7.3 -> 9.3 ms at 64)
-      }();
-      p.pace_kb = env_kb;
-    }
-  }
+  if (setup_pacing(p, gp, st)) return -1;
   int64_t max_tiles;
   if (KIND >= GK_WGRAD_DOWN) {
     p.num_mt_w = (p.M + TM - 1) / TM;
@@ -1512,6 +1526,7 @@ int launch_mx(const GemmProblem<__nv_bfloat16>& gp, cudaStream_t st) {
     int64_t a_strip = (int64_t)(PAIR ? 2 : 1) * BM * p.K;   // E4M3: one byte per element
     p.group_m = (int)std::max<int64_t>(1, std::min<int64_t>(64, budget / a_strip));
   }
+  if (setup_pacing(p, gp, st)) return -1;
   const int per_unit = PAIR ? 2 : 1;
   int64_t max_tiles = (int64_t)((R / BM + (PAIR ? El : 0)) / per_unit + 1) * nt;
   const int sms = gp.sm_limit > 0 ? std::min(gp.sm_limit, g_num_sms) : g_num_sms;
