@@ -387,13 +387,30 @@ def main():
         achieved = per_launch_flops / (avg_ms / 1000.0) / 1e12
         peak = peaks["bf16_tflops_sustained"]
         traffic, tsrc = load_traffic()
-        tb = traffic.get(dom, {}).get("bytes_per_launch") if traffic else None
+        # the committed capture is of the default workload (Mixtral, EP = 1, C = 1); other shapes: null
+        same = (args.config == "mixtral" and args.ep_emulate == 1 and not args.tokens and world == 1 and C == 1)
+        tb = traffic.get(dom, {}).get("bytes_per_launch") if (traffic and same) else None
         roof = {"bound": "tensor", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                 "frac": achieved / peak, "traffic": tb,
                 "traffic_source": f"{tsrc}: ncu --set full dram__bytes_read.sum + dram__bytes_write.sum per launch"
                 if tb else None,
                 "algorithmic_flops_per_launch": per_launch_flops,
                 "peak_source": f"{peaks['source']} bf16_tflops_sustained (kernel timed inside a long step)",
+                "share_of_step": prof[dom]["ms"] / tot_ms if tot_ms else None}
+    elif dom in ("dispatch_permute", "combine_unpermute") and prof[dom]["launches"]:
+        # HBM-bound permute kernels (small layers): algorithmic bytes per step, bf16 rows of h.
+        # dispatch: fwd reads T rows of x and writes s'' rows, bwd the same for x and dY;
+        # combine: fwd reads s'' rows of o and writes T rows of y, bwd the same for dX.
+        eb = 2 * h
+        bytes_step = (3 * T + 3 * rows_total) * eb if dom == "dispatch_permute" else (2 * rows_total + 2 * T) * eb
+        per_launch = bytes_step * args.steps / prof[dom]["launches"]
+        avg_ms = prof[dom]["ms"] / prof[dom]["launches"]
+        achieved = per_launch / (avg_ms / 1000.0) / 1e9
+        peak = peaks["hbm_gbs"]
+        roof = {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "GB/s",
+                "frac": achieved / peak, "traffic": None,
+                "algorithmic_bytes_per_launch": per_launch,
+                "peak_source": f"{peaks['source']} hbm_gbs (copy)",
                 "share_of_step": prof[dom]["ms"] / tot_ms if tot_ms else None}
     gemm_ms = sum(prof[s]["ms"] for s in FLOP_COEF) / args.steps
     all_gemm_tflops = 22 * h * g * rows_total / (gemm_ms / 1000.0) / 1e12 if gemm_ms else None
