@@ -50,6 +50,8 @@ def test_gpu_arm_line_tiny():
     assert (roof["bound"], roof["unit"]) in (("tensor", "TFLOP/s"), ("hbm", "GB/s"))
     assert 0 < roof["frac"] == roof["achieved"] / roof["peak"]
     assert roof["traffic"] is None   # the committed ncu capture is of the Mixtral workload, not this one
+    sr = line["step_roofline"]   # the north star's 3-term roofline of the whole step
+    assert sr["bound"] in ("tensor", "hbm", "nvlink") and 0 < sr["frac"] <= 1.0 and sr["t_roof4_ms"] >= sr["t_roof_ms"]
     e2e = line["e2e"]
     assert e2e["value"] > 0 and e2e["h2d_bytes_per_step"] > 0 and e2e["d2h_bytes_per_step"] > 0
     assert line["gpu_launches"] > 0
