@@ -303,9 +303,11 @@ def mx_weights(d: Dims, wg, wu, wd, mode: int = 1):
     return out
 
 
-def moe_mx(d: Dims, x, ids, w, wq, dy=None, mode: int = 1, wd=None):
+def moe_mx(d: Dims, x, ids, w, wq, dy=None, mode: int = 1, wd=None, wgrad_C: int = 0):
     """MX variant of the layer (mode 0: quantisers off).  wq from mx_weights(mode); wd the unquantised
-    W_down (needed with dy: the dA step keeps BF16 operands).
+    W_down (needed with dy: the dA step keeps BF16 operands).  wgrad_C = 0: weight gradients from
+    unquantised operands; wgrad_C = C >= 1: MXFP8 weight gradients (operand columns quantised along
+    each expert's copies in each of the C chunks; reading R28c).
     Returns y, or (y, dx, dscore, dwg, dwu, dwd) when dy is given."""
     x = _wt(x, d.in_dtype)
     ids = np.ascontiguousarray(ids, dtype=np.int32)
@@ -315,7 +317,7 @@ def moe_mx(d: Dims, x, ids, w, wq, dy=None, mode: int = 1, wd=None):
     arr = (C.POINTER(C.c_double) * 5)(*[np.ascontiguousarray(a).ctypes.data_as(C.POINTER(C.c_double)) for a in wq])
     if dy is None:
         st = lib().oracle_moe_mx(C.byref(d.c()), C.c_int32(mode), None, _p(x), _p(ids), _p(w), arr, None, _p(y),
-                                 None, None, None, None, None)
+                                 None, None, None, None, None, C.c_int32(0))
         assert st == 0
         return y
     dy = _wt(dy, d.in_dtype)
@@ -323,6 +325,6 @@ def moe_mx(d: Dims, x, ids, w, wq, dy=None, mode: int = 1, wd=None):
     dx = np.zeros((n, d.h)); ds = np.zeros((n, d.k))
     dwg = np.zeros((d.E, d.g, d.h)); dwu = np.zeros((d.E, d.g, d.h)); dwd = np.zeros((d.E, d.h, d.g))
     st = lib().oracle_moe_mx(C.byref(d.c()), C.c_int32(mode), _p(dy), _p(x), _p(ids), _p(w), arr, _p(wd), _p(y), _p(dx),
-                             _p(ds), _p(dwg), _p(dwu), _p(dwd))
+                             _p(ds), _p(dwg), _p(dwu), _p(dwd), C.c_int32(wgrad_C))
     assert st == 0
     return y, dx, ds, dwg, dwu, dwd

@@ -725,9 +725,10 @@ void oracle_router_backward(const oracle_dims* d, int64_t ntok, const void* x, c
 /*  - elements v / X rounded to FP8 E4M3 (bias 7, max 448, no inf) by          */
 /*    round-to-nearest-even, saturating at +-448;  dequant = e4m3(code) * X.    */
 /* Quantised operands: forward/recompute x and W_gate/W_up rows along h, a and */
-/* W_down rows along g; backward dX: dG/dU and W_gate/W_up columns along g.    */
-/* The dA GEMM (dY W_down, epilogue-bound) and the weight gradients keep       */
-/* unquantised operands.                                                        */
+/* W_down rows along g; backward dX: dG/dU and W_gate/W_up columns along g;    */
+/* weight gradients (wgrad_C >= 1, reading R28c): x, dY, dG/dU and a_w columns  */
+/* along the copies (tokens) of each expert in each chunk.  The dA GEMM         */
+/* (dY W_down, epilogue-bound) keeps unquantised operands.                      */
 /* mode 0 replaces every quantiser by the identity (then these functions equal */
 /* oracle_moe_forward / oracle_moe_tokens exactly) - a structural pin.          */
 /* ------------------------------------------------------------------------- */
@@ -912,13 +913,93 @@ static void expert_mx(const oracle_dims* d, int mode, const void* x, int64_t xof
     }
 }
 
-/* MX variant of the whole layer: y, and (dy != NULL) dx, dscore and dW (dW in the
- * canonical copy order, unquantised operands).  Outputs as oracle_moe_forward /
- * oracle_moe_backward.  wq from oracle_mx_weights with the same mode; wd the
+/* MXFP8 weight gradients (reading R28c; the Transformer-Engine-style "columnwise"
+ * operands): W_grad = sum over chunks (reading R18), and inside chunk j (partition of reading R1)
+ * the K dimension of expert e's weight-gradient GEMMs is its copies in the canonical order
+ * (src rank, token, slot; reading R3).  Every operand column is quantised in blocks of 32
+ * consecutive copies counted from the start of that list (the last block zero-padded - the
+ * 128-row segment padding).  Operands as the kernel holds them (reading R28b): x and dY as
+ * stored (bf16 inputs), dG / dU as stored (bf16), a_w = w * a as stored (bf16 of the fp32
+ * product, a as the dA step sees it).  dW_gate[e] += dG^T x, dW_up[e] += dU^T x,
+ * dW_down[e] += dY^T a_w, all on dequantised values, accumulated in fp64.
+ * mode 0: no rounding and no quantiser - then this equals accumulate_dw up to summation order. */
+static int accumulate_dw_mx(const oracle_dims* d, int mode, int32_t C, const void* x, const void* dy,
+                            const int32_t* ids, const double* w, const double* a_all, const double* dG_all,
+                            const double* dU_all, double* dwg, double* dwu, double* dwd)
+{
+    int64_t h = d->h, g = d->g, E = d->E, k = d->k, T = d->T, EP = d->EP;
+    memset(dwg, 0, sizeof(double) * (size_t)E * g * h);
+    memset(dwu, 0, sizeof(double) * (size_t)E * g * h);
+    memset(dwd, 0, sizeof(double) * (size_t)E * h * g);
+    int64_t nq = EP * T * k;
+    int64_t* list = (int64_t*)malloc(sizeof(int64_t) * (size_t)(nq > 0 ? nq : 1));
+    double* Xb = (double*)malloc(sizeof(double) * (size_t)32 * (2 * h + 3 * g));
+    if (!list || !Xb) { free(list); free(Xb); return 1; }
+    double *Yb = Xb + 32 * h, *Gb = Yb + 32 * h, *Ub = Gb + 32 * g, *Ab = Ub + 32 * g;
+    for (int32_t j = 0; j < C; j++) {
+        int64_t t0 = oracle_chunk_begin(T, C, j), t1 = oracle_chunk_begin(T, C, j + 1);
+        for (int32_t e = 0; e < E; e++) {
+            int64_t n = 0;
+            for (int64_t r = 0; r < EP; r++)
+                for (int64_t t = t0; t < t1; t++)
+                    for (int64_t sl = 0; sl < k; sl++) {
+                        int64_t q = (r * T + t) * k + sl;
+                        if (ids[q] == e) list[n++] = q;
+                    }
+            for (int64_t b0 = 0; b0 < n; b0 += 32) {
+                int64_t nb = n - b0 < 32 ? n - b0 : 32;
+                for (int64_t i = 0; i < 32; i++) {
+                    int64_t q = i < nb ? list[b0 + i] : -1;
+                    int64_t tok = q >= 0 ? q / k : 0;
+                    for (int64_t c = 0; c < h; c++) {
+                        Xb[i * h + c] = q >= 0 ? load(x, tok * h + c, d->in_dtype) : 0.0;
+                        Yb[i * h + c] = q >= 0 ? load(dy, tok * h + c, d->in_dtype) : 0.0;
+                    }
+                    for (int64_t c = 0; c < g; c++) {
+                        double gv = q >= 0 ? dG_all[q * g + c] : 0.0, uv = q >= 0 ? dU_all[q * g + c] : 0.0;
+                        double av = q >= 0 ? w[q] * a_all[q * g + c] : 0.0;
+                        Gb[i * g + c] = mode ? round_bf16(gv) : gv;
+                        Ub[i * g + c] = mode ? round_bf16(uv) : uv;
+                        Ab[i * g + c] = mode ? round_bf16(round_f32(av)) : av;
+                    }
+                }
+                /* columnwise blocks: 32 rows of one column (stride = the row length) */
+                for (int64_t c = 0; c < h; c++) { mx_qdq(Xb + c, 32, h, mode); mx_qdq(Yb + c, 32, h, mode); }
+                for (int64_t c = 0; c < g; c++) {
+                    mx_qdq(Gb + c, 32, g, mode); mx_qdq(Ub + c, 32, g, mode); mx_qdq(Ab + c, 32, g, mode);
+                }
+                #pragma omp parallel for schedule(static)
+                for (int64_t nn = 0; nn < g; nn++) {
+                    double* rg = dwg + ((int64_t)e * g + nn) * h;
+                    double* ru = dwu + ((int64_t)e * g + nn) * h;
+                    for (int64_t i = 0; i < nb; i++) {
+                        double gv = Gb[i * g + nn], uv = Ub[i * g + nn];
+                        for (int64_t c = 0; c < h; c++) { rg[c] += gv * Xb[i * h + c]; ru[c] += uv * Xb[i * h + c]; }
+                    }
+                }
+                #pragma omp parallel for schedule(static)
+                for (int64_t m = 0; m < h; m++) {
+                    double* rd = dwd + ((int64_t)e * h + m) * g;
+                    for (int64_t i = 0; i < nb; i++) {
+                        double yv = Yb[i * h + m];
+                        for (int64_t c = 0; c < g; c++) rd[c] += yv * Ab[i * g + c];
+                    }
+                }
+            }
+        }
+    }
+    free(list); free(Xb);
+    return 0;
+}
+
+/* MX variant of the whole layer: y, and (dy != NULL) dx, dscore and dW.  wgrad_C = 0: dW from
+ * unquantised operands in the canonical copy order (accumulate_dw); wgrad_C >= 1: MXFP8
+ * weight gradients over the chunk partition with C = wgrad_C (accumulate_dw_mx).  Outputs as
+ * oracle_moe_forward / oracle_moe_backward.  wq from oracle_mx_weights with the same mode; wd the
  * unquantised W_down (in_dtype) for the dA step. */
 int32_t oracle_moe_mx(const oracle_dims* d, int32_t mode, const void* dy, const void* x, const int32_t* ids,
                       const double* w, double* const* wq, const void* wd, double* y, double* dx, double* dscore,
-                      double* dwg, double* dwu, double* dwd)
+                      double* dwg, double* dwu, double* dwd, int32_t wgrad_C)
 {
     int64_t h = d->h, g = d->g, ntok = (int64_t)d->EP * d->T, nq = ntok * d->k;
     double *a_all = NULL, *dG_all = NULL, *dU_all = NULL, *dO_all = NULL;
@@ -965,12 +1046,16 @@ int32_t oracle_moe_mx(const oracle_dims* d, int32_t mode, const void* dy, const 
         }
         free(scratch); free(O);
     }
+    int32_t rc = 0;
     if (dy) {
         for (int64_t q = 0; q < nq; q++) order[q] = q;
-        accumulate_dw(d, x, ids, order, nq, a_all, dO_all, dG_all, dU_all, dwg, dwu, dwd);
+        if (wgrad_C >= 1)
+            rc = accumulate_dw_mx(d, mode, wgrad_C, x, dy, ids, w, a_all, dG_all, dU_all, dwg, dwu, dwd);
+        else
+            accumulate_dw(d, x, ids, order, nq, a_all, dO_all, dG_all, dU_all, dwg, dwu, dwd);
         free(a_all); free(dG_all); free(dU_all); free(dO_all); free(order);
     }
-    return 0;
+    return rc;
 }
 
 int32_t oracle_version(void) { return 1; }

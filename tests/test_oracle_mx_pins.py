@@ -150,3 +150,75 @@ def test_mx_layer_quantisation_error_is_small_but_present():
     y = oracle.moe_forward(d, x, ids, w, wg, wu, wd)
     err = np.abs(y_mx - y).max() / np.abs(y).max()
     assert 1e-4 < err < 0.1          # E4M3 keeps 3 mantissa bits: a few % at most, never zero
+
+
+# ---------------------------------------------------------------- MXFP8 weight gradients (R28c)
+def test_mx_wgrad_mode0_equals_exact_dw():
+    """Quantisers and roundings off: the chunked columnwise path is the definition W_grad = sum over
+    chunks of the copies' outer products (reading R18), whatever C."""
+    d, x, dy, wg, wu, wd, ids, w = _problem(T=40)
+    wq = oracle.mx_weights(d, wg, wu, wd, mode=0)
+    ref = oracle.moe_backward(d, dy, x, ids, w, wg, wu, wd)
+    for C in (1, 3):
+        *_, dwg, dwu, dwd = oracle.moe_mx(d, x, ids, w, wq, dy=dy, mode=0, wd=wd, wgrad_C=C)
+        for a, b in zip((dwg, dwu, dwd), ref[2:]):
+            assert np.abs(a - b).max() <= 1e-12 * np.abs(b).max()
+
+
+def test_mx_wgrad_brute_force():
+    """Independent re-derivation: per copy G, U, dG, dU, a_w as the kernel holds them (numpy, torch
+    float8 / bfloat16 conversions), then per chunk and expert the copies stacked in (token, slot)
+    order (reading R3, EP = 1), zero-padded to a multiple of 32 rows, every column quantised per
+    32-row block (_mxq along the copies), and dW_gate = dG^T x, dW_up = dU^T x, dW_down = dY^T a_w."""
+    T = 80
+    d, x, dy, wg, wu, wd, ids, w = _problem(T=T, seed=9)
+    wq = oracle.mx_weights(d, wg, wu, wd)
+    sig = lambda z: 1 / (1 + np.exp(-z))
+    bf = lambda v: torch.from_numpy(np.asarray(v, np.float64)).to(torch.bfloat16).to(torch.float64).numpy()
+    f32 = lambda v: np.asarray(v, np.float32).astype(np.float64)
+    per = {}
+    for t in range(T):
+        xq = _mxq(x[t], 0)
+        for s in range(d.k):
+            e = ids[t, s]
+            G, U = bf(_mxq(wg[e], 1) @ xq), bf(_mxq(wu[e], 1) @ xq)   # the recomputed G || U as stored
+            a = G * sig(G) * U
+            u = wd[e].astype(np.float64).T @ dy[t].astype(np.float64)
+            dA = w[t, s] * u
+            per[t, s] = (bf(dA * U * sig(G) * (1 + G * (1 - sig(G)))), bf(dA * G * sig(G)), bf(f32(w[t, s] * a)))
+    for C in (1, 2):
+        ref = [np.zeros((d.E, d.g, d.h)), np.zeros((d.E, d.g, d.h)), np.zeros((d.E, d.h, d.g))]
+        for j in range(C):
+            t0, t1 = j * T // C, (j + 1) * T // C
+            for e in range(d.E):
+                cp = [(t, s) for t in range(t0, t1) for s in range(d.k) if ids[t, s] == e]
+                n = -(-len(cp) // 32) * 32
+                if not cp:
+                    continue
+                pad = lambda rows, width: np.vstack([np.array(rows, np.float64), np.zeros((n - len(rows), width))])
+                colq = lambda m: np.vstack([_mxq(m[i:i + 32], 0) for i in range(0, n, 32)])
+                X = colq(pad([x[t] for t, _ in cp], d.h))
+                Y = colq(pad([dy[t] for t, _ in cp], d.h))
+                dG = colq(pad([per[c][0] for c in cp], d.g))
+                dU = colq(pad([per[c][1] for c in cp], d.g))
+                Aw = colq(pad([per[c][2] for c in cp], d.g))
+                ref[0][e] += dG.T @ X
+                ref[1][e] += dU.T @ X
+                ref[2][e] += Y.T @ Aw
+        *_, dwg, dwu, dwd = oracle.moe_mx(d, x, ids, w, wq, dy=dy, wd=wd, wgrad_C=C)
+        for got, r in zip((dwg, dwu, dwd), ref):
+            assert np.abs(got - r).max() <= 1e-10 * np.abs(r).max()
+
+
+def test_mx_wgrad_error_small_present_and_chunk_dependent():
+    """Against unquantised operands the MX weight gradients differ by a few % at most (3 mantissa
+    bits per operand) and never by zero; the blocks follow the chunk partition, so C matters."""
+    d, x, dy, wg, wu, wd, ids, w = _problem(T=64, seed=4)
+    wq = oracle.mx_weights(d, wg, wu, wd)
+    *_, e0, e1, e2 = oracle.moe_mx(d, x, ids, w, wq, dy=dy, wd=wd, wgrad_C=0)
+    outs = {C: oracle.moe_mx(d, x, ids, w, wq, dy=dy, wd=wd, wgrad_C=C)[3:] for C in (1, 2)}
+    for C, (g1, u1, d1) in outs.items():
+        for got, ref in ((g1, e0), (u1, e1), (d1, e2)):
+            err = np.abs(got - ref).max() / np.abs(ref).max()
+            assert 1e-4 < err < 0.1, (C, err)
+    assert not np.array_equal(outs[1][0], outs[2][0])
