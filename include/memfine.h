@@ -39,7 +39,7 @@
 extern "C" {
 #endif
 
-#define MEMFINE_ABI_VERSION 1
+#define MEMFINE_ABI_VERSION 2
 
 /* Status codes.  1 and 2 mirror the SPEC CLI exit codes. */
 typedef enum {
@@ -96,8 +96,12 @@ typedef struct {
  *    all-gather, send staging, per-(peer, local expert) all-to-allv, combine exchange - over a
  *    1-rank NCCL communicator, every segment (including the self segment) through ncclSend /
  *    ncclRecv.  memfine_create then takes a unique id.  Results equal the EP = 1 path; this is
- *    how the NCCL transport is exercised on a single GPU (NCCL refuses two ranks on one device). */
-enum { MEMFINE_FLAG_OVERLAP = 1, MEMFINE_FLAG_EP_PATH = 2 };
+ *    how the NCCL transport is exercised on a single GPU (NCCL refuses two ranks on one device).
+ *  MEMFINE_FLAG_MX_WGRAD (dtype MEMFINE_MXFP8, ep_size == 1, no EP_PATH): the weight-gradient
+ *    GEMMs also take MXFP8 operands - x, dY, dG || dU and a_w quantised columnwise (blocks of 32
+ *    copies of an expert within a chunk, reading R28c) - instead of BF16 ones.  Adds the
+ *    columnwise codes to the backward workspace ((h + 3g) * 33/32 bytes per row). */
+enum { MEMFINE_FLAG_OVERLAP = 1, MEMFINE_FLAG_EP_PATH = 2, MEMFINE_FLAG_MX_WGRAD = 4 };
 
 /* Memory budget for MACT (Eq. 3; Eq. 8). */
 typedef struct {
@@ -341,9 +345,10 @@ memfine_status memfine_last_stats(memfine_handle_t h, memfine_stats* out);
  * recorded on the launch stream and accumulates per-kernel-class device time.  Slots:
  * 0..5 the expert GEMMs (0 gate/up+SwiGLU, 1 down, 2 dA+fused epilogue, 3 dX,
  * 4 dW_down, 5 dW_gate||dW_up), 6 dispatch (histogram, scan, permute, padding), 7 combine /
- * unpermute-reduce, 8 memsets, 9 NCCL exchanges.  memfine_profile_read synchronises on the
+ * unpermute-reduce, 8 memsets, 9 NCCL exchanges, 10 the MX weight gradients' columnwise quantisation
+ * (MEMFINE_FLAG_MX_WGRAD).  memfine_profile_read synchronises on the
  * recorded events, returns the totals since the last read, and resets them. */
-#define MEMFINE_PROF_SLOTS 10
+#define MEMFINE_PROF_SLOTS 11
 typedef struct {
     int32_t launches[MEMFINE_PROF_SLOTS];
     double  ms[MEMFINE_PROF_SLOTS];

@@ -14,7 +14,7 @@ BF16, FP32, MXFP8 = 0, 1, 2
 RULE_EQ9, RULE_EXACT = 0, 1
 MODEL_PAPER, MODEL_IMPL = 0, 1
 EP_COPY, EP_P2P = 0, 1
-FLAG_OVERLAP, FLAG_EP_PATH = 1, 2
+FLAG_OVERLAP, FLAG_EP_PATH, FLAG_MX_WGRAD = 1, 2, 4
 FWD, BWD = 0, 1
 
 # Every symbol include/memfine.h declares (checked by tests/test_abi.py).
@@ -25,7 +25,8 @@ SYMBOLS = ("memfine_abi_version", "memfine_status_str", "memfine_nccl_unique_id"
            "memfine_mx_weights_bytes", "memfine_mx_quantize_weights", "memfine_mx_quantize")
 
 PROF_SLOTS = ("gemm_gateup_swiglu", "gemm_down", "gemm_dact_epilogue", "gemm_dx", "gemm_wgrad_down",
-              "gemm_wgrad_gateup", "dispatch_permute", "combine_unpermute", "memset", "nccl_exchange")
+              "gemm_wgrad_gateup", "dispatch_permute", "combine_unpermute", "memset", "nccl_exchange",
+              "mx_quant_colwise")
 
 
 class MemfineError(RuntimeError):
@@ -70,10 +71,10 @@ class Stats(C.Structure):
 
 
 class Profile(C.Structure):
-    _fields_ = [("launches", C.c_int32 * 10), ("ms", C.c_double * 10)]
+    _fields_ = [("launches", C.c_int32 * len(PROF_SLOTS)), ("ms", C.c_double * len(PROF_SLOTS))]
 
     def as_dict(self):
-        return {PROF_SLOTS[i]: {"launches": self.launches[i], "ms": self.ms[i]} for i in range(10)}
+        return {PROF_SLOTS[i]: {"launches": self.launches[i], "ms": self.ms[i]} for i in range(len(PROF_SLOTS))}
 
 
 _lib = None
@@ -119,7 +120,7 @@ def lib():
         L.memfine_mx_weights_bytes.argtypes = [C.POINTER(Dims), C.POINTER(u64)]
         L.memfine_mx_quantize_weights.argtypes = [vp, vp, vp, vp, vp, u64, vp]
         L.memfine_mx_quantize.argtypes = [vp, i64, i32, vp, vp, vp]
-        if L.memfine_abi_version() != 1:
+        if L.memfine_abi_version() != 2:
             raise RuntimeError("libmemfine.so ABI mismatch")
         _lib = L
     return _lib

@@ -361,7 +361,8 @@ struct Epi {
   static constexpr int WARP_BYTES = BUFS * CHUNK_BYTES;
   // MX N=256 kinds store straight from registers (early accumulator release): no staging, so the
   // mainloop gets the smem for more stages.
-  static constexpr int TOTAL = MX ? 0 : EPI_WARPS * WARP_BYTES;
+  // (MX weight gradients keep the fp32 staging: dW goes out by TMA store / reduce-add)
+  static constexpr int TOTAL = (MX && KIND < GK_WGRAD_DOWN) ? 0 : EPI_WARPS * WARP_BYTES;
 };
 
 struct Params {
@@ -477,7 +478,7 @@ __device__ __forceinline__ Tile tile_of(const Params& p, int t) {
     T.n0 = (r / gm) * BN;
     int s0 = __ldg(p.seg + T.e), s1 = __ldg(p.seg + T.e + 1);
     T.k0 = s0;
-    T.nkb = (s1 - s0) / BK;
+    T.nkb = (s1 - s0) / (MX ? 128 : BK);   // segments are 128-row padded
     return T;
   }
   int num_mt = PAIR ? p.info[kInfoPairs] : p.info[kInfoRowsPad] / BM;
@@ -551,7 +552,7 @@ __global__ void __launch_bounds__(THREADS, 1)
   constexpr uint32_t TMEM_COLS = MX ? 512 : 2 * ACC_COLS;
   constexpr uint32_t SF_COL = ACC_ST * ACC_COLS;        // MX: A scales at +0..3, B at +4..11
   static_assert(TMEM_COLS <= 512 && (!MX || ACC_ST * ACC_COLS + kMxSf <= 512), "TMEM");
-  static_assert(!MX || KIND == GK_GATEUP || KIND == GK_DOWN || KIND == GK_DX, "MX: gate/up, down, dX");
+  static_assert(!MX || KIND != GK_DACT, "MX: gate/up, down, dX, weight gradients (R28c)");
   constexpr uint32_t IDESC = idesc_bf16(PAIR ? 2 * BM : BM, MMA_N, CF::A_MN, CF::B_MN);
 
   extern __shared__ uint8_t smem_raw[];
@@ -657,9 +658,11 @@ __global__ void __launch_bounds__(THREADS, 1)
             // E4M3 A [128 rows x 128 K], this CTA's B rows (all, or its half in a pair) and the scale
             // chunks: own A rows' chunk, the whole B tile's chunks (TMA zero-fills chunks and rows
             // past the end - ragged N tiles, a pair's second m-tile past the buffer)
-            const int kc = kb * 128;
+            const int kc = (KIND >= GK_WGRAD_DOWN ? T.k0 : 0) + kb * 128;
             uint8_t* ssf = sb + B_BYTES;
-            const int KB = p.K >> 7;
+            // K chunks per 128 operand rows: the weight-gradient operands are the chunk's columnwise
+            // codes [M or N rows][rows_cap] (K = the copies, reading R28c)
+            const int KB = KIND >= GK_WGRAD_DOWN ? (int)(p.rows_cap >> 7) : p.K >> 7;
             constexpr int SFB_CH = MMA_N / 128;
             if (leader) mbar_expect_tx(full + stage, (PAIR ? 2 : 1) * (A_BYTES + B_BYTES + 512 + 512 * SFB_CH));
             auto L2 = [&](void* dst, const CUtensorMap* m, int c0, int c1) {
@@ -669,8 +672,17 @@ __global__ void __launch_bounds__(THREADS, 1)
               if (PAIR) tma_3d_pair(dst, m, full + stage, c0, c1, c2); else tma_3d(dst, m, full + stage, c0, c1, c2);
             };
             L2(sa, &tmA, kc, am0);
-            L2(ssf, &tmSA, 0, (am0 >> 7) * KB + kb);
-            if (KIND == GK_GATEUP) {
+            L2(ssf, &tmSA, 0, (am0 >> 7) * KB + (kc >> 7));
+            if (KIND >= GK_WGRAD_DOWN) {
+              // B(n, k) = codes_t[n][k]: this CTA's rows of the N tile, the whole tile's scale chunks
+              L2(sb, &tmB0, kc, T.n0 + (PAIR ? (int)rank * B_ROWS : 0));
+              const int nch = p.N >> 7;
+#pragma unroll
+              for (int i = 0; i < SFB_CH; i++) {
+                const int nc = (T.n0 >> 7) + i;
+                L2(ssf + 512 + 512 * i, &tmSB0, 0, (nc < nch ? nc : (T.n0 >> 7)) * KB + (kc >> 7));
+              }
+            } else if (KIND == GK_GATEUP) {
               if (PAIR) {
                 L3(sb, rank ? &tmB1 : &tmB0, kc, T.n0, T.e);       // CTA0: W_gate rows, CTA1: W_up rows
               } else {
@@ -898,7 +910,20 @@ __global__ void __launch_bounds__(THREADS, 1)
           float v[32];
 #pragma unroll
           for (int j = 0; j < 32; j++) v[j] = __uint_as_float(acc[i][j]);
-          if constexpr (KIND == GK_GATEUP) {
+          if constexpr (KIND >= GK_WGRAD_DOWN) {
+            // MX weight gradients (R28c): fp32 dW tile by TMA store (first chunk) / reduce-add
+            if (!rows_ok || n >= p.N) continue;
+            uint8_t* buf = next_buf();
+            stage_f32_row(buf, lane, v);
+            fence_async_smem();
+            __syncwarp();
+            if (lane == 0) {
+              if (KIND == GK_WGRAD_DOWN) tma_store_3d(&tmO0, buf, n, row0, T.e, p.beta != 0);
+              else if (row0 < p.g) tma_store_3d(&tmO0, buf, n, row0, T.e, p.beta != 0);
+              else tma_store_3d(&tmO1, buf, n, row0 - p.g, T.e, p.beta != 0);
+              bulk_commit();
+            }
+          } else if constexpr (KIND == GK_GATEUP) {
             if (!rows_ok || n >= p.g) continue;
             if (!p.store_gu) {
               // a = silu(G) U straight to MXFP8: this thread's 32 columns are one block
@@ -1396,6 +1421,11 @@ bool map_fp8_2d(CUtensorMap* m, const void* base, uint64_t K, uint64_t rows) {
   uint32_t b[2] = {128, 128};
   return make_map_t(m, CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, CU_TENSOR_MAP_SWIZZLE_128B, base, 2, d, b);
 }
+bool map_fp8_2d_box(CUtensorMap* m, const void* base, uint64_t K, uint64_t rows, uint32_t box_rows) {
+  uint64_t d[2] = {K, rows};
+  uint32_t b[2] = {128, box_rows};
+  return make_map_t(m, CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, CU_TENSOR_MAP_SWIZZLE_128B, base, 2, d, b);
+}
 bool map_fp8_3d(CUtensorMap* m, const void* base, uint64_t K, uint64_t rows, uint64_t El, uint32_t box_rows) {
   uint64_t d[3] = {K, rows, El};
   uint32_t b[3] = {128, box_rows, 1};
@@ -1500,6 +1530,34 @@ int launch_mx(const GemmProblem<__nv_bfloat16>& gp, cudaStream_t st) {
       ok &= map2d_st(&mO0, gp.O, h, R);
       mO1 = mO0;
       break;
+    case GK_WGRAD_DOWN:
+      // dW_down[e] (+)= dY^T a_w over the expert's copies: A = dY columnwise codes [h][R],
+      // B = a_w columnwise codes [g][R] (reading R28c)
+      p.M = gp.h; p.N = gp.g; p.K = (int)R;
+      ok &= map_fp8_2d(&mA, gp.mx_a.q, R, h);
+      ok &= map_fp8_2d_box(&mB0, gp.mx_b0.q, R, g, BOX);
+      mB1 = mB0;
+      ok &= map_sf(&mSB0, gp.mx_b0.sf, (g / 128) * (R / 128));
+      mSB1 = mSB0;
+      p.dW0 = gp.dWd;
+      p.beta = gp.wgrad_beta;
+      ok &= map3d_f32(&mO0, gp.dWd, g, h, El);
+      mO1 = mO0;
+      break;
+    case GK_WGRAD_GU:
+      // dW_gate || dW_up[e] (+)= dGU^T x: A = dG || dU columnwise codes [2g][R], B = x's [h][R]
+      p.M = 2 * gp.g; p.N = gp.h; p.K = (int)R;
+      ok &= map_fp8_2d(&mA, gp.mx_a.q, R, 2 * g);
+      ok &= map_fp8_2d_box(&mB0, gp.mx_b0.q, R, h, BOX);
+      mB1 = mB0;
+      ok &= map_sf(&mSB0, gp.mx_b0.sf, (h / 128) * (R / 128));
+      mSB1 = mSB0;
+      p.dW0 = gp.dWg;
+      p.dW1 = gp.dWu;
+      p.beta = gp.wgrad_beta;
+      ok &= map3d_f32(&mO0, gp.dWg, h, g, El);
+      ok &= map3d_f32(&mO1, gp.dWu, h, g, El);
+      break;
     default:  // GK_DX
       p.N = gp.h; p.K = 2 * gp.g;
       ok &= map_fp8_2d(&mA, gp.mx_a.q, 2 * g, R);
@@ -1511,7 +1569,8 @@ int launch_mx(const GemmProblem<__nv_bfloat16>& gp, cudaStream_t st) {
       mO1 = mO0;
       break;
   }
-  ok &= map_sf(&mSA, gp.mx_a.sf, (R / 128) * (uint64_t)(p.K / 128));
+  ok &= map_sf(&mSA, gp.mx_a.sf,
+                KIND >= GK_WGRAD_DOWN ? (uint64_t)(p.M / 128) * (R / 128) : (R / 128) * (uint64_t)(p.K / 128));
   if (!ok) return -1;
   constexpr int BN = CfgX<KIND, true>::BN;
   int nt = (p.N + BN - 1) / BN;
@@ -1521,14 +1580,22 @@ int launch_mx(const GemmProblem<__nv_bfloat16>& gp, cudaStream_t st) {
       const char* s = getenv("MEMFINE_L2_GROUP_MB");
       return s ? (int64_t)atoi(s) << 20 : (int64_t)-1;
     }();
-    constexpr int64_t kind_mb = (KIND == GK_DOWN || KIND == GK_DX) ? 8 : 24;
+    constexpr int64_t kind_mb = (KIND == GK_DOWN || KIND == GK_DX || KIND == GK_WGRAD_GU) ? 8
+                                : KIND == GK_WGRAD_DOWN ? 48 : 24;
     const int64_t budget = env_budget > 0 ? env_budget : kind_mb << 20;
-    int64_t a_strip = (int64_t)(PAIR ? 2 : 1) * BM * p.K;   // E4M3: one byte per element
+    const int64_t kdim = KIND >= GK_WGRAD_DOWN ? std::max<int64_t>(1, (int64_t)(R / El)) : p.K;
+    int64_t a_strip = (int64_t)(PAIR ? 2 : 1) * BM * kdim;   // E4M3: one byte per element
     p.group_m = (int)std::max<int64_t>(1, std::min<int64_t>(64, budget / a_strip));
   }
   if (setup_pacing(p, gp, st)) return -1;
   const int per_unit = PAIR ? 2 : 1;
-  int64_t max_tiles = (int64_t)((R / BM + (PAIR ? El : 0)) / per_unit + 1) * nt;
+  int64_t max_tiles;
+  if (KIND >= GK_WGRAD_DOWN) {
+    p.num_mt_w = (p.M + (PAIR ? 2 : 1) * BM - 1) / ((PAIR ? 2 : 1) * BM);
+    max_tiles = (int64_t)p.El * p.num_mt_w * nt;
+  } else {
+    max_tiles = (int64_t)((R / BM + (PAIR ? El : 0)) / per_unit + 1) * nt;
+  }
   const int sms = gp.sm_limit > 0 ? std::min(gp.sm_limit, g_num_sms) : g_num_sms;
   int units = (int)std::min<int64_t>(max_tiles, sms / per_unit);
   if (units <= 0) return 0;
@@ -1563,7 +1630,9 @@ int launch_gemm_sm100(const GemmProblem<__nv_bfloat16>& p, cudaStream_t st) {
       case GK_GATEUP: return sm100::launch_mx_kind<GK_GATEUP>(p, st);
       case GK_DOWN: return sm100::launch_mx_kind<GK_DOWN>(p, st);
       case GK_DX: return sm100::launch_mx_kind<GK_DX>(p, st);
-      default: break;   // dA and the weight gradients stay BF16 (reading R28)
+      case GK_WGRAD_DOWN: return sm100::launch_mx_kind<GK_WGRAD_DOWN>(p, st);   // reading R28c
+      case GK_WGRAD_GU: return sm100::launch_mx_kind<GK_WGRAD_GU>(p, st);
+      default: break;   // dA stays BF16 (reading R28)
     }
   }
   switch (p.kind) {

@@ -170,6 +170,20 @@ int sm100_num_sms();
 // Rows and K multiples of 128 (scale chunks).
 void launch_mx_quant_rows(const __nv_bfloat16* src, int64_t ld, int64_t rows_max, const int* info, int K,
                           uint8_t* q, uint8_t* sf, cudaStream_t st);
+// columnwise (R28c): per tensor, src [rows][Cc] (ld; rows = info's padded rows) -> q_t [Cc][Rcap]
+// blocked along the rows, with scales; up to 4 tensors in one launch
+struct MxColTensor {
+  const __nv_bfloat16* src;
+  int64_t ld;
+  int Cc;
+  uint8_t* q_t;
+  uint8_t* sf_t;
+};
+struct MxColTensors {
+  MxColTensor t[4];
+  int n;
+};
+void launch_mx_quant_t(const MxColTensors& tz, const int* info, int64_t Rcap, cudaStream_t st);
 // src [B][R][Cc] -> q_rows [B][R][Cc] blocked along Cc and q_t [B][Cc][R] blocked along R, one read
 void launch_mx_quant_dual(const __nv_bfloat16* src, int B, int R, int Cc, uint8_t* q_rows, uint8_t* sf_rows,
                           uint8_t* q_t, uint8_t* sf_t, cudaStream_t st);

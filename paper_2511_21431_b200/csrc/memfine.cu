@@ -126,8 +126,11 @@ bool dims_ok(const memfine_dims* d) {
   if (d->num_experts > 1024) return false;
   if (d->dtype != MEMFINE_BF16 && d->dtype != MEMFINE_FP32 && d->dtype != MEMFINE_MXFP8) return false;
   if (d->dtype == MEMFINE_MXFP8 && (d->hidden % 128 || d->ffn % 128)) return false;
-  if (d->flags & ~(MEMFINE_FLAG_OVERLAP | MEMFINE_FLAG_EP_PATH)) return false;
+  if (d->flags & ~(MEMFINE_FLAG_OVERLAP | MEMFINE_FLAG_EP_PATH | MEMFINE_FLAG_MX_WGRAD)) return false;
   if ((d->flags & MEMFINE_FLAG_EP_PATH) && d->ep_size != 1) return false;
+  if ((d->flags & MEMFINE_FLAG_MX_WGRAD) &&
+      (d->dtype != MEMFINE_MXFP8 || d->ep_size != 1 || (d->flags & MEMFINE_FLAG_EP_PATH)))
+    return false;
   return true;
 }
 
@@ -166,6 +169,7 @@ struct Layout {
   // MXFP8 operands (E4M3 codes + scale chunks): X, a (fwd) / X, dG||dU (bwd)
   uint8_t *Xq = nullptr, *Xsf = nullptr, *Aq = nullptr, *Asf = nullptr;
   uint8_t *GUq = nullptr, *GUsf = nullptr;
+  uint8_t *DYt = nullptr, *DYtsf = nullptr, *GUt = nullptr, *GUtsf = nullptr, *At = nullptr, *Atsf = nullptr;
   int64_t rows_cap = 0;
   uint64_t meta_bytes = 0, row_bytes = 0, total = 0;
 };
@@ -181,9 +185,10 @@ uint64_t row_bytes_of(const memfine_dims& d, int pass, int slots = 1) {
   if (d.dtype == MEMFINE_MXFP8) {
     // fwd: x gathered straight to Xq + scales, a straight to Aq + scales, O (bf16)
     if (pass == MEMFINE_FWD) return ep + 8 + (h + h / 32) + (g + g / 32) + D * h;
-    // bwd: bf16 X, dY, G||U, a_w (dA and the weight gradients stay BF16) + Xq, dGUq with scales;
-    // O aliases X
-    return ep + 12 + D * (h + h + 2 * g + g) + (h + h / 32) + (2 * g + 2 * g / 32);
+    // bwd: bf16 X, dY, G||U, a_w (dA stays BF16) + Xq, dGUq with scales; O aliases X.  MX_WGRAD:
+    // + the columnwise codes of dY, dG || dU and a_w (x's reuse Xq, dead after the recompute)
+    const uint64_t wg = (d.flags & MEMFINE_FLAG_MX_WGRAD) ? (h + h / 32) + (3 * g + 3 * g / 32) : 0;
+    return ep + 12 + D * (h + h + 2 * g + g) + (h + h / 32) + (2 * g + 2 * g / 32) + wg;
   }
   if (slots == 2) {
     // per slot: src_of, w_row, row addresses, (bwd: dw_row, dY_disp), X_disp (o / dX_disp written
@@ -273,6 +278,14 @@ Layout carve(const memfine_dims& d, int C, int pass, void* ws, int64_t rows_cap,
         L.A = b.take<char>((uint64_t)R * gg * D);
         L.GUq = b.take<uint8_t>((uint64_t)R * 2 * gg);
         L.GUsf = b.take<uint8_t>((uint64_t)R * 2 * gg / 32);
+        if (d.flags & MEMFINE_FLAG_MX_WGRAD) {   // columnwise codes [cols][R] (reading R28c)
+          L.DYt = b.take<uint8_t>((uint64_t)R * hh);
+          L.DYtsf = b.take<uint8_t>((uint64_t)R * hh / 32);
+          L.GUt = b.take<uint8_t>((uint64_t)R * 2 * gg);
+          L.GUtsf = b.take<uint8_t>((uint64_t)R * 2 * gg / 32);
+          L.At = b.take<uint8_t>((uint64_t)R * gg);
+          L.Atsf = b.take<uint8_t>((uint64_t)R * gg / 32);
+        }
         L.O = L.X;
       } else {
         L.Aq = b.take<uint8_t>((uint64_t)R * gg);
@@ -578,10 +591,35 @@ memfine_status bwd_ep1(memfine_handle_s* h, const T* dy, const T* x, const int32
     p.mx_gq_sf = nullptr;
     // B5: weight gradients accumulate across chunks (reading R18)
     p.wgrad_beta = beta;
-    p.kind = GK_WGRAD_DOWN;
-    if (int rc = run_gemm<T>(h, p, st)) return (memfine_status)rc;
-    p.kind = GK_WGRAD_GU;
-    if (int rc = run_gemm<T>(h, p, st)) return (memfine_status)rc;
+    if constexpr (std::is_same<T, __nv_bfloat16>::value) {
+      if (mx && (d.flags & MEMFINE_FLAG_MX_WGRAD)) {
+        // reading R28c: columnwise MXFP8 codes of x (into Xq: dead after the recompute), dY,
+        // dG || dU and a_w, then block-scaled weight-gradient GEMMs over them
+        prof_begin(h, 10, st);
+        MxColTensors tz{};
+        tz.t[0] = {(const __nv_bfloat16*)L.X, hd, hd, L.Xq, L.Xsf};
+        tz.t[1] = {(const __nv_bfloat16*)L.DY, hd, hd, L.DYt, L.DYtsf};
+        tz.t[2] = {(const __nv_bfloat16*)L.GU, 2 * g, 2 * g, L.GUt, L.GUtsf};
+        tz.t[3] = {(const __nv_bfloat16*)L.A, g, g, L.At, L.Atsf};
+        tz.n = 4;
+        launch_mx_quant_t(tz, L.m.info, R, st);
+        prof_end(h, st);
+        h->last.kernel_launches += 1;
+        p.kind = GK_WGRAD_DOWN;
+        set_mx(p, {L.DYt, L.DYtsf}, {L.At, L.Atsf}, {L.At, L.Atsf});
+        if (int rc = run_gemm<T>(h, p, st)) return (memfine_status)rc;
+        p.kind = GK_WGRAD_GU;
+        set_mx(p, {L.GUt, L.GUtsf}, {L.Xq, L.Xsf}, {L.Xq, L.Xsf});
+        if (int rc = run_gemm<T>(h, p, st)) return (memfine_status)rc;
+        p.mx = 0;
+      }
+    }
+    if (!(mx && (d.flags & MEMFINE_FLAG_MX_WGRAD))) {
+      p.kind = GK_WGRAD_DOWN;
+      if (int rc = run_gemm<T>(h, p, st)) return (memfine_status)rc;
+      p.kind = GK_WGRAD_GU;
+      if (int rc = run_gemm<T>(h, p, st)) return (memfine_status)rc;
+    }
     beta = 1;
     // B4: dX_disp = dG W_gate + dU W_up (overwrites X_disp, dead after B5)
     p.kind = GK_DX;

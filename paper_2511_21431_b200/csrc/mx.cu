@@ -99,6 +99,62 @@ __global__ void __launch_bounds__(256) mx_quant_dual_kernel(const __nv_bfloat16*
   }
 }
 
+// Columnwise ("transposed") quantisation of a chunk's activation rows for the MXFP8 weight
+// gradients (reading R28c): per tensor z, src [rows][Cc] bf16 (row stride ld; rows = the chunk's
+// padded rows from info) -> q_t [Cc][Rcap] E4M3 blocked along the rows (K = the copies), scales at
+// mx_sf_off(col, row / 32, Rcap).  Expert segments start at multiples of 128 rows, so every 32-row
+// block lies inside one segment (its padding rows are zero).  One launch for all tensors
+// (blockIdx.z); tile 128 x 128 through smem; a warp quantises 32 adjacent columns of one 32-row
+// block (conflict-free shared-memory reads along a row).
+__global__ void __launch_bounds__(256) mx_quant_t_kernel(MxColTensors tz, const int* __restrict__ info, int64_t Rcap) {
+  const MxColTensor& tt = tz.t[blockIdx.z];
+  if (blockIdx.z >= (unsigned)tz.n || (int)blockIdx.x * 128 >= tt.Cc) return;
+  const int64_t rows = __ldg(info + kInfoSkip) ? 0 : min(Rcap, (int64_t)__ldg(info + kInfoRowsPad));
+  const int64_t r0 = (int64_t)blockIdx.y * 128;
+  const int c0 = blockIdx.x * 128;
+  if (r0 >= rows) return;
+  __shared__ __nv_bfloat16 t[128][128 + 8];
+  const __nv_bfloat16* src = tt.src;
+#pragma unroll
+  for (int pass = 0; pass < 8; pass++) {
+    const int idx = pass * 256 + threadIdx.x;    // 16 x uint4 per row
+    const int rr = idx >> 4, cc = (idx & 15) * 8;
+    *reinterpret_cast<uint4*>(&t[rr][cc]) = *reinterpret_cast<const uint4*>(src + (r0 + rr) * tt.ld + c0 + cc);
+  }
+  __syncthreads();
+  const int col = threadIdx.x & 127;             // a column of the tile
+#pragma unroll
+  for (int k2 = 0; k2 < 2; k2++) {
+    const int kb = (threadIdx.x >> 7) * 2 + k2;  // 32-row block 0..3 of the tile
+    float v[32];
+    float amax = 0.f;
+#pragma unroll
+    for (int i = 0; i < 32; i++) {
+      v[i] = __bfloat162float(t[32 * kb + i][col]);
+      amax = fmaxf(amax, fabsf(v[i]));
+    }
+    const int E = mx_exp(amax);
+    const float inv = mx_inv_scale(E);
+    uint32_t o[8];
+#pragma unroll
+    for (int j = 0; j < 8; j++)
+      o[j] = mx_e4m3x2(v[4 * j] * inv, v[4 * j + 1] * inv) | (mx_e4m3x2(v[4 * j + 2] * inv, v[4 * j + 3] * inv) << 16);
+    const int64_t gc = c0 + col;
+    uint4* q = reinterpret_cast<uint4*>(tt.q_t + gc * Rcap + r0 + 32 * kb);
+    q[0] = make_uint4(o[0], o[1], o[2], o[3]);
+    q[1] = make_uint4(o[4], o[5], o[6], o[7]);
+    tt.sf_t[mx_sf_off(gc, (r0 >> 5) + kb, Rcap)] = (uint8_t)(E + 127);
+  }
+}
+
+void launch_mx_quant_t(const MxColTensors& tz, const int* info, int64_t Rcap, cudaStream_t st) {
+  int cmax = 0;
+  for (int i = 0; i < tz.n; i++) cmax = std::max(cmax, tz.t[i].Cc);
+  if (cmax <= 0 || Rcap <= 0 || tz.n <= 0) return;
+  dim3 grid((unsigned)(cmax / 128), (unsigned)(Rcap / 128), (unsigned)tz.n);
+  mx_quant_t_kernel<<<grid, 256, 0, st>>>(tz, info, Rcap);
+}
+
 void launch_mx_quant_dual(const __nv_bfloat16* src, int B, int R, int Cc, uint8_t* q_rows, uint8_t* sf_rows,
                           uint8_t* q_t, uint8_t* sf_t, cudaStream_t st) {
   if (B <= 0 || R <= 0 || Cc <= 0) return;

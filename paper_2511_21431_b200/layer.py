@@ -26,15 +26,17 @@ def _stream(stream=None):
 
 
 def make_dims(tokens, hidden, ffn, num_experts, topk, ep_size=1, ep_rank=0, dtype=torch.bfloat16,
-              mx: bool = False, overlap: bool = False, ep_path: bool = False) -> capi.Dims:
+              mx: bool = False, overlap: bool = False, ep_path: bool = False, mx_wgrad: bool = False) -> capi.Dims:
     """mx=True: MEMFINE_MXFP8 (bf16 storage, MXFP8 expert-GEMM operands; dtype must be bf16).
     overlap=True: MEMFINE_FLAG_OVERLAP (EP > 1, C > 1: exchange of chunk j+-1 on a comm stream
     while chunk j's GEMMs run; two slots of exchanged rows in the workspace).
-    ep_path=True (ep_size == 1): MEMFINE_FLAG_EP_PATH, the EP data path over a 1-rank NCCL comm."""
+    ep_path=True (ep_size == 1): MEMFINE_FLAG_EP_PATH, the EP data path over a 1-rank NCCL comm.
+    mx_wgrad=True (mx, ep_size == 1): MEMFINE_FLAG_MX_WGRAD, MXFP8 weight gradients (reading R28c)."""
     assert not mx or dtype == torch.bfloat16
     return capi.Dims(int(tokens), int(hidden), int(ffn), int(num_experts), int(topk), int(ep_size), int(ep_rank),
                      capi.MXFP8 if mx else _DT[dtype],
-                     (capi.FLAG_OVERLAP if overlap else 0) | (capi.FLAG_EP_PATH if ep_path else 0))
+                     (capi.FLAG_OVERLAP if overlap else 0) | (capi.FLAG_EP_PATH if ep_path else 0) |
+                     (capi.FLAG_MX_WGRAD if mx_wgrad else 0))
 
 
 def mx_weights_bytes(dims: capi.Dims) -> int:
@@ -111,8 +113,9 @@ class MemFine:
 
     def __init__(self, tokens, hidden, ffn, num_experts, topk, ep_size=1, ep_rank=0, dtype=torch.bfloat16,
                  process_group=None, local_group=None, mx: bool = False, overlap: bool = False,
-                 ep_path: bool = False):
-        self.dims = make_dims(tokens, hidden, ffn, num_experts, topk, ep_size, ep_rank, dtype, mx, overlap, ep_path)
+                 ep_path: bool = False, mx_wgrad: bool = False):
+        self.dims = make_dims(tokens, hidden, ffn, num_experts, topk, ep_size, ep_rank, dtype, mx, overlap, ep_path,
+                              mx_wgrad)
         self.dtype = dtype
         self.mx = mx
         self._wq = None

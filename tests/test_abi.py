@@ -25,7 +25,7 @@ def test_exports_every_declared_symbol(L):
     assert declared == set(capi.SYMBOLS)
     for name in declared:
         assert hasattr(L, name), name
-    assert L.memfine_abi_version() == 1
+    assert L.memfine_abi_version() == 2
     for s in range(8):
         assert capi.status_str(s)
 
@@ -161,7 +161,11 @@ def test_workspace_bytes_overlap_slots():
                 assert 0 < meta0 < meta1 <= 2 * meta0 + 256, (C_, pass_, r, meta0, meta1)
     out = C.c_uint64()
     bad = layer.make_dims(T, h, g, E, k)
-    bad.flags = 4   # unknown flag
+    bad.flags = 1 << 10   # unknown flag
+    assert capi.lib().memfine_workspace_bytes(None, 0, C.byref(bad), 1, 0, C.byref(out)) == capi.ERR_INVALID_ARG
+    bad = layer.make_dims(T, h, g, E, k, mx_wgrad=True)             # MX_WGRAD needs the MXFP8 dtype
+    assert capi.lib().memfine_workspace_bytes(None, 0, C.byref(bad), 1, 0, C.byref(out)) == capi.ERR_INVALID_ARG
+    bad = layer.make_dims(T, h, g, E, k, ep_size=2, mx=True, mx_wgrad=True)   # ... and EP = 1
     assert capi.lib().memfine_workspace_bytes(None, 0, C.byref(bad), 1, 0, C.byref(out)) == capi.ERR_INVALID_ARG
     bad = layer.make_dims(T, h, g, E, k, ep_size=2, ep_path=True)   # EP_PATH is for ep_size == 1
     assert capi.lib().memfine_workspace_bytes(None, 0, C.byref(bad), 1, 0, C.byref(out)) == capi.ERR_INVALID_ARG

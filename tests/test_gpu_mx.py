@@ -61,12 +61,12 @@ def _mx_run(p, C, **mf_kw):
                 dwg=dwg.cpu().numpy(), dwu=dwu.cpu().numpy(), dwd=dwd.cpu().numpy())
 
 
-def _mx_oracle(p):
+def _mx_oracle(p, wgrad_C=0):
     d = oracle_dims(p)
     a = [_np_in(t, p.dtype) for t in (p.x, p.dy, p.wg, p.wu, p.wd)]
     ids, w = p.ids.numpy(), p.w.numpy().astype(np.float64)
     wq = oracle.mx_weights(d, a[2], a[3], a[4])
-    y, dx, ds, dwg, dwu, dwd = oracle.moe_mx(d, a[0], ids, w, wq, dy=a[1], wd=a[4])
+    y, dx, ds, dwg, dwu, dwd = oracle.moe_mx(d, a[0], ids, w, wq, dy=a[1], wd=a[4], wgrad_C=wgrad_C)
     exact_y = oracle.moe_forward(d, a[0], ids, w, a[2], a[3], a[4])
     return dict(y=y, dx=dx, dscore=ds, dwg=dwg, dwu=dwu, dwd=dwd), exact_y
 
@@ -118,3 +118,22 @@ def test_mx_nccl_ep_path_bit_identical(C):
             assert rel_err(b[key], a[key]) <= 1e-6
         else:
             np.testing.assert_array_equal(a[key], b[key], err_msg=key)
+
+
+@pytest.mark.parametrize("T,h,g,E,k,C,zipf", [(300, 256, 384, 4, 2, 1, 0.0), (700, 384, 640, 8, 2, 3, 1.2),
+                                              (2048, 256, 256, 4, 2, 2, 1.2)])
+def test_mx_wgrad_matches_mx_oracle(T, h, g, E, k, C, zipf):
+    """MEMFINE_FLAG_MX_WGRAD (reading R28c): the weight gradients from columnwise MXFP8 operands -
+    blocks of 32 copies of an expert inside a chunk - against the oracle's definition of exactly
+    that (oracle.moe_mx(wgrad_C=C)); every other output is the MX variant's as before."""
+    p = make_problem(T, h, g, E, k, zipf_s=zipf, seed=37)
+    got = _mx_run(p, C, mx_wgrad=True)
+    ref, _ = _mx_oracle(p, wgrad_C=C)
+    ref_bf16w, _ = _mx_oracle(p, wgrad_C=0)
+    errs = {key: rel_err(got[key], ref[key]) for key in ("y", "dx", "dscore", "dwg", "dwu", "dwd")}
+    print("mx-wgrad vs oracle", {k_: f"{v:.2e}" for k_, v in errs.items()})
+    for key, e in errs.items():
+        assert e <= MX_TOL, f"{key}: {e}"
+    # the gradients really are quantised: closer to the MX-wgrad definition than to BF16 operands
+    for key in ("dwg", "dwu", "dwd"):
+        assert rel_err(got[key], ref[key]) < 0.5 * rel_err(got[key], ref_bf16w[key]), key
