@@ -122,29 +122,33 @@ __global__ void __launch_bounds__(256) mx_quant_t_kernel(MxColTensors tz, const 
     *reinterpret_cast<uint4*>(&t[rr][cc]) = *reinterpret_cast<const uint4*>(src + (r0 + rr) * tt.ld + c0 + cc);
   }
   __syncthreads();
-  const int col = threadIdx.x & 127;             // a column of the tile
+  // thread = (column pair, 32-row block): 64 pairs x 4 blocks; a warp reads 32 adjacent bf16x2 words
+  // of one row per step (conflict-free) and quantises two column blocks at once
+  const int cp = threadIdx.x & 63, kb = threadIdx.x >> 6;
+  float v0[32], v1[32];
+  float a0 = 0.f, a1 = 0.f;
 #pragma unroll
-  for (int k2 = 0; k2 < 2; k2++) {
-    const int kb = (threadIdx.x >> 7) * 2 + k2;  // 32-row block 0..3 of the tile
-    float v[32];
-    float amax = 0.f;
-#pragma unroll
-    for (int i = 0; i < 32; i++) {
-      v[i] = __bfloat162float(t[32 * kb + i][col]);
-      amax = fmaxf(amax, fabsf(v[i]));
-    }
+  for (int i = 0; i < 32; i++) {
+    const uint32_t u = *reinterpret_cast<const uint32_t*>(&t[32 * kb + i][2 * cp]);
+    v0[i] = __uint_as_float(u << 16);
+    v1[i] = __uint_as_float(u & 0xFFFF0000u);
+    a0 = fmaxf(a0, fabsf(v0[i]));
+    a1 = fmaxf(a1, fabsf(v1[i]));
+  }
+  auto emit = [&](const float (&v)[32], float amax, int64_t gc) {
     const int E = mx_exp(amax);
     const float inv = mx_inv_scale(E);
     uint32_t o[8];
 #pragma unroll
     for (int j = 0; j < 8; j++)
       o[j] = mx_e4m3x2(v[4 * j] * inv, v[4 * j + 1] * inv) | (mx_e4m3x2(v[4 * j + 2] * inv, v[4 * j + 3] * inv) << 16);
-    const int64_t gc = c0 + col;
     uint4* q = reinterpret_cast<uint4*>(tt.q_t + gc * Rcap + r0 + 32 * kb);
     q[0] = make_uint4(o[0], o[1], o[2], o[3]);
     q[1] = make_uint4(o[4], o[5], o[6], o[7]);
     tt.sf_t[mx_sf_off(gc, (r0 >> 5) + kb, Rcap)] = (uint8_t)(E + 127);
-  }
+  };
+  emit(v0, a0, c0 + 2 * cp);
+  emit(v1, a1, c0 + 2 * cp + 1);
 }
 
 void launch_mx_quant_t(const MxColTensors& tz, const int* info, int64_t Rcap, cudaStream_t st) {
