@@ -97,7 +97,7 @@ typedef struct {
  *    1-rank NCCL communicator, every segment (including the self segment) through ncclSend /
  *    ncclRecv.  memfine_create then takes a unique id.  Results equal the EP = 1 path; this is
  *    how the NCCL transport is exercised on a single GPU (NCCL refuses two ranks on one device).
- *  MEMFINE_FLAG_MX_WGRAD (dtype MEMFINE_MXFP8, ep_size == 1, no EP_PATH): the weight-gradient
+ *  MEMFINE_FLAG_MX_WGRAD (dtype MEMFINE_MXFP8; EP copy transport): the weight-gradient
  *    GEMMs also take MXFP8 operands - x, dY, dG || dU and a_w quantised columnwise (blocks of 32
  *    copies of an expert within a chunk, reading R28c) - instead of BF16 ones.  Adds the
  *    columnwise codes to the backward workspace ((h + 3g) * 33/32 bytes per row). */

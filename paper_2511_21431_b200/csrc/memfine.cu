@@ -128,9 +128,7 @@ bool dims_ok(const memfine_dims* d) {
   if (d->dtype == MEMFINE_MXFP8 && (d->hidden % 128 || d->ffn % 128)) return false;
   if (d->flags & ~(MEMFINE_FLAG_OVERLAP | MEMFINE_FLAG_EP_PATH | MEMFINE_FLAG_MX_WGRAD)) return false;
   if ((d->flags & MEMFINE_FLAG_EP_PATH) && d->ep_size != 1) return false;
-  if ((d->flags & MEMFINE_FLAG_MX_WGRAD) &&
-      (d->dtype != MEMFINE_MXFP8 || d->ep_size != 1 || (d->flags & MEMFINE_FLAG_EP_PATH)))
-    return false;
+  if ((d->flags & MEMFINE_FLAG_MX_WGRAD) && d->dtype != MEMFINE_MXFP8) return false;
   return true;
 }
 
@@ -472,6 +470,41 @@ void set_mx(GemmProblem<__nv_bfloat16>& p, const MxOp& a, const MxOp& b0, const 
   p.mx_b1 = b1;
 }
 
+// B5: the chunk's weight-gradient GEMMs (W_grad = sum over chunks, reading R18; p.wgrad_beta set by
+// the caller).  MEMFINE_FLAG_MX_WGRAD (reading R28c): one launch writes the columnwise E4M3 codes of
+// x (into Xq: dead after the recompute), dY, dG || dU and a_w, then block-scaled GEMMs over them.
+template <typename T>
+int run_wgrad(memfine_handle_s* h, GemmProblem<T>& p, const Layout& L, cudaStream_t st) {
+  if constexpr (std::is_same<T, __nv_bfloat16>::value) {
+    const memfine_dims& d = h->d;
+    if (d.dtype == MEMFINE_MXFP8 && (d.flags & MEMFINE_FLAG_MX_WGRAD)) {
+      const int hd = d.hidden, g = d.ffn;
+      prof_begin(h, 10, st);
+      MxColTensors tz{};
+      tz.t[0] = {(const __nv_bfloat16*)L.X, hd, hd, L.Xq, L.Xsf};
+      tz.t[1] = {(const __nv_bfloat16*)L.DY, hd, hd, L.DYt, L.DYtsf};
+      tz.t[2] = {(const __nv_bfloat16*)L.GU, 2 * g, 2 * g, L.GUt, L.GUtsf};
+      tz.t[3] = {(const __nv_bfloat16*)L.A, g, g, L.At, L.Atsf};
+      tz.n = 4;
+      launch_mx_quant_t(tz, L.m.info, L.rows_cap, st);
+      prof_end(h, st);
+      h->last.kernel_launches += 1;
+      p.kind = GK_WGRAD_DOWN;
+      set_mx(p, {L.DYt, L.DYtsf}, {L.At, L.Atsf}, {L.At, L.Atsf});
+      if (int rc = run_gemm<T>(h, p, st)) return rc;
+      p.kind = GK_WGRAD_GU;
+      set_mx(p, {L.GUt, L.GUtsf}, {L.Xq, L.Xsf}, {L.Xq, L.Xsf});
+      if (int rc = run_gemm<T>(h, p, st)) return rc;
+      p.mx = 0;
+      return 0;
+    }
+  }
+  p.kind = GK_WGRAD_DOWN;
+  if (int rc = run_gemm<T>(h, p, st)) return rc;
+  p.kind = GK_WGRAD_GU;
+  return run_gemm<T>(h, p, st);
+}
+
 // ------------------------------------------------------------------ the FCDA chunk loops (EP = 1)
 template <typename T>
 memfine_status fwd_ep1(memfine_handle_s* h, const T* x, const int32_t* ids, const float* w, const void* wg,
@@ -591,35 +624,7 @@ memfine_status bwd_ep1(memfine_handle_s* h, const T* dy, const T* x, const int32
     p.mx_gq_sf = nullptr;
     // B5: weight gradients accumulate across chunks (reading R18)
     p.wgrad_beta = beta;
-    if constexpr (std::is_same<T, __nv_bfloat16>::value) {
-      if (mx && (d.flags & MEMFINE_FLAG_MX_WGRAD)) {
-        // reading R28c: columnwise MXFP8 codes of x (into Xq: dead after the recompute), dY,
-        // dG || dU and a_w, then block-scaled weight-gradient GEMMs over them
-        prof_begin(h, 10, st);
-        MxColTensors tz{};
-        tz.t[0] = {(const __nv_bfloat16*)L.X, hd, hd, L.Xq, L.Xsf};
-        tz.t[1] = {(const __nv_bfloat16*)L.DY, hd, hd, L.DYt, L.DYtsf};
-        tz.t[2] = {(const __nv_bfloat16*)L.GU, 2 * g, 2 * g, L.GUt, L.GUtsf};
-        tz.t[3] = {(const __nv_bfloat16*)L.A, g, g, L.At, L.Atsf};
-        tz.n = 4;
-        launch_mx_quant_t(tz, L.m.info, R, st);
-        prof_end(h, st);
-        h->last.kernel_launches += 1;
-        p.kind = GK_WGRAD_DOWN;
-        set_mx(p, {L.DYt, L.DYtsf}, {L.At, L.Atsf}, {L.At, L.Atsf});
-        if (int rc = run_gemm<T>(h, p, st)) return (memfine_status)rc;
-        p.kind = GK_WGRAD_GU;
-        set_mx(p, {L.GUt, L.GUtsf}, {L.Xq, L.Xsf}, {L.Xq, L.Xsf});
-        if (int rc = run_gemm<T>(h, p, st)) return (memfine_status)rc;
-        p.mx = 0;
-      }
-    }
-    if (!(mx && (d.flags & MEMFINE_FLAG_MX_WGRAD))) {
-      p.kind = GK_WGRAD_DOWN;
-      if (int rc = run_gemm<T>(h, p, st)) return (memfine_status)rc;
-      p.kind = GK_WGRAD_GU;
-      if (int rc = run_gemm<T>(h, p, st)) return (memfine_status)rc;
-    }
+    if (int rc = run_wgrad<T>(h, p, L, st)) return (memfine_status)rc;
     beta = 1;
     // B4: dX_disp = dG W_gate + dU W_up (overwrites X_disp, dead after B5)
     p.kind = GK_DX;
@@ -1129,10 +1134,7 @@ memfine_status ep_run(memfine_handle_s* h, int pass, const T* dy, const T* x, co
       p.mx_gq = nullptr;
       p.mx_gq_sf = nullptr;
       p.wgrad_beta = beta;
-      p.kind = GK_WGRAD_DOWN;
-      if (int rc = run_gemm<T>(h, p, st)) return (memfine_status)rc;
-      p.kind = GK_WGRAD_GU;
-      if (int rc = run_gemm<T>(h, p, st)) return (memfine_status)rc;
+      if (int rc = run_wgrad<T>(h, p, L, st)) return (memfine_status)rc;
       beta = 1;
       p.kind = GK_DX;
       if constexpr (std::is_same<T, __nv_bfloat16>::value)

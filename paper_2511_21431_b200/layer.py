@@ -31,7 +31,7 @@ def make_dims(tokens, hidden, ffn, num_experts, topk, ep_size=1, ep_rank=0, dtyp
     overlap=True: MEMFINE_FLAG_OVERLAP (EP > 1, C > 1: exchange of chunk j+-1 on a comm stream
     while chunk j's GEMMs run; two slots of exchanged rows in the workspace).
     ep_path=True (ep_size == 1): MEMFINE_FLAG_EP_PATH, the EP data path over a 1-rank NCCL comm.
-    mx_wgrad=True (mx, ep_size == 1): MEMFINE_FLAG_MX_WGRAD, MXFP8 weight gradients (reading R28c)."""
+    mx_wgrad=True (mx): MEMFINE_FLAG_MX_WGRAD, MXFP8 weight gradients (reading R28c)."""
     assert not mx or dtype == torch.bfloat16
     return capi.Dims(int(tokens), int(hidden), int(ffn), int(num_experts), int(topk), int(ep_size), int(ep_rank),
                      capi.MXFP8 if mx else _DT[dtype],

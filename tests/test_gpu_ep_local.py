@@ -27,7 +27,7 @@ def _bits(t, dtype):
         t.contiguous().numpy().astype(np.float32)
 
 
-def _run_group(EP, C, dtype, transport, xs, dys, routes, wg, wu, wd, T, h, g, E, k, mx=False):
+def _run_group(EP, C, dtype, transport, xs, dys, routes, wg, wu, wd, T, h, g, E, k, mx=False, mx_wgrad=False):
     """Every rank of an in-process EP group: fwd + bwd; returns (per-rank outputs, counts seen)."""
     El = E // EP
     group = layer.LocalGroup(EP)
@@ -41,7 +41,7 @@ def _run_group(EP, C, dtype, transport, xs, dys, routes, wg, wu, wd, T, h, g, E,
             with torch.cuda.stream(st):
                 ov = transport == "overlap"
                 mf = layer.MemFine(T, h, g, E, k, ep_size=EP, ep_rank=r, dtype=dtype, local_group=group, overlap=ov,
-                                   mx=mx)
+                                   mx=mx, mx_wgrad=mx_wgrad)
                 mf.set_ep_transport(capi.EP_COPY if ov else transport)
                 if ov:
                     mf.set_comm_sms(16)
@@ -156,6 +156,38 @@ def test_ep_local_group_mx_matches_mx_oracle(EP, C):
     W = [_bits(t, dtype) for t in (wg, wu, wd)]
     wq = oracle.mx_weights(d, *W)
     y_ref, dx_ref, ds_ref, dwg_ref, dwu_ref, dwd_ref = oracle.moe_mx(d, xa, ida, wa, wq, dy=dya, wd=W[2])
+    for r in range(EP):
+        y, dx, ds, dwg, dwu, dwd = results[r]
+        sl, es = slice(r * T, (r + 1) * T), slice(r * El, (r + 1) * El)
+        errs = {"y": rel_err(y, y_ref[sl]), "dx": rel_err(dx, dx_ref[sl]), "dscore": rel_err(ds, ds_ref[sl]),
+                "dw_gate": rel_err(dwg, dwg_ref[es]), "dw_up": rel_err(dwu, dwu_ref[es]),
+                "dw_down": rel_err(dwd, dwd_ref[es])}
+        assert all(v <= MX_TOL for v in errs.values()), (r, errs)
+
+
+@pytest.mark.parametrize("EP,C", [(2, 1), (2, 3), (4, 2)])
+def test_ep_local_group_mx_wgrad_matches_oracle(EP, C):
+    """MXFP8 weight gradients with EP (reading R28c): each rank's K for its local expert e is the
+    chunk's copies in (src rank, token, slot) order - the received expert-major layout - quantised
+    columnwise in 32-copy blocks; against the oracle's definition over the EP ranks' chunks."""
+    from tests.test_gpu_mx import MX_TOL
+    T, h, g, E, k = 300, 256, 384, 8, 2
+    El = E // EP
+    dtype = torch.bfloat16
+    xs = [synth.make_x(T, h, rank=r, dtype=dtype) for r in range(EP)]
+    dys = [synth.make_dy(T, h, rank=r, dtype=dtype) for r in range(EP)]
+    routes = [synth.make_routing(T, E, k, rank=r, zipf_s=1.2, placement="contiguous") for r in range(EP)]
+    wg, wu, wd = synth.make_experts(range(E), h, g, dtype=dtype)
+    results, _ = _run_group(EP, C, dtype, capi.EP_COPY, xs, dys, routes, wg, wu, wd, T, h, g, E, k, mx=True,
+                            mx_wgrad=True)
+    d = oracle.Dims(T=T, h=h, g=g, E=E, k=k, EP=EP, in_dtype="bf16")
+    xa = np.concatenate([_bits(x, dtype) for x in xs])
+    dya = np.concatenate([_bits(x, dtype) for x in dys])
+    ida = np.concatenate([r[0] for r in routes])
+    wa = np.concatenate([r[1] for r in routes]).astype(np.float64)
+    W = [_bits(t, dtype) for t in (wg, wu, wd)]
+    wq = oracle.mx_weights(d, *W)
+    y_ref, dx_ref, ds_ref, dwg_ref, dwu_ref, dwd_ref = oracle.moe_mx(d, xa, ida, wa, wq, dy=dya, wd=W[2], wgrad_C=C)
     for r in range(EP):
         y, dx, ds, dwg, dwu, dwd = results[r]
         sl, es = slice(r * T, (r + 1) * T), slice(r * El, (r + 1) * El)

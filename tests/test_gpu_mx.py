@@ -104,15 +104,15 @@ def test_mx_errors():
         mf.mx_quantize_weights(g(p.wg), g(p.wu), g(p.wd), wq=small)
 
 
-@pytest.mark.parametrize("C", [1, 3])
-def test_mx_nccl_ep_path_bit_identical(C):
+@pytest.mark.parametrize("C,mx_wgrad", [(1, False), (3, False), (2, True)])
+def test_mx_nccl_ep_path_bit_identical(C, mx_wgrad):
     """MXFP8 over the NCCL transport (MEMFINE_FLAG_EP_PATH, 1-rank communicator): the rows travel
     in bf16 and are quantised on arrival - the same codes the EP = 1 gather writes - so every
     output equals the EP = 1 MX path bit for bit - except d_score, whose per-row partials from
     the dA GEMM's N tiles (g = 384: two) meet in an fp32 atomicAdd of run-dependent order."""
     p = make_problem(700, 256, 384, 8, 2, zipf_s=1.2, seed=5)
-    a = _mx_run(p, C)
-    b = _mx_run(p, C, ep_path=True)
+    a = _mx_run(p, C, mx_wgrad=mx_wgrad)
+    b = _mx_run(p, C, ep_path=True, mx_wgrad=mx_wgrad)
     for key in a:
         if key == "dscore":
             assert rel_err(b[key], a[key]) <= 1e-6
