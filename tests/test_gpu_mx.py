@@ -137,3 +137,20 @@ def test_mx_wgrad_matches_mx_oracle(T, h, g, E, k, C, zipf):
     # the gradients really are quantised: closer to the MX-wgrad definition than to BF16 operands
     for key in ("dwg", "dwu", "dwd"):
         assert rel_err(got[key], ref[key]) < 0.5 * rel_err(got[key], ref_bf16w[key]), key
+
+
+@pytest.mark.parametrize("C", [1, 2])
+def test_mx_wgrad_empty_expert_and_ragged_chunks(C):
+    """MX weight gradients with an expert that receives no copies (its dW tiles written as zeros by the
+    first chunk, skipped by the accumulating ones), an expert whose copies fall in one chunk only, and
+    chunks with ragged 32-copy blocks."""
+    T, E, k = 333, 6, 2
+    rng = np.random.default_rng(41)
+    ids = np.stack([rng.choice([0, 1, 2, 4], k, replace=False) for _ in range(T)]).astype(np.int32)  # 3, 5 empty
+    ids[T // 2:][ids[T // 2:] == 4] = 1          # expert 4 only in the first half of the tokens
+    p = make_problem(T, 256, 256, E, k, seed=43, ids=ids)
+    got = _mx_run(p, C, mx_wgrad=True)
+    ref, _ = _mx_oracle(p, wgrad_C=C)
+    for key in ("dwg", "dwu", "dwd"):
+        assert np.all(got[key][3] == 0) and np.all(got[key][5] == 0), key
+        assert rel_err(got[key], ref[key]) <= MX_TOL, key
