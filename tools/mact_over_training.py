@@ -64,6 +64,18 @@ def main():
                 dy = synth.make_dy(T, h, rank=r).to(dev)
                 f32 = dict(dtype=torch.float32, device=dev)
                 grads = [torch.zeros(t.shape, **f32) for t in (lwg, lwu, lwd)]
+                # warm-up (untimed): first launches of every kernel, tensor-map encodes, every C
+                ids_np, w_np = synth.make_routing(T, E, k, rank=r, zipf_s=skew(0, 0, L), placement="contiguous", seed=7)
+                ids, w = torch.from_numpy(ids_np).to(dev), torch.from_numpy(w_np).to(dev)
+                ch = mf.route_counts(ids, nsub=8, stream=st).cpu()
+                for C in (1, 2, 4, 8):
+                    ws = torch.empty(layer.workspace_bytes(ch, mf.dims, C, capi.BWD), dtype=torch.uint8, device=dev)
+                    barrier.wait()
+                    mf.moe_fwd(x, ids, w, lwg, lwu, lwd, C, ws, stream=st)
+                    mf.moe_bwd(dy, x, ids, w, lwg, lwu, lwd, C, ws, dw_gate=grads[0], dw_up=grads[1], dw_down=grads[2],
+                               accumulate_dw=True, stream=st)
+                    assert mf.sync(stream=st) == 0
+                    del ws
                 for i in range(I):
                     for l in range(L):
                         ids_np, w_np = synth.make_routing(T, E, k, rank=r, zipf_s=skew(i, l, L),
