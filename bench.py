@@ -243,7 +243,7 @@ def main():
     ap.add_argument("--alpha", type=float, default=0.9)
     ap.add_argument("--chunks", type=int, default=0, help="override the tuner's C")
     ap.add_argument("--sweep", type=int, default=1, help="also time every bin C (N=1 only)")
-    ap.add_argument("--cpu-tokens", type=int, default=12, help="cpu_baseline sample (~10 s of oracle work)")
+    ap.add_argument("--cpu-tokens", type=int, default=96, help="cpu_baseline sample (~15 s of oracle work on 16 cores)")
     ap.add_argument("--ref-tokens", type=int, default=4)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--placement", default=None)
