@@ -154,6 +154,41 @@ def device_weights(experts, h, g, dev):
     return tuple(torch.stack([o[i] for o in out]).contiguous() for i in range(3))
 
 
+def step_roofline(counts_h, h, g, k, T, El, C, ms, peaks, nvlink_gbs=900.0):
+    """The north star's roofline of a whole step, from the all-gathered counts
+    [EP][nsub][E]: per rank r, F_r = 22 h g s''_r FLOPs (fwd 6 + recompute 4 + bwd 12), P_r = 10 (k+1) h T
+    bytes of permute traffic (bf16), N_r = 10 h max(off-rank copies sent, received) bytes over NVLink;
+    t_roof = max_r max(F_r / tensor peak, P_r / HBM, N_r / NVLink).  t_roof4 adds the chunked method's
+    own HBM term W_r = C (8/3)|W_r| + (4C - 2)|W_r| (weights re-read per chunk, fp32 dW written once
+    and read-modify-written per later chunk; |W_r| = the rank's bf16 expert weights)."""
+    ch = counts_h.to(torch.int64)
+    EP = ch.shape[0]
+    per_dst = ch.sum(dim=1)                            # [src][E]
+    own = [int(per_dst[r, r * El:(r + 1) * El].sum()) for r in range(EP)]
+    sent = [int(per_dst[r].sum()) - own[r] for r in range(EP)]
+    recv = [int(per_dst[:, r * El:(r + 1) * El].sum()) - own[r] for r in range(EP)]
+    s_dd = [int(per_dst[:, r * El:(r + 1) * El].sum()) for r in range(EP)]
+    W_r = 3 * El * h * g * 2
+    terms = []
+    for r in range(EP):
+        F = 22.0 * h * g * s_dd[r]
+        P = 10.0 * (k + 1) * h * T
+        N = 10.0 * h * max(sent[r], recv[r])
+        Wb = C * (8.0 / 3.0) * W_r + (4 * C - 2) * W_r
+        terms.append((F / (peaks["bf16_tflops_sustained"] * 1e12), P / (peaks["hbm_gbs"] * 1e9),
+                      N / (nvlink_gbs * 1e9), (P + Wb) / (peaks["hbm_gbs"] * 1e9)))
+    t_roof = max(max(t[0], t[1], t[2]) for t in terms)
+    t_roof4 = max(max(t[0], t[3], t[2]) for t in terms)
+    hot = max(range(EP), key=lambda r: max(terms[r][:3]))
+    return {"t_roof_ms": t_roof * 1e3, "t_roof4_ms": t_roof4 * 1e3, "frac": t_roof / (ms / 1e3),
+            "frac4": t_roof4 / (ms / 1e3), "hot_rank": hot,
+            "bound": ["tensor", "hbm", "nvlink"][max(range(3), key=lambda i: terms[hot][i])],
+            "terms_ms_hot_rank": {"gemm_flops": terms[hot][0] * 1e3, "permute_bytes": terms[hot][1] * 1e3,
+                                  "a2a_bytes": terms[hot][2] * 1e3, "permute_plus_weights": terms[hot][3] * 1e3},
+            "peaks": {"tensor_tflops": peaks["bf16_tflops_sustained"], "hbm_gbs": peaks["hbm_gbs"],
+                      "nvlink_gbs": nvlink_gbs}}
+
+
 # ------------------------------------------------------------------------------------ oracle legs
 def oracle_sample_time(cfg, ntok: int, rank: int = 0):
     """Oracle (fp64, unchunked Eq. 4 + Eq. 5) fwd + bwd on ntok tokens of the workload; seconds."""
@@ -416,36 +451,7 @@ def main():
     all_gemm_tflops = 22 * h * g * rows_total / (gemm_ms / 1000.0) / 1e12 if gemm_ms else None
     step_tflops = 22 * h * g * rows_total / (ms / 1000.0) / 1e12
 
-    # ---------------------------------------------------------------- the north star's step roofline
-    # per rank r, F_r = 22 h g s''_r FLOPs (fwd 6 + recompute 4 + bwd 12), P_r = 10 (k+1) h T
-    # bytes of permute traffic (bf16), N_r = 10 h max(off-rank copies sent, received) bytes over NVLink;
-    # t_roof = max_r max(F_r / tensor peak, P_r / HBM, N_r / NVLink).  t_roof4 adds the chunked method's
-    # own HBM term W_r = C (8/3)|W_r| + (4C - 2)|W_r| (weights re-read per chunk, fp32 dW written once
-    # and read-modify-written per later chunk; |W_r| = the rank's bf16 expert weights).
-    nvlink_gbs = 900.0
-    ch = counts_h.to(torch.int64)                      # [EP][8][E]
-    per_dst = ch.sum(dim=1)                            # [src][E]
-    sent = [int(per_dst[r].sum()) - int(per_dst[r, r * El:(r + 1) * El].sum()) for r in range(EP)]
-    recv = [int(per_dst[:, r * El:(r + 1) * El].sum()) - int(per_dst[r, r * El:(r + 1) * El].sum()) for r in range(EP)]
-    s_dd = [int(per_dst[:, r * El:(r + 1) * El].sum()) for r in range(EP)]
-    W_r = 3 * El * h * g * 2
-    terms = []
-    for r in range(EP):
-        F = 22.0 * h * g * s_dd[r]
-        P = 10.0 * (k + 1) * h * T
-        N = 10.0 * h * max(sent[r], recv[r])
-        Wb = C * (8.0 / 3.0) * W_r + (4 * C - 2) * W_r
-        terms.append((F / (peaks["bf16_tflops_sustained"] * 1e12), P / (peaks["hbm_gbs"] * 1e9),
-                      N / (nvlink_gbs * 1e9), (P + Wb) / (peaks["hbm_gbs"] * 1e9)))
-    t_roof = max(max(t[0], t[1], t[2]) for t in terms)
-    t_roof4 = max(max(t[0], t[3], t[2]) for t in terms)
-    hot = max(range(EP), key=lambda r: max(terms[r][:3]))
-    step_roof = {"t_roof_ms": t_roof * 1e3, "t_roof4_ms": t_roof4 * 1e3, "frac": t_roof / (ms / 1e3),
-                 "frac4": t_roof4 / (ms / 1e3), "bound": ["tensor", "hbm", "nvlink"][max(range(3), key=lambda i: terms[hot][i])],
-                 "terms_ms_hot_rank": {"gemm_flops": terms[hot][0] * 1e3, "permute_bytes": terms[hot][1] * 1e3,
-                                       "a2a_bytes": terms[hot][2] * 1e3, "permute_plus_weights": terms[hot][3] * 1e3},
-                 "peaks": {"tensor_tflops": peaks["bf16_tflops_sustained"], "hbm_gbs": peaks["hbm_gbs"],
-                           "nvlink_gbs": nvlink_gbs}}
+    step_roof = step_roofline(counts_h, h, g, k, T, El, C, ms, peaks)
 
     # ---------------------------------------------------------------- e2e through the public API
     # Every step copies its inputs (x, dY, ids, scores) host->device from pinned memory and reads

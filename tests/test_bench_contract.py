@@ -59,3 +59,32 @@ def test_gpu_arm_line_tiny():
     # chunking: the peak activation falls with C (Table 2 rows 11-13 live for one chunk only)
     peaks = [line["per_C"][c]["peak_act_gb"] for c in sorted(line["per_C"], key=int)]
     assert all(a >= b for a, b in zip(peaks, peaks[1:]))
+
+
+def test_step_roofline_terms():
+    """The north star's 3-term step roofline on hand-made counts (EP = 2, E = 4, E_l = 2): rank 0 keeps
+    10 copies for expert 0 and sends 30 to expert 2; rank 1 sends 5 to expert 1 and keeps 20 for
+    expert 3.  s''_0 = 15, s''_1 = 50; off-rank traffic: rank 0 sends 30 / receives 5, rank 1 the
+    reverse - so rank 1 is hot on FLOPs and both move 30 rows."""
+    import importlib.util
+    import torch
+    spec = importlib.util.spec_from_file_location("bench_mod", os.path.join(ROOT, "bench.py"))
+    bench = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(bench)
+    counts = torch.zeros((2, 8, 4), dtype=torch.int32)
+    counts[0, 0, 0], counts[0, 3, 2] = 10, 30
+    counts[1, 5, 1], counts[1, 7, 3] = 5, 20
+    h, g, k, T, El, C = 64, 128, 2, 40, 2, 2
+    peaks = {"bf16_tflops_sustained": 1e-9, "hbm_gbs": 1e-3}       # FLOP/s 1e3, B/s 1e6
+    r = bench.step_roofline(counts, h, g, k, T, El, C, ms=1000.0, peaks=peaks, nvlink_gbs=1e-3)
+    F1 = 22 * h * g * 50 / 1e3                                       # seconds on the hot rank
+    P = 10 * (k + 1) * h * T / 1e6
+    N = 10 * h * 30 / 1e6
+    W = 3 * El * h * g * 2
+    P4 = (10 * (k + 1) * h * T + C * 8 / 3 * W + (4 * C - 2) * W) / 1e6
+    assert r["hot_rank"] == 1 and r["bound"] == "tensor"
+    assert abs(r["t_roof_ms"] - 1e3 * max(F1, P, N)) < 1e-6 * r["t_roof_ms"]
+    assert abs(r["t_roof4_ms"] - 1e3 * max(F1, P4, N)) < 1e-6 * r["t_roof4_ms"]
+    t = r["terms_ms_hot_rank"]
+    assert abs(t["a2a_bytes"] - 1e3 * N) < 1e-9 and abs(t["permute_bytes"] - 1e3 * P) < 1e-9
+    assert abs(r["frac"] - max(F1, P, N) / 1.0) < 1e-9
