@@ -56,20 +56,20 @@ __global__ void __launch_bounds__(256) mx_quant_rows_kernel(const __nv_bfloat16*
 __global__ void __launch_bounds__(256) mx_quant_dual_kernel(const __nv_bfloat16* __restrict__ src, int R, int Cc,
                                                             uint8_t* __restrict__ q_rows, uint8_t* __restrict__ sf_rows,
                                                             uint8_t* __restrict__ q_t, uint8_t* __restrict__ sf_t) {
-  __shared__ __nv_bfloat16 t[128][128 + 8];
+  // rows of 65 words: a warp reading one word per lane is conflict-free both along a row (lanes =
+  // adjacent column pairs) and down a column (lanes = adjacent rows, 65 = 1 mod 32)
+  __shared__ uint32_t t[128][65];
   const int b = blockIdx.z, r0 = blockIdx.y * 128, c0 = blockIdx.x * 128;
   const __nv_bfloat16* s = src + (int64_t)b * R * Cc;
 #pragma unroll
   for (int pass = 0; pass < 8; pass++) {
     const int idx = pass * 256 + threadIdx.x;    // 16 x uint4 per row
-    const int rr = idx >> 4, cc = (idx & 15) * 8;
-    *reinterpret_cast<uint4*>(&t[rr][cc]) = *reinterpret_cast<const uint4*>(s + (int64_t)(r0 + rr) * Cc + c0 + cc);
+    const int rr = idx >> 4, cw = (idx & 15) * 4;
+    const uint4 u = *reinterpret_cast<const uint4*>(s + (int64_t)(r0 + rr) * Cc + c0 + cw * 2);
+    t[rr][cw] = u.x; t[rr][cw + 1] = u.y; t[rr][cw + 2] = u.z; t[rr][cw + 3] = u.w;
   }
   __syncthreads();
-  auto quant32 = [](const float (&v)[32], uint8_t* q, uint8_t* sf) {
-    float amax = 0.f;
-#pragma unroll
-    for (int i = 0; i < 32; i++) amax = fmaxf(amax, fabsf(v[i]));
+  auto quant32 = [](const float (&v)[32], float amax, uint8_t* q, uint8_t* sf) {
     const int E = mx_exp(amax);
     const float inv = mx_inv_scale(E);
     uint32_t o[8];
@@ -80,22 +80,44 @@ __global__ void __launch_bounds__(256) mx_quant_dual_kernel(const __nv_bfloat16*
     reinterpret_cast<uint4*>(q)[1] = make_uint4(o[4], o[5], o[6], o[7]);
     *sf = (uint8_t)(E + 127);
   };
-  const int line = threadIdx.x >> 1;             // 0..127: a row (pass 1) / a column (pass 2)
+  {
+    // row-wise: thread = (row, half of the 128 columns): two 32-column blocks along Cc
+    const int row = threadIdx.x & 127, hf = threadIdx.x >> 7;
+    const int64_t gr = (int64_t)b * R + r0 + row;
 #pragma unroll
-  for (int k2 = 0; k2 < 2; k2++) {
-    const int kb = (threadIdx.x & 1) * 2 + k2;   // block 0..3 along the 128
-    float v[32];
-    // row-wise: row r0 + line, columns c0 + 32 kb ..
+    for (int k2 = 0; k2 < 2; k2++) {
+      const int kb = hf * 2 + k2;
+      float v[32];
+      float amax = 0.f;
 #pragma unroll
-    for (int i = 0; i < 32; i++) v[i] = __bfloat162float(t[line][32 * kb + i]);
-    const int64_t gr = (int64_t)b * R + r0 + line;
-    quant32(v, q_rows + gr * Cc + c0 + 32 * kb, sf_rows + mx_sf_off(gr, (c0 >> 5) + kb, Cc));
-    // column-wise: column c0 + line, rows r0 + 32 kb .. (output row of q_t)
+      for (int i = 0; i < 16; i++) {
+        const uint32_t u = t[row][16 * kb + i];
+        v[2 * i] = __uint_as_float(u << 16);
+        v[2 * i + 1] = __uint_as_float(u & 0xFFFF0000u);
+        amax = fmaxf(amax, fmaxf(fabsf(v[2 * i]), fabsf(v[2 * i + 1])));
+      }
+      quant32(v, amax, q_rows + gr * Cc + c0 + 32 * kb, sf_rows + mx_sf_off(gr, (c0 >> 5) + kb, Cc));
+    }
+  }
+  {
+    // column-wise: thread = (column pair, 32-row block), two columns at once along R
+    const int cp = threadIdx.x & 63, kb = threadIdx.x >> 6;
+    float v0[32], v1[32];
+    float a0 = 0.f, a1 = 0.f;
 #pragma unroll
-    for (int i = 0; i < 32; i++) v[i] = __bfloat162float(t[32 * kb + i][line]);
-    const int64_t gc = c0 + line;
-    quant32(v, q_t + ((int64_t)b * Cc + gc) * R + r0 + 32 * kb,
-            sf_t + (int64_t)b * Cc * (R / 32) + mx_sf_off(gc, (r0 >> 5) + kb, R));
+    for (int i = 0; i < 32; i++) {
+      const uint32_t u = t[32 * kb + i][cp];
+      v0[i] = __uint_as_float(u << 16);
+      v1[i] = __uint_as_float(u & 0xFFFF0000u);
+      a0 = fmaxf(a0, fabsf(v0[i]));
+      a1 = fmaxf(a1, fabsf(v1[i]));
+    }
+#pragma unroll
+    for (int hh = 0; hh < 2; hh++) {
+      const int64_t gc = c0 + 2 * cp + hh;
+      quant32(hh ? v1 : v0, hh ? a1 : a0, q_t + ((int64_t)b * Cc + gc) * R + r0 + 32 * kb,
+              sf_t + (int64_t)b * Cc * (R / 32) + mx_sf_off(gc, (r0 >> 5) + kb, R));
+    }
   }
 }
 
