@@ -122,10 +122,14 @@ int main() {
   cudaEventCreate(&e0);
   cudaEventCreate(&e1);
   printf("{");
-  for (int grid_mult = 1; grid_mult <= 2; grid_mult++)
+  // grid: every SM (x1, x2), then a subset of the SMs (how many SMs the HBM-bound dW accumulation
+  // needs if it shares the GPU with a tensor-bound GEMM)
+  const int grids[6] = {nsm, 2 * nsm, 16, 32, 64, 96};
+  for (int gi = 0; gi < 6; gi++)
     for (int m = 0; m < 4; m++) {
+      const int grid_mult = gi + 1;
       auto launch = [&]() {
-        const int g = nsm * grid_mult;
+        const int g = grids[gi];
         if (m == 0) rmw_kernel<0><<<g, WARPS * 32, smem>>>(map, d);
         if (m == 1) rmw_kernel<1><<<g, WARPS * 32, smem>>>(map, d);
         if (m == 2) rmw_kernel<2><<<g, WARPS * 32, smem>>>(map, d);
@@ -141,7 +145,7 @@ int main() {
       float ms = 0;
       cudaEventElapsedTime(&ms, e0, e1);
       const double gbs = traffic[m] * ROWS * (double)COLS * reps / (ms * 1e-3) / 1e9;
-      printf("%s\"%s_x%d\": %.0f", (grid_mult == 1 && m == 0) ? "" : ", ", names[m], grid_mult, gbs);
+      printf("%s\"%s_g%d\": %.0f", (gi == 0 && m == 0) ? "" : ", ", names[m], grids[gi], gbs);
     }
   printf(", \"unit\": \"GB/s of DRAM traffic (algorithmic)\", \"array_gb\": %.2f}\n", bytes / 1e9);
   return 0;
