@@ -127,7 +127,6 @@ int main() {
   const int grids[6] = {nsm, 2 * nsm, 16, 32, 64, 96};
   for (int gi = 0; gi < 6; gi++)
     for (int m = 0; m < 4; m++) {
-      const int grid_mult = gi + 1;
       auto launch = [&]() {
         const int g = grids[gi];
         if (m == 0) rmw_kernel<0><<<g, WARPS * 32, smem>>>(map, d);
