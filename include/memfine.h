@@ -315,7 +315,9 @@ memfine_status memfine_router_bwd(memfine_handle_t h, const void* x, const void*
  * amax <= 448 * 2^E (no element clips; E = 0 for an all-zero block); elements are E4M3,
  * round-to-nearest-even.  Quantised operands: x and W_gate/W_up rows along h, a and W_down rows
  * along g (forward and recompute); dG||dU and W_gate/W_up columns along g (dX).  The dA GEMM
- * (bound by its fused epilogue) and the weight gradients stay BF16 x BF16 -> fp32.  With EP > 1
+ * (bound by its fused epilogue) stays BF16 x BF16 -> fp32; so do the weight gradients unless
+ * MEMFINE_FLAG_MX_WGRAD (reading R28c: x, dY, dG||dU and a_w quantised along each expert's copies
+ * in a chunk, blocks of 32, "columnwise").  With EP > 1
  * (EP_COPY transport) the dispatched rows travel in bf16 and each rank quantises the rows it
  * received (the same codes: x is blocked along h, per row); EP_P2P returns MEMFINE_ERR_UNSUPPORTED.
  *
