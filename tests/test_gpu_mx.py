@@ -154,3 +154,17 @@ def test_mx_wgrad_empty_expert_and_ragged_chunks(C):
     for key in ("dwg", "dwu", "dwd"):
         assert np.all(got[key][3] == 0) and np.all(got[key][5] == 0), key
         assert rel_err(got[key], ref[key]) <= MX_TOL, key
+
+
+@pytest.mark.parametrize("mx_wgrad", [False, True])
+def test_mx_fewer_tokens_than_chunks(mx_wgrad):
+    """T < C (empty chunks issue nothing) with every copy on one expert (the others empty)."""
+    T, E, k, C = 5, 4, 2, 8
+    ids = np.tile(np.array([[0, 2]], np.int32), (T, 1))
+    p = make_problem(T, 128, 256, E, k, seed=47, ids=ids)
+    got = _mx_run(p, C, mx_wgrad=mx_wgrad)
+    ref, _ = _mx_oracle(p, wgrad_C=C if mx_wgrad else 0)
+    for key in ("y", "dx", "dscore", "dwg", "dwu", "dwd"):
+        assert rel_err(got[key], ref[key]) <= MX_TOL, key
+    for key in ("dwg", "dwu", "dwd"):
+        assert np.all(got[key][1] == 0) and np.all(got[key][3] == 0), key
