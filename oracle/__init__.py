@@ -328,3 +328,18 @@ def moe_mx(d: Dims, x, ids, w, wq, dy=None, mode: int = 1, wd=None, wgrad_C: int
                              _p(ds), _p(dwg), _p(dwu), _p(dwd), C.c_int32(wgrad_C))
     assert st == 0
     return y, dx, ds, dwg, dwu, dwd
+
+
+def moe_mx_tokens(d: Dims, toks, x, dy, ids, w, wg, wu, wd, mode: int = 1):
+    """MX layer on a token subset (full-size sampled parity): (y, dx, dscore) rows of toks, as
+    moe_mx would give them; weights are quantised one expert at a time."""
+    toks = np.ascontiguousarray(toks, dtype=np.int64)
+    x, dy, wg, wu, wd = (_wt(a, d.in_dtype) for a in (x, dy, wg, wu, wd))
+    ids = np.ascontiguousarray(ids, dtype=np.int32)
+    w = np.ascontiguousarray(w, dtype=np.float64)
+    n = len(toks)
+    y = np.zeros((n, d.h)); dx = np.zeros((n, d.h)); ds = np.zeros((n, d.k))
+    st = lib().oracle_moe_mx_tokens(C.byref(d.c()), C.c_int32(mode), C.c_int64(n), _p(toks), _p(dy), _p(x), _p(ids),
+                                    _p(w), _p(wg), _p(wu), _p(wd), _p(y), _p(dx), _p(ds))
+    assert st == 0
+    return y, dx, ds

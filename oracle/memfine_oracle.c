@@ -848,7 +848,7 @@ void oracle_mx_weights(const oracle_dims* d, int32_t mode, const void* wg, const
  * unquantised dW operands a, dO, dG, dU).  Same loop orders as expert_forward /
  * expert_backward, quantisers inserted. */
 static void expert_mx(const oracle_dims* d, int mode, const void* x, int64_t xoff, const void* dy, int64_t dyoff,
-                      double ws, double* const* wq, const void* wd, int32_t e, double* scratch,
+                      double ws, double* const* wq, int32_t ew, const void* wd, int32_t e, double* scratch,
                       double* O, double* a_out, double* dO_out, double* dG_out, double* dU_out, double* dxc,
                       double* dscore)
 {
@@ -860,8 +860,8 @@ static void expert_mx(const oracle_dims* d, int mode, const void* x, int64_t xof
     for (int64_t n = 0; n < g; n++) {
         double sg = 0.0, su = 0.0;
         for (int64_t c = 0; c < h; c++) {
-            sg += wq[0][((int64_t)e * g + n) * h + c] * xq[c];
-            su += wq[1][((int64_t)e * g + n) * h + c] * xq[c];
+            sg += wq[0][((int64_t)ew * g + n) * h + c] * xq[c];
+            su += wq[1][((int64_t)ew * g + n) * h + c] * xq[c];
         }
         G[n] = sg; U[n] = su;
         A[n] = sg * sigmoid(sg) * su;
@@ -870,7 +870,7 @@ static void expert_mx(const oracle_dims* d, int mode, const void* x, int64_t xof
     mx_qdq(Aq, g, 1, mode);
     for (int64_t m = 0; m < h; m++) {
         double so = 0.0;
-        for (int64_t n = 0; n < g; n++) so += wq[2][((int64_t)e * h + m) * g + n] * Aq[n];
+        for (int64_t n = 0; n < g; n++) so += wq[2][((int64_t)ew * h + m) * g + n] * Aq[n];
         O[m] = so;
     }
     if (!dy) return;
@@ -906,8 +906,8 @@ static void expert_mx(const oracle_dims* d, int mode, const void* x, int64_t xof
     for (int64_t c = 0; c < h; c++) {
         double s1 = 0.0, s2 = 0.0;
         for (int64_t n = 0; n < g; n++) {
-            s1 += wq[3][((int64_t)e * g + n) * h + c] * dGq[n];
-            s2 += wq[4][((int64_t)e * g + n) * h + c] * dUq[n];
+            s1 += wq[3][((int64_t)ew * g + n) * h + c] * dGq[n];
+            s2 += wq[4][((int64_t)ew * g + n) * h + c] * dUq[n];
         }
         dxc[c] = s1 + s2;
     }
@@ -1036,7 +1036,7 @@ int32_t oracle_moe_mx(const oracle_dims* d, int32_t mode, const void* dy, const 
                     }
                     continue;
                 }
-                expert_mx(d, mode, x, t * h, dy, t * h, w[q], wq, wd, e, scratch, O, aq, dOq, dGq, dUq, dxc,
+                expert_mx(d, mode, x, t * h, dy, t * h, w[q], wq, e, wd, e, scratch, O, aq, dOq, dGq, dUq, dxc,
                           dy ? dscore + q : NULL);
                 for (int64_t c = 0; c < h; c++) {
                     y[t * h + c] += w[q] * O[c];
@@ -1056,6 +1056,65 @@ int32_t oracle_moe_mx(const oracle_dims* d, int32_t mode, const void* dy, const 
         free(a_all); free(dG_all); free(dU_all); free(dO_all); free(order);
     }
     return rc;
+}
+
+/* MX layer on a token subset (full-size sampled parity): y, dx, dscore of tokens toks[0..ntok) exactly
+ * as oracle_moe_mx computes them (the per-token terms do not depend on other tokens), with the
+ * weights quantised one expert at a time (the five operand layouts of oracle_mx_weights), so the
+ * dequantised copies of all experts never exist at once. */
+int32_t oracle_moe_mx_tokens(const oracle_dims* d, int32_t mode, int64_t ntok, const int64_t* toks, const void* dy,
+                             const void* x, const int32_t* ids, const double* w, const void* wg, const void* wu,
+                             const void* wd, double* y, double* dx, double* dscore)
+{
+    int64_t h = d->h, g = d->g, k = d->k;
+    double* wqe[5];
+    for (int i = 0; i < 5; i++) wqe[i] = (double*)malloc(sizeof(double) * (size_t)g * h);
+    double* scratch = (double*)malloc(sizeof(double) * (size_t)(8 * g + 2 * h));
+    double* O = (double*)malloc(sizeof(double) * (size_t)(2 * h + 4 * g + h));
+    int ok = scratch && O;
+    for (int i = 0; i < 5; i++) ok = ok && wqe[i];
+    if (!ok) {
+        for (int i = 0; i < 5; i++) free(wqe[i]);
+        free(scratch); free(O);
+        return 1;
+    }
+    double *dxc = O + h, *a1 = dxc + h, *dG1 = a1 + g, *dU1 = dG1 + g, *dO1 = dU1 + g;
+    for (int64_t i = 0; i < ntok * h; i++) { y[i] = 0.0; if (dy) dx[i] = 0.0; }
+    for (int32_t e = 0; e < d->E; e++) {
+        int used = 0;
+        for (int64_t i = 0; i < ntok && !used; i++)
+            for (int64_t sl = 0; sl < k; sl++) used |= ids[toks[i] * k + sl] == e;
+        if (!used) continue;
+        int64_t off = (int64_t)e * g * h;
+        #pragma omp parallel for schedule(static)
+        for (int64_t i = 0; i < g * h; i++) {
+            wqe[0][i] = wqe[3][i] = load(wg, off + i, d->in_dtype);
+            wqe[1][i] = wqe[4][i] = load(wu, off + i, d->in_dtype);
+            wqe[2][i] = load(wd, off + i, d->in_dtype);
+        }
+        #pragma omp parallel for schedule(dynamic, 16)
+        for (int64_t r = 0; r < g; r++) { mx_qdq(wqe[0] + r * h, h, 1, mode); mx_qdq(wqe[1] + r * h, h, 1, mode); }
+        #pragma omp parallel for schedule(dynamic, 16)
+        for (int64_t c = 0; c < h; c++) { mx_qdq(wqe[3] + c, g, h, mode); mx_qdq(wqe[4] + c, g, h, mode); }
+        #pragma omp parallel for schedule(dynamic, 16)
+        for (int64_t r = 0; r < h; r++) mx_qdq(wqe[2] + r * g, g, 1, mode);
+        for (int64_t i = 0; i < ntok; i++) {
+            int64_t t = toks[i];
+            for (int64_t sl = 0; sl < k; sl++) {
+                int64_t q = t * k + sl;
+                if (ids[q] != e) continue;
+                expert_mx(d, mode, x, t * h, dy, t * h, w[q], wqe, 0, wd, e, scratch, O, a1, dO1, dG1, dU1, dxc,
+                          dy ? dscore + i * k + sl : NULL);
+                for (int64_t c = 0; c < h; c++) {
+                    y[i * h + c] += w[q] * O[c];
+                    if (dy) dx[i * h + c] += dxc[c];
+                }
+            }
+        }
+    }
+    for (int i = 0; i < 5; i++) free(wqe[i]);
+    free(scratch); free(O);
+    return 0;
 }
 
 int32_t oracle_version(void) { return 1; }

@@ -168,3 +168,21 @@ def test_mx_fewer_tokens_than_chunks(mx_wgrad):
         assert rel_err(got[key], ref[key]) <= MX_TOL, key
     for key in ("dwg", "dwu", "dwd"):
         assert np.all(got[key][1] == 0) and np.all(got[key][3] == 0), key
+
+
+@pytest.mark.parametrize("mx_wgrad", [False, True])
+def test_mx_mixtral_full_size_sampled(mx_wgrad):
+    """The MXFP8 variant at BASELINE configs[1]'s shape in bench.py's launch configuration (EP = 1,
+    16K tokens, C = 1): Y, dX and d_score of sampled tokens against the oracle's MX layer (weights
+    quantised one expert at a time); the weight gradients finite and non-zero."""
+    p = make_problem(16384, 4096, 14336, 8, 2, zipf_s=1.2, seed=5)
+    got = _mx_run(p, 1, mx_wgrad=mx_wgrad)
+    toks = np.random.default_rng(1).choice(16384, 6, replace=False)
+    d = oracle_dims(p)
+    a = [_np_in(t, p.dtype) for t in (p.x, p.dy, p.wg, p.wu, p.wd)]
+    ry, rdx, rds = oracle.moe_mx_tokens(d, toks, a[0], a[1], p.ids.numpy(), p.w.numpy().astype(np.float64),
+                                        a[2], a[3], a[4])
+    for key, ref in (("y", ry), ("dx", rdx), ("dscore", rds)):
+        assert rel_err(got[key][toks], ref) <= MX_TOL, key
+    for key in ("dwg", "dwu", "dwd"):
+        assert np.isfinite(got[key]).all() and np.abs(got[key]).max() > 0, key

@@ -222,3 +222,14 @@ def test_mx_wgrad_error_small_present_and_chunk_dependent():
             err = np.abs(got - ref).max() / np.abs(ref).max()
             assert 1e-4 < err < 0.1, (C, err)
     assert not np.array_equal(outs[1][0], outs[2][0])
+
+
+def test_mx_token_subset_equals_whole_layer():
+    """The full-size sampled evaluator (weights quantised one expert at a time) reproduces the whole
+    layer's rows bit for bit - it is the same per-copy arithmetic on a token subset."""
+    d, x, dy, wg, wu, wd, ids, w = _problem(T=40, seed=21)
+    wq = oracle.mx_weights(d, wg, wu, wd)
+    y, dx, ds, *_ = oracle.moe_mx(d, x, ids, w, wq, dy=dy, wd=wd)
+    toks = np.array([3, 17, 0, 39, 22])
+    ys, dxs, dss = oracle.moe_mx_tokens(d, toks, x, dy, ids, w, wg, wu, wd)
+    assert np.array_equal(ys, y[toks]) and np.array_equal(dxs, dx[toks]) and np.array_equal(dss, ds[toks])
