@@ -139,6 +139,14 @@ def test_edge_cases():
     _check_all(p, GpuRun(p), 2, oracle_fwd_bwd(p, 2))
 
 
+def test_maximum_experts_and_topk():
+    """The largest routing the ABI accepts: 1024 experts (the dispatch scan's limit) and top-16
+    (the copy-ranking limit) - ~8 copies per expert, every segment padded to 128 rows, 1024 expert
+    segments in the grouped GEMMs; C = 2."""
+    p = make_problem(512, 128, 128, 1024, 16, zipf_s=1.2, seed=8)
+    _check_all(p, GpuRun(p), 2, oracle_fwd_bwd(p, 2))
+
+
 def test_errors_surface():
     p = make_problem(64, 64, 128, 4, 2)
     run = GpuRun(p)
