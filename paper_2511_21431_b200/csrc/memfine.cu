@@ -1,5 +1,6 @@
 // memfine.cu — the C ABI of libmemfine.so: handle, MACT plan, workspace carving and the
 // FCDA chunk loops (Eq. 6 forward, Eq. 7 recompute backward).
+#include <nvtx3/nvToolsExt.h>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -91,6 +92,23 @@ struct memfine_handle_s {
 };
 
 namespace {
+// NVTX ranges (no-ops unless a tool injects NVTX): one per layer call and one per FCDA chunk, so ncu
+// `--nvtx --nvtx-include` / a timeline tool can select e.g. the backward of chunk 3.
+struct Nvtx {
+  explicit Nvtx(const char* s) { nvtxRangePushA(s); }
+  ~Nvtx() { nvtxRangePop(); }
+};
+const char* chunk_range_name(int pass, int j) {
+  static char names[2][64][24];
+  static bool init = false;
+  if (!init) {
+    for (int p = 0; p < 2; p++)
+      for (int c = 0; c < 64; c++) snprintf(names[p][c], sizeof names[p][c], "%s chunk %d", p ? "bwd" : "fwd", c);
+    init = true;
+  }
+  return names[pass ? 1 : 0][j & 63];
+}
+
 cudaEvent_t pool_event(memfine_handle_s* h) {
   if (h->pool_used == h->pool.size()) {
     cudaEvent_t e;
@@ -523,6 +541,7 @@ memfine_status fwd_ep1(memfine_handle_s* h, const T* x, const int32_t* ids, cons
   for (int j = 0; j < C; j++) {
     int64_t t0 = chunk_begin(d.tokens, C, j), t1 = chunk_begin(d.tokens, C, j + 1);
     if (t1 == t0) continue;
+    Nvtx chunk_range(chunk_range_name(0, j));
     int NB = (int)ceil_div64(t1 - t0, kTokPerBlk);
     prof_begin(h, 6, st);
     launch_dispatch_hist(ids, t0, t1, k, E, L.m, h->status_d, st);
@@ -591,6 +610,7 @@ memfine_status bwd_ep1(memfine_handle_s* h, const T* dy, const T* x, const int32
   for (int j = 0; j < C; j++) {
     int64_t t0 = chunk_begin(d.tokens, C, j), t1 = chunk_begin(d.tokens, C, j + 1);
     if (t1 == t0) continue;
+    Nvtx chunk_range(chunk_range_name(1, j));
     int NB = (int)ceil_div64(t1 - t0, kTokPerBlk);
     // B1: re-dispatch x and dy of the chunk (the recompute of Eq. 7 starts from X_j)
     prof_begin(h, 6, st);
@@ -1596,6 +1616,7 @@ memfine_status memfine_moe_fwd(memfine_handle_t h, const void* x, const int32_t*
   if (h->d.tokens > 0 && (!x || !ids || !w || !y)) return MEMFINE_ERR_INVALID_ARG;
   if (!w_gate || !w_up || !w_down || !ws) return MEMFINE_ERR_INVALID_ARG;
   cudaStream_t st = (cudaStream_t)stream;
+  Nvtx call_range("memfine_moe_fwd");
   begin_call(h, C, MEMFINE_FWD, ws_bytes, st);
   if (ep_path(h->d)) return memfine_ep_fwd(h, x, ids, w, w_gate, w_up, w_down, C, y, ws, ws_bytes, st);
   if (h->d.dtype != MEMFINE_FP32)
@@ -1612,6 +1633,7 @@ memfine_status memfine_moe_bwd(memfine_handle_t h, const void* dy, const void* x
   if (h->d.tokens > 0 && (!dy || !x || !ids || !w || !dx)) return MEMFINE_ERR_INVALID_ARG;
   if (!w_gate || !w_up || !w_down || !dw_gate || !dw_up || !dw_down || !ws) return MEMFINE_ERR_INVALID_ARG;
   cudaStream_t st = (cudaStream_t)stream;
+  Nvtx call_range("memfine_moe_bwd");
   begin_call(h, C, MEMFINE_BWD, ws_bytes, st);
   if (ep_path(h->d))
     return memfine_ep_bwd(h, dy, x, ids, w, w_gate, w_up, w_down, C, dx, dw_gate, dw_up, dw_down, dscore,
