@@ -1109,6 +1109,7 @@ memfine_status ep_run(memfine_handle_s* h, int pass, const T* dy, const T* x, co
   int beta = accumulate ? 1 : 0;  // first chunk overwrites dW, later chunks accumulate
   // A7-A8 / B2-B5 expert GEMMs of chunk j (on st)
   auto compute = [&](int j) -> memfine_status {
+    Nvtx chunk_range(chunk_range_name(pass == MEMFINE_BWD, j));
     const Layout& L = Ls[j % S];
     if (S == 2) MF_CUDA_OK(cudaStreamWaitEvent(st, h->ev_disp[j % 2], 0));
     GemmProblem<T> p = base_problem<T>(h, L, wg, wu, wd);
