@@ -319,7 +319,8 @@ memfine_status memfine_router_bwd(memfine_handle_t h, const void* x, const void*
  * MEMFINE_FLAG_MX_WGRAD (reading R28c: x, dY, dG||dU and a_w quantised along each expert's copies
  * in a chunk, blocks of 32, "columnwise").  With EP > 1
  * (EP_COPY transport) the dispatched rows travel in bf16 and each rank quantises the rows it
- * received (the same codes: x is blocked along h, per row); EP_P2P returns MEMFINE_ERR_UNSUPPORTED.
+ * received (the same codes: x is blocked along h, per row); over EP_P2P the pushed bf16 rows are quantised
+ * on arrival and the MX down / dX epilogues store o / dX rows into the sources' buffers.
  *
  * memfine_mx_weights_bytes: bytes of the quantised-weights buffer for dims (dtype MXFP8).
  * memfine_mx_quantize_weights: quantise the handle's local experts' bf16 weights (dev, the

@@ -954,7 +954,14 @@ __global__ void __launch_bounds__(THREADS, 1)
             }
           } else {
             if (!rows_ok || n >= p.h) continue;                 // DOWN / DX: N = h
-            store32_bf16(p.O + row * (int64_t)p.h + n, v);
+            if (p.row_addr) {
+              // fused EP combine (P2P transport): the row goes straight into its source rank's send
+              // buffer (peer memory) as the tile is produced
+              const uint64_t a = __ldg(p.row_addr + row);
+              if (a) store32_bf16(reinterpret_cast<__nv_bfloat16*>(a) + n, v);
+            } else {
+              store32_bf16(p.O + row * (int64_t)p.h + n, v);
+            }
           }
         }
         it++;

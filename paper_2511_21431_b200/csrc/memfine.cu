@@ -852,7 +852,10 @@ memfine_status ep_run_p2p(memfine_handle_s* h, int pass, const T* dy, const T* x
                           float* dwd, float* dscore, int accumulate, void* ws, uint64_t ws_bytes, cudaStream_t st) {
   const memfine_dims& d = h->d;
   const int E = d.num_experts, EP = d.ep_size, El = E / EP, k = d.topk, hd = d.hidden, me = d.ep_rank;
-  if (EP > kMaxPeers || d.dtype == MEMFINE_MXFP8) return MEMFINE_ERR_UNSUPPORTED;
+  if (EP > kMaxPeers) return MEMFINE_ERR_UNSUPPORTED;
+  const bool mx = d.dtype == MEMFINE_MXFP8;
+  if (mx && !h->mx_w) return MEMFINE_ERR_INVALID_ARG;   // memfine_mx_quantize_weights first
+  MxWeightsLayout W = mx_weights_layout(d, h->mx_w);
   if (int rc = ep_gather_counts(h, ids, C, st)) return (memfine_status)rc;
   // every rank's chunk tables and workspace layout, from the shared counts
   std::vector<std::vector<EpChunk>> tabs(EP);
@@ -944,12 +947,25 @@ memfine_status ep_run_p2p(memfine_handle_s* h, int pass, const T* dy, const T* x
     p.dWg = dwg;
     p.dWu = dwu;
     p.dWd = dwd;
+    if constexpr (std::is_same<T, __nv_bfloat16>::value)
+      if (mx) {   // MXFP8 (reading R28): the landed bf16 rows -> E4M3 + scale chunks
+        launch_mx_quant_rows((const __nv_bfloat16*)L.X, hd, L.rows_cap, L.m.info, hd, L.Xq, L.Xsf, st);
+        h->last.kernel_launches += 1;
+      }
     if (pass == MEMFINE_FWD) {
       p.kind = GK_GATEUP;
       p.store_a = 1;
+      if constexpr (std::is_same<T, __nv_bfloat16>::value)
+        if (mx) {
+          set_mx(p, {L.Xq, L.Xsf}, W.op[0], W.op[1]);
+          p.mx_aq = L.Aq;
+          p.mx_aq_sf = L.Asf;
+        }
       if (int rc = run_gemm<T>(h, p, st)) return (memfine_status)rc;
       p.kind = GK_DOWN;
       p.row_addr = L.m.row_addr;   // A8 + A9 fused: o rows stored into their source's send buffer
+      if constexpr (std::is_same<T, __nv_bfloat16>::value)
+        if (mx) set_mx(p, {L.Aq, L.Asf}, W.op[2], W.op[2]);
       if (int rc = run_gemm<T>(h, p, st)) return (memfine_status)rc;
       p2p_fence(h, st);  // (C) every o row for this rank's tokens has landed
       if (t1 > t0) launch_combine<T>((const T*)L.send, w, t0, t1, k, hd, L.m, out, st);
@@ -957,17 +973,25 @@ memfine_status ep_run_p2p(memfine_handle_s* h, int pass, const T* dy, const T* x
       p.kind = GK_GATEUP;
       p.store_a = 0;
       p.store_gu = 1;
+      if constexpr (std::is_same<T, __nv_bfloat16>::value)
+        if (mx) set_mx(p, {L.Xq, L.Xsf}, W.op[0], W.op[1]);
       if (int rc = run_gemm<T>(h, p, st)) return (memfine_status)rc;
       p.kind = GK_DACT;
+      p.mx = 0;
+      if (mx) {   // BF16 dA GEMM whose epilogue also writes dG || dU as E4M3 + scales
+        p.mx_gq = L.GUq;
+        p.mx_gq_sf = L.GUsf;
+      }
       if (int rc = run_gemm<T>(h, p, st)) return (memfine_status)rc;
+      p.mx_gq = nullptr;
+      p.mx_gq_sf = nullptr;
       p.wgrad_beta = beta;
-      p.kind = GK_WGRAD_DOWN;
-      if (int rc = run_gemm<T>(h, p, st)) return (memfine_status)rc;
-      p.kind = GK_WGRAD_GU;
-      if (int rc = run_gemm<T>(h, p, st)) return (memfine_status)rc;
+      if (int rc = run_wgrad<T>(h, p, L, st)) return (memfine_status)rc;
       beta = 1;
       p.kind = GK_DX;
       p.row_addr = L.m.row_addr;   // B4 + B6 fused: dX rows stored into their source's send buffer
+      if constexpr (std::is_same<T, __nv_bfloat16>::value)
+        if (mx) set_mx(p, {L.GUq, L.GUsf}, W.op[3], W.op[4]);
       if (int rc = run_gemm<T>(h, p, st)) return (memfine_status)rc;
       launch_p2p_push_dw(L.m.dw_row, L.m.row_addr_w, L.m.info, L.rows_cap, st);
       p2p_fence(h, st);  // (C)

@@ -195,3 +195,36 @@ def test_ep_local_group_mx_wgrad_matches_oracle(EP, C):
                 "dw_gate": rel_err(dwg, dwg_ref[es]), "dw_up": rel_err(dwu, dwu_ref[es]),
                 "dw_down": rel_err(dwd, dwd_ref[es])}
         assert all(v <= MX_TOL for v in errs.values()), (r, errs)
+
+
+@pytest.mark.parametrize("EP,C,mx_wgrad", [(2, 2, False), (4, 1, False), (2, 3, True)])
+def test_ep_local_group_mx_p2p_matches_oracle(EP, C, mx_wgrad):
+    """MXFP8 over the fused peer-memory exchange (EP_P2P): rows pushed in bf16 by the permute kernel
+    and quantised on arrival, o / dX rows stored into the sources' buffers by the MX down / dX
+    epilogues; every rank against the oracle's MX layer (and, with MX weight gradients, R28c)."""
+    from tests.test_gpu_mx import MX_TOL
+    T, h, g, E, k = 300, 256, 384, 8, 2
+    El = E // EP
+    dtype = torch.bfloat16
+    xs = [synth.make_x(T, h, rank=r, dtype=dtype) for r in range(EP)]
+    dys = [synth.make_dy(T, h, rank=r, dtype=dtype) for r in range(EP)]
+    routes = [synth.make_routing(T, E, k, rank=r, zipf_s=1.2, placement="contiguous") for r in range(EP)]
+    wg, wu, wd = synth.make_experts(range(E), h, g, dtype=dtype)
+    results, _ = _run_group(EP, C, dtype, capi.EP_P2P, xs, dys, routes, wg, wu, wd, T, h, g, E, k, mx=True,
+                            mx_wgrad=mx_wgrad)
+    d = oracle.Dims(T=T, h=h, g=g, E=E, k=k, EP=EP, in_dtype="bf16")
+    xa = np.concatenate([_bits(x, dtype) for x in xs])
+    dya = np.concatenate([_bits(x, dtype) for x in dys])
+    ida = np.concatenate([r[0] for r in routes])
+    wa = np.concatenate([r[1] for r in routes]).astype(np.float64)
+    W = [_bits(t, dtype) for t in (wg, wu, wd)]
+    wq = oracle.mx_weights(d, *W)
+    y_ref, dx_ref, ds_ref, dwg_ref, dwu_ref, dwd_ref = oracle.moe_mx(d, xa, ida, wa, wq, dy=dya, wd=W[2],
+                                                                    wgrad_C=C if mx_wgrad else 0)
+    for r in range(EP):
+        y, dx, ds, dwg, dwu, dwd = results[r]
+        sl, es = slice(r * T, (r + 1) * T), slice(r * El, (r + 1) * El)
+        errs = {"y": rel_err(y, y_ref[sl]), "dx": rel_err(dx, dx_ref[sl]), "dscore": rel_err(ds, ds_ref[sl]),
+                "dw_gate": rel_err(dwg, dwg_ref[es]), "dw_up": rel_err(dwu, dwu_ref[es]),
+                "dw_down": rel_err(dwd, dwd_ref[es])}
+        assert all(v <= MX_TOL for v in errs.values()), (r, errs)
