@@ -227,6 +227,13 @@ memfine_status memfine_register_workspace(memfine_handle_t h, void* ws, uint64_t
 memfine_status memfine_route_counts(memfine_handle_t h, const int32_t* ids_dev, int32_t nsub,
                                     int32_t* counts_dev, void* stream);
 
+/* m_g of Eq. 2 (§3): the number of micro-batches whose activations a pipeline stage
+ * holds, m_g = v*p + p - 2*r_pp - 1 for virtual-pipeline size v, pipeline size p and stage r_pp
+ * (0-based; reading R29), and m_g = 1 under full recomputation (full_recompute != 0).  MACT's s'_max
+ * is per PP stage: pass the result as memfine_budget.m_g of that stage's plan.
+ * v >= 1, p >= 1, 0 <= r_pp < p, else MEMFINE_ERR_INVALID_ARG. */
+memfine_status memfine_m_g(int32_t v, int32_t p, int32_t r_pp, int32_t full_recompute, int32_t* m_g);
+
 /* A3 (MACT): choose C from the counts.  counts: int32
  * [EP][nsub][E], HOST or DEVICE memory (detected).  Device counts are evaluated
  * by the library's single-CTA tuner kernel on the current device (one D2H of the

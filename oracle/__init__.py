@@ -343,3 +343,8 @@ def moe_mx_tokens(d: Dims, toks, x, dy, ids, w, wg, wu, wd, mode: int = 1):
                                     _p(w), _p(wg), _p(wu), _p(wd), _p(y), _p(dx), _p(ds))
     assert st == 0
     return y, dx, ds
+
+
+def m_g(v: int, p: int, r_pp: int, full_recompute: bool = False) -> int:
+    """Eq. 2's m_g: v p + p - 2 r_pp - 1, or 1 under full recomputation."""
+    return int(lib().oracle_m_g(C.c_int32(v), C.c_int32(p), C.c_int32(r_pp), C.c_int32(int(bool(full_recompute)))))

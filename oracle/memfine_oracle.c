@@ -1117,6 +1117,14 @@ int32_t oracle_moe_mx_tokens(const oracle_dims* d, int32_t mode, int64_t ntok, c
     return 0;
 }
 
+/* Eq. 2's m_g (§3): "Generally, m_g = (v p + p - 2 r_pp - 1), and when full
+ * recomputation is employed, then m_g = 1."  r_pp: the pipeline stage, 0-based (reading R29). */
+int32_t oracle_m_g(int32_t v, int32_t p, int32_t r_pp, int32_t full_recompute)
+{
+    if (full_recompute) return 1;
+    return v * p + p - 2 * r_pp - 1;
+}
+
 int32_t oracle_version(void) { return 1; }
 
 #ifdef _OPENMP

@@ -22,7 +22,7 @@ SYMBOLS = ("memfine_abi_version", "memfine_status_str", "memfine_nccl_unique_id"
            "memfine_destroy", "memfine_local_group_create", "memfine_local_group_destroy", "memfine_create_local", "memfine_set_ep_transport", "memfine_set_comm_sms", "memfine_register_workspace", "memfine_route_counts", "memfine_plan", "memfine_workspace_bytes", "memfine_a2a_plan",
            "memfine_moe_fwd", "memfine_moe_bwd", "memfine_router_fwd", "memfine_router_bwd", "memfine_sync", "memfine_last_stats",
            "memfine_profile_enable", "memfine_profile_read", "memfine_set_debug", "memfine_debug_perm",
-           "memfine_mx_weights_bytes", "memfine_mx_quantize_weights", "memfine_mx_quantize")
+           "memfine_mx_weights_bytes", "memfine_mx_quantize_weights", "memfine_mx_quantize", "memfine_m_g")
 
 PROF_SLOTS = ("gemm_gateup_swiglu", "gemm_down", "gemm_dact_epilogue", "gemm_dx", "gemm_wgrad_down",
               "gemm_wgrad_gateup", "dispatch_permute", "combine_unpermute", "memset", "nccl_exchange",

@@ -1247,6 +1247,13 @@ extern "C" {
 
 int32_t memfine_abi_version(void) { return MEMFINE_ABI_VERSION; }
 
+memfine_status memfine_m_g(int32_t v, int32_t p, int32_t r_pp, int32_t full_recompute, int32_t* m_g) {
+  if (!m_g || v < 1 || p < 1 || r_pp < 0 || r_pp >= p) return MEMFINE_ERR_INVALID_ARG;
+  // m_g = v p + p - 2 r_pp - 1 (>= 1 for 0 <= r_pp < p); 1 under full recomputation
+  *m_g = full_recompute ? 1 : v * p + p - 2 * r_pp - 1;
+  return MEMFINE_OK;
+}
+
 const char* memfine_status_str(memfine_status s) {
   switch (s) {
     case MEMFINE_OK: return "ok";

@@ -55,6 +55,14 @@ def mx_quantize(src: torch.Tensor, stream=None):
     return codes, scales
 
 
+def m_g(v: int, p: int, r_pp: int, full_recompute: bool = False) -> int:
+    """memfine_m_g: Eq. 2's m_g for pipeline stage r_pp (1 under full recomputation)."""
+    out = C.c_int32()
+    capi.check(capi.lib().memfine_m_g(int(v), int(p), int(r_pp), int(bool(full_recompute)), C.byref(out)),
+               "memfine_m_g")
+    return int(out.value)
+
+
 def plan(counts: torch.Tensor, dims: capi.Dims, budget: capi.Budget) -> dict:
     """memfine_plan: counts int32 [EP][nsub][E] on the host (CPU tensor) or the device."""
     assert counts.dtype == torch.int32 and counts.dim() == 3 and counts.is_contiguous()

@@ -197,3 +197,16 @@ def test_impl_model_picks_smallest_fitting_bin():
         b = capi.make_budget(static + ws[C_] - 1, 1.0, static, 0, model=capi.MODEL_IMPL)
         p = layer.plan(counts, dims0, b)
         assert p["C"] == (C_ * 2 if C_ < 8 else 8) and (p["clamped"] == (C_ == 8))
+
+
+def test_m_g_matches_oracle_and_validates():
+    import oracle
+    oracle.build()
+    for v in range(1, 4):
+        for p in range(1, 9):
+            for r in range(p):
+                for fr in (False, True):
+                    assert layer.m_g(v, p, r, fr) == oracle.m_g(v, p, r, fr)
+    out = C.c_int32()
+    for bad in ((0, 4, 0), (1, 0, 0), (1, 4, 4), (1, 4, -1)):
+        assert capi.lib().memfine_m_g(*bad, 0, C.byref(out)) == capi.ERR_INVALID_ARG

@@ -458,3 +458,21 @@ def test_router_ties_and_finite_differences(oracle_lib):
             am[idx] -= eps
             num = (f(ap, wr) - f(am, wr)) / (2 * eps) if arr is x else (f(x, ap) - f(x, am)) / (2 * eps)
             assert abs(num - an[idx]) <= 1e-6 * max(1.0, abs(an[idx]))
+
+
+def test_m_g_pipeline_stage_pins():
+    """Eq. 2's m_g (reading R29): full recomputation holds one micro-batch; without
+    pipelining (p = 1, v = 1) one micro-batch is live; the last stage of a plain 1F1B pipeline
+    (v = 1, r_pp = p - 1) runs each forward straight into its backward, so it holds one; every
+    stage earlier holds two more; every extra virtual stage adds p."""
+    import oracle
+    oracle.build()
+    assert oracle.m_g(3, 8, 5, full_recompute=True) == 1
+    assert oracle.m_g(1, 1, 0) == 1
+    for p in range(1, 9):
+        assert oracle.m_g(1, p, p - 1) == 1
+        for r in range(p - 1):
+            assert oracle.m_g(1, p, r) == oracle.m_g(1, p, r + 1) + 2
+        for v in range(1, 4):
+            for r in range(p):
+                assert oracle.m_g(v + 1, p, r) == oracle.m_g(v, p, r) + p
