@@ -22,6 +22,9 @@ python bench.py --config qwen3 --placement contiguous --sweep 0 --mx 0 --no-cpu-
 # config 5 and the MACT-over-training comparison (Methods 1-3)
 timeout 900 python tools/budget_sweep.py > "$out/budget_sweep.json" 2> "$out/budget_sweep.err"
 timeout 1200 python tools/mact_over_training.py > "$out/mact.json" 2> "$out/mact.err"
+# energy per FLOP at the power cap (cuBLAS vs the layer, sustained) and per-clock GEMM efficiency
+timeout 600 python tools/sustained_clock.py > "$out/sustained.json" 2> "$out/sustained.err"
+timeout 600 python tools/gemm_vs_cublas.py > "$out/gemm_vs_cublas.json" 2> "$out/gemm_vs_cublas.err"
 # ncu: launch list of the bench command, then one full capture (DRAM bytes per launch)
 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file "$out/launches.csv" \
   python bench.py --steps 2 --warmup 1 --mx 0 --sweep 0 --no-cpu-baseline > /dev/null 2>&1
