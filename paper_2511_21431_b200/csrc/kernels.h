@@ -90,6 +90,14 @@ template <typename T>
 void launch_router_bwd(const T* x, const T* wr, const int32_t* ids, const float* scores, const float* dscore,
                        int64_t ntok, int E, int h, int k, float* dlog, T* dx, int acc_dx, float* dwr, int acc_dw,
                        const ChunkMeta& m, cudaStream_t st);
+// bf16: logits and dW_r as cuBLAS GEMMs (cublas = a cublasHandle_t); nonzero return = a cuBLAS failure.
+// dhi/dlo: [T][E] bf16 scratch for the dense d_logits (hi + lo).
+int launch_router_fwd_bf16(void* cublas, const __nv_bfloat16* x, const __nv_bfloat16* wr, int64_t ntok, int E,
+                           int h, int k, float* logits, int32_t* ids, float* scores, cudaStream_t st);
+int launch_router_bwd_bf16(void* cublas, const __nv_bfloat16* x, const __nv_bfloat16* wr, const int32_t* ids,
+                           const float* scores, const float* dscore, int64_t ntok, int E, int h, int k, float* dlog,
+                           __nv_bfloat16* dhi, __nv_bfloat16* dlo, __nv_bfloat16* dx, int acc_dx, float* dwr,
+                           int acc_dw, cudaStream_t st);
 
 // ---------------------------------------------------------------- MACT tuner (A3)
 struct PlanParams {

@@ -1,5 +1,6 @@
 // memfine.cu — the C ABI of libmemfine.so: handle, MACT plan, workspace carving and the
 // FCDA chunk loops (Eq. 6 forward, Eq. 7 recompute backward).
+#include <cublas_v2.h>
 #include <nvtx3/nvToolsExt.h>
 #include <cstdio>
 #include <cstdlib>
@@ -60,6 +61,7 @@ struct memfine_handle_s {
   // router scratch (lazily allocated): logits, d_logits, counting sort of ids by expert
   char* router_scratch = nullptr;
   size_t router_bytes = 0;
+  void* cublas = nullptr;          // cublasHandle_t for the bf16 router GEMMs (created on first use)
   int device = 0;
   int num_sms = 148;
   int* status_h = nullptr;     // pinned, mapped: device-latched error word
@@ -1427,6 +1429,7 @@ memfine_status memfine_destroy(memfine_handle_t h) {
   if (!h) return MEMFINE_ERR_INVALID_ARG;
   if (h->tab_h) cudaFreeHost(h->tab_h);
   if (h->router_scratch) cudaFree(h->router_scratch);
+  if (h->cublas) cublasDestroy((cublasHandle_t)h->cublas);
   for (void* b : h->ipc_bases) cudaIpcCloseMemHandle(b);
   if (h->barrier_d) cudaFree(h->barrier_d);
   if (h->comm.comm) nccl_comm_destroy(&h->comm);
@@ -1717,6 +1720,8 @@ namespace {
 struct RouterScratch {
   float* logits;
   float* dlog;
+  __nv_bfloat16* dhi;   // bf16 path: dense d_logits [T][E] as hi + lo
+  __nv_bfloat16* dlo;
   ChunkMeta m;
   int64_t rows_cap;
 };
@@ -1728,6 +1733,8 @@ memfine_status router_scratch(memfine_handle_s* h, RouterScratch* rs) {
   Bump b(nullptr);
   b.take<float>((uint64_t)T * E);
   b.take<float>((uint64_t)T * k);
+  b.take<__nv_bfloat16>((uint64_t)T * E);
+  b.take<__nv_bfloat16>((uint64_t)T * E);
   b.take<int>((uint64_t)NB * E);
   for (int i = 0; i < 3; i++) b.take<int>(E + 1);
   b.take<int>(E + 1);
@@ -1744,6 +1751,8 @@ memfine_status router_scratch(memfine_handle_s* h, RouterScratch* rs) {
   Bump c(h->router_scratch);
   rs->logits = c.take<float>((uint64_t)T * E);
   rs->dlog = c.take<float>((uint64_t)T * k);
+  rs->dhi = c.take<__nv_bfloat16>((uint64_t)T * E);
+  rs->dlo = c.take<__nv_bfloat16>((uint64_t)T * E);
   rs->m = ChunkMeta{};
   rs->m.blk_cnt = c.take<int>((uint64_t)NB * E);
   rs->m.exp_cnt = c.take<int>(E + 1);
@@ -1754,6 +1763,11 @@ memfine_status router_scratch(memfine_handle_s* h, RouterScratch* rs) {
   rs->m.dest_of = c.take<int>((uint64_t)T * k);
   rs->m.src_of = c.take<int>((uint64_t)rows_cap);
   rs->rows_cap = rows_cap;
+  if (d.dtype != MEMFINE_FP32 && !h->cublas) {
+    cublasHandle_t cb = nullptr;
+    if (cublasCreate(&cb) != CUBLAS_STATUS_SUCCESS) return MEMFINE_ERR_CUDA;
+    h->cublas = cb;
+  }
   return MEMFINE_OK;
 }
 }  // namespace
@@ -1766,10 +1780,11 @@ memfine_status memfine_router_fwd(memfine_handle_t h, const void* x, const void*
   RouterScratch rs;
   if (int rc = router_scratch(h, &rs)) return (memfine_status)rc;
   float* lg = logits ? logits : rs.logits;
-  if (d.dtype != MEMFINE_FP32)
-    launch_router_fwd<__nv_bfloat16>((const __nv_bfloat16*)x, (const __nv_bfloat16*)w_router, d.tokens,
-                                     d.num_experts, d.hidden, d.topk, lg, ids, scores, st);
-  else
+  if (d.dtype != MEMFINE_FP32) {
+    if (launch_router_fwd_bf16(h->cublas, (const __nv_bfloat16*)x, (const __nv_bfloat16*)w_router, d.tokens,
+                               d.num_experts, d.hidden, d.topk, lg, ids, scores, st))
+      return MEMFINE_ERR_CUDA;
+  } else
     launch_router_fwd<float>((const float*)x, (const float*)w_router, d.tokens, d.num_experts, d.hidden, d.topk, lg,
                              ids, scores, st);
   return latch_cuda(h);
@@ -1785,7 +1800,14 @@ memfine_status memfine_router_bwd(memfine_handle_t h, const void* x, const void*
   RouterScratch rs;
   if (int rc = router_scratch(h, &rs)) return (memfine_status)rc;
   const int E = d.num_experts, k = d.topk;
-  // counting sort of the copies by expert (stable): segment e = rows [seg[e], seg[e] + cnt[e])
+  if (d.dtype != MEMFINE_FP32) {
+    if (launch_router_bwd_bf16(h->cublas, (const __nv_bfloat16*)x, (const __nv_bfloat16*)w_router, ids, scores,
+                               dscore, d.tokens, E, d.hidden, k, rs.dlog, rs.dhi, rs.dlo, (__nv_bfloat16*)dx,
+                               accumulate_dx, dw_router, accumulate_dw, st))
+      return MEMFINE_ERR_CUDA;
+    return latch_cuda(h);
+  }
+  // fp32: counting sort of the copies by expert (stable): segment e = rows [seg[e], seg[e] + cnt[e])
   int NB = (int)ceil_div64(d.tokens, kTokPerBlk);
   if (NB) {
     launch_dispatch_hist(ids, 0, d.tokens, k, E, rs.m, h->status_d, st);
@@ -1795,12 +1817,7 @@ memfine_status memfine_router_bwd(memfine_handle_t h, const void* x, const void*
     MF_CUDA_OK(cudaMemsetAsync(rs.m.seg, 0, sizeof(int) * (E + 1), st));
     MF_CUDA_OK(cudaMemsetAsync(rs.m.recv_cnt, 0, sizeof(int) * (E + 1), st));
   }
-  if (d.dtype != MEMFINE_FP32)
-    launch_router_bwd<__nv_bfloat16>((const __nv_bfloat16*)x, (const __nv_bfloat16*)w_router, ids, scores, dscore,
-                                     d.tokens, E, d.hidden, k, rs.dlog, (__nv_bfloat16*)dx, accumulate_dx, dw_router,
-                                     accumulate_dw, rs.m, st);
-  else
-    launch_router_bwd<float>((const float*)x, (const float*)w_router, ids, scores, dscore, d.tokens, E, d.hidden, k,
+  launch_router_bwd<float>((const float*)x, (const float*)w_router, ids, scores, dscore, d.tokens, E, d.hidden, k,
                              rs.dlog, (float*)dx, accumulate_dx, dw_router, accumulate_dw, rs.m, st);
   return latch_cuda(h);
 }

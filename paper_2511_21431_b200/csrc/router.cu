@@ -2,6 +2,7 @@
 // PAPER.md:83-84): logits = x W_r^T (fp32 accumulate), the k largest logits (ties: lower expert id),
 // scores = softmax over the k selected logits; and its backward consuming the layer's d_score.
 #include <algorithm>
+#include <cublas_v2.h>
 #include "kernels.h"
 
 namespace memfine {
@@ -90,12 +91,17 @@ __global__ void __launch_bounds__(256) router_topk_kernel(const float* __restric
 
 // ------------------------------------------------------------------ backward, one warp per token
 // d_logit_j = s_j (ds_j - sum_q s_q ds_q) on the selected slots; dx = sum_j d_logit_j W_r[id_j].
+// dense (bf16 path): the [T][E] d_logits as an exact-to-2^-17 bf16 pair hi + lo (zero off the selected
+// slots), the operands of the dW_r GEMM.  dx moves 16 B per lane when h allows.
 template <typename T>
 __global__ void __launch_bounds__(256) router_bwd_rows_kernel(const T* __restrict__ wr, const int32_t* __restrict__ ids,
                                                               const float* __restrict__ scores,
                                                               const float* __restrict__ dscore, int64_t ntok, int k,
-                                                              int h, float* __restrict__ dlog, T* __restrict__ dx,
+                                                              int h, int E, float* __restrict__ dlog,
+                                                              __nv_bfloat16* __restrict__ dhi,
+                                                              __nv_bfloat16* __restrict__ dlo, T* __restrict__ dx,
                                                               int accumulate) {
+  constexpr int V = 16 / sizeof(T);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t t = (int64_t)blockIdx.x * (blockDim.x >> 5) + warp;
   if (t >= ntok) return;
@@ -107,6 +113,41 @@ __global__ void __launch_bounds__(256) router_bwd_rows_kernel(const T* __restric
     dl[j] = scores[t * k + j] * (dscore[t * k + j] - dot);
     id[j] = ids[t * k + j];
     if (lane == 0) dlog[t * k + j] = dl[j];
+  }
+  if (dhi) {
+    for (int e = lane; e < E; e += 32) {
+      float v = 0.f;
+      for (int j = 0; j < k; j++) v = (id[j] == e) ? dl[j] : v;
+      const __nv_bfloat16 hi = __float2bfloat16(v);
+      dhi[t * E + e] = hi;
+      dlo[t * E + e] = __float2bfloat16(v - __bfloat162float(hi));
+    }
+  }
+  if (h % V == 0) {
+    for (int c = lane * V; c < h; c += 32 * V) {
+      float acc[V];
+      if (accumulate) {
+        const uint4 u = *reinterpret_cast<const uint4*>(dx + t * h + c);
+        const T* pv = reinterpret_cast<const T*>(&u);
+#pragma unroll
+        for (int i = 0; i < V; i++) acc[i] = Elt<T>::to_f(pv[i]);
+      } else {
+#pragma unroll
+        for (int i = 0; i < V; i++) acc[i] = 0.f;
+      }
+      for (int j = 0; j < k; j++) {
+        const uint4 u = __ldg(reinterpret_cast<const uint4*>(wr + (int64_t)id[j] * h + c));
+        const T* pv = reinterpret_cast<const T*>(&u);
+#pragma unroll
+        for (int i = 0; i < V; i++) acc[i] = fmaf(dl[j], Elt<T>::to_f(pv[i]), acc[i]);
+      }
+      uint4 o;
+      T* po = reinterpret_cast<T*>(&o);
+#pragma unroll
+      for (int i = 0; i < V; i++) po[i] = Elt<T>::from_f(acc[i]);
+      *reinterpret_cast<uint4*>(dx + t * h + c) = o;
+    }
+    return;
   }
   for (int c = lane; c < h; c += 32) {
     float acc = accumulate ? Elt<T>::to_f(dx[t * h + c]) : 0.f;
@@ -143,13 +184,54 @@ void launch_router_fwd(const T* x, const T* wr, int64_t ntok, int E, int h, int 
   router_topk_kernel<<<(unsigned)ceil_div64(ntok, 8), 256, 0, st>>>(logits, ntok, E, k, ids, scores);
 }
 
+// bf16: the logits are a plain dense GEMM (bf16 operands, fp32 accumulate and output) - cuBLAS on the
+// tensor cores.  Row-major logits [T][E] = column-major [E][T] = W_r (op T of the column-major [h][E]
+// view of W_r [E][h]) x x^T (column-major [h][T] view of x [T][h]).
+int launch_router_fwd_bf16(void* cublas, const __nv_bfloat16* x, const __nv_bfloat16* wr, int64_t ntok, int E,
+                           int h, int k, float* logits, int32_t* ids, float* scores, cudaStream_t st) {
+  if (ntok == 0) return 0;
+  cublasHandle_t cb = (cublasHandle_t)cublas;
+  const float one = 1.f, zero = 0.f;
+  if (cublasSetStream(cb, st) != CUBLAS_STATUS_SUCCESS) return 1;
+  if (cublasGemmEx(cb, CUBLAS_OP_T, CUBLAS_OP_N, E, (int)ntok, h, &one, wr, CUDA_R_16BF, h, x, CUDA_R_16BF, h,
+                   &zero, logits, CUDA_R_32F, E, CUBLAS_COMPUTE_32F, CUBLAS_GEMM_DEFAULT) != CUBLAS_STATUS_SUCCESS)
+    return 1;
+  router_topk_kernel<<<(unsigned)ceil_div64(ntok, 8), 256, 0, st>>>(logits, ntok, E, k, ids, scores);
+  return 0;
+}
+
+// bf16 backward: dx by the row kernel; dW_r (row-major [E][h] = column-major [h][E]) = x^T D with D the
+// dense d_logits [T][E] (column-major [E][T], op T), as two accumulating GEMMs over its hi and lo halves.
+int launch_router_bwd_bf16(void* cublas, const __nv_bfloat16* x, const __nv_bfloat16* wr, const int32_t* ids,
+                           const float* scores, const float* dscore, int64_t ntok, int E, int h, int k, float* dlog,
+                           __nv_bfloat16* dhi, __nv_bfloat16* dlo, __nv_bfloat16* dx, int acc_dx, float* dwr,
+                           int acc_dw, cudaStream_t st) {
+  if (ntok > 0)
+    router_bwd_rows_kernel<__nv_bfloat16><<<(unsigned)ceil_div64(ntok, 8), 256, 0, st>>>(
+        wr, ids, scores, dscore, ntok, k, h, E, dlog, dhi, dlo, dx, acc_dx);
+  if (ntok == 0) {
+    if (!acc_dw) return cudaMemsetAsync(dwr, 0, sizeof(float) * (size_t)E * h, st) != cudaSuccess;
+    return 0;
+  }
+  cublasHandle_t cb = (cublasHandle_t)cublas;
+  const float one = 1.f, beta0 = acc_dw ? 1.f : 0.f;
+  if (cublasSetStream(cb, st) != CUBLAS_STATUS_SUCCESS) return 1;
+  if (cublasGemmEx(cb, CUBLAS_OP_N, CUBLAS_OP_T, h, E, (int)ntok, &one, x, CUDA_R_16BF, h, dhi, CUDA_R_16BF, E,
+                   &beta0, dwr, CUDA_R_32F, h, CUBLAS_COMPUTE_32F, CUBLAS_GEMM_DEFAULT) != CUBLAS_STATUS_SUCCESS)
+    return 1;
+  if (cublasGemmEx(cb, CUBLAS_OP_N, CUBLAS_OP_T, h, E, (int)ntok, &one, x, CUDA_R_16BF, h, dlo, CUDA_R_16BF, E,
+                   &one, dwr, CUDA_R_32F, h, CUBLAS_COMPUTE_32F, CUBLAS_GEMM_DEFAULT) != CUBLAS_STATUS_SUCCESS)
+    return 1;
+  return 0;
+}
+
 template <typename T>
 void launch_router_bwd(const T* x, const T* wr, const int32_t* ids, const float* scores, const float* dscore,
                        int64_t ntok, int E, int h, int k, float* dlog, T* dx, int acc_dx, float* dwr, int acc_dw,
                        const ChunkMeta& m, cudaStream_t st) {
   if (ntok > 0)
-    router_bwd_rows_kernel<T><<<(unsigned)ceil_div64(ntok, 8), 256, 0, st>>>(wr, ids, scores, dscore, ntok, k, h,
-                                                                             dlog, dx, acc_dx);
+    router_bwd_rows_kernel<T><<<(unsigned)ceil_div64(ntok, 8), 256, 0, st>>>(wr, ids, scores, dscore, ntok, k, h, E,
+                                                                             dlog, nullptr, nullptr, dx, acc_dx);
   dim3 grid((unsigned)E, (unsigned)ceil_div64(h, 256));
   router_dw_kernel<T><<<grid, 256, 0, st>>>(x, dlog, m.seg, m.recv_cnt, m.src_of, k, h, dwr, acc_dw);
 }
