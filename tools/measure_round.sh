@@ -25,6 +25,7 @@ timeout 1200 python tools/mact_over_training.py > "$out/mact.json" 2> "$out/mact
 # energy per FLOP at the power cap (cuBLAS vs the layer, sustained) and per-clock GEMM efficiency
 timeout 600 python tools/sustained_clock.py > "$out/sustained.json" 2> "$out/sustained.err"
 timeout 600 python tools/gemm_vs_cublas.py > "$out/gemm_vs_cublas.json" 2> "$out/gemm_vs_cublas.err"
+timeout 300 python tools/router_bench.py > "$out/router.json" 2> "$out/router.err"
 # ncu: launch list of the bench command, then one full capture (DRAM bytes per launch)
 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file "$out/launches.csv" \
   python bench.py --steps 2 --warmup 1 --mx 0 --sweep 0 --no-cpu-baseline > /dev/null 2>&1
