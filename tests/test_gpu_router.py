@@ -75,3 +75,51 @@ def test_router_fwd_bwd(dtype, T, h, E, k):
     assert mf.sync() == 0
     assert rel_err(dwr2.cpu().numpy(), rdw) <= t_
     assert rel_err(dx2.float().cpu().numpy(), rdx) <= t_
+
+
+@pytest.mark.parametrize("T,h,E,k,bwd", [(16384, 4096, 8, 2, True), (8192, 7168, 256, 8, False)])
+def test_router_full_size(T, h, E, k, bwd):
+    """BASELINE sizes (Mixtral, DSv3) in bf16, the launch configuration tools/router_bench.py times:
+    logits / ids / scores on a sample of tokens (rows are independent); dx and dW_r over all tokens
+    at the Mixtral size (the oracle's dW_r loop is O(E T h): ~40 s at the DSv3 size, so there the
+    backward is covered by the small cases above)."""
+    dev = "cuda:0"
+    dtype = torch.bfloat16
+    x = synth.make_x(T, h, rank=5, dtype=dtype)
+    gen = torch.Generator().manual_seed(13)
+    wr = (torch.randn(E, h, generator=gen) / h ** 0.5).to(dtype)
+    mf = layer.MemFine(T, h, 64, E, k, dtype=dtype)
+    logits = torch.empty((T, E), dtype=torch.float32, device=dev)
+    xd, wd = x.to(dev), wr.to(dev)
+    ids, scores = mf.router_fwd(xd, wd, logits=logits)
+    assert mf.sync() == 0
+    rng = np.random.default_rng(T)
+    sample = np.unique(np.concatenate([[0, T - 1], rng.choice(T, 384, replace=False)]))
+    d = oracle.Dims(T=len(sample), h=h, g=1, E=E, k=k, in_dtype="bf16")
+    xs = _np(x, dtype)[sample]
+    ref_logits, _, _ = oracle.router_forward(d, xs, _np(wr, dtype))
+    assert rel_err(logits.cpu().numpy()[sample], ref_logits) <= 1e-5
+    g_ids = ids.cpu().numpy()
+    eps = 1e-5 * np.abs(ref_logits).max()
+    for i, t in enumerate(sample):
+        sel = g_ids[t]
+        assert len(set(sel.tolist())) == k and sel.min() >= 0 and sel.max() < E
+        rest = np.setdiff1d(np.arange(E), sel)
+        assert ref_logits[i, sel].min() >= ref_logits[i, rest].max() - eps
+    sl = np.take_along_axis(ref_logits, g_ids[sample].astype(np.int64), 1)
+    sl = np.exp(sl - sl.max(1, keepdims=True))
+    assert rel_err(scores.cpu().numpy()[sample], sl / sl.sum(1, keepdims=True)) <= 1e-5
+    if not bwd:
+        return
+    # backward over all tokens (dW_r needs every row)
+    ds = torch.from_numpy(np.random.default_rng(3).standard_normal((T, k)).astype(np.float32))
+    dx, dwr = mf.router_bwd(xd, wd, ids, scores, ds.to(dev))
+    assert mf.sync() == 0
+    dfull = oracle.Dims(T=T, h=h, g=1, E=E, k=k, in_dtype="bf16")
+    rdx, rdw = oracle.router_backward(dfull, _np(x, dtype), _np(wr, dtype), g_ids,
+                                      scores.cpu().numpy().astype(np.float64), ds.numpy().astype(np.float64))
+    e_dx = rel_err(dx.float().cpu().numpy(), rdx)
+    e_dw = rel_err(dwr.cpu().numpy(), rdw)
+    print(f"router full size T={T} E={E}: dx rel {e_dx:.2e}, dW_r rel {e_dw:.2e}")
+    assert e_dx <= tol(dtype)
+    assert e_dw <= tol(dtype)
