@@ -108,7 +108,14 @@ def test_router_full_size(T, h, E, k, bwd):
         assert ref_logits[i, sel].min() >= ref_logits[i, rest].max() - eps
     sl = np.take_along_axis(ref_logits, g_ids[sample].astype(np.int64), 1)
     sl = np.exp(sl - sl.max(1, keepdims=True))
-    assert rel_err(scores.cpu().numpy()[sample], sl / sl.sum(1, keepdims=True)) <= 1e-5
+    sref = sl / sl.sum(1, keepdims=True)
+    # softmax is 2-Lipschitz per score in the max logit error: |ds_j| <= s_j (|dl_j| + sum_q s_q |dl_q|)
+    # <= 2 s_j max|dl|, so the scores' bound follows from the logits' measured error (K = h long sums
+    # on the tensor cores put max|dl| at a few 1e-5 at the DSv3 size)
+    dl = np.abs(logits.cpu().numpy()[sample] - ref_logits).max()
+    e_s = np.abs(scores.cpu().numpy()[sample] - sref).max()
+    print(f"router full size T={T} E={E}: max|dlogit| {dl:.2e}, max|dscore| {e_s:.2e}")
+    assert e_s <= 2 * dl * sref.max() + 1e-6
     if not bwd:
         return
     # backward over all tokens (dW_r needs every row)
