@@ -130,3 +130,42 @@ def test_router_full_size(T, h, E, k, bwd):
     print(f"router full size T={T} E={E}: dx rel {e_dx:.2e}, dW_r rel {e_dw:.2e}")
     assert e_dx <= tol(dtype)
     assert e_dw <= tol(dtype)
+
+
+@pytest.mark.parametrize("T,h,E,k", [(0, 64, 8, 2), (1, 64, 1, 1), (5, 128, 33, 16), (130, 64, 1024, 3)])
+def test_router_edges(T, h, E, k):
+    """Degenerate router shapes in bf16 (the cuBLAS path): no tokens (dW_r overwritten with zeros or
+    left as is), one expert, k = 16 (the largest the kernels take), E = 1024 (the top-k mask's limit)."""
+    dev = "cuda:0"
+    dtype = torch.bfloat16
+    x = synth.make_x(max(T, 1), h, rank=6, dtype=dtype)[:T]
+    gen = torch.Generator().manual_seed(17)
+    wr = (torch.randn(E, h, generator=gen) / h ** 0.5).to(dtype)
+    mf = layer.MemFine(T, h, 64, E, k, dtype=dtype)
+    xd, wd = x.to(dev), wr.to(dev)
+    ids, scores = mf.router_fwd(xd, wd)
+    ds = torch.from_numpy(np.random.default_rng(4).standard_normal((T, k)).astype(np.float32)).to(dev)
+    dw0 = torch.randn(E, h, generator=gen).to(dev)
+    dx, dwr = mf.router_bwd(xd, wd, ids, scores, ds, dw_router=dw0.clone(), accumulate_dw=True)
+    dx2, dwr2 = mf.router_bwd(xd, wd, ids, scores, ds, dw_router=torch.full((E, h), 7.0, device=dev))
+    assert mf.sync() == 0
+    if T == 0:
+        assert torch.equal(dwr, dw0) and not dwr2.any()
+        return
+    d = oracle.Dims(T=T, h=h, g=1, E=E, k=k, in_dtype="bf16")
+    ref_logits, ref_ids, _ = oracle.router_forward(d, _np(x, dtype), _np(wr, dtype))
+    g_ids = ids.cpu().numpy()
+    eps = 1e-5 * np.abs(ref_logits).max()
+    for t in range(T):
+        sel = g_ids[t]
+        assert len(set(sel.tolist())) == k and sel.min() >= 0 and sel.max() < E
+        rest = np.setdiff1d(np.arange(E), sel)
+        if len(rest):
+            assert ref_logits[t, sel].min() >= ref_logits[t, rest].max() - eps
+    if E == 1:
+        assert torch.equal(scores.cpu(), torch.ones(T, 1))
+    rdx, rdw = oracle.router_backward(d, _np(x, dtype), _np(wr, dtype), g_ids,
+                                      scores.cpu().numpy().astype(np.float64), ds.cpu().numpy().astype(np.float64))
+    assert rel_err(dwr.cpu().numpy(), dw0.cpu().numpy() + rdw) <= tol(dtype)
+    assert rel_err(dwr2.cpu().numpy(), rdw) <= tol(dtype) or (not rdw.any() and not dwr2.any())
+    assert rel_err(dx2.float().cpu().numpy(), rdx) <= tol(dtype) or (not rdx.any() and not dx2.float().any())
