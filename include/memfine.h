@@ -305,7 +305,12 @@ memfine_status memfine_moe_bwd(memfine_handle_t h, const void* dy, const void* x
  *   logits = x W_r^T (fp32 accumulation), ids = the k largest logits (ties: lower expert id),
  *   scores = softmax over the k selected logits (the renormalised top-k convention).
  *   x dev [T][h], w_router dev [E][h] (dims.dtype, replicated on every EP rank), ids dev int32
- *   [T][k], scores dev fp32 [T][k], logits dev fp32 [T][E] (nullable: library scratch). */
+ *   [T][k], scores dev fp32 [T][k], logits dev fp32 [T][E] (nullable: library scratch).
+ *   BF16/MXFP8 handles: the logits GEMM (and the backward's dW_r GEMMs) run on cuBLAS (bf16 in, fp32
+ *   accumulate/out; a handle per memfine handle, created on first use - MEMFINE_ERR_CUDA if that or a
+ *   cuBLAS call fails); top-k, softmax and the backward's row kernel are the library's.  FP32 handles
+ *   use the library's CUDA-core GEMM (fp32 FMA, no TF32).  Stream-ordered; not graph-capture safe on
+ *   the first call of a handle (it allocates scratch and the cuBLAS handle). */
 memfine_status memfine_router_fwd(memfine_handle_t h, const void* x, const void* w_router, int32_t* ids,
                                   float* scores, float* logits, void* stream);
 /* Router backward from the layer's d_score (memfine_moe_bwd's dscore):
