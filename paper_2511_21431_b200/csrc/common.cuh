@@ -4,6 +4,8 @@
 #include <cuda_bf16.h>
 #include <cuda_fp8.h>
 #include <stdint.h>
+#include <stdlib.h>
+#include <utility>
 #include "../../include/memfine.h"
 
 namespace memfine {
@@ -48,6 +50,38 @@ template <> struct Elt<float> {
 
 // MUFU-based (ex2 + rcp, ~2 ulp): ample for bf16 outputs; the fp32-mode FFMA path uses the
 // IEEE-exact forms (1e-5 parity).
+// Programmatic dependent launch: a kernel launched with the PDL attribute may start while its
+// predecessor on the stream drains; pdl_wait() blocks until that predecessor has completed and its
+// memory is visible (a no-op without the attribute).  pdl_trigger() lets the successor launch early.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
+// PDL on the hot path's launches (MEMFINE_PDL=0 turns it off).
+inline bool use_pdl() {
+  static const int v = [] {
+    const char* s = getenv("MEMFINE_PDL");
+    return (s && s[0] == '0') ? 0 : 1;
+  }();
+  return v == 1;
+}
+// <<<grid, block, smem, st>>> with the PDL attribute: the kernel must call pdl_wait() before it
+// touches global memory a predecessor writes or reads.
+template <typename... KArgs, typename... Args>
+inline void launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                       Args&&... args) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute a[1];
+  a[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  a[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = a;
+  cfg.numAttrs = use_pdl() ? 1 : 0;
+  cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);   // errors surface via latch_cuda
+}
+
 __device__ __forceinline__ float silu_f(float z) { return __fdividef(z, 1.0f + __expf(-z)); }
 __device__ __forceinline__ float sigmoid_f(float z) { return __fdividef(1.0f, 1.0f + __expf(-z)); }
 __device__ __forceinline__ float silu_exact(float z) { return z / (1.0f + expf(-z)); }

@@ -604,6 +604,9 @@ __global__ void __launch_bounds__(THREADS, 1)
   if (PAIR) cluster_sync(); else __syncthreads();
   fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  // everything above (barrier init, TMEM alloc, descriptor prefetch) overlaps the predecessor's tail
+  pdl_wait();
+  pdl_trigger();
   const int ntiles = num_tiles<KIND, PAIR, MX>(p);
   (void)SF_COL;
 
@@ -1254,6 +1257,7 @@ int setup_pacing(Params& p, const GemmProblem<__nv_bfloat16>& gp, cudaStream_t s
 
 int g_num_sms = 0;
 
+
 bool use_pairs() {
   static int v = -1;
   if (v < 0) {
@@ -1403,13 +1407,15 @@ int launch(const GemmProblem<__nv_bfloat16>& gp, cudaStream_t st) {
   cfg.blockDim = dim3(THREADS);
   cfg.dynamicSmemBytes = SMEM;
   cfg.stream = st;
-  cudaLaunchAttribute attr[1];
+  cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributeClusterDimension;
   attr[0].val.clusterDim.x = per_unit;
   attr[0].val.clusterDim.y = 1;
   attr[0].val.clusterDim.z = 1;
+  attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = (use_pdl() && !p.wave_ctr) ? 2 : 1;   // (a pacing memset precedes a paced launch)
   CUtensorMap none;
   memset(&none, 0, sizeof none);
   if (cudaLaunchKernelEx(&cfg, gemm_kernel<KIND, PAIR>, p, mA, mB0, mB1, mO0, mO1, none, none, none) != cudaSuccess)
@@ -1611,13 +1617,15 @@ int launch_mx(const GemmProblem<__nv_bfloat16>& gp, cudaStream_t st) {
   cfg.blockDim = dim3(THREADS);
   cfg.dynamicSmemBytes = SMEM;
   cfg.stream = st;
-  cudaLaunchAttribute attr[1];
+  cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributeClusterDimension;
   attr[0].val.clusterDim.x = per_unit;
   attr[0].val.clusterDim.y = 1;
   attr[0].val.clusterDim.z = 1;
+  attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = use_pdl() ? 2 : 1;
   if (cudaLaunchKernelEx(&cfg, gemm_kernel<KIND, PAIR, true>, p, mA, mB0, mB1, mO0, mO1, mSA, mSB0, mSB1) !=
       cudaSuccess)
     return -1;

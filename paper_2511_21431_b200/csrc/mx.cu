@@ -14,6 +14,8 @@ __global__ void __launch_bounds__(256) mx_quant_rows_kernel(const __nv_bfloat16*
                                                             int64_t rows_max, const int* __restrict__ info,
                                                             int K, uint8_t* __restrict__ q,
                                                             uint8_t* __restrict__ sf) {
+  pdl_wait();
+  pdl_trigger();
   int64_t rows = rows_max;
   if (info) rows = __ldg(info + kInfoSkip) ? 0 : min(rows_max, (int64_t)__ldg(info + kInfoRowsPad));
   const int per_row = K >> 3;
@@ -129,6 +131,8 @@ __global__ void __launch_bounds__(256) mx_quant_dual_kernel(const __nv_bfloat16*
 // (blockIdx.z); tile 128 x 128 through smem; a warp quantises 32 adjacent columns of one 32-row
 // block (conflict-free shared-memory reads along a row).
 __global__ void __launch_bounds__(256) mx_quant_t_kernel(MxColTensors tz, const int* __restrict__ info, int64_t Rcap) {
+  pdl_wait();
+  pdl_trigger();
   const MxColTensor& tt = tz.t[blockIdx.z];
   if (blockIdx.z >= (unsigned)tz.n || (int)blockIdx.x * 128 >= tt.Cc) return;
   const int64_t rows = __ldg(info + kInfoSkip) ? 0 : min(Rcap, (int64_t)__ldg(info + kInfoRowsPad));
@@ -178,7 +182,7 @@ void launch_mx_quant_t(const MxColTensors& tz, const int* info, int64_t Rcap, cu
   for (int i = 0; i < tz.n; i++) cmax = std::max(cmax, tz.t[i].Cc);
   if (cmax <= 0 || Rcap <= 0 || tz.n <= 0) return;
   dim3 grid((unsigned)(cmax / 128), (unsigned)(Rcap / 128), (unsigned)tz.n);
-  mx_quant_t_kernel<<<grid, 256, 0, st>>>(tz, info, Rcap);
+  launch_pdl(mx_quant_t_kernel, dim3(grid), dim3(256), 0, st, tz, info, Rcap);
 }
 
 void launch_mx_quant_dual(const __nv_bfloat16* src, int B, int R, int Cc, uint8_t* q_rows, uint8_t* sf_rows,
@@ -193,7 +197,7 @@ void launch_mx_quant_rows(const __nv_bfloat16* src, int64_t ld, int64_t rows_max
   const int64_t n = rows_max * (K / 8);
   if (n <= 0) return;
   const int64_t blocks = std::min<int64_t>(ceil_div64(n, 256), (int64_t)sm100_num_sms() * 16);
-  mx_quant_rows_kernel<<<(unsigned)blocks, 256, 0, st>>>(src, ld, rows_max, info, K, q, sf);
+  launch_pdl(mx_quant_rows_kernel, dim3((unsigned)blocks), dim3(256), 0, st, src, ld, rows_max, info, K, q, sf);
 }
 
 

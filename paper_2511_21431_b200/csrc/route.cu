@@ -56,6 +56,8 @@ void launch_route_hist(const int32_t* ids, int64_t T, int k, int E, int nsub, in
 // ------------------------------------------------------------------------------------------
 __global__ void dispatch_hist_kernel(const int32_t* __restrict__ ids, int64_t t0, int64_t t1, int k, int E,
                                      int* __restrict__ blk_cnt, int* status) {
+  pdl_wait();
+  pdl_trigger();
   extern __shared__ int sc[];
   for (int e = threadIdx.x; e < E; e += blockDim.x) sc[e] = 0;
   __syncthreads();
@@ -74,7 +76,7 @@ void launch_dispatch_hist(const int32_t* ids, int64_t t0, int64_t t1, int k, int
                           int* status, cudaStream_t st) {
   int NB = (int)ceil_div64(t1 - t0, kTokPerBlk);
   if (NB == 0) return;
-  dispatch_hist_kernel<<<NB, 256, sizeof(int) * E, st>>>(ids, t0, t1, k, E, m.blk_cnt, status);
+  launch_pdl(dispatch_hist_kernel, dim3(NB), dim3(256), sizeof(int) * E, st, ids, t0, t1, k, E, m.blk_cnt, status);
 }
 
 // ------------------------------------------------------------------------------------------
@@ -97,6 +99,8 @@ __global__ void __launch_bounds__(1024) dispatch_scan_kernel(int NB, int E, int 
                                      int* __restrict__ blk, int* __restrict__ exp_cnt, int* __restrict__ recv_cnt,
                                      int* __restrict__ seg, int* __restrict__ pseg, int* __restrict__ info,
                                      int64_t* stats_rows, int64_t* stats_rows_pad, int chunk) {
+  pdl_wait();
+  pdl_trigger();
   __shared__ int base[1024];
   __shared__ int cnt_s[1024];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
@@ -179,7 +183,7 @@ __global__ void __launch_bounds__(1024) dispatch_scan_kernel(int NB, int E, int 
 
 void launch_dispatch_scan(int NB, int E, int El, int send_layout, int64_t rows_cap, const ChunkMeta& m,
                           int64_t* stats_rows, int64_t* stats_rows_pad, int chunk, cudaStream_t st) {
-  dispatch_scan_kernel<<<1, 1024, 0, st>>>(NB, E, El, send_layout, rows_cap, m.blk_cnt, m.exp_cnt, m.recv_cnt,
+  launch_pdl(dispatch_scan_kernel, dim3(1), dim3(1024), 0, st, NB, E, El, send_layout, rows_cap, m.blk_cnt, m.exp_cnt, m.recv_cnt,
                                            m.seg, m.pseg, m.info, stats_rows, stats_rows_pad, chunk);
 }
 
@@ -206,6 +210,8 @@ __global__ void __launch_bounds__(256) dispatch_index_kernel(
     const int32_t* __restrict__ ids, const float* __restrict__ w, int64_t t0, int64_t t1, int k, int E,
     const int* __restrict__ blk_off, int* __restrict__ dest_of, int* __restrict__ row_src,
     float* __restrict__ w_row, float* __restrict__ dw_row, const int* __restrict__ info) {
+  pdl_wait();
+  pdl_trigger();
   if (info[kInfoSkip]) return;
   extern __shared__ int smem[];
   int* run = smem;        // [E]
@@ -259,6 +265,8 @@ __global__ void __launch_bounds__(256) dispatch_scatter_kernel(
     const int* __restrict__ dest_of, const int* __restrict__ info, T* __restrict__ xd, T* __restrict__ dyd,
     const int* __restrict__ seg, const int* __restrict__ cnt, int El, int* __restrict__ src_of,
     float* __restrict__ w_row, float* __restrict__ dw_row) {
+  pdl_wait();
+  pdl_trigger();
   if (info[kInfoSkip]) return;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t nwarps = (int64_t)gridDim.x * (blockDim.x >> 5);
@@ -354,6 +362,8 @@ __global__ void __launch_bounds__(256) dispatch_scatter_mx_kernel(
     int* __restrict__ src_of, float* __restrict__ w_row, float* __restrict__ dw_row, const int* __restrict__ info,
     int write_x, __nv_bfloat16* __restrict__ xd, __nv_bfloat16* __restrict__ dyd, uint8_t* __restrict__ xq,
     uint8_t* __restrict__ xsf) {
+  pdl_wait();
+  pdl_trigger();
   if (info[kInfoSkip]) return;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t nwarps = (int64_t)gridDim.x * (blockDim.x >> 5);
@@ -425,7 +435,7 @@ void launch_dispatch_index(const int32_t* ids, const float* w, int64_t t0, int64
   int NB = (int)ceil_div64(t1 - t0, kTokPerBlk);
   if (NB == 0) return;
   size_t smem = sizeof(int) * ((size_t)E + (size_t)kTokPerBlk * k);
-  dispatch_index_kernel<<<NB, 256, smem, st>>>(ids, w, t0, t1, k, E, m.blk_cnt, m.dest_of, row_src, w_row, nullptr,
+  launch_pdl(dispatch_index_kernel, dim3(NB), dim3(256), smem, st, ids, w, t0, t1, k, E, m.blk_cnt, m.dest_of, row_src, w_row, nullptr,
                                                m.info);
 }
 
@@ -438,7 +448,7 @@ void launch_dispatch_scatter(const T* x, const T* dy, const int32_t* ids, const 
   if (NB == 0) return;
   size_t smem = sizeof(int) * ((size_t)E + (size_t)kTokPerBlk * k);
   int* row_src = expert_major ? m.src_of : m.send_src;
-  dispatch_index_kernel<<<NB, 256, smem, st>>>(ids, w, t0, t1, k, E, m.blk_cnt, m.dest_of, row_src, m.w_row,
+  launch_pdl(dispatch_index_kernel, dim3(NB), dim3(256), smem, st, ids, w, t0, t1, k, E, m.blk_cnt, m.dest_of, row_src, m.w_row,
                                                dy ? m.dw_row : nullptr, m.info);
   // token-order scatter (each source row read once; k <= 16, memfine_create checks) + the padding
   // rows of the expert-major layout zeroed in the same launch
@@ -446,13 +456,13 @@ void launch_dispatch_scatter(const T* x, const T* dy, const int32_t* ids, const 
                                             148 * 16);
   if constexpr (std::is_same<T, __nv_bfloat16>::value) {
     if (xq && expert_major) {
-      dispatch_scatter_mx_kernel<<<blocks, 256, 0, st>>>(x, dy, t0, t1, k, h, m.dest_of, m.seg, m.recv_cnt, El,
+      launch_pdl(dispatch_scatter_mx_kernel, dim3(blocks), dim3(256), 0, st, x, dy, t0, t1, k, h, m.dest_of, m.seg, m.recv_cnt, El,
                                                           m.src_of, m.w_row, dy ? m.dw_row : nullptr, m.info,
                                                           write_x ? 1 : 0, xd, dyd, xq, xsf);
       return;
     }
   }
-  dispatch_scatter_kernel<T><<<blocks, 256, 0, st>>>(x, dy, t0, t1, k, h, m.dest_of, m.info, xd, dyd,
+  launch_pdl(dispatch_scatter_kernel<T>, dim3(blocks), dim3(256), 0, st, x, dy, t0, t1, k, h, m.dest_of, m.info, xd, dyd,
                                                      expert_major ? m.seg : nullptr, m.recv_cnt, El, m.src_of,
                                                      m.w_row, dy ? m.dw_row : nullptr);
 }
@@ -463,6 +473,8 @@ template <typename T>
 __global__ void zero_padding_kernel(const int* __restrict__ seg, const int* __restrict__ recv_cnt, int h,
                                     const int* __restrict__ info, T* __restrict__ xd, T* __restrict__ dyd,
                                     int* __restrict__ src_of, float* __restrict__ w_row, float* __restrict__ dw_row) {
+  pdl_wait();
+  pdl_trigger();
   if (info[kInfoSkip]) return;
   int e = blockIdx.x;
   int r0 = seg[e] + recv_cnt[e], r1 = seg[e + 1];
@@ -486,7 +498,7 @@ __global__ void zero_padding_kernel(const int* __restrict__ seg, const int* __re
 
 template <typename T>
 void launch_zero_padding(int El, int h, const ChunkMeta& m, T* xd, T* dyd, cudaStream_t st) {
-  zero_padding_kernel<T><<<dim3(El, kRowAlign / 8), 256, 0, st>>>(m.seg, m.recv_cnt, h, m.info, xd, dyd, m.src_of,
+  launch_pdl(zero_padding_kernel<T>, dim3(dim3(El, kRowAlign / 8)), dim3(256), 0, st, m.seg, m.recv_cnt, h, m.info, xd, dyd, m.src_of,
                                                                  m.w_row, dyd ? m.dw_row : nullptr);
 }
 
@@ -557,6 +569,8 @@ __global__ void __launch_bounds__(256, 2) gather_reduce_kernel(
     const T* __restrict__ rows, const float* __restrict__ w, int64_t t0, int64_t t1, int k, int h,
     const int* __restrict__ dest_of, const int* __restrict__ info, T* __restrict__ out,
     const float* __restrict__ dw_row, float* __restrict__ dscore) {
+  pdl_wait();
+  pdl_trigger();
   if (info[kInfoSkip]) return;
   constexpr int SG = 8;                       // slots loaded per group
   constexpr int NC = sizeof(T) == 2 ? 2 : 1;  // column chunks per iteration
@@ -618,7 +632,7 @@ void launch_combine(const T* O, const float* w, int64_t t0, int64_t t1, int k, i
                     cudaStream_t st) {
   int64_t n = t1 - t0;
   if (n == 0) return;
-  gather_reduce_kernel<T, true><<<(unsigned)ceil_div64(n, 8), 256, 0, st>>>(O, w, t0, t1, k, h, m.dest_of, m.info,
+  launch_pdl(gather_reduce_kernel<T, true>, dim3((unsigned)ceil_div64(n, 8)), dim3(256), 0, st, O, w, t0, t1, k, h, m.dest_of, m.info,
                                                                            y, nullptr, nullptr);
 }
 
@@ -627,7 +641,7 @@ void launch_unpermute_reduce(const T* dXd, int64_t t0, int64_t t1, int k, int h,
                              float* dscore, cudaStream_t st) {
   int64_t n = t1 - t0;
   if (n == 0) return;
-  gather_reduce_kernel<T, false><<<(unsigned)ceil_div64(n, 8), 256, 0, st>>>(dXd, nullptr, t0, t1, k, h, m.dest_of,
+  launch_pdl(gather_reduce_kernel<T, false>, dim3((unsigned)ceil_div64(n, 8)), dim3(256), 0, st, dXd, nullptr, t0, t1, k, h, m.dest_of,
                                                                             m.info, dx, m.dw_row, dscore);
 }
 
