@@ -603,6 +603,7 @@ def main():
         "config": {**workload_config(cfg, args, world), "chunks": C, "tuner": plan,
                    "ep_transport": args.ep_transport if world > 1 else None,
                    "overlap": overlap and C > 1,
+                   "pdl": os.environ.get("MEMFINE_PDL", "1") != "0",   # programmatic dependent launch
                    "budget": {"gpu_capacity_bytes": cap, "alpha": args.alpha, "static_bytes": static},
                    "l2": "no flush: every step streams > 126 MB (weights 2.8 GB at EP=1, activations GBs)"},
         "peak_act_gb": peak_c, "peak_act_gb_unchunked": peak_1,
