@@ -190,6 +190,7 @@ struct MxColTensor {
 struct MxColTensors {
   MxColTensor t[4];
   int n;
+  int tile0[5];   // set by launch_mx_quant_t: first 128-column tile of each tensor in the flat grid
 };
 void launch_mx_quant_t(const MxColTensors& tz, const int* info, int64_t Rcap, cudaStream_t st);
 // src [B][R][Cc] -> q_rows [B][R][Cc] blocked along Cc and q_t [B][Cc][R] blocked along R, one read

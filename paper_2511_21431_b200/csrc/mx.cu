@@ -133,11 +133,13 @@ __global__ void __launch_bounds__(256) mx_quant_dual_kernel(const __nv_bfloat16*
 __global__ void __launch_bounds__(256) mx_quant_t_kernel(MxColTensors tz, const int* __restrict__ info, int64_t Rcap) {
   pdl_wait();
   pdl_trigger();
-  const MxColTensor& tt = tz.t[blockIdx.z];
-  if (blockIdx.z >= (unsigned)tz.n || (int)blockIdx.x * 128 >= tt.Cc) return;
+  // flat grid over the tensors' 128-column tiles (no empty blocks for the narrower tensors)
+  int z = 0;
+  while (z + 1 < tz.n && (int)blockIdx.x >= tz.tile0[z + 1]) z++;
+  const MxColTensor& tt = tz.t[z];
   const int64_t rows = __ldg(info + kInfoSkip) ? 0 : min(Rcap, (int64_t)__ldg(info + kInfoRowsPad));
   const int64_t r0 = (int64_t)blockIdx.y * 128;
-  const int c0 = blockIdx.x * 128;
+  const int c0 = ((int)blockIdx.x - tz.tile0[z]) * 128;
   if (r0 >= rows) return;
   __shared__ __nv_bfloat16 t[128][128 + 8];
   const __nv_bfloat16* src = tt.src;
@@ -178,11 +180,14 @@ __global__ void __launch_bounds__(256) mx_quant_t_kernel(MxColTensors tz, const 
 }
 
 void launch_mx_quant_t(const MxColTensors& tz, const int* info, int64_t Rcap, cudaStream_t st) {
-  int cmax = 0;
-  for (int i = 0; i < tz.n; i++) cmax = std::max(cmax, tz.t[i].Cc);
-  if (cmax <= 0 || Rcap <= 0 || tz.n <= 0) return;
-  dim3 grid((unsigned)(cmax / 128), (unsigned)(Rcap / 128), (unsigned)tz.n);
-  launch_pdl(mx_quant_t_kernel, dim3(grid), dim3(256), 0, st, tz, info, Rcap);
+  if (Rcap <= 0 || tz.n <= 0) return;
+  MxColTensors f = tz;
+  int tiles = 0;
+  for (int i = 0; i < f.n; i++) { f.tile0[i] = tiles; tiles += f.t[i].Cc / 128; }
+  for (int i = f.n; i < 5; i++) f.tile0[i] = tiles;
+  if (tiles <= 0) return;
+  dim3 grid((unsigned)tiles, (unsigned)(Rcap / 128));
+  launch_pdl(mx_quant_t_kernel, dim3(grid), dim3(256), 0, st, f, info, Rcap);
 }
 
 void launch_mx_quant_dual(const __nv_bfloat16* src, int B, int R, int Cc, uint8_t* q_rows, uint8_t* sf_rows,
