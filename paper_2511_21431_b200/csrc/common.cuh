@@ -56,13 +56,21 @@ template <> struct Elt<float> {
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 
-// PDL on the hot path's launches (MEMFINE_PDL=0 turns it off).
+// PDL on the hot path's launches (MEMFINE_PDL=0 turns it off).  Off for the calling thread while a
+// call runs kernels on two streams (MEMFINE_FLAG_OVERLAP): early-launched CTAs waiting on their
+// predecessor would hold SMs the comm stream's kernels need (measured: overlap mode 1.5-3 ms slower).
+inline thread_local int tl_pdl_off = 0;
+struct PdlOff {
+  int prev;
+  explicit PdlOff(bool off) : prev(tl_pdl_off) { if (off) tl_pdl_off = 1; }
+  ~PdlOff() { tl_pdl_off = prev; }
+};
 inline bool use_pdl() {
   static const int v = [] {
     const char* s = getenv("MEMFINE_PDL");
     return (s && s[0] == '0') ? 0 : 1;
   }();
-  return v == 1;
+  return v == 1 && !tl_pdl_off;
 }
 // <<<grid, block, smem, st>>> with the PDL attribute: the kernel must call pdl_wait() before it
 // touches global memory a predecessor writes or reads.

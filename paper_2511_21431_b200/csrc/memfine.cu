@@ -1652,6 +1652,7 @@ memfine_status memfine_moe_fwd(memfine_handle_t h, const void* x, const int32_t*
   if (!w_gate || !w_up || !w_down || !ws) return MEMFINE_ERR_INVALID_ARG;
   cudaStream_t st = (cudaStream_t)stream;
   Nvtx call_range("memfine_moe_fwd");
+  PdlOff pdl_off(ep_slots(h->d, C) == 2);
   begin_call(h, C, MEMFINE_FWD, ws_bytes, st);
   if (ep_path(h->d)) return memfine_ep_fwd(h, x, ids, w, w_gate, w_up, w_down, C, y, ws, ws_bytes, st);
   if (h->d.dtype != MEMFINE_FP32)
@@ -1669,6 +1670,7 @@ memfine_status memfine_moe_bwd(memfine_handle_t h, const void* dy, const void* x
   if (!w_gate || !w_up || !w_down || !dw_gate || !dw_up || !dw_down || !ws) return MEMFINE_ERR_INVALID_ARG;
   cudaStream_t st = (cudaStream_t)stream;
   Nvtx call_range("memfine_moe_bwd");
+  PdlOff pdl_off(ep_slots(h->d, C) == 2);
   begin_call(h, C, MEMFINE_BWD, ws_bytes, st);
   if (ep_path(h->d))
     return memfine_ep_bwd(h, dy, x, ids, w, w_gate, w_up, w_down, C, dx, dw_gate, dw_up, dw_down, dscore,
