@@ -75,7 +75,7 @@ typedef struct {
                            * MEMFINE_MXFP8 (bf16 storage; the gate/up, down and dX   *
                            *   GEMMs on MXFP8 operands, see memfine_mx_*; hidden,     *
                            *   ffn % 128 == 0; with EP the rows travel in bf16 and are *
-                           *   quantised on arrival; EP_COPY transport only)           */
+                           *   quantised on arrival; both EP transports)               */
     int32_t flags;        /* MEMFINE_FLAG_* (0 = none).  Part of the workspace layout:  *
                            * memfine_workspace_bytes and the fwd/bwd calls must see the *
                            * same flags.                                                */
@@ -200,7 +200,9 @@ memfine_status memfine_create_local(const memfine_dims* dims, memfine_group_t gr
  *    ep_size <= 16.  In-process groups map peers directly; across processes (NCCL handles) the
  *    workspace must first be registered with memfine_register_workspace, and ranks fence with a
  *    one-int NCCL all-reduce on the stream.
- * The workspace layout and size are the same for both. */
+ * The workspace layout and size are the same for both.  MEMFINE_EP_P2P on a handle created with
+ * MEMFINE_FLAG_OVERLAP returns MEMFINE_ERR_INVALID_ARG (the two-slot pipeline is the copy
+ * transport's; memfine_workspace_bytes sizes it from the dims alone). */
 enum { MEMFINE_EP_COPY = 0, MEMFINE_EP_P2P = 1 };
 memfine_status memfine_set_ep_transport(memfine_handle_t h, int32_t transport);
 

@@ -108,8 +108,9 @@ struct PlanParams {
 };
 // Shared host/device evaluation from per-(rank, sub-chunk) sums sub[r*nsub + j].
 __host__ __device__ int plan_from_subsums(const int64_t* sub, const PlanParams& p, memfine_plan_info* out);
-void launch_plan_kernel(const int32_t* counts_dev, const PlanParams& p, memfine_plan_info* out_mapped,
-                        int* rc_mapped, cudaStream_t st);
+// 0 = launched; -1 = launch failure (the result words are then not written)
+int launch_plan_kernel(const int32_t* counts_dev, const PlanParams& p, memfine_plan_info* out_mapped,
+                       int* rc_mapped, cudaStream_t st);
 
 // ---------------------------------------------------------------- expert GEMMs (A7, A8, B2-B5)
 enum GemmKind {

@@ -495,6 +495,22 @@ void set_mx(GemmProblem<__nv_bfloat16>& p, const MxOp& a, const MxOp& b0, const 
 // x (into Xq: dead after the recompute), dY, dG || dU and a_w, then block-scaled GEMMs over them.
 template <typename T>
 int run_wgrad(memfine_handle_s* h, GemmProblem<T>& p, const Layout& L, cudaStream_t st) {
+  if (p.rows_cap == 0) {
+    // No chunk of this call reaches this rank's experts (EP: every copy routed elsewhere).  The
+    // GEMM launchers return early on an empty row buffer, so the first chunk's overwrite of dW
+    // (beta = 0) is done here; later chunks add nothing.
+    if (!p.wgrad_beta) {
+      const memfine_dims& d = h->d;
+      const size_t wb = sizeof(float) * (size_t)(d.num_experts / d.ep_size) * d.ffn * d.hidden;
+      prof_begin(h, 8, st);
+      float* dws[3] = {p.dWg, p.dWu, p.dWd};
+      for (float* dw : dws)
+        if (cudaMemsetAsync(dw, 0, wb, st) != cudaSuccess) return MEMFINE_ERR_CUDA;
+      prof_end(h, st);
+      h->last.kernel_launches += 3;
+    }
+    return MEMFINE_OK;
+  }
   if constexpr (std::is_same<T, __nv_bfloat16>::value) {
     const memfine_dims& d = h->d;
     if (d.dtype == MEMFINE_MXFP8 && (d.flags & MEMFINE_FLAG_MX_WGRAD)) {
@@ -754,20 +770,13 @@ int local_exchange(memfine_handle_s* h, const int* counts, int C, int j, bool fo
 // One grouped exchange.  forward=true: send-layout rows -> receiver's expert-major rows;
 // forward=false: expert-major rows -> the source's send layout.  width = elements per row,
 // esize = bytes per element (row payload moved as bytes; NCCL dtype uint8) or 4 for fp32 scalars.
+// ks / ke: the buffers' kinds in the in-process group's pointer table (slot * 8 + kPtr*), passed
+// explicitly - a zero-row rank's arrays share one address, so they cannot be looked up by pointer.
 int ep_exchange(memfine_handle_s* h, const EpChunk& t, const int* counts, int C, int j, bool forward, char* send_buf,
-                char* expert_buf, size_t row_bytes, cudaStream_t st) {
+                char* expert_buf, size_t row_bytes, cudaStream_t st, int ks, int ke) {
   const memfine_dims& d = h->d;
   int E = d.num_experts, EP = d.ep_size, El = E / EP, me = d.ep_rank;
-  if (h->lg) {
-    // the buffer kinds are identified from the published pointer table
-    int ks = -1, ke = -1;
-    for (int k = 0; k < 16; k++) {
-      if (ks < 0 && h->lg->ptrs[me][k] == send_buf) ks = k;
-      if (ke < 0 && h->lg->ptrs[me][k] == expert_buf) ke = k;
-    }
-    if (ks < 0 || ke < 0) return 1;
-    return local_exchange(h, counts, C, j, forward, ks, ke, row_bytes, st);
-  }
+  if (h->lg) return local_exchange(h, counts, C, j, forward, ks, ke, row_bytes, st);
   if (nccl_group_start()) return 1;
   int rc = 0;
   for (int peer = 0; peer < EP && !rc; peer++) {
@@ -1100,10 +1109,15 @@ memfine_status ep_run(memfine_handle_s* h, int pass, const T* dy, const T* x, co
     launch_ep_recv_seg(h->counts_d, C, j, E, El, d.ep_rank, d.ep_size, L.rows_cap, L.m, h->rows_d,
                        h->rows_d + kMaxSub, cs);
     prof_begin(h, 9, cs);
-    if (ep_exchange(h, t, h->counts_h, C, j, true, (char*)L.send, (char*)L.X, rb, cs)) return MEMFINE_ERR_NCCL;
+    const int ko = 8 * (j % S);   // this slot's kinds in the in-process pointer table
+    if (ep_exchange(h, t, h->counts_h, C, j, true, (char*)L.send, (char*)L.X, rb, cs, ko + kPtrSend, ko + kPtrX))
+      return MEMFINE_ERR_NCCL;
     if (pass == MEMFINE_BWD) {
-      if (ep_exchange(h, t, h->counts_h, C, j, true, (char*)L.send_dy, (char*)L.DY, rb, cs)) return MEMFINE_ERR_NCCL;
-      if (ep_exchange(h, t, h->counts_h, C, j, true, (char*)L.send_w, (char*)L.m.w_row, 4, cs))
+      if (ep_exchange(h, t, h->counts_h, C, j, true, (char*)L.send_dy, (char*)L.DY, rb, cs, ko + kPtrSendDy,
+                      ko + kPtrDY))
+        return MEMFINE_ERR_NCCL;
+      if (ep_exchange(h, t, h->counts_h, C, j, true, (char*)L.send_w, (char*)L.m.w_row, 4, cs, ko + kPtrSendW,
+                      ko + kPtrWRow))
         return MEMFINE_ERR_NCCL;
       if (t.rows_pad) MF_CUDA_OK(cudaMemsetAsync(L.m.dw_row, 0, sizeof(float) * t.rows_pad, cs));
     }
@@ -1119,11 +1133,15 @@ memfine_status ep_run(memfine_handle_s* h, int pass, const T* dy, const T* x, co
     const EpChunk& t = tab[j];
     int64_t t0 = chunk_begin(d.tokens, C, j), t1 = chunk_begin(d.tokens, C, j + 1);
     if (S == 2) MF_CUDA_OK(cudaStreamWaitEvent(cs, h->ev_gemm[j % 2], 0));
-    if (ep_exchange(h, t, h->counts_h, C, j, false, (char*)L.send, (char*)L.O, rb, cs)) return MEMFINE_ERR_NCCL;
+    const int ko = 8 * (j % S);
+    if (ep_exchange(h, t, h->counts_h, C, j, false, (char*)L.send, (char*)L.O, rb, cs, ko + kPtrSend,
+                    ko + (L.O == L.X ? kPtrX : kPtrO)))
+      return MEMFINE_ERR_NCCL;
     if (pass == MEMFINE_FWD) {
       if (t1 > t0) launch_combine<T>((const T*)L.send, w, t0, t1, k, hd, L.m, out, cs);
     } else {
-      if (ep_exchange(h, t, h->counts_h, C, j, false, (char*)L.send_w, (char*)L.m.dw_row, 4, cs))
+      if (ep_exchange(h, t, h->counts_h, C, j, false, (char*)L.send_w, (char*)L.m.dw_row, 4, cs, ko + kPtrSendW,
+                      ko + kPtrDWRow))
         return MEMFINE_ERR_NCCL;
       ChunkMeta mb = L.m;
       mb.dw_row = L.send_w;
@@ -1360,6 +1378,9 @@ memfine_status memfine_set_ep_transport(memfine_handle_t h, int32_t transport) {
   if (!h || (transport != MEMFINE_EP_COPY && transport != MEMFINE_EP_P2P)) return MEMFINE_ERR_INVALID_ARG;
   if (transport == MEMFINE_EP_P2P && h->d.ep_size > kMaxPeers) return MEMFINE_ERR_UNSUPPORTED;
   if (transport == MEMFINE_EP_P2P && !h->lg && h->d.ep_size > 1 && !h->comm.comm) return MEMFINE_ERR_UNSUPPORTED;
+  // the two-slot chunk pipeline (and its workspace layout, which memfine_workspace_bytes derives from the
+  // dims alone) belongs to the copy transport
+  if (transport == MEMFINE_EP_P2P && (h->d.flags & MEMFINE_FLAG_OVERLAP)) return MEMFINE_ERR_INVALID_ARG;
   h->p2p = transport == MEMFINE_EP_P2P;
   return MEMFINE_OK;
 }
@@ -1506,13 +1527,17 @@ memfine_status memfine_plan(const int32_t* counts, int32_t nsub, const memfine_d
     cudaStream_t st;
     cudaDeviceSynchronize();  // counts may come from any stream of the caller
     cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking);
-    launch_plan_kernel(counts, p, out_d, rc_d, st);
+    const int lrc = launch_plan_kernel(counts, p, out_d, rc_d, st);
     cudaError_t e = cudaStreamSynchronize(st);
     cudaStreamDestroy(st);
     int rc = *rc_h;
+    if (lrc || e != cudaSuccess || rc < 0) {   // launch failure: the result words were never written
+      cudaGetLastError();
+      cudaFreeHost(out_h);
+      return MEMFINE_ERR_CUDA;
+    }
     *info = *out_h;
     cudaFreeHost(out_h);
-    if (e != cudaSuccess) return MEMFINE_ERR_CUDA;
     return (memfine_status)rc;
   }
   return plan_host(counts, nsub, dims, budget, info);

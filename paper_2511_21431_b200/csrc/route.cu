@@ -862,8 +862,10 @@ __host__ __device__ int plan_from_subsums(const int64_t* sub, const PlanParams& 
 
 // One CTA: per-(rank, sub-chunk) received-copy sums via smem reduction, then thread 0
 // evaluates Eqs. 8-9 and the bins; the result lands in pinned mapped host memory.
-__global__ void plan_kernel(const int32_t* __restrict__ counts, PlanParams p, memfine_plan_info* out, int* rc) {
-  extern __shared__ unsigned long long sub_u[];  // [EP * nsub]
+__global__ void plan_kernel(const int32_t* __restrict__ counts, PlanParams p, memfine_plan_info* out, int* rc,
+                            unsigned long long* sub_g) {
+  extern __shared__ unsigned long long sub_s[];  // [EP * nsub] (in global memory when it exceeds 48 KB)
+  unsigned long long* sub_u = sub_g ? sub_g : sub_s;
   int n = p.EP * p.nsub;
   for (int i = threadIdx.x; i < n; i += blockDim.x) sub_u[i] = 0ull;
   __syncthreads();
@@ -883,10 +885,16 @@ __global__ void plan_kernel(const int32_t* __restrict__ counts, PlanParams p, me
   }
 }
 
-void launch_plan_kernel(const int32_t* counts_dev, const PlanParams& p, memfine_plan_info* out_mapped, int* rc_mapped,
-                        cudaStream_t st) {
-  size_t smem = sizeof(unsigned long long) * (size_t)p.EP * p.nsub;
-  plan_kernel<<<1, 1024, smem, st>>>(counts_dev, p, out_mapped, rc_mapped);
+int launch_plan_kernel(const int32_t* counts_dev, const PlanParams& p, memfine_plan_info* out_mapped, int* rc_mapped,
+                       cudaStream_t st) {
+  // per-(rank, sub-chunk) sums: shared memory up to 48 KB (EP * nsub <= 6144), else a device scratch
+  const size_t bytes = sizeof(unsigned long long) * (size_t)p.EP * p.nsub;
+  unsigned long long* scratch = nullptr;
+  if (bytes > 48 * 1024 && cudaMallocAsync((void**)&scratch, bytes, st) != cudaSuccess) return -1;
+  plan_kernel<<<1, 1024, scratch ? 0 : bytes, st>>>(counts_dev, p, out_mapped, rc_mapped, scratch);
+  const cudaError_t e = cudaGetLastError();
+  if (scratch) cudaFreeAsync(scratch, st);
+  return e == cudaSuccess ? 0 : -1;
 }
 
 // ------------------------------------------------------------------------------------------

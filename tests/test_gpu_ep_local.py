@@ -27,7 +27,8 @@ def _bits(t, dtype):
         t.contiguous().numpy().astype(np.float32)
 
 
-def _run_group(EP, C, dtype, transport, xs, dys, routes, wg, wu, wd, T, h, g, E, k, mx=False, mx_wgrad=False):
+def _run_group(EP, C, dtype, transport, xs, dys, routes, wg, wu, wd, T, h, g, E, k, mx=False, mx_wgrad=False,
+               nan_dw=False):
     """Every rank of an in-process EP group: fwd + bwd; returns (per-rank outputs, counts seen)."""
     El = E // EP
     group = layer.LocalGroup(EP)
@@ -59,7 +60,11 @@ def _run_group(EP, C, dtype, transport, xs, dys, routes, wg, wu, wd, T, h, g, E,
                 wsb = max(layer.workspace_bytes(ch, mf.dims, C, capi.FWD), layer.workspace_bytes(ch, mf.dims, C, capi.BWD))
                 ws = torch.empty(wsb, dtype=torch.uint8, device=dev)
                 y = mf.moe_fwd(x, ids, w, lwg, lwu, lwd, C, ws, stream=st)
-                dx, dwg, dwu, dwd, ds = mf.moe_bwd(dy, x, ids, w, lwg, lwu, lwd, C, ws, stream=st)
+                kw = {}
+                if nan_dw:   # dW buffers holding garbage: the call must overwrite every element
+                    kw = {n_: torch.full(t_.shape, float("nan"), dtype=torch.float32, device=dev)
+                          for n_, t_ in (("dw_gate", lwg), ("dw_up", lwu), ("dw_down", lwd))}
+                dx, dwg, dwu, dwd, ds = mf.moe_bwd(dy, x, ids, w, lwg, lwu, lwd, C, ws, stream=st, **kw)
                 s_ = mf.sync(stream=st)
                 assert s_ == 0, capi.status_str(s_)
                 results[r] = [t.float().cpu().numpy() for t in (y, dx, ds, dwg, dwu, dwd)]
@@ -228,3 +233,73 @@ def test_ep_local_group_mx_p2p_matches_oracle(EP, C, mx_wgrad):
                 "dw_gate": rel_err(dwg, dwg_ref[es]), "dw_up": rel_err(dwu, dwu_ref[es]),
                 "dw_down": rel_err(dwd, dwd_ref[es])}
         assert all(v <= MX_TOL for v in errs.values()), (r, errs)
+
+
+def _oracle_ep(EP, C, dtype, xs, dys, routes, wg, wu, wd, T, h, g, E, k):
+    d = oracle.Dims(T=T, h=h, g=g, E=E, k=k, EP=EP, in_dtype="bf16" if dtype == torch.bfloat16 else "f32")
+    xa = np.concatenate([_bits(x, dtype) for x in xs])
+    dya = np.concatenate([_bits(x, dtype) for x in dys])
+    ida = np.concatenate([r[0] for r in routes])
+    wa = np.concatenate([r[1] for r in routes]).astype(np.float64)
+    W = [_bits(t, dtype) for t in (wg, wu, wd)]
+    y_ref, _, _ = oracle.fcda_forward(d, C, xa, ida, wa, *W)
+    dx_ref, ds_ref, dwg_ref, dwu_ref, dwd_ref, _, _ = oracle.fcda_backward(d, C, dya, xa, ida, wa, *W)
+    return y_ref, dx_ref, ds_ref, dwg_ref, dwu_ref, dwd_ref
+
+
+def _check_ranks(results, refs, EP, T, El, t_):
+    y_ref, dx_ref, ds_ref, dwg_ref, dwu_ref, dwd_ref = refs
+    for r in range(EP):
+        y, dx, ds, dwg, dwu, dwd = results[r]
+        sl, es = slice(r * T, (r + 1) * T), slice(r * El, (r + 1) * El)
+        errs = {"y": rel_err(y, y_ref[sl]), "dx": rel_err(dx, dx_ref[sl]), "dscore": rel_err(ds, ds_ref[sl]),
+                "dw_gate": rel_err(dwg, dwg_ref[es]), "dw_up": rel_err(dwu, dwu_ref[es]),
+                "dw_down": rel_err(dwd, dwd_ref[es])}
+        assert all(v <= t_ for v in errs.values()), (r, errs)
+        for name, a in (("dw_gate", dwg), ("dw_up", dwu), ("dw_down", dwd)):
+            assert np.isfinite(a).all(), (r, name)
+
+
+@pytest.mark.parametrize("transport", [capi.EP_COPY, capi.EP_P2P, "overlap"])
+@pytest.mark.parametrize("EP,C", [(2, 1), (4, 3)])
+def test_ep_rank_without_rows(EP, C, transport):
+    """A rank whose experts receive no copy in any chunk (hot-expert routing, the case MACT exists for):
+    its weight-gradient GEMMs have no rows, so the call itself must overwrite its dW with zeros (the dW
+    buffers start as NaN here), and its (empty) exchanges must still move every other rank's rows."""
+    T, h, g, E, k = 300, 128, 256, 8, 2
+    El = E // EP
+    dtype = torch.bfloat16
+    xs = [synth.make_x(T, h, rank=r, dtype=dtype) for r in range(EP)]
+    dys = [synth.make_dy(T, h, rank=r, dtype=dtype) for r in range(EP)]
+    cold = set(range((EP - 1) * El, E))               # the last rank's experts: never routed to
+    hot = [e for e in range(E) if e not in cold]
+    routes = []
+    for r in range(EP):
+        rng = np.random.default_rng(100 + r)
+        ids = np.stack([rng.choice(hot, k, replace=False) for _ in range(T)]).astype(np.int32)
+        lg = rng.standard_normal((T, k))
+        w = (np.exp(lg) / np.exp(lg).sum(1, keepdims=True)).astype(np.float32)
+        routes.append((ids, w))
+    wg, wu, wd = synth.make_experts(range(E), h, g, dtype=dtype)
+    results, _ = _run_group(EP, C, dtype, transport, xs, dys, routes, wg, wu, wd, T, h, g, E, k, nan_dw=True)
+    refs = _oracle_ep(EP, C, dtype, xs, dys, routes, wg, wu, wd, T, h, g, E, k)
+    _check_ranks(results, refs, EP, T, El, tol(dtype))
+    for a in results[EP - 1][3:]:
+        assert np.all(a == 0)
+
+
+@pytest.mark.parametrize("transport", [capi.EP_COPY, capi.EP_P2P])
+@pytest.mark.parametrize("E,C,dtype", [(16, 1, torch.bfloat16), (16, 3, torch.bfloat16), (32, 3, torch.bfloat16),
+                                       (32, 1, torch.float32)])
+def test_ep8_local_group_matches_oracle(E, C, dtype, transport):
+    """EP = 8 (the north star's box): E = 16 (2 local experts) and E = 32 (4), top-2 with Zipf skew and
+    the hot experts on rank 0; every rank's Y, dX, d_score and local dW against the oracle."""
+    EP, T, h, g, k = 8, 256, 128, 256, 2
+    El = E // EP
+    xs = [synth.make_x(T, h, rank=r, dtype=dtype) for r in range(EP)]
+    dys = [synth.make_dy(T, h, rank=r, dtype=dtype) for r in range(EP)]
+    routes = [synth.make_routing(T, E, k, rank=r, zipf_s=1.2, placement="contiguous") for r in range(EP)]
+    wg, wu, wd = synth.make_experts(range(E), h, g, dtype=dtype)
+    results, _ = _run_group(EP, C, dtype, transport, xs, dys, routes, wg, wu, wd, T, h, g, E, k)
+    refs = _oracle_ep(EP, C, dtype, xs, dys, routes, wg, wu, wd, T, h, g, E, k)
+    _check_ranks(results, refs, EP, T, El, tol(dtype))

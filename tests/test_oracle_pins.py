@@ -476,3 +476,63 @@ def test_m_g_pipeline_stage_pins():
         for v in range(1, 4):
             for r in range(p):
                 assert oracle.m_g(v + 1, p, r) == oracle.m_g(v, p, r) + p
+
+
+# ----------------------------------------------------------------------------- pins of the checkers themselves
+@pytest.mark.parametrize("EP,dtype", [(1, "f64"), (2, "f32")])
+def test_moe_tokens_equals_whole_layer_rows(oracle_lib, EP, dtype):
+    """oracle_moe_tokens (the full-size sampled checker) returns exactly the rows of the whole-layer
+    definitions: y of Eq. 4 (oracle_moe_forward), dx and d_score of Eq. 5 (oracle_moe_backward), for
+    any token subset in any order - including duplicate slots and out-of-range ids."""
+    rng = np.random.default_rng(23)
+    T, h, g, E, k = 24, 16, 24, 6, 3
+    x, dy, ids, w, wg, wu, wd = rand_problem(rng, T, h, g, E, k, EP=EP, distinct=False, dtype=dtype)
+    ids[3, 1] = E + 2          # an id outside [0, E): contributes nothing
+    ids[5, 2] = -1
+    d = Dims(T=T, h=h, g=g, E=E, k=k, EP=EP, in_dtype=dtype)
+    y = oracle.moe_forward(d, x, ids, w, wg, wu, wd)
+    dx, ds, *_ = oracle.moe_backward(d, dy, x, ids, w, wg, wu, wd)
+    toks = np.array([0, 5, 3, EP * T - 1, 7, 5, 11])
+    ys, dxs, dss = oracle.moe_tokens(d, toks, dy, x, ids, w, wg, wu, wd)
+    for got, ref in ((ys, y[toks]), (dxs, dx[toks]), (dss, ds[toks])):
+        assert np.abs(got - ref).max() <= 1e-13 * np.abs(ref).max()
+    assert dss[2, 1] == 0.0 and np.all(dss[1, 2] == 0.0)
+
+
+def test_plan_exact_rule_is_minimal(oracle_lib):
+    """Rule EXACT (reading R11) picks the SMALLEST bin whose true per-chunk maximum fits s'_max: every
+    smaller bin overflows, the chosen one fits, and a clamp means no bin fits.  Per-chunk loads are
+    recomputed here with numpy from the counts (chunk jc of C = sub-chunks [jc*8/C, (jc+1)*8/C)) and
+    s'_max from Eq. 8 directly."""
+    rng = np.random.default_rng(29)
+    bins = (1, 2, 4, 8)
+    seen = {b: 0 for b in bins}
+    clamped = 0
+    for _ in range(400):
+        EP = int(rng.choice([1, 2, 4]))
+        E = EP * int(rng.integers(1, 4))
+        h, g = int(rng.integers(1, 32)), int(rng.integers(1, 32))
+        counts = rng.integers(0, 40, size=(EP, 8, E)).astype(np.int64)
+        if rng.random() < 0.5:                         # skew: one hot rank and sub-chunk
+            counts[0, int(rng.integers(0, 8)), 0] += int(rng.integers(0, 400))
+        d = Dims(T=1, h=h, g=g, E=E, k=1, EP=EP)
+        beta = 2 * (2 * h + 2 * g)
+        budget = int(rng.integers(beta, 400 * beta))
+        st, p = oracle.plan(counts, d, budget_bytes=budget, bins=bins, rule=1)
+        assert st == 0
+        spm = budget // beta
+        assert p["s_prime_max"] == spm
+        El = E // EP
+        recv = counts.sum(axis=0).reshape(8, EP, El).sum(axis=2)        # [sub-chunk][receiving rank]
+        def chunk_max(C_):
+            return int(recv.reshape(C_, 8 // C_, EP).sum(axis=1).max())
+        fits = [chunk_max(b) <= spm for b in bins]
+        if p["clamped"]:
+            clamped += 1
+            assert not any(fits) and p["C"] == bins[-1] and not p["feasible"]
+        else:
+            i = bins.index(p["C"])
+            seen[p["C"]] += 1
+            assert fits[i] and not any(fits[:i]) and p["feasible"]
+            assert p["s_chunk_max"] == chunk_max(p["C"])
+    assert all(v > 0 for v in seen.values()) and clamped > 0
