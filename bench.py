@@ -7,8 +7,10 @@ Workload (BASELINE.json configs[1], the config its metric is quoted on): the Mix
 style layer — 8 experts, top-2, h = 4096, SwiGLU FFN 14336, 16K tokens per GPU, bf16
 storage / fp32 accumulation — with Zipf(1.2)-skewed synthetic routing (random popularity
 placement).  At N GPUs the experts are split EP = N ways and every rank holds its own 16K
-tokens (weak scaling).  One step = memfine_route_counts -> memfine_plan (device tuner) ->
-memfine_moe_fwd -> memfine_moe_bwd at the chunk count C the tuner picks for the budget.
+tokens (weak scaling).  One step = memfine_route_counts -> memfine_plan (the forward C: device
+tuner, paper model, rule EXACT; the backward C: exact backward workspace) -> memfine_moe_fwd ->
+memfine_moe_bwd, all inside the timed region.  `--gpus N` outside torchrun re-launches itself
+under torch.distributed.run with N ranks.
 
 ``--impl reference`` times the CPU oracle (oracle/, fp64, the method's reference
 definition) on a bounded sample of the same workload — the reference arm of this tier.
@@ -120,6 +122,8 @@ def dist_setup():
     if world > 1:
         import torch.distributed as dist
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        os.environ.setdefault("NCCL_DEBUG", "INFO")          # the communicators' init lines (nranks) on stderr
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
         torch.cuda.set_device(local)
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     else:
@@ -239,30 +243,58 @@ def workload_config(cfg, args, world: int) -> dict:
 
 
 def run_reference(args):
+    """The reference arm: the CPU oracle on rank 0 (the other ranks contribute no work); under torchrun
+    the ranks meet in a gloo group (CPU) for the barrier and the max over ranks of the timed region."""
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
-    if rank != 0:
-        return
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        dist.init_process_group("gloo")
     cfg = emulated_config(args)
     ntok = args.ref_tokens
     times = []
     cores = None
-    for i in range(args.warmup + args.steps):
-        dt, cores = oracle_sample_time(cfg, ntok, rank=i % 8)
-        if i >= args.warmup:
-            times.append(dt)
-    ms = 1000.0 * statistics.mean(times)
+    if rank == 0:
+        for i in range(args.warmup + args.steps):
+            dt, cores = oracle_sample_time(cfg, ntok, rank=i % 8)
+            if i >= args.warmup:
+                times.append(dt)
+    ms = 1000.0 * statistics.mean(times) if times else 0.0
+    if dist is not None:
+        t = torch.tensor([ms], dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+        dist.destroy_process_group()
+    if rank != 0:
+        return
     value = ntok / (ms / 1000.0)
-    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world,
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": max(world, args.gpus),
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": workload_config(cfg, args, world),
+            "config": workload_config(cfg, args, max(world, args.gpus)),
             "cpu_baseline": {"value": value, "unit": "tokens/s", "cores": cores, "kind": "oracle",
                              "sample": f"{ntok} tokens of the workload per step (all {cfg.E} experts, full "
                                        f"h={cfg.h}, g={cfg.g}), oracle fwd (Eq. 4) + bwd (Eq. 5) incl. dW, fp64; "
                                        f"cost linear in tokens"},
             "e2e": {"value": value, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
+
+
+def self_launch(argv, n: int) -> int:
+    """`python bench.py --gpus N` outside torchrun: re-run this script under torch.distributed.run with N
+    ranks on this node (rendezvous on 127.0.0.1, a free port); the ranks' output passes through."""
+    import socket
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + list(argv)
+    env = dict(os.environ)
+    env.setdefault("NCCL_DEBUG", "INFO")        # keep NCCL's communicator init lines (nranks) in the log
+    env.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+    return subprocess.call(cmd, env=env)
 
 
 # ------------------------------------------------------------------------------------ GPU arm
@@ -279,7 +311,8 @@ def main():
     ap.add_argument("--chunks", type=int, default=0, help="override the tuner's C")
     ap.add_argument("--sweep", type=int, default=1, help="also time every bin C (N=1 only)")
     ap.add_argument("--cpu-tokens", type=int, default=96, help="cpu_baseline sample (~15 s of oracle work on 16 cores)")
-    ap.add_argument("--ref-tokens", type=int, default=4)
+    ap.add_argument("--ref-tokens", type=int, default=16,
+                    help="reference arm: tokens per step (the oracle's fixed dW work is ~3 s; 16 tokens ~4 s more)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--placement", default=None)
     ap.add_argument("--ep-emulate", type=int, default=1,
@@ -292,7 +325,11 @@ def main():
     ap.add_argument("--ep-transport", default="copy", choices=["copy", "p2p"],
                     help="N>1: 'copy' = permute into send buffers + NCCL all-to-allv; 'p2p' = dispatch/combine "
                          "fused into the permute kernel and the GEMM epilogues over CUDA-IPC peer memory")
+    ap.add_argument("--fixed-c", action="store_true",
+                    help="skip the per-step MACT tuner calls (route_counts + plan) inside the timed step")
     args = ap.parse_args()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(self_launch(sys.argv[1:], args.gpus))
     if args.impl == "reference":
         return run_reference(args)
 
@@ -338,20 +375,38 @@ def main():
     counts_h = counts.cpu()
     cap = int(args.budget_gb * 1e9) if args.budget_gb else torch.cuda.get_device_properties(dev).total_memory
     static = sum(t.numel() * t.element_size() for t in (wg, wu, wd, dwg, dwu, dwd, x, dy, y, dx, ids, w, dscore))
-    budget = capi.make_budget(cap, args.alpha, static, 0, bins=bins)
-    plan = layer.plan(counts, mf.dims, budget)
-    assert plan["status"] == 0, plan
-    C = args.chunks or plan["C"]
+    # forward C: the paper's model (Eqs. 8-9, beta = D_t (2h + 2g)) with rule EXACT (the library default);
+    # backward C: the exact backward workspace (model IMPL, pass BWD), whose live set per row is larger
+    budget_f = capi.make_budget(cap, args.alpha, static, 0, bins=bins)
+    budget_b = capi.make_budget(cap, args.alpha, static, 0, bins=bins, model=capi.MODEL_IMPL, pass_=capi.BWD)
+    plan_f = layer.plan(counts, mf.dims, budget_f)
+    plan_b = layer.plan(counts, mf.dims, budget_b)
+    assert plan_f["status"] == 0 and plan_b["status"] == 0, (plan_f, plan_b)
+    C_f = args.chunks or plan_f["C"]
+    C_b = args.chunks or plan_b["C"]
+    C = C_b            # the chunked backward is the step's dominant part: reported as config.chunks
 
-    def ws_for(Cc):
+    def ws_for(Cc, Cb=None):
         fwd = layer.workspace_bytes(counts_h, mf.dims, Cc, capi.FWD)
-        bwd = layer.workspace_bytes(counts_h, mf.dims, Cc, capi.BWD)
+        bwd = layer.workspace_bytes(counts_h, mf.dims, Cb or Cc, capi.BWD)
         return fwd, bwd
 
-    def make_step(Cc, ws):
+    def tune(idss):
+        """A3 inside every step, as a training step runs it: counts (A1 + the A2 all-gather), then the
+        device tuner (forward C) and the exact-workspace planner (backward C)."""
+        cnt = mf.route_counts(idss, nsub=8)
+        cf = args.chunks or layer.plan(cnt, mf.dims, budget_f)["C"]
+        cb = args.chunks or layer.plan(cnt, mf.dims, budget_b)["C"]
+        return cf, cb
+
+    def make_step(Cc, ws, Cb=None, tuned=False):
         def step(xx=x, dyy=dy, idss=ids, ww=w):
-            mf.moe_fwd(xx, idss, ww, wg, wu, wd, Cc, ws, y=y)
-            mf.moe_bwd(dyy, xx, idss, ww, wg, wu, wd, Cc, ws, dx=dx, dw_gate=dwg, dw_up=dwu, dw_down=dwd,
+            cf, cb = Cc, Cb or Cc
+            if tuned:
+                cf, cb = tune(idss)
+                assert (cf, cb) == (Cc, Cb or Cc)      # fixed inputs: the tuner's choice is fixed too
+            mf.moe_fwd(xx, idss, ww, wg, wu, wd, cf, ws, y=y)
+            mf.moe_bwd(dyy, xx, idss, ww, wg, wu, wd, cb, ws, dx=dx, dw_gate=dwg, dw_up=dwu, dw_down=dwd,
                        dscore=dscore)
         return step
 
@@ -382,26 +437,37 @@ def main():
         assert st == 0, capi.status_str(st)
         return max_over_ranks(ms, world), profd
 
-    fwd_b, bwd_b = ws_for(C)
-    ws = torch.empty(max(fwd_b, bwd_b), dtype=torch.uint8, device=dev)
+    fwd_b, bwd_b = ws_for(C_f, C_b)
+    ws_bytes = max(fwd_b, bwd_b)
+    if world > 1 and args.ep_transport == "p2p":
+        # the fused exchange derives every peer's buffer addresses from one workspace size: the largest any
+        # rank needs (the counts are all-gathered, so every rank computes the same number)
+        for rr in range(world):
+            dr = layer.make_dims(T, h, g, E, k, ep_size=EP, ep_rank=rr, dtype=torch.bfloat16)
+            ws_bytes = max(ws_bytes, layer.workspace_bytes(counts_h, dr, C_f, capi.FWD),
+                           layer.workspace_bytes(counts_h, dr, C_b, capi.BWD))
+    ws = torch.empty(ws_bytes, dtype=torch.uint8, device=dev)
     if world > 1 and args.ep_transport == "p2p":
         mf.set_ep_transport(capi.EP_P2P)
         mf.register_workspace(ws)
-    step = make_step(C, ws)
+    step = make_step(C_f, ws, C_b, tuned=not args.fixed_c)
 
-    # launches per step (the library's own kernels)
+    # launches per step (the library's own kernels: the tuner's histogram + plan kernel, fwd, bwd)
     step()
     torch.cuda.synchronize()
     mf.sync()
     launches_fwd_bwd = None
-    mf.moe_fwd(x, ids, w, wg, wu, wd, C, ws, y=y)
+    mf.moe_fwd(x, ids, w, wg, wu, wd, C_f, ws, y=y)
     mf.sync()
-    lf = mf.last_stats()["kernel_launches"]
-    mf.moe_bwd(dy, x, ids, w, wg, wu, wd, C, ws, dx=dx, dw_gate=dwg, dw_up=dwu, dw_down=dwd, dscore=dscore)
+    fstats = mf.last_stats()
+    lf = fstats["kernel_launches"]
+    mf.moe_bwd(dy, x, ids, w, wg, wu, wd, C_b, ws, dx=dx, dw_gate=dwg, dw_up=dwu, dw_down=dwd, dscore=dscore)
     mf.sync()
     bstats = mf.last_stats()
-    launches_fwd_bwd = lf + bstats["kernel_launches"]
+    launches_fwd_bwd = lf + bstats["kernel_launches"] + (0 if args.fixed_c else 2)
     rows_total = sum(bstats["rows"])  # s''_r: copies this rank's experts processed per step
+    comm_ops = {"fwd": fstats.get("comm_ops", 0), "bwd": bstats.get("comm_ops", 0),
+                "per_chunk_fwd": fstats.get("comm_ops", 0) / C_f, "per_chunk_bwd": bstats.get("comm_ops", 0) / C_b}
 
     with ClockSampler(local) as clk:
         ms, prof = timed(step, args.steps, args.warmup, prof=True)
@@ -487,8 +553,9 @@ def main():
             comp.wait_event(in_ready[b])
             xx, dyy, idd, ww = ins[b]
             yy, dxx = outs[b]
-            mf.moe_fwd(xx, idd, ww, wg, wu, wd, C, ws, y=yy)
-            mf.moe_bwd(dyy, xx, idd, ww, wg, wu, wd, C, ws, dx=dxx, dw_gate=dwg, dw_up=dwu, dw_down=dwd,
+            cf, cb = (C_f, C_b) if args.fixed_c else tune(idd)
+            mf.moe_fwd(xx, idd, ww, wg, wu, wd, cf, ws, y=yy)
+            mf.moe_bwd(dyy, xx, idd, ww, wg, wu, wd, cb, ws, dx=dxx, dw_gate=dwg, dw_up=dwu, dw_down=dwd,
                        dscore=dscore)
             done[b].record(comp)
             with torch.cuda.stream(cs):
@@ -518,7 +585,7 @@ def main():
     per_C = {}
     if args.sweep and world == 1:
         for Cc in bins:
-            if Cc == C:
+            if Cc == C_f == C_b:
                 per_C[Cc] = {"ms_per_step": ms, "tokens_per_s": value, "peak_act_gb": peak_gb(Cc)}
                 continue
             try:   # a side measurement: a failure here must not cost the headline line
@@ -529,7 +596,7 @@ def main():
             except Exception as ex:  # noqa: BLE001
                 per_C[Cc] = {"error": f"{type(ex).__name__}: {ex}"[:300]}
                 torch.cuda.synchronize()
-    peak_c = peak_gb(C)
+    peak_c = max(fwd_b, bwd_b) / 1e9
     peak_1 = peak_gb(1)
     beta = 2 * (2 * h + 2 * g)
     paper_model = {Cc: beta * max(int(counts_h[:, j * (8 // Cc):(j + 1) * (8 // Cc), rank * El:(rank + 1) * El].sum())
@@ -600,7 +667,11 @@ def main():
         "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
-        "config": {**workload_config(cfg, args, world), "chunks": C, "tuner": plan,
+        "config": {**workload_config(cfg, args, world), "chunks": C,
+                   "tuner": {"in_timed_step": not args.fixed_c, "rule": "EXACT (library default)",
+                             "fwd": {"C": C_f, "model": "paper (Eqs. 8-9, beta = D_t (2h + 2g))", **plan_f},
+                             "bwd": {"C": C_b, "model": "IMPL (exact backward workspace)", **plan_b}},
+                   "comm_ops": comm_ops,
                    "ep_transport": args.ep_transport if world > 1 else None,
                    "overlap": overlap and C > 1,
                    "pdl": os.environ.get("MEMFINE_PDL", "1") != "0",   # programmatic dependent launch

@@ -54,7 +54,7 @@ typedef enum {
 } memfine_status;
 
 enum { MEMFINE_BF16 = 0, MEMFINE_FP32 = 1, MEMFINE_MXFP8 = 2 }; /* memfine_dims.dtype */
-enum { MEMFINE_RULE_EQ9 = 0, MEMFINE_RULE_EXACT = 1 }; /* memfine_budget.rule */
+enum { MEMFINE_RULE_EXACT = 0, MEMFINE_RULE_EQ9 = 1 }; /* memfine_budget.rule (0 = EXACT, the default) */
 enum { MEMFINE_FWD = 0, MEMFINE_BWD = 1 };           /* workspace pass      */
 enum { MEMFINE_MODEL_PAPER = 0, MEMFINE_MODEL_IMPL = 1 }; /* memfine_budget.model */
 
@@ -115,10 +115,13 @@ typedef struct {
     const int32_t* bins;         /* host; strictly increasing, bins[0] >= 1; NULL = {1,2,4,8}
                                                                          */
     int32_t  nbins;
-    int32_t  rule;               /* MEMFINE_RULE_EQ9: C = smallest bin >= ceil(s''/s'_max)
-                                    (Eq. 9 + "the large bin closest to c", reading R8);
-                                    MEMFINE_RULE_EXACT: smallest bin whose true per-chunk
-                                    maximum fits s'_max (every bin must divide nsub)        */
+    int32_t  rule;               /* MEMFINE_RULE_EXACT (0, the default): smallest bin whose true
+                                    per-chunk maximum max_j s''_{r,j}(C) fits s'_max (every bin
+                                    must divide nsub) - Eq. 3 holds for the chunks actually run;
+                                    MEMFINE_RULE_EQ9: C = smallest bin >= ceil(s''/s'_max)
+                                    (Eq. 9 + "the large bin closest to c", reading R8), the
+                                    paper's estimate, which assumes the chunk maximum is s''/C
+                                    (reading R11)                                            */
     int32_t  model;              /* MEMFINE_MODEL_PAPER: the paper's per-copy activation
                                     beta = D_t(2h+2g) (Table 2 rows 11-13; Eqs. 8-9 as above).
                                     MEMFINE_MODEL_IMPL: C = smallest bin whose EXACT workspace
@@ -157,6 +160,9 @@ typedef struct {
     int32_t  device_error;          /* latched memfine_status from the device, or 0         */
     int32_t  gemm_launches;         /* kernels launched by the last call                    */
     int32_t  kernel_launches;
+    int32_t  comm_ops;              /* point-to-point operations of the call's exchanges (EP path,
+                                       copy transport: ncclSend + ncclRecv calls, or device copies
+                                       in an in-process group); all chunks                      */
 } memfine_stats;
 
 /* ---------------------------------------------------------------------------------- */
@@ -308,11 +314,11 @@ memfine_status memfine_moe_bwd(memfine_handle_t h, const void* dy, const void* x
  *   scores = softmax over the k selected logits (the renormalised top-k convention).
  *   x dev [T][h], w_router dev [E][h] (dims.dtype, replicated on every EP rank), ids dev int32
  *   [T][k], scores dev fp32 [T][k], logits dev fp32 [T][E] (nullable: library scratch).
- *   BF16/MXFP8 handles: the logits GEMM (and the backward's dW_r GEMMs) run on cuBLAS (bf16 in, fp32
- *   accumulate/out; a handle per memfine handle, created on first use - MEMFINE_ERR_CUDA if that or a
- *   cuBLAS call fails); top-k, softmax and the backward's row kernel are the library's.  FP32 handles
- *   use the library's CUDA-core GEMM (fp32 FMA, no TF32).  Stream-ordered; not graph-capture safe on
- *   the first call of a handle (it allocates scratch and the cuBLAS handle). */
+ *   BF16/MXFP8 handles: the logits GEMM and the backward's dW_r GEMMs run on the library's tcgen05
+ *   expert-GEMM kernels (bf16 operands, fp32 accumulation in TMEM; the T tokens form one 128-row-padded
+ *   segment, TMA zero-fills past T and E); top-k, softmax and the backward's row kernel are the
+ *   library's.  FP32 handles use the library's CUDA-core GEMM (fp32 FMA, no TF32).  Stream-ordered; not
+ *   graph-capture safe on the first call of a handle (it allocates and initialises scratch). */
 memfine_status memfine_router_fwd(memfine_handle_t h, const void* x, const void* w_router, int32_t* ids,
                                   float* scores, float* logits, void* stream);
 /* Router backward from the layer's d_score (memfine_moe_bwd's dscore):
@@ -380,6 +386,22 @@ memfine_status memfine_profile_read(memfine_handle_t h, memfine_profile* out);
 memfine_status memfine_set_debug(memfine_handle_t h, int32_t enable);
 memfine_status memfine_debug_perm(memfine_handle_t h, int32_t chunk, int64_t* perm_host, int64_t cap,
                                   int64_t* n);
+/* Debug, ep_size == 1 (test infrastructure: the debug capture synchronises after each chunk's GEMMs).
+ * memfine_debug_rows: chunk `chunk` of the last fwd or bwd call, its expert-major padded rows' copy
+ *   index (i*k + slot) or -1 for a padding row; *n = the chunk's padded rows.  src_of_host NULL:
+ *   only *n.
+ * memfine_debug_mx (MXFP8 handles): the decisions the kernels took on one quantised operand of chunk
+ *   `chunk` of the last call - codes_host [rows][cols] E4M3 bytes, scales_host [rows*cols/32] E8M0
+ *   bytes in the scale-chunk layout of memfine_mx_quantize with K = cols.  which:
+ *     0 a (fwd), rows = the chunk's padded rows, cols = g (blocks along g)
+ *     1 dG || dU (bwd, the dX operand), rows = padded rows, cols = 2g
+ *     2 x, 3 dY, 4 dG || dU, 5 a_w: MEMFINE_FLAG_MX_WGRAD's columnwise operands (reading R28c),
+ *       rows = h / h / 2g / g operand columns, cols = the workspace's row capacity (blocks of 32
+ *       rows along it; only the chunk's padded rows are meaningful).
+ *   codes_host NULL: only *rows and *cols; cap_codes < rows*cols: MEMFINE_ERR_INVALID_ARG. */
+memfine_status memfine_debug_rows(memfine_handle_t h, int32_t chunk, int32_t* src_of_host, int64_t cap, int64_t* n);
+memfine_status memfine_debug_mx(memfine_handle_t h, int32_t chunk, int32_t which, uint8_t* codes_host,
+                                uint8_t* scales_host, int64_t cap_codes, int64_t* rows, int64_t* cols);
 
 #ifdef __cplusplus
 }

@@ -195,6 +195,23 @@ def moe_backward(d: Dims, dy, x, ids, w, wg, wu, wd):
     return dx, ds, dwg, dwu, dwd
 
 
+def moe_backward_experts(d: Dims, dy, x, ids, w, wg, wu, wd, sel):
+    """Eq. 5 with the weight gradients of the experts `sel` only: dx, dscore, dwg, dwu, dwd
+    ([len(sel)][g][h] / [len(sel)][h][g]) - the rows / expert slices of moe_backward."""
+    bf = d.in_dtype
+    dy, x, wg, wu, wd = (_wt(a, bf) for a in (dy, x, wg, wu, wd))
+    ids = np.ascontiguousarray(ids, dtype=np.int32)
+    w = np.ascontiguousarray(w, dtype=np.float64)
+    sel = np.ascontiguousarray(sel, dtype=np.int32)
+    n, m = d.EP * d.T, len(sel)
+    dx = np.zeros((n, d.h)); ds = np.zeros((n, d.k))
+    dwg = np.zeros((m, d.g, d.h)); dwu = np.zeros((m, d.g, d.h)); dwd = np.zeros((m, d.h, d.g))
+    st = lib().oracle_moe_backward_experts(C.byref(d.c()), _p(dy), _p(x), _p(ids), _p(w), _p(wg), _p(wu), _p(wd),
+                                           C.c_int32(m), _p(sel), _p(dx), _p(ds), _p(dwg), _p(dwu), _p(dwd))
+    assert st == 0
+    return dx, ds, dwg, dwu, dwd
+
+
 def fcda_forward(d: Dims, C_: int, x, ids, w, wg, wu, wd, D_t: int = 2):
     """Eq. 6 chunk loop.  Returns y, chunk_bytes [EP][C], peak [EP] (paper meter)."""
     bf = d.in_dtype
@@ -303,46 +320,96 @@ def mx_weights(d: Dims, wg, wu, wd, mode: int = 1):
     return out
 
 
-def moe_mx(d: Dims, x, ids, w, wq, dy=None, mode: int = 1, wd=None, wgrad_C: int = 0):
+class _MxFed(C.Structure):
+    _fields_ = [("a_q", C.c_void_p), ("dgu_q", C.c_void_p), ("dgu_col_q", C.c_void_p), ("aw_col_q", C.c_void_p)]
+
+
+class _MxExact(C.Structure):
+    _fields_ = [("a", C.c_void_p), ("dgu", C.c_void_p), ("gu", C.c_void_p), ("da", C.c_void_p)]
+
+
+def _mx_exact(n, g, with_dy):
+    arr = {"a": np.zeros((n, g)), "gu": np.zeros((n, 2 * g)),
+           "dgu": np.zeros((n, 2 * g)) if with_dy else None, "da": np.zeros((n, g)) if with_dy else None}
+    ptr = lambda v: v.ctypes.data if v is not None else None
+    return arr, _MxExact(ptr(arr["a"]), ptr(arr["dgu"]), ptr(arr["gu"]), ptr(arr["da"]))
+
+
+def _mx_fed(fed, nq, g):
+    """fed: None or a dict with any of a_q [nq][g], dgu_q [nq][2g], dgu_col_q [nq][2g], aw_col_q [nq][g]
+    (another implementation's decisions, dequantised per copy).  Returns (struct or None, keep-alive)."""
+    if not fed:
+        return None, []
+    widths = {"a_q": g, "dgu_q": 2 * g, "dgu_col_q": 2 * g, "aw_col_q": g}
+    keep, ptrs = [], {}
+    for key, wdt in widths.items():
+        v = fed.get(key)
+        if v is None:
+            ptrs[key] = None
+            continue
+        v = np.ascontiguousarray(v, dtype=np.float64).reshape(nq, wdt)
+        keep.append(v)
+        ptrs[key] = v.ctypes.data
+    return _MxFed(**ptrs), keep
+
+
+def moe_mx(d: Dims, x, ids, w, wq, dy=None, mode: int = 1, wd=None, wgrad_C: int = 0, fed=None,
+           return_exact: bool = False):
     """MX variant of the layer (mode 0: quantisers off).  wq from mx_weights(mode); wd the unquantised
     W_down (needed with dy: the dA step keeps BF16 operands).  wgrad_C = 0: weight gradients from
     unquantised operands; wgrad_C = C >= 1: MXFP8 weight gradients (operand columns quantised along
-    each expert's copies in each of the C chunks; reading R28c).
-    Returns y, or (y, dx, dscore, dwg, dwu, dwd) when dy is given."""
+    each expert's copies in each of the C chunks; reading R28c).  Every code is decided on
+    the exact value; fed (see _mx_fed) replaces those decisions by another implementation's.
+    Returns y, or (y, dx, dscore, dwg, dwu, dwd) when dy is given; with return_exact a further dict
+    {"a": [nq][g], "dgu": [nq][2g], "gu": [nq][2g], "da": [nq][g]} of the exact values per copy
+    (a, dG || dU: what the quantisers act on; G || U, dA: what those are functions of)."""
     x = _wt(x, d.in_dtype)
     ids = np.ascontiguousarray(ids, dtype=np.int32)
     w = np.ascontiguousarray(w, dtype=np.float64)
     n = d.EP * d.T
+    nq = n * d.k
     y = np.zeros((n, d.h))
     arr = (C.POINTER(C.c_double) * 5)(*[np.ascontiguousarray(a).ctypes.data_as(C.POINTER(C.c_double)) for a in wq])
+    fs, keep = _mx_fed(fed, nq, d.g)
+    exact, ex = _mx_exact(nq, d.g, dy is not None) if return_exact else (None, None)
+    fp = C.byref(fs) if fs is not None else None
+    ep = C.byref(ex) if ex is not None else None
     if dy is None:
         st = lib().oracle_moe_mx(C.byref(d.c()), C.c_int32(mode), None, _p(x), _p(ids), _p(w), arr, None, _p(y),
-                                 None, None, None, None, None, C.c_int32(0))
+                                 None, None, None, None, None, C.c_int32(0), fp, ep)
         assert st == 0
-        return y
+        del keep
+        return (y, exact) if return_exact else y
     dy = _wt(dy, d.in_dtype)
     wd = _wt(wd, d.in_dtype)
     dx = np.zeros((n, d.h)); ds = np.zeros((n, d.k))
     dwg = np.zeros((d.E, d.g, d.h)); dwu = np.zeros((d.E, d.g, d.h)); dwd = np.zeros((d.E, d.h, d.g))
     st = lib().oracle_moe_mx(C.byref(d.c()), C.c_int32(mode), _p(dy), _p(x), _p(ids), _p(w), arr, _p(wd), _p(y), _p(dx),
-                             _p(ds), _p(dwg), _p(dwu), _p(dwd), C.c_int32(wgrad_C))
+                             _p(ds), _p(dwg), _p(dwu), _p(dwd), C.c_int32(wgrad_C), fp, ep)
     assert st == 0
-    return y, dx, ds, dwg, dwu, dwd
+    del keep
+    out = (y, dx, ds, dwg, dwu, dwd)
+    return out + (exact,) if return_exact else out
 
 
-def moe_mx_tokens(d: Dims, toks, x, dy, ids, w, wg, wu, wd, mode: int = 1):
+def moe_mx_tokens(d: Dims, toks, x, dy, ids, w, wg, wu, wd, mode: int = 1, fed=None, return_exact: bool = False):
     """MX layer on a token subset (full-size sampled parity): (y, dx, dscore) rows of toks, as
-    moe_mx would give them; weights are quantised one expert at a time."""
+    moe_mx would give them; weights are quantised one expert at a time.  fed / return_exact as in
+    moe_mx, indexed by the sampled copy p*k + slot (a_q and dgu_q only)."""
     toks = np.ascontiguousarray(toks, dtype=np.int64)
     x, dy, wg, wu, wd = (_wt(a, d.in_dtype) for a in (x, dy, wg, wu, wd))
     ids = np.ascontiguousarray(ids, dtype=np.int32)
     w = np.ascontiguousarray(w, dtype=np.float64)
     n = len(toks)
     y = np.zeros((n, d.h)); dx = np.zeros((n, d.h)); ds = np.zeros((n, d.k))
+    fs, keep = _mx_fed(fed, n * d.k, d.g)
+    exact, ex = _mx_exact(n * d.k, d.g, True) if return_exact else (None, None)
     st = lib().oracle_moe_mx_tokens(C.byref(d.c()), C.c_int32(mode), C.c_int64(n), _p(toks), _p(dy), _p(x), _p(ids),
-                                    _p(w), _p(wg), _p(wu), _p(wd), _p(y), _p(dx), _p(ds))
+                                    _p(w), _p(wg), _p(wu), _p(wd), _p(y), _p(dx), _p(ds),
+                                    C.byref(fs) if fs is not None else None, C.byref(ex) if ex is not None else None)
     assert st == 0
-    return y, dx, ds
+    del keep
+    return (y, dx, ds, exact) if return_exact else (y, dx, ds)
 
 
 def m_g(v: int, p: int, r_pp: int, full_recompute: bool = False) -> int:

@@ -476,6 +476,41 @@ int32_t oracle_moe_backward(const oracle_dims* d, const void* dy, const void* x,
     return 0;
 }
 
+/* Eq. 5 for a subset of experts: dx and dscore as oracle_moe_backward, and the weight gradients of
+ * the experts sel[0..nsel) only (dwg/dwu [nsel][g][h], dwd [nsel][h][g]), each accumulated over its
+ * copies in the canonical order exactly as oracle_moe_backward does - for full-size checks, where
+ * all experts' fp64 gradients would not fit in host memory at once. */
+int32_t oracle_moe_backward_experts(const oracle_dims* d, const void* dy, const void* x, const int32_t* ids,
+                                    const double* w, const void* wg, const void* wu, const void* wd, int32_t nsel,
+                                    const int32_t* sel, double* dx, double* dscore, double* dwg, double* dwu,
+                                    double* dwd)
+{
+    int64_t h = d->h, g = d->g, nq = (int64_t)d->EP * d->T * d->k;
+    double* a_all = (double*)malloc(sizeof(double) * (size_t)(nq > 0 ? nq : 1) * g);
+    double* dG_all = (double*)malloc(sizeof(double) * (size_t)(nq > 0 ? nq : 1) * g);
+    double* dU_all = (double*)malloc(sizeof(double) * (size_t)(nq > 0 ? nq : 1) * g);
+    double* dO_all = (double*)malloc(sizeof(double) * (size_t)(nq > 0 ? nq : 1) * h);
+    int64_t* order = (int64_t*)malloc(sizeof(int64_t) * (size_t)(nq > 0 ? nq : 1));
+    int32_t* ids_e = (int32_t*)malloc(sizeof(int32_t) * (size_t)(nq > 0 ? nq : 1));
+    if (!a_all || !dG_all || !dU_all || !dO_all || !order || !ids_e) {
+        free(a_all); free(dG_all); free(dU_all); free(dO_all); free(order); free(ids_e);
+        return 1;
+    }
+    backward_copies(d, dy, x, ids, w, wg, wu, wd, dx, dscore, a_all, dO_all, dG_all, dU_all);
+    for (int64_t q = 0; q < nq; q++) order[q] = q;   /* (src, token, slot) ascending */
+    /* expert sel[i] becomes expert i of a problem with nsel experts: accumulate_dw visits the same
+     * copies in the same order */
+    for (int64_t q = 0; q < nq; q++) {
+        ids_e[q] = -1;
+        for (int32_t i = 0; i < nsel; i++) if (ids[q] == sel[i]) { ids_e[q] = i; break; }
+    }
+    oracle_dims ds = *d;
+    ds.E = nsel;
+    accumulate_dw(&ds, x, ids_e, order, nq, a_all, dO_all, dG_all, dU_all, dwg, dwu, dwd);
+    free(a_all); free(dG_all); free(dU_all); free(dO_all); free(order); free(ids_e);
+    return 0;
+}
+
 /* ------------------------------------------------------------------------- */
 /* FCDA, Eq. 6 / Eq. 7, written as the paper's chunk loop with the meter.     */
 /* ------------------------------------------------------------------------- */
@@ -786,22 +821,25 @@ void oracle_mx_quantize(const void* v, int32_t in_dtype, int64_t n, uint8_t* cod
     }
 }
 
-/* Decision precision (reading R28b): a quantised code is decided on the value as the
- * kernel holds it - a in fp32 (from the fp32 accumulators), dG / dU in bf16 (as stored for the
- * weight gradients) - so these are rounded (to nearest even) before their blocks are quantised;
- * and the backward's dA step works from the recomputed G || U as stored (bf16), since a code
- * flip amplifies that 2^-9 difference to a 2^-4 E4M3 step. */
-static double round_f32(double v) { return (double)(float)v; }
-static double round_bf16(double v)
-{
-    float f = (float)v;
-    uint32_t u;
-    memcpy(&u, &f, sizeof u);
-    if ((u & 0x7F800000u) != 0x7F800000u) u += 0x7FFFu + ((u >> 16) & 1u);
-    u &= 0xFFFF0000u;
-    memcpy(&f, &u, sizeof f);
-    return (double)f;
-}
+/* Every quantiser below acts on the EXACT value of its operand (fp64 here), as the definition
+ * above states; an implementation that holds the operand in a narrower format before quantising
+ * may decide a neighbouring code at a near-tie.  For parity against such an implementation the
+ * layer functions accept the other side's decisions ("fed" codes, dequantised per copy) and also
+ * return the exact pre-quantisation values, so a test can (i) check every fed code against the
+ * exact value it encodes and (ii) compare everything downstream of the decisions.  Without fed
+ * codes the oracle decides every code itself. */
+typedef struct {
+    const double* a_q;       /* [nq][g]  a (forward, along g), dequantised                   */
+    const double* dgu_q;     /* [nq][2g] dG || dU (dX operand, along g), dequantised          */
+    const double* dgu_col_q; /* [nq][2g] dG || dU columnwise (R28c weight gradients)          */
+    const double* aw_col_q;  /* [nq][g]  a_w = w a columnwise (R28c)                          */
+} oracle_mx_fed;
+typedef struct {
+    double* a;               /* [nq][g]  exact a = silu(G) U                                  */
+    double* dgu;             /* [nq][2g] exact dG || dU                                       */
+    double* gu;              /* [nq][2g] exact G || U (what a, dG, dU are functions of)        */
+    double* da;              /* [nq][g]  exact dA = w W_down^T dY                             */
+} oracle_mx_exact;
 
 /* quantise-dequantise n strided doubles in place (blocks of 32 along the stride) */
 static void mx_qdq(double* v, int64_t n, int64_t stride, int mode)
@@ -844,13 +882,13 @@ void oracle_mx_weights(const oracle_dims* d, int32_t mode, const void* wg, const
     }
 }
 
-/* One copy, MX variant: forward (y term), backward (dx term, d_score, and the
- * unquantised dW operands a, dO, dG, dU).  Same loop orders as expert_forward /
- * expert_backward, quantisers inserted. */
+/* One copy, MX variant: forward (o), backward (dx term, d_score, and the exact dW operands a,
+ * dO, dG, dU).  Same loop orders as expert_forward / expert_backward, quantisers inserted.
+ * aq_in / dgq_in: fed dequantised a [g] / dG || dU [2g] (NULL: quantise the exact values). */
 static void expert_mx(const oracle_dims* d, int mode, const void* x, int64_t xoff, const void* dy, int64_t dyoff,
                       double ws, double* const* wq, int32_t ew, const void* wd, int32_t e, double* scratch,
                       double* O, double* a_out, double* dO_out, double* dG_out, double* dU_out, double* dxc,
-                      double* dscore)
+                      double* dscore, const double* aq_in, const double* dgq_in, double* gu_out, double* da_out)
 {
     int64_t h = d->h, g = d->g;
     double *xq = scratch, *G = xq + h, *U = G + g, *A = U + g, *Aq = A + g, *dyq = Aq + g, *dA = dyq + h;
@@ -865,25 +903,19 @@ static void expert_mx(const oracle_dims* d, int mode, const void* x, int64_t xof
         }
         G[n] = sg; U[n] = su;
         A[n] = sg * sigmoid(sg) * su;
-        Aq[n] = mode ? round_f32(A[n]) : A[n];
+        Aq[n] = aq_in ? aq_in[n] : A[n];
     }
-    mx_qdq(Aq, g, 1, mode);
+    if (!aq_in) mx_qdq(Aq, g, 1, mode);
     for (int64_t m = 0; m < h; m++) {
         double so = 0.0;
         for (int64_t n = 0; n < g; n++) so += wq[2][((int64_t)ew * h + m) * g + n] * Aq[n];
         O[m] = so;
     }
+    for (int64_t n = 0; n < g; n++) a_out[n] = A[n];
+    if (gu_out) { memcpy(gu_out, G, sizeof(double) * (size_t)g); memcpy(gu_out + g, U, sizeof(double) * (size_t)g); }
     if (!dy) return;
     for (int64_t m = 0; m < h; m++) dyq[m] = load(dy, dyoff + m, d->in_dtype);   /* dA: unquantised */
     /* u = W_down^T dY (BF16 operands);  d_score = <u, a>;  dA = w u (reading R15) */
-    /* G, U, a as the dA step sees them (mode 1: recomputed G || U stored as bf16) */
-    for (int64_t n = 0; n < g; n++) {
-        if (mode) {
-            G[n] = round_bf16(G[n]);
-            U[n] = round_bf16(U[n]);
-            A[n] = G[n] * sigmoid(G[n]) * U[n];
-        }
-    }
     double dwv = 0.0;
     for (int64_t n = 0; n < g; n++) {
         double s = 0.0;
@@ -892,17 +924,19 @@ static void expert_mx(const oracle_dims* d, int mode, const void* x, int64_t xof
         dA[n] = ws * s;
     }
     *dscore = dwv;
+    if (da_out) memcpy(da_out, dA, sizeof(double) * (size_t)g);
     for (int64_t m = 0; m < h; m++) dO_out[m] = ws * load(dy, dyoff + m, d->in_dtype);
     for (int64_t n = 0; n < g; n++) {
         double sg = sigmoid(G[n]);
         dG_out[n] = dA[n] * U[n] * sg * (1.0 + G[n] * (1.0 - sg));
         dU_out[n] = dA[n] * G[n] * sg;
-        dGq[n] = mode ? round_bf16(dG_out[n]) : dG_out[n];
-        dUq[n] = mode ? round_bf16(dU_out[n]) : dU_out[n];
-        a_out[n] = A[n];
+        dGq[n] = dgq_in ? dgq_in[n] : dG_out[n];
+        dUq[n] = dgq_in ? dgq_in[g + n] : dU_out[n];
     }
-    mx_qdq(dGq, g, 1, mode);
-    mx_qdq(dUq, g, 1, mode);
+    if (!dgq_in) {
+        mx_qdq(dGq, g, 1, mode);
+        mx_qdq(dUq, g, 1, mode);
+    }
     for (int64_t c = 0; c < h; c++) {
         double s1 = 0.0, s2 = 0.0;
         for (int64_t n = 0; n < g; n++) {
@@ -918,20 +952,20 @@ static void expert_mx(const oracle_dims* d, int mode, const void* x, int64_t xof
  * the K dimension of expert e's weight-gradient GEMMs is its copies in the canonical order
  * (src rank, token, slot; reading R3).  Every operand column is quantised in blocks of 32
  * consecutive copies counted from the start of that list (the last block zero-padded - the
- * 128-row segment padding).  Operands as the kernel holds them (reading R28b): x and dY as
- * stored (bf16 inputs), dG / dU as stored (bf16), a_w = w * a as stored (bf16 of the fp32
- * product, a as the dA step sees it).  dW_gate[e] += dG^T x, dW_up[e] += dU^T x,
- * dW_down[e] += dY^T a_w, all on dequantised values, accumulated in fp64.
- * mode 0: no rounding and no quantiser - then this equals accumulate_dw up to summation order. */
+ * 128-row segment padding).  Operands: x and dY (the layer's inputs), dG, dU and a_w = w a, all
+ * exact values (or, for dG || dU and a_w, the fed dequantised columnwise values).
+ * dW_gate[e] += dG^T x, dW_up[e] += dU^T x, dW_down[e] += dY^T a_w, accumulated in fp64.
+ * mode 0: no quantiser - then this equals accumulate_dw up to summation order. */
 static int accumulate_dw_mx(const oracle_dims* d, int mode, int32_t C, const void* x, const void* dy,
                             const int32_t* ids, const double* w, const double* a_all, const double* dG_all,
-                            const double* dU_all, double* dwg, double* dwu, double* dwd)
+                            const double* dU_all, const oracle_mx_fed* fed, double* dwg, double* dwu, double* dwd)
 {
     int64_t h = d->h, g = d->g, E = d->E, k = d->k, T = d->T, EP = d->EP;
     memset(dwg, 0, sizeof(double) * (size_t)E * g * h);
     memset(dwu, 0, sizeof(double) * (size_t)E * g * h);
     memset(dwd, 0, sizeof(double) * (size_t)E * h * g);
     int64_t nq = EP * T * k;
+    const int fed_gu = fed && fed->dgu_col_q, fed_aw = fed && fed->aw_col_q;
     int64_t* list = (int64_t*)malloc(sizeof(int64_t) * (size_t)(nq > 0 ? nq : 1));
     double* Xb = (double*)malloc(sizeof(double) * (size_t)32 * (2 * h + 3 * g));
     if (!list || !Xb) { free(list); free(Xb); return 1; }
@@ -956,17 +990,16 @@ static int accumulate_dw_mx(const oracle_dims* d, int mode, int32_t C, const voi
                         Yb[i * h + c] = q >= 0 ? load(dy, tok * h + c, d->in_dtype) : 0.0;
                     }
                     for (int64_t c = 0; c < g; c++) {
-                        double gv = q >= 0 ? dG_all[q * g + c] : 0.0, uv = q >= 0 ? dU_all[q * g + c] : 0.0;
-                        double av = q >= 0 ? w[q] * a_all[q * g + c] : 0.0;
-                        Gb[i * g + c] = mode ? round_bf16(gv) : gv;
-                        Ub[i * g + c] = mode ? round_bf16(uv) : uv;
-                        Ab[i * g + c] = mode ? round_bf16(round_f32(av)) : av;
+                        Gb[i * g + c] = q < 0 ? 0.0 : fed_gu ? fed->dgu_col_q[q * 2 * g + c] : dG_all[q * g + c];
+                        Ub[i * g + c] = q < 0 ? 0.0 : fed_gu ? fed->dgu_col_q[q * 2 * g + g + c] : dU_all[q * g + c];
+                        Ab[i * g + c] = q < 0 ? 0.0 : fed_aw ? fed->aw_col_q[q * g + c] : w[q] * a_all[q * g + c];
                     }
                 }
                 /* columnwise blocks: 32 rows of one column (stride = the row length) */
                 for (int64_t c = 0; c < h; c++) { mx_qdq(Xb + c, 32, h, mode); mx_qdq(Yb + c, 32, h, mode); }
                 for (int64_t c = 0; c < g; c++) {
-                    mx_qdq(Gb + c, 32, g, mode); mx_qdq(Ub + c, 32, g, mode); mx_qdq(Ab + c, 32, g, mode);
+                    if (!fed_gu) { mx_qdq(Gb + c, 32, g, mode); mx_qdq(Ub + c, 32, g, mode); }
+                    if (!fed_aw) mx_qdq(Ab + c, 32, g, mode);
                 }
                 #pragma omp parallel for schedule(static)
                 for (int64_t nn = 0; nn < g; nn++) {
@@ -996,10 +1029,13 @@ static int accumulate_dw_mx(const oracle_dims* d, int mode, int32_t C, const voi
  * unquantised operands in the canonical copy order (accumulate_dw); wgrad_C >= 1: MXFP8
  * weight gradients over the chunk partition with C = wgrad_C (accumulate_dw_mx).  Outputs as
  * oracle_moe_forward / oracle_moe_backward.  wq from oracle_mx_weights with the same mode; wd the
- * unquantised W_down (in_dtype) for the dA step. */
+ * unquantised W_down (in_dtype) for the dA step.  fed (nullable, members nullable): another
+ * implementation's decisions, dequantised per copy q = (src*T + i)*k + slot; ex (nullable, members
+ * nullable): the exact a, dG || dU, G || U and dA per copy (a and G || U also without dy). */
 int32_t oracle_moe_mx(const oracle_dims* d, int32_t mode, const void* dy, const void* x, const int32_t* ids,
                       const double* w, double* const* wq, const void* wd, double* y, double* dx, double* dscore,
-                      double* dwg, double* dwu, double* dwd, int32_t wgrad_C)
+                      double* dwg, double* dwu, double* dwd, int32_t wgrad_C, const oracle_mx_fed* fed,
+                      const oracle_mx_exact* ex)
 {
     int64_t h = d->h, g = d->g, ntok = (int64_t)d->EP * d->T, nq = ntok * d->k;
     double *a_all = NULL, *dG_all = NULL, *dU_all = NULL, *dO_all = NULL;
@@ -1034,10 +1070,21 @@ int32_t oracle_moe_mx(const oracle_dims* d, int32_t mode, const void* dy, const 
                         memset(aq, 0, sizeof(double) * (size_t)g); memset(dGq, 0, sizeof(double) * (size_t)g);
                         memset(dUq, 0, sizeof(double) * (size_t)g); memset(dOq, 0, sizeof(double) * (size_t)h);
                     }
+                    if (ex && ex->a) memset(ex->a + q * g, 0, sizeof(double) * (size_t)g);
+                    if (ex && ex->dgu) memset(ex->dgu + q * 2 * g, 0, sizeof(double) * (size_t)(2 * g));
+                    if (ex && ex->gu) memset(ex->gu + q * 2 * g, 0, sizeof(double) * (size_t)(2 * g));
+                    if (ex && ex->da) memset(ex->da + q * g, 0, sizeof(double) * (size_t)g);
                     continue;
                 }
                 expert_mx(d, mode, x, t * h, dy, t * h, w[q], wq, e, wd, e, scratch, O, aq, dOq, dGq, dUq, dxc,
-                          dy ? dscore + q : NULL);
+                          dy ? dscore + q : NULL, fed && fed->a_q ? fed->a_q + q * g : NULL,
+                          fed && fed->dgu_q ? fed->dgu_q + q * 2 * g : NULL,
+                          ex && ex->gu ? ex->gu + q * 2 * g : NULL, ex && ex->da && dy ? ex->da + q * g : NULL);
+                if (ex && ex->a) memcpy(ex->a + q * g, aq, sizeof(double) * (size_t)g);
+                if (ex && ex->dgu && dy) {
+                    memcpy(ex->dgu + q * 2 * g, dGq, sizeof(double) * (size_t)g);
+                    memcpy(ex->dgu + q * 2 * g + g, dUq, sizeof(double) * (size_t)g);
+                }
                 for (int64_t c = 0; c < h; c++) {
                     y[t * h + c] += w[q] * O[c];
                     if (dy) dx[t * h + c] += dxc[c];
@@ -1050,7 +1097,7 @@ int32_t oracle_moe_mx(const oracle_dims* d, int32_t mode, const void* dy, const 
     if (dy) {
         for (int64_t q = 0; q < nq; q++) order[q] = q;
         if (wgrad_C >= 1)
-            rc = accumulate_dw_mx(d, mode, wgrad_C, x, dy, ids, w, a_all, dG_all, dU_all, dwg, dwu, dwd);
+            rc = accumulate_dw_mx(d, mode, wgrad_C, x, dy, ids, w, a_all, dG_all, dU_all, fed, dwg, dwu, dwd);
         else
             accumulate_dw(d, x, ids, order, nq, a_all, dO_all, dG_all, dU_all, dwg, dwu, dwd);
         free(a_all); free(dG_all); free(dU_all); free(dO_all); free(order);
@@ -1061,10 +1108,12 @@ int32_t oracle_moe_mx(const oracle_dims* d, int32_t mode, const void* dy, const 
 /* MX layer on a token subset (full-size sampled parity): y, dx, dscore of tokens toks[0..ntok) exactly
  * as oracle_moe_mx computes them (the per-token terms do not depend on other tokens), with the
  * weights quantised one expert at a time (the five operand layouts of oracle_mx_weights), so the
- * dequantised copies of all experts never exist at once. */
+ * dequantised copies of all experts never exist at once.  fed / ex as in oracle_moe_mx, indexed by
+ * the sampled copy p*k + slot (a_q, dgu_q only; ex->a, ex->dgu). */
 int32_t oracle_moe_mx_tokens(const oracle_dims* d, int32_t mode, int64_t ntok, const int64_t* toks, const void* dy,
                              const void* x, const int32_t* ids, const double* w, const void* wg, const void* wu,
-                             const void* wd, double* y, double* dx, double* dscore)
+                             const void* wd, double* y, double* dx, double* dscore, const oracle_mx_fed* fed,
+                             const oracle_mx_exact* ex)
 {
     int64_t h = d->h, g = d->g, k = d->k;
     double* wqe[5];
@@ -1101,10 +1150,17 @@ int32_t oracle_moe_mx_tokens(const oracle_dims* d, int32_t mode, int64_t ntok, c
         for (int64_t i = 0; i < ntok; i++) {
             int64_t t = toks[i];
             for (int64_t sl = 0; sl < k; sl++) {
-                int64_t q = t * k + sl;
+                int64_t q = t * k + sl, p = i * k + sl;
                 if (ids[q] != e) continue;
                 expert_mx(d, mode, x, t * h, dy, t * h, w[q], wqe, 0, wd, e, scratch, O, a1, dO1, dG1, dU1, dxc,
-                          dy ? dscore + i * k + sl : NULL);
+                          dy ? dscore + p : NULL, fed && fed->a_q ? fed->a_q + p * g : NULL,
+                          fed && fed->dgu_q ? fed->dgu_q + p * 2 * g : NULL,
+                          ex && ex->gu ? ex->gu + p * 2 * g : NULL, ex && ex->da && dy ? ex->da + p * g : NULL);
+                if (ex && ex->a) memcpy(ex->a + p * g, a1, sizeof(double) * (size_t)g);
+                if (ex && ex->dgu && dy) {
+                    memcpy(ex->dgu + p * 2 * g, dG1, sizeof(double) * (size_t)g);
+                    memcpy(ex->dgu + p * 2 * g + g, dU1, sizeof(double) * (size_t)g);
+                }
                 for (int64_t c = 0; c < h; c++) {
                     y[i * h + c] += w[q] * O[c];
                     if (dy) dx[i * h + c] += dxc[c];

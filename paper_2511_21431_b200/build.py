@@ -62,7 +62,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
         list(ex.map(run, jobs))
     if jobs or force or _stale(LIB, objs):
         tmp = LIB + f".tmp{os.getpid()}"
-        run([nvcc()] + ARCH + ["-shared", "-o", tmp] + objs + ["-ldl", "-lcublas", "-Xlinker", "-rpath=" + os.path.join(os.path.dirname(os.path.dirname(nvcc())), "lib64")])
+        run([nvcc()] + ARCH + ["-shared", "-o", tmp] + objs + ["-ldl"])
         os.replace(tmp, LIB)
     return LIB
 

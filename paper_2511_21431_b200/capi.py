@@ -11,7 +11,7 @@ LIB_PATH = os.path.join(_PKG, "libmemfine.so")
 
 OK, ERR_INVALID_ARG, ERR_INFEASIBLE, ERR_ROUTING, ERR_CUDA, ERR_NCCL, ERR_WORKSPACE, ERR_UNSUPPORTED = range(8)
 BF16, FP32, MXFP8 = 0, 1, 2
-RULE_EQ9, RULE_EXACT = 0, 1
+RULE_EXACT, RULE_EQ9 = 0, 1      # memfine_budget.rule: EXACT is the default (0)
 MODEL_PAPER, MODEL_IMPL = 0, 1
 EP_COPY, EP_P2P = 0, 1
 FLAG_OVERLAP, FLAG_EP_PATH, FLAG_MX_WGRAD = 1, 2, 4
@@ -22,6 +22,7 @@ SYMBOLS = ("memfine_abi_version", "memfine_status_str", "memfine_nccl_unique_id"
            "memfine_destroy", "memfine_local_group_create", "memfine_local_group_destroy", "memfine_create_local", "memfine_set_ep_transport", "memfine_set_comm_sms", "memfine_register_workspace", "memfine_route_counts", "memfine_plan", "memfine_workspace_bytes", "memfine_a2a_plan",
            "memfine_moe_fwd", "memfine_moe_bwd", "memfine_router_fwd", "memfine_router_bwd", "memfine_sync", "memfine_last_stats",
            "memfine_profile_enable", "memfine_profile_read", "memfine_set_debug", "memfine_debug_perm",
+           "memfine_debug_rows", "memfine_debug_mx",
            "memfine_mx_weights_bytes", "memfine_mx_quantize_weights", "memfine_mx_quantize", "memfine_m_g")
 
 PROF_SLOTS = ("gemm_gateup_swiglu", "gemm_down", "gemm_dact_epilogue", "gemm_dx", "gemm_wgrad_down",
@@ -60,14 +61,16 @@ class PlanInfo(C.Structure):
 class Stats(C.Structure):
     _fields_ = [("C", C.c_int32), ("pass_", C.c_int32), ("rows", C.c_int64 * 64), ("rows_padded", C.c_int64 * 64),
                 ("workspace_used_bytes", C.c_uint64), ("workspace_given_bytes", C.c_uint64),
-                ("device_error", C.c_int32), ("gemm_launches", C.c_int32), ("kernel_launches", C.c_int32)]
+                ("device_error", C.c_int32), ("gemm_launches", C.c_int32), ("kernel_launches", C.c_int32),
+                ("comm_ops", C.c_int32)]
 
     def as_dict(self):
         n = self.C
         return {"C": n, "pass": self.pass_, "rows": list(self.rows[:n]), "rows_padded": list(self.rows_padded[:n]),
                 "workspace_used_bytes": self.workspace_used_bytes,
                 "workspace_given_bytes": self.workspace_given_bytes, "device_error": self.device_error,
-                "gemm_launches": self.gemm_launches, "kernel_launches": self.kernel_launches}
+                "gemm_launches": self.gemm_launches, "kernel_launches": self.kernel_launches,
+                "comm_ops": self.comm_ops}
 
 
 class Profile(C.Structure):
@@ -117,6 +120,8 @@ def lib():
         L.memfine_profile_read.argtypes = [vp, C.POINTER(Profile)]
         L.memfine_set_debug.argtypes = [vp, i32]
         L.memfine_debug_perm.argtypes = [vp, i32, vp, i64, C.POINTER(i64)]
+        L.memfine_debug_rows.argtypes = [vp, i32, vp, i64, C.POINTER(i64)]
+        L.memfine_debug_mx.argtypes = [vp, i32, i32, vp, vp, i64, C.POINTER(i64), C.POINTER(i64)]
         L.memfine_mx_weights_bytes.argtypes = [C.POINTER(Dims), C.POINTER(u64)]
         L.memfine_mx_quantize_weights.argtypes = [vp, vp, vp, vp, vp, u64, vp]
         L.memfine_mx_quantize.argtypes = [vp, i64, i32, vp, vp, vp]
@@ -137,7 +142,7 @@ def check(status: int, where: str) -> None:
 
 def make_budget(gpu_capacity_bytes: int, alpha: float = 1.0, static_bytes: int = 0, other_act_bytes: int = 0,
                 m_g: int = 1, tp: int = 1, cp: int = 1, micro_batch: int = 1, bins=(1, 2, 4, 8),
-                rule: int = RULE_EQ9, model: int = MODEL_PAPER, pass_: int = BWD):
+                rule: int = RULE_EXACT, model: int = MODEL_PAPER, pass_: int = BWD):
     arr = (C.c_int32 * len(bins))(*bins) if bins is not None else None
     b = Budget(int(gpu_capacity_bytes), float(alpha), int(static_bytes), int(other_act_bytes), m_g, tp, cp,
                micro_batch, C.cast(arr, C.POINTER(C.c_int32)) if arr is not None else None,

@@ -261,6 +261,14 @@ __device__ __forceinline__ void stage_bf16_row_packed(uint8_t* buf, int r, const
     *reinterpret_cast<uint4*>(row + ((c ^ ((r >> 1) & 3)) << 4)) =
         make_uint4(u[4 * c], u[4 * c + 1], u[4 * c + 2], u[4 * c + 3]);
 }
+// fp32, 16 columns: 32 rows x 64 B in the SWIZZLE_64B layout (the bf16 staging's row shape)
+__device__ __forceinline__ void stage_f32_row16(uint8_t* buf, int r, const float* v) {
+  uint8_t* row = buf + r * 64;
+#pragma unroll
+  for (int c = 0; c < 4; c++)
+    *reinterpret_cast<float4*>(row + ((c ^ ((r >> 1) & 3)) << 4)) =
+        make_float4(v[4 * c], v[4 * c + 1], v[4 * c + 2], v[4 * c + 3]);
+}
 __device__ __forceinline__ void stage_f32_row(uint8_t* buf, int r, const float* v) {
   uint8_t* row = buf + r * 128;
 #pragma unroll
@@ -396,6 +404,7 @@ struct Params {
   uint8_t* mx_gq;      // dA (BF16 GEMM) in the MX variant: dG||dU also quantised for the dX GEMM
   uint8_t* mx_gq_sf;
   int mx_split_n;
+  int out_f32;         // DOWN: fp32 output (the router's logits), 16-column TMA stores
 };
 
 struct Tile {
@@ -1026,13 +1035,28 @@ __global__ void __launch_bounds__(THREADS, 1)
           }
         } else if (KIND == GK_DOWN || KIND == GK_DX) {
           if (rows_ok && n < p.h) {
-            uint8_t* buf = next_buf();
-            stage_bf16_row(buf, lane, v);
-            fence_async_smem();
-            __syncwarp();
-            if (lane == 0) {
-              tma_store_2d(&tmO0, buf, n, row0);
-              bulk_commit();
+            if (KIND == GK_DOWN && p.out_f32) {
+              // fp32 output (the router's logits): two 16-column stores per 32-column chunk
+#pragma unroll
+              for (int h2 = 0; h2 < 2; h2++) {
+                uint8_t* buf = next_buf();
+                stage_f32_row16(buf, lane, v + 16 * h2);
+                fence_async_smem();
+                __syncwarp();
+                if (lane == 0) {
+                  tma_store_2d(&tmO0, buf, n + 16 * h2, row0);
+                  bulk_commit();
+                }
+              }
+            } else {
+              uint8_t* buf = next_buf();
+              stage_bf16_row(buf, lane, v);
+              fence_async_smem();
+              __syncwarp();
+              if (lane == 0) {
+                tma_store_2d(&tmO0, buf, n, row0);
+                bulk_commit();
+              }
             }
           }
         } else if (KIND == GK_DACT) {
@@ -1212,10 +1236,21 @@ bool map3d_f32(CUtensorMap* m, const void* base, uint64_t d0, uint64_t d1, uint6
   return make_map_t(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, CU_TENSOR_MAP_SWIZZLE_128B, base, 3, d, b);
 }
 
-bool map2d(CUtensorMap* m, const void* base, uint64_t inner, uint64_t outer, uint32_t box_in, uint32_t box_out) {
-  uint64_t d[2] = {inner, outer}, s[1] = {inner * 2};
+bool map2d(CUtensorMap* m, const void* base, uint64_t inner, uint64_t outer, uint32_t box_in, uint32_t box_out,
+           uint64_t ld = 0) {
+  uint64_t d[2] = {inner, outer}, s[1] = {(ld ? ld : inner) * 2};
   uint32_t b[2] = {box_in, box_out};
   return make_map(m, base, 2, d, s, b);
+}
+// fp32 [outer][ld] store map over the first `inner` columns, boxes of 16 x 32 (SWIZZLE_64B)
+bool map2d_st_f32(CUtensorMap* m, const void* base, uint64_t inner, uint64_t ld, uint64_t outer) {
+  auto fn = encode_fn();
+  if (!fn) return false;
+  cuuint64_t gd[2] = {inner, outer}, gs[1] = {ld * 4};
+  cuuint32_t bx[2] = {16, 32}, es[2] = {1, 1};
+  return fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<void*>(base), gd, gs, bx, es,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 bool map3d(CUtensorMap* m, const void* base, uint64_t d0, uint64_t d1, uint64_t d2, uint32_t b0, uint32_t b1) {
   uint64_t d[3] = {d0, d1, d2}, s[2] = {d0 * 2, d0 * d1 * 2};
@@ -1306,8 +1341,10 @@ int launch(const GemmProblem<__nv_bfloat16>& gp, cudaStream_t st) {
   p.row_addr = gp.row_addr;
   p.mx_gq = gp.mx_gq;
   p.mx_gq_sf = gp.mx_gq_sf;
+  p.out_f32 = gp.out_f32;
   const uint64_t R = (uint64_t)gp.rows_cap, h = gp.h, g = gp.g, El = gp.El;
   if (R == 0) return 0;
+  const uint64_t Rin = gp.rows_in > 0 ? (uint64_t)gp.rows_in : R;   // rows the operand maps hold
   CUtensorMap mA, mB0, mB1, mO0, mO1;
   bool ok = true;
   const uint32_t gu_rows = PAIR ? BN : BN;  // per-CTA B box rows for GATEUP (one of W_gate / W_up)
@@ -1322,10 +1359,11 @@ int launch(const GemmProblem<__nv_bfloat16>& gp, cudaStream_t st) {
       break;
     case GK_DOWN:
       p.N = gp.h; p.K = gp.g;
-      ok &= map2d(&mA, gp.A, g, R, BK, BM);
+      ok &= map2d(&mA, gp.A, g, Rin, BK, BM);
       ok &= map3d(&mB0, gp.Wd, g, h, El, BK, B_ROWS);
       mB1 = mB0;
-      ok &= map2d_st(&mO0, gp.O, h, R);
+      if (gp.out_f32) ok &= map2d_st_f32(&mO0, gp.O, h, gp.ld_out > 0 ? (uint64_t)gp.ld_out : h, Rin);
+      else ok &= map2d_st(&mO0, gp.O, h, R);
       mO1 = mO0;
       break;
     case GK_DACT:
@@ -1346,8 +1384,8 @@ int launch(const GemmProblem<__nv_bfloat16>& gp, cudaStream_t st) {
       break;
     case GK_WGRAD_DOWN:
       p.M = gp.h; p.N = gp.g;
-      ok &= map2d(&mA, gp.DY, h, R, 64, BK);        // A(m,k) = dY[s0+k][m]
-      ok &= map2d(&mB0, gp.A, g, R, 64, BK);        // B(n,k) = a_w[s0+k][n]
+      ok &= map2d(&mA, gp.DY, h, Rin, 64, BK, gp.ld_a > 0 ? (uint64_t)gp.ld_a : 0);   // A(m,k) = dY[s0+k][m]
+      ok &= map2d(&mB0, gp.A, g, Rin, 64, BK);      // B(n,k) = a_w[s0+k][n]
       mB1 = mB0;
       p.dW0 = gp.dWd;
       ok &= map3d_f32(&mO0, gp.dWd, g, h, El);

@@ -30,8 +30,10 @@ void launch_dispatch_hist(const int32_t* ids, int64_t t0, int64_t t1, int k, int
 // send_layout 0: EP=1 expert-major padded layout; 1: EP send layout (global expert order).
 void launch_dispatch_scan(int NB, int E, int El, int send_layout, int64_t rows_cap, const ChunkMeta& m,
                           int64_t* stats_rows, int64_t* stats_rows_pad, int chunk, cudaStream_t st);
+// gskip (nullable): per-chunk global skip flags (N1 device plan) OR-ed into the chunk's info word
 void launch_ep_recv_seg(const int* counts, int C, int j, int E, int El, int me, int EP, int64_t rows_cap,
-                        const ChunkMeta& m, int64_t* stats_rows, int64_t* stats_rows_pad, cudaStream_t st);
+                        const ChunkMeta& m, int64_t* stats_rows, int64_t* stats_rows_pad, cudaStream_t st,
+                        const int* gskip = nullptr);
 // Index pass (stable ranks) + row gather.  expert_major: EP=1 padded layout (padding rows zeroed,
 // rows_cap bounds the grid); otherwise the EP send layout.
 template <typename T>
@@ -81,6 +83,33 @@ void launch_p2p_row_addr(const int* seg, const int* recv_cnt, int El, int EP, co
 void launch_p2p_push_dw(const float* dw_row, const uint64_t* row_addr_w, const int* info, int64_t rows_cap,
                         cudaStream_t st);
 
+// ---------------------------------------------------------------- N1: device-planned exchange, no host sync
+// Every rank owns a small sync area (memfine_register_workspace), mapped by every peer:
+//   epoch (uint64, this rank's call counter) | flags[kSyncPhases][kMaxPeers] (uint64, written by peers) |
+//   counts[2][kMaxPeers][kMaxSub * E] (int32, the count all-gather landing zone, by call parity)
+// A flag value is epoch * 256 + code; waits spin (acquire, system scope) until every peer's flag reaches
+// the target, with a bounded spin (latched error, never a hang).
+constexpr int kSyncPhases = 4;   // 0 counts, 1 pushed(j), 2 combined(j), 3 done(j)
+constexpr int kSyncDoneCall = 255;
+struct SyncPeers {
+  uint64_t* area[kMaxPeers];     // every rank's sync area (own entry = local)
+  int n;
+};
+uint64_t sync_area_bytes(int E);
+// epoch += 1 (one thread; the first kernel of every device-planned call)
+void launch_sync_epoch(uint64_t* area, cudaStream_t st);
+// this rank's counts [C][E] -> every peer's counts slot (call parity), then flag phase 0 = epoch*256
+void launch_sync_push_counts(const int* mine, int C, int E, const SyncPeers& sp, int me, cudaStream_t st);
+// flag `phase` of this rank in every peer's area := epoch * 256 + code (after a system-scope fence)
+void launch_sync_signal(const SyncPeers& sp, int me, int phase, int code, cudaStream_t st);
+// wait until every peer's flag `phase` in the local area >= epoch * 256 + code (code may be negative)
+void launch_sync_wait(uint64_t* area, int EP, int me, int phase, int code, int* status, cudaStream_t st);
+// the landed counts of this call [EP][C][E] -> counts_all; then, per chunk j, the fused-exchange table
+// (see PeerTable's comment) into p2p_tab + j (4E+1), and gskip[j] = 1 if ANY rank's padded rows exceed
+// rows_cap or its send rows exceed send_cap (identical on every rank: the same counts)
+void launch_p2p_tables(const uint64_t* area, int C, int E, int El, int EP, int me, int64_t rows_cap,
+                       int64_t send_cap, int* counts_all, int* p2p_tab, int* gskip, int* status, cudaStream_t st);
+
 // ---------------------------------------------------------------- router (N3)
 template <typename T>
 void launch_router_fwd(const T* x, const T* wr, int64_t ntok, int E, int h, int k, float* logits, int32_t* ids,
@@ -90,14 +119,13 @@ template <typename T>
 void launch_router_bwd(const T* x, const T* wr, const int32_t* ids, const float* scores, const float* dscore,
                        int64_t ntok, int E, int h, int k, float* dlog, T* dx, int acc_dx, float* dwr, int acc_dw,
                        const ChunkMeta& m, cudaStream_t st);
-// bf16: logits and dW_r as cuBLAS GEMMs (cublas = a cublasHandle_t); nonzero return = a cuBLAS failure.
-// dhi/dlo: [T][E] bf16 scratch for the dense d_logits (hi + lo).
-int launch_router_fwd_bf16(void* cublas, const __nv_bfloat16* x, const __nv_bfloat16* wr, int64_t ntok, int E,
-                           int h, int k, float* logits, int32_t* ids, float* scores, cudaStream_t st);
-int launch_router_bwd_bf16(void* cublas, const __nv_bfloat16* x, const __nv_bfloat16* wr, const int32_t* ids,
-                           const float* scores, const float* dscore, int64_t ntok, int E, int h, int k, float* dlog,
-                           __nv_bfloat16* dhi, __nv_bfloat16* dlo, __nv_bfloat16* dx, int acc_dx, float* dwr,
-                           int acc_dw, cudaStream_t st);
+// bf16: the logits GEMM (x W_r^T, fp32 out) and the dW_r GEMMs (d_logits^T x over the hi and lo halves) run
+// on the expert-GEMM kernels (GK_DOWN with out_f32, GK_WGRAD_DOWN); these are the row kernels around them.
+void launch_router_topk(const float* logits, int64_t ld, int64_t ntok, int E, int k, int32_t* ids, float* scores,
+                        float* out, cudaStream_t st);
+void launch_router_bwd_rows_bf16(const __nv_bfloat16* wr, const int32_t* ids, const float* scores, const float* dscore,
+                                 int64_t ntok, int E, int h, int k, float* dlog, __nv_bfloat16* dhi,
+                                 __nv_bfloat16* dlo, int ldd, __nv_bfloat16* dx, int acc_dx, cudaStream_t st);
 
 // ---------------------------------------------------------------- MACT tuner (A3)
 struct PlanParams {
@@ -165,6 +193,13 @@ struct GemmProblem {
   uint8_t* mx_gq_sf;         // ... with scales (non-null = on)
   int sm_limit;              // > 0: launch on at most this many SMs (MEMFINE_FLAG_OVERLAP comm reserve)
   int pace;                  // 1: no other kernel shares the SMs (EP = 1, one stream): wave pacing is safe
+  // the router's GEMMs on the same kernels (N3): logits = x W_r^T as a DOWN launch storing fp32, and
+  // dW_r = d_logits^T x as a WGRAD_DOWN launch (0 = off / defaults)
+  int out_f32;               // DOWN: O is fp32 [rows][ld_out] (columns >= h clipped)
+  int64_t ld_out;            // DOWN out_f32: O's row stride in elements (default h)
+  int64_t ld_a;              // WGRAD_DOWN: DY's row stride in elements (default h)
+  int64_t rows_in;           // rows present in the row-major operands (TMA zero-fills rows up to the
+                             // 128-padded K / M loops; default rows_cap)
 };
 
 // CUDA-core FFMA path (MEMFINE_FP32 mode; K12 of SURVEY §2.4).

@@ -1,6 +1,5 @@
 // memfine.cu — the C ABI of libmemfine.so: handle, MACT plan, workspace carving and the
 // FCDA chunk loops (Eq. 6 forward, Eq. 7 recompute backward).
-#include <cublas_v2.h>
 #include <nvtx3/nvToolsExt.h>
 #include <cstdio>
 #include <cstdlib>
@@ -29,7 +28,7 @@ struct memfine_group_s {
   int arrived = 0, gen = 0;
   std::vector<cudaEvent_t> ready, done;
   std::vector<std::array<char*, 20>> ptrs;  // per rank: buffers of the current call ([slot*8 + kind];
-                                            // kPtrWs: workspace)
+                                            // kPtrWs: workspace, kPtrSync: P2P sync area)
   void barrier() {
     std::unique_lock<std::mutex> lk(m);
     int g = gen;
@@ -43,25 +42,28 @@ struct memfine_group_s {
   }
 };
 
+struct memfine_handle_s;
+memfine_status register_local(memfine_handle_s* h, void* ws, uint64_t ws_bytes);
+
 struct memfine_handle_s {
   memfine_dims d;
   memfine_group_s* lg = nullptr;   // in-process EP group (instead of NCCL)
   int p2p = 0;                     // fused exchange over peer memory (MEMFINE_EP_P2P)
-  int fence_ctr = 0;
-  int* tab_h = nullptr;            // pinned staging of the per-chunk P2P tables
-  size_t tab_cap = 0;
-  // multi-process P2P: every rank's registered workspace, mapped here with CUDA IPC
+  // P2P (N1, device-planned): the registered workspace and sync area of every rank (own entries local;
+  // in-process peers directly, other processes through CUDA IPC), the all-gathered counts and the
+  // per-chunk global skip flags
   void* reg_ws = nullptr;
   uint64_t reg_bytes = 0;
   std::vector<char*> peer_ws;      // [EP] (own entry = reg_ws)
+  std::vector<uint64_t*> peer_sync;// [EP] (own entry = sync_d)
+  uint64_t* sync_d = nullptr;      // this rank's sync area (sync_area_bytes)
+  int* gskip_d = nullptr;          // [kMaxSub]
   std::vector<void*> ipc_bases;    // opened peer allocation bases (to close)
-  int* barrier_d = nullptr;
   // MXFP8: the bound quantised weights (memfine_mx_quantize_weights)
   const uint8_t* mx_w = nullptr;
   // router scratch (lazily allocated): logits, d_logits, counting sort of ids by expert
   char* router_scratch = nullptr;
   size_t router_bytes = 0;
-  void* cublas = nullptr;          // cublasHandle_t for the bf16 router GEMMs (created on first use)
   int device = 0;
   int num_sms = 148;
   int* status_h = nullptr;     // pinned, mapped: device-latched error word
@@ -72,6 +74,11 @@ struct memfine_handle_s {
   uint64_t last_meta = 0, last_row_bytes = 0;
   int debug = 0;
   std::vector<std::vector<int64_t>> debug_perm;
+  // debug (EP = 1): per chunk of the last call, the expert-major rows' copy indices and the MXFP8
+  // decisions (codes + scale chunks) of the operands the kernels quantise (memfine_debug_mx)
+  struct DbgMx { std::vector<uint8_t> q, sf; int64_t rows = 0, cols = 0; };
+  std::vector<std::array<DbgMx, 6>> dbg_mx;
+  std::vector<std::vector<int32_t>> dbg_src;
   // expert parallel
   NcclComm comm{};
   int* counts_d = nullptr;     // [EP][C][E] all-gathered chunk counts (device)
@@ -190,6 +197,7 @@ struct Layout {
   uint8_t *DYt = nullptr, *DYtsf = nullptr, *GUt = nullptr, *GUtsf = nullptr, *At = nullptr, *Atsf = nullptr;
   int64_t rows_cap = 0;
   uint64_t meta_bytes = 0, row_bytes = 0, total = 0;
+  bool o_alias = false;   // O is carved over X (by layout, not by address: zero-row arrays share one)
 };
 
 // MEMFINE_FLAG_OVERLAP: two slots of the exchanged rows (chunk j+1 lands while chunk j computes).
@@ -266,6 +274,7 @@ Layout carve(const memfine_dims& d, int C, int pass, void* ws, int64_t rows_cap,
       }
       L.X = b.take<char>((uint64_t)R * d.hidden * D);
       L.O = L.X;
+      L.o_alias = true;
     }
     void* GU = pass == MEMFINE_BWD ? b.take<char>((uint64_t)R * 2 * d.ffn * D) : nullptr;
     void* A = b.take<char>((uint64_t)R * d.ffn * D);
@@ -305,9 +314,11 @@ Layout carve(const memfine_dims& d, int C, int pass, void* ws, int64_t rows_cap,
           L.Atsf = b.take<uint8_t>((uint64_t)R * gg / 32);
         }
         L.O = L.X;
+        L.o_alias = true;
       } else {
         L.Aq = b.take<uint8_t>((uint64_t)R * gg);
         L.Asf = b.take<uint8_t>((uint64_t)R * gg / 32);
+        L.o_alias = ep_path(d);
         L.O = ep_path(d) ? L.X : b.take<char>((uint64_t)R * hh * D);
       }
     } else if (pass == MEMFINE_BWD) {
@@ -315,6 +326,7 @@ Layout carve(const memfine_dims& d, int C, int pass, void* ws, int64_t rows_cap,
       L.GU = b.take<char>((uint64_t)R * 2 * d.ffn * D);
       L.A = b.take<char>((uint64_t)R * d.ffn * D);
       L.O = L.X;
+      L.o_alias = true;
     } else {
       L.A = b.take<char>((uint64_t)R * d.ffn * D);
       L.O = b.take<char>((uint64_t)R * d.hidden * D);
@@ -541,6 +553,32 @@ int run_wgrad(memfine_handle_s* h, GemmProblem<T>& p, const Layout& L, cudaStrea
   return run_gemm<T>(h, p, st);
 }
 
+// ------------------------------------------------------------------ debug capture (EP = 1)
+// Synchronises and copies device state to the host; only with memfine_set_debug(1).
+void dbg_rows(memfine_handle_s* h, int j, const int* src_of, cudaStream_t st) {
+  cudaStreamSynchronize(st);
+  if ((int)h->dbg_src.size() <= j) h->dbg_src.resize(j + 1);
+  const int64_t rp = h->rows_h[kMaxSub + j];
+  h->dbg_src[j].assign(rp > 0 ? rp : 0, -1);
+  if (rp > 0) cudaMemcpy(h->dbg_src[j].data(), src_of, sizeof(int) * rp, cudaMemcpyDeviceToHost);
+}
+// which: 0 a [rows_pad][g], 1 dG||dU [rows_pad][2g] (rowwise); 2 x, 3 dY [h][Rcap], 4 dG||dU [2g][Rcap],
+// 5 a_w [g][Rcap] (columnwise, reading R28c).  Scales in the tcgen05 chunk layout with K = cols.
+void dbg_mx(memfine_handle_s* h, int j, int which, const uint8_t* q, const uint8_t* sf, int64_t rows, int64_t cols,
+            cudaStream_t st) {
+  cudaStreamSynchronize(st);
+  if ((int)h->dbg_mx.size() <= j) h->dbg_mx.resize(j + 1);
+  auto& D = h->dbg_mx[j][which];
+  D.rows = rows;
+  D.cols = cols;
+  D.q.assign((size_t)(rows * cols), 0);
+  D.sf.assign((size_t)(rows * cols / 32), 0);
+  if (rows * cols > 0) {
+    cudaMemcpy(D.q.data(), q, D.q.size(), cudaMemcpyDeviceToHost);
+    cudaMemcpy(D.sf.data(), sf, D.sf.size(), cudaMemcpyDeviceToHost);
+  }
+}
+
 // ------------------------------------------------------------------ the FCDA chunk loops (EP = 1)
 template <typename T>
 memfine_status fwd_ep1(memfine_handle_s* h, const T* x, const int32_t* ids, const float* w, const void* wg,
@@ -587,6 +625,10 @@ memfine_status fwd_ep1(memfine_handle_s* h, const T* x, const int32_t* ids, cons
         p.mx_aq_sf = L.Asf;
       }
     if (int rc = run_gemm<T>(h, p, st)) return (memfine_status)rc;
+    if (h->debug) {
+      dbg_rows(h, j, L.m.src_of, st);
+      if (mx) dbg_mx(h, j, 0, L.Aq, L.Asf, h->rows_h[kMaxSub + j], d.ffn, st);
+    }
     p.kind = GK_DOWN;
     if constexpr (std::is_same<T, __nv_bfloat16>::value)
       if (mx) set_mx(p, {L.Aq, L.Asf}, W.op[2], W.op[2]);
@@ -660,10 +702,20 @@ memfine_status bwd_ep1(memfine_handle_s* h, const T* dy, const T* x, const int32
     if (int rc = run_gemm<T>(h, p, st)) return (memfine_status)rc;
     p.mx_gq = nullptr;
     p.mx_gq_sf = nullptr;
+    if (h->debug) {
+      dbg_rows(h, j, L.m.src_of, st);
+      if (mx) dbg_mx(h, j, 1, L.GUq, L.GUsf, h->rows_h[kMaxSub + j], 2 * (int64_t)g, st);
+    }
     // B5: weight gradients accumulate across chunks (reading R18)
     p.wgrad_beta = beta;
     if (int rc = run_wgrad<T>(h, p, L, st)) return (memfine_status)rc;
     beta = 1;
+    if (h->debug && mx && (d.flags & MEMFINE_FLAG_MX_WGRAD)) {
+      dbg_mx(h, j, 2, L.Xq, L.Xsf, hd, L.rows_cap, st);
+      dbg_mx(h, j, 3, L.DYt, L.DYtsf, hd, L.rows_cap, st);
+      dbg_mx(h, j, 4, L.GUt, L.GUtsf, 2 * (int64_t)g, L.rows_cap, st);
+      dbg_mx(h, j, 5, L.At, L.Atsf, g, L.rows_cap, st);
+    }
     // B4: dX_disp = dG W_gate + dU W_up (overwrites X_disp, dead after B5)
     p.kind = GK_DX;
     if constexpr (std::is_same<T, __nv_bfloat16>::value)
@@ -716,7 +768,7 @@ EpChunk ep_chunk_table(const memfine_dims& d, const int* counts, int C, int j) {
 
 // ---- in-process group transport
 enum { kPtrSend = 0, kPtrSendDy = 1, kPtrSendW = 2, kPtrX = 3, kPtrDY = 4, kPtrO = 5, kPtrWRow = 6, kPtrDWRow = 7,
-       kPtrWs = 16 };
+       kPtrWs = 16, kPtrSync = 17, kPtrWsBytes = 18 };
 
 // all ranks' device work before this point is visible to every rank's stream after it
 void local_fence(memfine_handle_s* h, cudaStream_t st, std::vector<cudaEvent_t>& evs) {
@@ -752,6 +804,7 @@ int local_exchange(memfine_handle_s* h, const int* counts, int C, int j, bool fo
         char* src = g->ptrs[p][kind_send] + s0 * row_bytes;
         char* dst = g->ptrs[me][kind_expert] + mine.recv_off[(size_t)p * El + el] * row_bytes;
         if (cudaMemcpyAsync(dst, src, n * row_bytes, cudaMemcpyDeviceToDevice, st)) return 1;
+        h->last.comm_ops++;
       } else {
         // rows p computed for my copies of its expert (p, el) -> my send layout
         int eg = p * El + el;
@@ -760,6 +813,7 @@ int local_exchange(memfine_handle_s* h, const int* counts, int C, int j, bool fo
         char* src = g->ptrs[p][kind_expert] + theirs.recv_off[(size_t)me * El + el] * row_bytes;
         char* dst = g->ptrs[me][kind_send] + s0 * row_bytes;
         if (cudaMemcpyAsync(dst, src, n * row_bytes, cudaMemcpyDeviceToDevice, st)) return 1;
+        h->last.comm_ops++;
       }
     }
   }
@@ -792,6 +846,7 @@ int ep_exchange(memfine_handle_s* h, const EpChunk& t, const int* counts, int C,
           char* b = expert_buf + r0 * row_bytes;
           if (cudaMemcpyAsync(forward ? b : a, forward ? a : b, sn * row_bytes, cudaMemcpyDeviceToDevice, st))
             rc = 1;
+          h->last.comm_ops++;
         }
         continue;
       }
@@ -802,6 +857,7 @@ int ep_exchange(memfine_handle_s* h, const EpChunk& t, const int* counts, int C,
         if (rn) rc |= nccl_send(&h->comm, expert_buf + r0 * row_bytes, rn * row_bytes, 0, peer, st);
         if (sn) rc |= nccl_recv(&h->comm, send_buf + s0 * row_bytes, sn * row_bytes, 0, peer, st);
       }
+      h->last.comm_ops += (sn ? 1 : 0) + (rn ? 1 : 0);
     }
   }
   (void)counts; (void)C; (void)j;
@@ -844,19 +900,17 @@ int ep_gather_counts(memfine_handle_s* h, const int32_t* ids, int C, cudaStream_
   return MEMFINE_OK;
 }
 
-// Alternating event sets so consecutive fences never re-record an event a peer may still wait on.
-void p2p_fence(memfine_handle_s* h, cudaStream_t st) {
-  if (h->lg) {
-    local_fence(h, st, (h->fence_ctr++ & 1) ? h->lg->done : h->lg->ready);
-  } else {
-    // an all-reduce completes on every rank only after every rank's prior stream work
-    nccl_stream_barrier(&h->comm, h->barrier_d, st);
-  }
-}
-
-// EP with the exchange fused into the kernels over peer memory: the permute
-// pushes each token row straight into the receiver's expert-major buffer, and the down / dX GEMM
-// epilogues store each output row straight into its source rank's send buffer, tile by tile.
+// EP with the exchange fused into the kernels over peer memory, planned on the device:
+// the count all-gather ("the first notification") is a push into every peer's sync area, the
+// per-chunk tables and the capacity check come from a device kernel, and ranks fence with per-peer flags
+// (epoch-stamped, spin-waited on the device) - the host never waits, so a call is graph-capturable.  The
+// workspace layout does not depend on the counts: rows_cap follows from ws_bytes (as at EP = 1) and the send
+// staging holds the chunk's T_j k copies, so every rank derives every peer's buffer addresses from the
+// registered workspaces (all ranks register the same ws_bytes).  Per chunk j:
+//   wait done(j-1) of every peer -> push rows into the receivers' expert-major buffers -> signal pushed(j),
+//   wait pushed(j) -> GEMMs, whose down / dX epilogues store each output row into its source's send buffer
+//   -> signal combined(j), wait combined(j) -> combine / unpermute -> signal done(j).
+// A rank pushes chunk j+1 as soon as its receivers are done with chunk j, while it may still compute.
 template <typename T>
 memfine_status ep_run_p2p(memfine_handle_s* h, int pass, const T* dy, const T* x, const int32_t* ids, const float* w,
                           const void* wg, const void* wu, const void* wd, int C, T* out, float* dwg, float* dwu,
@@ -867,71 +921,49 @@ memfine_status ep_run_p2p(memfine_handle_s* h, int pass, const T* dy, const T* x
   const bool mx = d.dtype == MEMFINE_MXFP8;
   if (mx && !h->mx_w) return MEMFINE_ERR_INVALID_ARG;   // memfine_mx_quantize_weights first
   MxWeightsLayout W = mx_weights_layout(d, h->mx_w);
-  if (int rc = ep_gather_counts(h, ids, C, st)) return (memfine_status)rc;
-  // every rank's chunk tables and workspace layout, from the shared counts
-  std::vector<std::vector<EpChunk>> tabs(EP);
-  std::vector<int64_t> rows_max(EP, 0), send_max(EP, 0);
-  for (int r = 0; r < EP; r++) {
-    memfine_dims dr = d;
-    dr.ep_rank = r;
-    for (int j = 0; j < C; j++) {
-      tabs[r].push_back(ep_chunk_table(dr, h->counts_h, C, j));
-      rows_max[r] = std::max(rows_max[r], tabs[r][j].rows_pad);
-      send_max[r] = std::max(send_max[r], tabs[r][j].send);
-    }
+  if (ws != h->reg_ws || ws_bytes != h->reg_bytes || (int)h->peer_ws.size() != EP) {
+    // in-process groups register on first use (every rank's call reaches the same point); across
+    // processes memfine_register_workspace(ws, ws_bytes) must come first, on every rank
+    if (!h->lg) return MEMFINE_ERR_INVALID_ARG;
+    if (memfine_status rc = register_local(h, ws, ws_bytes)) return rc;
   }
-  Layout L = carve(d, C, pass, ws, rows_max[me], send_max[me]);
-  if (L.total > ws_bytes) return MEMFINE_ERR_WORKSPACE;
+  const int64_t S = tmax_chunk(d, C) * k;
+  const int64_t R = rows_fitting(d, C, pass, ws_bytes, S);
+  if (R <= 0) return MEMFINE_ERR_WORKSPACE;
+  Layout L = carve(d, C, pass, ws, R, S);
   h->last_meta = L.meta_bytes;
   h->last_row_bytes = L.row_bytes;
-  if (h->lg) {
-    h->lg->ptrs[me][kPtrWs] = (char*)ws;
-    h->lg->barrier();  // every rank published its workspace
-  } else if (ws != h->reg_ws || (int)h->peer_ws.size() != EP) {
-    return MEMFINE_ERR_INVALID_ARG;  // P2P across processes needs memfine_register_workspace(ws) first
-  }
   PeerTable pt{};
   pt.n = EP;
+  SyncPeers sp{};
+  sp.n = EP;
   for (int r = 0; r < EP; r++) {
     memfine_dims dr = d;
     dr.ep_rank = r;
-    char* base_r = h->lg ? h->lg->ptrs[r][kPtrWs] : h->peer_ws[r];
-    Layout Lr = carve(dr, C, pass, base_r, rows_max[r], send_max[r]);
+    Layout Lr = carve(dr, C, pass, h->peer_ws[r], R, S);   // the same offsets in every rank's workspace
     pt.X[r] = (char*)Lr.X;
     pt.DY[r] = (char*)Lr.DY;
     pt.w_row[r] = (char*)Lr.m.w_row;
     pt.send[r] = (char*)Lr.send;
     pt.send_w[r] = pass == MEMFINE_BWD ? (char*)Lr.send_w : nullptr;
+    sp.area[r] = h->peer_sync[r];
   }
-  // per-chunk tables -> device (one H2D from pinned staging; the call already synchronised once)
-  const size_t per = 4 * (size_t)E + 1;
-  if (h->tab_cap < per * C) {
-    if (h->tab_h) cudaFreeHost(h->tab_h);
-    h->tab_h = nullptr;
-    h->tab_cap = 0;
-    MF_CUDA_OK(cudaHostAlloc((void**)&h->tab_h, sizeof(int) * per * C, cudaHostAllocDefault));
-    h->tab_cap = per * C;
-  }
-  for (int j = 0; j < C; j++) {
-    int* tj = h->tab_h + per * j;
-    for (int e = 0; e <= E; e++) tj[e] = (int)tabs[me][j].send_off[e];
-    int* land = tj + E + 1;
-    int* roff = land + EP * El;
-    int* ret = roff + EP * El;
-    for (int p = 0; p < EP; p++)
-      for (int el = 0; el < El; el++) {
-        land[p * El + el] = (int)tabs[p][j].recv_off[(size_t)me * El + el];
-        roff[p * El + el] = (int)tabs[me][j].recv_off[(size_t)p * El + el];
-        ret[p * El + el] = (int)tabs[p][j].send_off[me * El + el];
-      }
-  }
-  MF_CUDA_OK(cudaMemcpyAsync(L.m.p2p_tab, h->tab_h, sizeof(int) * per * C, cudaMemcpyHostToDevice, st));
+  uint64_t* area = h->sync_d;
+  // A1 + A2 on the device: this rank's per-chunk counts, pushed into every peer's landing zone
+  launch_sync_epoch(area, st);
+  int* mine = h->counts_d + (int64_t)me * C * E;
+  launch_route_hist(ids, d.tokens, k, E, C, mine, h->status_d, st);
+  launch_sync_push_counts(mine, C, E, sp, me, st);
+  launch_sync_wait(area, EP, me, 0, 0, h->status_d, st);
+  // A3's per-chunk split and offset tables, and the capacity check, from the landed counts
+  launch_p2p_tables(area, C, E, El, EP, me, R, S, h->counts_d, L.m.p2p_tab, h->gskip_d, h->status_d, st);
+  h->last.kernel_launches += 6;
   int beta = accumulate ? 1 : 0;
   if (pass == MEMFINE_BWD && dscore && d.tokens > 0)
     MF_CUDA_OK(cudaMemsetAsync(dscore, 0, sizeof(float) * d.tokens * k, st));
   const int rb = hd * (int)sizeof(T);
+  const size_t per = 4 * (size_t)E + 1;
   for (int j = 0; j < C; j++) {
-    const EpChunk& t = tabs[me][j];
     const int* tab_j = L.m.p2p_tab + per * j;
     int64_t t0 = chunk_begin(d.tokens, C, j), t1 = chunk_begin(d.tokens, C, j + 1);
     int NB = (int)ceil_div64(t1 - t0, kTokPerBlk);
@@ -941,19 +973,22 @@ memfine_status ep_run_p2p(memfine_handle_s* h, int pass, const T* dy, const T* x
       launch_dispatch_index(ids, w, t0, t1, k, E, L.m, L.m.send_src, nullptr, st);
       h->last.kernel_launches += 3;
     }
-    launch_ep_recv_seg(h->counts_d, C, j, E, El, me, EP, L.rows_cap, L.m, h->rows_d, h->rows_d + kMaxSub, st);
+    launch_ep_recv_seg(h->counts_d, C, j, E, El, me, EP, L.rows_cap, L.m, h->rows_d, h->rows_d + kMaxSub, st,
+                       h->gskip_d);
     prof_begin(h, 9, st);
-    p2p_fence(h, st);  // (A) every rank is done with its buffers of the previous chunk
+    // every peer is done with its buffers of the previous chunk (or of the previous call)
+    launch_sync_wait(area, EP, me, 3, j == 0 ? -1 : j, h->status_d, st);
     if (NB)
       launch_p2p_push<T>(x, pass == MEMFINE_BWD ? dy : nullptr, w, k, hd, E, El, EP, tab_j, L.m.send_src, L.m.info,
-                         pt, t.send, st);
-    p2p_fence(h, st);  // (B) every row pushed into this rank has landed
+                         pt, (t1 - t0) * k, st);
+    launch_sync_signal(sp, me, 1, j + 1, st);
+    launch_sync_wait(area, EP, me, 1, j + 1, h->status_d, st);   // every row pushed into this rank landed
     prof_end(h, st);
     launch_zero_padding<T>(El, hd, L.m, (T*)L.X, pass == MEMFINE_BWD ? (T*)L.DY : nullptr, st);
-    if (pass == MEMFINE_BWD && t.rows_pad) MF_CUDA_OK(cudaMemsetAsync(L.m.dw_row, 0, sizeof(float) * t.rows_pad, st));
+    if (pass == MEMFINE_BWD) MF_CUDA_OK(cudaMemsetAsync(L.m.dw_row, 0, sizeof(float) * L.rows_cap, st));
     launch_p2p_row_addr(L.m.seg, L.m.recv_cnt, El, EP, tab_j, E, L.m.info, pt, rb, L.m.row_addr,
                         pass == MEMFINE_BWD ? L.m.row_addr_w : nullptr, L.rows_cap, st);
-    h->last.kernel_launches += 3;
+    h->last.kernel_launches += 6;
     GemmProblem<T> p = base_problem<T>(h, L, wg, wu, wd);
     p.dWg = dwg;
     p.dWu = dwu;
@@ -978,7 +1013,8 @@ memfine_status ep_run_p2p(memfine_handle_s* h, int pass, const T* dy, const T* x
       if constexpr (std::is_same<T, __nv_bfloat16>::value)
         if (mx) set_mx(p, {L.Aq, L.Asf}, W.op[2], W.op[2]);
       if (int rc = run_gemm<T>(h, p, st)) return (memfine_status)rc;
-      p2p_fence(h, st);  // (C) every o row for this rank's tokens has landed
+      launch_sync_signal(sp, me, 2, j + 1, st);
+      launch_sync_wait(area, EP, me, 2, j + 1, h->status_d, st);   // every o row of this rank's tokens landed
       if (t1 > t0) launch_combine<T>((const T*)L.send, w, t0, t1, k, hd, L.m, out, st);
     } else {
       p.kind = GK_GATEUP;
@@ -1005,15 +1041,20 @@ memfine_status ep_run_p2p(memfine_handle_s* h, int pass, const T* dy, const T* x
         if (mx) set_mx(p, {L.GUq, L.GUsf}, W.op[3], W.op[4]);
       if (int rc = run_gemm<T>(h, p, st)) return (memfine_status)rc;
       launch_p2p_push_dw(L.m.dw_row, L.m.row_addr_w, L.m.info, L.rows_cap, st);
-      p2p_fence(h, st);  // (C)
+      launch_sync_signal(sp, me, 2, j + 1, st);
+      launch_sync_wait(area, EP, me, 2, j + 1, h->status_d, st);   // every dX row and d_w landed
       ChunkMeta mb = L.m;
       mb.dw_row = L.send_w;
       if (t1 > t0) launch_unpermute_reduce<T>((const T*)L.send, t0, t1, k, hd, mb, out, dscore, st);
     }
-    h->last.kernel_launches += 2;
+    // this rank's buffers of chunk j are free for the peers' pushes / stores of chunk j+1 (or the next call)
+    launch_sync_signal(sp, me, 3, j + 1 == C ? kSyncDoneCall : j + 1, st);
+    h->last.kernel_launches += 5;
   }
   return latch_cuda(h);
 }
+
+
 
 // The comm stream of MEMFINE_FLAG_OVERLAP (created on first use, highest priority).
 int ensure_comm_stream(memfine_handle_s* h) {
@@ -1071,7 +1112,7 @@ memfine_status ep_run(memfine_handle_s* h, int pass, const T* dy, const T* x, co
       Q[kPtrSendW] = (char*)L.send_w;
       Q[kPtrX] = (char*)L.X;
       Q[kPtrDY] = (char*)L.DY;
-      Q[kPtrO] = L.O == L.X ? nullptr : (char*)L.O;  // O aliases X in the backward and with two slots
+      Q[kPtrO] = L.o_alias ? nullptr : (char*)L.O;  // O aliases X in the backward and with two slots
       Q[kPtrWRow] = (char*)L.m.w_row;
       Q[kPtrDWRow] = (char*)L.m.dw_row;
     }
@@ -1110,15 +1151,19 @@ memfine_status ep_run(memfine_handle_s* h, int pass, const T* dy, const T* x, co
                        h->rows_d + kMaxSub, cs);
     prof_begin(h, 9, cs);
     const int ko = 8 * (j % S);   // this slot's kinds in the in-process pointer table
-    if (ep_exchange(h, t, h->counts_h, C, j, true, (char*)L.send, (char*)L.X, rb, cs, ko + kPtrSend, ko + kPtrX))
-      return MEMFINE_ERR_NCCL;
+    // B1: x, dY and the scores of the chunk move in ONE NCCL group (one fused launch per chunk)
+    const bool grp = pass == MEMFINE_BWD && !h->lg;
+    if (grp && nccl_group_start()) return MEMFINE_ERR_NCCL;
+    int erc = ep_exchange(h, t, h->counts_h, C, j, true, (char*)L.send, (char*)L.X, rb, cs, ko + kPtrSend, ko + kPtrX);
     if (pass == MEMFINE_BWD) {
-      if (ep_exchange(h, t, h->counts_h, C, j, true, (char*)L.send_dy, (char*)L.DY, rb, cs, ko + kPtrSendDy,
-                      ko + kPtrDY))
-        return MEMFINE_ERR_NCCL;
-      if (ep_exchange(h, t, h->counts_h, C, j, true, (char*)L.send_w, (char*)L.m.w_row, 4, cs, ko + kPtrSendW,
-                      ko + kPtrWRow))
-        return MEMFINE_ERR_NCCL;
+      erc |= ep_exchange(h, t, h->counts_h, C, j, true, (char*)L.send_dy, (char*)L.DY, rb, cs, ko + kPtrSendDy,
+                         ko + kPtrDY);
+      erc |= ep_exchange(h, t, h->counts_h, C, j, true, (char*)L.send_w, (char*)L.m.w_row, 4, cs, ko + kPtrSendW,
+                         ko + kPtrWRow);
+    }
+    if (grp && nccl_group_end()) return MEMFINE_ERR_NCCL;
+    if (erc) return MEMFINE_ERR_NCCL;
+    if (pass == MEMFINE_BWD) {
       if (t.rows_pad) MF_CUDA_OK(cudaMemsetAsync(L.m.dw_row, 0, sizeof(float) * t.rows_pad, cs));
     }
     prof_end(h, cs);
@@ -1134,15 +1179,19 @@ memfine_status ep_run(memfine_handle_s* h, int pass, const T* dy, const T* x, co
     int64_t t0 = chunk_begin(d.tokens, C, j), t1 = chunk_begin(d.tokens, C, j + 1);
     if (S == 2) MF_CUDA_OK(cudaStreamWaitEvent(cs, h->ev_gemm[j % 2], 0));
     const int ko = 8 * (j % S);
-    if (ep_exchange(h, t, h->counts_h, C, j, false, (char*)L.send, (char*)L.O, rb, cs, ko + kPtrSend,
-                    ko + (L.O == L.X ? kPtrX : kPtrO)))
-      return MEMFINE_ERR_NCCL;
+    // B6: dX rows and d_score of the chunk in ONE NCCL group
+    const bool grp = pass == MEMFINE_BWD && !h->lg;
+    if (grp && nccl_group_start()) return MEMFINE_ERR_NCCL;
+    int erc = ep_exchange(h, t, h->counts_h, C, j, false, (char*)L.send, (char*)L.O, rb, cs, ko + kPtrSend,
+                          ko + (L.o_alias ? kPtrX : kPtrO));
+    if (pass == MEMFINE_BWD)
+      erc |= ep_exchange(h, t, h->counts_h, C, j, false, (char*)L.send_w, (char*)L.m.dw_row, 4, cs, ko + kPtrSendW,
+                         ko + kPtrDWRow);
+    if (grp && nccl_group_end()) return MEMFINE_ERR_NCCL;
+    if (erc) return MEMFINE_ERR_NCCL;
     if (pass == MEMFINE_FWD) {
       if (t1 > t0) launch_combine<T>((const T*)L.send, w, t0, t1, k, hd, L.m, out, cs);
     } else {
-      if (ep_exchange(h, t, h->counts_h, C, j, false, (char*)L.send_w, (char*)L.m.dw_row, 4, cs, ko + kPtrSendW,
-                      ko + kPtrDWRow))
-        return MEMFINE_ERR_NCCL;
       ChunkMeta mb = L.m;
       mb.dw_row = L.send_w;
       if (t1 > t0) launch_unpermute_reduce<T>((const T*)L.send, t0, t1, k, hd, mb, out, dscore, cs);
@@ -1253,6 +1302,10 @@ memfine_status memfine_ep_bwd(memfine_handle_s* h, const void* dy, const void* x
 
 void begin_call(memfine_handle_s* h, int C, int pass, uint64_t ws_bytes, cudaStream_t st) {
   h->last = memfine_stats{};
+  if (h->debug) {
+    h->dbg_mx.assign(C, {});
+    h->dbg_src.assign(C, {});
+  }
   h->last.C = C;
   h->last.pass = pass;
   h->last.workspace_given_bytes = ws_bytes;
@@ -1263,6 +1316,58 @@ void begin_call(memfine_handle_s* h, int C, int pass, uint64_t ws_bytes, cudaStr
 }  // namespace
 
 // =================================================================================== C ABI
+// Per-handle device state of the device-planned P2P exchange (N1): sync area (zeroed; the "done" flags
+// start at the previous-call marker so the first call's chunk 0 may push), skip flags, counts.
+memfine_status p2p_alloc_sync(memfine_handle_s* h) {
+  const memfine_dims& d = h->d;
+  const size_t sb = sync_area_bytes(d.num_experts);
+  if (!h->sync_d) {
+    MF_CUDA_OK(cudaMalloc((void**)&h->sync_d, sb));
+    MF_CUDA_OK(cudaMalloc((void**)&h->gskip_d, sizeof(int) * kMaxSub));
+  }
+  const size_t need = (size_t)d.ep_size * kMaxSub * d.num_experts;
+  if (need > h->counts_cap) {
+    if (h->counts_d) cudaFree(h->counts_d);
+    if (h->counts_h) cudaFreeHost(h->counts_h);
+    h->counts_d = nullptr;
+    h->counts_h = nullptr;
+    h->counts_cap = 0;
+    MF_CUDA_OK(cudaMalloc((void**)&h->counts_d, need * sizeof(int)));
+    MF_CUDA_OK(cudaHostAlloc((void**)&h->counts_h, need * sizeof(int), cudaHostAllocDefault));
+    h->counts_cap = need;
+  }
+  std::vector<uint64_t> init(1 + (size_t)kSyncPhases * kMaxPeers, 0);
+  for (int p = 0; p < kMaxPeers; p++) init[1 + 3 * kMaxPeers + p] = kSyncDoneCall;   // epoch 0, call done
+  MF_CUDA_OK(cudaMemset(h->sync_d, 0, sb));
+  MF_CUDA_OK(cudaMemcpy(h->sync_d, init.data(), init.size() * sizeof(uint64_t), cudaMemcpyHostToDevice));
+  MF_CUDA_OK(cudaDeviceSynchronize());
+  return MEMFINE_OK;
+}
+
+memfine_status register_local(memfine_handle_s* h, void* ws, uint64_t ws_bytes) {
+  memfine_group_s* g = h->lg;
+  const int EP = h->d.ep_size, me = h->d.ep_rank;
+  memfine_status rc = p2p_alloc_sync(h);
+  g->ptrs[me][kPtrWs] = (char*)ws;
+  g->ptrs[me][kPtrSync] = (char*)h->sync_d;
+  g->ptrs[me][kPtrWsBytes] = (char*)(uintptr_t)(rc == MEMFINE_OK ? ws_bytes : 0);
+  g->barrier();   // every rank published its workspace and sync area
+  h->peer_ws.assign(EP, nullptr);
+  h->peer_sync.assign(EP, nullptr);
+  bool same = true;
+  for (int r = 0; r < EP; r++) {
+    h->peer_ws[r] = g->ptrs[r][kPtrWs];
+    h->peer_sync[r] = (uint64_t*)g->ptrs[r][kPtrSync];
+    same = same && (uint64_t)(uintptr_t)g->ptrs[r][kPtrWsBytes] == ws_bytes;
+  }
+  g->barrier();   // nobody republishes before every rank has read
+  if (rc != MEMFINE_OK) return rc;
+  if (!same) return MEMFINE_ERR_INVALID_ARG;   // the fused exchange needs one workspace size on every rank
+  h->reg_ws = ws;
+  h->reg_bytes = ws_bytes;
+  return MEMFINE_OK;
+}
+
 extern "C" {
 
 int32_t memfine_abi_version(void) { return MEMFINE_ABI_VERSION; }
@@ -1389,12 +1494,14 @@ memfine_status memfine_set_ep_transport(memfine_handle_t h, int32_t transport) {
 // the records over the handle's NCCL communicator, open every peer's mapping.
 memfine_status memfine_register_workspace(memfine_handle_t h, void* ws, uint64_t ws_bytes, void* stream) {
   if (!h || !ws) return MEMFINE_ERR_INVALID_ARG;
-  if (h->lg || h->d.ep_size == 1) {  // nothing to map: in-process peers / single rank
+  if (h->lg) return register_local(h, ws, ws_bytes);
+  if (!ep_path(h->d)) {   // a single rank without the EP path: nothing to map
     h->reg_ws = ws;
     h->reg_bytes = ws_bytes;
     return MEMFINE_OK;
   }
   if (!h->comm.comm) return MEMFINE_ERR_NCCL;
+  if (memfine_status rc = p2p_alloc_sync(h)) return rc;
   cudaStream_t st = (cudaStream_t)stream;
   // allocation base of ws
   typedef CUresult (*RangeFn)(CUdeviceptr*, size_t*, CUdeviceptr);
@@ -1410,9 +1517,13 @@ memfine_status memfine_register_workspace(memfine_handle_t h, void* ws, uint64_t
   CUdeviceptr base = 0;
   size_t size = 0;
   if (range_fn(&base, &size, (CUdeviceptr)ws) != CUDA_SUCCESS) return MEMFINE_ERR_CUDA;
-  struct Rec { cudaIpcMemHandle_t hdl; uint64_t offset, bytes; };
+  struct Rec { cudaIpcMemHandle_t hdl, sync; uint64_t offset, bytes; };
   Rec mine{};
-  if (cudaIpcGetMemHandle(&mine.hdl, (void*)base) != cudaSuccess) { cudaGetLastError(); return MEMFINE_ERR_CUDA; }
+  if (cudaIpcGetMemHandle(&mine.hdl, (void*)base) != cudaSuccess ||
+      cudaIpcGetMemHandle(&mine.sync, (void*)h->sync_d) != cudaSuccess) {
+    cudaGetLastError();
+    return MEMFINE_ERR_CUDA;
+  }
   mine.offset = (uint64_t)((char*)ws - (char*)base);
   mine.bytes = ws_bytes;
   const int EP = h->d.ep_size, me = h->d.ep_rank;
@@ -1430,17 +1541,29 @@ memfine_status memfine_register_workspace(memfine_handle_t h, void* ws, uint64_t
   for (void* b : h->ipc_bases) cudaIpcCloseMemHandle(b);
   h->ipc_bases.clear();
   h->peer_ws.assign(EP, nullptr);
+  h->peer_sync.assign(EP, nullptr);
   for (int r = 0; r < EP; r++) {
-    if (r == me) { h->peer_ws[r] = (char*)ws; continue; }
+    if (all[r].bytes != ws_bytes) return MEMFINE_ERR_INVALID_ARG;   // one workspace size on every rank
+    if (r == me) {
+      h->peer_ws[r] = (char*)ws;
+      h->peer_sync[r] = h->sync_d;
+      continue;
+    }
     void* pb = nullptr;
-    if (cudaIpcOpenMemHandle(&pb, all[r].hdl, cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) {
+    void* ps = nullptr;
+    if (cudaIpcOpenMemHandle(&pb, all[r].hdl, cudaIpcMemLazyEnablePeerAccess) != cudaSuccess ||
+        cudaIpcOpenMemHandle(&ps, all[r].sync, cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) {
       cudaGetLastError();
       return MEMFINE_ERR_CUDA;
     }
     h->ipc_bases.push_back(pb);
+    h->ipc_bases.push_back(ps);
     h->peer_ws[r] = (char*)pb + all[r].offset;
+    h->peer_sync[r] = (uint64_t*)ps;
   }
-  if (!h->barrier_d) MF_CUDA_OK(cudaMalloc((void**)&h->barrier_d, sizeof(int)));
+  // every rank has opened every mapping and initialised its flags before anyone signals
+  if (nccl_stream_barrier(&h->comm, h->gskip_d, st)) return MEMFINE_ERR_NCCL;
+  MF_CUDA_OK(cudaStreamSynchronize(st));
   h->reg_ws = ws;
   h->reg_bytes = ws_bytes;
   return MEMFINE_OK;
@@ -1448,11 +1571,10 @@ memfine_status memfine_register_workspace(memfine_handle_t h, void* ws, uint64_t
 
 memfine_status memfine_destroy(memfine_handle_t h) {
   if (!h) return MEMFINE_ERR_INVALID_ARG;
-  if (h->tab_h) cudaFreeHost(h->tab_h);
   if (h->router_scratch) cudaFree(h->router_scratch);
-  if (h->cublas) cublasDestroy((cublasHandle_t)h->cublas);
   for (void* b : h->ipc_bases) cudaIpcCloseMemHandle(b);
-  if (h->barrier_d) cudaFree(h->barrier_d);
+  if (h->sync_d) cudaFree(h->sync_d);
+  if (h->gskip_d) cudaFree(h->gskip_d);
   if (h->comm.comm) nccl_comm_destroy(&h->comm);
   if (h->status_h) cudaFreeHost(h->status_h);
   if (h->rows_h) cudaFreeHost(h->rows_h);
@@ -1513,31 +1635,39 @@ memfine_status memfine_plan(const int32_t* counts, int32_t nsub, const memfine_d
     return plan_impl(counts, nsub, dims, budget, info);
   }
   if (is_device_ptr(counts)) {
-    // A3 on the device: the single-CTA tuner kernel reads the (all-gathered) counts in HBM.
-    memfine_plan_info* out_h = nullptr;
-    int* rc_h = nullptr;
-    if (cudaHostAlloc((void**)&out_h, sizeof(memfine_plan_info) + 16, cudaHostAllocMapped) != cudaSuccess)
-      return MEMFINE_ERR_CUDA;
-    rc_h = (int*)(out_h + 1);
+    // A3 on the device: the single-CTA tuner kernel reads the (all-gathered) counts in HBM.  Its result
+    // lands in pinned mapped memory; buffer and stream are kept per host thread and device (a layer
+    // call plans every step).
+    struct PlanCtx { int dev = -1; memfine_plan_info* out_h = nullptr; cudaStream_t st = nullptr; };
+    static thread_local PlanCtx ctx;
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) { cudaGetLastError(); return MEMFINE_ERR_CUDA; }
+    if (ctx.dev != dev) {
+      if (ctx.out_h) cudaFreeHost(ctx.out_h);
+      if (ctx.st) cudaStreamDestroy(ctx.st);
+      ctx = PlanCtx{};
+      if (cudaHostAlloc((void**)&ctx.out_h, sizeof(memfine_plan_info) + 16, cudaHostAllocMapped) != cudaSuccess ||
+          cudaStreamCreateWithFlags(&ctx.st, cudaStreamNonBlocking) != cudaSuccess) {
+        cudaGetLastError();
+        return MEMFINE_ERR_CUDA;
+      }
+      ctx.dev = dev;
+    }
+    memfine_plan_info* out_h = ctx.out_h;
+    int* rc_h = (int*)(out_h + 1);
     *rc_h = -1;
     memfine_plan_info* out_d;
-    int* rc_d;
     cudaHostGetDevicePointer((void**)&out_d, out_h, 0);
-    rc_d = (int*)(out_d + 1);
-    cudaStream_t st;
+    int* rc_d = (int*)(out_d + 1);
     cudaDeviceSynchronize();  // counts may come from any stream of the caller
-    cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking);
-    const int lrc = launch_plan_kernel(counts, p, out_d, rc_d, st);
-    cudaError_t e = cudaStreamSynchronize(st);
-    cudaStreamDestroy(st);
+    const int lrc = launch_plan_kernel(counts, p, out_d, rc_d, ctx.st);
+    cudaError_t e = cudaStreamSynchronize(ctx.st);
     int rc = *rc_h;
     if (lrc || e != cudaSuccess || rc < 0) {   // launch failure: the result words were never written
       cudaGetLastError();
-      cudaFreeHost(out_h);
       return MEMFINE_ERR_CUDA;
     }
     *info = *out_h;
-    cudaFreeHost(out_h);
     return (memfine_status)rc;
   }
   return plan_host(counts, nsub, dims, budget, info);
@@ -1744,58 +1874,90 @@ memfine_status memfine_mx_quantize(const void* src, int64_t rows, int32_t K, voi
 
 // ---------------------------------------------------------------- router (N3)
 namespace {
+// Router scratch (per handle, allocated on first use): the GEMM-written logits [T][E4] (fp32, row stride a
+// multiple of 16 B for TMA), d_logits, the dense bf16 hi / lo d_logits [T_pad][E8] (rows and columns past
+// T, E stay zero: the dW_r GEMM's K loop runs over whole 128-row blocks), the one-segment metadata the
+// expert-GEMM scheduler reads (seg, pseg, info), and the fp32 path's counting sort.
 struct RouterScratch {
   float* logits;
   float* dlog;
-  __nv_bfloat16* dhi;   // bf16 path: dense d_logits [T][E] as hi + lo
+  __nv_bfloat16* dhi;
   __nv_bfloat16* dlo;
+  int* gseg;     // {0, T_pad}
+  int* gpseg;    // {0, pairs}
+  int* ginfo;    // kInfoWords
   ChunkMeta m;
-  int64_t rows_cap;
+  int64_t rows_cap, T_pad;
+  int E4, E8;
 };
 memfine_status router_scratch(memfine_handle_s* h, RouterScratch* rs) {
   const memfine_dims& d = h->d;
   const int E = d.num_experts, k = d.topk;
   const int64_t T = d.tokens, NB = std::max<int64_t>(1, ceil_div64(T, kTokPerBlk));
   const int64_t rows_cap = round_up64(T * k + (int64_t)E * (kRowAlign - 1), kRowAlign);
+  const int64_t T_pad = round_up64(std::max<int64_t>(T, 1), kRowAlign);
+  const int E4 = (int)round_up64(E, 4), E8 = (int)round_up64(E, 8);
+  auto layout = [&](Bump& b, RouterScratch* o) {
+    float* lg = b.take<float>((uint64_t)T * E4);
+    float* dl = b.take<float>((uint64_t)T * k);
+    __nv_bfloat16* hi = b.take<__nv_bfloat16>((uint64_t)T_pad * E8);
+    __nv_bfloat16* lo = b.take<__nv_bfloat16>((uint64_t)T_pad * E8);
+    int* gs = b.take<int>(2);
+    int* gp = b.take<int>(2);
+    int* gi = b.take<int>(kInfoWords);
+    ChunkMeta m{};
+    m.blk_cnt = b.take<int>((uint64_t)NB * E);
+    m.exp_cnt = b.take<int>(E + 1);
+    m.recv_cnt = b.take<int>(E + 1);
+    m.seg = b.take<int>(E + 1);
+    m.pseg = b.take<int>(E + 1);
+    m.info = b.take<int>(kInfoWords);
+    m.dest_of = b.take<int>((uint64_t)T * k);
+    m.src_of = b.take<int>((uint64_t)rows_cap);
+    if (o) *o = RouterScratch{lg, dl, hi, lo, gs, gp, gi, m, rows_cap, T_pad, E4, E8};
+  };
   Bump b(nullptr);
-  b.take<float>((uint64_t)T * E);
-  b.take<float>((uint64_t)T * k);
-  b.take<__nv_bfloat16>((uint64_t)T * E);
-  b.take<__nv_bfloat16>((uint64_t)T * E);
-  b.take<int>((uint64_t)NB * E);
-  for (int i = 0; i < 3; i++) b.take<int>(E + 1);
-  b.take<int>(E + 1);
-  b.take<int>(kInfoWords);
-  b.take<int>((uint64_t)T * k);
-  b.take<int>((uint64_t)rows_cap);
+  layout(b, nullptr);
   if (b.off > h->router_bytes) {
     if (h->router_scratch) cudaFree(h->router_scratch);
     h->router_scratch = nullptr;
     h->router_bytes = 0;
     MF_CUDA_OK(cudaMalloc((void**)&h->router_scratch, b.off));
     h->router_bytes = b.off;
+    Bump c(h->router_scratch);
+    layout(c, rs);
+    // zero padding of hi / lo, and the scheduler's metadata of the one T-row segment (fixed per handle)
+    MF_CUDA_OK(cudaMemset(rs->dhi, 0, sizeof(__nv_bfloat16) * (size_t)T_pad * E8));
+    MF_CUDA_OK(cudaMemset(rs->dlo, 0, sizeof(__nv_bfloat16) * (size_t)T_pad * E8));
+    const int mt = (int)(T_pad / kRowAlign), pairs = (mt + 1) / 2;
+    int meta[4 + kInfoWords] = {0, (int)T_pad, 0, pairs};
+    meta[4 + kInfoRows] = (int)T;
+    meta[4 + kInfoRowsPad] = (int)T_pad;
+    meta[4 + kInfoSend] = (int)T;
+    meta[4 + kInfoSkip] = 0;
+    meta[4 + kInfoPairs] = pairs;
+    MF_CUDA_OK(cudaMemcpy(rs->gseg, meta, sizeof(int) * 2, cudaMemcpyHostToDevice));
+    MF_CUDA_OK(cudaMemcpy(rs->gpseg, meta + 2, sizeof(int) * 2, cudaMemcpyHostToDevice));
+    MF_CUDA_OK(cudaMemcpy(rs->ginfo, meta + 4, sizeof(int) * kInfoWords, cudaMemcpyHostToDevice));
+    return MEMFINE_OK;
   }
   Bump c(h->router_scratch);
-  rs->logits = c.take<float>((uint64_t)T * E);
-  rs->dlog = c.take<float>((uint64_t)T * k);
-  rs->dhi = c.take<__nv_bfloat16>((uint64_t)T * E);
-  rs->dlo = c.take<__nv_bfloat16>((uint64_t)T * E);
-  rs->m = ChunkMeta{};
-  rs->m.blk_cnt = c.take<int>((uint64_t)NB * E);
-  rs->m.exp_cnt = c.take<int>(E + 1);
-  rs->m.recv_cnt = c.take<int>(E + 1);
-  rs->m.seg = c.take<int>(E + 1);
-  rs->m.pseg = c.take<int>(E + 1);
-  rs->m.info = c.take<int>(kInfoWords);
-  rs->m.dest_of = c.take<int>((uint64_t)T * k);
-  rs->m.src_of = c.take<int>((uint64_t)rows_cap);
-  rs->rows_cap = rows_cap;
-  if (d.dtype != MEMFINE_FP32 && !h->cublas) {
-    cublasHandle_t cb = nullptr;
-    if (cublasCreate(&cb) != CUBLAS_STATUS_SUCCESS) return MEMFINE_ERR_CUDA;
-    h->cublas = cb;
-  }
+  layout(c, rs);
   return MEMFINE_OK;
+}
+
+// The router's dense contractions on the expert-GEMM kernels: one "expert" whose rows are the T tokens.
+GemmProblem<__nv_bfloat16> router_problem(const memfine_handle_s* h, const RouterScratch& rs) {
+  GemmProblem<__nv_bfloat16> p{};
+  p.El = 1;
+  p.h = h->d.num_experts;    // N of the logits GEMM, M of the dW_r GEMM
+  p.g = h->d.hidden;         // K of the logits GEMM, N of the dW_r GEMM
+  p.rows_cap = rs.T_pad;
+  p.rows_in = h->d.tokens;
+  p.seg = rs.gseg;
+  p.pseg = rs.gpseg;
+  p.info = rs.ginfo;
+  return p;
 }
 }  // namespace
 
@@ -1806,14 +1968,24 @@ memfine_status memfine_router_fwd(memfine_handle_t h, const void* x, const void*
   cudaStream_t st = (cudaStream_t)stream;
   RouterScratch rs;
   if (int rc = router_scratch(h, &rs)) return (memfine_status)rc;
-  float* lg = logits ? logits : rs.logits;
   if (d.dtype != MEMFINE_FP32) {
-    if (launch_router_fwd_bf16(h->cublas, (const __nv_bfloat16*)x, (const __nv_bfloat16*)w_router, d.tokens,
-                               d.num_experts, d.hidden, d.topk, lg, ids, scores, st))
-      return MEMFINE_ERR_CUDA;
-  } else
-    launch_router_fwd<float>((const float*)x, (const float*)w_router, d.tokens, d.num_experts, d.hidden, d.topk, lg,
-                             ids, scores, st);
+    if (d.tokens == 0) return MEMFINE_OK;
+    // logits = x W_r^T: a DOWN launch (A = x [T][h] K-major, B = W_r [1][E][h]) storing fp32 [T][E4]
+    GemmProblem<__nv_bfloat16> p = router_problem(h, rs);
+    p.kind = GK_DOWN;
+    p.A = (__nv_bfloat16*)x;
+    p.Wd = (const __nv_bfloat16*)w_router;
+    p.O = (__nv_bfloat16*)rs.logits;
+    p.out_f32 = 1;
+    p.ld_out = rs.E4;
+    if (int rc = run_gemm<__nv_bfloat16>(h, p, st)) return (memfine_status)rc;
+    launch_router_topk(rs.logits, rs.E4, d.tokens, d.num_experts, d.topk, ids, scores, logits, st);
+    h->last.kernel_launches += 1;
+    return latch_cuda(h);
+  }
+  float* lg = logits ? logits : rs.logits;
+  launch_router_fwd<float>((const float*)x, (const float*)w_router, d.tokens, d.num_experts, d.hidden, d.topk, lg,
+                           ids, scores, st);
   return latch_cuda(h);
 }
 
@@ -1828,10 +2000,25 @@ memfine_status memfine_router_bwd(memfine_handle_t h, const void* x, const void*
   if (int rc = router_scratch(h, &rs)) return (memfine_status)rc;
   const int E = d.num_experts, k = d.topk;
   if (d.dtype != MEMFINE_FP32) {
-    if (launch_router_bwd_bf16(h->cublas, (const __nv_bfloat16*)x, (const __nv_bfloat16*)w_router, ids, scores,
-                               dscore, d.tokens, E, d.hidden, k, rs.dlog, rs.dhi, rs.dlo, (__nv_bfloat16*)dx,
-                               accumulate_dx, dw_router, accumulate_dw, st))
-      return MEMFINE_ERR_CUDA;
+    if (d.tokens == 0) {
+      if (!accumulate_dw) MF_CUDA_OK(cudaMemsetAsync(dw_router, 0, sizeof(float) * (size_t)E * d.hidden, st));
+      return MEMFINE_OK;
+    }
+    launch_router_bwd_rows_bf16((const __nv_bfloat16*)w_router, ids, scores, dscore, d.tokens, E, d.hidden, k,
+                                rs.dlog, rs.dhi, rs.dlo, rs.E8, (__nv_bfloat16*)dx, accumulate_dx, st);
+    h->last.kernel_launches += 1;
+    // dW_r (+)= d_logits^T x = hi^T x + lo^T x: two WGRAD_DOWN launches (K = the T_pad token rows)
+    GemmProblem<__nv_bfloat16> p = router_problem(h, rs);
+    p.kind = GK_WGRAD_DOWN;
+    p.A = (__nv_bfloat16*)x;
+    p.ld_a = rs.E8;
+    p.dWd = dw_router;
+    p.DY = rs.dhi;
+    p.wgrad_beta = accumulate_dw ? 1 : 0;
+    if (int rc = run_gemm<__nv_bfloat16>(h, p, st)) return (memfine_status)rc;
+    p.DY = rs.dlo;
+    p.wgrad_beta = 1;
+    if (int rc = run_gemm<__nv_bfloat16>(h, p, st)) return (memfine_status)rc;
     return latch_cuda(h);
   }
   // fp32: counting sort of the copies by expert (stable): segment e = rows [seg[e], seg[e] + cnt[e])
@@ -1896,6 +2083,32 @@ memfine_status memfine_profile_read(memfine_handle_t h, memfine_profile* out) {
 memfine_status memfine_set_debug(memfine_handle_t h, int32_t enable) {
   if (!h) return MEMFINE_ERR_INVALID_ARG;
   h->debug = enable ? 1 : 0;
+  return MEMFINE_OK;
+}
+
+memfine_status memfine_debug_rows(memfine_handle_t h, int32_t chunk, int32_t* src_of_host, int64_t cap, int64_t* n) {
+  if (!h || !n || chunk < 0 || chunk >= (int)h->dbg_src.size()) return MEMFINE_ERR_INVALID_ARG;
+  const auto& v = h->dbg_src[chunk];
+  *n = (int64_t)v.size();
+  if (src_of_host) {
+    if (cap < (int64_t)v.size()) return MEMFINE_ERR_INVALID_ARG;
+    std::copy(v.begin(), v.end(), src_of_host);
+  }
+  return MEMFINE_OK;
+}
+
+memfine_status memfine_debug_mx(memfine_handle_t h, int32_t chunk, int32_t which, uint8_t* codes_host,
+                                uint8_t* scales_host, int64_t cap_codes, int64_t* rows, int64_t* cols) {
+  if (!h || !rows || !cols || chunk < 0 || chunk >= (int)h->dbg_mx.size() || which < 0 || which >= 6)
+    return MEMFINE_ERR_INVALID_ARG;
+  const auto& D = h->dbg_mx[chunk][which];
+  *rows = D.rows;
+  *cols = D.cols;
+  if (codes_host) {
+    if (cap_codes < (int64_t)D.q.size() || !scales_host) return MEMFINE_ERR_INVALID_ARG;
+    std::copy(D.q.begin(), D.q.end(), codes_host);
+    std::copy(D.sf.begin(), D.sf.end(), scales_host);
+  }
   return MEMFINE_OK;
 }
 

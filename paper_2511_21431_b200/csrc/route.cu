@@ -627,11 +627,116 @@ __global__ void __launch_bounds__(256, 2) gather_reduce_kernel(
   }
 }
 
+// bf16 combine / unpermute-reduce (A10, B7): one warp per token, 32 B per lane per load (LDG.256),
+// NC = 2 column chunks of 512 per iteration and SG slots loaded before the FMAs, so a warp keeps
+// SG x 2 x 1 KB in flight (the per-slot loop had 512 B).  Slots are accumulated in ascending order
+// from 0 with fma(w_s, v, acc) - bit-identical to the generic kernel above.
+__device__ __forceinline__ void ldg256_nc(const void* p, uint32_t (&v)[8]) {
+  asm volatile("ld.global.nc.L1::no_allocate.v8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+               : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7])
+               : "l"(p));
+}
+__device__ __forceinline__ void stg256(void* p, const uint32_t (&v)[8]) {
+  asm volatile("st.global.v8.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};" ::"l"(p), "r"(v[0]), "r"(v[1]), "r"(v[2]),
+               "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7])
+               : "memory");
+}
+
+template <bool WEIGHTED, int SG>
+__global__ void __launch_bounds__(256, SG <= 2 ? 3 : 2) gather_reduce_bf16_kernel(
+    const __nv_bfloat16* __restrict__ rows, const float* __restrict__ w, int64_t t0, int64_t t1, int k, int h,
+    const int* __restrict__ dest_of, const int* __restrict__ info, __nv_bfloat16* __restrict__ out,
+    const float* __restrict__ dw_row, float* __restrict__ dscore) {
+  pdl_wait();
+  pdl_trigger();
+  if (info[kInfoSkip]) return;
+  constexpr int NC = 2;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t i = t0 + (int64_t)blockIdx.x * (blockDim.x >> 5) + warp;
+  if (i >= t1) return;
+  __shared__ int pos_s[8][16];
+  __shared__ float ws_s[8][16];
+  int* pos = pos_s[warp];
+  float* ws = ws_s[warp];
+  const int kk = k < 16 ? k : 16;
+  if (lane < 16) {
+    pos[lane] = lane < kk ? dest_of[(i - t0) * k + lane] : -1;
+    ws[lane] = (WEIGHTED && lane < kk) ? __ldg(w + i * k + lane) : 1.0f;
+  }
+  __syncwarp();
+  if (dscore && lane < k) {
+    const int p = dest_of[(i - t0) * k + lane];
+    dscore[i * k + lane] = p >= 0 ? dw_row[p] : 0.0f;
+  }
+  for (int c0 = lane * 16; c0 < h; c0 += 512 * NC) {
+    float acc[NC][16];
+#pragma unroll
+    for (int q = 0; q < NC; q++)
+#pragma unroll
+      for (int u = 0; u < 16; u++) acc[q][u] = 0.f;
+    for (int g0 = 0; g0 < kk; g0 += SG) {
+      uint32_t raw[SG][NC][8];
+#pragma unroll
+      for (int s = 0; s < SG; s++)
+#pragma unroll
+        for (int q = 0; q < NC; q++) {
+          const int c = c0 + q * 512;
+          if (g0 + s < kk && pos[g0 + s] >= 0 && c < h) {
+            ldg256_nc(rows + (int64_t)pos[g0 + s] * h + c, raw[s][q]);
+          } else {
+#pragma unroll
+            for (int u = 0; u < 8; u++) raw[s][q][u] = 0u;
+          }
+        }
+#pragma unroll
+      for (int s = 0; s < SG; s++) {
+        if (g0 + s >= kk || pos[g0 + s] < 0) continue;
+        const float ww = ws[g0 + s];
+#pragma unroll
+        for (int q = 0; q < NC; q++)
+#pragma unroll
+          for (int u = 0; u < 8; u++) {
+            acc[q][2 * u] = fmaf(ww, __uint_as_float(raw[s][q][u] << 16), acc[q][2 * u]);
+            acc[q][2 * u + 1] = fmaf(ww, __uint_as_float(raw[s][q][u] & 0xFFFF0000u), acc[q][2 * u + 1]);
+          }
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < NC; q++) {
+      const int c = c0 + q * 512;
+      if (c >= h) continue;
+      uint32_t o[8];
+#pragma unroll
+      for (int u = 0; u < 8; u++) {
+        __nv_bfloat162 b = __floats2bfloat162_rn(acc[q][2 * u], acc[q][2 * u + 1]);
+        o[u] = *reinterpret_cast<uint32_t*>(&b);
+      }
+      stg256(out + i * h + c, o);
+    }
+  }
+}
+
+template <bool WEIGHTED>
+void launch_gather_reduce_bf16(const __nv_bfloat16* rows, const float* w, int64_t t0, int64_t t1, int k, int h,
+                               const ChunkMeta& m, __nv_bfloat16* out, const float* dw_row, float* dscore,
+                               cudaStream_t st) {
+  const dim3 grid((unsigned)ceil_div64(t1 - t0, 8));
+  if (k <= 2)
+    launch_pdl(gather_reduce_bf16_kernel<WEIGHTED, 2>, grid, dim3(256), 0, st, rows, w, t0, t1, k, h, m.dest_of,
+               m.info, out, dw_row, dscore);
+  else
+    launch_pdl(gather_reduce_bf16_kernel<WEIGHTED, 4>, grid, dim3(256), 0, st, rows, w, t0, t1, k, h, m.dest_of,
+               m.info, out, dw_row, dscore);
+}
+
 template <typename T>
 void launch_combine(const T* O, const float* w, int64_t t0, int64_t t1, int k, int h, const ChunkMeta& m, T* y,
                     cudaStream_t st) {
   int64_t n = t1 - t0;
   if (n == 0) return;
+  if constexpr (std::is_same<T, __nv_bfloat16>::value) {
+    if (h % 16 == 0) return launch_gather_reduce_bf16<true>(O, w, t0, t1, k, h, m, y, nullptr, nullptr, st);
+  }
   launch_pdl(gather_reduce_kernel<T, true>, dim3((unsigned)ceil_div64(n, 8)), dim3(256), 0, st, O, w, t0, t1, k, h, m.dest_of, m.info,
                                                                            y, nullptr, nullptr);
 }
@@ -641,6 +746,9 @@ void launch_unpermute_reduce(const T* dXd, int64_t t0, int64_t t1, int k, int h,
                              float* dscore, cudaStream_t st) {
   int64_t n = t1 - t0;
   if (n == 0) return;
+  if constexpr (std::is_same<T, __nv_bfloat16>::value) {
+    if (h % 16 == 0) return launch_gather_reduce_bf16<false>(dXd, nullptr, t0, t1, k, h, m, dx, m.dw_row, dscore, st);
+  }
   launch_pdl(gather_reduce_kernel<T, false>, dim3((unsigned)ceil_div64(n, 8)), dim3(256), 0, st, dXd, nullptr, t0, t1, k, h, m.dest_of,
                                                                             m.info, dx, m.dw_row, dscore);
 }
@@ -650,7 +758,7 @@ void launch_unpermute_reduce(const T* dXd, int64_t t0, int64_t t1, int k, int h,
 __global__ void ep_recv_seg_kernel(const int* __restrict__ counts, int C, int j, int E, int El, int me, int EP,
                                    int64_t rows_cap, int* __restrict__ seg, int* __restrict__ pseg,
                                    int* __restrict__ recv_cnt, int* __restrict__ info, int64_t* stats_rows,
-                                   int64_t* stats_rows_pad) {
+                                   int64_t* stats_rows_pad, const int* __restrict__ gskip) {
   if (threadIdx.x != 0) return;
   int acc = 0, rows = 0, pairs = 0;
   for (int el = 0; el < El; el++) {
@@ -669,14 +777,15 @@ __global__ void ep_recv_seg_kernel(const int* __restrict__ counts, int C, int j,
   info[kInfoPairs] = pairs;
   info[kInfoRows] = rows;
   info[kInfoRowsPad] = acc;
-  info[kInfoSkip] = acc > rows_cap ? 1 : 0;
+  info[kInfoSkip] = (acc > rows_cap || (gskip && gskip[j])) ? 1 : 0;
   if (stats_rows) { stats_rows[j] = rows; stats_rows_pad[j] = acc; }
 }
 
 void launch_ep_recv_seg(const int* counts, int C, int j, int E, int El, int me, int EP, int64_t rows_cap,
-                        const ChunkMeta& m, int64_t* stats_rows, int64_t* stats_rows_pad, cudaStream_t st) {
+                        const ChunkMeta& m, int64_t* stats_rows, int64_t* stats_rows_pad, cudaStream_t st,
+                        const int* gskip) {
   ep_recv_seg_kernel<<<1, 32, 0, st>>>(counts, C, j, E, El, me, EP, rows_cap, m.seg, m.pseg, m.recv_cnt, m.info,
-                                       stats_rows, stats_rows_pad);
+                                       stats_rows, stats_rows_pad, gskip);
 }
 
 // ------------------------------------------------------------------------------------------
@@ -687,6 +796,7 @@ __global__ void __launch_bounds__(256) p2p_push_kernel(const T* __restrict__ x, 
                                                        const float* __restrict__ w, int k, int h, int E, int El,
                                                        const int* __restrict__ tab, const int* __restrict__ send_src,
                                                        const int* __restrict__ info, PeerTable pt) {
+  if (info[kInfoSkip]) return;
   const int rows = info[kInfoSend];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int nwarps = gridDim.x * (blockDim.x >> 5);
@@ -738,7 +848,7 @@ void launch_p2p_push(const T* x, const T* dy, const float* w, int k, int h, int 
 __global__ void p2p_row_addr_kernel(const int* __restrict__ seg, const int* __restrict__ recv_cnt, int El, int EP,
                                     const int* __restrict__ tab, int E, const int* __restrict__ info, PeerTable pt,
                                     int row_bytes, uint64_t* __restrict__ row_addr, uint64_t* __restrict__ row_addr_w) {
-  const int rows = info[kInfoRowsPad];
+  const int rows = info[kInfoSkip] ? 0 : info[kInfoRowsPad];
   const int* recv_off = tab + E + 1 + EP * El;
   const int* ret = recv_off + EP * El;
   for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < rows; r += gridDim.x * blockDim.x) {
@@ -769,6 +879,7 @@ void launch_p2p_row_addr(const int* seg, const int* recv_cnt, int El, int EP, co
 
 __global__ void p2p_push_dw_kernel(const float* __restrict__ dw_row, const uint64_t* __restrict__ row_addr_w,
                                    const int* __restrict__ info) {
+  if (info[kInfoSkip]) return;
   const int rows = info[kInfoRowsPad];
   for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < rows; r += gridDim.x * blockDim.x) {
     uint64_t a = row_addr_w[r];
@@ -781,6 +892,145 @@ void launch_p2p_push_dw(const float* dw_row, const uint64_t* row_addr_w, const i
   if (rows_cap <= 0) return;
   int blocks = (int)std::min<int64_t>(ceil_div64(rows_cap, 256), 148 * 8);
   p2p_push_dw_kernel<<<blocks, 256, 0, st>>>(dw_row, row_addr_w, info);
+}
+
+// ------------------------------------------------------------------------------------------
+// N1: device-planned exchange ("first notification"): the count
+// all-gather, the chunk tables and the fences run on the device; the host never waits.
+// ------------------------------------------------------------------------------------------
+uint64_t sync_area_bytes(int E) {
+  return sizeof(uint64_t) * (1 + (uint64_t)kSyncPhases * kMaxPeers) +
+         sizeof(int) * 2ull * kMaxPeers * kMaxSub * (uint64_t)E;
+}
+__device__ __forceinline__ uint64_t* sync_flags(uint64_t* area) { return area + 1; }
+__device__ __forceinline__ int* sync_counts(uint64_t* area, int E, int parity, int src) {
+  return reinterpret_cast<int*>(area + 1 + kSyncPhases * kMaxPeers) + ((int64_t)parity * kMaxPeers + src) * kMaxSub * E;
+}
+__device__ __forceinline__ void st_release_sys(uint64_t* p, uint64_t v) {
+  asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ uint64_t ld_acquire_sys(const uint64_t* p) {
+  uint64_t v;
+  asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ uint64_t globaltimer() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+__global__ void sync_epoch_kernel(uint64_t* area) {
+  if (threadIdx.x == 0 && blockIdx.x == 0) area[0] += 1;
+}
+void launch_sync_epoch(uint64_t* area, cudaStream_t st) { sync_epoch_kernel<<<1, 32, 0, st>>>(area); }
+
+// block p: this rank's counts into peer p's landing zone, then (after the block's stores) its flag
+__global__ void sync_push_counts_kernel(const int* __restrict__ mine, int n, int E, SyncPeers sp, int me) {
+  const int p = blockIdx.x;
+  const uint64_t ep = sp.area[me][0];
+  int* dst = sync_counts(sp.area[p], E, (int)(ep & 1), me);
+  for (int i = threadIdx.x; i < n; i += blockDim.x) dst[i] = mine[i];
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence_system();
+    st_release_sys(sync_flags(sp.area[p]) + 0 * kMaxPeers + me, ep * 256);
+  }
+}
+void launch_sync_push_counts(const int* mine, int C, int E, const SyncPeers& sp, int me, cudaStream_t st) {
+  sync_push_counts_kernel<<<sp.n, 256, 0, st>>>(mine, C * E, E, sp, me);
+}
+
+__global__ void sync_signal_kernel(SyncPeers sp, int me, int phase, int code) {
+  if (threadIdx.x != 0) return;
+  const uint64_t v = sp.area[me][0] * 256 + (uint64_t)code;
+  __threadfence_system();   // this stream's earlier kernels (their peer stores) before the flag
+  for (int p = 0; p < sp.n; p++) st_release_sys(sync_flags(sp.area[p]) + phase * kMaxPeers + me, v);
+}
+void launch_sync_signal(const SyncPeers& sp, int me, int phase, int code, cudaStream_t st) {
+  sync_signal_kernel<<<1, 32, 0, st>>>(sp, me, phase, code);
+}
+
+__global__ void sync_wait_kernel(uint64_t* area, int EP, int me, int phase, int code, int* status) {
+  const int p = threadIdx.x;
+  if (p >= EP || p == me) return;
+  const uint64_t target = (uint64_t)((int64_t)area[0] * 256 + code);
+  const uint64_t* f = sync_flags(area) + phase * kMaxPeers + p;
+  const uint64_t t0 = globaltimer();
+  while (ld_acquire_sys(f) < target) {
+    if (globaltimer() - t0 > 20000000000ull) {   // 20 s: a peer never arrived - latch, do not hang
+      latch_error(status, MEMFINE_ERR_CUDA);
+      return;
+    }
+    __nanosleep(256);
+  }
+}
+void launch_sync_wait(uint64_t* area, int EP, int me, int phase, int code, int* status, cudaStream_t st) {
+  sync_wait_kernel<<<1, 32, 0, st>>>(area, EP, me, phase, code, status);
+}
+
+// One block per chunk j: the landed counts -> counts_all [EP][C][E] (block 0 copies), and chunk j's
+// table: send_off (this rank's chunk copies over global experts), land[p][el] (where this rank's rows of
+// expert (p, el) start in p's expert-major buffer), recv_off[s][el] (where s's rows of my local expert el
+// start in mine), ret[s][el] (s's send-layout position of its copies of (me, el)); plus the global skip.
+__global__ void p2p_tables_kernel(const uint64_t* __restrict__ area_c, int C, int E, int El, int EP, int me,
+                                  int64_t rows_cap, int64_t send_cap, int* __restrict__ counts_all,
+                                  int* __restrict__ p2p_tab, int* __restrict__ gskip, int* status) {
+  uint64_t* area = const_cast<uint64_t*>(area_c);
+  const int parity = (int)(area[0] & 1);
+  const int j = blockIdx.x;
+  auto cnt = [&](int src, int e) -> int { return sync_counts(area, E, parity, src)[(int64_t)j * E + e]; };
+  if (j == 0)
+    for (int i = threadIdx.x; i < EP * C * E; i += blockDim.x) {
+      const int src = i / (C * E), r = i % (C * E);
+      counts_all[i] = sync_counts(area, E, parity, src)[r];
+    }
+  int* tab = p2p_tab + (int64_t)j * (4 * E + 1);
+  int* send_off = tab;
+  int* land = tab + E + 1;
+  int* roff = land + EP * El;
+  int* ret = roff + EP * El;
+  __shared__ int bad;
+  if (threadIdx.x == 0) bad = 0;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int acc = 0;
+    for (int e = 0; e < E; e++) { send_off[e] = acc; acc += cnt(me, e); }
+    send_off[E] = acc;
+  }
+  // per rank p (one thread each): p's padded expert-major layout for chunk j and its send prefix
+  for (int p = threadIdx.x; p < EP; p += blockDim.x) {
+    int64_t acc = 0, sendp = 0;
+    for (int e = 0; e < E; e++) sendp += cnt(p, e);
+    for (int el = 0; el < El; el++) {
+      int64_t run = acc;
+      for (int s = 0; s < EP; s++) {
+        const int c = cnt(s, p * El + el);
+        if (s == me) land[p * El + el] = (int)run;   // my rows of expert (p, el) in p's buffer
+        if (p == me) roff[s * El + el] = (int)run;   // s's rows of my expert el in my buffer
+        run += c;
+      }
+      acc += (run - acc + kRowAlign - 1) / kRowAlign * kRowAlign;
+    }
+    // ret[p][el]: p's send-layout position of its copies of my expert el = prefix over global experts
+    int64_t pre = 0;
+    for (int e = 0; e < me * El; e++) pre += cnt(p, e);
+    for (int el = 0; el < El; el++) {
+      ret[p * El + el] = (int)pre;
+      pre += cnt(p, me * El + el);
+    }
+    if (acc > rows_cap || sendp > send_cap) atomicOr(&bad, 1);
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    gskip[j] = bad;
+    if (bad) latch_error(status, MEMFINE_ERR_WORKSPACE);
+  }
+}
+void launch_p2p_tables(const uint64_t* area, int C, int E, int El, int EP, int me, int64_t rows_cap,
+                       int64_t send_cap, int* counts_all, int* p2p_tab, int* gskip, int* status, cudaStream_t st) {
+  p2p_tables_kernel<<<C, 256, 0, st>>>(area, C, E, El, EP, me, rows_cap, send_cap, counts_all, p2p_tab, gskip,
+                                       status);
 }
 
 // ------------------------------------------------------------------------------------------

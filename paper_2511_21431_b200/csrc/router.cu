@@ -2,7 +2,6 @@
 // PAPER.md:83-84): logits = x W_r^T (fp32 accumulate), the k largest logits (ties: lower expert id),
 // scores = softmax over the k selected logits; and its backward consuming the layer's d_score.
 #include <algorithm>
-#include <cublas_v2.h>
 #include "kernels.h"
 
 namespace memfine {
@@ -50,12 +49,16 @@ __global__ void __launch_bounds__(256) router_logits_kernel(const T* __restrict_
 }
 
 // ------------------------------------------------------------------ top-k + softmax, one warp per token
+// logits row stride ld (>= E); out (nullable): the logits copied to a dense [T][E] array
 __global__ void __launch_bounds__(256) router_topk_kernel(const float* __restrict__ logits, int64_t ntok, int E, int k,
-                                                          int32_t* __restrict__ ids, float* __restrict__ scores) {
+                                                          int32_t* __restrict__ ids, float* __restrict__ scores,
+                                                          int64_t ld, float* __restrict__ out) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t t = (int64_t)blockIdx.x * (blockDim.x >> 5) + warp;
   if (t >= ntok) return;
-  const float* lg = logits + t * E;
+  const float* lg = logits + t * ld;
+  if (out)
+    for (int e = lane; e < E; e += 32) out[t * E + e] = lg[e];
   uint32_t taken = 0;   // bit s: this lane's s-th expert (lane + 32 s) is chosen (E <= 1024)
   float sel_v[16];
   int sel_i[16];
@@ -100,7 +103,7 @@ __global__ void __launch_bounds__(256) router_bwd_rows_kernel(const T* __restric
                                                               int h, int E, float* __restrict__ dlog,
                                                               __nv_bfloat16* __restrict__ dhi,
                                                               __nv_bfloat16* __restrict__ dlo, T* __restrict__ dx,
-                                                              int accumulate) {
+                                                              int accumulate, int ldd) {
   constexpr int V = 16 / sizeof(T);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t t = (int64_t)blockIdx.x * (blockDim.x >> 5) + warp;
@@ -119,8 +122,8 @@ __global__ void __launch_bounds__(256) router_bwd_rows_kernel(const T* __restric
       float v = 0.f;
       for (int j = 0; j < k; j++) v = (id[j] == e) ? dl[j] : v;
       const __nv_bfloat16 hi = __float2bfloat16(v);
-      dhi[t * E + e] = hi;
-      dlo[t * E + e] = __float2bfloat16(v - __bfloat162float(hi));
+      dhi[t * ldd + e] = hi;
+      dlo[t * ldd + e] = __float2bfloat16(v - __bfloat162float(hi));
     }
   }
   if (h % V == 0) {
@@ -181,48 +184,25 @@ void launch_router_fwd(const T* x, const T* wr, int64_t ntok, int E, int h, int 
   if (ntok == 0) return;
   dim3 grid((unsigned)ceil_div64(E, 64), (unsigned)ceil_div64(ntok, 64));
   router_logits_kernel<T><<<grid, 256, 0, st>>>(x, wr, ntok, E, h, logits);
-  router_topk_kernel<<<(unsigned)ceil_div64(ntok, 8), 256, 0, st>>>(logits, ntok, E, k, ids, scores);
+  router_topk_kernel<<<(unsigned)ceil_div64(ntok, 8), 256, 0, st>>>(logits, ntok, E, k, ids, scores, E, nullptr);
 }
 
-// bf16: the logits are a plain dense GEMM (bf16 operands, fp32 accumulate and output) - cuBLAS on the
-// tensor cores.  Row-major logits [T][E] = column-major [E][T] = W_r (op T of the column-major [h][E]
-// view of W_r [E][h]) x x^T (column-major [h][T] view of x [T][h]).
-int launch_router_fwd_bf16(void* cublas, const __nv_bfloat16* x, const __nv_bfloat16* wr, int64_t ntok, int E,
-                           int h, int k, float* logits, int32_t* ids, float* scores, cudaStream_t st) {
-  if (ntok == 0) return 0;
-  cublasHandle_t cb = (cublasHandle_t)cublas;
-  const float one = 1.f, zero = 0.f;
-  if (cublasSetStream(cb, st) != CUBLAS_STATUS_SUCCESS) return 1;
-  if (cublasGemmEx(cb, CUBLAS_OP_T, CUBLAS_OP_N, E, (int)ntok, h, &one, wr, CUDA_R_16BF, h, x, CUDA_R_16BF, h,
-                   &zero, logits, CUDA_R_32F, E, CUBLAS_COMPUTE_32F, CUBLAS_GEMM_DEFAULT) != CUBLAS_STATUS_SUCCESS)
-    return 1;
-  router_topk_kernel<<<(unsigned)ceil_div64(ntok, 8), 256, 0, st>>>(logits, ntok, E, k, ids, scores);
-  return 0;
+// bf16 forward epilogue: top-k + softmax over the fp32 logits [T][ld] the tcgen05 GEMM wrote (memfine.cu
+// runs the logits GEMM on the expert-GEMM kernels); out (nullable) receives the dense [T][E] logits.
+void launch_router_topk(const float* logits, int64_t ld, int64_t ntok, int E, int k, int32_t* ids, float* scores,
+                        float* out, cudaStream_t st) {
+  if (ntok == 0) return;
+  router_topk_kernel<<<(unsigned)ceil_div64(ntok, 8), 256, 0, st>>>(logits, ntok, E, k, ids, scores, ld, out);
 }
 
-// bf16 backward: dx by the row kernel; dW_r (row-major [E][h] = column-major [h][E]) = x^T D with D the
-// dense d_logits [T][E] (column-major [E][T], op T), as two accumulating GEMMs over its hi and lo halves.
-int launch_router_bwd_bf16(void* cublas, const __nv_bfloat16* x, const __nv_bfloat16* wr, const int32_t* ids,
-                           const float* scores, const float* dscore, int64_t ntok, int E, int h, int k, float* dlog,
-                           __nv_bfloat16* dhi, __nv_bfloat16* dlo, __nv_bfloat16* dx, int acc_dx, float* dwr,
-                           int acc_dw, cudaStream_t st) {
-  if (ntok > 0)
-    router_bwd_rows_kernel<__nv_bfloat16><<<(unsigned)ceil_div64(ntok, 8), 256, 0, st>>>(
-        wr, ids, scores, dscore, ntok, k, h, E, dlog, dhi, dlo, dx, acc_dx);
-  if (ntok == 0) {
-    if (!acc_dw) return cudaMemsetAsync(dwr, 0, sizeof(float) * (size_t)E * h, st) != cudaSuccess;
-    return 0;
-  }
-  cublasHandle_t cb = (cublasHandle_t)cublas;
-  const float one = 1.f, beta0 = acc_dw ? 1.f : 0.f;
-  if (cublasSetStream(cb, st) != CUBLAS_STATUS_SUCCESS) return 1;
-  if (cublasGemmEx(cb, CUBLAS_OP_N, CUBLAS_OP_T, h, E, (int)ntok, &one, x, CUDA_R_16BF, h, dhi, CUDA_R_16BF, E,
-                   &beta0, dwr, CUDA_R_32F, h, CUBLAS_COMPUTE_32F, CUBLAS_GEMM_DEFAULT) != CUBLAS_STATUS_SUCCESS)
-    return 1;
-  if (cublasGemmEx(cb, CUBLAS_OP_N, CUBLAS_OP_T, h, E, (int)ntok, &one, x, CUDA_R_16BF, h, dlo, CUDA_R_16BF, E,
-                   &one, dwr, CUDA_R_32F, h, CUBLAS_COMPUTE_32F, CUBLAS_GEMM_DEFAULT) != CUBLAS_STATUS_SUCCESS)
-    return 1;
-  return 0;
+// bf16 backward rows: d_logits, dx (+)= d_logits W_r, and the dense d_logits [T][ldd] as the bf16 pair hi + lo
+// (exact to ~2^-17 relative; zero off the selected slots) - the operands of the tcgen05 dW_r GEMMs.
+void launch_router_bwd_rows_bf16(const __nv_bfloat16* wr, const int32_t* ids, const float* scores, const float* dscore,
+                                 int64_t ntok, int E, int h, int k, float* dlog, __nv_bfloat16* dhi,
+                                 __nv_bfloat16* dlo, int ldd, __nv_bfloat16* dx, int acc_dx, cudaStream_t st) {
+  if (ntok == 0) return;
+  router_bwd_rows_kernel<__nv_bfloat16><<<(unsigned)ceil_div64(ntok, 8), 256, 0, st>>>(
+      wr, ids, scores, dscore, ntok, k, h, E, dlog, dhi, dlo, dx, acc_dx, ldd);
 }
 
 template <typename T>
@@ -231,7 +211,7 @@ void launch_router_bwd(const T* x, const T* wr, const int32_t* ids, const float*
                        const ChunkMeta& m, cudaStream_t st) {
   if (ntok > 0)
     router_bwd_rows_kernel<T><<<(unsigned)ceil_div64(ntok, 8), 256, 0, st>>>(wr, ids, scores, dscore, ntok, k, h, E,
-                                                                             dlog, nullptr, nullptr, dx, acc_dx);
+                                                                             dlog, nullptr, nullptr, dx, acc_dx, E);
   dim3 grid((unsigned)E, (unsigned)ceil_div64(h, 256));
   router_dw_kernel<T><<<grid, 256, 0, st>>>(x, dlog, m.seg, m.recv_cnt, m.src_of, k, h, dwr, acc_dw);
 }

@@ -278,3 +278,27 @@ class MemFine:
         capi.check(capi.lib().memfine_debug_perm(self.h, chunk, out.ctypes.data_as(C.c_void_p), out.size,
                                                  C.byref(n)), "memfine_debug_perm")
         return out[:n.value]
+
+    def debug_rows(self, chunk: int):
+        """The last call's chunk `chunk`: copy index (i*k + slot) of every expert-major padded row, -1 padding."""
+        import numpy as np
+        n = C.c_int64()
+        capi.check(capi.lib().memfine_debug_rows(self.h, chunk, None, 0, C.byref(n)), "memfine_debug_rows")
+        out = np.zeros(max(1, n.value), dtype=np.int32)
+        capi.check(capi.lib().memfine_debug_rows(self.h, chunk, out.ctypes.data_as(C.c_void_p), out.size,
+                                                 C.byref(n)), "memfine_debug_rows")
+        return out[:n.value]
+
+    def debug_mx(self, chunk: int, which: int):
+        """MXFP8 decisions of the last call's chunk (memfine_debug_mx): (codes uint8 [rows][cols], scale
+        bytes uint8 [rows*cols/32] in the scale-chunk layout with K = cols)."""
+        import numpy as np
+        r, c = C.c_int64(), C.c_int64()
+        capi.check(capi.lib().memfine_debug_mx(self.h, chunk, which, None, None, 0, C.byref(r), C.byref(c)),
+                   "memfine_debug_mx")
+        q = np.zeros(max(1, r.value * c.value), dtype=np.uint8)
+        sf = np.zeros(max(1, r.value * c.value // 32), dtype=np.uint8)
+        capi.check(capi.lib().memfine_debug_mx(self.h, chunk, which, q.ctypes.data_as(C.c_void_p),
+                                               sf.ctypes.data_as(C.c_void_p), q.size, C.byref(r), C.byref(c)),
+                   "memfine_debug_mx")
+        return q[:r.value * c.value].reshape(r.value, c.value), sf[:r.value * c.value // 32]

@@ -119,3 +119,34 @@ def tol(dtype) -> float:
     """BASELINE.json north star: max relative error <= 2e-2 (bf16) / 1e-5 (fp32 mode), read as
     max|got-ref| / max|ref| per tensor (reading R21)."""
     return 2e-2 if dtype == torch.bfloat16 else 1e-5
+
+
+def tile_covering_tokens(src_of, k, rng, stride=1):
+    """Sampled tokens whose copies hit every 128-row m-tile of the expert-major padded layout (src_of:
+    each row's copy index i*k + slot, -1 for padding - memfine_debug_rows), chosen greedily: a tile
+    already hit by an earlier token's other copy takes no new token.  stride > 1: every stride-th tile
+    plus every tile holding an expert segment's last rows (the ragged tails)."""
+    src_of = np.asarray(src_of)
+    tile_of = {}
+    for r in np.nonzero(src_of >= 0)[0]:
+        tile_of[int(src_of[r])] = r // 128
+    ntiles = (len(src_of) + 127) // 128
+    want = set(range(0, ntiles, stride))
+    for t in range(ntiles):       # a tile followed by padding ends a segment
+        blk = src_of[t * 128:(t + 1) * 128]
+        if len(blk) and blk[-1] < 0 and (blk >= 0).any():
+            want.add(t)
+    covered, toks = set(), []
+    for t0 in rng.permutation(np.arange(0, len(src_of), 128)):
+        if t0 // 128 in covered or t0 // 128 not in want:
+            continue
+        live = src_of[t0:t0 + 128]
+        live = live[live >= 0]
+        if not len(live):
+            continue
+        tok = int(rng.choice(live)) // k
+        toks.append(tok)
+        for s in range(k):
+            if tok * k + s in tile_of:
+                covered.add(tile_of[tok * k + s])
+    return np.array(sorted(set(toks)), np.int64)

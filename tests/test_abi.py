@@ -40,9 +40,13 @@ def test_create_fails_loudly_without_gpu(L):
 
 def test_argument_validation(L):
     d = layer.make_dims(16, 64, 64, 4, 2)
-    counts = torch.zeros((1, 1, 4), dtype=torch.int32)
+    counts = torch.zeros((1, 8, 4), dtype=torch.int32)
     b = capi.make_budget(10**9)
     assert layer.plan(counts, d, b)["status"] == 0
+    # the default rule EXACT needs every bin to divide the sub-chunk count; EQ9 does not
+    c1 = torch.zeros((1, 1, 4), dtype=torch.int32)
+    assert layer.plan(c1, d, b)["status"] == capi.ERR_INVALID_ARG
+    assert layer.plan(c1, d, capi.make_budget(10**9, rule=capi.RULE_EQ9))["status"] == 0
     bad = layer.make_dims(16, 60, 64, 4, 2)       # hidden % 64
     assert layer.plan(counts, bad, b)["status"] == capi.ERR_INVALID_ARG
     assert layer.plan(counts, d, capi.make_budget(10**9, bins=(2, 2)))["status"] == capi.ERR_INVALID_ARG
@@ -57,9 +61,11 @@ def test_argument_validation(L):
 
 
 def _both(counts_np, h, g, E, EP, budget, static, other, bins, rule, D_t=2, m_g=1):
+    """rule: the oracle's numbering (0 EQ9, 1 EXACT)."""
     d = layer.make_dims(1, h, g, E, 1, ep_size=EP, dtype=torch.bfloat16 if D_t == 2 else torch.float32)
+    lib_rule = capi.RULE_EQ9 if rule == 0 else capi.RULE_EXACT
     got = layer.plan(torch.from_numpy(counts_np.astype(np.int32)), d,
-                     capi.make_budget(budget, 1.0, static, other, m_g=m_g, bins=bins, rule=rule))
+                     capi.make_budget(budget, 1.0, static, other, m_g=m_g, bins=bins, rule=lib_rule))
     od = oracle.Dims(T=1, h=h, g=g, E=E, k=1, EP=EP)
     st, ref = oracle.plan(counts_np.astype(np.int64), od, budget_bytes=budget, static_bytes=static,
                           other_act_bytes=other, m_g=m_g, D_t=D_t, bins=bins, rule=rule)

@@ -36,6 +36,16 @@ def test_reference_arm_line():
     assert "workload" in line["config"]
 
 
+def test_multi_rank_launcher_reference_arm():
+    """`bench.py --gpus 2` without torchrun re-launches itself under torch.distributed.run (2 ranks on
+    this node, rendezvous on 127.0.0.1); the ranks meet in a gloo group, rank 0 alone works and prints
+    the one line, the other exits 0 - the driver's plain multi-GPU command, exercised on CPU."""
+    line = _run(["--impl", "reference", "--gpus", "2", "--config", "tiny", "--steps", "1", "--warmup", "0",
+                 "--ref-tokens", "4"], timeout=600)
+    assert line["impl"] == "reference" and line["n_gpus"] == 2 and line["value"] > 0
+    assert line["config"]["ep"] == 2
+
+
 @pytest.mark.gpu
 def test_gpu_arm_line_tiny():
     line = _run(["--config", "tiny", "--steps", "3", "--warmup", "3", "--cpu-tokens", "4"], timeout=900)
@@ -45,6 +55,9 @@ def test_gpu_arm_line_tiny():
         assert k in line, k
     assert line["n_gpus"] == 1 and line["steps"] == 3 and line["warmup"] == 3 and line["value"] > 0
     assert line["dtype"] == "bf16" and line["higher_is_better"] is True
+    tuner = line["config"]["tuner"]
+    assert tuner["in_timed_step"] and tuner["rule"].startswith("EXACT")
+    assert tuner["fwd"]["C"] >= 1 and tuner["bwd"]["C"] >= 1
     roof = line["roofline"]
     # the tiny layer is bound by its permute kernels, not the GEMMs
     assert (roof["bound"], roof["unit"]) in (("tensor", "TFLOP/s"), ("hbm", "GB/s"))

@@ -49,7 +49,8 @@ def _worker(rank, world, port, errq):
             allv = [torch.empty_like(vec) for _ in range(world)]
             dist.all_gather(allv, vec)
             assert all(torch.equal(v, vec) for v in allv), "ranks disagree on the plan"
-            st, ro = oracle.plan(counts.numpy().astype(np.int64), od, budget_bytes=budget, static_bytes=1000)
+            st, ro = oracle.plan(counts.numpy().astype(np.int64), od, budget_bytes=budget, static_bytes=1000,
+                                 rule=1)   # the library default, rule EXACT
             assert st == p["status"]
             if st == 0:
                 assert ro["C"] == p["C"] and ro["hot_rank"] == p["hot_rank"] and ro["s_dd_max"] == p["s_dd_max"]

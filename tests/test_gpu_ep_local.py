@@ -57,7 +57,13 @@ def _run_group(EP, C, dtype, transport, xs, dys, routes, wg, wu, wd, T, h, g, E,
                 st.synchronize()
                 ch = counts.cpu()
                 counts_seen[r] = ch.numpy().copy()
-                wsb = max(layer.workspace_bytes(ch, mf.dims, C, capi.FWD), layer.workspace_bytes(ch, mf.dims, C, capi.BWD))
+                # one size on every rank (the fused exchange derives every peer's layout from it): the
+                # largest any rank needs, from the all-gathered counts
+                wsb = 0
+                for rr in range(EP):
+                    dr = layer.make_dims(T, h, g, E, k, ep_size=EP, ep_rank=rr, dtype=dtype, mx=mx, overlap=ov,
+                                         mx_wgrad=mx_wgrad)
+                    wsb = max(wsb, layer.workspace_bytes(ch, dr, C, capi.FWD), layer.workspace_bytes(ch, dr, C, capi.BWD))
                 ws = torch.empty(wsb, dtype=torch.uint8, device=dev)
                 y = mf.moe_fwd(x, ids, w, lwg, lwu, lwd, C, ws, stream=st)
                 kw = {}
@@ -140,11 +146,44 @@ def test_ep_overlap_bit_identical(EP, C):
             np.testing.assert_array_equal(u, v, err_msg=f"rank {r} {name}")
 
 
+def _ep1_mx_reference(EP, C, xs, dys, routes, wg, wu, wd, T, h, g, E, k, mx_wgrad):
+    """The EP group's problem on ONE rank (EP = 1 MX path) with the tokens in chunk-major order - for
+    each chunk j every source rank's tokens [jT/C, (j+1)T/C) in rank order - so that (T % C == 0) the
+    EP = 1 chunk j holds exactly the EP chunk j's copies, each expert's in the EP receive order (src
+    rank, token, slot; reading R3).  Returns per-rank (y, dx, dscore) and all experts' dW."""
+    from tests.test_gpu_mx import _mx_run
+    from tests.harness import Problem
+    assert T % C == 0
+    perm = np.array([r * T + i for j in range(C) for r in range(EP) for i in range(j * T // C, (j + 1) * T // C)])
+    cat = lambda ts: torch.cat(ts)[torch.from_numpy(perm)].contiguous()
+    ids = np.concatenate([r_[0] for r_ in routes])[perm]
+    w = np.concatenate([r_[1] for r_ in routes])[perm]
+    p = Problem(EP * T, h, g, E, k, torch.bfloat16, cat(xs), cat(dys), torch.from_numpy(np.ascontiguousarray(ids)),
+                torch.from_numpy(np.ascontiguousarray(w)), wg, wu, wd)
+    out, _ = _mx_run(p, C, mx_wgrad=mx_wgrad)
+    inv = np.argsort(perm)
+    per_rank = [{key: out[key][inv][r * T:(r + 1) * T] for key in ("y", "dx", "dscore")} for r in range(EP)]
+    return per_rank, out
+
+
+def _check_mx_ep_vs_ep1(results, per_rank, ep1, EP, El):
+    """EP MX == the EP = 1 MX path (itself checked against the oracle in tests/test_gpu_mx.py): the rows
+    travel in bf16 and are quantised on arrival to the same codes, every row and every dW element
+    sees the same operands in the same order - bit for bit, except d_score, whose per-row partials
+    from the dA GEMM's N tiles meet in fp32 atomics of run-dependent order."""
+    for r in range(EP):
+        y, dx, ds, dwg, dwu, dwd = results[r]
+        np.testing.assert_array_equal(y, per_rank[r]["y"], err_msg=f"rank {r} y")
+        np.testing.assert_array_equal(dx, per_rank[r]["dx"], err_msg=f"rank {r} dx")
+        assert rel_err(ds, per_rank[r]["dscore"]) <= 1e-6, r
+        es = slice(r * El, (r + 1) * El)
+        for name, a_ in (("dwg", dwg), ("dwu", dwu), ("dwd", dwd)):
+            np.testing.assert_array_equal(a_, ep1[name][es], err_msg=f"rank {r} {name}")
+
+
 @pytest.mark.parametrize("EP,C", [(2, 1), (2, 3), (4, 2)])
-def test_ep_local_group_mx_matches_mx_oracle(EP, C):
-    """MXFP8 with EP (reading R28): rows travel in bf16, each rank quantises what it received; every
-    rank's Y, dX, d_score and local dW against the oracle's MX layer over all ranks' tokens."""
-    from tests.test_gpu_mx import MX_TOL
+def test_ep_local_group_mx_matches_ep1(EP, C):
+    """MXFP8 with EP (reading R28): rows travel in bf16, each rank quantises what it received."""
     T, h, g, E, k = 300, 256, 384, 8, 2
     El = E // EP
     dtype = torch.bfloat16
@@ -153,29 +192,15 @@ def test_ep_local_group_mx_matches_mx_oracle(EP, C):
     routes = [synth.make_routing(T, E, k, rank=r, zipf_s=1.2, placement="contiguous") for r in range(EP)]
     wg, wu, wd = synth.make_experts(range(E), h, g, dtype=dtype)
     results, _ = _run_group(EP, C, dtype, capi.EP_COPY, xs, dys, routes, wg, wu, wd, T, h, g, E, k, mx=True)
-    d = oracle.Dims(T=T * EP, h=h, g=g, E=E, k=k, in_dtype="bf16")
-    xa = np.concatenate([_bits(x, dtype) for x in xs])
-    dya = np.concatenate([_bits(x, dtype) for x in dys])
-    ida = np.concatenate([r[0] for r in routes])
-    wa = np.concatenate([r[1] for r in routes]).astype(np.float64)
-    W = [_bits(t, dtype) for t in (wg, wu, wd)]
-    wq = oracle.mx_weights(d, *W)
-    y_ref, dx_ref, ds_ref, dwg_ref, dwu_ref, dwd_ref = oracle.moe_mx(d, xa, ida, wa, wq, dy=dya, wd=W[2])
-    for r in range(EP):
-        y, dx, ds, dwg, dwu, dwd = results[r]
-        sl, es = slice(r * T, (r + 1) * T), slice(r * El, (r + 1) * El)
-        errs = {"y": rel_err(y, y_ref[sl]), "dx": rel_err(dx, dx_ref[sl]), "dscore": rel_err(ds, ds_ref[sl]),
-                "dw_gate": rel_err(dwg, dwg_ref[es]), "dw_up": rel_err(dwu, dwu_ref[es]),
-                "dw_down": rel_err(dwd, dwd_ref[es])}
-        assert all(v <= MX_TOL for v in errs.values()), (r, errs)
+    per_rank, ep1 = _ep1_mx_reference(EP, C, xs, dys, routes, wg, wu, wd, T, h, g, E, k, False)
+    _check_mx_ep_vs_ep1(results, per_rank, ep1, EP, El)
 
 
 @pytest.mark.parametrize("EP,C", [(2, 1), (2, 3), (4, 2)])
-def test_ep_local_group_mx_wgrad_matches_oracle(EP, C):
+def test_ep_local_group_mx_wgrad_matches_ep1(EP, C):
     """MXFP8 weight gradients with EP (reading R28c): each rank's K for its local expert e is the
     chunk's copies in (src rank, token, slot) order - the received expert-major layout - quantised
-    columnwise in 32-copy blocks; against the oracle's definition over the EP ranks' chunks."""
-    from tests.test_gpu_mx import MX_TOL
+    columnwise in 32-copy blocks, exactly as the EP = 1 path does on the chunk-major token order."""
     T, h, g, E, k = 300, 256, 384, 8, 2
     El = E // EP
     dtype = torch.bfloat16
@@ -185,29 +210,15 @@ def test_ep_local_group_mx_wgrad_matches_oracle(EP, C):
     wg, wu, wd = synth.make_experts(range(E), h, g, dtype=dtype)
     results, _ = _run_group(EP, C, dtype, capi.EP_COPY, xs, dys, routes, wg, wu, wd, T, h, g, E, k, mx=True,
                             mx_wgrad=True)
-    d = oracle.Dims(T=T, h=h, g=g, E=E, k=k, EP=EP, in_dtype="bf16")
-    xa = np.concatenate([_bits(x, dtype) for x in xs])
-    dya = np.concatenate([_bits(x, dtype) for x in dys])
-    ida = np.concatenate([r[0] for r in routes])
-    wa = np.concatenate([r[1] for r in routes]).astype(np.float64)
-    W = [_bits(t, dtype) for t in (wg, wu, wd)]
-    wq = oracle.mx_weights(d, *W)
-    y_ref, dx_ref, ds_ref, dwg_ref, dwu_ref, dwd_ref = oracle.moe_mx(d, xa, ida, wa, wq, dy=dya, wd=W[2], wgrad_C=C)
-    for r in range(EP):
-        y, dx, ds, dwg, dwu, dwd = results[r]
-        sl, es = slice(r * T, (r + 1) * T), slice(r * El, (r + 1) * El)
-        errs = {"y": rel_err(y, y_ref[sl]), "dx": rel_err(dx, dx_ref[sl]), "dscore": rel_err(ds, ds_ref[sl]),
-                "dw_gate": rel_err(dwg, dwg_ref[es]), "dw_up": rel_err(dwu, dwu_ref[es]),
-                "dw_down": rel_err(dwd, dwd_ref[es])}
-        assert all(v <= MX_TOL for v in errs.values()), (r, errs)
+    per_rank, ep1 = _ep1_mx_reference(EP, C, xs, dys, routes, wg, wu, wd, T, h, g, E, k, True)
+    _check_mx_ep_vs_ep1(results, per_rank, ep1, EP, El)
 
 
 @pytest.mark.parametrize("EP,C,mx_wgrad", [(2, 2, False), (4, 1, False), (2, 3, True)])
-def test_ep_local_group_mx_p2p_matches_oracle(EP, C, mx_wgrad):
+def test_ep_local_group_mx_p2p_matches_ep1(EP, C, mx_wgrad):
     """MXFP8 over the fused peer-memory exchange (EP_P2P): rows pushed in bf16 by the permute kernel
     and quantised on arrival, o / dX rows stored into the sources' buffers by the MX down / dX
-    epilogues; every rank against the oracle's MX layer (and, with MX weight gradients, R28c)."""
-    from tests.test_gpu_mx import MX_TOL
+    epilogues; every rank against the EP = 1 MX path (and, with MX weight gradients, R28c)."""
     T, h, g, E, k = 300, 256, 384, 8, 2
     El = E // EP
     dtype = torch.bfloat16
@@ -217,22 +228,8 @@ def test_ep_local_group_mx_p2p_matches_oracle(EP, C, mx_wgrad):
     wg, wu, wd = synth.make_experts(range(E), h, g, dtype=dtype)
     results, _ = _run_group(EP, C, dtype, capi.EP_P2P, xs, dys, routes, wg, wu, wd, T, h, g, E, k, mx=True,
                             mx_wgrad=mx_wgrad)
-    d = oracle.Dims(T=T, h=h, g=g, E=E, k=k, EP=EP, in_dtype="bf16")
-    xa = np.concatenate([_bits(x, dtype) for x in xs])
-    dya = np.concatenate([_bits(x, dtype) for x in dys])
-    ida = np.concatenate([r[0] for r in routes])
-    wa = np.concatenate([r[1] for r in routes]).astype(np.float64)
-    W = [_bits(t, dtype) for t in (wg, wu, wd)]
-    wq = oracle.mx_weights(d, *W)
-    y_ref, dx_ref, ds_ref, dwg_ref, dwu_ref, dwd_ref = oracle.moe_mx(d, xa, ida, wa, wq, dy=dya, wd=W[2],
-                                                                    wgrad_C=C if mx_wgrad else 0)
-    for r in range(EP):
-        y, dx, ds, dwg, dwu, dwd = results[r]
-        sl, es = slice(r * T, (r + 1) * T), slice(r * El, (r + 1) * El)
-        errs = {"y": rel_err(y, y_ref[sl]), "dx": rel_err(dx, dx_ref[sl]), "dscore": rel_err(ds, ds_ref[sl]),
-                "dw_gate": rel_err(dwg, dwg_ref[es]), "dw_up": rel_err(dwu, dwu_ref[es]),
-                "dw_down": rel_err(dwd, dwd_ref[es])}
-        assert all(v <= MX_TOL for v in errs.values()), (r, errs)
+    per_rank, ep1 = _ep1_mx_reference(EP, C, xs, dys, routes, wg, wu, wd, T, h, g, E, k, mx_wgrad)
+    _check_mx_ep_vs_ep1(results, per_rank, ep1, EP, El)
 
 
 def _oracle_ep(EP, C, dtype, xs, dys, routes, wg, wu, wd, T, h, g, E, k):
@@ -303,3 +300,84 @@ def test_ep8_local_group_matches_oracle(E, C, dtype, transport):
     results, _ = _run_group(EP, C, dtype, transport, xs, dys, routes, wg, wu, wd, T, h, g, E, k)
     refs = _oracle_ep(EP, C, dtype, xs, dys, routes, wg, wu, wd, T, h, g, E, k)
     _check_ranks(results, refs, EP, T, El, tol(dtype))
+
+
+def test_ep_p2p_graph_capture_no_host_sync():
+    """N1: the device-planned P2P exchange - the count all-gather pushed into the peers'
+    sync areas, the chunk tables built on the device, per-peer epoch flags instead of host fences - never
+    waits on the host, so every rank's fwd + bwd captures into a CUDA graph (thread-local capture, all ranks
+    at once) and the replays, run concurrently, reproduce the eager outputs bit for bit (d_score: its
+    atomics)."""
+    EP, C, T, h, g, E, k = 4, 2, 300, 128, 256, 8, 2
+    dtype = torch.bfloat16
+    El = E // EP
+    xs = [synth.make_x(T, h, rank=r, dtype=dtype) for r in range(EP)]
+    dys = [synth.make_dy(T, h, rank=r, dtype=dtype) for r in range(EP)]
+    routes = [synth.make_routing(T, E, k, rank=r, zipf_s=1.2, placement="contiguous") for r in range(EP)]
+    wg, wu, wd = synth.make_experts(range(E), h, g, dtype=dtype)
+    group = layer.LocalGroup(EP)
+    bar = threading.Barrier(EP)
+    res, errors = [None] * EP, []
+
+    def rank_main(r):
+        try:
+            torch.cuda.set_device(0)
+            st = torch.cuda.Stream()
+            dev = "cuda:0"
+            with torch.cuda.stream(st):
+                mf = layer.MemFine(T, h, g, E, k, ep_size=EP, ep_rank=r, dtype=dtype, local_group=group)
+                mf.set_ep_transport(capi.EP_P2P)
+                x, dy = xs[r].to(dev), dys[r].to(dev)
+                ids = torch.from_numpy(routes[r][0]).to(dev)
+                w = torch.from_numpy(routes[r][1]).to(dev)
+                lwg, lwu, lwd = (t[r * El:(r + 1) * El].contiguous().to(dev) for t in (wg, wu, wd))
+                ch = mf.route_counts(ids, nsub=C, stream=st).cpu()
+                wsb = 0
+                for rr in range(EP):
+                    dr = layer.make_dims(T, h, g, E, k, ep_size=EP, ep_rank=rr, dtype=dtype)
+                    wsb = max(wsb, layer.workspace_bytes(ch, dr, C, capi.FWD), layer.workspace_bytes(ch, dr, C, capi.BWD))
+                ws = torch.empty(wsb, dtype=torch.uint8, device=dev)
+                f32 = dict(dtype=torch.float32, device=dev)
+                y, dx = torch.empty_like(x), torch.empty_like(x)
+                gr = [torch.empty(t.shape, **f32) for t in (lwg, lwu, lwd)]
+                ds = torch.empty(w.shape, **f32)
+
+                def step():
+                    mf.moe_fwd(x, ids, w, lwg, lwu, lwd, C, ws, y=y, stream=st)
+                    mf.moe_bwd(dy, x, ids, w, lwg, lwu, lwd, C, ws, dx=dx, dw_gate=gr[0], dw_up=gr[1], dw_down=gr[2],
+                               dscore=ds, stream=st)
+
+                step()                                  # eager: registers the workspace, loads the kernels
+                assert mf.sync(stream=st) == 0
+                ref = [t.clone() for t in (y, dx, *gr, ds)]
+                bar.wait()
+                graph = torch.cuda.CUDAGraph()
+                with torch.cuda.graph(graph, stream=st, capture_error_mode="thread_local"):
+                    step()
+                for t in (y, dx, *gr, ds):
+                    t.fill_(float("nan"))
+                st.synchronize()
+                bar.wait()                              # every rank captured: replay all at once
+                for _ in range(2):
+                    graph.replay()
+                st.synchronize()
+                assert mf.sync(stream=st) == 0
+                res[r] = (ref, [t.clone() for t in (y, dx, *gr, ds)])
+                mf.close()
+        except BaseException:  # noqa: BLE001
+            import traceback
+            errors.append(f"rank {r}: {traceback.format_exc()}")
+            bar.abort()
+
+    ths = [threading.Thread(target=rank_main, args=(r,)) for r in range(EP)]
+    for t in ths:
+        t.start()
+    for t in ths:
+        t.join(timeout=300)
+    group.close()
+    assert not errors, "\n".join(errors)
+    for r in range(EP):
+        ref, got = res[r]
+        for name, a_, b_ in zip(("y", "dx", "dw_gate", "dw_up", "dw_down"), ref[:5], got[:5]):
+            assert torch.equal(a_, b_), f"rank {r} {name}"
+        assert (ref[5] - got[5]).abs().max().item() <= 1e-5 * ref[5].abs().max().item()

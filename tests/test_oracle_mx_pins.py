@@ -114,9 +114,10 @@ def _mxq(v, axis):
 
 
 def test_mx_layer_one_token_brute_force():
+    """Every code decided on the exact value (reading R28): numpy/torch re-derivation of one token."""
     d, x, dy, wg, wu, wd, ids, w = _problem()
     wq = oracle.mx_weights(d, wg, wu, wd)
-    y, dx, ds, *_ = oracle.moe_mx(d, x, ids, w, wq, dy=dy, wd=wd)
+    y, dx, ds, *_, ex = oracle.moe_mx(d, x, ids, w, wq, dy=dy, wd=wd, return_exact=True)
     t = 2
     sig = lambda z: 1 / (1 + np.exp(-z))
     xq = _mxq(x[t], 0)
@@ -126,19 +127,63 @@ def test_mx_layer_one_token_brute_force():
         G = _mxq(wg[e], 1) @ xq                  # W_gate rows blocked along h
         U = _mxq(wu[e], 1) @ xq
         a = G * sig(G) * U
-        o = _mxq(wd[e], 1) @ _mxq(a.astype(np.float32), 0)   # W_down rows and a (as fp32) along g
+        o = _mxq(wd[e], 1) @ _mxq(a, 0)          # W_down rows and a along g
         y_ref += w[t, s] * o
-        bf = lambda v: torch.from_numpy(v).to(torch.bfloat16).to(torch.float64).numpy()
-        G, U = bf(G), bf(U)                      # the dA step reads the recomputed G || U as bf16
-        a = G * sig(G) * U
         u = wd[e].astype(np.float64).T @ dy[t].astype(np.float64)   # dA: BF16 operands, not quantised
         ds_ref[s] = u @ a
         dA = w[t, s] * u
         dG = dA * U * sig(G) * (1 + G * (1 - sig(G)))
         dU = dA * G * sig(G)
-        dx_ref += _mxq(wg[e], 0).T @ _mxq(bf(dG), 0) + _mxq(wu[e], 0).T @ _mxq(bf(dU), 0)   # columns along g
+        dx_ref += _mxq(wg[e], 0).T @ _mxq(dG, 0) + _mxq(wu[e], 0).T @ _mxq(dU, 0)   # columns along g
+        q = t * d.k + s                          # the exact values the oracle reports per copy
+        assert np.abs(ex["a"][q] - a).max() <= 1e-12 * np.abs(a).max()
+        assert np.abs(ex["gu"][q] - np.concatenate([G, U])).max() <= 1e-12 * np.abs(np.concatenate([G, U])).max()
+        assert np.abs(ex["da"][q] - dA).max() <= 1e-12 * np.abs(dA).max()
+        assert np.abs(ex["dgu"][q] - np.concatenate([dG, dU])).max() <= 1e-12 * np.abs(np.concatenate([dG, dU])).max()
     for got, ref in ((y[t], y_ref), (dx[t], dx_ref), (ds[t], ds_ref)):
         assert np.abs(got - ref).max() <= 1e-10 * np.abs(ref).max()
+
+
+def test_mx_fed_own_decisions_change_nothing():
+    """Feeding the oracle's own decisions (its exact values quantised by an independent routine) back
+    in reproduces its outputs: the fed path replaces the quantiser and nothing else."""
+    d, x, dy, wg, wu, wd, ids, w = _problem()
+    wq = oracle.mx_weights(d, wg, wu, wd)
+    ref = oracle.moe_mx(d, x, ids, w, wq, dy=dy, wd=wd, return_exact=True)
+    ex = ref[-1]
+    g = d.g
+    fed = {"a_q": _mxq(ex["a"], 1),
+           "dgu_q": np.concatenate([_mxq(ex["dgu"][:, :g], 1), _mxq(ex["dgu"][:, g:], 1)], axis=1)}
+    got = oracle.moe_mx(d, x, ids, w, wq, dy=dy, wd=wd, fed=fed)
+    for a, b in zip(got, ref[:-1]):
+        assert np.abs(a - b).max() <= 1e-12 * max(1e-300, np.abs(b).max())
+
+
+def test_mx_fed_codes_enter_linearly():
+    """A fed decision moves the output by exactly its own term: perturbing copy q's a by da moves
+    y[token] by w_q W_down^q(e) da; perturbing its dG || dU moves dx[token] by W_gate^q(e)^T ddG +
+    W_up^q(e)^T ddU (the column-quantised weights) - which pins the copy indexing of the fed arrays."""
+    d, x, dy, wg, wu, wd, ids, w = _problem(T=6)
+    wq = oracle.mx_weights(d, wg, wu, wd)
+    ex = oracle.moe_mx(d, x, ids, w, wq, dy=dy, wd=wd, return_exact=True)[-1]
+    g, k = d.g, d.k
+    base = {"a_q": _mxq(ex["a"], 1),
+            "dgu_q": np.concatenate([_mxq(ex["dgu"][:, :g], 1), _mxq(ex["dgu"][:, g:], 1)], axis=1)}
+    y0, dx0, *_ = oracle.moe_mx(d, x, ids, w, wq, dy=dy, wd=wd, fed=base)
+    rng = np.random.default_rng(11)
+    for q in (1, 7, 10):
+        t, e = q // k, ids[q // k, q % k]
+        da, dgu = rng.standard_normal(g), rng.standard_normal(2 * g)
+        fed = {key: v.copy() for key, v in base.items()}
+        fed["a_q"][q] += da
+        fed["dgu_q"][q] += dgu
+        y1, dx1, *_ = oracle.moe_mx(d, x, ids, w, wq, dy=dy, wd=wd, fed=fed)
+        want_y = w[t, q % k] * (wq[2][e] @ da)
+        want_dx = wq[3][e].T @ dgu[:g] + wq[4][e].T @ dgu[g:]
+        assert np.abs((y1 - y0)[t] - want_y).max() <= 1e-10 * np.abs(want_y).max()
+        assert np.abs((dx1 - dx0)[t] - want_dx).max() <= 1e-10 * np.abs(want_dx).max()
+        others = np.arange(d.T) != t
+        assert np.array_equal(y1[others], y0[others]) and np.array_equal(dx1[others], dx0[others])
 
 
 def test_mx_layer_quantisation_error_is_small_but_present():
@@ -166,26 +211,24 @@ def test_mx_wgrad_mode0_equals_exact_dw():
 
 
 def test_mx_wgrad_brute_force():
-    """Independent re-derivation: per copy G, U, dG, dU, a_w as the kernel holds them (numpy, torch
-    float8 / bfloat16 conversions), then per chunk and expert the copies stacked in (token, slot)
+    """Independent re-derivation: per copy the exact G, U, dG, dU, a_w (numpy, torch float8
+    conversion), then per chunk and expert the copies stacked in (token, slot)
     order (reading R3, EP = 1), zero-padded to a multiple of 32 rows, every column quantised per
     32-row block (_mxq along the copies), and dW_gate = dG^T x, dW_up = dU^T x, dW_down = dY^T a_w."""
     T = 80
     d, x, dy, wg, wu, wd, ids, w = _problem(T=T, seed=9)
     wq = oracle.mx_weights(d, wg, wu, wd)
     sig = lambda z: 1 / (1 + np.exp(-z))
-    bf = lambda v: torch.from_numpy(np.asarray(v, np.float64)).to(torch.bfloat16).to(torch.float64).numpy()
-    f32 = lambda v: np.asarray(v, np.float32).astype(np.float64)
     per = {}
     for t in range(T):
         xq = _mxq(x[t], 0)
         for s in range(d.k):
             e = ids[t, s]
-            G, U = bf(_mxq(wg[e], 1) @ xq), bf(_mxq(wu[e], 1) @ xq)   # the recomputed G || U as stored
+            G, U = _mxq(wg[e], 1) @ xq, _mxq(wu[e], 1) @ xq     # exact values (reading R28)
             a = G * sig(G) * U
             u = wd[e].astype(np.float64).T @ dy[t].astype(np.float64)
             dA = w[t, s] * u
-            per[t, s] = (bf(dA * U * sig(G) * (1 + G * (1 - sig(G)))), bf(dA * G * sig(G)), bf(f32(w[t, s] * a)))
+            per[t, s] = (dA * U * sig(G) * (1 + G * (1 - sig(G))), dA * G * sig(G), w[t, s] * a)
     for C in (1, 2):
         ref = [np.zeros((d.E, d.g, d.h)), np.zeros((d.E, d.g, d.h)), np.zeros((d.E, d.h, d.g))]
         for j in range(C):
@@ -233,3 +276,44 @@ def test_mx_token_subset_equals_whole_layer():
     toks = np.array([3, 17, 0, 39, 22])
     ys, dxs, dss = oracle.moe_mx_tokens(d, toks, x, dy, ids, w, wg, wu, wd)
     assert np.array_equal(ys, y[toks]) and np.array_equal(dxs, dx[toks]) and np.array_equal(dss, ds[toks])
+
+
+def test_mx_wgrad_fed_columnwise_codes_enter_linearly():
+    """A fed columnwise dG || dU (a_w) value of copy q moves dW_gate / dW_up (dW_down) of its expert by
+    the outer product with that copy's columnwise-quantised x (dY) row - nothing else moves."""
+    T = 40
+    d, x, dy, wg, wu, wd, ids, w = _problem(T=T, seed=12)
+    wq = oracle.mx_weights(d, wg, wu, wd)
+    g, k = d.g, d.k
+    *_, ex = oracle.moe_mx(d, x, ids, w, wq, dy=dy, wd=wd, return_exact=True)
+    # columnwise decisions of the exact values, blocked as reading R28c says (C = 1, EP = 1)
+    gu_col, aw_col = np.zeros((T * k, 2 * g)), np.zeros((T * k, g))
+    xq_col, yq_col = np.zeros((T * k, d.h)), np.zeros((T * k, d.h))
+    aw = ex["a"] * w.reshape(-1)[:, None]
+    for e in range(d.E):
+        cp = [t * k + s for t in range(T) for s in range(k) if ids[t, s] == e]
+        for b in range(0, len(cp), 32):
+            rows = cp[b:b + 32]
+            pad = lambda m: np.vstack([m, np.zeros((32 - len(rows), m.shape[1]))])
+            gu_col[rows] = _mxq(pad(ex["dgu"][rows]), 0)[:len(rows)]
+            aw_col[rows] = _mxq(pad(aw[rows]), 0)[:len(rows)]
+            xq_col[rows] = _mxq(pad(x[[q // k for q in rows]].astype(np.float64)), 0)[:len(rows)]
+            yq_col[rows] = _mxq(pad(dy[[q // k for q in rows]].astype(np.float64)), 0)[:len(rows)]
+    base = {"dgu_col_q": gu_col, "aw_col_q": aw_col}
+    r0 = oracle.moe_mx(d, x, ids, w, wq, dy=dy, wd=wd, wgrad_C=1, fed=base)
+    own = oracle.moe_mx(d, x, ids, w, wq, dy=dy, wd=wd, wgrad_C=1)
+    for a, b in zip(r0[3:], own[3:]):            # feeding its own decisions back changes nothing
+        assert np.abs(a - b).max() <= 1e-12 * np.abs(b).max()
+    rng = np.random.default_rng(13)
+    q = 9
+    e = ids[q // k, q % k]
+    dgu, daw = rng.standard_normal(2 * g), rng.standard_normal(g)
+    fed = {key: v.copy() for key, v in base.items()}
+    fed["dgu_col_q"][q] += dgu
+    fed["aw_col_q"][q] += daw
+    r1 = oracle.moe_mx(d, x, ids, w, wq, dy=dy, wd=wd, wgrad_C=1, fed=fed)
+    want = (np.outer(dgu[:g], xq_col[q]), np.outer(dgu[g:], xq_col[q]), np.outer(yq_col[q], daw))
+    for got1, got0, wnt in zip(r1[3:], r0[3:], want):
+        diff = got1 - got0
+        assert np.abs(diff[e] - wnt).max() <= 1e-10 * np.abs(wnt).max()
+        assert np.array_equal(np.delete(got1, e, 0), np.delete(got0, e, 0))

@@ -536,3 +536,18 @@ def test_plan_exact_rule_is_minimal(oracle_lib):
             assert fits[i] and not any(fits[:i]) and p["feasible"]
             assert p["s_chunk_max"] == chunk_max(p["C"])
     assert all(v > 0 for v in seen.values()) and clamped > 0
+
+
+def test_moe_backward_experts_equals_whole_layer_slices(oracle_lib):
+    """oracle_moe_backward_experts (the full-size dW checker) returns exactly moe_backward's expert
+    slices (same copies, same canonical order: bit-identical) and its dx / d_score."""
+    rng = np.random.default_rng(31)
+    T, h, g, E, k = 30, 16, 24, 6, 2
+    x, dy, ids, w, wg, wu, wd = rand_problem(rng, T, h, g, E, k, EP=2, dtype="f32")
+    d = Dims(T=T, h=h, g=g, E=E, k=k, EP=2, in_dtype="f32")
+    ref = oracle.moe_backward(d, dy, x, ids, w, wg, wu, wd)
+    sel = [4, 0, 5]
+    got = oracle.moe_backward_experts(d, dy, x, ids, w, wg, wu, wd, sel)
+    assert np.array_equal(got[0], ref[0]) and np.array_equal(got[1], ref[1])
+    for a, b in zip(got[2:], ref[2:]):
+        assert np.array_equal(a, b[sel])
