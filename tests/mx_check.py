@@ -94,8 +94,12 @@ def check_decisions_tol(v_exact, codes, E_gpu, tol, what=""):
     v = np.asarray(v_exact, np.float64)
     amax = np.abs(v).max(axis=1)
     tol = np.asarray(tol, np.float64) + 2.0 ** -20 * amax[:, None]
-    E_lo = scale_exp(np.maximum(np.abs(v) - tol, 0).max(axis=1))
+    lo_amax = np.maximum(np.abs(v) - tol, 0).max(axis=1)
+    # a window reaching 0 admits any smaller scale (the rule's E = 0 for an all-zero block is a convention,
+    # not the limit of small amax)
+    E_lo = np.where(lo_amax > 0, scale_exp(lo_amax), -127)
     E_hi = scale_exp((np.abs(v) + tol).max(axis=1))
+    E_hi = np.where((np.abs(v) + tol).max(axis=1) > 0, E_hi, 0)
     bad_E = (E_gpu < E_lo) | (E_gpu > E_hi)
     assert not bad_E.any(), f"{what}: {int(bad_E.sum())} block scales outside the window"
     sc = np.ldexp(1.0, E_gpu)[:, None]
