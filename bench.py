@@ -391,13 +391,17 @@ def main():
         bwd = layer.workspace_bytes(counts_h, mf.dims, Cb or Cc, capi.BWD)
         return fwd, bwd
 
-    def tune(idss):
+    def tune_on(idss, stream):
         """A3 inside every step, as a training step runs it: counts (A1 + the A2 all-gather), then the
-        device tuner (forward C) and the exact-workspace planner (backward C)."""
-        cnt = mf.route_counts(idss, nsub=8)
-        cf = args.chunks or layer.plan(cnt, mf.dims, budget_f)["C"]
-        cb = args.chunks or layer.plan(cnt, mf.dims, budget_b)["C"]
+        device tuner (forward C) and the exact-workspace planner (backward C), in `stream`'s order (only
+        that stream is synchronised)."""
+        cnt = mf.route_counts(idss, nsub=8, stream=stream)
+        cf = args.chunks or layer.plan(cnt, mf.dims, budget_f, stream=stream)["C"]
+        cb = args.chunks or layer.plan(cnt, mf.dims, budget_b, stream=stream)["C"]
         return cf, cb
+
+    def tune(idss):
+        return tune_on(idss, torch.cuda.current_stream())
 
     def make_step(Cc, ws, Cb=None, tuned=False):
         def step(xx=x, dyy=dy, idss=ids, ww=w):
@@ -530,6 +534,7 @@ def main():
     ins = [tuple(torch.empty_like(t) for t in (x, dy, ids, w)) for _ in range(2)]
     outs = [(y, dx), (torch.empty_like(y), torch.empty_like(dx))]
     cs = torch.cuda.Stream()
+    ts = torch.cuda.Stream()
     comp = torch.cuda.current_stream()
 
     def e2e_run(K):
@@ -545,15 +550,33 @@ def main():
                     dst.copy_(src, non_blocking=True)
                 in_ready[b].record(cs)
 
+        # EP = 1: step i+1's tuner (route_counts + plan) runs on its own stream as soon as its ids have
+        # landed, while step i computes, so the host's wait for C never leaves the GPU idle.  EP > 1: the
+        # count all-gather shares the NCCL communicator with the step's exchanges, so it stays in order
+        # on the compute stream.
+        ahead = world == 1 and not args.fixed_c
+
+        def plan_ahead(b):
+            ts.wait_event(in_ready[b])
+            with torch.cuda.stream(ts):
+                return tune_on(ins[b][2], ts)
+
         h2d(0)
         if K > 1:
             h2d(1)
+        nxt = plan_ahead(0) if ahead else None
         for i in range(K):
             b = i % 2
             comp.wait_event(in_ready[b])
             xx, dyy, idd, ww = ins[b]
             yy, dxx = outs[b]
-            cf, cb = (C_f, C_b) if args.fixed_c else tune(idd)
+            if args.fixed_c:
+                cf, cb = C_f, C_b
+            elif ahead:
+                cf, cb = nxt
+                comp.wait_stream(ts)    # (the counts were read on ts)
+            else:
+                cf, cb = tune(idd)
             mf.moe_fwd(xx, idd, ww, wg, wu, wd, cf, ws, y=yy)
             mf.moe_bwd(dyy, xx, idd, ww, wg, wu, wd, cb, ws, dx=dxx, dw_gate=dwg, dw_up=dwu, dw_down=dwd,
                        dscore=dscore)
@@ -562,6 +585,8 @@ def main():
                 cs.wait_event(done[b])
                 out_h[b][0].copy_(yy, non_blocking=True)
                 out_h[b][1].copy_(dxx, non_blocking=True)
+            if ahead and i + 1 < K:
+                nxt = plan_ahead((i + 1) % 2)
             if i + 2 < K:
                 h2d(b)   # waits (stream order on cs) for the D2H above, which waited for step i
         comp.wait_stream(cs)

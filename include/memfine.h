@@ -254,6 +254,12 @@ memfine_status memfine_m_g(int32_t v, int32_t p, int32_t r_pp, int32_t full_reco
  * D_t = 2 for MEMFINE_BF16, 4 for MEMFINE_FP32. */
 memfine_status memfine_plan(const int32_t* counts, int32_t nsub, const memfine_dims* dims,
                             const memfine_budget* budget, memfine_plan_info* info);
+/* memfine_plan with device counts read in `stream` order: the tuner kernel (or, for MEMFINE_MODEL_IMPL,
+ * the D2H copy of the counts) runs on `stream` and only `stream` is synchronised - the caller's other
+ * streams (e.g. the next step's input copies) keep running.  memfine_plan instead synchronises the whole
+ * device first, because its counts may come from any stream.  Host counts: identical to memfine_plan. */
+memfine_status memfine_plan_stream(const int32_t* counts, int32_t nsub, const memfine_dims* dims,
+                                   const memfine_budget* budget, memfine_plan_info* info, void* stream);
 
 /* Exact workspace bytes the fwd (pass = MEMFINE_FWD) or bwd (MEMFINE_BWD) call
  * needs for this routing and C.  counts_host: int32 [EP][nsub][E] from

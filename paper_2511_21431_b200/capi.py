@@ -19,7 +19,7 @@ FWD, BWD = 0, 1
 
 # Every symbol include/memfine.h declares (checked by tests/test_abi.py).
 SYMBOLS = ("memfine_abi_version", "memfine_status_str", "memfine_nccl_unique_id", "memfine_create",
-           "memfine_destroy", "memfine_local_group_create", "memfine_local_group_destroy", "memfine_create_local", "memfine_set_ep_transport", "memfine_set_comm_sms", "memfine_register_workspace", "memfine_route_counts", "memfine_plan", "memfine_workspace_bytes", "memfine_a2a_plan",
+           "memfine_destroy", "memfine_local_group_create", "memfine_local_group_destroy", "memfine_create_local", "memfine_set_ep_transport", "memfine_set_comm_sms", "memfine_register_workspace", "memfine_route_counts", "memfine_plan", "memfine_plan_stream", "memfine_workspace_bytes", "memfine_a2a_plan",
            "memfine_moe_fwd", "memfine_moe_bwd", "memfine_router_fwd", "memfine_router_bwd", "memfine_sync", "memfine_last_stats",
            "memfine_profile_enable", "memfine_profile_read", "memfine_set_debug", "memfine_debug_perm",
            "memfine_debug_rows", "memfine_debug_mx",
@@ -108,6 +108,7 @@ def lib():
         L.memfine_register_workspace.argtypes = [vp, vp, u64, vp]
         L.memfine_route_counts.argtypes = [vp, vp, i32, vp, vp]
         L.memfine_plan.argtypes = [vp, i32, C.POINTER(Dims), C.POINTER(Budget), C.POINTER(PlanInfo)]
+        L.memfine_plan_stream.argtypes = [vp, i32, C.POINTER(Dims), C.POINTER(Budget), C.POINTER(PlanInfo), vp]
         L.memfine_workspace_bytes.argtypes = [vp, i32, C.POINTER(Dims), i32, i32, C.POINTER(u64)]
         L.memfine_a2a_plan.argtypes = [vp, i32, C.POINTER(Dims), i32, i32, vp, vp, vp, vp]
         L.memfine_moe_fwd.argtypes = [vp, vp, vp, vp, vp, vp, vp, i32, vp, vp, u64, vp]

@@ -1618,32 +1618,26 @@ memfine_status plan_host(const int32_t* counts, int32_t nsub, const memfine_dims
 memfine_status plan_impl(const int32_t* counts_host, int32_t nsub, const memfine_dims* dims,
                          const memfine_budget* budget, memfine_plan_info* info);
 
-memfine_status memfine_plan(const int32_t* counts, int32_t nsub, const memfine_dims* dims, const memfine_budget* budget,
-                            memfine_plan_info* info) {
+// ordered = true: device counts are read in `stream` order and only `stream` is synchronised (the other
+// streams of the caller keep running); false: the whole device is synchronised first (counts may come
+// from any stream).
+memfine_status plan_any(const int32_t* counts, int32_t nsub, const memfine_dims* dims, const memfine_budget* budget,
+                        memfine_plan_info* info, cudaStream_t stream, bool ordered) {
   if (!counts || !info) return MEMFINE_ERR_INVALID_ARG;
   PlanParams p;
   if (int rc = budget_to_params(dims, budget, nsub, &p)) return (memfine_status)rc;
   memset(info, 0, sizeof *info);
-  if (budget->model == MEMFINE_MODEL_IMPL) {
-    if (is_device_ptr(counts)) {
-      std::vector<int32_t> hc((size_t)p.EP * nsub * p.E);
-      cudaDeviceSynchronize();
-      if (cudaMemcpy(hc.data(), counts, hc.size() * sizeof(int32_t), cudaMemcpyDeviceToHost) != cudaSuccess)
-        return MEMFINE_ERR_CUDA;
-      return plan_impl(hc.data(), nsub, dims, budget, info);
-    }
-    return plan_impl(counts, nsub, dims, budget, info);
-  }
-  if (is_device_ptr(counts)) {
-    // A3 on the device: the single-CTA tuner kernel reads the (all-gathered) counts in HBM.  Its result
-    // lands in pinned mapped memory; buffer and stream are kept per host thread and device (a layer
-    // call plans every step).
-    struct PlanCtx { int dev = -1; memfine_plan_info* out_h = nullptr; cudaStream_t st = nullptr; };
-    static thread_local PlanCtx ctx;
+  // per host thread and device: pinned result words and a stream (a layer plans every step)
+  struct PlanCtx { int dev = -1; memfine_plan_info* out_h = nullptr; cudaStream_t st = nullptr;
+                   std::vector<int32_t> hc; int32_t* pin = nullptr; size_t pin_n = 0; };
+  static thread_local PlanCtx ctx;
+  const bool dev_counts = is_device_ptr(counts);
+  if (dev_counts) {
     int dev = 0;
     if (cudaGetDevice(&dev) != cudaSuccess) { cudaGetLastError(); return MEMFINE_ERR_CUDA; }
     if (ctx.dev != dev) {
       if (ctx.out_h) cudaFreeHost(ctx.out_h);
+      if (ctx.pin) cudaFreeHost(ctx.pin);
       if (ctx.st) cudaStreamDestroy(ctx.st);
       ctx = PlanCtx{};
       if (cudaHostAlloc((void**)&ctx.out_h, sizeof(memfine_plan_info) + 16, cudaHostAllocMapped) != cudaSuccess ||
@@ -1653,15 +1647,36 @@ memfine_status memfine_plan(const int32_t* counts, int32_t nsub, const memfine_d
       }
       ctx.dev = dev;
     }
+  }
+  cudaStream_t st = ordered ? stream : ctx.st;
+  if (dev_counts && !ordered) cudaDeviceSynchronize();   // counts may come from any stream of the caller
+  if (budget->model == MEMFINE_MODEL_IMPL) {
+    if (dev_counts) {
+      const size_t n = (size_t)p.EP * nsub * p.E;
+      if (ctx.pin_n < n) {
+        if (ctx.pin) cudaFreeHost(ctx.pin);
+        ctx.pin = nullptr;
+        ctx.pin_n = 0;
+        MF_CUDA_OK(cudaHostAlloc((void**)&ctx.pin, n * sizeof(int32_t), cudaHostAllocDefault));
+        ctx.pin_n = n;
+      }
+      MF_CUDA_OK(cudaMemcpyAsync(ctx.pin, counts, n * sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+      MF_CUDA_OK(cudaStreamSynchronize(st));
+      return plan_impl(ctx.pin, nsub, dims, budget, info);
+    }
+    return plan_impl(counts, nsub, dims, budget, info);
+  }
+  if (dev_counts) {
+    // A3 on the device: the single-CTA tuner kernel reads the (all-gathered) counts in HBM; its result
+    // lands in pinned mapped memory
     memfine_plan_info* out_h = ctx.out_h;
     int* rc_h = (int*)(out_h + 1);
     *rc_h = -1;
     memfine_plan_info* out_d;
     cudaHostGetDevicePointer((void**)&out_d, out_h, 0);
     int* rc_d = (int*)(out_d + 1);
-    cudaDeviceSynchronize();  // counts may come from any stream of the caller
-    const int lrc = launch_plan_kernel(counts, p, out_d, rc_d, ctx.st);
-    cudaError_t e = cudaStreamSynchronize(ctx.st);
+    const int lrc = launch_plan_kernel(counts, p, out_d, rc_d, st);
+    cudaError_t e = cudaStreamSynchronize(st);
     int rc = *rc_h;
     if (lrc || e != cudaSuccess || rc < 0) {   // launch failure: the result words were never written
       cudaGetLastError();
@@ -1671,6 +1686,16 @@ memfine_status memfine_plan(const int32_t* counts, int32_t nsub, const memfine_d
     return (memfine_status)rc;
   }
   return plan_host(counts, nsub, dims, budget, info);
+}
+
+memfine_status memfine_plan(const int32_t* counts, int32_t nsub, const memfine_dims* dims, const memfine_budget* budget,
+                            memfine_plan_info* info) {
+  return plan_any(counts, nsub, dims, budget, info, nullptr, false);
+}
+
+memfine_status memfine_plan_stream(const int32_t* counts, int32_t nsub, const memfine_dims* dims,
+                                   const memfine_budget* budget, memfine_plan_info* info, void* stream) {
+  return plan_any(counts, nsub, dims, budget, info, (cudaStream_t)stream, true);
 }
 
 memfine_status plan_host(const int32_t* counts, int32_t nsub, const memfine_dims* dims, const memfine_budget* budget,

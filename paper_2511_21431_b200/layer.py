@@ -63,11 +63,17 @@ def m_g(v: int, p: int, r_pp: int, full_recompute: bool = False) -> int:
     return int(out.value)
 
 
-def plan(counts: torch.Tensor, dims: capi.Dims, budget: capi.Budget) -> dict:
-    """memfine_plan: counts int32 [EP][nsub][E] on the host (CPU tensor) or the device."""
+def plan(counts: torch.Tensor, dims: capi.Dims, budget: capi.Budget, stream=False) -> dict:
+    """memfine_plan: counts int32 [EP][nsub][E] on the host (CPU tensor) or the device.  stream: False =
+    memfine_plan (synchronises the device); None or a torch stream = memfine_plan_stream on that stream
+    (None: the current stream) - the caller's other streams keep running."""
     assert counts.dtype == torch.int32 and counts.dim() == 3 and counts.is_contiguous()
     info = capi.PlanInfo()
-    st = capi.lib().memfine_plan(_ptr(counts), counts.shape[1], C.byref(dims), C.byref(budget), C.byref(info))
+    if stream is False:
+        st = capi.lib().memfine_plan(_ptr(counts), counts.shape[1], C.byref(dims), C.byref(budget), C.byref(info))
+    else:
+        st = capi.lib().memfine_plan_stream(_ptr(counts), counts.shape[1], C.byref(dims), C.byref(budget),
+                                            C.byref(info), _stream(stream))
     d = info.as_dict()
     d["status"] = int(st)
     return d

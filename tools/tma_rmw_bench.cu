@@ -35,6 +35,33 @@ __global__ void __launch_bounds__(WARPS * 32) rmw_kernel(const __grid_constant__
   const int nbx = COLS / BOX, nby = ROWS / BOX;
   const int64_t nbox = (int64_t)nbx * nby;
   const int64_t gw = (int64_t)blockIdx.x * WARPS + warp, nw = (int64_t)gridDim.x * WARPS;
+  if (MODE == 4) {
+    // red.global.add.v4.f32 from registers (fire-and-forget vector reductions at L2, no smem staging)
+    for (int64_t b = gw; b < nbox; b += nw) {
+      const int bx = (int)(b % nbx), by = (int)(b / nbx);
+#pragma unroll
+      for (int i = 0; i < 8; i++) {
+        const int r = by * BOX + i * 4 + (lane >> 3), c = bx * BOX + (lane & 7) * 4;
+        asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(base + (int64_t)r * COLS + c), "f"(1.f),
+                     "f"(1.f), "f"(1.f), "f"(1.f)
+                     : "memory");
+      }
+    }
+    return;
+  }
+  if (MODE == 5) {
+    // the GEMM epilogue's layout: each lane owns one row and 32 consecutive columns (128 B)
+    for (int64_t b = gw; b < nbox; b += nw) {
+      const int bx = (int)(b % nbx), by = (int)(b / nbx);
+      float* row = base + (int64_t)(by * BOX + lane) * COLS + bx * BOX;
+#pragma unroll
+      for (int i = 0; i < 8; i++)
+        asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(row + 4 * i), "f"(1.f), "f"(1.f), "f"(1.f),
+                     "f"(1.f)
+                     : "memory");
+    }
+    return;
+  }
   if (MODE == 3) {
     // thread read-add-write: each warp takes a box row by row (32 rows x 128 B)
     for (int64_t b = gw; b < nbox; b += nw) {
@@ -64,7 +91,8 @@ __global__ void __launch_bounds__(WARPS * 32) rmw_kernel(const __grid_constant__
     const int bx = (int)(b % nbx), by = (int)(b / nbx);
     const int slot = it % DEPTH;
     uint8_t* s = buf + slot * 4096;
-    if (it >= DEPTH) asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(DEPTH - 1) : "memory");
+    if (MODE == 6) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");   // one box in flight per warp
+    else if (it >= DEPTH) asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(DEPTH - 1) : "memory");
     if (MODE == 2) {
       asm volatile("mbarrier.arrive.expect_tx.shared.b64 _, [%0], %1;" ::"r"(su32(&bars[warp][slot])), "r"(4096));
       asm volatile(
@@ -78,7 +106,7 @@ __global__ void __launch_bounds__(WARPS * 32) rmw_kernel(const __grid_constant__
       phase[slot] ^= 1;
     }
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-    if (MODE == 0)
+    if (MODE == 0 || MODE == 6)
       asm volatile("cp.reduce.async.bulk.tensor.2d.global.shared::cta.add.tile.bulk_group [%0, {%2, %3}], [%1];" ::"l"(
                        &map), "r"(su32(s)), "r"(bx * BOX), "r"(by * BOX)
                    : "memory");
@@ -116,8 +144,9 @@ int main() {
   CK(cudaFuncSetAttribute(rmw_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
   CK(cudaFuncSetAttribute(rmw_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
   CK(cudaFuncSetAttribute(rmw_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-  const char* names[4] = {"reduce", "store", "ldst", "ldg"};
-  const double traffic[4] = {8.0, 4.0, 8.0, 8.0};
+  CK(cudaFuncSetAttribute(rmw_kernel<6>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+  const char* names[7] = {"reduce", "store", "ldst", "ldg", "redv4", "redv4_rowlane", "reduce_depth1"};
+  const double traffic[7] = {8.0, 4.0, 8.0, 8.0, 8.0, 8.0, 8.0};
   cudaEvent_t e0, e1;
   cudaEventCreate(&e0);
   cudaEventCreate(&e1);
@@ -126,13 +155,16 @@ int main() {
   // needs if it shares the GPU with a tensor-bound GEMM)
   const int grids[6] = {nsm, 2 * nsm, 16, 32, 64, 96};
   for (int gi = 0; gi < 6; gi++)
-    for (int m = 0; m < 4; m++) {
+    for (int m = 0; m < 7; m++) {
       auto launch = [&]() {
         const int g = grids[gi];
         if (m == 0) rmw_kernel<0><<<g, WARPS * 32, smem>>>(map, d);
         if (m == 1) rmw_kernel<1><<<g, WARPS * 32, smem>>>(map, d);
         if (m == 2) rmw_kernel<2><<<g, WARPS * 32, smem>>>(map, d);
         if (m == 3) rmw_kernel<3><<<g, WARPS * 32, 0>>>(map, d);
+        if (m == 4) rmw_kernel<4><<<g, WARPS * 32, 0>>>(map, d);
+        if (m == 5) rmw_kernel<5><<<g, WARPS * 32, 0>>>(map, d);
+        if (m == 6) rmw_kernel<6><<<g, WARPS * 32, smem>>>(map, d);
       };
       launch();
       CK(cudaDeviceSynchronize());
