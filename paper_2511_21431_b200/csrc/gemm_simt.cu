@@ -184,4 +184,6 @@ int launch_gemm_simt(const GemmProblem<T>& p, cudaStream_t st) {
 template int launch_gemm_simt<float>(const GemmProblem<float>&, cudaStream_t);
 template int launch_gemm_simt<__nv_bfloat16>(const GemmProblem<__nv_bfloat16>&, cudaStream_t);
 
+const void* kernel_anchor_simt() { return (const void*)gemm_simt_kernel<float, true>; }
+
 }  // namespace memfine

@@ -1701,4 +1701,6 @@ int launch_gemm_sm100(const GemmProblem<__nv_bfloat16>& p, cudaStream_t st) {
 
 int sm100_num_sms() { return sm100::g_num_sms ? sm100::g_num_sms : 148; }
 
+const void* kernel_anchor_sm100() { return (const void*)sm100::gemm_kernel<GK_DOWN, true>; }
+
 }  // namespace memfine

@@ -208,6 +208,13 @@ int launch_gemm_simt(const GemmProblem<T>& p, cudaStream_t st);
 // tcgen05 / TMEM / TMA path (MEMFINE_BF16).  Returns number of launches or <0 on error.
 int launch_gemm_sm100(const GemmProblem<__nv_bfloat16>& p, cudaStream_t st);
 int sm100_num_sms();
+// One kernel of each translation unit (each .cu registers its own module): memfine.cu's preload finds the
+// module of each and loads every function in it (lazy loading vs spinning inter-rank waits).
+const void* kernel_anchor_route();
+const void* kernel_anchor_mx();
+const void* kernel_anchor_router();
+const void* kernel_anchor_simt();
+const void* kernel_anchor_sm100();
 
 // ---------------------------------------------------------------- MXFP8 quantisation (mx.cu)
 // info != null: rows = the chunk's padded rows (0 if skipped), capped at rows_max; else rows_max.

@@ -15,6 +15,7 @@
 
 #include "kernels.h"
 #include <cuda.h>
+#include <cudaTypedefs.h>
 #include "nccl_shim.h"
 
 using namespace memfine;
@@ -1318,8 +1319,52 @@ void begin_call(memfine_handle_s* h, int C, int pass, uint64_t ws_bytes, cudaStr
 // =================================================================================== C ABI
 // Per-handle device state of the device-planned P2P exchange (N1): sync area (zeroed; the "done" flags
 // start at the previous-call marker so the first call's chunk 0 may push), skip flags, counts.
+// Lazy module loading (CUDA_MODULE_LOADING=LAZY, the CUDA 12 default) loads a kernel at its first launch, and a
+// load waits for the kernels already running on the device.  The device-planned P2P exchange has kernels of one
+// rank spin-wait on flags raised by another rank's kernels; in an in-process group a first launch in one rank's
+// thread would wait behind the other rank's spinning kernel, which waits for this rank (measured: 20-60 s stalls
+// until the bounded spin latches an error, in ~half the runs).  So every function of every module of the library
+// is loaded before the first P2P call.  Driver entry points through the runtime (no -lcuda).
+memfine_status preload_all_kernels() {
+  static std::once_flag once;
+  static memfine_status rc = MEMFINE_OK;
+  std::call_once(once, [] {
+    void *p_mod = nullptr, *p_cnt = nullptr, *p_enum = nullptr, *p_load = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    bool ok = cudaGetDriverEntryPoint("cuFuncGetModule", &p_mod, cudaEnableDefault, &q) == cudaSuccess && p_mod &&
+              cudaGetDriverEntryPoint("cuModuleGetFunctionCount", &p_cnt, cudaEnableDefault, &q) == cudaSuccess &&
+              p_cnt && cudaGetDriverEntryPoint("cuModuleEnumerateFunctions", &p_enum, cudaEnableDefault, &q) ==
+              cudaSuccess && p_enum && cudaGetDriverEntryPoint("cuFuncLoad", &p_load, cudaEnableDefault, &q) ==
+              cudaSuccess && p_load;
+    if (!ok) { cudaGetLastError(); rc = MEMFINE_ERR_CUDA; return; }
+    auto get_mod = (PFN_cuFuncGetModule_v11000)p_mod;
+    auto count = (PFN_cuModuleGetFunctionCount_v12040)p_cnt;
+    auto enumerate = (PFN_cuModuleEnumerateFunctions_v12040)p_enum;
+    auto load = (PFN_cuFuncLoad_v12040)p_load;
+    const void* anchors[] = {kernel_anchor_route(), kernel_anchor_mx(), kernel_anchor_router(), kernel_anchor_simt(),
+                             kernel_anchor_sm100()};
+    for (const void* a : anchors) {
+      cudaFunction_t f;
+      CUmodule mod;
+      unsigned n = 0;
+      if (cudaGetFuncBySymbol(&f, a) != cudaSuccess || get_mod(&mod, (CUfunction)f) != CUDA_SUCCESS ||
+          count(&n, mod) != CUDA_SUCCESS) {
+        cudaGetLastError();
+        rc = MEMFINE_ERR_CUDA;
+        return;
+      }
+      std::vector<CUfunction> fs(n);
+      if (n && enumerate(fs.data(), n, mod) != CUDA_SUCCESS) { rc = MEMFINE_ERR_CUDA; return; }
+      for (CUfunction fn : fs)
+        if (load(fn) != CUDA_SUCCESS) { rc = MEMFINE_ERR_CUDA; return; }
+    }
+  });
+  return rc;
+}
+
 memfine_status p2p_alloc_sync(memfine_handle_s* h) {
   const memfine_dims& d = h->d;
+  if (memfine_status rc = preload_all_kernels()) return rc;
   const size_t sb = sync_area_bytes(d.num_experts);
   if (!h->sync_d) {
     MF_CUDA_OK(cudaMalloc((void**)&h->sync_d, sb));
@@ -2065,7 +2110,10 @@ memfine_status memfine_sync(memfine_handle_t h, void* stream) {
   if (!h) return MEMFINE_ERR_INVALID_ARG;
   if (cudaStreamSynchronize((cudaStream_t)stream) != cudaSuccess) { cudaGetLastError(); return MEMFINE_ERR_CUDA; }
   int e = __atomic_exchange_n(h->status_h, 0, __ATOMIC_SEQ_CST);
-  if (e) h->last.device_error = e;
+  if (e) {
+    h->last.device_error = e;
+    fflush(stdout);   // device-side diagnostics (printf of the timed-out waits) before the caller reports
+  }
   // stats: rows per chunk and the workspace high-water they imply
   uint64_t maxpad = 0;
   for (int j = 0; j < h->last.C && j < kMaxSub; j++) {

@@ -206,4 +206,6 @@ void launch_mx_quant_rows(const __nv_bfloat16* src, int64_t ld, int64_t rows_max
 }
 
 
+const void* kernel_anchor_mx() { return (const void*)mx_quant_t_kernel; }
+
 }  // namespace memfine

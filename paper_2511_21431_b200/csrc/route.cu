@@ -2,6 +2,7 @@
 // MACT tuner kernel.  HBM-bound data movement:
 // 16-byte vector loads/stores along contiguous rows, one warp per routed copy / token.
 #include <algorithm>
+#include <cstdio>
 #include <type_traits>
 #include "kernels.h"
 
@@ -959,6 +960,9 @@ __global__ void sync_wait_kernel(uint64_t* area, int EP, int me, int phase, int 
   const uint64_t t0 = globaltimer();
   while (ld_acquire_sys(f) < target) {
     if (globaltimer() - t0 > 20000000000ull) {   // 20 s: a peer never arrived - latch, do not hang
+      printf("memfine: rank %d timed out waiting for rank %d, phase %d: flag %llu < target %llu (epoch %llu)\n", me,
+             p, phase, (unsigned long long)ld_acquire_sys(f), (unsigned long long)target,
+             (unsigned long long)area[0]);
       latch_error(status, MEMFINE_ERR_CUDA);
       return;
     }
@@ -1171,5 +1175,7 @@ template void launch_unpermute_reduce<__nv_bfloat16>(const __nv_bfloat16*, int64
                                                      const ChunkMeta&, __nv_bfloat16*, float*, cudaStream_t);
 template void launch_unpermute_reduce<float>(const float*, int64_t, int64_t, int, int, const ChunkMeta&, float*,
                                              float*, cudaStream_t);
+
+const void* kernel_anchor_route() { return (const void*)sync_wait_kernel; }
 
 }  // namespace memfine

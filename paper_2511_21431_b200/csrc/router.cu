@@ -227,4 +227,6 @@ template void launch_router_bwd<float>(const float*, const float*, const int32_t
                                        int, int, int, float*, float*, int, float*, int, const ChunkMeta&,
                                        cudaStream_t);
 
+const void* kernel_anchor_router() { return (const void*)router_topk_kernel; }
+
 }  // namespace memfine
