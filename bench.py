@@ -43,6 +43,30 @@ FLOP_COEF = {"gemm_gateup_swiglu": 8, "gemm_down": 2, "gemm_dact_epilogue": 2, "
              "gemm_wgrad_down": 2, "gemm_wgrad_gateup": 4}
 
 
+def paper_context(per_C, peak_gb):
+    """The paper's headline numbers with the hardware it states (context, not the target), beside this run's
+    analogues: Method 1 = no chunking (C = 1; the expert activations are recomputed in the backward either way),
+    Method 2 = fixed c_k = 8, MACT's c_k = 2 (what MACT picked for both of the paper's models, Table 4)."""
+    paper = {"activation_reduction_pct": 48.03, "throughput_vs_method1_pct": 4.42,
+             "method2_vs_method1_pct": -5.40, "method3_vs_method2_pct_model1": 18.26,
+             "setup": "32 GPUs with 64 GB each (model unnamed), two reduced-layer DeepSeek-V3-based models, "
+                      "t=1 p=4 e=32, BF16, Megatron-LM (PAPER.md:209, 232, 238)"}
+    this = {}
+    try:
+        ms = {int(c): v["ms_per_step"] for c, v in per_C.items() if "ms_per_step" in v}
+        if 1 in ms and 2 in ms:
+            this["activation_reduction_pct_c2"] = 100.0 * (1.0 - peak_gb(2) / peak_gb(1))
+            this["throughput_c2_vs_c1_pct"] = 100.0 * (ms[1] / ms[2] - 1.0)
+        if 1 in ms and 8 in ms:
+            this["activation_reduction_pct_c8"] = 100.0 * (1.0 - peak_gb(8) / peak_gb(1))
+            this["throughput_c8_vs_c1_pct"] = 100.0 * (ms[1] / ms[8] - 1.0)
+        if 2 in ms and 8 in ms:
+            this["throughput_c2_vs_c8_pct"] = 100.0 * (ms[8] / ms[2] - 1.0)
+    except Exception as ex:  # noqa: BLE001
+        this = {"error": f"{type(ex).__name__}: {ex}"[:200]}
+    return {"paper": paper, "this_run": this}
+
+
 def load_traffic():
     """DRAM bytes per launch per kernel class from the committed ncu capture (tools/ncu_traffic.py)."""
     import glob
@@ -714,6 +738,7 @@ def main():
                 "d2h_bytes_per_step": d2h, "ms_per_step": ms_e2e},
         "gpu_launches": launches_fwd_bwd * args.steps,
         "variants": variants,
+        "paper_context": paper_context(per_C, peak_gb),
     }
     if world == 1 and not args.no_cpu_baseline:
         try:

@@ -1,19 +1,22 @@
 // gemm_sm100.cu — grouped expert GEMMs on the 5th-generation tensor cores (sm_100a).
 //
 // One persistent, warp-specialised kernel template serves the six expert GEMMs of the
-// chunked MoE layer.  Per CTA (one per SM, 192 threads):
+// chunked MoE layer.  Per CTA (one per SM, 320 threads = 10 warps):
 //   warp 0      TMA producer: cp.async.bulk.tensor 2D/3D loads, 128B swizzle, mbarrier tx
-//   warp 1      TMEM allocator + MMA issuer: tcgen05.mma.cta_group::1.kind::f16, BF16 in,
-//               FP32 accumulators in TMEM, tcgen05.commit -> mbarriers
+//   warp 1      TMEM allocator + MMA issuer: tcgen05.mma (BF16 kind::f16 or MXFP8
+//               kind::mxf8f6f4.block_scale), FP32 accumulators in TMEM, tcgen05.commit -> mbarriers
 //   warps 2..9  epilogue: tcgen05.ld 32x32b -> registers -> fused MoE epilogue -> global;
 //               two warps per TMEM lane quarter (warp % 4), each taking half of the columns
-// A 4-stage smem ring (48 KB/stage) feeds the MMA; two TMEM accumulator stages (512 cols)
-// let the epilogue of tile i overlap the mainloop of tile i+1.
+// Default tiles are 256 x 256 per 2-CTA cluster (tcgen05.mma.cta_group::2, M = 256, issued by the
+// even CTA; each CTA stages its 128 A rows and half of B): 32 KB per stage per CTA, as many stages as
+// fit next to the epilogue staging (up to 6; nstage()).  Two TMEM accumulator stages (2 x 256 columns)
+// let the epilogue of tile i overlap the mainloop of tile i+1 (MXFP8 N = 256: one stage + scale
+// columns, drained early into registers).  MEMFINE_GEMM_CTA=1: 1-CTA 128 x 256 tiles (cta_group::1).
 //
 // Rows are the expert-major padded layout (every local expert's segment padded to 128
 // rows), so an M tile never straddles experts and the weight-gradient K loop (over tokens)
-// never straddles either; padded rows are zero.  Tile order is grouped (8 M tiles x all N
-// tiles) so the weights and activations a wave touches stay in the 126 MB L2.
+// never straddles either; padded rows are zero.  Tile order is grouped (group_m M tiles x all N
+// tiles, group_m sized per kind so the group's A strips fit an L2 budget).
 #include <cuda.h>
 #include <cudaTypedefs.h>
 #include <mutex>

@@ -69,6 +69,9 @@ def test_gpu_arm_line_tiny():
     assert e2e["value"] > 0 and e2e["h2d_bytes_per_step"] > 0 and e2e["d2h_bytes_per_step"] > 0
     assert line["gpu_launches"] > 0
     assert line["cpu_baseline"]["kind"] == "oracle"
+    pc = line["paper_context"]   # the paper's numbers with its hardware, beside this run's analogues
+    assert pc["paper"]["activation_reduction_pct"] == 48.03 and pc["paper"]["throughput_vs_method1_pct"] == 4.42
+    assert "activation_reduction_pct_c2" in pc["this_run"]
     # chunking: the peak activation falls with C (Table 2 rows 11-13 live for one chunk only)
     peaks = [line["per_C"][c]["peak_act_gb"] for c in sorted(line["per_C"], key=int)]
     assert all(a >= b for a, b in zip(peaks, peaks[1:]))
