@@ -549,30 +549,36 @@ def main():
 
     # ---------------------------------------------------------------- e2e through the public API
     # Every step copies its inputs (x, dY, ids, scores) host->device from pinned memory and reads
-    # its results (y, dX) device->host, inside the timed region.  Copies run on a second stream,
-    # double-buffered: step i+1's inputs and step i-1's results move while step i computes.
+    # its results (y, dX) device->host, inside the timed region.  Inputs and results are double-buffered
+    # and move on two copy streams (one per direction: the H2D and D2H copy engines run concurrently):
+    # step i+2's inputs land and step i's results leave while step i+1 computes.
     pin = lambda t: t.pin_memory()
     xh, dyh, idsh, wh = pin(x_h), pin(dy_h), pin(ids_h), pin(w_h)
     out_h = [(torch.empty(y.shape, dtype=y.dtype).pin_memory(), torch.empty(dx.shape, dtype=dx.dtype).pin_memory())
              for _ in range(2)]
     ins = [tuple(torch.empty_like(t) for t in (x, dy, ids, w)) for _ in range(2)]
     outs = [(y, dx), (torch.empty_like(y), torch.empty_like(dx))]
-    cs = torch.cuda.Stream()
+    cs_in = torch.cuda.Stream()    # H2D
+    cs_out = torch.cuda.Stream()   # D2H
     ts = torch.cuda.Stream()
     comp = torch.cuda.current_stream()
 
     def e2e_run(K):
-        in_ready = [torch.cuda.Event() for _ in range(2)]
-        done = [torch.cuda.Event() for _ in range(2)]
+        in_ready = [torch.cuda.Event() for _ in range(2)]    # buffer b's inputs landed
+        done = [torch.cuda.Event() for _ in range(2)]        # the step using buffer b finished
+        out_read = [torch.cuda.Event() for _ in range(2)]    # buffer b's results left the device
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(comp)
-        cs.wait_stream(comp)
+        cs_in.wait_stream(comp)
+        cs_out.wait_stream(comp)
 
-        def h2d(b):
-            with torch.cuda.stream(cs):
+        def h2d(b, after=None):
+            with torch.cuda.stream(cs_in):
+                if after is not None:
+                    cs_in.wait_event(after)   # the step that read ins[b] before has finished
                 for dst, src in zip(ins[b], (xh, dyh, idsh, wh)):
                     dst.copy_(src, non_blocking=True)
-                in_ready[b].record(cs)
+                in_ready[b].record(cs_in)
 
         # EP = 1: step i+1's tuner (route_counts + plan) runs on its own stream as soon as its ids have
         # landed, while step i computes, so the host's wait for C never leaves the GPU idle.  EP > 1: the
@@ -592,6 +598,8 @@ def main():
         for i in range(K):
             b = i % 2
             comp.wait_event(in_ready[b])
+            if i >= 2:
+                comp.wait_event(out_read[b])   # step i-2's results have left outs[b]
             xx, dyy, idd, ww = ins[b]
             yy, dxx = outs[b]
             if args.fixed_c:
@@ -605,15 +613,17 @@ def main():
             mf.moe_bwd(dyy, xx, idd, ww, wg, wu, wd, cb, ws, dx=dxx, dw_gate=dwg, dw_up=dwu, dw_down=dwd,
                        dscore=dscore)
             done[b].record(comp)
-            with torch.cuda.stream(cs):
-                cs.wait_event(done[b])
+            with torch.cuda.stream(cs_out):
+                cs_out.wait_event(done[b])
                 out_h[b][0].copy_(yy, non_blocking=True)
                 out_h[b][1].copy_(dxx, non_blocking=True)
+                out_read[b].record(cs_out)
+            if i + 2 < K:
+                h2d(b, after=done[b])
             if ahead and i + 1 < K:
                 nxt = plan_ahead((i + 1) % 2)
-            if i + 2 < K:
-                h2d(b)   # waits (stream order on cs) for the D2H above, which waited for step i
-        comp.wait_stream(cs)
+        comp.wait_stream(cs_out)
+        comp.wait_stream(cs_in)
         e1.record(comp)
         torch.cuda.synchronize()
         return e0.elapsed_time(e1) / K
