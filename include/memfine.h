@@ -204,8 +204,9 @@ memfine_status memfine_create_local(const memfine_dims* dims, memfine_group_t gr
  *    buffer, and the down / dX GEMM epilogues store each output row straight into its source
  *    rank's combine buffer as the tile is produced; ranks fence with events (in-process group).
  *    ep_size <= 16.  In-process groups map peers directly; across processes (NCCL handles) the
- *    workspace must first be registered with memfine_register_workspace, and ranks fence with a
- *    one-int NCCL all-reduce on the stream.
+ *    workspace must first be registered with memfine_register_workspace (or, without NCCL, exported
+ *    and imported: memfine_create_ipc), and ranks fence with epoch-stamped per-peer flags in each
+ *    other's sync areas, waited on by device kernels (no host synchronisation inside a call).
  * The workspace layout and size are the same for both.  MEMFINE_EP_P2P on a handle created with
  * MEMFINE_FLAG_OVERLAP returns MEMFINE_ERR_INVALID_ARG (the two-slot pipeline is the copy
  * transport's; memfine_workspace_bytes sizes it from the dims alone). */
@@ -224,6 +225,28 @@ memfine_status memfine_set_comm_sms(memfine_handle_t h, int32_t n);
  * same ws (MEMFINE_ERR_INVALID_ARG otherwise).  For in-process groups and ep_size == 1 it only
  * records ws.  Synchronises `stream`. */
 memfine_status memfine_register_workspace(memfine_handle_t h, void* ws, uint64_t ws_bytes, void* stream);
+
+/* N1 across processes WITHOUT NCCL (EP data flow PAPER.md:30, the count exchange
+ * PAPER.md:200): an expert-parallel handle whose only transport is the device-planned peer-memory
+ * exchange (MEMFINE_EP_P2P), for ranks in separate processes that exchange their workspace mappings
+ * through the caller's own channel (e.g. torch.distributed over gloo) - two processes sharing one
+ * device included.  dims->ep_size in [2, 16]; flags without MEMFINE_FLAG_EP_PATH / MEMFINE_FLAG_OVERLAP.
+ * memfine_route_counts on such a handle fills only this rank's rows of counts_dev (the caller
+ * all-gathers them to size the workspace); the layer calls themselves need no host collective (the
+ * counts travel through the peers' sync areas).  memfine_set_ep_transport accepts MEMFINE_EP_P2P only. */
+memfine_status memfine_create_ipc(const memfine_dims* dims, memfine_handle_t* out);
+#define MEMFINE_IPC_RECORD_BYTES 256
+/* This rank's mapping record (MEMFINE_IPC_RECORD_BYTES bytes, opaque: CUDA IPC handles of the allocation
+ * holding ws and of the handle's sync area, ws's offset and ws_bytes) written to `record`; allocates and
+ * initialises the sync area and loads every kernel of the library (a first launch must not wait behind a
+ * peer's spinning kernel).  Synchronises the device.  Every rank must pass the same ws_bytes. */
+memfine_status memfine_ipc_export(memfine_handle_t h, void* ws, uint64_t ws_bytes, uint8_t* record);
+/* Map every peer's workspace and sync area from the ep_size records (rank order, record r at
+ * records + r * MEMFINE_IPC_RECORD_BYTES; this rank's own must come from memfine_ipc_export on this
+ * handle).  The caller runs a host barrier after every rank's import and before the first layer call;
+ * fwd / bwd must then pass the exported ws and ws_bytes.  MEMFINE_ERR_INVALID_ARG if the ranks' ws_bytes
+ * differ or this rank did not export; MEMFINE_ERR_CUDA if a mapping fails. */
+memfine_status memfine_ipc_import(memfine_handle_t h, const uint8_t* records);
 
 /* A1 + A2: per-sub-chunk expert histogram of this rank's routing,
  * then the all-gather of every rank's histogram ("the first notification",

@@ -16,10 +16,11 @@ MODEL_PAPER, MODEL_IMPL = 0, 1
 EP_COPY, EP_P2P = 0, 1
 FLAG_OVERLAP, FLAG_EP_PATH, FLAG_MX_WGRAD = 1, 2, 4
 FWD, BWD = 0, 1
+IPC_RECORD_BYTES = 256   # MEMFINE_IPC_RECORD_BYTES
 
 # Every symbol include/memfine.h declares (checked by tests/test_abi.py).
 SYMBOLS = ("memfine_abi_version", "memfine_status_str", "memfine_nccl_unique_id", "memfine_create",
-           "memfine_destroy", "memfine_local_group_create", "memfine_local_group_destroy", "memfine_create_local", "memfine_set_ep_transport", "memfine_set_comm_sms", "memfine_register_workspace", "memfine_route_counts", "memfine_plan", "memfine_plan_stream", "memfine_workspace_bytes", "memfine_a2a_plan",
+           "memfine_destroy", "memfine_local_group_create", "memfine_local_group_destroy", "memfine_create_local", "memfine_create_ipc", "memfine_ipc_export", "memfine_ipc_import", "memfine_set_ep_transport", "memfine_set_comm_sms", "memfine_register_workspace", "memfine_route_counts", "memfine_plan", "memfine_plan_stream", "memfine_workspace_bytes", "memfine_a2a_plan",
            "memfine_moe_fwd", "memfine_moe_bwd", "memfine_router_fwd", "memfine_router_bwd", "memfine_sync", "memfine_last_stats",
            "memfine_profile_enable", "memfine_profile_read", "memfine_set_debug", "memfine_debug_perm",
            "memfine_debug_rows", "memfine_debug_mx",
@@ -106,6 +107,9 @@ def lib():
         L.memfine_set_ep_transport.argtypes = [vp, i32]
         L.memfine_set_comm_sms.argtypes = [vp, i32]
         L.memfine_register_workspace.argtypes = [vp, vp, u64, vp]
+        L.memfine_create_ipc.argtypes = [C.POINTER(Dims), C.POINTER(vp)]
+        L.memfine_ipc_export.argtypes = [vp, vp, u64, vp]
+        L.memfine_ipc_import.argtypes = [vp, vp]
         L.memfine_route_counts.argtypes = [vp, vp, i32, vp, vp]
         L.memfine_plan.argtypes = [vp, i32, C.POINTER(Dims), C.POINTER(Budget), C.POINTER(PlanInfo)]
         L.memfine_plan_stream.argtypes = [vp, i32, C.POINTER(Dims), C.POINTER(Budget), C.POINTER(PlanInfo), vp]

@@ -50,6 +50,9 @@ struct memfine_handle_s {
   memfine_dims d;
   memfine_group_s* lg = nullptr;   // in-process EP group (instead of NCCL)
   int p2p = 0;                     // fused exchange over peer memory (MEMFINE_EP_P2P)
+  int ipc_only = 0;                // memfine_create_ipc: no NCCL; mappings via memfine_ipc_export / _import
+  void* exp_ws = nullptr;          // memfine_ipc_export: the exported workspace
+  uint64_t exp_bytes = 0;
   // P2P (N1, device-planned): the registered workspace and sync area of every rank (own entries local;
   // in-process peers directly, other processes through CUDA IPC), the all-gathered counts and the
   // per-chunk global skip flags
@@ -1527,6 +1530,7 @@ memfine_status memfine_set_comm_sms(memfine_handle_t h, int32_t n) {
 memfine_status memfine_set_ep_transport(memfine_handle_t h, int32_t transport) {
   if (!h || (transport != MEMFINE_EP_COPY && transport != MEMFINE_EP_P2P)) return MEMFINE_ERR_INVALID_ARG;
   if (transport == MEMFINE_EP_P2P && h->d.ep_size > kMaxPeers) return MEMFINE_ERR_UNSUPPORTED;
+  if (h->ipc_only) return transport == MEMFINE_EP_P2P ? MEMFINE_OK : MEMFINE_ERR_UNSUPPORTED;   // no NCCL
   if (transport == MEMFINE_EP_P2P && !h->lg && h->d.ep_size > 1 && !h->comm.comm) return MEMFINE_ERR_UNSUPPORTED;
   // the two-slot chunk pipeline (and its workspace layout, which memfine_workspace_bytes derives from the
   // dims alone) belongs to the copy transport
@@ -1537,17 +1541,15 @@ memfine_status memfine_set_ep_transport(memfine_handle_t h, int32_t transport) {
 
 // Multi-process P2P: export the allocation holding ws (base + offset) through CUDA IPC, all-gather
 // the records over the handle's NCCL communicator, open every peer's mapping.
-memfine_status memfine_register_workspace(memfine_handle_t h, void* ws, uint64_t ws_bytes, void* stream) {
-  if (!h || !ws) return MEMFINE_ERR_INVALID_ARG;
-  if (h->lg) return register_local(h, ws, ws_bytes);
-  if (!ep_path(h->d)) {   // a single rank without the EP path: nothing to map
-    h->reg_ws = ws;
-    h->reg_bytes = ws_bytes;
-    return MEMFINE_OK;
-  }
-  if (!h->comm.comm) return MEMFINE_ERR_NCCL;
+// CUDA IPC mapping record of one rank (memfine_ipc_export / memfine_register_workspace)
+struct IpcRec {
+  cudaIpcMemHandle_t hdl, sync;
+  uint64_t offset, bytes;
+};
+static_assert(sizeof(IpcRec) <= MEMFINE_IPC_RECORD_BYTES, "record");
+
+memfine_status ipc_export_rec(memfine_handle_s* h, void* ws, uint64_t ws_bytes, IpcRec* out) {
   if (memfine_status rc = p2p_alloc_sync(h)) return rc;
-  cudaStream_t st = (cudaStream_t)stream;
   // allocation base of ws
   typedef CUresult (*RangeFn)(CUdeviceptr*, size_t*, CUdeviceptr);
   static RangeFn range_fn = nullptr;
@@ -1562,33 +1564,29 @@ memfine_status memfine_register_workspace(memfine_handle_t h, void* ws, uint64_t
   CUdeviceptr base = 0;
   size_t size = 0;
   if (range_fn(&base, &size, (CUdeviceptr)ws) != CUDA_SUCCESS) return MEMFINE_ERR_CUDA;
-  struct Rec { cudaIpcMemHandle_t hdl, sync; uint64_t offset, bytes; };
-  Rec mine{};
-  if (cudaIpcGetMemHandle(&mine.hdl, (void*)base) != cudaSuccess ||
-      cudaIpcGetMemHandle(&mine.sync, (void*)h->sync_d) != cudaSuccess) {
+  memset(out, 0, sizeof *out);
+  if (cudaIpcGetMemHandle(&out->hdl, (void*)base) != cudaSuccess ||
+      cudaIpcGetMemHandle(&out->sync, (void*)h->sync_d) != cudaSuccess) {
     cudaGetLastError();
     return MEMFINE_ERR_CUDA;
   }
-  mine.offset = (uint64_t)((char*)ws - (char*)base);
-  mine.bytes = ws_bytes;
+  out->offset = (uint64_t)((char*)ws - (char*)base);
+  out->bytes = ws_bytes;
+  return MEMFINE_OK;
+}
+
+// map every peer's workspace and sync area (all[r], rank order); this rank's entries stay local
+memfine_status ipc_import_recs(memfine_handle_s* h, const IpcRec* all, void* ws, uint64_t ws_bytes) {
   const int EP = h->d.ep_size, me = h->d.ep_rank;
-  char* dbuf = nullptr;
-  MF_CUDA_OK(cudaMalloc((void**)&dbuf, sizeof(Rec) * (EP + 1)));
-  MF_CUDA_OK(cudaMemcpyAsync(dbuf + sizeof(Rec) * EP, &mine, sizeof(Rec), cudaMemcpyHostToDevice, st));
-  if (nccl_all_gather_bytes(&h->comm, dbuf + sizeof(Rec) * EP, dbuf, sizeof(Rec), st)) {
-    cudaFree(dbuf);
-    return MEMFINE_ERR_NCCL;
-  }
-  std::vector<Rec> all(EP);
-  cudaMemcpyAsync(all.data(), dbuf, sizeof(Rec) * EP, cudaMemcpyDeviceToHost, st);
-  cudaStreamSynchronize(st);
-  cudaFree(dbuf);
   for (void* b : h->ipc_bases) cudaIpcCloseMemHandle(b);
   h->ipc_bases.clear();
   h->peer_ws.assign(EP, nullptr);
   h->peer_sync.assign(EP, nullptr);
-  for (int r = 0; r < EP; r++) {
+  h->reg_ws = nullptr;
+  h->reg_bytes = 0;
+  for (int r = 0; r < EP; r++)
     if (all[r].bytes != ws_bytes) return MEMFINE_ERR_INVALID_ARG;   // one workspace size on every rank
+  for (int r = 0; r < EP; r++) {
     if (r == me) {
       h->peer_ws[r] = (char*)ws;
       h->peer_sync[r] = h->sync_d;
@@ -1606,12 +1604,75 @@ memfine_status memfine_register_workspace(memfine_handle_t h, void* ws, uint64_t
     h->peer_ws[r] = (char*)pb + all[r].offset;
     h->peer_sync[r] = (uint64_t*)ps;
   }
-  // every rank has opened every mapping and initialised its flags before anyone signals
-  if (nccl_stream_barrier(&h->comm, h->gskip_d, st)) return MEMFINE_ERR_NCCL;
-  MF_CUDA_OK(cudaStreamSynchronize(st));
   h->reg_ws = ws;
   h->reg_bytes = ws_bytes;
   return MEMFINE_OK;
+}
+
+memfine_status memfine_register_workspace(memfine_handle_t h, void* ws, uint64_t ws_bytes, void* stream) {
+  if (!h || !ws) return MEMFINE_ERR_INVALID_ARG;
+  if (h->lg) return register_local(h, ws, ws_bytes);
+  if (h->ipc_only) return MEMFINE_ERR_INVALID_ARG;   // memfine_ipc_export / memfine_ipc_import
+  if (!ep_path(h->d)) {   // a single rank without the EP path: nothing to map
+    h->reg_ws = ws;
+    h->reg_bytes = ws_bytes;
+    return MEMFINE_OK;
+  }
+  if (!h->comm.comm) return MEMFINE_ERR_NCCL;
+  cudaStream_t st = (cudaStream_t)stream;
+  IpcRec mine;
+  if (memfine_status rc = ipc_export_rec(h, ws, ws_bytes, &mine)) return rc;
+  const int EP = h->d.ep_size;
+  char* dbuf = nullptr;
+  MF_CUDA_OK(cudaMalloc((void**)&dbuf, sizeof(IpcRec) * (EP + 1)));
+  MF_CUDA_OK(cudaMemcpyAsync(dbuf + sizeof(IpcRec) * EP, &mine, sizeof(IpcRec), cudaMemcpyHostToDevice, st));
+  if (nccl_all_gather_bytes(&h->comm, dbuf + sizeof(IpcRec) * EP, dbuf, sizeof(IpcRec), st)) {
+    cudaFree(dbuf);
+    return MEMFINE_ERR_NCCL;
+  }
+  std::vector<IpcRec> all(EP);
+  cudaMemcpyAsync(all.data(), dbuf, sizeof(IpcRec) * EP, cudaMemcpyDeviceToHost, st);
+  cudaStreamSynchronize(st);
+  cudaFree(dbuf);
+  if (memfine_status rc = ipc_import_recs(h, all.data(), ws, ws_bytes)) return rc;
+  // every rank has opened every mapping and initialised its flags before anyone signals
+  if (nccl_stream_barrier(&h->comm, h->gskip_d, st)) return MEMFINE_ERR_NCCL;
+  MF_CUDA_OK(cudaStreamSynchronize(st));
+  return MEMFINE_OK;
+}
+
+memfine_status memfine_create_ipc(const memfine_dims* dims, memfine_handle_t* out) {
+  if (!out || !dims || !dims_ok(dims)) return MEMFINE_ERR_INVALID_ARG;
+  if (dims->ep_size < 2 || dims->ep_size > kMaxPeers) return MEMFINE_ERR_INVALID_ARG;
+  if (dims->flags & (MEMFINE_FLAG_EP_PATH | MEMFINE_FLAG_OVERLAP)) return MEMFINE_ERR_INVALID_ARG;
+  memfine_dims d1 = *dims;
+  d1.ep_size = 1;   // create with the single-rank path (no communicator), then switch to the EP layout
+  d1.ep_rank = 0;
+  memfine_status st = memfine_create(&d1, nullptr, out);
+  if (st != MEMFINE_OK) return st;
+  (*out)->d.ep_size = dims->ep_size;
+  (*out)->d.ep_rank = dims->ep_rank;
+  (*out)->ipc_only = 1;
+  (*out)->p2p = 1;
+  return MEMFINE_OK;
+}
+
+memfine_status memfine_ipc_export(memfine_handle_t h, void* ws, uint64_t ws_bytes, uint8_t* record) {
+  if (!h || !ws || !record || !h->ipc_only) return MEMFINE_ERR_INVALID_ARG;
+  IpcRec mine;
+  if (memfine_status rc = ipc_export_rec(h, ws, ws_bytes, &mine)) return rc;
+  memset(record, 0, MEMFINE_IPC_RECORD_BYTES);
+  memcpy(record, &mine, sizeof mine);
+  h->exp_ws = ws;
+  h->exp_bytes = ws_bytes;
+  return MEMFINE_OK;
+}
+
+memfine_status memfine_ipc_import(memfine_handle_t h, const uint8_t* records) {
+  if (!h || !records || !h->ipc_only || !h->exp_ws) return MEMFINE_ERR_INVALID_ARG;
+  std::vector<IpcRec> all(h->d.ep_size);
+  for (int r = 0; r < h->d.ep_size; r++) memcpy(&all[r], records + (size_t)r * MEMFINE_IPC_RECORD_BYTES, sizeof(IpcRec));
+  return ipc_import_recs(h, all.data(), h->exp_ws, h->exp_bytes);
 }
 
 memfine_status memfine_destroy(memfine_handle_t h) {
@@ -1652,7 +1713,7 @@ memfine_status memfine_route_counts(memfine_handle_t h, const int32_t* ids_dev, 
         MF_CUDA_OK(cudaMemcpyAsync(counts_dev + (int64_t)r * nsub * d.num_experts, h->lg->ptrs[r][0], nb,
                                    cudaMemcpyDeviceToDevice, st));
     local_fence(h, st, h->lg->done);
-  } else if (ep_path(d)) {
+  } else if (ep_path(d) && !h->ipc_only) {   // (IPC handles: the caller all-gathers)
     if (nccl_all_gather_int(&h->comm, mine, counts_dev, (size_t)nsub * d.num_experts, st)) return MEMFINE_ERR_NCCL;
   }
   return MEMFINE_OK;

@@ -127,7 +127,7 @@ class MemFine:
 
     def __init__(self, tokens, hidden, ffn, num_experts, topk, ep_size=1, ep_rank=0, dtype=torch.bfloat16,
                  process_group=None, local_group=None, mx: bool = False, overlap: bool = False,
-                 ep_path: bool = False, mx_wgrad: bool = False):
+                 ep_path: bool = False, mx_wgrad: bool = False, ipc: bool = False):
         self.dims = make_dims(tokens, hidden, ffn, num_experts, topk, ep_size, ep_rank, dtype, mx, overlap, ep_path,
                               mx_wgrad)
         self.dtype = dtype
@@ -139,6 +139,11 @@ class MemFine:
             h = C.c_void_p()
             capi.check(capi.lib().memfine_create_local(C.byref(self.dims), local_group.g, C.byref(h)),
                        "memfine_create_local")
+            self.h = h
+            return
+        if ipc:   # memfine_create_ipc: P2P transport only, mappings exchanged by the caller (no NCCL)
+            h = C.c_void_p()
+            capi.check(capi.lib().memfine_create_ipc(C.byref(self.dims), C.byref(h)), "memfine_create_ipc")
             self.h = h
             return
         uid = None
@@ -272,6 +277,17 @@ class MemFine:
         for the fused peer-memory exchange."""
         capi.check(capi.lib().memfine_register_workspace(self.h, _ptr(ws), ws.numel(), _stream(stream)),
                    "memfine_register_workspace")
+
+    def ipc_export(self, ws: torch.Tensor) -> bytes:
+        """memfine_ipc_export: this rank's mapping record for workspace ws (IPC handles)."""
+        rec = (C.c_uint8 * capi.IPC_RECORD_BYTES)()
+        capi.check(capi.lib().memfine_ipc_export(self.h, _ptr(ws), ws.numel(), rec), "memfine_ipc_export")
+        return bytes(rec)
+
+    def ipc_import(self, records):
+        """memfine_ipc_import: every rank's record (rank order); the caller barriers afterwards."""
+        buf = (C.c_uint8 * (capi.IPC_RECORD_BYTES * len(records))).from_buffer_copy(b"".join(records))
+        capi.check(capi.lib().memfine_ipc_import(self.h, buf), "memfine_ipc_import")
 
     def set_debug(self, on: bool = True):
         capi.check(capi.lib().memfine_set_debug(self.h, int(on)), "memfine_set_debug")

@@ -14,7 +14,7 @@ python -m pytest tests -m gpu -q > "$out/gputests.log" 2>&1
 # the headline line (Mixtral layer, EP = 1, tuner's C; per-C sweep, MXFP8 variants, cpu_baseline)
 python bench.py > "$out/bench.json" 2> "$out/bench.err"
 # the other BASELINE configs on one GPU
-for c in "dsv3 8" "qwen3 8" "qwen3 1"; do
+for c in "mixtral 8" "dsv3 8" "qwen3 8" "qwen3 1"; do
   set -- $c
   python bench.py --config "$1" --ep-emulate "$2" --sweep 1 --no-cpu-baseline > "$out/cfg_$1_ep$2.json" 2>&1
 done
