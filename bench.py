@@ -249,8 +249,16 @@ def emulated_config(args):
     cfg = synth.CONFIGS[args.config]
     if args.ep_emulate > 1:
         import dataclasses
-        assert cfg.E % args.ep_emulate == 0 and cfg.k <= cfg.E // args.ep_emulate
-        cfg = dataclasses.replace(cfg, E=cfg.E // args.ep_emulate)
+        assert cfg.E % args.ep_emulate == 0
+        El = cfg.E // args.ep_emulate
+        if cfg.k <= El:
+            cfg = dataclasses.replace(cfg, E=El)
+        else:
+            # fewer local experts than top-k (Mixtral at EP = 8: one expert per rank): the same T k copies as
+            # T k / k' tokens with top-k' = E_l distinct local experts - identical expert GEMM and weight-gradient
+            # shapes; the permute moves the same copies from k/k' times as many token rows
+            assert (cfg.T * cfg.k) % El == 0
+            cfg = dataclasses.replace(cfg, E=El, k=El, T=cfg.T * cfg.k // El)
     return cfg
 
 
@@ -258,9 +266,12 @@ def workload_config(cfg, args, world: int) -> dict:
     """The workload both arms are measured on (config.workload of the JSON line)."""
     T = args.tokens or cfg.T
     placement = args.placement or cfg.placement
+    k0 = synth.CONFIGS[args.config].k
     emu = (f" [one rank's load at EP={args.ep_emulate}: {T}x{cfg.k} copies over E/{args.ep_emulate}="
-           f"{cfg.E} local experts, run at EP=1]") if args.ep_emulate > 1 else ""
-    return {"workload": f"{cfg.name}-style MoE layer: E={cfg.E * args.ep_emulate} top-{cfg.k} h={cfg.h} SwiGLU "
+           f"{cfg.E} local experts, run at EP=1"
+           + (f"; top-{k0} routing over {cfg.E} local expert(s) emulated as {T} tokens top-{cfg.k}" if cfg.k != k0
+              else "") + "]") if args.ep_emulate > 1 else ""
+    return {"workload": f"{cfg.name}-style MoE layer: E={cfg.E * args.ep_emulate} top-{k0} h={cfg.h} SwiGLU "
                         f"ffn={cfg.g}, {T} tokens/GPU, Zipf({cfg.zipf_s}) routing ({placement} placement), "
                         f"EP={world}{emu}",
             "tokens_per_gpu": T, "ep": world}

@@ -1,14 +1,17 @@
-# A/B two builds of libmemfine.so on one box: the in-tree build (new) against $1 (base), interleaved runs of
-# the bench (extra bench args after the first argument).
-set -u
-base=$1; shift
+# A/B of several builds of libmemfine.so on ONE box, interleaved: each ab_libs/<name>.so (git-ignored, but it
+# travels to the box with the snapshot - gpurun_out/ does not) is copied over the in-tree library and the bench
+# runs with the given arguments; two rounds.  The in-tree library is restored at the end.
+#   bash tools/lib_ab.sh "base S X" --mx 0 --sweep 0        -> gpurun_out/ab/<name>_<round>.json
+set -eu
+names=$1; shift
 out=gpurun_out/ab; mkdir -p $out
-cp paper_2511_21431_b200/libmemfine.so $out/libmemfine_new.so
+lib=paper_2511_21431_b200/libmemfine.so
+cp $lib $out/.intree.so
+for n in $names; do [ -f ab_libs/$n.so ] || { echo "missing ab_libs/$n.so" >&2; exit 1; }; done
 for i in 1 2; do
-  for v in new base; do
-    cp $out/libmemfine_$v.so paper_2511_21431_b200/libmemfine.so
-    [ $v = base ] && cp $base paper_2511_21431_b200/libmemfine.so
-    timeout 900 python bench.py --no-cpu-baseline "$@" > $out/${v}_$i.json 2> $out/${v}_$i.err
+  for n in $names; do
+    cp ab_libs/$n.so $lib
+    timeout 900 python bench.py --no-cpu-baseline "$@" > $out/${n}_$i.json 2> $out/${n}_$i.err || true
   done
 done
-cp $out/libmemfine_new.so paper_2511_21431_b200/libmemfine.so
+cp $out/.intree.so $lib
