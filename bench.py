@@ -271,10 +271,11 @@ def workload_config(cfg, args, world: int) -> dict:
            f"{cfg.E} local experts, run at EP=1"
            + (f"; top-{k0} routing over {cfg.E} local expert(s) emulated as {T} tokens top-{cfg.k}" if cfg.k != k0
               else "") + "]") if args.ep_emulate > 1 else ""
+    T_tok = T * cfg.k // k0
     return {"workload": f"{cfg.name}-style MoE layer: E={cfg.E * args.ep_emulate} top-{k0} h={cfg.h} SwiGLU "
-                        f"ffn={cfg.g}, {T} tokens/GPU, Zipf({cfg.zipf_s}) routing ({placement} placement), "
+                        f"ffn={cfg.g}, {T_tok} tokens/GPU, Zipf({cfg.zipf_s}) routing ({placement} placement), "
                         f"EP={world}{emu}",
-            "tokens_per_gpu": T, "ep": world}
+            "tokens_per_gpu": T_tok, "ep": world}
 
 
 def run_reference(args):
@@ -375,6 +376,9 @@ def main():
     cfg = emulated_config(args)
     placement = args.placement or cfg.placement
     T = args.tokens or cfg.T
+    # tokens/s counts the workload's own tokens: an EP emulation that runs T k copies as T k / k' top-k' tokens
+    # (fewer local experts than top-k) still processes the copies of T k' / k tokens of the real layer
+    T_tok = T * cfg.k // synth.CONFIGS[args.config].k
     EP = world
     assert cfg.E % EP == 0
     El = cfg.E // EP
@@ -513,7 +517,7 @@ def main():
         # the same timed region again without event bracketing (the headline number)
         ms_plain, _ = timed(step, args.steps, 1, prof=False)
     ms = ms_plain
-    value = EP * T / (ms / 1000.0)
+    value = EP * T_tok / (ms / 1000.0)
 
     # ---------------------------------------------------------------- roofline of the dominant kernel
     peaks = load_peaks()
@@ -661,7 +665,7 @@ def main():
             try:   # a side measurement: a failure here must not cost the headline line
                 wsc = torch.empty(int(peak_gb(Cc) * 1e9) + 1, dtype=torch.uint8, device=dev)
                 msc, _ = timed(make_step(Cc, wsc), max(3, args.steps // 2), 1)
-                per_C[Cc] = {"ms_per_step": msc, "tokens_per_s": EP * T / (msc / 1000.0), "peak_act_gb": peak_gb(Cc)}
+                per_C[Cc] = {"ms_per_step": msc, "tokens_per_s": EP * T_tok / (msc / 1000.0), "peak_act_gb": peak_gb(Cc)}
                 del wsc
             except Exception as ex:  # noqa: BLE001
                 per_C[Cc] = {"error": f"{type(ex).__name__}: {ex}"[:300]}
@@ -715,7 +719,7 @@ def main():
                 torch.cuda.synchronize()
                 dev_y = float((y.float() - y_bf16).abs().max() / y_bf16.abs().max())
                 variants[vname] = {
-                    "ms_per_step": msx, "tokens_per_s": EP * T / (msx / 1000.0),
+                    "ms_per_step": msx, "tokens_per_s": EP * T_tok / (msx / 1000.0),
                     "speedup_vs_bf16": ms / msx,
                     "operands": "E4M3 + E8M0 scale per 32 along K (tcgen05 kind::mxf8f6f4.block_scale) for gate/up, "
                                 "down and dX" + (" and the weight gradients (columnwise along the copies, reading R28c)"
@@ -755,7 +759,7 @@ def main():
         "gemm_tflops_all_kernels": all_gemm_tflops, "step_tflops": step_tflops,
         "kernel_ms_per_step": {s: v["ms"] / args.steps for s, v in prof.items() if v["launches"]},
         "clocks": clk.summary(),
-        "e2e": {"value": EP * T / (ms_e2e / 1000.0), "unit": "tokens/s", "h2d_bytes_per_step": h2d,
+        "e2e": {"value": EP * T_tok / (ms_e2e / 1000.0), "unit": "tokens/s", "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h, "ms_per_step": ms_e2e},
         "gpu_launches": launches_fwd_bwd * args.steps,
         "variants": variants,
