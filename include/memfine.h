@@ -82,7 +82,7 @@ typedef struct {
 } memfine_dims;
 
 /* memfine_dims.flags
- *  MEMFINE_FLAG_OVERLAP (ep_size > 1, C > 1, EP_COPY transport): pipeline the FCDA chunk loop
+ *  MEMFINE_FLAG_OVERLAP (ep_size > 1, C > 1; either transport): pipeline the FCDA chunk loop
  *    over two streams, "the per-chunk dispatch and combine overlapped chunk by chunk with the
  *    grouped GEMM" (north star; Eq. 6 / 7 order is unchanged): chunk j+1's
  *    permute + dispatch all-to-allv and chunk j-1's combine all-to-allv + unpermute run on the
@@ -90,8 +90,11 @@ typedef struct {
  *    workspace holds two slots of the exchanged rows (send staging, X_disp, dY_disp, per-row
  *    scores and metadata); G||U and a stay single (compute-only).  In the forward o is written
  *    over X_disp, so the forward's per-row bytes do not grow; the backward's grow by 2h*D_t.
- *    Ignored (layout and bytes identical to flags = 0) when ep_size == 1 (without EP_PATH), C == 1
- *    or MXFP8.
+ *    With MEMFINE_EP_P2P the comm stream runs chunk j+1's permute + pushes into the peers' buffers
+ *    and chunk j-1's flag wait + combine / unpermute; chunk j's GEMMs (whose epilogues store into
+ *    the sources' buffers) run on the caller's stream; slot reuse is fenced by the peers' done(j-2)
+ *    flags.  Ignored (layout and bytes identical to flags = 0) when ep_size == 1 (without EP_PATH),
+ *    C == 1 or MXFP8.
  *  MEMFINE_FLAG_EP_PATH (ep_size == 1 only): run the expert-parallel data path - count
  *    all-gather, send staging, per-(peer, local expert) all-to-allv, combine exchange - over a
  *    1-rank NCCL communicator, every segment (including the self segment) through ncclSend /
@@ -207,9 +210,8 @@ memfine_status memfine_create_local(const memfine_dims* dims, memfine_group_t gr
  *    workspace must first be registered with memfine_register_workspace (or, without NCCL, exported
  *    and imported: memfine_create_ipc), and ranks fence with epoch-stamped per-peer flags in each
  *    other's sync areas, waited on by device kernels (no host synchronisation inside a call).
- * The workspace layout and size are the same for both.  MEMFINE_EP_P2P on a handle created with
- * MEMFINE_FLAG_OVERLAP returns MEMFINE_ERR_INVALID_ARG (the two-slot pipeline is the copy
- * transport's; memfine_workspace_bytes sizes it from the dims alone). */
+ * The workspace layout and size are the same for both (with MEMFINE_FLAG_OVERLAP: two slots for either,
+ * sized by memfine_workspace_bytes from the dims). */
 enum { MEMFINE_EP_COPY = 0, MEMFINE_EP_P2P = 1 };
 memfine_status memfine_set_ep_transport(memfine_handle_t h, int32_t transport);
 

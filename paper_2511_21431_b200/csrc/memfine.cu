@@ -915,6 +915,8 @@ int ep_gather_counts(memfine_handle_s* h, const int32_t* ids, int C, cudaStream_
 //   wait pushed(j) -> GEMMs, whose down / dX epilogues store each output row into its source's send buffer
 //   -> signal combined(j), wait combined(j) -> combine / unpermute -> signal done(j).
 // A rank pushes chunk j+1 as soon as its receivers are done with chunk j, while it may still compute.
+int ensure_comm_stream(memfine_handle_s* h);
+
 template <typename T>
 memfine_status ep_run_p2p(memfine_handle_s* h, int pass, const T* dy, const T* x, const int32_t* ids, const float* w,
                           const void* wg, const void* wu, const void* wd, int C, T* out, float* dwg, float* dwu,
@@ -927,29 +929,36 @@ memfine_status ep_run_p2p(memfine_handle_s* h, int pass, const T* dy, const T* x
   MxWeightsLayout W = mx_weights_layout(d, h->mx_w);
   if (ws != h->reg_ws || ws_bytes != h->reg_bytes || (int)h->peer_ws.size() != EP) {
     // in-process groups register on first use (every rank's call reaches the same point); across
-    // processes memfine_register_workspace(ws, ws_bytes) must come first, on every rank
+    // processes memfine_register_workspace(ws, ws_bytes) (or memfine_ipc_import) must come first, on every rank
     if (!h->lg) return MEMFINE_ERR_INVALID_ARG;
     if (memfine_status rc = register_local(h, ws, ws_bytes)) return rc;
   }
-  const int64_t S = tmax_chunk(d, C) * k;
-  const int64_t R = rows_fitting(d, C, pass, ws_bytes, S);
+  // MEMFINE_FLAG_OVERLAP (C > 1, not MXFP8): two workspace slots; chunk j's pushes (and j-1's combine) run on
+  // the comm stream while chunk j-1's GEMMs run on the caller's stream
+  const int S = ep_slots(d, C);
+  const int64_t Srows = tmax_chunk(d, C) * k;
+  const int64_t R = rows_fitting(d, C, pass, ws_bytes, Srows);
   if (R <= 0) return MEMFINE_ERR_WORKSPACE;
-  Layout L = carve(d, C, pass, ws, R, S);
-  h->last_meta = L.meta_bytes;
-  h->last_row_bytes = L.row_bytes;
-  PeerTable pt{};
-  pt.n = EP;
+  Layout Ls[2];
+  carve(d, C, pass, ws, R, Srows, Ls);
+  h->last_meta = Ls[0].meta_bytes;
+  h->last_row_bytes = Ls[0].row_bytes;
+  PeerTable pt[2] = {};
   SyncPeers sp{};
   sp.n = EP;
   for (int r = 0; r < EP; r++) {
     memfine_dims dr = d;
     dr.ep_rank = r;
-    Layout Lr = carve(dr, C, pass, h->peer_ws[r], R, S);   // the same offsets in every rank's workspace
-    pt.X[r] = (char*)Lr.X;
-    pt.DY[r] = (char*)Lr.DY;
-    pt.w_row[r] = (char*)Lr.m.w_row;
-    pt.send[r] = (char*)Lr.send;
-    pt.send_w[r] = pass == MEMFINE_BWD ? (char*)Lr.send_w : nullptr;
+    Layout Lr[2];
+    carve(dr, C, pass, h->peer_ws[r], R, Srows, Lr);   // the same offsets in every rank's workspace
+    for (int sl = 0; sl < S; sl++) {
+      pt[sl].n = EP;
+      pt[sl].X[r] = (char*)Lr[sl].X;
+      pt[sl].DY[r] = (char*)Lr[sl].DY;
+      pt[sl].w_row[r] = (char*)Lr[sl].m.w_row;
+      pt[sl].send[r] = (char*)Lr[sl].send;
+      pt[sl].send_w[r] = pass == MEMFINE_BWD ? (char*)Lr[sl].send_w : nullptr;
+    }
     sp.area[r] = h->peer_sync[r];
   }
   uint64_t* area = h->sync_d;
@@ -959,49 +968,72 @@ memfine_status ep_run_p2p(memfine_handle_s* h, int pass, const T* dy, const T* x
   launch_route_hist(ids, d.tokens, k, E, C, mine, h->status_d, st);
   launch_sync_push_counts(mine, C, E, sp, me, st);
   launch_sync_wait(area, EP, me, 0, 0, h->status_d, st);
-  // A3's per-chunk split and offset tables, and the capacity check, from the landed counts
-  launch_p2p_tables(area, C, E, El, EP, me, R, S, h->counts_d, L.m.p2p_tab, h->gskip_d, h->status_d, st);
+  // A3's per-chunk split and offset tables (every chunk's, in slot 0's array), and the capacity check
+  int* tabs = Ls[0].m.p2p_tab;
+  launch_p2p_tables(area, C, E, El, EP, me, R, Srows, h->counts_d, tabs, h->gskip_d, h->status_d, st);
   h->last.kernel_launches += 6;
   int beta = accumulate ? 1 : 0;
   if (pass == MEMFINE_BWD && dscore && d.tokens > 0)
     MF_CUDA_OK(cudaMemsetAsync(dscore, 0, sizeof(float) * d.tokens * k, st));
+  cudaStream_t cs = st;
+  if (S == 2) {
+    if (ensure_comm_stream(h)) return MEMFINE_ERR_CUDA;
+    cs = h->cs;
+    MF_CUDA_OK(cudaEventRecord(h->ev_fork, st));   // counts, tables, dscore zeroing
+    MF_CUDA_OK(cudaStreamWaitEvent(cs, h->ev_fork, 0));
+  }
   const int rb = hd * (int)sizeof(T);
   const size_t per = 4 * (size_t)E + 1;
-  for (int j = 0; j < C; j++) {
-    const int* tab_j = L.m.p2p_tab + per * j;
+  // Per chunk j (slot j % S), flags epoch-stamped with code j + 1:
+  //   dispatch(j) [cs]: wait done(j - S) of every peer (their slot is free) -> push rows -> signal pushed(j),
+  //                     wait pushed(j) -> padding, row addresses
+  //   compute(j)  [st]: GEMMs, whose down / dX epilogues store each output row into its source's send buffer
+  //                     -> signal combined(j)
+  //   combine(j)  [cs]: wait combined(j) -> combine / unpermute -> signal done(j)
+  // With one slot everything runs in that order on st; with two, cs issues dispatch(j+1) before combine(j).
+  auto dispatch = [&](int j) -> memfine_status {
+    const Layout& L = Ls[j % S];
+    const int* tab_j = tabs + per * j;
     int64_t t0 = chunk_begin(d.tokens, C, j), t1 = chunk_begin(d.tokens, C, j + 1);
     int NB = (int)ceil_div64(t1 - t0, kTokPerBlk);
     if (NB) {
-      launch_dispatch_hist(ids, t0, t1, k, E, L.m, h->status_d, st);
-      launch_dispatch_scan(NB, E, El, 1, L.rows_cap, L.m, nullptr, nullptr, j, st);
-      launch_dispatch_index(ids, w, t0, t1, k, E, L.m, L.m.send_src, nullptr, st);
+      launch_dispatch_hist(ids, t0, t1, k, E, L.m, h->status_d, cs);
+      launch_dispatch_scan(NB, E, El, 1, L.rows_cap, L.m, nullptr, nullptr, j, cs);
+      launch_dispatch_index(ids, w, t0, t1, k, E, L.m, L.m.send_src, nullptr, cs);
       h->last.kernel_launches += 3;
     }
-    launch_ep_recv_seg(h->counts_d, C, j, E, El, me, EP, L.rows_cap, L.m, h->rows_d, h->rows_d + kMaxSub, st,
+    launch_ep_recv_seg(h->counts_d, C, j, E, El, me, EP, L.rows_cap, L.m, h->rows_d, h->rows_d + kMaxSub, cs,
                        h->gskip_d);
-    prof_begin(h, 9, st);
-    // every peer is done with its buffers of the previous chunk (or of the previous call)
-    launch_sync_wait(area, EP, me, 3, j == 0 ? -1 : j, h->status_d, st);
+    prof_begin(h, 9, cs);
+    // every peer is done with its buffers of slot j % S (chunk j - S, or the previous call)
+    launch_sync_wait(area, EP, me, 3, j < S ? -1 : j - S + 1, h->status_d, cs);
     if (NB)
       launch_p2p_push<T>(x, pass == MEMFINE_BWD ? dy : nullptr, w, k, hd, E, El, EP, tab_j, L.m.send_src, L.m.info,
-                         pt, (t1 - t0) * k, st);
-    launch_sync_signal(sp, me, 1, j + 1, st);
-    launch_sync_wait(area, EP, me, 1, j + 1, h->status_d, st);   // every row pushed into this rank landed
-    prof_end(h, st);
-    launch_zero_padding<T>(El, hd, L.m, (T*)L.X, pass == MEMFINE_BWD ? (T*)L.DY : nullptr, st);
-    if (pass == MEMFINE_BWD) MF_CUDA_OK(cudaMemsetAsync(L.m.dw_row, 0, sizeof(float) * L.rows_cap, st));
-    launch_p2p_row_addr(L.m.seg, L.m.recv_cnt, El, EP, tab_j, E, L.m.info, pt, rb, L.m.row_addr,
-                        pass == MEMFINE_BWD ? L.m.row_addr_w : nullptr, L.rows_cap, st);
+                         pt[j % S], (t1 - t0) * k, cs);
+    launch_sync_signal(sp, me, 1, j + 1, cs);
+    launch_sync_wait(area, EP, me, 1, j + 1, h->status_d, cs);   // every row pushed into this rank landed
+    prof_end(h, cs);
+    launch_zero_padding<T>(El, hd, L.m, (T*)L.X, pass == MEMFINE_BWD ? (T*)L.DY : nullptr, cs);
+    if (pass == MEMFINE_BWD) MF_CUDA_OK(cudaMemsetAsync(L.m.dw_row, 0, sizeof(float) * L.rows_cap, cs));
+    launch_p2p_row_addr(L.m.seg, L.m.recv_cnt, El, EP, tab_j, E, L.m.info, pt[j % S], rb, L.m.row_addr,
+                        pass == MEMFINE_BWD ? L.m.row_addr_w : nullptr, L.rows_cap, cs);
     h->last.kernel_launches += 6;
+    if constexpr (std::is_same<T, __nv_bfloat16>::value)
+      if (mx) {   // MXFP8 (reading R28): the landed bf16 rows -> E4M3 + scale chunks
+        launch_mx_quant_rows((const __nv_bfloat16*)L.X, hd, L.rows_cap, L.m.info, hd, L.Xq, L.Xsf, cs);
+        h->last.kernel_launches += 1;
+      }
+    if (S == 2) MF_CUDA_OK(cudaEventRecord(h->ev_disp[j % 2], cs));
+    return MEMFINE_OK;
+  };
+  auto compute = [&](int j) -> memfine_status {
+    const Layout& L = Ls[j % S];
+    if (S == 2) MF_CUDA_OK(cudaStreamWaitEvent(st, h->ev_disp[j % 2], 0));
     GemmProblem<T> p = base_problem<T>(h, L, wg, wu, wd);
     p.dWg = dwg;
     p.dWu = dwu;
     p.dWd = dwd;
-    if constexpr (std::is_same<T, __nv_bfloat16>::value)
-      if (mx) {   // MXFP8 (reading R28): the landed bf16 rows -> E4M3 + scale chunks
-        launch_mx_quant_rows((const __nv_bfloat16*)L.X, hd, L.rows_cap, L.m.info, hd, L.Xq, L.Xsf, st);
-        h->last.kernel_launches += 1;
-      }
+    if (S == 2) p.sm_limit = h->num_sms - h->comm_sms;
     if (pass == MEMFINE_FWD) {
       p.kind = GK_GATEUP;
       p.store_a = 1;
@@ -1017,9 +1049,6 @@ memfine_status ep_run_p2p(memfine_handle_s* h, int pass, const T* dy, const T* x
       if constexpr (std::is_same<T, __nv_bfloat16>::value)
         if (mx) set_mx(p, {L.Aq, L.Asf}, W.op[2], W.op[2]);
       if (int rc = run_gemm<T>(h, p, st)) return (memfine_status)rc;
-      launch_sync_signal(sp, me, 2, j + 1, st);
-      launch_sync_wait(area, EP, me, 2, j + 1, h->status_d, st);   // every o row of this rank's tokens landed
-      if (t1 > t0) launch_combine<T>((const T*)L.send, w, t0, t1, k, hd, L.m, out, st);
     } else {
       p.kind = GK_GATEUP;
       p.store_a = 0;
@@ -1045,15 +1074,46 @@ memfine_status ep_run_p2p(memfine_handle_s* h, int pass, const T* dy, const T* x
         if (mx) set_mx(p, {L.GUq, L.GUsf}, W.op[3], W.op[4]);
       if (int rc = run_gemm<T>(h, p, st)) return (memfine_status)rc;
       launch_p2p_push_dw(L.m.dw_row, L.m.row_addr_w, L.m.info, L.rows_cap, st);
-      launch_sync_signal(sp, me, 2, j + 1, st);
-      launch_sync_wait(area, EP, me, 2, j + 1, h->status_d, st);   // every dX row and d_w landed
+      h->last.kernel_launches += 1;
+    }
+    launch_sync_signal(sp, me, 2, j + 1, st);
+    h->last.kernel_launches += 1;
+    if (S == 2) MF_CUDA_OK(cudaEventRecord(h->ev_gemm[j % 2], st));
+    return MEMFINE_OK;
+  };
+  auto combine = [&](int j) -> memfine_status {
+    const Layout& L = Ls[j % S];
+    int64_t t0 = chunk_begin(d.tokens, C, j), t1 = chunk_begin(d.tokens, C, j + 1);
+    if (S == 2) MF_CUDA_OK(cudaStreamWaitEvent(cs, h->ev_gemm[j % 2], 0));
+    launch_sync_wait(area, EP, me, 2, j + 1, h->status_d, cs);   // every o / dX row of this rank's tokens landed
+    if (pass == MEMFINE_FWD) {
+      if (t1 > t0) launch_combine<T>((const T*)L.send, w, t0, t1, k, hd, L.m, out, cs);
+    } else {
       ChunkMeta mb = L.m;
       mb.dw_row = L.send_w;
-      if (t1 > t0) launch_unpermute_reduce<T>((const T*)L.send, t0, t1, k, hd, mb, out, dscore, st);
+      if (t1 > t0) launch_unpermute_reduce<T>((const T*)L.send, t0, t1, k, hd, mb, out, dscore, cs);
     }
-    // this rank's buffers of chunk j are free for the peers' pushes / stores of chunk j+1 (or the next call)
-    launch_sync_signal(sp, me, 3, j + 1 == C ? kSyncDoneCall : j + 1, st);
-    h->last.kernel_launches += 5;
+    // this rank's buffers of slot j % S are free for the peers' pushes / stores of chunk j + S (or the next call)
+    launch_sync_signal(sp, me, 3, j + 1 == C ? kSyncDoneCall : j + 1, cs);
+    h->last.kernel_launches += 3;
+    return MEMFINE_OK;
+  };
+  if (S == 1) {
+    for (int j = 0; j < C; j++) {
+      if (memfine_status rc = dispatch(j)) return rc;
+      if (memfine_status rc = compute(j)) return rc;
+      if (memfine_status rc = combine(j)) return rc;
+    }
+  } else {
+    if (memfine_status rc = dispatch(0)) return rc;
+    for (int j = 0; j < C; j++) {
+      if (j + 1 < C)
+        if (memfine_status rc = dispatch(j + 1)) return rc;
+      if (memfine_status rc = compute(j)) return rc;
+      if (memfine_status rc = combine(j)) return rc;
+    }
+    MF_CUDA_OK(cudaEventRecord(h->ev_join, cs));
+    MF_CUDA_OK(cudaStreamWaitEvent(st, h->ev_join, 0));
   }
   return latch_cuda(h);
 }
@@ -1532,9 +1592,6 @@ memfine_status memfine_set_ep_transport(memfine_handle_t h, int32_t transport) {
   if (transport == MEMFINE_EP_P2P && h->d.ep_size > kMaxPeers) return MEMFINE_ERR_UNSUPPORTED;
   if (h->ipc_only) return transport == MEMFINE_EP_P2P ? MEMFINE_OK : MEMFINE_ERR_UNSUPPORTED;   // no NCCL
   if (transport == MEMFINE_EP_P2P && !h->lg && h->d.ep_size > 1 && !h->comm.comm) return MEMFINE_ERR_UNSUPPORTED;
-  // the two-slot chunk pipeline (and its workspace layout, which memfine_workspace_bytes derives from the
-  // dims alone) belongs to the copy transport
-  if (transport == MEMFINE_EP_P2P && (h->d.flags & MEMFINE_FLAG_OVERLAP)) return MEMFINE_ERR_INVALID_ARG;
   h->p2p = transport == MEMFINE_EP_P2P;
   return MEMFINE_OK;
 }

@@ -40,10 +40,11 @@ def _run_group(EP, C, dtype, transport, xs, dys, routes, wg, wu, wd, T, h, g, E,
             torch.cuda.set_device(0)
             st = torch.cuda.Stream()
             with torch.cuda.stream(st):
-                ov = transport == "overlap"
+                ov = transport in ("overlap", "p2p_overlap")
                 mf = layer.MemFine(T, h, g, E, k, ep_size=EP, ep_rank=r, dtype=dtype, local_group=group, overlap=ov,
                                    mx=mx, mx_wgrad=mx_wgrad)
-                mf.set_ep_transport(capi.EP_COPY if ov else transport)
+                mf.set_ep_transport(capi.EP_P2P if transport == "p2p_overlap" else
+                                    capi.EP_COPY if ov else transport)
                 if ov:
                     mf.set_comm_sms(16)
                 dev = "cuda:0"
@@ -89,7 +90,7 @@ def _run_group(EP, C, dtype, transport, xs, dys, routes, wg, wu, wd, T, h, g, E,
     return results, counts_seen
 
 
-@pytest.mark.parametrize("transport", [capi.EP_COPY, capi.EP_P2P, "overlap"])
+@pytest.mark.parametrize("transport", [capi.EP_COPY, capi.EP_P2P, "overlap", "p2p_overlap"])
 @pytest.mark.parametrize("EP,C,dtype", [(2, 1, torch.bfloat16), (2, 3, torch.bfloat16), (4, 2, torch.bfloat16),
                                         (4, 1, torch.float32), (2, 2, torch.float32)])
 def test_ep_local_group_matches_oracle(EP, C, dtype, transport):
@@ -144,6 +145,16 @@ def test_ep_overlap_bit_identical(EP, C):
     for r in range(EP):
         for name, u, v in zip(("y", "dx", "dscore", "dw_gate", "dw_up", "dw_down"), a[r], b[r]):
             np.testing.assert_array_equal(u, v, err_msg=f"rank {r} {name}")
+    # the fused peer-memory exchange with the same two-slot pipeline (pushes of chunk j+1 and the combine of
+    # chunk j-1 on the comm stream while chunk j's GEMMs run): bit-identical to its own one-stream order
+    c, _ = _run_group(EP, C, dtype, capi.EP_P2P, xs, dys, routes, wg, wu, wd, T, h, g, E, k)
+    d_, _ = _run_group(EP, C, dtype, "p2p_overlap", xs, dys, routes, wg, wu, wd, T, h, g, E, k)
+    for r in range(EP):
+        for name, u, v in zip(("y", "dx", "dscore", "dw_gate", "dw_up", "dw_down"), c[r], d_[r]):
+            if name == "dscore":   # (its dA partials meet in fp32 atomics of run-dependent order)
+                assert rel_err(v, u) <= 1e-6, (r, name)
+            else:
+                np.testing.assert_array_equal(u, v, err_msg=f"rank {r} p2p {name}")
 
 
 def _ep1_mx_reference(EP, C, xs, dys, routes, wg, wu, wd, T, h, g, E, k, mx_wgrad):
@@ -257,7 +268,7 @@ def _check_ranks(results, refs, EP, T, El, t_):
             assert np.isfinite(a).all(), (r, name)
 
 
-@pytest.mark.parametrize("transport", [capi.EP_COPY, capi.EP_P2P, "overlap"])
+@pytest.mark.parametrize("transport", [capi.EP_COPY, capi.EP_P2P, "overlap", "p2p_overlap"])
 @pytest.mark.parametrize("EP,C", [(2, 1), (4, 3)])
 def test_ep_rank_without_rows(EP, C, transport):
     """A rank whose experts receive no copy in any chunk (hot-expert routing, the case MACT exists for):

@@ -1,3 +1,2 @@
-out=gpurun_out/t4; mkdir -p $out
-timeout 900 python -m pytest tests/test_gpu_parity.py tests/test_gpu_router.py -x -q > $out/tests.log 2>&1; echo "rc=$?" >> $out/tests.log
-bash tools/lib_ab.sh "base W" --mx 0
+out=gpurun_out/t5; mkdir -p $out
+timeout 1500 python -m pytest tests/test_gpu_ep_local.py tests/test_gpu_ipc_p2p.py tests/test_gpu_nccl_ep_path.py -x -q > $out/ep.log 2>&1; echo "rc=$?" >> $out/ep.log
