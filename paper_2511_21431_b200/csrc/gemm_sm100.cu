@@ -415,6 +415,7 @@ struct Tile {
   int m0;     // first row of the (pair) tile: padded row (M-tiled kinds) or dW row (WGRAD)
   int m_end;  // rows >= m_end are not stored (expert segment end / M)
   int n0, k0, nkb;
+  int halves = 1;   // QD (quad) tiles: 2 = two 256-row pair halves sharing the B tile, 1 = the last odd pair
 };
 
 // 2-CTA helpers (cta_group::2): the pair's leader is the even CTA of the cluster.
@@ -462,21 +463,46 @@ __device__ __forceinline__ void mbar_arrive_leader(uint64_t* b) {
   asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(su32(b) & kPeerMask) : "memory");
 }
 
-template <int KIND, bool PAIR, bool MX = false>
-__device__ __forceinline__ int num_tiles(const Params& p) {
+template <int KIND, bool PAIR, bool MX = false, bool QD = false>
+__device__ __forceinline__ int num_tiles(const Params& p, const int* qseg = nullptr) {
   constexpr int BN = CfgX<KIND, MX>::BN;
   int nt = (p.N + BN - 1) / BN;
   if (KIND >= GK_WGRAD_DOWN) return p.El * p.num_mt_w * nt;
   if (p.info[kInfoSkip]) return 0;
+  if (QD) return qseg[p.El] * nt;
   return (PAIR ? p.info[kInfoPairs] : p.info[kInfoRowsPad] / BM) * nt;
 }
 
-template <int KIND, bool PAIR, bool MX = false>
-__device__ __forceinline__ Tile tile_of(const Params& p, int t) {
+template <int KIND, bool PAIR, bool MX = false, bool QD = false>
+__device__ __forceinline__ Tile tile_of(const Params& p, int t, const int* qseg = nullptr) {
   constexpr int BN = CfgX<KIND, MX>::BN;
   constexpr int TM = PAIR ? 2 * BM : BM;  // rows per (pair) tile
   int nt = (p.N + BN - 1) / BN;
   Tile T;
+  if (QD) {
+    // quad tiles: two consecutive 256-row pairs of one expert (qseg: shared-memory prefix of
+    // ceil(pairs_e / 2)); an expert's odd last pair makes a one-half tile
+    const int nq = qseg[p.El];
+    const int gsz = p.group_m * nt;
+    const int gi = t / gsz, first = gi * p.group_m;
+    const int gm = min(nq - first, p.group_m);
+    const int r = t % gsz;
+    const int mq = first + r % gm;
+    T.n0 = (r / gm) * BN;
+    int lo = 0, hi = p.El;   // qseg[lo] <= mq < qseg[hi]
+    while (hi - lo > 1) {
+      const int mid = (lo + hi) >> 1;
+      if (qseg[mid] <= mq) lo = mid; else hi = mid;
+    }
+    T.e = lo;
+    const int ps0 = __ldg(p.pseg + lo), pair = ps0 + (mq - qseg[lo]) * 2;
+    T.halves = min(2, __ldg(p.pseg + lo + 1) - pair);
+    T.m0 = __ldg(p.seg + lo) + (pair - ps0) * TM;
+    T.m_end = __ldg(p.seg + lo + 1);
+    T.k0 = 0;
+    T.nkb = p.K / BK;
+    return T;
+  }
   if (KIND >= GK_WGRAD_DOWN) {
     int per = p.num_mt_w * nt;
     T.e = t / per;
@@ -515,21 +541,25 @@ __device__ __forceinline__ Tile tile_of(const Params& p, int t) {
 }
 
 // MX stage: A 128 x 128 B + B (N rows) x 128 B (E4M3, 128 K per stage) + 1.5 KB scale chunks, 1 KB aligned
-template <int KIND, bool PAIR, bool MX = false>
+template <int KIND, bool PAIR, bool MX = false, bool QD = false>
 __host__ __device__ constexpr int stage_bytes() {
   return MX ? (A_BYTES + CfgX<KIND, MX>::NACC * CfgX<KIND, MX>::BN * 128 / (PAIR ? 2 : 1) + 1536 + 1023) / 1024 * 1024
-            : A_BYTES + (PAIR ? Cfg<KIND>::NACC * Cfg<KIND>::BN / 2 : Cfg<KIND>::NACC * Cfg<KIND>::BN) * BK * 2;
+            : A_BYTES * (QD ? 2 : 1) +
+                  (PAIR ? Cfg<KIND>::NACC * Cfg<KIND>::BN / 2 : Cfg<KIND>::NACC * Cfg<KIND>::BN) * BK * 2;
 }
+// QD: 1 KB more for the quad prefix (E_l <= 255)
+constexpr int kQsegBytes = 1024;
 // as many 1024-aligned stages as fit next to the epilogue staging (227 KB per CTA)
-template <int KIND, bool PAIR, bool MX = false>
+template <int KIND, bool PAIR, bool MX = false, bool QD = false>
 __host__ __device__ constexpr int nstage() {
-  return (232448 - 1024 - 512 - Epi<KIND, MX>::TOTAL) / stage_bytes<KIND, PAIR, MX>() > 6
+  return (232448 - 1024 - 512 - (QD ? kQsegBytes : 0) - Epi<KIND, MX>::TOTAL) / stage_bytes<KIND, PAIR, MX, QD>() > 6
              ? 6
-             : (232448 - 1024 - 512 - Epi<KIND, MX>::TOTAL) / stage_bytes<KIND, PAIR, MX>();
+             : (232448 - 1024 - 512 - (QD ? kQsegBytes : 0) - Epi<KIND, MX>::TOTAL) / stage_bytes<KIND, PAIR, MX, QD>();
 }
-template <int KIND, bool PAIR, bool MX = false>
+template <int KIND, bool PAIR, bool MX = false, bool QD = false>
 __host__ __device__ constexpr int smem_bytes() {
-  return nstage<KIND, PAIR, MX>() * stage_bytes<KIND, PAIR, MX>() + Epi<KIND, MX>::TOTAL + 1024 + 512;
+  return nstage<KIND, PAIR, MX, QD>() * stage_bytes<KIND, PAIR, MX, QD>() + Epi<KIND, MX>::TOTAL + 1024 + 512 +
+         (QD ? kQsegBytes : 0);
 }
 
 // ------------------------------------------------------------------ the kernel
@@ -543,7 +573,11 @@ __host__ __device__ constexpr int smem_bytes() {
 //            stages its 128 A rows and half of B, so the tensor core's smem reads per CTA halve;
 //            scale chunks come by TMA (uint32 rows of 512 B): each CTA holds its own A scales and
 //            the full B tile's scales.
-template <int KIND, bool PAIR, bool MX = false>
+// QD = true (BF16 DOWN / DX, pairs): 512 x 256 tiles per CTA pair - two M = 256 halves sharing each staged B
+//            tile, so every B byte feeds twice the rows (a quarter fewer operand fills per FLOP); each CTA
+//            stages 2 x 128 A rows, the two halves' accumulators fill all 512 TMEM columns (one stage:
+//            the epilogue of a tile is not overlapped, which the long K of these two GEMMs hides).
+template <int KIND, bool PAIR, bool MX = false, bool QD = false>
 __global__ void __launch_bounds__(THREADS, 1)
     gemm_kernel(const __grid_constant__ Params p, const __grid_constant__ CUtensorMap tmA,
                 const __grid_constant__ CUtensorMap tmB0, const __grid_constant__ CUtensorMap tmB1,
@@ -557,10 +591,12 @@ __global__ void __launch_bounds__(THREADS, 1)
   constexpr bool G2 = PAIR;                             // cta_group::2 pair
   constexpr int B_ROWS = G2 ? MMA_N / 2 : MMA_N;        // B rows (N) staged per CTA
   constexpr int B_BYTES = B_ROWS * BK * 2;               // (MX: B_ROWS x 128 E4M3 = the same bytes)
-  constexpr int STAGE_BYTES = stage_bytes<KIND, PAIR, MX>();
-  constexpr int NSTAGE = nstage<KIND, PAIR, MX>();
-  constexpr int ACC_COLS = MMA_N;                       // per accumulator stage
-  constexpr int ACC_ST = (MX && MMA_N == 256) ? 1 : 2;  // accumulator stages (MX N=256: scales take TMEM)
+  constexpr int STAGE_BYTES = stage_bytes<KIND, PAIR, MX, QD>();
+  constexpr int NSTAGE = nstage<KIND, PAIR, MX, QD>();
+  constexpr int A_ST = QD ? 2 * A_BYTES : A_BYTES;       // A bytes per stage (QD: both halves' rows)
+  static_assert(!QD || (PAIR && !MX && MMA_N == 256 && (KIND == GK_DOWN || KIND == GK_DX)), "QD tiles");
+  constexpr int ACC_COLS = MMA_N;                       // per accumulator stage (QD: per half)
+  constexpr int ACC_ST = ((MX && MMA_N == 256) || QD) ? 1 : 2;  // accumulator stages (MX N=256: scales take TMEM)
   constexpr uint32_t TMEM_COLS = MX ? 512 : 2 * ACC_COLS;
   constexpr uint32_t SF_COL = ACC_ST * ACC_COLS;        // MX: A scales at +0..3, B at +4..11
   static_assert(TMEM_COLS <= 512 && (!MX || ACC_ST * ACC_COLS + kMxSf <= 512), "TMEM");
@@ -576,6 +612,7 @@ __global__ void __launch_bounds__(THREADS, 1)
   uint64_t* tempty = tfull + 2;
   uint64_t* ebar = tempty + 2;                          // [EPI_WARPS][2] epilogue TMA-load barriers (dA)
   uint32_t* tmem_slot = (uint32_t*)(ebar + 2 * EPI_WARPS);
+  int* qseg = (int*)(epi_smem + Epi<KIND, MX>::TOTAL + 512);   // QD: [E_l + 1] quad prefix (after the barriers)
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t rank = PAIR ? cta_rank_in_cluster() : 0;
@@ -619,7 +656,27 @@ __global__ void __launch_bounds__(THREADS, 1)
   // everything above (barrier init, TMEM alloc, descriptor prefetch) overlaps the predecessor's tail
   pdl_wait();
   pdl_trigger();
-  const int ntiles = num_tiles<KIND, PAIR, MX>(p);
+  if constexpr (QD) {
+    // the quad prefix qseg[e] = sum over e' < e of ceil(pairs_e' / 2), from the pair prefix the dispatch scan
+    // wrote (read after griddepcontrol.wait); warp 2, 32 experts per step
+    if (warp == 2) {
+      int carry = 0;
+      if (lane == 0) qseg[0] = 0;
+      for (int base = 0; base < p.El; base += 32) {
+        const int e = base + lane;
+        int v = e < p.El ? (__ldg(p.pseg + e + 1) - __ldg(p.pseg + e) + 1) >> 1 : 0;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const int u = __shfl_up_sync(0xffffffffu, v, o);
+          if (lane >= o) v += u;
+        }
+        if (e < p.El) qseg[e + 1] = carry + v;
+        carry += __shfl_sync(0xffffffffu, v, 31);
+      }
+    }
+    __syncthreads();
+  }
+  const int ntiles = num_tiles<KIND, PAIR, MX, QD>(p, qseg);
   (void)SF_COL;
 
   if (warp == 0) {
@@ -651,7 +708,7 @@ __global__ void __launch_bounds__(THREADS, 1)
         step++;
       };
       for (int t = cid; t < ntiles; t += ncid) {
-        Tile T = tile_of<KIND, PAIR, MX>(p, t);
+        Tile T = tile_of<KIND, PAIR, MX, QD>(p, t, qseg);
         const int am0 = T.m0 + (int)rank * BM;              // this CTA's A rows
         if (KIND >= GK_WGRAD_DOWN && p.wave_ctr && leader) {
           // weight gradients: one step per tile, taken even by tiles without rows (nkb = 0)
@@ -668,7 +725,7 @@ __global__ void __launch_bounds__(THREADS, 1)
           }
           mbar_wait(empty + stage, phase ^ 1);
           uint8_t* sa = smem + stage * STAGE_BYTES;
-          uint8_t* sb = sa + A_BYTES;
+          uint8_t* sb = sa + A_ST;
           if constexpr (MX) {
             // E4M3 A [128 rows x 128 K], this CTA's B rows (all, or its half in a pair) and the scale
             // chunks: own A rows' chunk, the whole B tile's chunks (TMA zero-fills chunks and rows
@@ -722,7 +779,8 @@ __global__ void __launch_bounds__(THREADS, 1)
             if (++stage == NSTAGE) { stage = 0; phase ^= 1; }
             continue;
           }
-          if (leader) mbar_expect_tx(full + stage, (PAIR ? 2 : 1) * STAGE_BYTES);
+          if (leader)
+            mbar_expect_tx(full + stage, (PAIR ? 2 : 1) * (QD ? A_BYTES * T.halves + (STAGE_BYTES - A_ST) : STAGE_BYTES));
           int kc = T.k0 + kb * BK;
           auto LA = [&](void* dst, const CUtensorMap* m, int c0, int c1) {
             if (PAIR) tma_2d_pair(dst, m, full + stage, c0, c1); else tma_2d(dst, m, full + stage, c0, c1);
@@ -737,6 +795,7 @@ __global__ void __launch_bounds__(THREADS, 1)
             LA(sa + 8192, &tmA, am0 + 64, kc);
           } else {
             LA(sa, &tmA, kc, am0);
+            if (QD && T.halves == 2) LA(sa + A_BYTES, &tmA, kc, am0 + 2 * BM);   // the second half's rows
           }
           // B: this CTA's share of the N columns
           const int bn0 = T.n0 + (PAIR ? (int)rank * B_ROWS : 0);
@@ -772,7 +831,7 @@ __global__ void __launch_bounds__(THREADS, 1)
       uint32_t phase = 0;
       int it = 0;
       for (int t = cid; t < ntiles; t += ncid) {
-        Tile T = tile_of<KIND, PAIR, MX>(p, t);
+        Tile T = tile_of<KIND, PAIR, MX, QD>(p, t, qseg);
         if (T.nkb == 0) continue;
         int as = it % ACC_ST;
         uint32_t aph = (it / ACC_ST) & 1;
@@ -783,7 +842,7 @@ __global__ void __launch_bounds__(THREADS, 1)
           mbar_wait(full + stage, phase);
           fence_after();
           uint32_t sa = su32(smem + stage * STAGE_BYTES);
-          uint32_t sb = sa + A_BYTES;
+          uint32_t sb = sa + A_ST;
           if constexpr (MX) {
             // scales smem -> TMEM (executes in order with the MMAs: the previous stage's MMAs
             // have read the columns before these copies land)
@@ -824,6 +883,14 @@ __global__ void __launch_bounds__(THREADS, 1)
             uint64_t bd = CF::B_MN ? sdesc(sb + k * 2048, 8192, 1024) : sdesc(sb + k * 32, 16, 1024);
             if (PAIR) mma_bf16_pair(dbase, ad, bd, IDESC, (kb | k) != 0);
             else mma_bf16(dbase, ad, bd, IDESC, (kb | k) != 0);
+          }
+          if (QD && T.halves == 2) {
+            // the second half: its own A rows, the same staged B tile, the other 256 TMEM columns
+#pragma unroll
+            for (int k = 0; k < BK / 16; k++)
+              mma_bf16_pair(dbase + ACC_COLS, sdesc(sa + A_BYTES + k * 32, 16, 1024),
+                            CF::B_MN ? sdesc(sb + k * 2048, 8192, 1024) : sdesc(sb + k * 32, 16, 1024), IDESC,
+                            (kb | k) != 0);
           }
           if (PAIR) mma_commit_pair(empty + stage); else mma_commit(empty + stage);
           if (++stage == NSTAGE) { stage = 0; phase ^= 1; }
@@ -869,10 +936,10 @@ __global__ void __launch_bounds__(THREADS, 1)
       return b;
     };
     for (int t = cid; t < ntiles; t += ncid) {
-      Tile T = tile_of<KIND, PAIR, MX>(p, t);
-      const int row0 = T.m0 + (int)rank * BM + q * 32;     // first row of this warp's 32 rows
-      const int rowi = row0 + lane;
-      const bool rows_ok = row0 < T.m_end;                 // warp-uniform (halves are 128-row aligned)
+      Tile T = tile_of<KIND, PAIR, MX, QD>(p, t, qseg);
+      int row0 = T.m0 + (int)rank * BM + q * 32;           // first row of this warp's 32 rows
+      int rowi = row0 + lane;
+      bool rows_ok = row0 < T.m_end;                       // warp-uniform (halves are 128-row aligned)
       if (T.nkb == 0) {
         if (KIND >= GK_WGRAD_DOWN && !p.beta && rows_ok) {
           // an expert without rows in the first chunk: its dW tile is zero
@@ -897,7 +964,7 @@ __global__ void __launch_bounds__(THREADS, 1)
       }
       int as = it % ACC_ST;
       uint32_t aph = (it / ACC_ST) & 1;
-      const int64_t row = rowi;
+      int64_t row = rowi;
       if constexpr (MX && ACC_ST == 1) {
         // One accumulator stage (the scales take the rest of TMEM): drain this warp's slice of
         // the tile into registers, free TMEM for the next tile's MMAs, then run the epilogue from
@@ -992,6 +1059,14 @@ __global__ void __launch_bounds__(THREADS, 1)
       mbar_wait(tfull + as, aph);
       fence_after();
       uint32_t tb = tmem_base + as * ACC_COLS + ((uint32_t)(q * 32) << 16);
+      for (int hh = 0; hh < (QD ? T.halves : 1); hh++) {
+      if (QD && hh) {   // the quad tile's second half: 256 rows further, the other 256 TMEM columns
+        row0 += 2 * BM;
+        rowi += 2 * BM;
+        row += 2 * BM;
+        rows_ok = row0 < T.m_end;
+        tb += ACC_COLS;
+      }
 #pragma unroll 1
       for (int c = half * CPW; c < (half + 1) * CPW; c += 32) {
         const int n = T.n0 + c;
@@ -1152,6 +1227,7 @@ __global__ void __launch_bounds__(THREADS, 1)
           }
         }
       }
+      }   // halves
       if (KIND == GK_DACT && rows_ok) atomicAdd(p.dw_row + row, dwp);
       fence_before();
       __syncwarp();
@@ -1305,17 +1381,17 @@ bool use_pairs() {
   return v == 1;
 }
 
-template <int KIND, bool PAIR>
+template <int KIND, bool PAIR, bool QD = false>
 int launch(const GemmProblem<__nv_bfloat16>& gp, cudaStream_t st) {
   using CF = Cfg<KIND>;
   constexpr int BN = CF::BN;
   constexpr int MMA_N = CF::NACC * BN;
   constexpr int B_ROWS = PAIR ? MMA_N / 2 : MMA_N;
-  constexpr int SMEM = smem_bytes<KIND, PAIR>();
+  constexpr int SMEM = smem_bytes<KIND, PAIR, false, QD>();
   static_assert(SMEM <= 232448, "smem");
   static bool attr_set = false;
   if (!attr_set) {
-    if (cudaFuncSetAttribute(gemm_kernel<KIND, PAIR>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM) !=
+    if (cudaFuncSetAttribute(gemm_kernel<KIND, PAIR, false, QD>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM) !=
         cudaSuccess)
       return -1;
     attr_set = true;
@@ -1425,7 +1501,7 @@ int launch(const GemmProblem<__nv_bfloat16>& gp, cudaStream_t st) {
                                 : KIND == GK_WGRAD_DOWN ? 48 : 24;
     const int64_t budget = env_budget >= 0 ? env_budget : kind_mb << 20;
     int64_t kdim = (KIND >= GK_WGRAD_DOWN) ? (int64_t)std::max<int64_t>(1, R / std::max<uint64_t>(1, El)) : p.K;
-    int64_t a_strip = (int64_t)TM * kdim * 2, b_strip = (int64_t)BN * kdim * 2;
+    int64_t a_strip = (int64_t)TM * (QD ? 2 : 1) * kdim * 2, b_strip = (int64_t)BN * kdim * 2;
     if (budget) {
       p.group_m = (int)std::max<int64_t>(1, std::min<int64_t>(64, budget / std::max<int64_t>(1, a_strip)));
     } else {
@@ -1439,7 +1515,8 @@ int launch(const GemmProblem<__nv_bfloat16>& gp, cudaStream_t st) {
     p.num_mt_w = (p.M + TM - 1) / TM;
     max_tiles = (int64_t)p.El * p.num_mt_w * nt;
   } else {
-    max_tiles = (int64_t)((R / BM + (PAIR ? El : 0)) / (PAIR ? 2 : 1) + 1) * nt;
+    max_tiles = QD ? (int64_t)((R / BM + 3 * El) / 4 + 1) * nt
+                   : (int64_t)((R / BM + (PAIR ? El : 0)) / (PAIR ? 2 : 1) + 1) * nt;
   }
   int units = (int)std::min<int64_t>(max_tiles, units_hw);
   if (units <= 0) return 0;
@@ -1459,13 +1536,27 @@ int launch(const GemmProblem<__nv_bfloat16>& gp, cudaStream_t st) {
   cfg.numAttrs = (use_pdl() && !p.wave_ctr) ? 2 : 1;   // (a pacing memset precedes a paced launch)
   CUtensorMap none;
   memset(&none, 0, sizeof none);
-  if (cudaLaunchKernelEx(&cfg, gemm_kernel<KIND, PAIR>, p, mA, mB0, mB1, mO0, mO1, none, none, none) != cudaSuccess)
+  if (cudaLaunchKernelEx(&cfg, gemm_kernel<KIND, PAIR, false, QD>, p, mA, mB0, mB1, mO0, mO1, none, none, none) !=
+      cudaSuccess)
     return -1;
   return 1;
 }
 
 template <int KIND>
 int launch_kind(const GemmProblem<__nv_bfloat16>& gp, cudaStream_t st) {
+  if constexpr (KIND == GK_DOWN || KIND == GK_DX) {
+    // 512 x 256 quad tiles for the two long-K GEMMs (MEMFINE_QUAD=0: 256 x 256 pairs; =2: quads whatever the
+    // size - tests); the quad prefix lives in 1 KB of shared memory (E_l <= 255); the router's fp32-output DOWN
+    // launch keeps pairs.  Read per launch (a test flips it).
+    const char* qs = getenv("MEMFINE_QUAD");
+    const int env_quad = qs ? atoi(qs) : 1;
+    // quads halve the tile count, so they need enough work per launch to keep the last wave's tail small:
+    // at least 8 waves of quad tiles at the chunk's row capacity (the full-size C = 1 Mixtral layer has 14)
+    const int64_t quads = gp.rows_cap / (4 * BM) + 1, nt_q = (gp.h + 255) / 256;
+    const int units = (g_num_sms ? g_num_sms : 148) / 2;
+    if (use_pairs() && env_quad && !gp.out_f32 && gp.El <= 255 && (env_quad == 2 || quads * nt_q >= 8 * units))
+      return launch<KIND, true, true>(gp, st);
+  }
   return use_pairs() ? launch<KIND, true>(gp, st) : launch<KIND, false>(gp, st);
 }
 

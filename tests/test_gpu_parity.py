@@ -49,6 +49,25 @@ def test_tiny_config(dtype, C):
     _check_all(p, run, C, ref)
 
 
+@pytest.mark.parametrize("T,h,g,E", [(1000, 256, 384, 8), (2600, 512, 256, 5)])
+def test_quad_tiles_match_pairs_and_oracle(T, h, g, E, monkeypatch):
+    """The 512 x 256 quad tiles of the down and dX GEMMs (two 256-row pair halves sharing each staged B tile;
+    an expert's odd last pair is a one-half tile), forced on with MEMFINE_QUAD=2 at sizes the automatic
+    choice would leave to pairs: Y and dX bit-identical to the 256 x 256 pair tiles (the same MMAs in the
+    same K order per row), everything within tolerance of the oracle, at C = 1 and 3."""
+    p = make_problem(T, h, g, E, 2, dtype=torch.bfloat16, zipf_s=1.2, placement="contiguous", seed=5)
+    run = GpuRun(p)
+    for C in (1, 3):
+        ref = oracle_fwd_bwd(p, C)
+        monkeypatch.setenv("MEMFINE_QUAD", "0")
+        y0, dx0, _, _, _ = _check_all(p, run, C, ref)
+        y0, dx0 = y0.clone(), dx0.clone()
+        monkeypatch.setenv("MEMFINE_QUAD", "2")
+        y1, dx1, _, _, _ = _check_all(p, run, C, ref)
+        assert torch.equal(y0.view(torch.int16), y1.view(torch.int16)), C
+        assert torch.equal(dx0.view(torch.int16), dx1.view(torch.int16)), C
+
+
 @pytest.mark.parametrize("dtype", [torch.bfloat16, torch.float32])
 def test_medium_ragged_skewed(dtype):
     """Several M/N/K tiles, ragged token count (1000), Zipf(1.2) skew, C = 1 and 3."""

@@ -8,7 +8,7 @@ out=gpurun_out/ab; mkdir -p $out
 lib=paper_2511_21431_b200/libmemfine.so
 cp $lib $out/.intree.so
 for n in $names; do [ -f ab_libs/$n.so ] || { echo "missing ab_libs/$n.so" >&2; exit 1; }; done
-for i in 1 2; do
+for i in $(seq 1 ${AB_ROUNDS:-2}); do
   for n in $names; do
     cp ab_libs/$n.so $lib
     timeout 900 python bench.py --no-cpu-baseline "$@" > $out/${n}_$i.json 2> $out/${n}_$i.err || true
