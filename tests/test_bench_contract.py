@@ -104,3 +104,25 @@ def test_step_roofline_terms():
     t = r["terms_ms_hot_rank"]
     assert abs(t["a2a_bytes"] - 1e3 * N) < 1e-9 and abs(t["permute_bytes"] - 1e3 * P) < 1e-9
     assert abs(r["frac"] - max(F1, P, N) / 1.0) < 1e-9
+
+
+def test_ep_emulation_shapes():
+    """--ep-emulate R runs one rank's expert load at EP = R on one GPU: the config's T k copies over E/R
+    local experts.  With fewer local experts than top-k (Mixtral at EP = 8: one expert per rank) the copies
+    run as T k / E_l tokens of top-E_l routing - the same expert GEMM shapes - while tokens/s and the
+    workload still count the real layer's T tokens per GPU."""
+    import argparse
+    import importlib.util
+    spec = importlib.util.spec_from_file_location("bench_mod", os.path.join(ROOT, "bench.py"))
+    b = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(b)
+    import synth
+    for name, R in (("mixtral", 8), ("dsv3", 8), ("qwen3", 8), ("mixtral", 1)):
+        a = argparse.Namespace(config=name, ep_emulate=R, tokens=0, placement=None)
+        cfg, cfg0 = b.emulated_config(a), synth.CONFIGS[name]
+        assert cfg.E == cfg0.E // R and cfg.k <= cfg.E
+        assert cfg.T * cfg.k == cfg0.T * cfg0.k                    # the same copies
+        wl = b.workload_config(cfg, a, 1)
+        assert wl["tokens_per_gpu"] == cfg0.T and f"top-{cfg0.k}" in wl["workload"]
+    a = argparse.Namespace(config="mixtral", ep_emulate=8, tokens=0, placement=None)
+    assert (b.emulated_config(a).E, b.emulated_config(a).k, b.emulated_config(a).T) == (1, 1, 32768)
