@@ -66,11 +66,18 @@ def _run_group(EP, C, dtype, transport, xs, dys, routes, wg, wu, wd, T, h, g, E,
                                          mx_wgrad=mx_wgrad)
                     wsb = max(wsb, layer.workspace_bytes(ch, dr, C, capi.FWD), layer.workspace_bytes(ch, dr, C, capi.BWD))
                 ws = torch.empty(wsb, dtype=torch.uint8, device=dev)
-                y = mf.moe_fwd(x, ids, w, lwg, lwu, lwd, C, ws, stream=st)
-                kw = {}
-                if nan_dw:   # dW buffers holding garbage: the call must overwrite every element
-                    kw = {n_: torch.full(t_.shape, float("nan"), dtype=torch.float32, device=dev)
-                          for n_, t_ in (("dw_gate", lwg), ("dw_up", lwu), ("dw_down", lwd))}
+                # Every device allocation of this rank happens BEFORE its first layer call: with the fused
+                # peer-memory exchange another rank's kernels spin on flags this rank raises, and a
+                # cudaMalloc issued by this thread in between (e.g. torch allocating the backward's outputs)
+                # may wait for the device to go idle - i.e. for that spin - while holding up this rank's
+                # launches (seen as a 20 s wait timeout in the two-slot P2P mode).
+                f32 = dict(dtype=torch.float32, device=dev)
+                y = torch.empty_like(x)
+                kw = {"dx": torch.empty_like(x), "dscore": torch.empty(w.shape, **f32)}
+                fill = float("nan") if nan_dw else 0.0   # nan_dw: garbage dW, the call must overwrite every element
+                kw.update({n_: torch.full(t_.shape, fill, **f32)
+                           for n_, t_ in (("dw_gate", lwg), ("dw_up", lwu), ("dw_down", lwd))})
+                y = mf.moe_fwd(x, ids, w, lwg, lwu, lwd, C, ws, y=y, stream=st)
                 dx, dwg, dwu, dwd, ds = mf.moe_bwd(dy, x, ids, w, lwg, lwu, lwd, C, ws, stream=st, **kw)
                 s_ = mf.sync(stream=st)
                 assert s_ == 0, capi.status_str(s_)
