@@ -529,7 +529,10 @@ def main():
         per_launch_flops = flops_step * args.steps / prof[dom]["launches"]
         avg_ms = prof[dom]["ms"] / prof[dom]["launches"]
         achieved = per_launch_flops / (avg_ms / 1000.0) / 1e12
-        peak = peaks["bf16_tflops_sustained"]
+        # the sustained peak for a kernel inside a long step at the power cap; a short step that never reaches
+        # the capped clock can run its GEMMs above it - then the burst figure is the ceiling that applies
+        burst = achieved > peaks["bf16_tflops_sustained"]
+        peak = peaks["bf16_tflops"] if burst else peaks["bf16_tflops_sustained"]
         traffic, tsrc = load_traffic()
         # the committed capture is of the default workload (Mixtral, EP = 1, C = 1); other shapes: null
         same = (args.config == "mixtral" and args.ep_emulate == 1 and not args.tokens and world == 1 and C == 1)
@@ -539,7 +542,9 @@ def main():
                 "traffic_source": f"{tsrc}: ncu --set full dram__bytes_read.sum + dram__bytes_write.sum per launch"
                 if tb else None,
                 "algorithmic_flops_per_launch": per_launch_flops,
-                "peak_source": f"{peaks['source']} bf16_tflops_sustained (kernel timed inside a long step)",
+                "peak_source": (f"{peaks['source']} bf16_tflops (burst: the kernel ran above the sustained rate, "
+                                "the step did not reach the power-capped clock)") if burst else
+                               f"{peaks['source']} bf16_tflops_sustained (kernel timed inside a long step)",
                 "share_of_step": prof[dom]["ms"] / tot_ms if tot_ms else None}
     elif dom in ("dispatch_permute", "combine_unpermute") and prof[dom]["launches"]:
         # HBM-bound permute kernels (small layers): algorithmic bytes per step, bf16 rows of h.
