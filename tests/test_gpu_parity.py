@@ -201,10 +201,13 @@ def test_errors_surface():
 
 
 @pytest.mark.slow
-def test_mixtral_full_size_sampled():
+@pytest.mark.parametrize("C", [1, 2])
+def test_mixtral_full_size_sampled(C, monkeypatch):
     """BASELINE configs[1] shape at EP=1 (8 experts, top-2, h=4096, FFN=14336, 16K tokens):
     integer outputs in full; Y / dX / d_score vs the oracle on tokens sampled so that every 128-row
-    m-tile of every expert segment of both chunks holds at least one of their copies."""
+    m-tile of every expert segment of every chunk holds at least one of their copies.  C = 1 is the
+    bench's launch configuration, where the down and dX GEMMs run 512 x 256 quad tiles: there Y and dX
+    must also equal the 256 x 256 pair tiles' bit for bit."""
     p = make_problem(16384, 4096, 14336, 8, 2, zipf_s=1.2, seed=5)
     run = GpuRun(p)
     d = oracle_dims(p)
@@ -212,12 +215,21 @@ def test_mixtral_full_size_sampled():
     ref, _ = oracle.route_counts(d, p.ids.numpy(), 8)
     np.testing.assert_array_equal(c, ref)
     run.mf.set_debug(True)      # the expert-major row layout, to sample every m-tile
-    y, st, _, _ = run.fwd(2)
+    y, st, _, _ = run.fwd(C)
     assert st == 0
-    rows = [run.mf.debug_rows(j) for j in range(2)]
+    rows = [run.mf.debug_rows(j) for j in range(C)]
     run.mf.set_debug(False)
-    (dx, dwg, dwu, dwd, ds), st, _, _ = run.bwd(2)
+    (dx, dwg, dwu, dwd, ds), st, _, _ = run.bwd(C)
     assert st == 0
+    if C == 1:
+        y, dx = y.clone(), dx.clone()
+        monkeypatch.setenv("MEMFINE_QUAD", "0")
+        y0, st, _, _ = run.fwd(C)
+        assert st == 0
+        (dx0, _, _, _, _), st, _, _ = run.bwd(C)
+        assert st == 0
+        assert torch.equal(y.view(torch.int16), y0.view(torch.int16))
+        assert torch.equal(dx.view(torch.int16), dx0.view(torch.int16))
     rng = np.random.default_rng(0)
     toks = np.unique(np.concatenate([tile_covering_tokens(r, p.k, rng) for r in rows]))
     ry, rdx, rds = oracle_tokens(p, toks)
