@@ -232,7 +232,8 @@ memfine_status memfine_register_workspace(memfine_handle_t h, void* ws, uint64_t
  * PAPER.md:200): an expert-parallel handle whose only transport is the device-planned peer-memory
  * exchange (MEMFINE_EP_P2P), for ranks in separate processes that exchange their workspace mappings
  * through the caller's own channel (e.g. torch.distributed over gloo) - two processes sharing one
- * device included.  dims->ep_size in [2, 16]; flags without MEMFINE_FLAG_EP_PATH / MEMFINE_FLAG_OVERLAP.
+ * device included.  dims->ep_size in [2, 16]; flags without MEMFINE_FLAG_EP_PATH (MEMFINE_FLAG_OVERLAP selects
+ * the two-slot, two-stream chunk pipeline of the exchange).
  * memfine_route_counts on such a handle fills only this rank's rows of counts_dev (the caller
  * all-gathers them to size the workspace); the layer calls themselves need no host collective (the
  * counts travel through the peers' sync areas).  memfine_set_ep_transport accepts MEMFINE_EP_P2P only. */

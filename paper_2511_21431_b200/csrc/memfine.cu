@@ -1701,14 +1701,16 @@ memfine_status memfine_register_workspace(memfine_handle_t h, void* ws, uint64_t
 memfine_status memfine_create_ipc(const memfine_dims* dims, memfine_handle_t* out) {
   if (!out || !dims || !dims_ok(dims)) return MEMFINE_ERR_INVALID_ARG;
   if (dims->ep_size < 2 || dims->ep_size > kMaxPeers) return MEMFINE_ERR_INVALID_ARG;
-  if (dims->flags & (MEMFINE_FLAG_EP_PATH | MEMFINE_FLAG_OVERLAP)) return MEMFINE_ERR_INVALID_ARG;
+  if (dims->flags & MEMFINE_FLAG_EP_PATH) return MEMFINE_ERR_INVALID_ARG;
   memfine_dims d1 = *dims;
   d1.ep_size = 1;   // create with the single-rank path (no communicator), then switch to the EP layout
   d1.ep_rank = 0;
+  d1.flags &= ~MEMFINE_FLAG_OVERLAP;
   memfine_status st = memfine_create(&d1, nullptr, out);
   if (st != MEMFINE_OK) return st;
   (*out)->d.ep_size = dims->ep_size;
   (*out)->d.ep_rank = dims->ep_rank;
+  (*out)->d.flags = dims->flags;   // (MEMFINE_FLAG_OVERLAP: the two-slot pipeline of the peer-memory exchange)
   (*out)->ipc_only = 1;
   (*out)->p2p = 1;
   return MEMFINE_OK;

@@ -30,7 +30,7 @@ def _free_port():
     return p
 
 
-def _worker(rank, world, port, C, out_dir):
+def _worker(rank, world, port, C, overlap, out_dir):
     import torch.distributed as dist
     from paper_2511_21431_b200 import capi, layer
     os.environ["MASTER_ADDR"] = "127.0.0.1"
@@ -47,7 +47,7 @@ def _worker(rank, world, port, C, out_dir):
         ids, w = torch.from_numpy(ids_np).to(dev), torch.from_numpy(w_np).to(dev)
         wg, wu, wd = synth.make_experts(range(E), H, G, dtype=dt)
         lwg, lwu, lwd = (t[rank * El:(rank + 1) * El].contiguous().to(dev) for t in (wg, wu, wd))
-        mf = layer.MemFine(T, H, G, E, K, ep_size=world, ep_rank=rank, dtype=dt, ipc=True)
+        mf = layer.MemFine(T, H, G, E, K, ep_size=world, ep_rank=rank, dtype=dt, ipc=True, overlap=overlap)
         # A1 on this rank; the all-gather (A2) through gloo here, only to size the workspace - inside the
         # layer calls the counts travel through the peers' sync areas
         counts = mf.route_counts(ids, nsub=C)
@@ -57,7 +57,7 @@ def _worker(rank, world, port, C, out_dir):
         ch = torch.stack(rows).contiguous()
         wsb = 0
         for r in range(world):
-            dr = layer.make_dims(T, H, G, E, K, ep_size=world, ep_rank=r, dtype=dt)
+            dr = layer.make_dims(T, H, G, E, K, ep_size=world, ep_rank=r, dtype=dt, overlap=overlap)
             wsb = max(wsb, layer.workspace_bytes(ch, dr, C, capi.FWD), layer.workspace_bytes(ch, dr, C, capi.BWD))
         ws = torch.empty(wsb, dtype=torch.uint8, device=dev)
         rec = mf.ipc_export(ws)
@@ -79,13 +79,13 @@ def _worker(rank, world, port, C, out_dir):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("C", [1, 2])
-def test_ipc_p2p_two_processes_match_oracle(C, tmp_path):
+@pytest.mark.parametrize("C,overlap", [(1, False), (2, False), (3, True)])
+def test_ipc_p2p_two_processes_match_oracle(C, overlap, tmp_path):
     if not torch.cuda.is_available():
         pytest.skip("needs a CUDA device")
     import torch.multiprocessing as mp
     world = 2
-    mp.start_processes(_worker, args=(world, _free_port(), C, str(tmp_path)), nprocs=world, join=True,
+    mp.start_processes(_worker, args=(world, _free_port(), C, overlap, str(tmp_path)), nprocs=world, join=True,
                        start_method="spawn")
     res = [dict(np.load(tmp_path / f"rank{r}.npz")) for r in range(world)]
     for r in range(world):
