@@ -207,14 +207,26 @@ def step_roofline(counts_h, h, g, k, T, El, C, ms, peaks, nvlink_gbs=900.0):
                       N / (nvlink_gbs * 1e9), (P + Wb) / (peaks["hbm_gbs"] * 1e9)))
     t_roof = max(max(t[0], t[1], t[2]) for t in terms)
     t_roof4 = max(max(t[0], t[3], t[2]) for t in terms)
+    # the same terms with the tensor-bound and HBM-bound work NOT overlapped (what a step that runs
+    # its dW read-modify-writes and weight re-reads between the GEMMs can reach at best)
+    t_serial = max(t[0] + t[3] + t[2] for t in terms)
     hot = max(range(EP), key=lambda r: max(terms[r][:3]))
     return {"t_roof_ms": t_roof * 1e3, "t_roof4_ms": t_roof4 * 1e3, "frac": t_roof / (ms / 1e3),
-            "frac4": t_roof4 / (ms / 1e3), "hot_rank": hot,
+            "frac4": t_roof4 / (ms / 1e3), "t_serial_ms": t_serial * 1e3, "frac_serial": t_serial / (ms / 1e3),
+            "hot_rank": hot,
             "bound": ["tensor", "hbm", "nvlink"][max(range(3), key=lambda i: terms[hot][i])],
             "terms_ms_hot_rank": {"gemm_flops": terms[hot][0] * 1e3, "permute_bytes": terms[hot][1] * 1e3,
                                   "a2a_bytes": terms[hot][2] * 1e3, "permute_plus_weights": terms[hot][3] * 1e3},
             "peaks": {"tensor_tflops": peaks["bf16_tflops_sustained"], "hbm_gbs": peaks["hbm_gbs"],
                       "nvlink_gbs": nvlink_gbs}}
+
+
+def per_c_roofline(counts_h, h, g, k, T, El, C, ms, peaks):
+    """The per-C entry's roofline: t_roof4 (tensor and the chunked method's HBM bytes overlapped, the
+    lower bound) and t_serial (not overlapped), both from step_roofline."""
+    r = step_roofline(counts_h, h, g, k, T, El, C, ms, peaks)
+    return {"t_roof4_ms": r["t_roof4_ms"], "frac4": r["frac4"], "t_serial_ms": r["t_serial_ms"],
+            "frac_serial": r["frac_serial"], "hbm_ms_hot_rank": r["terms_ms_hot_rank"]["permute_plus_weights"]}
 
 
 # ------------------------------------------------------------------------------------ oracle legs
@@ -665,12 +677,14 @@ def main():
     if args.sweep and world == 1:
         for Cc in bins:
             if Cc == C_f == C_b:
-                per_C[Cc] = {"ms_per_step": ms, "tokens_per_s": value, "peak_act_gb": peak_gb(Cc)}
+                per_C[Cc] = {"ms_per_step": ms, "tokens_per_s": value, "peak_act_gb": peak_gb(Cc),
+                             "roofline": per_c_roofline(counts_h, h, g, k, T, El, Cc, ms, peaks)}
                 continue
             try:   # a side measurement: a failure here must not cost the headline line
                 wsc = torch.empty(int(peak_gb(Cc) * 1e9) + 1, dtype=torch.uint8, device=dev)
                 msc, _ = timed(make_step(Cc, wsc), max(3, args.steps // 2), 1)
-                per_C[Cc] = {"ms_per_step": msc, "tokens_per_s": EP * T_tok / (msc / 1000.0), "peak_act_gb": peak_gb(Cc)}
+                per_C[Cc] = {"ms_per_step": msc, "tokens_per_s": EP * T_tok / (msc / 1000.0), "peak_act_gb": peak_gb(Cc),
+                             "roofline": per_c_roofline(counts_h, h, g, k, T, El, Cc, msc, peaks)}
                 del wsc
             except Exception as ex:  # noqa: BLE001
                 per_C[Cc] = {"error": f"{type(ex).__name__}: {ex}"[:300]}
