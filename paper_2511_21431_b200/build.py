@@ -29,8 +29,10 @@ def nvcc() -> str:
 
 
 def flags():
+    # MEMFINE_NVCC_EXTRA: extra -D switches for experiment builds (tools/lib_ab.sh A/Bs)
+    extra = os.environ.get("MEMFINE_NVCC_EXTRA", "").split()
     return ARCH + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O3", "--expt-relaxed-constexpr",
-                   "-I", os.path.join(ROOT, "include"), "-I", nccl_include()]
+                   "-I", os.path.join(ROOT, "include"), "-I", nccl_include()] + extra
 
 
 def _stale(obj: str, deps) -> bool:
