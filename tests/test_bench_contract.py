@@ -104,6 +104,14 @@ def test_step_roofline_terms():
     t = r["terms_ms_hot_rank"]
     assert abs(t["a2a_bytes"] - 1e3 * N) < 1e-9 and abs(t["permute_bytes"] - 1e3 * P) < 1e-9
     assert abs(r["frac"] - max(F1, P, N) / 1.0) < 1e-9
+    # t_serial: the same terms not overlapped, on the rank where their sum is largest
+    F0 = 22 * h * g * 15 / 1e3
+    N0 = N
+    assert abs(r["t_serial_ms"] - 1e3 * max(F0 + P4 + N0, F1 + P4 + N)) < 1e-6 * r["t_serial_ms"]
+    pc = bench.per_c_roofline(counts, h, g, k, T, El, C, 1000.0, peaks)     # NVLink at its default 900 GB/s
+    r9 = bench.step_roofline(counts, h, g, k, T, El, C, ms=1000.0, peaks=peaks)
+    assert pc["t_roof4_ms"] == r9["t_roof4_ms"] and pc["t_serial_ms"] == r9["t_serial_ms"]
+    assert pc["t_serial_ms"] >= pc["t_roof4_ms"]
 
 
 def test_ep_emulation_shapes():
