@@ -1542,6 +1542,8 @@ int launch(const GemmProblem<__nv_bfloat16>& gp, cudaStream_t st) {
   return 1;
 }
 
+constexpr int64_t kQuadMinK = 8192;
+
 template <int KIND>
 int launch_kind(const GemmProblem<__nv_bfloat16>& gp, cudaStream_t st) {
   if constexpr (KIND == GK_DOWN || KIND == GK_DX) {
@@ -1554,7 +1556,13 @@ int launch_kind(const GemmProblem<__nv_bfloat16>& gp, cudaStream_t st) {
     // at least 8 waves of quad tiles at the chunk's row capacity (the full-size C = 1 Mixtral layer has 14)
     const int64_t quads = gp.rows_cap / (4 * BM) + 1, nt_q = (gp.h + 255) / 256;
     const int units = (g_num_sms ? g_num_sms : 148) / 2;
-    if (use_pairs() && env_quad && !gp.out_f32 && gp.El <= 255 && (env_quad == 2 || quads * nt_q >= 8 * units))
+    // and a long K: a quad's accumulator is single-buffered, so its drain is exposed once per tile; at
+    // K >= 8192 (Mixtral's down, K = g = 14336, and dX, K = 2g) that is a few % of the mainloop, at the
+    // short K of DeepSeek-V3 / Qwen3 (down K = 2048 / 1536, dX 4096 / 3072) the pairs' double-buffered
+    // accumulators win (profiles/r02d_lib_ab_quad_k)
+    const int64_t K = KIND == GK_DOWN ? (int64_t)gp.g : 2 * (int64_t)gp.g;
+    if (use_pairs() && env_quad && !gp.out_f32 && gp.El <= 255 &&
+        (env_quad == 2 || (quads * nt_q >= 8 * units && K >= kQuadMinK)))
       return launch<KIND, true, true>(gp, st);
   }
   return use_pairs() ? launch<KIND, true>(gp, st) : launch<KIND, false>(gp, st);
