@@ -32,9 +32,6 @@ namespace sm100 {
 
 constexpr int BM = 128, BK = 64, EPI_WARPS = 8, THREADS = 64 + 32 * EPI_WARPS;
 constexpr int A_BYTES = BM * BK * 2;  // 16 KB
-#ifndef MEMFINE_DACT_A_EVLAST
-#define MEMFINE_DACT_A_EVLAST 0
-#endif
 
 // ------------------------------------------------------------------ PTX wrappers
 __device__ __forceinline__ uint32_t su32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
@@ -438,15 +435,6 @@ __device__ __forceinline__ void tma_2d_pair(void* dst, const CUtensorMap* m, uin
       "l"(m), "r"(su32(bar) & kPeerMask), "r"(c0), "r"(c1)
       : "memory");
 }
-// the same with an L2 cache policy (createpolicy)
-__device__ __forceinline__ void tma_2d_pair_hint(void* dst, const CUtensorMap* m, uint64_t* bar, int c0, int c1,
-                                                 uint64_t pol) {
-  asm volatile(
-      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], "
-      "[%1, {%3, %4}], [%2], %5;" ::"r"(su32(dst)),
-      "l"(m), "r"(su32(bar) & kPeerMask), "r"(c0), "r"(c1), "l"(pol)
-      : "memory");
-}
 __device__ __forceinline__ void tma_3d_pair(void* dst, const CUtensorMap* m, uint64_t* bar, int c0, int c1, int c2) {
   asm volatile(
       "cp.async.bulk.tensor.3d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, "
@@ -805,10 +793,6 @@ __global__ void __launch_bounds__(THREADS, 1)
             // A(m,k) = rows[kc + k][am0 + m]: two 64-wide MN atoms of 64 K rows
             LA(sa, &tmA, am0, kc);
             LA(sa + 8192, &tmA, am0 + 64, kc);
-          } else if (MEMFINE_DACT_A_EVLAST && KIND == GK_DACT && PAIR) {
-            uint64_t pol;
-            asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
-            tma_2d_pair_hint(sa, &tmA, full + stage, kc, am0, pol);
           } else {
             LA(sa, &tmA, kc, am0);
             if (QD && T.halves == 2) LA(sa + A_BYTES, &tmA, kc, am0 + 2 * BM);   // the second half's rows
