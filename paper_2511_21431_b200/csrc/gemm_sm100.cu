@@ -136,6 +136,16 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&r)[16]) {
   asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }
 
+__device__ __forceinline__ float ex2_ftz(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+__device__ __forceinline__ float rcp_ftz(float x) {
+  float y;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
 __device__ __forceinline__ uint32_t pack_bf16(float a, float b) {
   __nv_bfloat162 v = __floats2bfloat162_rn(a, b);
   return *reinterpret_cast<uint32_t*>(&v);
@@ -1050,6 +1060,7 @@ __global__ void __launch_bounds__(THREADS, 1)
         continue;
       }
       float dwp = 0.f;
+      float2 dwp2 = make_float2(0.f, 0.f);   // dA: d_w partials of the even / odd columns
       float wrow = 0.f;
       if (KIND == GK_DACT && rows_ok) {
         wrow = p.w_row[row];
@@ -1159,26 +1170,34 @@ __global__ void __launch_bounds__(THREADS, 1)
               }
               __syncwarp();
               uint32_t og[8], ou[8], oa[8];
+              // the two columns of each bf16 pair in one register pair: packed fp32x2 FMUL2 / FADD2 / FFMA2 (half
+              // the FP32 issue of scalar math - the epilogue's instruction stream is what slows the MMA stream
+              // beside it, profiles/r02_dact_and_tail_experiments.md §7); per element the same fp32 formulas:
+              //   s = 1 / (1 + 2^(-G log2 e)), silu = G s, a = silu U, dA = w u, dU = dA silu,
+              //   dG = dA U (s + silu (1 - s)), a_w = w a, d_w += u a
+              const float2 w2 = make_float2(wrow, wrow);
+              const float2 one2 = make_float2(1.f, 1.f), mone2 = make_float2(-1.f, -1.f);
+              const float2 nl2e = make_float2(-1.4426950408889634f, -1.4426950408889634f);
 #pragma unroll
               for (int j = 0; j < 8; j++) {
-                float r2v[2][3];
-#pragma unroll
-                for (int q2 = 0; q2 < 2; q2++) {
-                  const int i = 16 * h2 + 2 * j + q2;
-                  const uint32_t gw = gcur[j], uw = ucur[j];
-                  const float G = __uint_as_float(q2 ? (gw & 0xFFFF0000u) : (gw << 16));
-                  const float U = __uint_as_float(q2 ? (uw & 0xFFFF0000u) : (uw << 16));
-                  const float sg = sigmoid_f(G);
-                  const float a = G * sg * U;
-                  dwp = fmaf(v[i], a, dwp);
-                  const float dA = wrow * v[i];
-                  r2v[q2][0] = dA * U * sg * (1.f + G * (1.f - sg));
-                  r2v[q2][1] = dA * G * sg;
-                  r2v[q2][2] = wrow * a;
-                }
-                og[j] = pack_bf16(r2v[0][0], r2v[1][0]);
-                ou[j] = pack_bf16(r2v[0][1], r2v[1][1]);
-                oa[j] = pack_bf16(r2v[0][2], r2v[1][2]);
+                const uint32_t gw = gcur[j], uw = ucur[j];
+                const float2 G2 = make_float2(__uint_as_float(gw << 16), __uint_as_float(gw & 0xFFFF0000u));
+                const float2 U2 = make_float2(__uint_as_float(uw << 16), __uint_as_float(uw & 0xFFFF0000u));
+                const float2 v2 = make_float2(v[16 * h2 + 2 * j], v[16 * h2 + 2 * j + 1]);
+                const float2 t2 = __fmul2_rn(G2, nl2e);
+                const float2 den = __fadd2_rn(make_float2(ex2_ftz(t2.x), ex2_ftz(t2.y)), one2);
+                const float2 sg = make_float2(rcp_ftz(den.x), rcp_ftz(den.y));
+                const float2 silu = __fmul2_rn(G2, sg);
+                const float2 a2 = __fmul2_rn(silu, U2);
+                dwp2 = __ffma2_rn(v2, a2, dwp2);
+                const float2 dA2 = __fmul2_rn(w2, v2);
+                const float2 ds = __ffma2_rn(silu, __ffma2_rn(sg, mone2, one2), sg);   // s + silu (1 - s)
+                const float2 dG2 = __fmul2_rn(__fmul2_rn(dA2, U2), ds);
+                const float2 dU2 = __fmul2_rn(dA2, silu);
+                const float2 aw2 = __fmul2_rn(w2, a2);
+                og[j] = pack_bf16(dG2.x, dG2.y);
+                ou[j] = pack_bf16(dU2.x, dU2.y);
+                oa[j] = pack_bf16(aw2.x, aw2.y);
               }
               if (p.mx_gq) {
                 // MX variant: dG and dU of this 32-column block -> E4M3 + scale for the dX GEMM
@@ -1228,7 +1247,7 @@ __global__ void __launch_bounds__(THREADS, 1)
         }
       }
       }   // halves
-      if (KIND == GK_DACT && rows_ok) atomicAdd(p.dw_row + row, dwp);
+      if (KIND == GK_DACT && rows_ok) atomicAdd(p.dw_row + row, dwp + dwp2.x + dwp2.y);
       fence_before();
       __syncwarp();
       if (lane == 0) {
