@@ -1098,9 +1098,20 @@ __global__ void __launch_bounds__(THREADS, 1)
               stage_bf16_row(buf, lane, v);
               stage_bf16_row(buf + 2048, lane, u);
             } else {
+              // a = silu(G) U on packed fp32x2 (FMUL2 / FADD2, ftz ex2 / rcp; see the dA epilogue)
               float a[32];
+              const float2 one2 = make_float2(1.f, 1.f);
+              const float2 nl2e = make_float2(-1.4426950408889634f, -1.4426950408889634f);
 #pragma unroll
-              for (int i = 0; i < 32; i++) a[i] = silu_f(v[i]) * u[i];
+              for (int i = 0; i < 32; i += 2) {
+                const float2 G2 = make_float2(v[i], v[i + 1]);
+                const float2 t2 = __fmul2_rn(G2, nl2e);
+                const float2 den = __fadd2_rn(make_float2(ex2_ftz(t2.x), ex2_ftz(t2.y)), one2);
+                const float2 a2 = __fmul2_rn(__fmul2_rn(G2, make_float2(rcp_ftz(den.x), rcp_ftz(den.y))),
+                                             make_float2(u[i], u[i + 1]));
+                a[i] = a2.x;
+                a[i + 1] = a2.y;
+              }
               stage_bf16_row(buf, lane, a);
             }
             fence_async_smem();
